@@ -1,0 +1,195 @@
+/*
+ * csplat.h -- C ABI of the B200 (sm_100a) hot path of "Compact 3D Gaussian
+ * Splatting for Dense Visual SLAM" (arXiv 2403.11247).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n; readings R1..R26 and
+ * the decision arithmetic (DA) are defined in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Ownership: every data pointer is a caller-owned CUDA DEVICE pointer
+ *    (e.g. from torch.empty(device="cuda")), unless the comment says "host".
+ *    Struct arguments themselves live in HOST memory and are read during the
+ *    call only.  The library never allocates, frees or retains device
+ *    memory beyond the call; scratch comes from a caller buffer sized by
+ *    csplat_workspace_bytes().
+ *  - Asynchrony: all work is enqueued on `stream` (a cudaStream_t; NULL = the
+ *    legacy default stream).  Results are valid once the stream reaches the
+ *    end of the enqueued work.  Only csplat_bin_tiles with CSPLAT_SYNC (and
+ *    argument validation) synchronises with the host.
+ *  - Layouts: Gaussian attributes are planar SoA [k][n] float32; images are
+ *    planar [c][H][W] float32; codebooks [L][P][d] float32; indices [L][n]
+ *    uint8 (P <= 256) or uint16; the 64-byte projected record is described in
+ *    DESIGN.md §4.
+ *  - Alignment: every float plane and record buffer must be 16-byte aligned
+ *    (CSPLAT_ERR_ALIGNMENT otherwise).
+ *  - Errors: every function returns a csplat_status; it never aborts and
+ *    never throws across the ABI.  CSPLAT_ERR_CUDA carries the CUDA error text
+ *    in csplat_last_error() (thread-local).  Device faults surface as
+ *    CSPLAT_ERR_CUDA on a later call or at the caller's next synchronisation.
+ *    Non-finite attribute values are culled (never propagated).  n = 0 is
+ *    valid (black images, zero gradients).
+ *  - Device: compute capability 10.0 (B200) only; otherwise
+ *    CSPLAT_ERR_UNSUPPORTED.
+ */
+#ifndef CSPLAT_H
+#define CSPLAT_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum csplat_status {
+    CSPLAT_OK = 0,
+    CSPLAT_ERR_INVALID_ARG = 1,  /* null required pointer, n < 0, W/H <= 0, fx/fy <= 0, !(0<near<far), L/P/d out of range */
+    CSPLAT_ERR_ALIGNMENT = 2,    /* a plane or record buffer is not 16-byte aligned */
+    CSPLAT_ERR_CAPACITY = 3,     /* more (tile, Gaussian) pairs than pair_capacity (CSPLAT_SYNC only) */
+    CSPLAT_ERR_WORKSPACE = 4,    /* ws_bytes < csplat_workspace_bytes(...) */
+    CSPLAT_ERR_CUDA = 5,         /* launch / runtime error; text in csplat_last_error */
+    CSPLAT_ERR_UNSUPPORTED = 6   /* device is not compute capability 10.x */
+};
+
+#define CSPLAT_TILE 16           /* screen tile edge in pixels (R4) */
+#define CSPLAT_RECORD_BYTES 64   /* projected record size */
+
+/* Flags */
+#define CSPLAT_SYNC 1u           /* bin_tiles: read n_pairs back, return CAPACITY if it exceeds the capacity */
+#define CSPLAT_POSE_ONLY 2u      /* render_bwd: only the pose gradient (tracking) */
+#define CSPLAT_ACCUMULATE 4u     /* render_bwd: add into the outputs instead of overwriting */
+
+/* Pinhole intrinsics K ("known camera intrinsic K"), image size, clip (R21). */
+typedef struct {
+    float fx, fy, cx, cy;
+    int32_t width, height;
+    float near_z, far_z;
+} csplat_camera;
+
+/* World->camera [R|t], row-major 3x4, HOST memory ("{R_i|t_i}"). */
+typedef struct { float m[12]; } csplat_view;
+
+/* Renderer constants: mask threshold eps (Eq 6; R12, default 0.01),
+ * alpha cap (R1, 0.99), transmittance cutoff (R3, 1e-4), 2D dilation (R5, 0.3). */
+typedef struct { float mask_eps, alpha_max, t_min, dilation; } csplat_params;
+
+/* Gaussian map (Eq 6; parameterisation R15), device SoA planes.
+ * n_dev (optional, device int64): if non-NULL, only the first *n_dev <= n
+ * Gaussians exist (e.g. the survivor count written by csplat_mask_prune);
+ * the rest are treated as culled. */
+typedef struct {
+    int64_t n;
+    const int64_t *n_dev;
+    const float *mean;       /* [3][n] world position                  */
+    const float *opacity;    /* [n]    opacity logit, o = sigmoid(.)    */
+    const float *rgb;        /* [3][n] colour c_i of Eq 3              */
+    const float *log_scale;  /* [3][n] log of the scale S (Eq 1)       */
+    const float *quat;       /* [4][n] rotation R as wxyz quaternion   */
+    const float *mask;       /* [n]    mask logit m (Eq 6)             */
+} csplat_gaussians;
+
+/* Mutable Gaussian planes (output of csplat_mask_prune), capacity >= n. */
+typedef struct {
+    int64_t capacity;
+    float *mean, *opacity, *rgb, *log_scale, *quat, *mask;
+} csplat_gaussians_out;
+
+/* R-VQ geometry codebooks (Eq 10; R16-R18): log-scale (d=3) and
+ * quaternion (d=4) codes, and per-Gaussian indices [L][n]. */
+typedef struct {
+    int32_t stages, size, idx_bytes, reserved;  /* L, P, 1 or 2 */
+    const float *scale_codes;  /* [L][P][3] */
+    const float *rot_codes;    /* [L][P][4] */
+    const void *scale_idx;     /* [L][n] uint8/uint16 */
+    const void *rot_idx;       /* [L][n] uint8/uint16 */
+} csplat_codebook;
+
+/* Gradients: planes [k][n] like csplat_gaussians (any may be NULL to skip),
+ * pose[6] = dL/d(omega, v) for the left perturbation V' = Exp(xi) V (R22). */
+typedef struct {
+    float *mean, *opacity, *rgb, *log_scale, *quat, *mask;
+    float *pose;
+} csplat_grads;
+
+/* a1 + a2(decode) + a3: projection (Eq 1-2) with the binary mask
+ * (Eq 6-7) and R-VQ decode (Eq 10; cb may be NULL for raw
+ * geometry).  Writes the 64-byte record rec[n] and the touched-tile count
+ * count[n] (0 = culled), bit-exactly as DESIGN.md §3 (DA). */
+int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const csplat_camera *cam,
+                   const csplat_view *view, const csplat_params *prm, void *rec, int32_t *count,
+                   void *stream);
+
+/* a4 + a5: tile binning and (tile, depth) ordering (R4, R11).
+ * Outputs, for n_pairs = sum(count) pairs:
+ *   pair_gid[pair_capacity]   Gaussian index per pair, ordered by (tile, bits(z_c), index)
+ *   pair_rec[pair_capacity]   the 64-byte record of each pair, same order (the
+ *                             contiguous payload the renderer streams with TMA)
+ *   tile_range[T][2]          [start, end) of every tile, T = ceil(W/16)*ceil(H/16)
+ *   n_pairs_dev               device int64: the total (may exceed the capacity)
+ * Pairs beyond pair_capacity are dropped (ranges clamped); with CSPLAT_SYNC the
+ * call synchronises and returns CSPLAT_ERR_CAPACITY in that case.
+ * ws: csplat_workspace_bytes(CSPLAT_OP_BIN_TILES, n, pair_capacity, cam). */
+int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csplat_camera *cam,
+                     int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                     uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
+                     size_t ws_bytes, void *stream);
+
+/* a6: front-to-back compositing of colour, depth and silhouette (Eq 3-5,
+ * P:98-109; R1-R3, R7-R10).  Outputs color [3][H][W], depth, silhouette,
+ * t_final [H][W] float32 and n_contrib [H][W] int32 (local index + 1 of the
+ * last composited entry of the pixel's tile list; the backward's replay bound). */
+int csplat_render_fwd(const void *pair_rec, const uint32_t *tile_range, const csplat_camera *cam,
+                      const csplat_params *prm, float *color, float *depth, float *silhouette,
+                      float *t_final, int32_t *n_contrib, void *stream);
+
+/* a7 + a8: backward of a6 through a3, a2-decode and the STE mask (Eq 6), with
+ * the pose gradient (R14, R20, R22, R23).  d_color [3][H][W], d_depth,
+ * d_silhouette [H][W] are dL/d(outputs).  The forward-state arguments (rec,
+ * pair_rec, tile_range, t_final, n_contrib) must come from csplat_project /
+ * csplat_bin_tiles / csplat_render_fwd on the same inputs (not verified).
+ * Gradients are w.r.t. mean, opacity logit, rgb, (decoded) log-scale, (decoded)
+ * quaternion, mask logit and pose.  flags: CSPLAT_POSE_ONLY, CSPLAT_ACCUMULATE.
+ * ws: csplat_workspace_bytes(CSPLAT_OP_RENDER_BWD, n, 0, cam). */
+int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
+                      const csplat_camera *cam, const csplat_view *view, const csplat_params *prm,
+                      const void *rec, const void *pair_rec, const uint32_t *tile_range,
+                      const float *t_final, const int32_t *n_contrib, const float *d_color,
+                      const float *d_depth, const float *d_silhouette, uint32_t flags,
+                      const csplat_grads *out, void *ws, size_t ws_bytes, void *stream);
+
+/* a2: greedy residual VQ assignment (Eq 10; R17): for each of the n
+ * d-dimensional vectors x [d][n] and each stage l, idx[l][i] = argmin_k
+ * ||C^l[k] - (x_i - S_hat^{l-1}_i)||^2 (DA distances, ties to the lowest k).
+ * codes [L][P][d]; idx_out [L][n] with idx_bytes 1 (P <= 256) or 2;
+ * recon_out [d][n] (optional) = S_hat^L.  n_dev optional (see csplat_gaussians).
+ * Limits: 1 <= d <= 8, 1 <= L <= 16, 1 <= P <= 65536. */
+int csplat_rvq_assign(const float *x, int64_t n, const int64_t *n_dev, int32_t d,
+                      const float *codes, int32_t L, int32_t P, void *idx_out, int32_t idx_bytes,
+                      float *recon_out, void *stream);
+
+/* a9: mask prune (Fig 3): keep Gaussian i iff
+ * m_i > tau (Eq 6 / R12), compact all planes of `in` (and, if in_idx is not
+ * NULL, its scale/rot index planes into out_scale_idx / out_rot_idx [L][cap])
+ * preserving order.  reset_mask_logit: if not NaN, survivors' mask is set to
+ * it (sliding-window reset).  keep_map [n] (optional) = new index or -1.
+ * n_kept_dev: device int64 survivor count.
+ * ws: csplat_workspace_bytes(CSPLAT_OP_MASK_PRUNE, n, 0, NULL). */
+int csplat_mask_prune(const csplat_gaussians *in, const csplat_codebook *in_idx, float mask_eps,
+                      float reset_mask_logit, const csplat_gaussians_out *out,
+                      void *out_scale_idx, void *out_rot_idx, int32_t *keep_map,
+                      int64_t *n_kept_dev, void *ws, size_t ws_bytes, void *stream);
+
+enum csplat_op { CSPLAT_OP_BIN_TILES = 1, CSPLAT_OP_RENDER_BWD = 2, CSPLAT_OP_MASK_PRUNE = 3 };
+
+/* Scratch bytes needed by `op` for n Gaussians / pair_capacity pairs. */
+size_t csplat_workspace_bytes(int op, int64_t n, int64_t pair_capacity, const csplat_camera *cam);
+
+/* Copies the calling thread's last error text into buf (host); returns its length. */
+int csplat_last_error(char *buf, size_t len);
+const char *csplat_status_string(int status);
+/* ABI version (major << 16 | minor). */
+int csplat_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

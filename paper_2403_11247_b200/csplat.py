@@ -1,0 +1,318 @@
+"""Thin Python binding over libcsplat.so (include/csplat.h).
+
+Argument marshalling only: torch tensors supply device memory and the current
+CUDA stream; every step of the hot path runs in the library's sm_100a kernels.
+There is no CPU fallback -- if the library is missing or the device is not a
+B200 the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libcsplat.so")
+
+TILE = 16
+RECORD_BYTES = 64
+SYNC, POSE_ONLY, ACCUMULATE = 1, 2, 4
+OP_BIN_TILES, OP_RENDER_BWD, OP_MASK_PRUNE = 1, 2, 3
+
+
+class CsplatError(RuntimeError):
+    pass
+
+
+class Camera(C.Structure):
+    _fields_ = [("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("width", C.c_int32), ("height", C.c_int32), ("near_z", C.c_float),
+                ("far_z", C.c_float)]
+
+
+class View(C.Structure):
+    _fields_ = [("m", C.c_float * 12)]
+
+
+class Params(C.Structure):
+    _fields_ = [("mask_eps", C.c_float), ("alpha_max", C.c_float), ("t_min", C.c_float),
+                ("dilation", C.c_float)]
+
+
+class Gaussians(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_dev", C.c_void_p), ("mean", C.c_void_p),
+                ("opacity", C.c_void_p), ("rgb", C.c_void_p), ("log_scale", C.c_void_p),
+                ("quat", C.c_void_p), ("mask", C.c_void_p)]
+
+
+class GaussiansOut(C.Structure):
+    _fields_ = [("capacity", C.c_int64), ("mean", C.c_void_p), ("opacity", C.c_void_p),
+                ("rgb", C.c_void_p), ("log_scale", C.c_void_p), ("quat", C.c_void_p),
+                ("mask", C.c_void_p)]
+
+
+class Codebook(C.Structure):
+    _fields_ = [("stages", C.c_int32), ("size", C.c_int32), ("idx_bytes", C.c_int32),
+                ("reserved", C.c_int32), ("scale_codes", C.c_void_p), ("rot_codes", C.c_void_p),
+                ("scale_idx", C.c_void_p), ("rot_idx", C.c_void_p)]
+
+
+class Grads(C.Structure):
+    _fields_ = [("mean", C.c_void_p), ("opacity", C.c_void_p), ("rgb", C.c_void_p),
+                ("log_scale", C.c_void_p), ("quat", C.c_void_p), ("mask", C.c_void_p),
+                ("pose", C.c_void_p)]
+
+
+EXPORTS = ["csplat_project", "csplat_bin_tiles", "csplat_render_fwd", "csplat_render_bwd",
+           "csplat_rvq_assign", "csplat_mask_prune", "csplat_workspace_bytes",
+           "csplat_last_error", "csplat_status_string", "csplat_version"]
+
+_lib = None
+
+
+def lib():
+    """Load libcsplat.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CsplatError(f"{LIB_PATH} is missing: build it with __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32, u32 = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32
+        L.csplat_project.argtypes = [vp] * 8
+        L.csplat_bin_tiles.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp, vp, u32, vp, C.c_size_t, vp]
+        L.csplat_render_fwd.argtypes = [vp] * 10
+        L.csplat_render_bwd.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
+        L.csplat_rvq_assign.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp]
+        L.csplat_mask_prune.argtypes = [vp, vp, C.c_float, C.c_float, vp, vp, vp, vp, vp, vp,
+                                        C.c_size_t, vp]
+        L.csplat_workspace_bytes.argtypes = [C.c_int, i64, i64, vp]
+        L.csplat_workspace_bytes.restype = C.c_size_t
+        L.csplat_last_error.argtypes = [C.c_char_p, C.c_size_t]
+        L.csplat_status_string.argtypes = [C.c_int]
+        L.csplat_status_string.restype = C.c_char_p
+        for name in EXPORTS:
+            if name not in ("csplat_workspace_bytes", "csplat_status_string"):
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        buf = C.create_string_buffer(512)
+        lib().csplat_last_error(buf, 512)
+        raise CsplatError(f"{what}: {lib().csplat_status_string(status).decode()} "
+                          f"({buf.value.decode(errors='replace')})")
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def camera(cam: dict) -> Camera:
+    return Camera(cam["fx"], cam["fy"], cam["cx"], cam["cy"], cam["width"], cam["height"],
+                  cam.get("near", 0.01), cam.get("far", 100.0))
+
+
+def view(v) -> View:
+    vv = View()
+    vals = v.reshape(-1).tolist() if hasattr(v, "reshape") else list(v)
+    for i, x in enumerate(vals[:12]):
+        vv.m[i] = float(x)
+    return vv
+
+
+def params(mask_eps=0.01, alpha_max=0.99, t_min=1e-4, dilation=0.3) -> Params:
+    return Params(mask_eps, alpha_max, t_min, dilation)
+
+
+def tiles(cam: dict):
+    return (cam["width"] + TILE - 1) // TILE, (cam["height"] + TILE - 1) // TILE
+
+
+@dataclass
+class GaussianMap:
+    """Device SoA planes (float32, contiguous) in the ABI layout."""
+    mean: torch.Tensor       # [3, n]
+    opacity: torch.Tensor    # [n]
+    rgb: torch.Tensor        # [3, n]
+    log_scale: torch.Tensor  # [3, n]
+    quat: torch.Tensor       # [4, n]
+    mask: torch.Tensor       # [n]
+    n_dev: torch.Tensor | None = None
+
+    @property
+    def n(self):
+        return int(self.opacity.shape[-1])
+
+    @staticmethod
+    def from_numpy(planes: dict, device="cuda"):
+        return GaussianMap(**{k: torch.as_tensor(planes[k], dtype=torch.float32).contiguous()
+                              .to(device) for k in ("mean", "opacity", "rgb", "log_scale",
+                                                    "quat", "mask")})
+
+    def struct(self) -> Gaussians:
+        return Gaussians(self.n, _ptr(self.n_dev), _ptr(self.mean), _ptr(self.opacity),
+                         _ptr(self.rgb), _ptr(self.log_scale), _ptr(self.quat), _ptr(self.mask))
+
+
+@dataclass
+class CodebookT:
+    scale_codes: torch.Tensor  # [L, P, 3]
+    rot_codes: torch.Tensor    # [L, P, 4]
+    scale_idx: torch.Tensor    # [L, n] uint8/int16
+    rot_idx: torch.Tensor
+
+    def struct(self) -> Codebook:
+        L, P = self.scale_codes.shape[:2]
+        ib = self.scale_idx.element_size()
+        return Codebook(L, P, ib, 0, _ptr(self.scale_codes), _ptr(self.rot_codes),
+                        _ptr(self.scale_idx), _ptr(self.rot_idx))
+
+
+def _byref(x):
+    return C.byref(x) if x is not None else None
+
+
+def project(g: GaussianMap, cam: dict, v, prm: Params | None = None, cb: CodebookT | None = None,
+            rec=None, count=None, stream=None):
+    """a1+a2(decode)+a3.  Returns (rec [n,16] int32 view of the 64-B records, count [n])."""
+    n = g.n
+    dev = g.opacity.device
+    rec = rec if rec is not None else torch.empty((max(n, 1), 16), dtype=torch.int32, device=dev)
+    count = count if count is not None else torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    _check(lib().csplat_project(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
+                                C.byref(view(v)), C.byref(prm or params()), _ptr(rec),
+                                _ptr(count), _stream(stream)), "csplat_project")
+    return rec[:n], count[:n]
+
+
+def workspace_bytes(op: int, n: int, pairs: int = 0, cam: dict | None = None) -> int:
+    c = camera(cam) if cam is not None else None
+    return int(lib().csplat_workspace_bytes(op, n, pairs, _byref(c)))
+
+
+def bin_tiles(rec, count, cam: dict, capacity: int, ws=None, out=None, sync=True, stream=None):
+    """a4+a5.  Returns dict(pair_gid, pair_rec, tile_range, n_pairs_dev[, n_pairs])."""
+    n = int(count.shape[0])
+    dev = rec.device
+    tx, ty = tiles(cam)
+    if out is None:
+        out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
+                   pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
+                   tile_range=torch.empty((tx * ty, 2), dtype=torch.int32, device=dev),
+                   n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_BIN_TILES, n, capacity, cam), dtype=torch.uint8,
+                         device=dev)
+    st = lib().csplat_bin_tiles(_ptr(rec), _ptr(count), n, C.byref(camera(cam)), capacity,
+                                _ptr(out["pair_gid"]), _ptr(out["pair_rec"]),
+                                _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]),
+                                SYNC if sync else 0, _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "csplat_bin_tiles")
+    return out
+
+
+def render_fwd(pair_rec, tile_range, cam: dict, prm: Params | None = None, out=None,
+               stream=None):
+    """a6.  Returns dict(color [3,H,W], depth, sil, t_final [H,W], n_contrib [H,W])."""
+    H, W = cam["height"], cam["width"]
+    dev = tile_range.device
+    if out is None:
+        out = dict(color=torch.empty((3, H, W), device=dev),
+                   depth=torch.empty((H, W), device=dev), sil=torch.empty((H, W), device=dev),
+                   t_final=torch.empty((H, W), device=dev),
+                   n_contrib=torch.empty((H, W), dtype=torch.int32, device=dev))
+    _check(lib().csplat_render_fwd(_ptr(pair_rec), _ptr(tile_range), C.byref(camera(cam)),
+                                   C.byref(prm or params()), _ptr(out["color"]),
+                                   _ptr(out["depth"]), _ptr(out["sil"]), _ptr(out["t_final"]),
+                                   _ptr(out["n_contrib"]), _stream(stream)), "csplat_render_fwd")
+    return out
+
+
+GRAD_SHAPES = dict(mean=3, opacity=1, rgb=3, log_scale=3, quat=4, mask=1)
+
+
+def alloc_grads(n: int, device="cuda", pose_only=False):
+    g = {} if pose_only else {k: torch.zeros((c, n) if c > 1 else (n,), device=device)
+                              for k, c in GRAD_SHAPES.items()}
+    g["pose"] = torch.zeros(6, device=device)
+    return g
+
+
+def render_bwd(g: GaussianMap, cam: dict, v, rec, pair_rec, tile_range, t_final, n_contrib,
+               d_color, d_depth, d_sil, prm: Params | None = None, cb: CodebookT | None = None,
+               flags: int = 0, grads=None, ws=None, stream=None):
+    """a7+a8.  Returns the grads dict (mean, opacity, rgb, log_scale, quat, mask, pose)."""
+    n = g.n
+    dev = g.opacity.device
+    if grads is None:
+        grads = alloc_grads(n, dev, pose_only=bool(flags & POSE_ONLY))
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_RENDER_BWD, n), dtype=torch.uint8, device=dev)
+    gr = Grads(*[_ptr(grads.get(k)) for k in ("mean", "opacity", "rgb", "log_scale", "quat",
+                                               "mask", "pose")])
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    _check(lib().csplat_render_bwd(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
+                                   C.byref(view(v)), C.byref(prm or params()), _ptr(rec),
+                                   _ptr(pair_rec), _ptr(tile_range), _ptr(t_final),
+                                   _ptr(n_contrib), _ptr(d_color), _ptr(d_depth), _ptr(d_sil),
+                                   flags, C.byref(gr), _ptr(ws), ws.numel(), _stream(stream)),
+           "csplat_render_bwd")
+    return grads
+
+
+def rvq_assign(x, codes, idx_bytes=None, n_dev=None, idx=None, recon=None, want_recon=True,
+               stream=None):
+    """a2: x [d, n] float32, codes [L, P, d] -> idx [L, n] (uint8/int16), recon [d, n]."""
+    d, n = x.shape
+    L, P, d2 = codes.shape
+    assert d2 == d
+    if idx_bytes is None:
+        idx_bytes = 1 if P <= 256 else 2
+    dev = x.device
+    if idx is None:
+        idx = torch.empty((L, max(n, 1)), dtype=torch.uint8 if idx_bytes == 1 else torch.int16,
+                          device=dev)
+    if recon is None and want_recon:
+        recon = torch.empty((d, max(n, 1)), device=dev)
+    _check(lib().csplat_rvq_assign(_ptr(x), n, _ptr(n_dev), d, _ptr(codes), L, P, _ptr(idx),
+                                   idx_bytes, _ptr(recon), _stream(stream)), "csplat_rvq_assign")
+    return idx, recon
+
+
+def mask_prune(g: GaussianMap, cb: CodebookT | None = None, mask_eps=0.01,
+               reset_mask_logit=float("nan"), out: GaussianMap | None = None, out_idx=None,
+               keep_map=None, n_kept=None, ws=None, stream=None):
+    """a9.  Returns (out GaussianMap with capacity n and n_dev = survivor count, out_idx,
+    keep_map, n_kept_dev)."""
+    n = g.n
+    dev = g.opacity.device
+    if out is None:
+        out = GaussianMap(**{k: torch.empty_like(getattr(g, k)) for k in
+                             ("mean", "opacity", "rgb", "log_scale", "quat", "mask")})
+    if cb is not None and out_idx is None:
+        out_idx = (torch.empty_like(cb.scale_idx), torch.empty_like(cb.rot_idx))
+    if n_kept is None:
+        n_kept = torch.zeros(1, dtype=torch.int64, device=dev)
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_MASK_PRUNE, n), dtype=torch.uint8, device=dev)
+    o = GaussiansOut(out.n, _ptr(out.mean), _ptr(out.opacity), _ptr(out.rgb),
+                     _ptr(out.log_scale), _ptr(out.quat), _ptr(out.mask))
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    _check(lib().csplat_mask_prune(C.byref(gs), _byref(cbs), mask_eps, reset_mask_logit,
+                                   C.byref(o), _ptr(out_idx[0]) if out_idx else None,
+                                   _ptr(out_idx[1]) if out_idx else None, _ptr(keep_map),
+                                   _ptr(n_kept), _ptr(ws), ws.numel(), _stream(stream)),
+           "csplat_mask_prune")
+    out.n_dev = n_kept
+    return out, out_idx, keep_map, n_kept

@@ -1,0 +1,308 @@
+// api.cu -- the extern "C" boundary of libcsplat (include/csplat.h): argument
+// validation, device check, workspace sizing, error reporting, and the kernel
+// launches of the other translation units.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace {
+
+thread_local char g_err[512] = {0};
+
+void set_err(const char *msg) {
+  std::snprintf(g_err, sizeof(g_err), "%s", msg);
+}
+
+int cuda_status(cudaError_t e, const char *where) {
+  if (e == cudaSuccess) return CSPLAT_OK;
+  std::snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorName(e),
+                cudaGetErrorString(e));
+  return CSPLAT_ERR_CUDA;
+}
+
+int check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  static thread_local int cached_dev = -1, cached_ok = 0;
+  if (cached_dev == dev) return cached_ok ? CSPLAT_OK : CSPLAT_ERR_UNSUPPORTED;
+  int major = 0;
+  e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+  cached_dev = dev;
+  cached_ok = major == 10;
+  if (!cached_ok) {
+    set_err("csplat requires a compute capability 10.x (B200, sm_100a) device");
+    return CSPLAT_ERR_UNSUPPORTED;
+  }
+  return CSPLAT_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int invalid(const char *msg) {
+  set_err(msg);
+  return CSPLAT_ERR_INVALID_ARG;
+}
+
+int check_camera(const csplat_camera *c) {
+  if (!c) return invalid("camera is NULL");
+  if (c->width <= 0 || c->height <= 0 || c->width > 65535 || c->height > 65535)
+    return invalid("camera width/height out of range (1..65535)");
+  if (!(c->fx > 0) || !(c->fy > 0)) return invalid("fx, fy must be > 0");
+  if (!(c->near_z > 0) || !(c->far_z > c->near_z)) return invalid("need 0 < near < far");
+  if (!std::isfinite(c->cx) || !std::isfinite(c->cy)) return invalid("cx, cy must be finite");
+  return CSPLAT_OK;
+}
+
+int check_gaussians(const csplat_gaussians *g, bool need_rgb = true) {
+  if (!g) return invalid("gaussians is NULL");
+  if (g->n < 0 || g->n > 0xffffffffLL) return invalid("n out of range");
+  if (g->n == 0) return CSPLAT_OK;
+  if (!g->mean || !g->opacity || !g->mask || (need_rgb && !g->rgb))
+    return invalid("a required Gaussian plane is NULL");
+  const void *ps[6] = {g->mean, g->opacity, g->rgb, g->log_scale, g->quat, g->mask};
+  for (const void *p : ps)
+    if (p && !aligned16(p)) {
+      set_err("Gaussian planes must be 16-byte aligned");
+      return CSPLAT_ERR_ALIGNMENT;
+    }
+  return CSPLAT_OK;
+}
+
+int check_codebook(const csplat_codebook *cb, bool need_codes) {
+  if (!cb) return CSPLAT_OK;
+  if (cb->stages < 1 || cb->stages > 16) return invalid("codebook stages must be 1..16");
+  if (cb->size < 1 || cb->size > 65536) return invalid("codebook size must be 1..65536");
+  if (cb->idx_bytes != 1 && cb->idx_bytes != 2) return invalid("idx_bytes must be 1 or 2");
+  if (cb->idx_bytes == 1 && cb->size > 256) return invalid("idx_bytes=1 needs size <= 256");
+  if (!cb->scale_idx || !cb->rot_idx) return invalid("codebook index planes are NULL");
+  if (need_codes) {
+    if (!cb->scale_codes || !cb->rot_codes) return invalid("codebook codes are NULL");
+    if (!aligned16(cb->rot_codes)) {
+      set_err("rot_codes must be 16-byte aligned");
+      return CSPLAT_ERR_ALIGNMENT;
+    }
+  }
+  return CSPLAT_OK;
+}
+
+csplat::DecodeArgs decode_args(const csplat_codebook *cb) {
+  csplat::DecodeArgs d{};
+  d.L = cb->stages;
+  d.P = cb->size;
+  d.idx_bytes = cb->idx_bytes;
+  d.scale_codes = cb->scale_codes;
+  d.rot_codes = cb->rot_codes;
+  d.scale_idx = cb->scale_idx;
+  d.rot_idx = cb->rot_idx;
+  return d;
+}
+
+float mask_tau(float eps) {
+  // R12: tau = fl32(ln(eps / (1 - eps))) evaluated in double
+  const double e = (double)eps;
+  return (float)std::log(e / (1.0 - e));
+}
+
+#define RET_IF(x)            \
+  do {                       \
+    const int _s = (x);      \
+    if (_s != CSPLAT_OK) return _s; \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int csplat_version(void) { return (1 << 16) | 0; }
+
+const char *csplat_status_string(int s) {
+  switch (s) {
+    case CSPLAT_OK: return "ok";
+    case CSPLAT_ERR_INVALID_ARG: return "invalid argument";
+    case CSPLAT_ERR_ALIGNMENT: return "misaligned buffer";
+    case CSPLAT_ERR_CAPACITY: return "pair capacity exceeded";
+    case CSPLAT_ERR_WORKSPACE: return "workspace too small";
+    case CSPLAT_ERR_CUDA: return "CUDA error";
+    case CSPLAT_ERR_UNSUPPORTED: return "unsupported device";
+    default: return "unknown status";
+  }
+}
+
+int csplat_last_error(char *buf, size_t len) {
+  const int n = (int)std::strlen(g_err);
+  if (buf && len) {
+    std::strncpy(buf, g_err, len - 1);
+    buf[len - 1] = 0;
+  }
+  return n;
+}
+
+size_t csplat_workspace_bytes(int op, int64_t n, int64_t pairs, const csplat_camera *cam) {
+  switch (op) {
+    case CSPLAT_OP_BIN_TILES: return cam ? csplat::bin_workspace_bytes(n, pairs, *cam) : 0;
+    case CSPLAT_OP_RENDER_BWD: return csplat::bwd_workspace_bytes(n);
+    case CSPLAT_OP_MASK_PRUNE: return csplat::prune_workspace_bytes(n);
+    default: return 0;
+  }
+}
+
+int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const csplat_camera *cam,
+                   const csplat_view *view, const csplat_params *prm, void *rec, int32_t *count,
+                   void *stream) {
+  RET_IF(check_gaussians(g));
+  RET_IF(check_camera(cam));
+  RET_IF(check_codebook(cb, true));
+  if (!view || !prm) return invalid("view/params NULL");
+  if (g->n > 0 && (!rec || !count)) return invalid("rec/count NULL");
+  if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  if (!(prm->mask_eps > 0.f) || !(prm->mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
+  RET_IF(check_device());
+  csplat::DecodeArgs d;
+  if (cb) d = decode_args(cb);
+  return cuda_status(csplat::launch_project(*g, cb ? &d : nullptr, *cam, *view,
+                                            mask_tau(prm->mask_eps), prm->dilation, rec, count,
+                                            static_cast<cudaStream_t>(stream)),
+                     "csplat_project");
+}
+
+int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csplat_camera *cam,
+                     int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                     uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
+                     size_t ws_bytes, void *stream) {
+  RET_IF(check_camera(cam));
+  if (n < 0 || pair_capacity < 0 || pair_capacity > 0xffffffffLL) return invalid("n/capacity out of range");
+  if (!tile_range || !n_pairs_dev) return invalid("tile_range/n_pairs NULL");
+  if (n > 0 && (!rec || !count)) return invalid("rec/count NULL");
+  if (pair_capacity > 0 && (!pair_gid || !pair_rec)) return invalid("pair_gid/pair_rec NULL");
+  if (!aligned16(rec) || !aligned16(pair_rec)) {
+    set_err("rec/pair_rec must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  const size_t need = csplat::bin_workspace_bytes(n, pair_capacity, *cam);
+  if (!ws || ws_bytes < need) {
+    set_err("bin_tiles workspace too small");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  RET_IF(check_device());
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RET_IF(cuda_status(csplat::launch_bin(rec, count, n, *cam, pair_capacity, pair_gid, pair_rec,
+                                        tile_range, n_pairs_dev, ws, s),
+                     "csplat_bin_tiles"));
+  if (flags & CSPLAT_SYNC) {
+    int64_t total = 0;
+    RET_IF(cuda_status(cudaMemcpyAsync(&total, n_pairs_dev, sizeof(total), cudaMemcpyDeviceToHost, s),
+                       "csplat_bin_tiles readback"));
+    RET_IF(cuda_status(cudaStreamSynchronize(s), "csplat_bin_tiles sync"));
+    if (total > pair_capacity) {
+      std::snprintf(g_err, sizeof(g_err), "%lld pairs exceed capacity %lld", (long long)total,
+                    (long long)pair_capacity);
+      return CSPLAT_ERR_CAPACITY;
+    }
+  }
+  return CSPLAT_OK;
+}
+
+int csplat_render_fwd(const void *pair_rec, const uint32_t *tile_range, const csplat_camera *cam,
+                      const csplat_params *prm, float *color, float *depth, float *silhouette,
+                      float *t_final, int32_t *n_contrib, void *stream) {
+  RET_IF(check_camera(cam));
+  if (!prm || !tile_range || !color || !depth || !silhouette || !t_final || !n_contrib)
+    return invalid("render_fwd: NULL argument");
+  if (!aligned16(pair_rec)) {
+    set_err("pair_rec must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_render_fwd(pair_rec, tile_range, *cam, *prm, color, depth,
+                                               silhouette, t_final, n_contrib,
+                                               static_cast<cudaStream_t>(stream)),
+                     "csplat_render_fwd");
+}
+
+int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
+                      const csplat_camera *cam, const csplat_view *view, const csplat_params *prm,
+                      const void *rec, const void *pair_rec, const uint32_t *tile_range,
+                      const float *t_final, const int32_t *n_contrib, const float *d_color,
+                      const float *d_depth, const float *d_silhouette, uint32_t flags,
+                      const csplat_grads *out, void *ws, size_t ws_bytes, void *stream) {
+  RET_IF(check_gaussians(g, false));
+  RET_IF(check_camera(cam));
+  RET_IF(check_codebook(cb, true));
+  if (!view || !prm || !out || !tile_range || !t_final || !n_contrib || !d_color || !d_depth ||
+      !d_silhouette)
+    return invalid("render_bwd: NULL argument");
+  if (g->n > 0 && !rec) return invalid("rec NULL");
+  if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
+  if (!aligned16(rec) || !aligned16(pair_rec)) {
+    set_err("rec/pair_rec must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  if (!ws || ws_bytes < csplat::bwd_workspace_bytes(g->n) || !aligned16(ws)) {
+    set_err("render_bwd workspace too small or misaligned");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  RET_IF(check_device());
+  csplat::DecodeArgs d;
+  if (cb) d = decode_args(cb);
+  return cuda_status(csplat::launch_render_bwd(*g, cb ? &d : nullptr, *cam, *view, *prm, rec,
+                                               pair_rec, tile_range, t_final, n_contrib, d_color,
+                                               d_depth, d_silhouette, flags, *out, ws,
+                                               static_cast<cudaStream_t>(stream)),
+                     "csplat_render_bwd");
+}
+
+int csplat_rvq_assign(const float *x, int64_t n, const int64_t *n_dev, int32_t d,
+                      const float *codes, int32_t L, int32_t P, void *idx_out, int32_t idx_bytes,
+                      float *recon_out, void *stream) {
+  if (n < 0) return invalid("n < 0");
+  if (d < 1 || d > 8) return invalid("d must be 1..8");
+  if (L < 1 || L > 16) return invalid("L must be 1..16");
+  if (P < 1 || P > 65536) return invalid("P must be 1..65536");
+  if (idx_bytes != 1 && idx_bytes != 2) return invalid("idx_bytes must be 1 or 2");
+  if (idx_bytes == 1 && P > 256) return invalid("idx_bytes=1 needs P <= 256");
+  if (n > 0 && (!x || !codes || !idx_out)) return invalid("rvq: NULL argument");
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_rvq(x, n, n_dev, d, codes, L, P, idx_out, idx_bytes, recon_out,
+                                        static_cast<cudaStream_t>(stream)),
+                     "csplat_rvq_assign");
+}
+
+int csplat_mask_prune(const csplat_gaussians *in, const csplat_codebook *in_idx, float mask_eps,
+                      float reset_mask_logit, const csplat_gaussians_out *out,
+                      void *out_scale_idx, void *out_rot_idx, int32_t *keep_map,
+                      int64_t *n_kept_dev, void *ws, size_t ws_bytes, void *stream) {
+  RET_IF(check_gaussians(in));
+  if (in->n > 0 && (!in->log_scale || !in->quat)) return invalid("log_scale/quat NULL");
+  if (!out || !n_kept_dev) return invalid("out/n_kept NULL");
+  if (out->capacity < in->n) return invalid("out capacity < n");
+  if (in->n > 0 && (!out->mean || !out->opacity || !out->rgb || !out->log_scale || !out->quat ||
+                    !out->mask))
+    return invalid("an output plane is NULL");
+  if (in_idx) {
+    RET_IF(check_codebook(in_idx, false));
+    if (!out_scale_idx || !out_rot_idx) return invalid("output index planes NULL");
+  }
+  if (!(mask_eps > 0.f) || !(mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
+  if (!ws || ws_bytes < csplat::prune_workspace_bytes(in->n)) {
+    set_err("mask_prune workspace too small");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  RET_IF(check_device());
+  csplat::DecodeArgs d;
+  if (in_idx) d = decode_args(in_idx);
+  return cuda_status(csplat::launch_prune(*in, in_idx ? &d : nullptr, mask_tau(mask_eps),
+                                          reset_mask_logit, *out, out_scale_idx, out_rot_idx,
+                                          keep_map, n_kept_dev, ws,
+                                          static_cast<cudaStream_t>(stream)),
+                     "csplat_mask_prune");
+}
+
+}  // extern "C"

@@ -1,0 +1,187 @@
+// common.cuh -- internal helpers of libcsplat (sm_100a).  Not part of the ABI.
+//
+// Decision arithmetic (DA): every value that feeds a discrete
+// decision is computed with the explicitly rounded intrinsics below, which
+// nvcc never contracts into FMAs or reassociates.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "csplat.h"
+
+namespace csplat {
+
+constexpr int kTile = CSPLAT_TILE;
+constexpr int kRecWords = 16;
+
+#define DADD __fadd_rn
+#define DSUB __fsub_rn
+#define DMUL __fmul_rn
+#define DDIV __fdiv_rn
+#define DFMA __fmaf_rn
+#define DSQRT __fsqrt_rn
+
+// exact 2^k for k in [-126, 127]
+__device__ __forceinline__ float da_pow2(int k) { return __int_as_float((k + 127) << 23); }
+
+// DA exp (DESIGN.md §3 "pexp")
+__device__ __forceinline__ float da_pexp(float x) {
+  x = fminf(fmaxf(x, -86.0f), 88.0f);
+  const float k = rintf(DMUL(x, 1.44269504f));
+  float r = DFMA(-k, 0.693145751953125f, x);
+  r = DFMA(-k, 1.42860677e-06f, r);
+  float p = 1.98412698e-4f;
+  p = DFMA(p, r, 1.38888889e-3f);
+  p = DFMA(p, r, 8.33333333e-3f);
+  p = DFMA(p, r, 4.16666667e-2f);
+  p = DFMA(p, r, 0.166666667f);
+  p = DFMA(p, r, 0.5f);
+  p = DFMA(p, r, 1.0f);
+  p = DFMA(p, r, 1.0f);
+  return DMUL(p, da_pow2((int)k));
+}
+
+// DA log for normal positive x (DESIGN.md §3 "plog"); frexp done on the bits.
+__device__ __forceinline__ float da_plog(float x) {
+  const uint32_t b = __float_as_uint(x);
+  int e = (int)((b >> 23) & 0xffu) - 126;
+  float m = __uint_as_float((b & 0x807fffffu) | (126u << 23));  // [0.5, 1)
+  if (m < 0.707106781f) {
+    m = DADD(m, m);
+    e = e - 1;
+  }
+  const float f = DSUB(m, 1.0f);
+  const float s = DDIV(f, DADD(2.0f, f));
+  const float t = DMUL(s, s);
+  float p = DFMA(t, 0.111111111f, 0.142857143f);
+  p = DFMA(t, p, 0.2f);
+  p = DFMA(t, p, 0.333333333f);
+  p = DFMA(t, p, 1.0f);
+  const float ef = (float)e;
+  return DFMA(ef, 0.693145751953125f, DFMA(ef, 1.42860677e-06f, DMUL(DADD(s, s), p)));
+}
+
+__device__ __forceinline__ float da_sigm(float x) {
+  return DDIV(1.0f, DADD(1.0f, da_pexp(-x)));
+}
+
+// Per-pixel DA q of a record ("per pixel").
+__device__ __forceinline__ float da_q(float px, float py, float u, float v, float ca, float cb2,
+                                      float cc) {
+  const float dx = DSUB(px, u), dy = DSUB(py, v);
+  return DFMA(DMUL(ca, dx), dx, DFMA(DMUL(cb2, dx), dy, DMUL(DMUL(cc, dy), dy)));
+}
+
+__device__ __forceinline__ int64_t eff_n(int64_t n, const int64_t *n_dev) {
+  if (!n_dev) return n;
+  const int64_t m = *n_dev;
+  return m < n ? (m < 0 ? 0 : m) : n;
+}
+
+// --- Blackwell async-copy plumbing (TMA bulk copies + mbarriers) ----------
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 1-D TMA bulk copy global -> shared, completion signalled on `bar`.
+__device__ __forceinline__ void tma_load_1d(void *dst_smem, const void *src_gmem, uint32_t bytes,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// --- host-side launchers (defined in the .cu files) -------------------------
+
+struct CamInfo {
+  int W, H, tiles_x, tiles_y;
+};
+inline CamInfo cam_info(const csplat_camera &c) {
+  CamInfo i;
+  i.W = c.width;
+  i.H = c.height;
+  i.tiles_x = (c.width + kTile - 1) / kTile;
+  i.tiles_y = (c.height + kTile - 1) / kTile;
+  return i;
+}
+
+struct DecodeArgs {
+  int L, P, idx_bytes;
+  const float *scale_codes, *rot_codes;
+  const void *scale_idx, *rot_idx;
+};
+
+cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
+                           const csplat_camera &cam, const csplat_view &view, float tau,
+                           float dilation, void *rec, int32_t *count, cudaStream_t s);
+
+size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam);
+cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
+                       int64_t cap, uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                       int64_t *n_pairs_dev, void *ws, cudaStream_t s);
+
+cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
+                              const csplat_camera &cam, const csplat_params &prm, float *color,
+                              float *depth, float *sil, float *t_final, int32_t *n_contrib,
+                              cudaStream_t s);
+
+size_t bwd_workspace_bytes(int64_t n);
+cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
+                              const csplat_camera &cam, const csplat_view &view,
+                              const csplat_params &prm, const void *rec, const void *pair_rec,
+                              const uint32_t *tile_range, const float *t_final,
+                              const int32_t *n_contrib, const float *d_color, const float *d_depth,
+                              const float *d_sil, uint32_t flags, const csplat_grads &out,
+                              void *ws, cudaStream_t s);
+
+cudaError_t launch_rvq(const float *x, int64_t n, const int64_t *n_dev, int d, const float *codes,
+                       int L, int P, void *idx, int idx_bytes, float *recon, cudaStream_t s);
+
+size_t prune_workspace_bytes(int64_t n);
+cudaError_t launch_prune(const csplat_gaussians &in, const DecodeArgs *idx, float tau,
+                         float reset, const csplat_gaussians_out &out, void *out_sidx,
+                         void *out_ridx, int32_t *keep_map, int64_t *n_kept, void *ws,
+                         cudaStream_t s);
+
+}  // namespace csplat

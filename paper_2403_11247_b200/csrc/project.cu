@@ -1,0 +1,197 @@
+// project.cu -- a1 (mask, Eq 6-7), a2 decode (Eq 10) and a3
+// (EWA projection, Eq 1-2) in decision arithmetic.
+//
+// One thread per Gaussian: coalesced SoA loads of the 15 attribute planes,
+// the R-VQ decode gathers from the (L1/L2-resident) codebooks, and one 64-byte
+// record written as four 16-byte stores.  HBM-bound: 60 B in + 64 B + 4 B out
+// per Gaussian (raw geometry); DA keeps it at ~300 instructions per Gaussian.
+#include "common.cuh"
+
+namespace csplat {
+
+struct ProjConst {
+  float V[12];
+  float fx, fy, cx, cy, Wf, Hf, near_z, far_z;
+  float lx_lo, lx_hi, ly_lo, ly_hi;
+  float tau, dil;
+};
+
+__device__ __forceinline__ uint32_t load_idx(const void *p, int bytes, int64_t off) {
+  return bytes == 1 ? (uint32_t)((const uint8_t *)p)[off] : (uint32_t)((const uint16_t *)p)[off];
+}
+
+__global__ void __launch_bounds__(256) k_project(
+    int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
+    const float *__restrict__ opac, const float *__restrict__ rgb,
+    const float *__restrict__ lsc, const float *__restrict__ quat,
+    const float *__restrict__ mask, DecodeArgs dec, int use_dec, ProjConst pc,
+    float4 *__restrict__ rec, int32_t *__restrict__ count) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t ne = eff_n(n, n_dev);
+  float4 *r = rec + i * 4;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  bool ok = i < ne;
+  float m = ok ? mask[i] : 0.f;
+  ok = ok && (m > pc.tau);  // Eq 6: M = 1[Sig(m) > eps]  <=>  m > tau (R12)
+  float ls0 = 0, ls1 = 0, ls2 = 0, qw = 0, qx = 0, qy = 0, qz = 0;
+  float mx = 0, my = 0, mz = 0, o = 0, cr = 0, cg = 0, cb = 0;
+  if (ok) {
+    if (use_dec) {
+      // Eq 10: S_hat^L = sum_l C^l[i^l], summed in stage order (R17, R20)
+      for (int l = 0; l < dec.L; l++) {
+        const uint32_t si = load_idx(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i);
+        const uint32_t ri = load_idx(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i);
+        const float *sc = dec.scale_codes + ((int64_t)l * dec.P + si) * 3;
+        const float4 rc = __ldg(reinterpret_cast<const float4 *>(dec.rot_codes) +
+                                ((int64_t)l * dec.P + ri));
+        const float s0 = __ldg(sc), s1 = __ldg(sc + 1), s2 = __ldg(sc + 2);
+        if (l == 0) {
+          ls0 = s0; ls1 = s1; ls2 = s2;
+          qw = rc.x; qx = rc.y; qy = rc.z; qz = rc.w;
+        } else {
+          ls0 = DADD(ls0, s0); ls1 = DADD(ls1, s1); ls2 = DADD(ls2, s2);
+          qw = DADD(qw, rc.x); qx = DADD(qx, rc.y); qy = DADD(qy, rc.z); qz = DADD(qz, rc.w);
+        }
+      }
+    } else {
+      ls0 = lsc[i]; ls1 = lsc[n + i]; ls2 = lsc[2 * n + i];
+      qw = quat[i]; qx = quat[n + i]; qy = quat[2 * n + i]; qz = quat[3 * n + i];
+    }
+    mx = mean[i]; my = mean[n + i]; mz = mean[2 * n + i];
+    o = opac[i];
+    cr = rgb[i]; cg = rgb[n + i]; cb = rgb[2 * n + i];
+    ok = isfinite(mx) && isfinite(my) && isfinite(mz) && isfinite(o) && isfinite(ls0) &&
+         isfinite(ls1) && isfinite(ls2) && isfinite(qw) && isfinite(qx) && isfinite(qy) &&
+         isfinite(qz) && isfinite(cr) && isfinite(cg) && isfinite(cb);
+  }
+  float oh = 0, k2 = 0, xc = 0, yc = 0, zc = 0;
+  if (ok) {
+    oh = da_sigm(o);
+    const float a255 = DMUL(255.0f, oh);
+    ok = a255 > 1.0f;  // alpha >= 1/255 reachable (R2)
+    k2 = DMUL(2.0f, da_plog(a255));
+    const float *V = pc.V;
+    xc = DADD(DADD(DADD(DMUL(V[0], mx), DMUL(V[1], my)), DMUL(V[2], mz)), V[3]);
+    yc = DADD(DADD(DADD(DMUL(V[4], mx), DMUL(V[5], my)), DMUL(V[6], mz)), V[7]);
+    zc = DADD(DADD(DADD(DMUL(V[8], mx), DMUL(V[9], my)), DMUL(V[10], mz)), V[11]);
+    ok = ok && (zc > pc.near_z) && (zc < pc.far_z);  // R21
+  }
+  float nq = 0;
+  if (ok) {
+    nq = DADD(DADD(DADD(DMUL(qw, qw), DMUL(qx, qx)), DMUL(qy, qy)), DMUL(qz, qz));
+    ok = nq > 0.0f;
+  }
+  if (!ok) {
+    r[0] = z4; r[1] = z4; r[2] = z4; r[3] = z4;
+    count[i] = 0;
+    return;
+  }
+  const float s0 = da_pexp(ls0), s1 = da_pexp(ls1), s2 = da_pexp(ls2);
+  const float rn = DDIV(1.0f, DSQRT(nq));
+  const float w = DMUL(qw, rn), x = DMUL(qx, rn), y = DMUL(qy, rn), z = DMUL(qz, rn);
+  float R[3][3];
+  R[0][0] = DSUB(1.0f, DMUL(2.0f, DADD(DMUL(y, y), DMUL(z, z))));
+  R[0][1] = DMUL(2.0f, DSUB(DMUL(x, y), DMUL(w, z)));
+  R[0][2] = DMUL(2.0f, DADD(DMUL(x, z), DMUL(w, y)));
+  R[1][0] = DMUL(2.0f, DADD(DMUL(x, y), DMUL(w, z)));
+  R[1][1] = DSUB(1.0f, DMUL(2.0f, DADD(DMUL(x, x), DMUL(z, z))));
+  R[1][2] = DMUL(2.0f, DSUB(DMUL(y, z), DMUL(w, x)));
+  R[2][0] = DMUL(2.0f, DSUB(DMUL(x, z), DMUL(w, y)));
+  R[2][1] = DMUL(2.0f, DADD(DMUL(y, z), DMUL(w, x)));
+  R[2][2] = DSUB(1.0f, DMUL(2.0f, DADD(DMUL(x, x), DMUL(y, y))));
+  const float sv[3] = {s0, s1, s2};
+  float M[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+#pragma unroll
+    for (int b = 0; b < 3; b++) M[a][b] = DMUL(R[a][b], sv[b]);
+  float S[3][3];  // Eq 1: Sigma = R S S^T R^T
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+#pragma unroll
+    for (int b = a; b < 3; b++) {
+      S[a][b] = DADD(DADD(DMUL(M[a][0], M[b][0]), DMUL(M[a][1], M[b][1])), DMUL(M[a][2], M[b][2]));
+      S[b][a] = S[a][b];
+    }
+  const float iz = DDIV(1.0f, zc);
+  const float txz = DMUL(xc, iz), tyz = DMUL(yc, iz);
+  const float tx = DMUL(fminf(fmaxf(txz, pc.lx_lo), pc.lx_hi), zc);  // R6
+  const float ty = DMUL(fminf(fmaxf(tyz, pc.ly_lo), pc.ly_hi), zc);
+  const float iz2 = DMUL(iz, iz);
+  const float J00 = DMUL(pc.fx, iz), J02 = DMUL(-DMUL(pc.fx, tx), iz2);
+  const float J11 = DMUL(pc.fy, iz), J12 = DMUL(-DMUL(pc.fy, ty), iz2);
+  const float *V = pc.V;
+  float A[2][3];  // A = J W
+#pragma unroll
+  for (int j = 0; j < 3; j++) {
+    A[0][j] = DADD(DMUL(J00, V[j]), DMUL(J02, V[8 + j]));
+    A[1][j] = DADD(DMUL(J11, V[4 + j]), DMUL(J12, V[8 + j]));
+  }
+  float B[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int j = 0; j < 3; j++)
+      B[a][j] = DADD(DADD(DMUL(A[a][0], S[0][j]), DMUL(A[a][1], S[1][j])), DMUL(A[a][2], S[2][j]));
+  // Eq 2 (+ R5 dilation)
+  const float sa = DADD(DADD(DADD(DMUL(B[0][0], A[0][0]), DMUL(B[0][1], A[0][1])), DMUL(B[0][2], A[0][2])), pc.dil);
+  const float sb = DADD(DADD(DMUL(B[0][0], A[1][0]), DMUL(B[0][1], A[1][1])), DMUL(B[0][2], A[1][2]));
+  const float sc = DADD(DADD(DADD(DMUL(B[1][0], A[1][0]), DMUL(B[1][1], A[1][1])), DMUL(B[1][2], A[1][2])), pc.dil);
+  const float det = DSUB(DMUL(sa, sc), DMUL(sb, sb));
+  bool ok2 = det > 0.0f;
+  const float ca = DDIV(sc, det), cbn = DDIV(-sb, det), cc = DDIV(sa, det);
+  const float u = DADD(DMUL(pc.fx, txz), pc.cx), v = DADD(DMUL(pc.fy, tyz), pc.cy);
+  const float ex = DADD(DSQRT(DMUL(k2, sa)), 1e-3f), ey = DADD(DSQRT(DMUL(k2, sc)), 1e-3f);
+  const float X0 = ceilf(DSUB(u, ex)), X1 = floorf(DADD(u, ex));
+  const float Y0 = ceilf(DSUB(v, ey)), Y1 = floorf(DADD(v, ey));
+  ok2 = ok2 && (X0 <= DSUB(pc.Wf, 1.0f)) && (X1 >= 0.0f) && (Y0 <= DSUB(pc.Hf, 1.0f)) &&
+        (Y1 >= 0.0f) && (X0 <= X1) && (Y0 <= Y1);
+  if (!ok2) {
+    r[0] = z4; r[1] = z4; r[2] = z4; r[3] = z4;
+    count[i] = 0;
+    return;
+  }
+  const int px0 = (int)fmaxf(X0, 0.0f), px1 = (int)fminf(X1, DSUB(pc.Wf, 1.0f));
+  const int py0 = (int)fmaxf(Y0, 0.0f), py1 = (int)fminf(Y1, DSUB(pc.Hf, 1.0f));
+  const int tx0 = px0 / kTile, tx1 = px1 / kTile, ty0 = py0 / kTile, ty1 = py1 / kTile;
+  r[0] = make_float4(u, v, ca, DADD(cbn, cbn));
+  r[1] = make_float4(cc, oh, k2, zc);
+  r[2] = make_float4(cr, cg, cb, __uint_as_float((uint32_t)i));
+  r[3] = make_float4(__uint_as_float((uint32_t)px0 | ((uint32_t)px1 << 16)),
+                     __uint_as_float((uint32_t)py0 | ((uint32_t)py1 << 16)), 0.f, 0.f);
+  count[i] = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+}
+
+cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
+                           const csplat_camera &cam, const csplat_view &view, float tau,
+                           float dilation, void *rec, int32_t *count, cudaStream_t s) {
+  if (g.n == 0) return cudaSuccess;
+  ProjConst pc;
+  for (int k = 0; k < 12; k++) pc.V[k] = view.m[k];
+  pc.fx = cam.fx; pc.fy = cam.fy; pc.cx = cam.cx; pc.cy = cam.cy;
+  pc.Wf = (float)cam.width; pc.Hf = (float)cam.height;
+  pc.near_z = cam.near_z; pc.far_z = cam.far_z;
+  // J clamp limits (R6), in DA on the host (IEEE float ops, no contraction:
+  // the library's host code is compiled with -fno-fast-math / fp-contract off).
+  volatile float Wf = pc.Wf, Hf = pc.Hf, c015 = 0.15f;
+  volatile float t1 = c015 * Wf, t2 = c015 * Hf;
+  volatile float a1 = pc.cx + t1, a2 = Wf - pc.cx, a3 = pc.cy + t2, a4 = Hf - pc.cy;
+  volatile float b2 = a2 + t1, b4 = a4 + t2;
+  pc.lx_lo = -(a1 / pc.fx);
+  pc.lx_hi = b2 / pc.fx;
+  pc.ly_lo = -(a3 / pc.fy);
+  pc.ly_hi = b4 / pc.fy;
+  pc.tau = tau;
+  pc.dil = dilation;
+  DecodeArgs d{};
+  if (dec) d = *dec;
+  const int threads = 256;
+  const int64_t blocks = (g.n + threads - 1) / threads;
+  k_project<<<(unsigned)blocks, threads, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.rgb,
+                                                 g.log_scale, g.quat, g.mask, d, dec ? 1 : 0, pc,
+                                                 reinterpret_cast<float4 *>(rec), count);
+  return cudaGetLastError();
+}
+
+}  // namespace csplat

@@ -1,0 +1,146 @@
+"""One pass of the whole hot path over one view,
+with every buffer preallocated so the step can be replayed or captured in a
+CUDA graph:
+
+    mask_prune (a9, a1)  ->  rvq_assign scale + rotation (a2)
+    -> project with R-VQ decode + mask (a1, a2, a3) -> bin_tiles (a4, a5)
+    -> render_fwd (a6) -> render_bwd incl. chain, STE and pose (a7, a8)
+
+Every stage is a libcsplat call (paper_2403_11247_b200.csplat); torch only
+provides device memory and streams.  The survivor count of the prune stays on
+the device (n_dev), so the step has no host synchronisation.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import csplat as cs
+
+
+class RenderStep:
+    def __init__(self, planes: dict, cam: dict, codebook: dict | None, device="cuda",
+                 prm: cs.Params | None = None, pair_capacity: int | None = None,
+                 flags: int = 0):
+        self.cam = dict(cam)
+        self.prm = prm or cs.params()
+        self.flags = flags
+        self.dev = torch.device(device)
+        self.g = cs.GaussianMap.from_numpy(planes, device=self.dev)
+        n = self.n = self.g.n
+        H, W = cam["height"], cam["width"]
+        # a9 outputs (capacity n) and the device survivor count
+        self.pruned = cs.GaussianMap(**{k: torch.empty_like(getattr(self.g, k)) for k in
+                                        ("mean", "opacity", "rgb", "log_scale", "quat", "mask")})
+        self.n_kept = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.keep_map = torch.empty(n, dtype=torch.int32, device=self.dev)
+        self.ws_prune = torch.empty(cs.workspace_bytes(cs.OP_MASK_PRUNE, n), dtype=torch.uint8,
+                                    device=self.dev)
+        # a2 codebooks and indices
+        self.codes = None
+        if codebook is not None:
+            sc = torch.as_tensor(codebook["scale_codes"], dtype=torch.float32).contiguous().to(self.dev)
+            rc = torch.as_tensor(codebook["rot_codes"], dtype=torch.float32).contiguous().to(self.dev)
+            L, P = sc.shape[:2]
+            dt = torch.uint8 if P <= 256 else torch.int16
+            self.cb = cs.CodebookT(sc, rc, torch.zeros((L, n), dtype=dt, device=self.dev),
+                                   torch.zeros((L, n), dtype=dt, device=self.dev))
+        else:
+            self.cb = None
+        # a3 outputs
+        self.rec = torch.empty((n, 16), dtype=torch.int32, device=self.dev)
+        self.count = torch.empty(n, dtype=torch.int32, device=self.dev)
+        # a4/a5: size the pair buffers from a probe bin of this scene at the first view
+        tx, ty = cs.tiles(cam)
+        self.tile_range = torch.empty((tx * ty, 2), dtype=torch.int32, device=self.dev)
+        self.n_pairs = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.capacity = pair_capacity or 1
+        self._alloc_pairs(self.capacity)
+        # a6 outputs
+        self.img = dict(color=torch.empty((3, H, W), device=self.dev),
+                        depth=torch.empty((H, W), device=self.dev),
+                        sil=torch.empty((H, W), device=self.dev),
+                        t_final=torch.empty((H, W), device=self.dev),
+                        n_contrib=torch.empty((H, W), dtype=torch.int32, device=self.dev))
+        # a7/a8
+        self.grads = cs.alloc_grads(n, self.dev, pose_only=bool(flags & cs.POSE_ONLY))
+        self.ws_bwd = torch.empty(cs.workspace_bytes(cs.OP_RENDER_BWD, n), dtype=torch.uint8,
+                                  device=self.dev)
+        self.upstream = None
+        self.graph = None
+
+    def _alloc_pairs(self, cap):
+        self.capacity = cap
+        self.pair_gid = torch.empty(cap, dtype=torch.int32, device=self.dev)
+        self.pair_rec = torch.empty((cap, 16), dtype=torch.int32, device=self.dev)
+        self.ws_bin = torch.empty(cs.workspace_bytes(cs.OP_BIN_TILES, self.n, cap, self.cam),
+                                  dtype=torch.uint8, device=self.dev)
+
+    def size_pairs(self, view, margin=1.25, views=()):
+        """Run the front of the path once (synchronously) to size the pair buffers."""
+        worst = 0
+        for v in [view, *views]:
+            self.front(v, sync_probe=True)
+            worst = max(worst, int(self.n_pairs.item()))
+        cap = int(worst * margin) + 4096
+        if cap > self.capacity:
+            self._alloc_pairs(cap)
+        return worst
+
+    def set_upstream(self, d_color, d_depth, d_sil):
+        self.upstream = (d_color, d_depth, d_sil)
+
+    # ---- stages -------------------------------------------------------------
+    def front(self, view, sync_probe=False):
+        """a9 -> a2 -> a3 -> a4/a5."""
+        g = self.pruned
+        # the codebook indices are re-assigned below, so only attribute planes are compacted
+        cs.mask_prune(self.g, None, self.prm.mask_eps, float("nan"), out=g,
+                      keep_map=self.keep_map, n_kept=self.n_kept, ws=self.ws_prune)
+        if self.cb is not None:
+            cs.rvq_assign(g.log_scale, self.cb.scale_codes, n_dev=self.n_kept,
+                          idx=self.cb.scale_idx, want_recon=False)
+            cs.rvq_assign(g.quat, self.cb.rot_codes, n_dev=self.n_kept, idx=self.cb.rot_idx,
+                          want_recon=False)
+        cs.project(g, self.cam, view, self.prm, self.cb, rec=self.rec, count=self.count)
+        if sync_probe:
+            big = max(self.capacity, 64 * self.n + 4096)
+            if big > self.capacity:
+                self._alloc_pairs(big)
+        cs.bin_tiles(self.rec, self.count, self.cam, self.capacity, ws=self.ws_bin,
+                     out=dict(pair_gid=self.pair_gid, pair_rec=self.pair_rec,
+                              tile_range=self.tile_range, n_pairs_dev=self.n_pairs),
+                     sync=sync_probe)
+
+    def forward(self):
+        cs.render_fwd(self.pair_rec, self.tile_range, self.cam, self.prm, out=self.img)
+
+    def backward(self, view, flags=None):
+        dC, dD, dS = self.upstream
+        cs.render_bwd(self.pruned, self.cam, view, self.rec, self.pair_rec, self.tile_range,
+                      self.img["t_final"], self.img["n_contrib"], dC, dD, dS, self.prm, self.cb,
+                      self.flags if flags is None else flags, grads=self.grads, ws=self.ws_bwd)
+
+    def step(self, view):
+        self.front(view)
+        self.forward()
+        self.backward(view)
+
+    def check_capacity(self):
+        n = int(self.n_pairs.item())
+        if n > self.capacity:
+            raise cs.CsplatError(f"{n} pairs exceed the capacity {self.capacity}")
+        return n
+
+    # ---- CUDA graph ------------------------------------------------------
+    def capture(self, view):
+        s = torch.cuda.Stream(device=self.dev)
+        s.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(s):
+            self.step(view)          # warm (and any lazy attribute setup) outside capture
+        torch.cuda.current_stream(self.dev).wait_stream(s)
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(view)
+        self.graph = g
+        return g

@@ -1,0 +1,299 @@
+"""GPU parity (-m gpu): the CUDA path, called through the C ABI, against the CPU
+oracle on the same seeded inputs (DESIGN.md §6 comparison policy).
+
+Bit-exact: records, counts, pair lists/order, tile ranges, R-VQ indices and
+reconstructions, survivors, keep_map.  Images: max |diff| <= 1e-4 off the
+oracle-flagged pixels, n_contrib exact there.  Gradients: rel-L2 <= 1e-3 per
+group with flagged pixels' upstream zeroed on both sides."""
+import numpy as np
+import pytest
+
+from scenes import synth
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+GROUPS = ["mean", "opacity", "rgb", "log_scale", "quat", "mask", "pose"]
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    import oracle
+    from paper_2403_11247_b200 import _build, csplat
+    _build.build()
+    oracle.build()
+    assert torch.cuda.is_available()
+    return dict(torch=torch, cs=csplat, orc=oracle, dev=torch.device("cuda:0"))
+
+
+def _codebooks(env, sc):
+    """Assign codebook indices on both sides (a2) and return both views."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sco, rco = sc.codebook["scale_codes"], sc.codebook["rot_codes"]
+    si_o, _ = orc.rvq_assign(sc.log_scale, sco)
+    ri_o, _ = orc.rvq_assign(sc.quat, rco)
+    sct, rct = torch.tensor(sco, device=dev), torch.tensor(rco, device=dev)
+    si, _ = cs.rvq_assign(torch.tensor(sc.log_scale, device=dev), sct)
+    ri, _ = cs.rvq_assign(torch.tensor(sc.quat, device=dev), rct)
+    assert np.array_equal(si.cpu().numpy().astype(np.uint16), si_o)
+    assert np.array_equal(ri.cpu().numpy().astype(np.uint16), ri_o)
+    return (cs.CodebookT(sct, rct, si, ri),
+            dict(scale_codes=sco, rot_codes=rco, scale_idx=si_o, rot_idx=ri_o))
+
+
+def run_and_compare(env, sc, view=None, use_codebook=True, prm=None, bwd=True, seed=1,
+                    flags=0):
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    cam = sc.cam
+    v = sc.views[0] if view is None else view
+    H, W = cam["height"], cam["width"]
+    cb, cbo = _codebooks(env, sc) if use_codebook and sc.codebook is not None else (None, None)
+    prm_o = orc.params(*(prm or (0.01, 0.99, 1e-4, 0.3)))
+    prm_c = cs.params(*(prm or (0.01, 0.99, 1e-4, 0.3)))
+    S = orc.Scene(**sc.planes())
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    # a3
+    rec_o, cnt_o = orc.project(S, cam, v, prm_o, codebook=cbo)
+    rec, cnt = cs.project(g, cam, v, prm_c, cb=cb)
+    rec_g = rec.cpu().numpy().view(np.uint32)
+    bad = np.nonzero((rec_g != rec_o).any(1))[0]
+    assert bad.size == 0, f"{bad.size} records differ, first {bad[:5]}"
+    assert np.array_equal(cnt.cpu().numpy(), cnt_o)
+    # a4/a5
+    gid_o, rng_o = orc.bin_tiles(rec_o, cnt_o, cam)
+    b = cs.bin_tiles(rec, cnt, cam, capacity=len(gid_o) + 128)
+    npairs = int(b["n_pairs_dev"].item())
+    assert npairs == len(gid_o)
+    gid_g = b["pair_gid"][:npairs].cpu().numpy().view(np.uint32)
+    assert np.array_equal(gid_g, gid_o)
+    assert np.array_equal(b["tile_range"].cpu().numpy().view(np.uint32), rng_o)
+    prec = b["pair_rec"][:npairs].cpu().numpy().view(np.uint32)
+    assert np.array_equal(prec, rec_o[gid_o])
+    # a6
+    out = cs.render_fwd(b["pair_rec"], b["tile_range"], cam, prm_c)
+    fo = orc.render_fwd(rec_o, gid_o, rng_o, cam, prm_o)
+    ok = fo["flags"] == 0
+    assert (~ok).sum() <= max(2, 1e-4 * H * W), (~ok).sum()
+    for k in ("depth", "sil", "t_final"):
+        err = np.abs(out[k].cpu().numpy() - fo[k])[ok]
+        assert err.size == 0 or err.max() <= IMG_TOL, (k, err.max())
+    cerr = np.abs(out["color"].cpu().numpy() - fo["color"])[:, ok]
+    assert cerr.size == 0 or cerr.max() <= IMG_TOL
+    assert np.array_equal(out["n_contrib"].cpu().numpy()[ok], fo["n_contrib"][ok])
+    res = dict(fo=fo, out=out, npairs=npairs)
+    if not bwd:
+        return res
+    # a7/a8
+    rng = np.random.default_rng(seed)
+    dC, dD, dS = synth.upstream(rng, H, W)
+    dC[:, ~ok] = 0
+    dD[~ok] = 0
+    dS[~ok] = 0
+    gr = cs.render_bwd(g, cam, v, rec, b["pair_rec"], b["tile_range"], out["t_final"],
+                       out["n_contrib"], torch.tensor(dC, device=dev), torch.tensor(dD, device=dev),
+                       torch.tensor(dS, device=dev), prm_c, cb=cb, flags=flags)
+    go = orc.render_bwd(S, cam, v, rec_o, gid_o, rng_o, dC, dD, dS, prm_o, codebook=cbo)
+    errs = {}
+    for k in GROUPS:
+        if flags & cs.POSE_ONLY and k != "pose":
+            continue
+        a = gr[k].double().cpu().numpy().reshape(-1)
+        r = go[k].reshape(-1)
+        errs[k] = np.linalg.norm(a - r) / max(np.linalg.norm(r), 1e-30)
+    assert all(e <= GRAD_TOL for e in errs.values()), errs
+    res["grad_err"] = errs
+    return res
+
+
+# ------------------------------------------------------------------ a2 / a9
+
+@pytest.mark.parametrize("LPd", [(1, 1, 3), (2, 16, 3), (2, 16, 4), (4, 256, 3), (4, 256, 4),
+                                 (3, 1000, 4), (1, 64, 7)])
+def test_rvq_parity(env, LPd):
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    L, P, d = LPd
+    rng = np.random.default_rng(L * 1000 + P + d)
+    n = 20011
+    x = rng.standard_normal((d, n)).astype(np.float32) * 0.3 - 5.0
+    codes = np.zeros((L, P, d), dtype=np.float32)
+    codes[0] = x[:, rng.choice(n, P, replace=False)].T
+    for l in range(1, L):
+        codes[l] = rng.standard_normal((P, d)) * 0.3 * 0.35 ** l
+    if P > 4:
+        codes[0, P - 1] = codes[0, 2]    # duplicate code: lowest index must win
+    idx_o, rec_o = orc.rvq_assign(x, codes)
+    idx, rec = cs.rvq_assign(torch.tensor(x, device=dev), torch.tensor(codes, device=dev))
+    assert np.array_equal(idx.cpu().numpy().astype(np.uint16), idx_o)
+    assert np.array_equal(rec.cpu().numpy(), rec_o)
+
+
+def test_rvq_parity_c4_sample(env):
+    """C4 codebook shape (4 x 256, log-scale and quaternion) on 100k Gaussians."""
+    sc = synth.scannet_scene(0, n=100_000)
+    _codebooks(env, sc)
+
+
+@pytest.mark.parametrize("with_idx,reset", [(False, float("nan")), (True, float("nan")),
+                                            (True, 1.0)])
+def test_prune_parity(env, with_idx, reset):
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.scannet_scene(0, n=50_000, parity=True)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    cb = None
+    idx_planes = []
+    if with_idx:
+        cb, cbo = _codebooks(env, sc)
+        idx_planes = list(cbo["scale_idx"]) + list(cbo["rot_idx"])
+    km = torch.empty(g.n, dtype=torch.int32, device=dev)
+    out, out_idx, km, nk = cs.mask_prune(g, cb, reset_mask_logit=reset, keep_map=km)
+    names = ["mean", "opacity", "rgb", "log_scale", "quat", "mask"]
+    planes = []
+    for k in names:
+        planes += list(getattr(sc, k).reshape(-1, sc.n))
+    outs_o, iouts_o, km_o, nk_o = orc.mask_prune(planes, idx_planes, mask_plane=14,
+                                                 reset_mask=reset)
+    k = int(nk.item())
+    assert k == nk_o
+    assert np.array_equal(km.cpu().numpy(), km_o)
+    p = 0
+    for name in names:
+        t = getattr(out, name).cpu().numpy().reshape(-1, sc.n)
+        for r in range(t.shape[0]):
+            assert np.array_equal(t[r, :k], outs_o[p]), name
+            p += 1
+    if with_idx:
+        L = cb.scale_idx.shape[0]
+        si = out_idx[0].cpu().numpy().astype(np.uint16)
+        ri = out_idx[1].cpu().numpy().astype(np.uint16)
+        for l in range(L):
+            assert np.array_equal(si[l, :k], iouts_o[l])
+            assert np.array_equal(ri[l, :k], iouts_o[L + l])
+
+
+# ------------------------------------------------------------------ a1-a8
+
+@pytest.mark.parametrize("seed", list(range(10)))
+def test_tiny_scene_parity(env, seed):
+    """C1 and seeds 0-9 of C1-shaped scenes: full fwd+bwd parity."""
+    run_and_compare(env, synth.tiny_scene(seed))
+
+
+def test_tiny_scene_raw_geometry(env):
+    run_and_compare(env, synth.tiny_scene(3), use_codebook=False)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_mid_scene_parity(env, seed):
+    """160x120 (ragged last tile row), 3000 Gaussians, 2x16 R-VQ, perturbed pose."""
+    sc = synth.mid_scene(seed)
+    view = synth.perturbed_view(np.random.default_rng(seed), rot_deg=3, trans=0.05)
+    run_and_compare(env, sc, view=view)
+
+
+def test_mid_scene_pose_only(env):
+    torch, cs = env["torch"], env["cs"]
+    sc = synth.mid_scene(4)
+    run_and_compare(env, sc, flags=cs.POSE_ONLY)
+
+
+def test_smooth_params_parity(env):
+    """No alpha cap and no termination (alpha_max = 1, t_min = 0)."""
+    sc = synth.mid_scene(5)
+    sc.opacity = np.minimum(sc.opacity, 2.0).astype(np.float32)
+    run_and_compare(env, sc, prm=(0.01, 1.0, 0.0, 0.3))
+
+
+def test_empty_and_all_culled(env):
+    torch, cs, dev = env["torch"], env["cs"], env["dev"]
+    sc = synth.tiny_scene(0)
+    sc.mask[:] = -20.0
+    res = run_and_compare(env, sc)
+    assert res["npairs"] == 0
+    assert float(res["out"]["sil"].abs().max()) == 0.0
+
+
+def test_long_tile_lists(env):
+    """Buckets longer than a warp's shared-memory slice (CTA-wide sort) and
+    longer than the CTA's shared memory (global-memory sort)."""
+    rng = np.random.default_rng(9)
+    for n in (1500, 13000):
+        cam = dict(fx=20.0, fy=20.0, cx=7.5, cy=7.5, width=32, height=16, near=0.01, far=100.0)
+        z = rng.uniform(1, 5, n)
+        px, py = rng.uniform(0, 15, n), rng.uniform(0, 15, n)
+        mean = np.stack([(px - 7.5) / 20 * z, (py - 7.5) / 20 * z, z]).astype(np.float32)
+        sc = synth.SynthScene(mean, rng.normal(-1, 1, n).astype(np.float32),
+                              rng.uniform(0, 1, (3, n)).astype(np.float32),
+                              np.log(np.full((3, n), 0.02) * z).astype(np.float32),
+                              synth._unit_quats(rng, n), np.full(n, 3.0, np.float32), cam,
+                              [synth.IDENTITY_VIEW.copy()])
+        res = run_and_compare(env, sc, use_codebook=False, bwd=(n < 5000))
+        assert res["npairs"] >= n
+
+
+def test_capacity_overflow_reported(env):
+    torch, cs, dev = env["torch"], env["cs"], env["dev"]
+    sc = synth.tiny_scene(0)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec, cnt = cs.project(g, sc.cam, sc.views[0])
+    with pytest.raises(cs.CsplatError, match="capacity"):
+        cs.bin_tiles(rec, cnt, sc.cam, capacity=5, sync=True)
+
+
+def test_pipeline_step_matches_stages(env):
+    """The graph-capturable RenderStep (prune -> R-VQ -> project -> bin -> fwd ->
+    bwd) reproduces the oracle on the pruned, decoded map."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    from paper_2403_11247_b200.pipeline import RenderStep
+    sc = synth.mid_scene(6)
+    v = sc.views[0]
+    st = RenderStep(sc.planes(), sc.cam, sc.codebook, device=dev)
+    st.size_pairs(v)
+    H, W = sc.cam["height"], sc.cam["width"]
+    dC, dD, dS = synth.upstream(np.random.default_rng(2), H, W)
+    st.set_upstream(*(torch.tensor(a, device=dev) for a in (dC, dD, dS)))
+    st.capture(v)
+    st.graph.replay()
+    torch.cuda.synchronize()
+    k = int(st.n_kept.item())
+    keep = sc.mask > orc.mask_tau(0.01)
+    assert k == keep.sum()
+    pl = {kk: vv[..., keep] for kk, vv in sc.planes().items()}
+    si, _ = orc.rvq_assign(pl["log_scale"], sc.codebook["scale_codes"])
+    ri, _ = orc.rvq_assign(pl["quat"], sc.codebook["rot_codes"])
+    cbo = dict(scale_codes=sc.codebook["scale_codes"], rot_codes=sc.codebook["rot_codes"],
+               scale_idx=si, rot_idx=ri)
+    S = orc.Scene(**pl)
+    rec_o, cnt_o = orc.project(S, sc.cam, v, codebook=cbo)
+    gid_o, rng_o = orc.bin_tiles(rec_o, cnt_o, sc.cam)
+    fo = orc.render_fwd(rec_o, gid_o, rng_o, sc.cam)
+    ok = fo["flags"] == 0
+    assert np.abs(st.img["sil"].cpu().numpy() - fo["sil"])[ok].max() <= IMG_TOL
+    assert np.abs(st.img["color"].cpu().numpy() - fo["color"])[:, ok].max() <= IMG_TOL
+    assert int(st.n_pairs.item()) == len(gid_o)
+    assert np.array_equal(st.pair_gid[:len(gid_o)].cpu().numpy().view(np.uint32), gid_o)
+    dC[:, ~ok] = 0; dD[~ok] = 0; dS[~ok] = 0
+    st.set_upstream(*(torch.tensor(a, device=dev) for a in (dC, dD, dS)))
+    st.step(v)
+    torch.cuda.synchronize()
+    go = orc.render_bwd(S, sc.cam, v, rec_o, gid_o, rng_o, dC, dD, dS, codebook=cbo)
+    for name in GROUPS:
+        a = st.grads[name].double().cpu().numpy()
+        a = a.reshape(-1) if name == "pose" else a.reshape(-1, st.n)[:, :k].reshape(-1)
+        r = go[name].reshape(-1)
+        assert np.linalg.norm(a - r) / np.linalg.norm(r) <= GRAD_TOL, name
+
+
+# ------------------------------------------------------------------ bench config (C2)
+
+@pytest.mark.slow
+def test_replica_c2_full_parity(env):
+    """BASELINE config C2 (1200x680, 200k Gaussians, 75% masked-in, R-VQ 4x256)
+    at full size in the launch configuration bench.py times: every record,
+    pair and pixel, and all gradients, against the oracle."""
+    sc = synth.replica_scene(0)
+    res = run_and_compare(env, sc)
+    fo = res["fo"]
+    assert res["npairs"] > 100_000
+    assert fo["e_pix"] > 10_000_000
