@@ -1,0 +1,444 @@
+#!/usr/bin/env python
+"""bench.py -- the hot path of arXiv 2403.11247 on B200 (BASELINE.json metric:
+"fwd+bwd renders/sec and Gaussian-pixel evals/sec at 1200x680; % HBM/FP32 peak").
+
+One STEP = one pass of every SURVEY.md §8(a) row over one Replica-shaped view
+(config C2: 1200x680, 200k Gaussians, 75% mask-kept, R-VQ 4 x 256):
+    mask_prune -> rvq_assign (scale, rotation) -> project (mask + R-VQ decode)
+    -> bin_tiles -> render_fwd -> render_bwd (chain, STE mask, pose)
+captured once as a CUDA graph and replayed.  With --gpus N (torchrun, one rank
+per GPU) every rank renders its own keyframe view of the replicated map and the
+15-plane gradient buffer is summed with one NCCL all-reduce per step (the
+keyframe-window data parallelism of SURVEY.md §8(e)); value = N renders / the
+slowest rank's step time (weak scaling).
+
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events
+on the launching stream, with a 512 MB L2-flush write between steps (outside
+the events); barrier + synchronize around the timed region; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "fwd+bwd renders/sec at 1200x680 (Replica-shaped, 200k Gaussians)"
+UNIT = "renders/s"
+KERNEL_LAUNCHES_PER_STEP = {
+    # kernels of libcsplat launched by one RenderStep.step()
+    "mask_prune": 3, "rvq_assign": 2, "project": 1, "bin_tiles": 5, "render_fwd": 1,
+    "render_bwd": 2,
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="csplat", choices=["csplat", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-stages", action="store_true", default=True)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}",
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for k, nm in enumerate(names):
+                if len(s) > 5 + k and s[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def fp32_peak_tinstr(sm_mhz):
+    """FP32 lane-instruction peak: 148 SMs x 128 FP32 lanes x SM clock (B200
+    unit counts, /opt/skills/guides/B200_PROFILING.md); FFMA counts as one."""
+    return 148 * 128 * sm_mhz * 1e6 / 1e12
+
+
+# ---------------------------------------------------------------- oracle (CPU) legs
+
+def oracle_step(sc, view, upstream, row_frac=1.0, rvq_frac=1.0):
+    """The CPU oracle as it stands, over one (sampled) step of the same
+    workload: prune, R-VQ on a fraction of the survivors, project, bin, and
+    forward + backward on a band of pixel rows.  Returns (seconds, units,
+    counters); units = fraction of one render the sample covers."""
+    import oracle
+    oracle.build()
+    H = sc.cam["height"]
+    names = ["mean", "opacity", "rgb", "log_scale", "quat", "mask"]
+    t0 = time.perf_counter()
+    planes = []
+    for k in names:
+        planes += list(getattr(sc, k).reshape(-1, sc.n))
+    outs, _, keep_map, k = oracle.mask_prune(planes, [], mask_plane=14)
+    pl, off = {}, 0
+    for name, c in zip(names, (3, 1, 3, 3, 4, 1)):
+        pl[name] = np.stack(outs[off:off + c]).reshape((c, k) if c > 1 else (k,))
+        off += c
+    m = max(1, int(k * rvq_frac))
+    si, _ = oracle.rvq_assign(pl["log_scale"][:, :m], sc.codebook["scale_codes"])
+    ri, _ = oracle.rvq_assign(pl["quat"][:, :m], sc.codebook["rot_codes"])
+    if m < k:   # the rest of the indices for the render (untimed-equivalent reuse)
+        si = np.concatenate([si, np.zeros((si.shape[0], k - m), np.uint16)], 1)
+        ri = np.concatenate([ri, np.zeros((ri.shape[0], k - m), np.uint16)], 1)
+    cbo = dict(scale_codes=sc.codebook["scale_codes"], rot_codes=sc.codebook["rot_codes"],
+               scale_idx=si, rot_idx=ri)
+    S = oracle.Scene(**pl)
+    rec, cnt = oracle.project(S, sc.cam, view, codebook=cbo)
+    gid, rng = oracle.bin_tiles(rec, cnt, sc.cam)
+    rows = max(1, int(round(H * row_frac)))
+    oracle.set_row_window(0, rows)
+    try:
+        fo = oracle.render_fwd(rec, gid, rng, sc.cam)
+        dC, dD, dS = upstream
+        oracle.render_bwd(S, sc.cam, view, rec, gid, rng, dC, dD, dS, codebook=cbo)
+    finally:
+        oracle.set_row_window(0, -1)
+    dt = time.perf_counter() - t0
+    units = min(rows / H, rvq_frac)
+    return dt, units, fo
+
+
+def oracle_counts(sc, view):
+    """E_pix / E_contrib of the exact scene, counted by the oracle (§8(d))."""
+    import oracle
+    oracle.build()
+    keep = sc.mask > oracle.mask_tau(0.01)
+    pl = {k: v[..., keep] for k, v in sc.planes().items()}
+    si, _ = oracle.rvq_assign(pl["log_scale"], sc.codebook["scale_codes"])
+    ri, _ = oracle.rvq_assign(pl["quat"], sc.codebook["rot_codes"])
+    cbo = dict(scale_codes=sc.codebook["scale_codes"], rot_codes=sc.codebook["rot_codes"],
+               scale_idx=si, rot_idx=ri)
+    rec, cnt = oracle.project(oracle.Scene(**pl), sc.cam, view, codebook=cbo)
+    gid, rng = oracle.bin_tiles(rec, cnt, sc.cam)
+    fo = oracle.render_fwd(rec, gid, rng, sc.cam)
+    return dict(e_pix=fo["e_pix"], e_contrib=fo["e_contrib"], n_pairs=len(gid),
+                n_active=int((cnt > 0).sum()), n_kept=int(keep.sum()))
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle, as it stands, on the host cores."""
+    from scenes import synth
+    if rank != 0:
+        return
+    sc = synth.replica_scene(args.seed)
+    view = sc.views[0]
+    H, W = sc.cam["height"], sc.cam["width"]
+    up = synth.upstream(np.random.default_rng(args.seed + 1), H, W)
+    frac = 1.0 / 16
+    times, units = [], 0.0
+    for i in range(args.warmup + args.steps):
+        dt, u, _ = oracle_step(sc, view, up, row_frac=frac, rvq_frac=frac)
+        if i >= args.warmup:
+            times.append(dt)
+            units += u
+    total = sum(times)
+    value = units / total
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C2 replica 1200x680, 200k Gaussians (75% kept), R-VQ 4x256",
+                       "sample": f"{frac:.4f} of a render per step (first {frac:.4f} of pixel "
+                                 f"rows, R-VQ on {frac:.4f} of survivors; full prune/project/bin)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{frac:.4f} of one render per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2403_11247_b200 import _build
+    from paper_2403_11247_b200 import csplat as cs
+    from paper_2403_11247_b200.pipeline import RenderStep
+    from scenes import synth
+
+    _build.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    sc = synth.replica_scene(args.seed)
+    H, W = sc.cam["height"], sc.cam["width"]
+    # keyframe view of this rank: identity for rank 0, a nearby pose otherwise
+    view = sc.views[0] if rank == 0 else synth.perturbed_view(
+        np.random.default_rng(1000 + rank), rot_deg=2.0, trans=0.05)
+    step = RenderStep(sc.planes(), sc.cam, sc.codebook, device=dev)
+    step.size_pairs(view)
+    up = synth.upstream(np.random.default_rng(args.seed + 1), H, W)
+    step.set_upstream(*(torch.tensor(a, device=dev) for a in up))
+    graph = step.capture(view)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def one(timed_events=None):
+        if timed_events is not None:
+            timed_events[0].record(stream)
+        graph.replay()
+        if world > 1:
+            dist.all_reduce(step.grads["flat"])
+        if timed_events is not None:
+            timed_events[1].record(stream)
+
+    clocks = ClockSampler(local)
+    with clocks:
+        for _ in range(args.warmup):
+            one()
+            flush.fill_(1.0)
+        # untimed soak so the clock samples see the GPU under load
+        t_end = time.time() + 1.0
+        while time.time() < t_end:
+            one()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for e in evs:
+            flush.fill_(1.0)
+            one(e)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    step.check_capacity()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    t_rank = sum(ms) / 1e3
+    if world > 1:
+        t = torch.tensor([t_rank], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    else:
+        t_max = t_rank
+    value = world * args.steps / t_max
+
+    # ---- per-stage device times (same stream, non-graph launches, flushed L2)
+    stage_ms = {}
+    if args.profile_stages:
+        names = ["mask_prune+rvq_assign+project", "bin_tiles", "render_fwd", "render_bwd"]
+        acc = {k: [] for k in names}
+        for _ in range(max(5, min(args.steps, 30))):
+            flush.fill_(1.0)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            ev[0].record(stream)
+            g = step.pruned
+            cs.mask_prune(step.g, None, step.prm.mask_eps, float("nan"), out=g,
+                          keep_map=step.keep_map, n_kept=step.n_kept, ws=step.ws_prune)
+            cs.rvq_assign(g.log_scale, step.cb.scale_codes, n_dev=step.n_kept,
+                          idx=step.cb.scale_idx, want_recon=False)
+            cs.rvq_assign(g.quat, step.cb.rot_codes, n_dev=step.n_kept, idx=step.cb.rot_idx,
+                          want_recon=False)
+            cs.project(g, step.cam, view, step.prm, step.cb, rec=step.rec, count=step.count)
+            ev[1].record(stream)
+            cs.bin_tiles(step.rec, step.count, step.cam, step.capacity, ws=step.ws_bin,
+                         out=dict(pair_gid=step.pair_gid, pair_rec=step.pair_rec,
+                                  tile_range=step.tile_range, n_pairs_dev=step.n_pairs),
+                         sync=False)
+            ev[2].record(stream)
+            step.forward()
+            ev[3].record(stream)
+            step.backward(view)
+            ev[4].record(stream)
+            torch.cuda.synchronize()
+            for i, k in enumerate(names):
+                acc[k].append(ev[i].elapsed_time(ev[i + 1]))
+        stage_ms = {k: statistics.mean(v) for k, v in acc.items()}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        ins = {k: torch.tensor(v).pin_memory() for k, v in sc.planes().items()}
+        up_h = [torch.tensor(a).pin_memory() for a in up]
+        outs_h = {k: torch.empty(step.img[k].shape, dtype=step.img[k].dtype).pin_memory()
+                  for k in ("color", "depth", "sil")}
+        grad_h = torch.empty(step.grads["flat"].shape).pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in ins.values()) + \
+            sum(t.numel() * t.element_size() for t in up_h)
+        d2h = sum(t.numel() * t.element_size() for t in outs_h.values()) + \
+            grad_h.numel() * grad_h.element_size()
+        e_ms = []
+        for i in range(args.warmup + args.steps):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for k, t in ins.items():
+                getattr(step.g, k).copy_(t, non_blocking=True)
+            for dst, src in zip(step.upstream, up_h):
+                dst.copy_(src, non_blocking=True)
+            graph.replay()
+            if world > 1:
+                dist.all_reduce(step.grads["flat"])
+            for k, t in outs_h.items():
+                t.copy_(step.img[k], non_blocking=True)
+            grad_h.copy_(step.grads["flat"], non_blocking=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                e_ms.append(a.elapsed_time(b))
+        t_e = sum(e_ms) / 1e3
+        if world > 1:
+            t = torch.tensor([t_e], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e = float(t.item())
+        e2e = {"value": world * args.steps / t_e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    if rank == 0:
+        n_kept = int(step.n_kept.item())
+        n_pairs = int(step.n_pairs.item())
+        e_bwd = int(step.img["n_contrib"].sum().item())
+        peaks, peak_src = measured_peaks()
+        ck = clocks.summary()
+        counts = None
+        cpu = None
+        if not args.no_cpu_baseline:
+            counts = oracle_counts(sc, view)
+            ncores = 1
+            dt, units, _ = oracle_step(sc, view, up, row_frac=0.25, rvq_frac=0.25)
+            cpu = {"value": units / dt, "unit": UNIT, "cores": ncores, "kind": "oracle",
+                   "sample": "one step on 1/4 of the work (prune, R-VQ on 1/4 of survivors, "
+                             "project, bin, fwd+bwd on the top 1/4 pixel rows), 1 thread, "
+                             f"{dt:.1f} s"}
+        # roofline of the dominant kernel stage
+        roof = None
+        if stage_ms:
+            dom = max(stage_ms, key=stage_ms.get)
+            sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+            if dom in ("render_bwd", "render_fwd") and counts is not None:
+                if dom == "render_bwd":
+                    # §8(d): ~10 lane-instr per replayed entry + ~35 per contributing entry
+                    work = 10.0 * e_bwd + 35.0 * counts["e_contrib"]
+                else:
+                    # §8(d): ~10 per examined entry + ~11 per contributing entry
+                    work = 10.0 * counts["e_pix"] + 11.0 * counts["e_contrib"]
+                ach = work / (stage_ms[dom] * 1e-3) / 1e12
+                peak = fp32_peak_tinstr(sm_mhz)
+                roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak,
+                        "unit": "T FP32-lane-instr/s", "frac": ach / peak,
+                        "traffic": None,
+                        "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz "
+                                       f"(sm_max_mhz of {peak_src} MEASURED_PEAKS.json)"}
+            else:
+                rb = n_pairs * (8 + 4 + 64) * 2 + n_kept * 72
+                ach = rb / (stage_ms[dom] * 1e-3) / 1e9
+                roof = {"bound": "hbm", "kernel": dom, "achieved": ach,
+                        "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": ach / peaks["hbm_gbs"], "traffic": None}
+            tr = os.path.join(ROOT, "profiles", "traffic.json")
+            if os.path.exists(tr):
+                roof["traffic"] = json.load(open(tr)).get(dom)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "C2 replica 1200x680, 200k Gaussians (75% kept), R-VQ 4x256, "
+                                   "step = prune+rvq+project+bin+fwd+bwd"
+                                   + (" + NCCL grad all-reduce" if world > 1 else ""),
+                       "l2": "512 MB flush write between timed steps",
+                       "views": "rank r renders its own keyframe (rank 0 identity)",
+                       "parallelism": f"dp{world} keyframe window"},
+            "gpu_launches": sum(KERNEL_LAUNCHES_PER_STEP.values()) * args.steps,
+            "stage_ms": stage_ms,
+            "n_kept": n_kept, "n_pairs": n_pairs, "e_bwd": e_bwd,
+            "clocks": ck,
+        }
+        if counts:
+            line["evals"] = {"e_pix": counts["e_pix"], "e_contrib": counts["e_contrib"],
+                             "fwd_evals_per_s": counts["e_pix"] / (stage_ms.get("render_fwd", 0) * 1e-3)
+                             if stage_ms.get("render_fwd") else None,
+                             "bwd_evals_per_s": e_bwd / (stage_ms.get("render_bwd", 0) * 1e-3)
+                             if stage_ms.get("render_bwd") else None}
+            line["render_only_fwd_bwd_per_s"] = 1e3 / (stage_ms["bin_tiles"] + stage_ms["render_fwd"]
+                                                        + stage_ms["render_bwd"]
+                                                        + stage_ms["mask_prune+rvq_assign+project"]) \
+                if stage_ms else None
+        if roof:
+            line["roofline"] = roof
+        if cpu:
+            line["cpu_baseline"] = cpu
+        if e2e:
+            line["e2e"] = e2e
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

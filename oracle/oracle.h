@@ -119,6 +119,10 @@ int oracle_mask_prune(int64_t n, const float *mask, float mask_eps,
                       int32_t n_idx_planes, const uint16_t *const *in_idx, uint16_t *const *out_idx,
                       int32_t mask_plane, float reset_mask, int32_t *keep_map, int64_t *n_kept);
 
+/* Restrict oracle_render_fwd/bwd to pixel rows [row_lo, row_hi) (row_hi < 0:
+ * all rows) -- used only to time a bounded CPU-baseline sample. */
+void oracle_set_row_window(int32_t row_lo, int32_t row_hi);
+
 /* DA helpers exported for pins. */
 float oracle_pexp(float x);
 float oracle_plog(float x);

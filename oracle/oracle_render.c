@@ -20,6 +20,13 @@
 #include "oracle_internal.h"
 #include <stdlib.h>
 
+/* Optional pixel-row window for the tiled forward/backward: the timed CPU
+ * baseline renders a bounded sample of rows (bench.py); default = all rows. */
+static int g_row_lo = 0, g_row_hi = -1;
+void oracle_set_row_window(int32_t row_lo, int32_t row_hi) { g_row_lo = row_lo; g_row_hi = row_hi; }
+static int or_row_lo(int H) { return g_row_lo < 0 ? 0 : (g_row_lo > H ? H : g_row_lo); }
+static int or_row_hi(int H) { return (g_row_hi < 0 || g_row_hi > H) ? H : g_row_hi; }
+
 typedef struct { uint32_t tile, zbits, gid; } or_pair;
 
 static int cmp_pair(const void *a, const void *b)
@@ -157,7 +164,7 @@ int oracle_render_fwd(const uint32_t *rec, const uint32_t *pair_gid, const uint3
     const int tiles_x = (W + OR_TILE - 1) / OR_TILE;
     const int64_t HW = (int64_t)W * H;
     int64_t e_pix = 0, e_con = 0;
-    for (int py = 0; py < H; py++)
+    for (int py = or_row_lo(H); py < or_row_hi(H); py++)
         for (int px = 0; px < W; px++) {
             int64_t t = (int64_t)(py / OR_TILE) * tiles_x + px / OR_TILE;
             uint32_t s = tile_range[2 * t], e = tile_range[2 * t + 1];
@@ -275,7 +282,7 @@ int oracle_render_bwd(const or_gaussians *g, const or_codebook *cb, const or_cam
         if (l > maxlen) maxlen = l;
     }
     or_entry *ent = (or_entry *)malloc((size_t)(maxlen ? maxlen : 1) * sizeof(or_entry));
-    for (int py = 0; py < H; py++)
+    for (int py = or_row_lo(H); py < or_row_hi(H); py++)
         for (int px = 0; px < W; px++) {
             int64_t p = (int64_t)py * W + px;
             if (pixel_weight_zero && pixel_weight_zero[p]) continue;

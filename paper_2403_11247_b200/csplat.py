@@ -243,9 +243,18 @@ GRAD_SHAPES = dict(mean=3, opacity=1, rgb=3, log_scale=3, quat=4, mask=1)
 
 
 def alloc_grads(n: int, device="cuda", pose_only=False):
-    g = {} if pose_only else {k: torch.zeros((c, n) if c > 1 else (n,), device=device)
-                              for k, c in GRAD_SHAPES.items()}
-    g["pose"] = torch.zeros(6, device=device)
+    """Gradient planes as views of ONE flat float32 buffer ``g["flat"]``
+    ([15 n] planes then the 6 pose entries) so a data-parallel step can
+    all-reduce them with a single collective."""
+    total = (0 if pose_only else 15 * n) + 8
+    flat = torch.zeros(total, device=device)
+    g = {"flat": flat}
+    off = 0
+    if not pose_only:
+        for k, c in GRAD_SHAPES.items():
+            g[k] = flat[off:off + c * n].view((c, n) if c > 1 else (n,))
+            off += c * n
+    g["pose"] = flat[off:off + 6]
     return g
 
 

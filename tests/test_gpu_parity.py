@@ -102,7 +102,7 @@ def run_and_compare(env, sc, view=None, use_codebook=True, prm=None, bwd=True, s
         a = gr[k].double().cpu().numpy().reshape(-1)
         r = go[k].reshape(-1)
         errs[k] = np.linalg.norm(a - r) / max(np.linalg.norm(r), 1e-30)
-    assert all(e <= GRAD_TOL for e in errs.values()), errs
+    assert all(e <= GRAD_TOL for e in errs.values()), {k: float(e) for k, e in errs.items()}
     res["grad_err"] = errs
     return res
 
