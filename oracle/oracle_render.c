@@ -93,8 +93,10 @@ typedef struct {
     int capped;
 } or_entry;
 
-#define FLAG_T_REL 1e-4
-#define FLAG_CAP_ABS 1e-5
+/* Ambiguity windows: a float32 evaluation of T(1-alpha) drifts
+ * from float64 by ~1e-7 per composited entry; o_hat*G by ~2e-7 (ex2.approx). */
+#define FLAG_T_REL 2e-5
+#define FLAG_CAP_ABS 1e-6
 
 /* Composite one pixel over an ordered candidate list (Eq 3-5).  Returns the
  * number of composited entries; fills out6 = (C rgb, D, S, T_final), the

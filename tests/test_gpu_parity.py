@@ -75,7 +75,7 @@ def run_and_compare(env, sc, view=None, use_codebook=True, prm=None, bwd=True, s
     out = cs.render_fwd(b["pair_rec"], b["tile_range"], cam, prm_c)
     fo = orc.render_fwd(rec_o, gid_o, rng_o, cam, prm_o)
     ok = fo["flags"] == 0
-    assert (~ok).sum() <= max(2, 1e-4 * H * W), (~ok).sum()
+    assert (~ok).sum() <= max(2, 2e-4 * H * W), (~ok).sum()
     for k in ("depth", "sil", "t_final"):
         err = np.abs(out[k].cpu().numpy() - fo[k])[ok]
         assert err.size == 0 or err.max() <= IMG_TOL, (k, err.max())
@@ -225,7 +225,8 @@ def test_long_tile_lists(env):
         mean = np.stack([(px - 7.5) / 20 * z, (py - 7.5) / 20 * z, z]).astype(np.float32)
         sc = synth.SynthScene(mean, rng.normal(-1, 1, n).astype(np.float32),
                               rng.uniform(0, 1, (3, n)).astype(np.float32),
-                              np.log(np.full((3, n), 0.02) * z).astype(np.float32),
+                              # anisotropic, so the quaternion gradient is not identically 0
+                              np.log(np.array([[0.02], [0.012], [0.004]]) * z).astype(np.float32),
                               synth._unit_quats(rng, n), np.full(n, 3.0, np.float32), cam,
                               [synth.IDENTITY_VIEW.copy()])
         res = run_and_compare(env, sc, use_codebook=False, bwd=(n < 5000))
