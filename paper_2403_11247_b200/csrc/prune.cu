@@ -12,7 +12,7 @@
 namespace csplat {
 
 constexpr int kPT = 256;         // threads per CTA
-constexpr int kPItems = 16;      // rounds per CTA
+constexpr int kPItems = 2;       // rounds per CTA (keeps >= 2 waves of CTAs at 200k)
 constexpr int kPTile = kPT * kPItems;
 
 size_t prune_workspace_bytes(int64_t n) {

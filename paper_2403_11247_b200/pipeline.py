@@ -90,8 +90,9 @@ class RenderStep:
         self.upstream = (d_color, d_depth, d_sil)
 
     # ---- stages -------------------------------------------------------------
-    def front(self, view, sync_probe=False):
-        """a9 -> a2 -> a3 -> a4/a5."""
+    def prepare(self):
+        """a9 (mask prune) -> a2 (R-VQ assignment of the survivors): once per
+        iteration, shared by every view rendered from the same map."""
         g = self.pruned
         # the codebook indices are re-assigned below, so only attribute planes are compacted
         cs.mask_prune(self.g, None, self.prm.mask_eps, float("nan"), out=g,
@@ -101,6 +102,20 @@ class RenderStep:
                           idx=self.cb.scale_idx, want_recon=False)
             cs.rvq_assign(g.quat, self.cb.rot_codes, n_dev=self.n_kept, idx=self.cb.rot_idx,
                           want_recon=False)
+
+    def render(self, view, flags=None, pose=None):
+        """a3 -> a4/a5 -> a6 -> a7/a8 for one view of the prepared map."""
+        self.project_bin(view)
+        self.forward()
+        self.backward(view, flags, pose)
+
+    def front(self, view, sync_probe=False):
+        """a9 -> a2 -> a3 -> a4/a5."""
+        self.prepare()
+        self.project_bin(view, sync_probe)
+
+    def project_bin(self, view, sync_probe=False):
+        g = self.pruned
         cs.project(g, self.cam, view, self.prm, self.cb, rec=self.rec, count=self.count)
         if sync_probe:
             big = max(self.capacity, 64 * self.n + 4096)
@@ -114,11 +129,12 @@ class RenderStep:
     def forward(self):
         cs.render_fwd(self.pair_rec, self.tile_range, self.cam, self.prm, out=self.img)
 
-    def backward(self, view, flags=None):
+    def backward(self, view, flags=None, pose=None):
         dC, dD, dS = self.upstream
+        grads = self.grads if pose is None else dict(self.grads, pose=pose)
         cs.render_bwd(self.pruned, self.cam, view, self.rec, self.pair_rec, self.tile_range,
                       self.img["t_final"], self.img["n_contrib"], dC, dD, dS, self.prm, self.cb,
-                      self.flags if flags is None else flags, grads=self.grads, ws=self.ws_bwd)
+                      self.flags if flags is None else flags, grads=grads, ws=self.ws_bwd)
 
     def step(self, view):
         self.front(view)

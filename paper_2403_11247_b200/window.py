@@ -1,0 +1,75 @@
+"""Keyframe-window data parallelism (north_star "the mapping
+and global-BA keyframe window").
+
+Every rank holds a full replica of the Gaussian map and renders the keyframes
+{i : i mod G = rank} of the window (fwd + bwd, gradients ACCUMULATEd into one
+flat fp32 buffer of 15 planes).  The one exchange of an iteration is a SUM
+all-reduce of that buffer (torch.distributed / NCCL over NVLink on GPUs, gloo
+in the CPU tests).  Per-keyframe pose gradients stay on the rank that owns the
+keyframe -- no collective for them.  Because every rank receives the identical
+reduced buffer, a deterministic update keeps the replicas bit-identical.
+
+The render backend is injected (``render_fn(kf, grads, pose)``): on a GPU it
+is ``RenderStep.render`` (libcsplat kernels); the gloo tests use a host stub,
+so the sharding/reduction logic is exercised without a GPU.
+"""
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import torch
+import torch.distributed as dist
+
+
+def shard(n_keyframes: int, rank: int, world: int) -> list[int]:
+    """Round-robin keyframe ownership: keyframe i -> rank i mod world."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    return list(range(rank, n_keyframes, world))
+
+
+class WindowStep:
+    def __init__(self, n_keyframes: int, flat_grad: torch.Tensor,
+                 render_fn: Callable[[int, torch.Tensor], None],
+                 prepare_fn: Callable[[], None] | None = None, rank: int | None = None,
+                 world: int | None = None, group=None):
+        self.world = world if world is not None else (dist.get_world_size(group)
+                                                      if dist.is_initialized() else 1)
+        self.rank = rank if rank is not None else (dist.get_rank(group)
+                                                   if dist.is_initialized() else 0)
+        self.group = group
+        self.local = shard(n_keyframes, self.rank, self.world)
+        self.flat = flat_grad
+        self.render_fn = render_fn
+        self.prepare_fn = prepare_fn
+        self.poses = {k: torch.zeros(6, dtype=flat_grad.dtype, device=flat_grad.device)
+                      for k in self.local}
+
+    def run(self):
+        """One window iteration: local renders accumulate, then one all-reduce."""
+        self.flat.zero_()
+        if self.prepare_fn is not None:
+            self.prepare_fn()
+        for k in self.local:
+            self.poses[k].zero_()
+            self.render_fn(k, self.poses[k])
+        if self.world > 1:
+            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
+        return self.flat
+
+
+def apply_sgd(params: Sequence[torch.Tensor], grads: Sequence[torch.Tensor], lr: float):
+    """A deterministic replicated update (identical on every rank)."""
+    with torch.no_grad():
+        for p, g in zip(params, grads):
+            p.sub_(lr * g)
+
+
+def gpu_window(step, views, rank=None, world=None, group=None):
+    """WindowStep over a RenderStep: `views[i]` is keyframe i's world->camera view."""
+    from . import csplat as cs
+
+    def render(k, pose):
+        step.render(views[k], flags=cs.ACCUMULATE, pose=pose)
+
+    return WindowStep(len(views), step.grads["flat"], render, step.prepare, rank, world, group)

@@ -298,3 +298,34 @@ def test_replica_c2_full_parity(env):
     fo = res["fo"]
     assert res["npairs"] > 100_000
     assert fo["e_pix"] > 10_000_000
+
+
+def test_window_accumulate_matches_sum_of_views(env):
+    """§8(e) on one GPU: a window iteration over 3 keyframes (ACCUMULATE into the
+    flat buffer) equals the sum of the 3 single-view backward passes; each
+    keyframe's pose gradient equals its own single-view pose gradient."""
+    torch, cs, dev = env["torch"], env["cs"], env["dev"]
+    from paper_2403_11247_b200.pipeline import RenderStep
+    from paper_2403_11247_b200.window import gpu_window
+    sc = synth.mid_scene(7)
+    rng = np.random.default_rng(3)
+    views = [sc.views[0]] + [synth.perturbed_view(rng, 2.0, 0.03) for _ in range(2)]
+    st = RenderStep(sc.planes(), sc.cam, sc.codebook, device=dev)
+    st.size_pairs(views[0], views=views[1:])
+    H, W = sc.cam["height"], sc.cam["width"]
+    st.set_upstream(*(torch.tensor(a, device=dev) for a in synth.upstream(rng, H, W)))
+    singles, poses = [], []
+    for v in views:
+        st.prepare()
+        st.render(v)
+        singles.append(st.grads["flat"].clone())
+        poses.append(st.grads["pose"].clone())
+    win = gpu_window(st, views, rank=0, world=1)
+    flat = win.run().clone()
+    torch.cuda.synchronize()
+    ref = sum(s.double() for s in singles)
+    n = st.n
+    err = (flat[:15 * n].double() - ref[:15 * n]).norm() / ref[:15 * n].norm()
+    assert err < 1e-5
+    for k in range(3):
+        assert torch.allclose(win.poses[k], poses[k], rtol=1e-4, atol=1e-4)
