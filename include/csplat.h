@@ -58,7 +58,8 @@ enum csplat_status {
 #define CSPLAT_POSE_ONLY 2u      /* render_bwd: only the pose gradient (tracking) */
 #define CSPLAT_ACCUMULATE 4u     /* render_bwd: add into the outputs instead of overwriting */
 
-/* Pinhole intrinsics K ("known camera intrinsic K"), image size, clip (R21). */
+/* Pinhole intrinsics K ("known camera intrinsic K"), image size
+ * (1..32767 pixels per side), clip (R21). */
 typedef struct {
     float fx, fy, cx, cy;
     int32_t width, height;

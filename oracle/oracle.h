@@ -59,7 +59,7 @@ typedef struct {
 
 /* Projected record: 16 x 32-bit words per Gaussian (layout in DESIGN.md):
  * 0 u, 1 v, 2 ca, 3 cb+cb, 4 cc, 5 o_hat, 6 k2, 7 z_c, 8 r, 9 g, 10 b,
- * 11 gid (u32), 12 px0|px1<<16, 13 py0|py1<<16, 14 0, 15 0.
+ * 11 gid (u32), 12 px0|py0<<16, 13 px1|py1<<16 (inclusive pixel rectangle), 14 0, 15 0.
  * Culled Gaussians: all 16 words 0 and count 0. */
 #define OR_REC_WORDS 16
 #define OR_TILE 16

@@ -192,8 +192,8 @@ int oracle_project(const or_gaussians *g, const or_codebook *cb, const or_camera
         r[9] = or_f2u(cg);
         r[10] = or_f2u(cbl);
         r[11] = (uint32_t)i;
-        r[12] = (uint32_t)px0 | ((uint32_t)px1 << 16);
-        r[13] = (uint32_t)py0 | ((uint32_t)py1 << 16);
+        r[12] = (uint32_t)px0 | ((uint32_t)py0 << 16);   /* rectangle low corner  */
+        r[13] = (uint32_t)px1 | ((uint32_t)py1 << 16);   /* rectangle high corner */
         count[i] = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
     }
     return 0;

@@ -54,7 +54,7 @@ int oracle_bin_tiles(const uint32_t *rec, const int32_t *count, int64_t n, const
     for (int64_t i = 0; i < n; i++) {
         if (count[i] <= 0) continue;
         const uint32_t *r = rec + i * OR_REC_WORDS;
-        int px0 = r[12] & 0xffff, px1 = r[12] >> 16, py0 = r[13] & 0xffff, py1 = r[13] >> 16;
+        int px0 = r[12] & 0xffff, py0 = r[12] >> 16, px1 = r[13] & 0xffff, py1 = r[13] >> 16;
         for (int ty = py0 / OR_TILE; ty <= py1 / OR_TILE; ty++)
             for (int tx = px0 / OR_TILE; tx <= px1 / OR_TILE; tx++) {
                 pairs[k].tile = (uint32_t)(ty * tiles_x + tx);

@@ -8,7 +8,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcsplat.so")
-SOURCES = ["api.cu", "project.cu", "bin.cu", "render_fwd.cu", "render_bwd.cu", "rvq.cu", "prune.cu"]
+SOURCES = ["api.cu", "project.cu", "bin.cu", "render_fwd.cu", "render_bwd.cu", "chain.cu", "rvq.cu",
+           "prune.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

@@ -49,8 +49,8 @@ int invalid(const char *msg) {
 
 int check_camera(const csplat_camera *c) {
   if (!c) return invalid("camera is NULL");
-  if (c->width <= 0 || c->height <= 0 || c->width > 65535 || c->height > 65535)
-    return invalid("camera width/height out of range (1..65535)");
+  if (c->width <= 0 || c->height <= 0 || c->width > 32767 || c->height > 32767)
+    return invalid("camera width/height out of range (1..32767)");
   if (!(c->fx > 0) || !(c->fy > 0)) return invalid("fx, fy must be > 0");
   if (!(c->near_z > 0) || !(c->far_z > c->near_z)) return invalid("need 0 < near < far");
   if (!std::isfinite(c->cx) || !std::isfinite(c->cy)) return invalid("cx, cy must be finite");

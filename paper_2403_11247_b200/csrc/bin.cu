@@ -96,8 +96,9 @@ __device__ __forceinline__ void expand_warp(int64_t base, int64_t n, const int32
     const uint32_t ory = __shfl_sync(0xffffffffu, ry, owner);
     const uint32_t ozb = __shfl_sync(0xffffffffu, zb, owner);
     if (k < total) {
-      const int tx0 = (int)(orx & 0xffffu) / kTile, tx1 = (int)(orx >> 16) / kTile;
-      const int ty0 = (int)(ory & 0xffffu) / kTile;
+      // rx = px0 | py0 << 16 (low corner), ry = px1 | py1 << 16 (high corner)
+      const int tx0 = (int)(orx & 0xffffu) / kTile, tx1 = (int)(ory & 0xffffu) / kTile;
+      const int ty0 = (int)(orx >> 16) / kTile;
       const int w = tx1 - tx0 + 1;
       const int li = k - oe;
       const int tile = (ty0 + li / w) * tiles_x + tx0 + li % w;

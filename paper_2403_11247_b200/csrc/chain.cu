@@ -1,0 +1,262 @@
+// chain.cu -- a8: the per-Gaussian chain rule of the backward:
+// the 2D gradient accumulated by k_render_bwd (u, v, conic, o_hat, z, rgb) is
+// mapped through the conic inverse, Sigma' = J W Sigma W^T J^T (Eq 2), Sigma =
+// R S S^T R^T (Eq 1), the quaternion normalisation, the exp/sigmoid
+// activations (R15), the straight-through mask (Eq 6, R14) and the camera
+// pose (left perturbation, R22).  One thread per Gaussian; the 6-vector pose
+// gradient is reduced per CTA (warp shuffles, then shared memory) and added
+// with 6 atomics per CTA.  HBM-bound: 48 B accumulator + ~60 B attributes +
+// 64 B record in, 60 B out per Gaussian.
+#include "common.cuh"
+
+namespace csplat {
+
+struct ChainConst {
+  float W[9], t[3];
+  float fx, fy, lx_lo, lx_hi, ly_lo, ly_hi, dil;
+};
+
+__device__ __forceinline__ uint32_t load_idx2(const void *p, int bytes, int64_t off) {
+  return bytes == 1 ? (uint32_t)((const uint8_t *)p)[off] : (uint32_t)((const uint16_t *)p)[off];
+}
+
+__global__ void __launch_bounds__(256) k_chain(
+    int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
+    const float *__restrict__ opac, const float *__restrict__ lsc, const float *__restrict__ quat,
+    const float *__restrict__ mask, DecodeArgs dec, int use_dec, ChainConst cc,
+    const float4 *__restrict__ rec4, const float4 *__restrict__ acc4, uint32_t flags,
+    csplat_grads out) {
+  __shared__ float red[8][6];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ne = eff_n(n, n_dev);
+  float pose[6] = {0, 0, 0, 0, 0, 0};
+  float g[15];
+#pragma unroll
+  for (int k = 0; k < 15; k++) g[k] = 0.f;
+  bool alive = false;
+  if (i < ne) alive = rec4[i * 4 + 1].y != 0.0f;  // o_hat word is 0 iff culled
+  if (alive) {
+    const float4 a0 = acc4[i * 3 + 0], a1 = acc4[i * 3 + 1], a2 = acc4[i * 3 + 2];
+    const float gu = a0.x, gv = a0.y, gca = a0.z, gcb = a0.w, gcc = a1.x, goh = a1.y, gz = a1.z;
+    g[4] = a1.w;  // rgb
+    g[5] = a2.x;
+    g[6] = a2.y;
+    float ls[3], qv[4];
+    if (use_dec) {
+      for (int l = 0; l < dec.L; l++) {
+        const uint32_t si = load_idx2(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i);
+        const uint32_t ri = load_idx2(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i);
+        const float *sc = dec.scale_codes + ((int64_t)l * dec.P + si) * 3;
+        const float *rc = dec.rot_codes + ((int64_t)l * dec.P + ri) * 4;
+        for (int k = 0; k < 3; k++) ls[k] = l ? DADD(ls[k], sc[k]) : sc[k];
+        for (int k = 0; k < 4; k++) qv[k] = l ? DADD(qv[k], rc[k]) : rc[k];
+      }
+    } else {
+      for (int k = 0; k < 3; k++) ls[k] = lsc[k * n + i];
+      for (int k = 0; k < 4; k++) qv[k] = quat[k * n + i];
+    }
+    const float s[3] = {__expf(ls[0]), __expf(ls[1]), __expf(ls[2])};
+    const float qn2 = qv[0] * qv[0] + qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3];
+    const float qinv = rsqrtf(qn2);
+    const float w = qv[0] * qinv, x = qv[1] * qinv, y = qv[2] * qinv, z = qv[3] * qinv;
+    float R[3][3];
+    R[0][0] = 1.f - 2.f * (y * y + z * z); R[0][1] = 2.f * (x * y - w * z); R[0][2] = 2.f * (x * z + w * y);
+    R[1][0] = 2.f * (x * y + w * z); R[1][1] = 1.f - 2.f * (x * x + z * z); R[1][2] = 2.f * (y * z - w * x);
+    R[2][0] = 2.f * (x * z - w * y); R[2][1] = 2.f * (y * z + w * x); R[2][2] = 1.f - 2.f * (x * x + y * y);
+    float Mm[3][3], Sg[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) Mm[a][b] = R[a][b] * s[b];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) Sg[a][b] = Mm[a][0] * Mm[b][0] + Mm[a][1] * Mm[b][1] + Mm[a][2] * Mm[b][2];
+    const float *Wm = cc.W;
+    const float mu[3] = {mean[i], mean[n + i], mean[2 * n + i]};
+    float pc[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) pc[a] = Wm[3 * a] * mu[0] + Wm[3 * a + 1] * mu[1] + Wm[3 * a + 2] * mu[2] + cc.t[a];
+    const float X = pc[0], Y = pc[1], Z = pc[2];
+    const float iz = 1.f / Z, iz2 = iz * iz;
+    const float rxz = X * iz, ryz = Y * iz;
+    const bool clx = rxz < cc.lx_lo || rxz > cc.lx_hi;
+    const bool cly = ryz < cc.ly_lo || ryz > cc.ly_hi;
+    const float cxr = fminf(fmaxf(rxz, cc.lx_lo), cc.lx_hi), cyr = fminf(fmaxf(ryz, cc.ly_lo), cc.ly_hi);
+    const float tx = clx ? cxr * Z : X, ty = cly ? cyr * Z : Y;
+    const float fx = cc.fx, fy = cc.fy;
+    const float J00 = fx * iz, J02 = -fx * tx * iz2, J11 = fy * iz, J12 = -fy * ty * iz2;
+    float A[2][3];
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+      A[0][j] = J00 * Wm[j] + J02 * Wm[6 + j];
+      A[1][j] = J11 * Wm[3 + j] + J12 * Wm[6 + j];
+    }
+    float AS[2][3];  // A Sigma
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int j = 0; j < 3; j++) AS[a][j] = A[a][0] * Sg[0][j] + A[a][1] * Sg[1][j] + A[a][2] * Sg[2][j];
+    const float sa = AS[0][0] * A[0][0] + AS[0][1] * A[0][1] + AS[0][2] * A[0][2] + cc.dil;
+    const float sb = AS[0][0] * A[1][0] + AS[0][1] * A[1][1] + AS[0][2] * A[1][2];
+    const float sc2 = AS[1][0] * A[1][0] + AS[1][1] * A[1][1] + AS[1][2] * A[1][2] + cc.dil;
+    const float idet = 1.f / (sa * sc2 - sb * sb);
+    const float Q00 = sc2 * idet, Q01 = -sb * idet, Q11 = sa * idet;
+    // dL/dSigma' = -Q G_Q Q, G_Q = [[gca, gcb/2], [gcb/2, gcc]]
+    const float h = 0.5f * gcb;
+    const float T00 = Q00 * gca + Q01 * h, T01 = Q00 * h + Q01 * gcc;
+    const float T10 = Q01 * gca + Q11 * h, T11 = Q01 * h + Q11 * gcc;
+    const float G00 = -(T00 * Q00 + T01 * Q01), G01 = -(T00 * Q01 + T01 * Q11);
+    const float G11 = -(T10 * Q01 + T11 * Q11);
+    // GA = 2 G2 A Sigma  (2x3),  GS = A^T G2 A (3x3)
+    float GA[2][3], G2A[2][3];
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+      GA[0][j] = 2.f * (G00 * AS[0][j] + G01 * AS[1][j]);
+      GA[1][j] = 2.f * (G01 * AS[0][j] + G11 * AS[1][j]);
+      G2A[0][j] = G00 * A[0][j] + G01 * A[1][j];
+      G2A[1][j] = G01 * A[0][j] + G11 * A[1][j];
+    }
+    float GS[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) GS[a][b] = A[0][a] * G2A[0][b] + A[1][a] * G2A[1][b];
+    // dL/dJ = GA W^T (only J00, J02, J11, J12 vary)
+    const float GJ00 = GA[0][0] * Wm[0] + GA[0][1] * Wm[1] + GA[0][2] * Wm[2];
+    const float GJ02 = GA[0][0] * Wm[6] + GA[0][1] * Wm[7] + GA[0][2] * Wm[8];
+    const float GJ11 = GA[1][0] * Wm[3] + GA[1][1] * Wm[4] + GA[1][2] * Wm[5];
+    const float GJ12 = GA[1][0] * Wm[6] + GA[1][1] * Wm[7] + GA[1][2] * Wm[8];
+    float gpc[3];
+    gpc[0] = gu * fx * iz;
+    gpc[1] = gv * fy * iz;
+    gpc[2] = gz - (gu * fx * X + gv * fy * Y) * iz2 - (GJ00 * fx + GJ11 * fy) * iz2;
+    if (!clx) {
+      gpc[0] -= GJ02 * fx * iz2;
+      gpc[2] += GJ02 * 2.f * fx * X * iz2 * iz;
+    } else {
+      gpc[2] += GJ02 * fx * cxr * iz2;  // J02 = -fx c / Z
+    }
+    if (!cly) {
+      gpc[1] -= GJ12 * fy * iz2;
+      gpc[2] += GJ12 * 2.f * fy * Y * iz2 * iz;
+    } else {
+      gpc[2] += GJ12 * fy * cyr * iz2;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; a++) g[a] = Wm[a] * gpc[0] + Wm[3 + a] * gpc[1] + Wm[6 + a] * gpc[2];
+    // pose: v, and omega via p_c and via W in A = J W (Mw = W GA^T J)
+    pose[3] = gpc[0];
+    pose[4] = gpc[1];
+    pose[5] = gpc[2];
+    pose[0] = Y * gpc[2] - Z * gpc[1];
+    pose[1] = Z * gpc[0] - X * gpc[2];
+    pose[2] = X * gpc[1] - Y * gpc[0];
+    float Jm[2][3] = {{J00, 0.f, J02}, {0.f, J11, J12}};
+    float Mw[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      // (GA^T J)[l][b] = sum_k GA[k][l] J[k][b];  Mw[a][b] = sum_l W[a][l] (GA^T J)[l][b]
+      const float c0 = Wm[3 * a] * GA[0][0] + Wm[3 * a + 1] * GA[0][1] + Wm[3 * a + 2] * GA[0][2];
+      const float c1 = Wm[3 * a] * GA[1][0] + Wm[3 * a + 1] * GA[1][1] + Wm[3 * a + 2] * GA[1][2];
+#pragma unroll
+      for (int b = 0; b < 3; b++) Mw[a][b] = c0 * Jm[0][b] + c1 * Jm[1][b];
+    }
+    pose[0] += Mw[1][2] - Mw[2][1];
+    pose[1] += Mw[2][0] - Mw[0][2];
+    pose[2] += Mw[0][1] - Mw[1][0];
+    // opacity (Eq 7, M = 1): o_hat = sig(o)
+    const float oh = rec4[i * 4 + 1].y;
+    g[3] = goh * oh * (1.f - oh);
+    float gM = goh * oh;
+    // Sigma = Mm Mm^T: dL/dMm = 2 GS Mm
+    float GM[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) GM[a][b] = 2.f * (GS[a][0] * Mm[0][b] + GS[a][1] * Mm[1][b] + GS[a][2] * Mm[2][b]);
+#pragma unroll
+    for (int b = 0; b < 3; b++) {
+      const float gsb = R[0][b] * GM[0][b] + R[1][b] * GM[1][b] + R[2][b] * GM[2][b];
+      g[7 + b] = gsb * s[b];  // d/d log-scale
+      gM += gsb * s[b];
+    }
+    float GR[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+      for (int b = 0; b < 3; b++) GR[a][b] = GM[a][b] * s[b];
+    const float gw = 2.f * (-z * GR[0][1] + y * GR[0][2] + z * GR[1][0] - x * GR[1][2] - y * GR[2][0] + x * GR[2][1]);
+    const float gx = 2.f * (y * GR[0][1] + z * GR[0][2] + y * GR[1][0] - 2.f * x * GR[1][1] - w * GR[1][2] +
+                            z * GR[2][0] + w * GR[2][1] - 2.f * x * GR[2][2]);
+    const float gy = 2.f * (-2.f * y * GR[0][0] + x * GR[0][1] + w * GR[0][2] + x * GR[1][0] + z * GR[1][2] -
+                            w * GR[2][0] + z * GR[2][1] - 2.f * y * GR[2][2]);
+    const float gzq = 2.f * (-2.f * z * GR[0][0] - w * GR[0][1] + x * GR[0][2] + w * GR[1][0] - 2.f * z * GR[1][1] +
+                             y * GR[1][2] + x * GR[2][0] + y * GR[2][1]);
+    const float dot = w * gw + x * gx + y * gy + z * gzq;
+    g[10] = (gw - w * dot) * qinv;
+    g[11] = (gx - x * dot) * qinv;
+    g[12] = (gy - y * dot) * qinv;
+    g[13] = (gzq - z * dot) * qinv;
+    // Eq 6 straight-through: dL/dm = dL/dM Sig'(m)
+    const float sm = 1.f / (1.f + __expf(-mask[i]));
+    g[14] = gM * sm * (1.f - sm);
+  }
+  if (!(flags & CSPLAT_POSE_ONLY) && i < n) {
+    const bool accu = (flags & CSPLAT_ACCUMULATE) != 0;
+    auto put = [&](float *plane, int k, int64_t off) {
+      if (!plane) return;
+      if (accu) plane[off] += g[k];
+      else plane[off] = g[k];
+    };
+    for (int k = 0; k < 3; k++) put(out.mean, k, (int64_t)k * n + i);
+    put(out.opacity, 3, i);
+    for (int k = 0; k < 3; k++) put(out.rgb, 4 + k, (int64_t)k * n + i);
+    for (int k = 0; k < 3; k++) put(out.log_scale, 7 + k, (int64_t)k * n + i);
+    for (int k = 0; k < 4; k++) put(out.quat, 10 + k, (int64_t)k * n + i);
+    put(out.mask, 14, i);
+  }
+  if (out.pose) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      const float v = warp_sum(pose[k]);
+      if (lane == 0) red[wid][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      float s = 0.f;
+      for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[w][threadIdx.x];
+      atomicAdd(out.pose + threadIdx.x, s);
+    }
+  }
+}
+
+cudaError_t launch_chain(const csplat_gaussians &g, const DecodeArgs *dec,
+                         const csplat_camera &cam, const csplat_view &view,
+                         const csplat_params &prm, const void *rec, const float *acc,
+                         uint32_t flags, const csplat_grads &out, cudaStream_t s) {
+  ChainConst cc;
+  for (int a = 0; a < 3; a++) {
+    for (int b = 0; b < 3; b++) cc.W[3 * a + b] = view.m[4 * a + b];
+    cc.t[a] = view.m[4 * a + 3];
+  }
+  cc.fx = cam.fx;
+  cc.fy = cam.fy;
+  const float Wf = (float)cam.width, Hf = (float)cam.height;
+  cc.lx_lo = -((cam.cx + 0.15f * Wf) / cam.fx);
+  cc.lx_hi = ((Wf - cam.cx) + 0.15f * Wf) / cam.fx;
+  cc.ly_lo = -((cam.cy + 0.15f * Hf) / cam.fy);
+  cc.ly_hi = ((Hf - cam.cy) + 0.15f * Hf) / cam.fy;
+  cc.dil = prm.dilation;
+  DecodeArgs d{};
+  if (dec) d = *dec;
+  const int64_t blocks = (g.n + 255) / 256;
+  k_chain<<<(unsigned)blocks, 256, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.log_scale, g.quat,
+                                           g.mask, d, dec ? 1 : 0, cc,
+                                           static_cast<const float4 *>(rec),
+                                           reinterpret_cast<const float4 *>(acc), flags, out);
+  return cudaGetLastError();
+}
+
+}  // namespace csplat

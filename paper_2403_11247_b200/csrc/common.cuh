@@ -167,6 +167,10 @@ cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               cudaStream_t s);
 
 size_t bwd_workspace_bytes(int64_t n);
+cudaError_t launch_chain(const csplat_gaussians &g, const DecodeArgs *dec,
+                         const csplat_camera &cam, const csplat_view &view,
+                         const csplat_params &prm, const void *rec, const float *acc,
+                         uint32_t flags, const csplat_grads &out, cudaStream_t s);
 cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                               const csplat_camera &cam, const csplat_view &view,
                               const csplat_params &prm, const void *rec, const void *pair_rec,

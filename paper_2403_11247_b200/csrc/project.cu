@@ -158,8 +158,9 @@ __global__ void __launch_bounds__(256) k_project(
   r[0] = make_float4(u, v, ca, DADD(cbn, cbn));
   r[1] = make_float4(cc, oh, k2, zc);
   r[2] = make_float4(cr, cg, cb, __uint_as_float((uint32_t)i));
-  r[3] = make_float4(__uint_as_float((uint32_t)px0 | ((uint32_t)px1 << 16)),
-                     __uint_as_float((uint32_t)py0 | ((uint32_t)py1 << 16)), 0.f, 0.f);
+  // inclusive pixel rectangle as two u16x2 corners (low | high), DESIGN.md §4
+  r[3] = make_float4(__uint_as_float((uint32_t)px0 | ((uint32_t)py0 << 16)),
+                     __uint_as_float((uint32_t)px1 | ((uint32_t)py1 << 16)), 0.f, 0.f);
   count[i] = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
 }
 

@@ -1,25 +1,58 @@
 // render_fwd.cu -- a6: front-to-back alpha compositing of colour, depth and
 // silhouette (Eq 3-5; readings R1-R3, R7-R10).
 //
-// One CTA per 16x16 screen tile, one thread per pixel; the 8 warps each own an
-// 8x4 pixel rectangle (tighter than 16x2 rows for the warp-level cull).  The
-// tile's records are a contiguous slice of the pair-ordered payload written by
-// csplat_bin_tiles, so they are streamed into shared memory with 1-D TMA bulk
-// copies (cp.async.bulk, mbarrier complete_tx) through a kStages-deep ring of
-// kBatch-record batches; thread 0 is the producer.  Every record is read from
-// shared memory as a broadcast.  A warp skips a record whose pixel rectangle
-// misses the warp's 8x4 pixels (result-invariant); the CTA stops when every
-// pixel has terminated (T(1-alpha) < t_min, R3) -- checked once per batch.
-// The per-pixel q test is the DA of DESIGN.md §3 (bit-exact with the oracle);
-// alpha, T and the sums are float32 with ex2.approx.
+// One CTA of 128 threads per 16x16 screen tile; each thread owns two vertically
+// adjacent pixels (they share dx and the per-record loads), so a warp owns an
+// 8x8 pixel block.  The tile's records are a contiguous slice of the
+// pair-ordered payload written by csplat_bin_tiles and are streamed into
+// shared memory by 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx)
+// through a kStages-deep ring of kBatch-record batches; thread 0 is the
+// producer; every record is read from shared memory as a broadcast.  A warp
+// skips a record whose pixel rectangle misses its 8x8 block (two SWAR u16x2
+// subtractions; result-invariant).  The CTA stops once every pixel terminated
+// (T(1-alpha) < t_min, R3), checked once per batch.  The per-pixel q test is
+// the DA of DESIGN.md §3 (bit-exact with the oracle); alpha, T and the sums
+// are float32 with ex2.approx.
 #include "common.cuh"
 
 namespace csplat {
 
 constexpr int kBatch = 32;   // records per TMA batch (2 KB)
 constexpr int kStages = 4;   // ring depth
+constexpr int kFwdThreads = 128;
 
-__global__ void __launch_bounds__(256) k_render_fwd(
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct PixState {
+  float T, r, g, b, D, S;
+  int32_t last;
+  int done;  // 0 = still compositing
+};
+
+// Composite one record into one pixel whose DA q test passed (Eq 3-5).
+__device__ __forceinline__ void composite(PixState &p, float q, float oh, float z,
+                                          const float4 &rgb, float amax, float tmin, int idx) {
+  const float alpha = fminf(amax, oh * ex2_approx(q * -0.72134752f));  // exp(-q/2)
+  const float test = p.T * (1.0f - alpha);
+  if (test < tmin) {  // R3: the triggering entry is not composited
+    p.done = 1;
+    return;
+  }
+  const float w = alpha * p.T;
+  p.r = fmaf(rgb.x, w, p.r);  // Eq 3
+  p.g = fmaf(rgb.y, w, p.g);
+  p.b = fmaf(rgb.z, w, p.b);
+  p.D = fmaf(z, w, p.D);      // Eq 4 (R8)
+  p.S += w;                   // Eq 5 (R9)
+  p.T = test;
+  p.last = idx;
+}
+
+__global__ void __launch_bounds__(kFwdThreads) k_render_fwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, float tmin, float *__restrict__ color, float *__restrict__ depth,
     float *__restrict__ sil, float *__restrict__ t_final, int32_t *__restrict__ n_contrib) {
@@ -28,9 +61,11 @@ __global__ void __launch_bounds__(256) k_render_fwd(
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * 4;
-  const int px = wx0 + (lane & 7), py = wy0 + (lane >> 3);
-  const bool inside = px < W && py < H;
+  const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * 8;
+  const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * 2, py1 = py0 + 1;
+  // warp block corners as u16x2 for the SWAR rectangle test
+  const uint32_t wlo = (uint32_t)wx0 | ((uint32_t)wy0 << 16);
+  const uint32_t whi_x = ((uint32_t)(wx0 + 7) | ((uint32_t)(wy0 + 7) << 16)) | 0x80008000u;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
   const int len = (int)(end - start);
   const int nb = (len + kBatch - 1) / kBatch;
@@ -52,58 +87,54 @@ __global__ void __launch_bounds__(256) k_render_fwd(
   if (tid == 0)
     for (; issued < min(kStages - 1, nb); issued++) issue(issued);
 
-  float T = 1.0f, cr = 0.f, cg = 0.f, cbl = 0.f, D = 0.f, S = 0.f;
-  int32_t last = 0;
-  bool done = !inside;
-  const float fpx = (float)px, fpy = (float)py;
+  PixState p0{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, (px < W && py0 < H) ? 0 : 1};
+  PixState p1{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, (px < W && py1 < H) ? 0 : 1};
+  const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
   int b = 0;
   for (; b < nb; b++) {
-    if (__syncthreads_and(done)) break;
+    if (__syncthreads_and(p0.done & p1.done)) break;
     if (tid == 0 && issued < nb && issued <= b + kStages - 1) issue(issued++);
     mbar_wait(&full[b % kStages], (uint32_t)(b / kStages) & 1u);
     const float4 *rb = buf[b % kStages];
     const int cnt = min(kBatch, len - b * kBatch);
+#pragma unroll 2
     for (int e = 0; e < cnt; e++) {
       const float4 r3 = rb[e * 4 + 3];
-      const uint32_t rx = __float_as_uint(r3.x), ry = __float_as_uint(r3.y);
-      // warp-level cull: record's pixel rectangle vs this warp's 8x4 pixels
-      if ((int)(rx & 0xffffu) > wx0 + 7 || (int)(rx >> 16) < wx0 || (int)(ry & 0xffffu) > wy0 + 3 ||
-          (int)(ry >> 16) < wy0)
-        continue;
-      if (done) continue;
-      const float4 r0 = rb[e * 4 + 0];
-      const float4 r1 = rb[e * 4 + 1];
-      const float q = da_q(fpx, fpy, r0.x, r0.y, r0.z, r0.w, r1.x);
-      if (!(q >= 0.0f && q <= r1.z)) continue;  // R2 (DA)
-      const float alpha = fminf(amax, r1.y * __expf(-0.5f * q));
-      const float test = T * (1.0f - alpha);
-      if (test < tmin) {  // R3: the triggering entry is not composited
-        done = true;
-        continue;
-      }
-      const float4 r2 = rb[e * 4 + 2];
-      const float w = alpha * T;
-      cr = fmaf(r2.x, w, cr);   // Eq 3
-      cg = fmaf(r2.y, w, cg);
-      cbl = fmaf(r2.z, w, cbl);
-      D = fmaf(r1.w, w, D);     // Eq 4 (R8)
-      S += w;                   // Eq 5 (R9)
-      T = test;
-      last = b * kBatch + e + 1;
+      // warp-level cull: record rectangle [lo, hi] vs the warp's 8x8 block
+      const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
+      const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
+      if ((t1 & t2 & 0x80008000u) != 0x80008000u) continue;
+      const float4 r0 = rb[e * 4 + 0];  // u, v, ca, cb+cb
+      const float4 r1 = rb[e * 4 + 1];  // cc, o_hat, k2, z
+      const float dx = DSUB(fpx, r0.x);
+      const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
+      const float dy0 = DSUB(fpy0, r0.y), dy1 = DSUB(fpy1, r0.y);
+      const float q0 = DFMA(cadx, dx, DFMA(cbdx, dy0, DMUL(DMUL(r1.x, dy0), dy0)));
+      const float q1 = DFMA(cadx, dx, DFMA(cbdx, dy1, DMUL(DMUL(r1.x, dy1), dy1)));
+      const bool h0 = (p0.done == 0) & (q0 >= 0.0f) & (q0 <= r1.z);  // R2 (DA)
+      const bool h1 = (p1.done == 0) & (q1 >= 0.0f) & (q1 <= r1.z);
+      if (!(h0 | h1)) continue;
+      const float4 r2 = rb[e * 4 + 2];  // r, g, b, gid
+      const int idx = b * kBatch + e + 1;
+      if (h0) composite(p0, q0, r1.y, r1.w, r2, amax, tmin, idx);
+      if (h1) composite(p1, q1, r1.y, r1.w, r2, amax, tmin, idx);
     }
   }
   // never leave the CTA with bulk copies in flight into its shared memory
   if (tid == 0)
     for (int bb = b; bb < issued; bb++) mbar_wait(&full[bb % kStages], (uint32_t)(bb / kStages) & 1u);
-  if (inside) {
-    const int64_t p = (int64_t)py * W + px, HW = (int64_t)W * H;
-    color[p] = cr;
-    color[HW + p] = cg;
-    color[2 * HW + p] = cbl;
-    depth[p] = D;
-    sil[p] = S;
-    t_final[p] = T;
-    n_contrib[p] = last;
+  const int64_t HW = (int64_t)W * H;
+  if (px < W) {
+    if (py0 < H) {
+      const int64_t p = (int64_t)py0 * W + px;
+      color[p] = p0.r; color[HW + p] = p0.g; color[2 * HW + p] = p0.b;
+      depth[p] = p0.D; sil[p] = p0.S; t_final[p] = p0.T; n_contrib[p] = p0.last;
+    }
+    if (py1 < H) {
+      const int64_t p = (int64_t)py1 * W + px;
+      color[p] = p1.r; color[HW + p] = p1.g; color[2 * HW + p] = p1.b;
+      depth[p] = p1.D; sil[p] = p1.S; t_final[p] = p1.T; n_contrib[p] = p1.last;
+    }
   }
 }
 
@@ -113,9 +144,9 @@ cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               cudaStream_t s) {
   const CamInfo ci = cam_info(cam);
   const int T = ci.tiles_x * ci.tiles_y;
-  k_render_fwd<<<T, 256, 0, s>>>(static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H,
-                                 ci.tiles_x, prm.alpha_max, prm.t_min, color, depth, sil, t_final,
-                                 n_contrib);
+  k_render_fwd<<<T, kFwdThreads, 0, s>>>(static_cast<const float4 *>(pair_rec), tile_range, ci.W,
+                                         ci.H, ci.tiles_x, prm.alpha_max, prm.t_min, color, depth,
+                                         sil, t_final, n_contrib);
   return cudaGetLastError();
 }
 

@@ -100,8 +100,8 @@ def test_projection_closed_form(orc):
         assert np.allclose(sigma_prime_from_rec(rec[i]) + 0.3 * np.eye(2), ref["sigma_prime"],
                            rtol=1e-5, atol=1e-5)
     assert abs(f[0, 6] - g["on_axis"]["k2"]) < 2e-6
-    px0, px1 = rec[0, 12] & 0xFFFF, rec[0, 12] >> 16
-    py0, py1 = rec[0, 13] & 0xFFFF, rec[0, 13] >> 16
+    px0, py0 = rec[0, 12] & 0xFFFF, rec[0, 12] >> 16
+    px1, py1 = rec[0, 13] & 0xFFFF, rec[0, 13] >> 16
     assert [px0, px1] == g["on_axis"]["pixel_rect"]["x"]
     assert [py0, py1] == g["on_axis"]["pixel_rect"]["y"]
     # tiles: x 24..40 -> tiles 1..2, y 16..32 -> tiles 1..2
@@ -189,8 +189,8 @@ def test_binning_bruteforce(orc):
         tx, ty = orc.tiles(sc.cam)
         pairs = []
         for i in np.nonzero(cnt)[0]:
-            x0, x1 = rec[i, 12] & 0xFFFF, rec[i, 12] >> 16
-            y0, y1 = rec[i, 13] & 0xFFFF, rec[i, 13] >> 16
+            x0, y0 = rec[i, 12] & 0xFFFF, rec[i, 12] >> 16
+            x1, y1 = rec[i, 13] & 0xFFFF, rec[i, 13] >> 16
             for t in range(tx * ty):
                 bx0, by0 = (t % tx) * 16, (t // tx) * 16
                 if x0 <= bx0 + 15 and x1 >= bx0 and y0 <= by0 + 15 and y1 >= by0:
