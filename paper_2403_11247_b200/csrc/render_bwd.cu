@@ -63,7 +63,9 @@ __device__ __forceinline__ bool bwd_pixel(BPix &p, int j, float dx, float dy, co
   const float araw = r1.y * G;
   const bool capped = !(araw < amax);
   const float alpha = fminf(amax, araw);
-  const float Tj = __fdividef(p.T, 1.0f - alpha);
+  float rcp;  // 1 / (1 - alpha) with alpha <= alpha_max < 1 (R1): no range fix-up needed
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(1.0f - alpha));
+  const float Tj = p.T * rcp;
   const float w = alpha * Tj;
   const float vv = fmaf(r2.x, p.gr, fmaf(r2.y, p.gg, fmaf(r2.z, p.gb, fmaf(r1.w, p.gd, p.gs))));
   const float dLda = Tj * (vv - p.B);
