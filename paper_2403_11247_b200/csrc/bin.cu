@@ -21,8 +21,8 @@
 
 namespace csplat {
 
-constexpr int kWarpCap = 512;         // keys per warp bucket in shared memory
-constexpr int kSortWarps = 8;         // warps per CTA in k_sort_tiles
+constexpr int kCtaCap = 2048;         // keys per tile sorted by k_sort_tiles (16 KB smem)
+constexpr int kSortThreads = 128;     // threads per tile in k_sort_tiles
 constexpr int kLongSmemKeys = 12288;  // 96 KB: CTA-wide shared-memory sort limit
 
 struct BinWs {
@@ -184,10 +184,12 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long *a, int len, int
                                              Sync sync) {
   int np2 = 1;
   while (np2 < len) np2 <<= 1;
+  // index of the lower element of pair t in a block of 2j (j a power of two)
+  auto lower = [](int t, int j) { return ((t & ~(j - 1)) << 1) | (t & (j - 1)); };
   for (int k = 2; k <= np2; k <<= 1) {
     const int half = k >> 1;
     for (int t = tid; t < np2 / 2; t += nthr) {
-      const int i = (t / half) * k + (t % half);
+      const int i = lower(t, half);
       const int p = i ^ (k - 1);
       if (p < len) {
         const unsigned long long x = a[i], y = a[p];
@@ -197,7 +199,7 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long *a, int len, int
     sync();
     for (int j = half >> 1; j > 0; j >>= 1) {
       for (int t = tid; t < np2 / 2; t += nthr) {
-        const int i = (t / j) * 2 * j + (t % j);
+        const int i = lower(t, j);
         const int p = i + j;
         if (p < len) {
           const unsigned long long x = a[i], y = a[p];
@@ -224,26 +226,31 @@ __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len
   }
 }
 
-__global__ void __launch_bounds__(kSortWarps * 32) k_sort_tiles(
+// One 128-thread CTA per tile: enough warps in flight to hide the latency of
+// the record gathers in emit_sorted (one warp per tile left SMs at ~30%
+// occupancy: there are only ~3k tiles per view).
+__global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int64_t T, const uint32_t *__restrict__ range, const unsigned long long *__restrict__ keys,
     const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid, uint4 *__restrict__ pair_rec,
     uint32_t *__restrict__ long_list, uint32_t *__restrict__ long_count) {
-  __shared__ unsigned long long sk[kSortWarps][kWarpCap];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t tile = (int64_t)blockIdx.x * kSortWarps + wid;
-  if (tile >= T) return;
+  __shared__ unsigned long long sk[kCtaCap];
+  const int64_t tile = blockIdx.x;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
   const int len = (int)(end - start);
   if (len == 0) return;
-  if (len > kWarpCap) {
-    if (lane == 0) long_list[atomicAdd(long_count, 1u)] = (uint32_t)tile;
+  if (len > kCtaCap) {
+    if (threadIdx.x == 0) long_list[atomicAdd(long_count, 1u)] = (uint32_t)tile;
     return;
   }
-  unsigned long long *a = sk[wid];
-  for (int k = lane; k < len; k += 32) a[k] = keys[start + k];
-  __syncwarp();
-  bitonic_sort(a, len, lane, 32, [] { __syncwarp(); });
-  emit_sorted(a, len, start, lane, 32, rec4, pair_gid, pair_rec);
+  for (int k = threadIdx.x; k < len; k += kSortThreads) sk[k] = keys[start + k];
+  __syncthreads();
+  if (len <= 32) {  // one warp sorts a short list; the others only help emit
+    if (threadIdx.x < 32) bitonic_sort(sk, len, threadIdx.x, 32, [] { __syncwarp(); });
+    __syncthreads();
+  } else {
+    bitonic_sort(sk, len, threadIdx.x, kSortThreads, [] { __syncthreads(); });
+  }
+  emit_sorted(sk, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, pair_rec);
 }
 
 __global__ void __launch_bounds__(1024) k_sort_long(const uint32_t *__restrict__ range,
@@ -296,8 +303,7 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   if (n > 0)
     k_scatter<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, tile_range, w.cur,
                                                w.keys);
-  const int64_t sblocks = (T + kSortWarps - 1) / kSortWarps;
-  k_sort_tiles<<<(unsigned)sblocks, kSortWarps * 32, 0, s>>>(
+  k_sort_tiles<<<(unsigned)T, kSortThreads, 0, s>>>(
       T, tile_range, w.keys, rec4, pair_gid, static_cast<uint4 *>(pair_rec), w.long_list,
       w.long_count);
   const size_t lsm = kLongSmemKeys * sizeof(unsigned long long);

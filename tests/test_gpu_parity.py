@@ -218,7 +218,7 @@ def test_long_tile_lists(env):
     """Buckets longer than a warp's shared-memory slice (CTA-wide sort) and
     longer than the CTA's shared memory (global-memory sort)."""
     rng = np.random.default_rng(9)
-    for n in (1500, 13000):
+    for n in (1500, 4000, 13000):   # CTA sort / CTA-wide long sort / global-memory sort
         cam = dict(fx=20.0, fy=20.0, cx=7.5, cy=7.5, width=32, height=16, near=0.01, far=100.0)
         z = rng.uniform(1, 5, n)
         px, py = rng.uniform(0, 15, n), rng.uniform(0, 15, n)
