@@ -52,6 +52,155 @@ __device__ __forceinline__ void group_argmin(float &d, int &k) {
   }
 }
 
+// Resolve a block of 4 distances against the running (best, index): only when
+// the block's minimum beats the running best (a handful of times per stage)
+// is the lowest index of that minimum searched; ties keep the earlier index.
+__device__ __forceinline__ void block_argmin4(float d0, float d1, float d2, float d3, int k0,
+                                              float &best, int &bk) {
+  const float m = fminf(fminf(d0, d1), fminf(d2, d3));  // NaN-ignoring, exact
+  if (m < best) {
+    best = m;
+    bk = d0 == m ? k0 : (d1 == m ? k0 + 1 : (d2 == m ? k0 + 2 : k0 + 3));
+  }
+}
+
+// Chunked variant: group lane `sub` scans the contiguous code range
+// [sub*P/S, (sub+1)*P/S) of every stage (P % (4S) == 0), reading a padded,
+// bank-conflict-free shared-memory copy of the codebook with 16-byte loads.
+template <int D, int S>
+__global__ void __launch_bounds__(kRvqThreads) k_rvq_chunked(
+    const float *__restrict__ x, int64_t n, const int64_t *__restrict__ n_dev,
+    const float *__restrict__ codes_g, int L, int P, void *__restrict__ idx, int idx_bytes,
+    float *__restrict__ recon) {
+  extern __shared__ __align__(128) float sc[];
+  __shared__ __align__(8) uint64_t bar;
+  const int chunk = P / S;                 // codes per lane
+  const int cstride = chunk * D + 4;       // padded chunk (floats): distinct banks per lane
+  const int lstride = S * cstride;         // one stage
+  // stage the codebook with L*S 1-D TMA bulk copies (each chunk is contiguous
+  // in global memory), into the padded layout
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    const uint32_t cbytes = (uint32_t)(chunk * D * sizeof(float));
+    mbar_arrive_expect_tx(&bar, cbytes * L * S);
+    for (int l = 0; l < L; l++)
+      for (int s = 0; s < S; s++)
+        tma_load_1d(sc + l * lstride + s * cstride, codes_g + ((int64_t)l * P + s * chunk) * D,
+                    cbytes, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int64_t ne = eff_n(n, n_dev);
+  const int sub = threadIdx.x % S;
+  const int64_t ia0 = 2 * (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / S);
+  const bool live = ia0 < ne;
+  // only whole warps may leave (group shuffles need a converged warp); this
+  // drops the work of the vectors beyond the device-side count n_dev
+  if (__all_sync(0xffffffffu, !live)) return;
+  const int64_t ia = live ? ia0 : 0;
+  const bool has_b = live && ia + 1 < ne;
+  const int64_t ib = has_b ? ia + 1 : ia;
+  float xa[D], xb[D], sa[D], sb[D];
+#pragma unroll
+  for (int j = 0; j < D; j++) {
+    xa[j] = x[(int64_t)j * n + ia];
+    xb[j] = x[(int64_t)j * n + ib];
+    sa[j] = sb[j] = 0.0f;
+  }
+  for (int l = 0; l < L; l++) {
+    f2_t r[D];
+#pragma unroll
+    for (int j = 0; j < D; j++) r[j] = pk2(DSUB(xa[j], sa[j]), DSUB(xb[j], sb[j]));  // S - S_hat
+    const float4 *C4 = reinterpret_cast<const float4 *>(sc + l * lstride + sub * cstride);
+    const int kbase = sub * chunk;
+    float da = __int_as_float(0x7f800000), db = da;  // +inf: NaN distances are never taken
+    int blka = 0, blkb = 0;                          // block (of kBlk codes) of the best
+    f2_t acc0 = 0ull;
+    constexpr int kBlk = 8;
+    // distances of the kBlk codes of block i (bit-identical whenever recomputed)
+    auto block_dist = [&](int i, f2_t (&acc)[kBlk]) {
+      float cv[kBlk * D];
+#pragma unroll
+      for (int q = 0; q < 2 * D; q++) {  // kBlk * D floats = 2D float4 loads
+        const float4 v = C4[(i * D) / 4 + q];
+        cv[4 * q] = v.x; cv[4 * q + 1] = v.y; cv[4 * q + 2] = v.z; cv[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int c = 0; c < kBlk; c++) {
+        acc[c] = 0ull;  // (+0, +0): fma(e, e, 0) = e*e exactly
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+          const float cf = cv[c * D + j];
+          const f2_t e = sub2(pk2(cf, cf), r[j]);
+          acc[c] = fma2(e, e, acc[c]);
+        }
+      }
+    };
+    // scan: track only the minimum and the block holding its first occurrence
+    for (int i = 0; i < chunk; i += kBlk) {
+      f2_t acc[kBlk];
+      block_dist(i, acc);
+      if (i == 0) acc0 = acc[0];
+      const float ma = fminf(fminf(fminf(lo2(acc[0]), lo2(acc[1])), fminf(lo2(acc[2]), lo2(acc[3]))),
+                             fminf(fminf(lo2(acc[4]), lo2(acc[5])), fminf(lo2(acc[6]), lo2(acc[7]))));
+      const float mb = fminf(fminf(fminf(hi2(acc[0]), hi2(acc[1])), fminf(hi2(acc[2]), hi2(acc[3]))),
+                             fminf(fminf(hi2(acc[4]), hi2(acc[5])), fminf(hi2(acc[6]), hi2(acc[7]))));
+      blka = ma < da ? i : blka;  // strict: an earlier block keeps a tie
+      blkb = mb < db ? i : blkb;
+      da = fminf(da, ma);
+      db = fminf(db, mb);
+    }
+    // resolve the first code of the winning blocks that attains the minimum
+    int besta = kbase + blka, bestb = kbase + blkb;
+    {
+      f2_t acc[kBlk];
+      block_dist(blka, acc);
+#pragma unroll
+      for (int c = kBlk - 1; c >= 0; c--)
+        if (lo2(acc[c]) == da) besta = kbase + blka + c;
+      block_dist(blkb, acc);
+#pragma unroll
+      for (int c = kBlk - 1; c >= 0; c--)
+        if (hi2(acc[c]) == db) bestb = kbase + blkb + c;
+    }
+    // the sequential scan keeps k = 0 when d_0 is NaN (no later d compares below it)
+    if (sub == 0) {
+      if (lo2(acc0) != lo2(acc0)) { da = -__int_as_float(0x7f800000); besta = 0; }
+      if (hi2(acc0) != hi2(acc0)) { db = -__int_as_float(0x7f800000); bestb = 0; }
+    }
+    group_argmin<S>(da, besta);
+    group_argmin<S>(db, bestb);
+    if (sub == 0 && live) {
+      if (idx_bytes == 1) {
+        uint8_t *o = static_cast<uint8_t *>(idx) + (int64_t)l * n;
+        o[ia] = (uint8_t)besta;
+        if (has_b) o[ib] = (uint8_t)bestb;
+      } else {
+        uint16_t *o = static_cast<uint16_t *>(idx) + (int64_t)l * n;
+        o[ia] = (uint16_t)besta;
+        if (has_b) o[ib] = (uint16_t)bestb;
+      }
+    }
+    const float *Cl = sc + l * lstride;
+    const int sa_s = besta / chunk, sa_i = besta - sa_s * chunk;
+    const int sb_s = bestb / chunk, sb_i = bestb - sb_s * chunk;
+#pragma unroll
+    for (int j = 0; j < D; j++) {  // S_hat^l in stage order
+      const float ca = Cl[sa_s * cstride + sa_i * D + j], cb = Cl[sb_s * cstride + sb_i * D + j];
+      sa[j] = l == 0 ? ca : DADD(sa[j], ca);
+      sb[j] = l == 0 ? cb : DADD(sb[j], cb);
+    }
+  }
+  if (recon && sub == 0 && live) {
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+      recon[(int64_t)j * n + ia] = sa[j];
+      if (has_b) recon[(int64_t)j * n + ib] = sb[j];
+    }
+  }
+}
+
 template <int D, int S, bool SMEM>
 __global__ void __launch_bounds__(kRvqThreads) k_rvq(const float *__restrict__ x, int64_t n,
                                                      const int64_t *__restrict__ n_dev,
@@ -162,6 +311,23 @@ template <int D>
 static cudaError_t run_rvq_d(const float *x, int64_t n, const int64_t *n_dev, const float *codes,
                              int L, int P, void *idx, int idx_bytes, float *recon,
                              cudaStream_t s) {
+  constexpr int S = 4;
+  const size_t chunked_bytes = (size_t)L * S * ((P / S) * D + 4) * sizeof(float);
+  // TMA chunk copies need 16-byte aligned sources and sizes
+  if (P % (8 * S) == 0 && chunked_bytes <= 200 * 1024 &&
+      (reinterpret_cast<uintptr_t>(codes) & 15u) == 0) {
+    if (chunked_bytes > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_rvq_chunked<D, S>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)chunked_bytes);
+      if (e != cudaSuccess) return e;
+    }
+    const int64_t threads = (n + 1) / 2 * S;
+    const int64_t blocks = (threads + kRvqThreads - 1) / kRvqThreads;
+    k_rvq_chunked<D, S><<<(unsigned)blocks, kRvqThreads, chunked_bytes, s>>>(
+        x, n, n_dev, codes, L, P, idx, idx_bytes, recon);
+    return cudaGetLastError();
+  }
   if (P >= 16) return run_rvq<D, 4>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s);
   return run_rvq<D, 1>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s);
 }
