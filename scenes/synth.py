@@ -148,6 +148,55 @@ def scannet_scene(seed=0, n=1_000_000, parity=False):
     return sc
 
 
+def look_view(centre, yaw):
+    """World->camera [R|t] of a camera at `centre` looking along
+    (cos yaw, 0, sin yaw) with image y along world +y."""
+    f = np.array([math.cos(yaw), 0.0, math.sin(yaw)])
+    y = np.array([0.0, 1.0, 0.0])
+    x = np.cross(y, f)
+    R = np.stack([x, y, f])
+    t = -R @ np.asarray(centre, dtype=np.float64)
+    return np.concatenate([R, t[:, None]], axis=1).astype(np.float32)
+
+
+def window_scene(seed=0, n=500_000, n_keyframes=64, cam=None, codebook_LP=(4, 256)):
+    """C5: Gaussians on the six faces of the box [-3,3]x[-1.5,1.5]x[-3,3]
+    (area-weighted, 2 mm jitter) seen by n_keyframes inward-facing Replica
+    cameras on a 1 m circle (yaw theta + pi + 0.3 sin 3 theta)."""
+    rng = np.random.default_rng(seed)
+    cam = dict(cam or CAMERAS["replica"])
+    hx, hy, hz = 3.0, 1.5, 3.0
+    faces = [  # (axis, sign, area)
+        (0, -1, 4 * hy * hz), (0, 1, 4 * hy * hz), (1, -1, 4 * hx * hz), (1, 1, 4 * hx * hz),
+        (2, -1, 4 * hx * hy), (2, 1, 4 * hx * hy)]
+    areas = np.array([f[2] for f in faces])
+    which = rng.choice(6, size=n, p=areas / areas.sum())
+    pts = np.stack([rng.uniform(-hx, hx, n), rng.uniform(-hy, hy, n), rng.uniform(-hz, hz, n)])
+    half = np.array([hx, hy, hz])
+    for fi, (ax, sg, _) in enumerate(faces):
+        sel = which == fi
+        pts[ax, sel] = sg * half[ax]
+    pts += rng.normal(0, 0.002, pts.shape)
+    # distance to the camera circle (radius 1 m in the y = 0 plane)
+    rxz = np.hypot(pts[0], pts[2])
+    d = np.hypot(rxz - 1.0, pts[1])
+    s_px = rng.lognormal(math.log(2.5), 0.35, (3, n))
+    s_px[2] *= 0.2
+    log_scale = np.log(s_px * np.maximum(d, 0.3) / cam["fx"]).astype(np.float32)
+    quat = _unit_quats(rng, n)
+    opacity = rng.normal(3.0, 1.5, n).astype(np.float32)
+    rgb = rng.uniform(0, 1, (3, n)).astype(np.float32)
+    mask = np.where(rng.uniform(0, 1, n) < 0.75, 3.0, -8.0).astype(np.float32)
+    views = []
+    for i in range(n_keyframes):
+        th = 2 * math.pi * i / n_keyframes
+        views.append(look_view((math.cos(th), 0.0, math.sin(th)), th + math.pi + 0.3 * math.sin(3 * th)))
+    sc = SynthScene(pts.astype(np.float32), opacity, rgb, log_scale, quat, mask, cam, views)
+    if codebook_LP:
+        sc.codebook = random_codebooks(rng, log_scale, quat, *codebook_LP)
+    return sc
+
+
 def mid_scene(seed=0, n=3000, width=160, height=120):
     """Mid-size parity scene: several tiles in x and y plus a ragged tail
     (160x120 -> 10x8 tiles, the last tile row half empty)."""

@@ -329,3 +329,51 @@ def test_window_accumulate_matches_sum_of_views(env):
     assert err < 1e-5
     for k in range(3):
         assert torch.allclose(win.poses[k], poses[k], rtol=1e-4, atol=1e-4)
+
+
+# ------------------------------------------------------------------ configs C3, C4, C5
+
+@pytest.mark.slow
+def test_c3_tum_tracking_pose_only_parity(env):
+    """C3: TUM-shaped 640x480, 100k Gaussians, R-VQ 4x256, a tracking pose
+    (1 deg about a seeded axis + 2 cm) and a POSE_ONLY backward."""
+    cs = env["cs"]
+    sc = synth.tum_scene(0)
+    view = synth.perturbed_view(np.random.default_rng(11), rot_deg=1.0, trans=0.02)
+    run_and_compare(env, sc, view=view, flags=cs.POSE_ONLY)
+
+
+@pytest.mark.slow
+def test_c4_scannet_prune_and_rvq_parity(env):
+    """C4: ScanNet-shaped 1M unpruned Gaussians: mask-prune (survivors,
+    keep_map, every plane) and 4-stage x 256 R-VQ of the survivors' scale and
+    rotation, bit-exact."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.scannet_scene(0)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    km = torch.empty(g.n, dtype=torch.int32, device=dev)
+    out, _, km, nk = cs.mask_prune(g, keep_map=km)
+    keep = sc.mask > orc.mask_tau(0.01)
+    k = int(nk.item())
+    assert k == int(keep.sum()) and 0.45 * sc.n < k < 0.57 * sc.n
+    km_ref = np.where(keep, np.cumsum(keep) - 1, -1).astype(np.int32)
+    assert np.array_equal(km.cpu().numpy(), km_ref)
+    for name in ("mean", "log_scale", "quat", "opacity"):
+        a = getattr(out, name).cpu().numpy().reshape(-1, sc.n)[:, :k]
+        assert np.array_equal(a, getattr(sc, name).reshape(-1, sc.n)[:, keep]), name
+    for name, cname in (("log_scale", "scale_codes"), ("quat", "rot_codes")):
+        codes = sc.codebook[cname]
+        idx, rec = cs.rvq_assign(getattr(out, name), torch.tensor(codes, device=dev),
+                                 n_dev=nk)
+        idx_o, rec_o = orc.rvq_assign(getattr(sc, name)[:, keep], codes)
+        assert np.array_equal(idx.cpu().numpy()[:, :k].astype(np.uint16), idx_o), name
+        assert np.array_equal(rec.cpu().numpy()[:, :k], rec_o), name
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("kf", [0, 21])
+def test_c5_window_keyframe_parity(env, kf):
+    """C5: 500k Gaussians on the box faces, inward-facing keyframe `kf` of 64,
+    R-VQ 4x256: full fwd + bwd parity of one keyframe render."""
+    sc = synth.window_scene(0)
+    run_and_compare(env, sc, view=sc.views[kf])
