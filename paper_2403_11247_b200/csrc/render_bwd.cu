@@ -2,20 +2,23 @@
 // P:98-109) -- the paper's "functions to manage depth, pose, and cumulative
 // opacity during both forward and backward propagation"; R23.
 //
-// One CTA of 128 threads per 16x16 tile, two vertically adjacent pixels per
-// thread (8x8 pixels per warp), replaying the tile list back to front with the
-// same TMA-streamed batches as the forward.  Per pixel, from T_final and
-// n_contrib: T_j = T_{j+1} / (1 - alpha_j), v_j = <rgb_j, dL/dC> + z_j dL/dD +
-// dL/dS, dL/dalpha_j = T_j (v_j - B_j), B_{j-1} = alpha_j v_j + (1-alpha_j) B_j.
+// One CTA per 16x16 tile: 4 pixel warps (two vertically adjacent pixels per
+// thread, 8x8 pixels per warp) plus 1 producer warp.  The producer streams the
+// tile's records back to front with 1-D TMA bulk copies into a kBS-slot ring
+// (mbarrier full[] with complete_tx) and, once all pixel warps have released a
+// slot (mbarrier empty[], one arrival per warp), folds the warps' per-entry
+// partial sums for that batch into the global [n][12] accumulator with three
+// red.global.add.v4.f32 per (tile, Gaussian).  The pixel warps never wait for
+// each other: no CTA barrier inside the replay, so a warp with a heavy 8x8
+// block does not stall the others.
 //
-// Reduction of the ten per-(pixel, entry) partials (u, v, ca, cb, cc, o_hat,
-// z, r, g, b): a thread first adds its two pixels in registers; each warp then
-// stores its lanes' partials for a group of kG entries as rows of shared
-// memory and sums every row with the lanes transposed (lane l sums row l, l+32,
-// ... with conflict-free rotated LDS.128) -- about 2 instructions per (entry,
-// value) instead of the 10 of a shuffle butterfly.  The 4 warps' sums meet in
-// shared memory and leave the CTA as three red.global.add.v4.f32 per (tile,
-// Gaussian) into the [n][12] accumulator consumed by the chain (chain.cu).
+// Per pixel, from T_final and n_contrib: T_j = T_{j+1} / (1 - alpha_j),
+// v_j = <rgb_j, dL/dC> + z_j dL/dD + dL/dS, dL/dalpha_j = T_j (v_j - B_j),
+// B_{j-1} = alpha_j v_j + (1-alpha_j) B_j.  A thread adds its two pixels'
+// ten partials (u, v, ca, cb, cc, o_hat, z, r, g, b) in registers; the warp
+// stores the lanes' partials of kG entries as shared-memory rows and each lane
+// sums whole rows with rotated LDS.128 (a transposed reduction: ~2
+// instructions per (entry, value) instead of a 10-instruction shuffle tree).
 #include "common.cuh"
 
 namespace csplat {
@@ -23,26 +26,31 @@ namespace csplat {
 constexpr int kBB = 32;           // records per TMA batch
 constexpr int kBS = 3;            // ring depth
 constexpr int kAcc = 12;          // accumulator floats per Gaussian
-constexpr int kBwdThreads = 128;  // 4 warps x 32 lanes x 2 pixels = one 16x16 tile
-constexpr int kBwdWarps = kBwdThreads / 32;
+constexpr int kCW = 4;            // pixel (consumer) warps: 4 x 32 lanes x 2 pixels = 16x16
+constexpr int kBwdThreads = (kCW + 1) * 32;  // + 1 producer warp
 constexpr int kG = 4;             // entries per transposed-reduction group (smem vs occupancy)
 constexpr int kV = 10;            // partials per (pixel, entry)
 
 size_t bwd_workspace_bytes(int64_t n) { return (size_t)(n > 0 ? n : 1) * kAcc * sizeof(float); }
 
 struct BwdSmem {
-  float4 buf[kBS][kBB * 4];               // staged records
-  float4 red[kBwdWarps][kG * kV][8];      // per-warp rows of 32 lane partials
-  float part[kBwdWarps][kBB][kAcc];       // per-warp sums per batch entry
-  uint64_t full[kBS];
-  uint32_t act[kBwdWarps][kG];
-  int smax;
+  float4 buf[kBS][kBB * 4];             // staged records
+  float4 red[kCW][kG * kV][8];          // per-warp rows of 32 lane partials
+  float part[kBS][kCW][kBB][kAcc];      // per-slot, per-warp sums per batch entry
+  uint64_t full[kBS], empty[kBS];
+  uint32_t pact[kBS][kCW];              // did warp w write part[slot][w]?
+  uint32_t act[kCW][kG];
+  int wmax[kCW];
 };
 
 __device__ __forceinline__ float ex2_approx_b(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 struct BPix {
@@ -98,126 +106,161 @@ __global__ void __launch_bounds__(kBwdThreads) k_render_bwd(
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const uint32_t start = range[2 * tile];
+  const bool producer = wid == kCW;
+
+  // ---- pixel state (pixel warps only)
   const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * 8;
   const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * 2, py1 = py0 + 1;
-  const uint32_t wlo = (uint32_t)wx0 | ((uint32_t)wy0 << 16);
-  const uint32_t whi_x = ((uint32_t)(wx0 + 7) | ((uint32_t)(wy0 + 7) << 16)) | 0x80008000u;
-  const uint32_t start = range[2 * tile];
-  const int64_t HW = (int64_t)W * H;
-
   BPix pp[2];
 #pragma unroll
   for (int k = 0; k < 2; k++) {
     const int py = k ? py1 : py0;
     BPix &p = pp[k];
     p.T = 1.f; p.B = 0.f; p.gr = p.gg = p.gb = p.gd = p.gs = 0.f; p.last = 0;
-    if (px < W && py < H) {
-      const int64_t q = (int64_t)py * W + px;
+    if (!producer && px < W && py < H) {
+      const int64_t HW = (int64_t)W * H, q = (int64_t)py * W + px;
       p.T = t_final[q];
       p.last = n_contrib[q];
       p.gr = dC[q]; p.gg = dC[HW + q]; p.gb = dC[2 * HW + q];
       p.gd = dD[q]; p.gs = dS[q];
     }
   }
-  if (tid == 0) {
-    sm.smax = 0;
-    for (int s = 0; s < kBS; s++) mbar_init(&sm.full[s], 1);
+  const int mylast = max(pp[0].last, pp[1].last);
+  const int wmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)mylast);
+  if (!producer && lane == 0) sm.wmax[wid] = wmax;
+  if (tid == kCW * 32) {
+    for (int s = 0; s < kBS; s++) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kCW);
+    }
     fence_mbar_init();
   }
   __syncthreads();
-  const int mylast = max(pp[0].last, pp[1].last);
-  const int wmax = __reduce_max_sync(0xffffffffu, (unsigned)mylast);
-  if (lane == 0) atomicMax(&sm.smax, wmax);
-  __syncthreads();
-  const int maxlast = sm.smax;
-  const int nb = (maxlast + kBB - 1) / kBB;
-  int issued = 0;
-  auto issue = [&](int k) {  // replay batch k covers entries of batch b = nb - 1 - k
-    const int b = nb - 1 - k;
-    const int cnt = min(kBB, maxlast - b * kBB);
-    const uint32_t bytes = (uint32_t)cnt * CSPLAT_RECORD_BYTES;
-    uint64_t *bar = &sm.full[k % kBS];
-    mbar_arrive_expect_tx(bar, bytes);
-    tma_load_1d(&sm.buf[k % kBS][0], pair_rec + ((int64_t)start + (int64_t)b * kBB) * 4, bytes,
-                bar);
-  };
-  if (tid == 0)
-    for (; issued < min(kBS - 1, nb); issued++) issue(issued);
+  int maxlast = 0;
+#pragma unroll
+  for (int w = 0; w < kCW; w++) maxlast = max(maxlast, sm.wmax[w]);
+  const int nb = (maxlast + kBB - 1) / kBB;  // replay batch k covers batch b = nb - 1 - k
+  auto batch_cnt = [&](int k) { return min(kBB, maxlast - (nb - 1 - k) * kBB); };
 
+  if (producer) {
+    // fold the pixel warps' partials of replay batch k (slot s) into the accumulator
+    auto flush = [&](int k, int s) {
+      const int cnt = batch_cnt(k);
+      const float4 *rb = sm.buf[s];
+      for (int p = lane; p < cnt * 3; p += 32) {
+        const int e = p / 3, c = p - (p / 3) * 3;
+        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < kCW; w++) {
+          if (!sm.pact[s][w]) continue;
+          const float4 t4 = reinterpret_cast<const float4 *>(sm.part[s][w][e])[c];
+          s4.x += t4.x; s4.y += t4.y; s4.z += t4.z; s4.w += t4.w;
+        }
+        if (c == 2) { s4.z = 0.f; s4.w = 0.f; }  // padding slots
+        if (s4.x != 0.f || s4.y != 0.f || s4.z != 0.f || s4.w != 0.f) {
+          const uint32_t gid = __float_as_uint(rb[e * 4 + 2].w);
+          red_add_v4(acc + (int64_t)gid * kAcc + c * 4, s4.x, s4.y, s4.z, s4.w);
+        }
+      }
+    };
+    for (int k = 0; k < nb; k++) {
+      const int s = k % kBS;
+      if (k >= kBS) {  // slot s held replay batch k - kBS: wait for all pixel warps
+        mbar_wait(&sm.empty[s], (uint32_t)((k / kBS) - 1) & 1u);
+        flush(k - kBS, s);
+        __syncwarp();  // every lane has read the slot's gids before it is overwritten
+      }
+      if (lane == 0) {
+        const int b = nb - 1 - k;
+        const uint32_t bytes = (uint32_t)batch_cnt(k) * CSPLAT_RECORD_BYTES;
+        mbar_arrive_expect_tx(&sm.full[s], bytes);
+        tma_load_1d(&sm.buf[s][0], pair_rec + ((int64_t)start + (int64_t)b * kBB) * 4, bytes,
+                    &sm.full[s]);
+      }
+      __syncwarp();
+    }
+    for (int k = max(0, nb - kBS); k < nb; k++) {  // drain the last slots
+      const int s = k % kBS;
+      mbar_wait(&sm.empty[s], (uint32_t)(k / kBS) & 1u);
+      flush(k, s);
+    }
+    return;
+  }
+
+  // ---- pixel warps
+  const uint32_t wlo = (uint32_t)wx0 | ((uint32_t)wy0 << 16);
+  const uint32_t whi_x = ((uint32_t)(wx0 + 7) | ((uint32_t)(wy0 + 7) << 16)) | 0x80008000u;
   const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
   float(*red)[8 * 4] = reinterpret_cast<float(*)[8 * 4]>(sm.red[wid]);  // [kG*kV][32]
   for (int k = 0; k < nb; k++) {
-    __syncthreads();  // slot of batch k-1 and part[] are free again
-    if (tid == 0 && issued < nb && issued <= k + kBS - 1) issue(issued++);
-    mbar_wait(&sm.full[k % kBS], (uint32_t)(k / kBS) & 1u);
-    const float4 *rb = sm.buf[k % kBS];
+    const int s = k % kBS;
     const int b = nb - 1 - k;
-    const int cnt = min(kBB, maxlast - b * kBB);
-    for (int g0 = 0; g0 < cnt; g0 += kG) {  // processing index g0 + s <-> entry cnt-1-g0-s
-      const int ng = min(kG, cnt - g0);
-      for (int s = 0; s < ng; s++) {
-        const int e = cnt - 1 - g0 - s;
-        const int j = b * kBB + e;
-        const float4 r3 = rb[e * 4 + 3];
-        const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
-        const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
-        bool any = false;
-        // warp-uniform: the record's rectangle meets this warp's 8x8 block and
-        // the entry is inside some lane's replay range
-        if ((t1 & t2 & 0x80008000u) == 0x80008000u && j < wmax) {
-          const float4 r0 = rb[e * 4 + 0];
-          const float4 r1 = rb[e * 4 + 1];
-          const float4 r2 = rb[e * 4 + 2];
-          float v[kV];
+    const int cnt = batch_cnt(k);
+    mbar_wait(&sm.full[s], (uint32_t)(k / kBS) & 1u);
+    const bool work = b * kBB < wmax;  // warp-uniform: some lane replays into this batch
+    if (work) {
+      const float4 *rb = sm.buf[s];
+      for (int g0 = 0; g0 < cnt; g0 += kG) {  // processing index g0 + q <-> entry cnt-1-g0-q
+        const int ng = min(kG, cnt - g0);
+        for (int q = 0; q < ng; q++) {
+          const int e = cnt - 1 - g0 - q;
+          const int j = b * kBB + e;
+          const float4 r3 = rb[e * 4 + 3];
+          const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
+          const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
+          bool any = false;
+          // warp-uniform: the record's rectangle meets this warp's 8x8 block and
+          // the entry is inside some lane's replay range
+          if ((t1 & t2 & 0x80008000u) == 0x80008000u && j < wmax) {
+            const float4 r0 = rb[e * 4 + 0];
+            const float4 r1 = rb[e * 4 + 1];
+            const float4 r2 = rb[e * 4 + 2];
+            float v[kV];
 #pragma unroll
-          for (int c = 0; c < kV; c++) v[c] = 0.f;
-          const float dx = DSUB(fpx, r0.x);
-          bool a = bwd_pixel(pp[0], j, dx, DSUB(fpy0, r0.y), r0, r1, r2, amax, v);
-          a |= bwd_pixel(pp[1], j, dx, DSUB(fpy1, r0.y), r0, r1, r2, amax, v);
-          any = __any_sync(0xffffffffu, a);
-          if (any) {  // every lane writes its (possibly zero) partials
+            for (int c = 0; c < kV; c++) v[c] = 0.f;
+            const float dx = DSUB(fpx, r0.x);
+            bool a = bwd_pixel(pp[0], j, dx, DSUB(fpy0, r0.y), r0, r1, r2, amax, v);
+            a |= bwd_pixel(pp[1], j, dx, DSUB(fpy1, r0.y), r0, r1, r2, amax, v);
+            any = __any_sync(0xffffffffu, a);
+            if (any) {  // every lane writes its (possibly zero) partials
 #pragma unroll
-            for (int c = 0; c < kV; c++) red[s * kV + c][lane] = v[c];
+              for (int c = 0; c < kV; c++) red[q * kV + c][lane] = v[c];
+            }
           }
+          if (lane == 0) sm.act[wid][q] = any ? 1u : 0u;
         }
-        if (lane == 0) sm.act[wid][s] = any ? 1u : 0u;
-      }
-      __syncwarp();
-      // transposed sums: lane l owns rows l, l+32, l+64 of the ng*kV rows
-      for (int r = lane; r < ng * kV; r += 32) {
-        const int s = r / kV, c = r - s * kV;
-        float sum = 0.f;
-        if (sm.act[wid][s]) {
-          const float4 *row = sm.red[wid][r];
+        __syncwarp();
+        // transposed sums: lane l owns rows l, l+32 of the ng*kV rows
+        for (int r = lane; r < ng * kV; r += 32) {
+          const int q = r / kV, c = r - q * kV;
+          float sum = 0.f;
+          if (sm.act[wid][q]) {
+            // 32 partials as 8 rotated 16-byte chunks, summed on packed FADD2
+            const float4 *row = sm.red[wid][r];
+            unsigned long long s01 = 0ull, s23 = 0ull;
 #pragma unroll
-          for (int t = 0; t < 8; t++) {
-            const float4 x = row[(t + lane) & 7];
-            sum += (x.x + x.y) + (x.z + x.w);
+            for (int t = 0; t < 8; t++) {
+              const float4 x = row[(t + lane) & 7];
+              unsigned long long a, b;
+              asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(x.x), "f"(x.y));
+              asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(x.z), "f"(x.w));
+              asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s01) : "l"(a));
+              asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s23) : "l"(b));
+            }
+            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s01) : "l"(s23));
+            sum = __uint_as_float((uint32_t)s01) + __uint_as_float((uint32_t)(s01 >> 32));
           }
+          sm.part[s][wid][cnt - 1 - g0 - q][c] = sum;
         }
-        sm.part[wid][cnt - 1 - g0 - s][c] = sum;
+        __syncwarp();
       }
-      __syncwarp();
     }
-    __syncthreads();
-    // combine the 4 warps: thread (e, c) owns float4 c of entry e
-    if (tid < cnt * 3) {
-      const int e = tid / 3, c = tid - (tid / 3) * 3;
-      float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int w = 0; w < kBwdWarps; w++) {
-        const float4 t4 = reinterpret_cast<const float4 *>(sm.part[w][e])[c];
-        s4.x += t4.x; s4.y += t4.y; s4.z += t4.z; s4.w += t4.w;
-      }
-      if (c == 2) { s4.z = 0.f; s4.w = 0.f; }  // padding slots
-      if (s4.x != 0.f || s4.y != 0.f || s4.z != 0.f || s4.w != 0.f) {
-        const uint32_t gid = __float_as_uint(rb[e * 4 + 2].w);
-        red_add_v4(acc + (int64_t)gid * kAcc + c * 4, s4.x, s4.y, s4.z, s4.w);
-      }
+    if (lane == 0) {
+      sm.pact[s][wid] = work ? 1u : 0u;
+      mbar_arrive(&sm.empty[s]);  // release: part[s][wid] and the slot are done
     }
   }
-  if (tid == 0)
-    for (int kk = nb; kk < issued; kk++) mbar_wait(&sm.full[kk % kBS], (uint32_t)(kk / kBS) & 1u);
 }
 
 cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
