@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tracking", action="store_true")
     ap.add_argument("--profile-stages", action="store_true", default=True)
     return ap.parse_args()
 
@@ -149,6 +150,51 @@ def stage_rooflines(stage_ms, counts, n_kept, n_pairs, e_bwd, peaks, step):
         al("render_fwd", 10.0 * counts["e_pix"] + 11.0 * counts["e_contrib"])
         al("render_bwd", 10.0 * e_bwd + 35.0 * counts["e_contrib"])
     return out
+
+
+def bench_tracking(dev, flush, iters=40, frames=3):
+    """NEXT-1 on config C3: TUM-shaped 640x480, 100k Gaussians, R-VQ 4x256;
+    observed images rendered at the true pose; each frame = 40 pose-only
+    iterations (project, bin, fwd, tracking loss, bwd POSE_ONLY, host pose
+    step) from a 1 deg / 2 cm perturbation.  CUDA-event timed per frame."""
+    import torch
+    from paper_2403_11247_b200 import csplat as cs
+    from paper_2403_11247_b200.pipeline import RenderStep
+    from paper_2403_11247_b200.tracking import Tracker, pose_error
+    from scenes import synth
+    sc = synth.tum_scene(0)
+    gt = sc.views[0]
+    start = synth.perturbed_view(np.random.default_rng(11), rot_deg=1.0, trans=0.02)
+    obs = RenderStep(sc.planes(), sc.cam, sc.codebook, device=dev)
+    obs.size_pairs(gt)
+    obs.front(gt)
+    obs.forward()
+    obs_c, obs_d = obs.img["color"].clone(), obs.img["depth"].clone()
+    st = RenderStep(sc.planes(), sc.cam, sc.codebook, device=dev, flags=cs.POSE_ONLY)
+    st.size_pairs(start, views=[gt])
+    tr = Tracker(st, obs_c, obs_d)
+    tr.track(start, iters=3)  # warm-up
+    stream = torch.cuda.current_stream(dev)
+    times, errs, losses = [], [], None
+    for _ in range(frames):
+        flush.fill_(1.0)
+        tr.step.prepare()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        view, losses = tr.track(start, iters=iters, lr_rot=5e-4, lr_trans=5e-4)
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+        errs.append(pose_error(view, gt))
+    st.check_capacity()
+    ms = statistics.median(times)
+    return {"workload": "C3 TUM 640x480, 100k Gaussians, R-VQ 4x256, pose-only",
+            "iters_per_frame": iters, "ms_per_frame": ms, "ms_per_iter": ms / iters,
+            "iters_per_s": 1e3 * iters / ms, "frames_per_s": 1e3 / ms,
+            "loss_first_last": [losses[0], losses[-1]],
+            "pose_err_start_deg_m": list(pose_error(start, gt)),
+            "pose_err_end_deg_m": list(errs[-1]),
+            "note": "includes one 36-byte device->host read per iteration for the host pose step"}
 
 
 # ---------------------------------------------------------------- oracle (CPU) legs
@@ -398,6 +444,11 @@ def main():
         e2e = {"value": world * args.steps / t_e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
 
+    # ---- NEXT-1: C3 TUM tracking (40 pose-only iterations per frame), rank 0 only
+    tracking = None
+    if rank == 0 and not args.no_tracking:
+        tracking = bench_tracking(dev, flush)
+
     if rank == 0:
         n_kept = int(step.n_kept.item())
         n_pairs = int(step.n_pairs.item())
@@ -478,6 +529,8 @@ def main():
                                                         + stage_ms["render_bwd"])
             line["stage_roofline"] = stage_rooflines(stage_ms, counts, n_kept, n_pairs, e_bwd,
                                                      peaks, step)
+        if tracking:
+            line["tracking_c3"] = tracking
         if roof:
             line["roofline"] = roof
         if cpu:

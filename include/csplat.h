@@ -179,7 +179,29 @@ int csplat_mask_prune(const csplat_gaussians *in, const csplat_codebook *in_idx,
                       void *out_scale_idx, void *out_rot_idx, int32_t *keep_map,
                       int64_t *n_kept_dev, void *ws, size_t ws_bytes, void *stream);
 
-enum csplat_op { CSPLAT_OP_BIN_TILES = 1, CSPLAT_OP_RENDER_BWD = 2, CSPLAT_OP_MASK_PRUNE = 3 };
+/* NEXT-1: the tracking objective of Sec 3.4 -- Eq 12 gated by the
+ * rendered silhouette as in Eq 14; the SIFT reprojection term is
+ * out of scope (reading R27 in DESIGN.md).  Per pixel p: g = 1[S_p > sil_gate],
+ * v = 1[obs_depth_p > 0];  L_c = (1/HW) sum g |C - C_obs|^2,
+ * L_d = (1/|R|) sum g v (D - D_obs)^2 with |R| = #valid-depth pixels (>= 1),
+ * L_t = L_c + lambda_depth L_d.  Writes the upstream gradients of
+ * csplat_render_bwd: d_color = 2 g (C - C_obs)/HW, d_depth = 2 lambda g v
+ * (D - D_obs)/|R|, d_silhouette = 0 (the gate is not differentiated), and
+ * loss3_dev (optional, device float[3]) = (L_t, L_c, L_d).  Inputs planar
+ * [3][H][W] / [H][W] float32 (device).  ws: csplat_workspace_bytes(
+ * CSPLAT_OP_TRACKING_LOSS, 0, 0, NULL). */
+int csplat_tracking_loss(const float *color, const float *depth, const float *silhouette,
+                         const float *obs_color, const float *obs_depth, int32_t width,
+                         int32_t height, float lambda_depth, float sil_gate, float *d_color,
+                         float *d_depth, float *d_silhouette, float *loss3_dev, void *ws,
+                         size_t ws_bytes, void *stream);
+
+enum csplat_op {
+  CSPLAT_OP_BIN_TILES = 1,
+  CSPLAT_OP_RENDER_BWD = 2,
+  CSPLAT_OP_MASK_PRUNE = 3,
+  CSPLAT_OP_TRACKING_LOSS = 4
+};
 
 /* Scratch bytes needed by `op` for n Gaussians / pair_capacity pairs. */
 size_t csplat_workspace_bytes(int op, int64_t n, int64_t pair_capacity, const csplat_camera *cam);

@@ -19,7 +19,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["oracle_project.c", "oracle_render.c", "oracle_rvq_prune.c"]
+_SRCS = ["oracle_project.c", "oracle_render.c", "oracle_rvq_prune.c", "oracle_loss.c"]
 
 REC_WORDS = 16
 TILE = 16
@@ -283,6 +283,23 @@ def smooth_bwd(scene: Scene, cam: dict, v, d_color, d_depth, d_sil, prm: Params 
     out = {k: grads[s] for k, s in GRAD_SLICES.items()}
     out["pose"] = pose
     return out
+
+
+def tracking_loss(color, depth, sil, obs_color, obs_depth, lambda_d=1.0, gate=0.99):
+    """NEXT-1 (Eq 12 + Eq 14 gate): upstream grads (dC, dD, dS), (L_t, L_c, L_d), flags."""
+    color = np.ascontiguousarray(color, dtype=np.float64)
+    depth = np.ascontiguousarray(depth, dtype=np.float64)
+    sil = np.ascontiguousarray(sil, dtype=np.float64)
+    oc = _f32(obs_color)
+    od = _f32(obs_depth)
+    H, W = depth.shape
+    dC = np.zeros_like(color); dD = np.zeros_like(depth); dS = np.zeros_like(sil)
+    loss = np.zeros(3); flags = np.zeros((H, W), dtype=np.uint8)
+    rc = lib().oracle_tracking_loss(_p(color), _p(depth), _p(sil), _p(oc), _p(od), C.c_int32(W),
+                                    C.c_int32(H), C.c_double(lambda_d), C.c_double(gate), _p(dC),
+                                    _p(dD), _p(dS), _p(loss), _p(flags))
+    assert rc == 0
+    return (dC, dD, dS), loss, flags
 
 
 def rvq_assign(x, codes):

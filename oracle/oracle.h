@@ -119,6 +119,13 @@ int oracle_mask_prune(int64_t n, const float *mask, float mask_eps,
                       int32_t n_idx_planes, const uint16_t *const *in_idx, uint16_t *const *out_idx,
                       int32_t mask_plane, float reset_mask, int32_t *keep_map, int64_t *n_kept);
 
+/* NEXT-1 tracking loss (Eq 12 gated by Eq 14, reading R27): upstream
+ * gradients dL/d(colour, depth, silhouette) and loss3 = (L_t, L_c, L_d). */
+int oracle_tracking_loss(const double *color, const double *depth, const double *sil,
+                         const float *obs_color, const float *obs_depth, int32_t width,
+                         int32_t height, double lambda_d, double gate, double *d_color,
+                         double *d_depth, double *d_sil, double *loss3, uint8_t *flags);
+
 /* Restrict oracle_render_fwd/bwd to pixel rows [row_lo, row_hi) (row_hi < 0:
  * all rows) -- used only to time a bounded CPU-baseline sample. */
 void oracle_set_row_window(int32_t row_lo, int32_t row_hi);

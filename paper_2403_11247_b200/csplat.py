@@ -67,8 +67,10 @@ class Grads(C.Structure):
 
 
 EXPORTS = ["csplat_project", "csplat_bin_tiles", "csplat_render_fwd", "csplat_render_bwd",
-           "csplat_rvq_assign", "csplat_mask_prune", "csplat_workspace_bytes",
-           "csplat_last_error", "csplat_status_string", "csplat_version"]
+           "csplat_rvq_assign", "csplat_mask_prune", "csplat_tracking_loss",
+           "csplat_workspace_bytes", "csplat_last_error", "csplat_status_string",
+           "csplat_version"]
+OP_TRACKING_LOSS = 4
 
 _lib = None
 
@@ -88,6 +90,8 @@ def lib():
         L.csplat_rvq_assign.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp]
         L.csplat_mask_prune.argtypes = [vp, vp, C.c_float, C.c_float, vp, vp, vp, vp, vp, vp,
                                         C.c_size_t, vp]
+        L.csplat_tracking_loss.argtypes = [vp] * 5 + [i32, i32, C.c_float, C.c_float] + \
+            [vp] * 5 + [C.c_size_t, vp]
         L.csplat_workspace_bytes.argtypes = [C.c_int, i64, i64, vp]
         L.csplat_workspace_bytes.restype = C.c_size_t
         L.csplat_last_error.argtypes = [C.c_char_p, C.c_size_t]
@@ -278,6 +282,27 @@ def render_bwd(g: GaussianMap, cam: dict, v, rec, pair_rec, tile_range, t_final,
                                    flags, C.byref(gr), _ptr(ws), ws.numel(), _stream(stream)),
            "csplat_render_bwd")
     return grads
+
+
+def tracking_loss(img: dict, obs_color, obs_depth, lambda_depth=1.0, sil_gate=0.99, out=None,
+                  loss3=None, ws=None, stream=None):
+    """NEXT-1 (Eq 12 gated by Eq 14): upstream grads (d_color, d_depth, d_sil) of the
+    rendered images `img` (render_fwd output) and loss3 = (L_t, L_c, L_d) on the device."""
+    color, depth, sil = img["color"], img["depth"], img["sil"]
+    H, W = depth.shape
+    dev = depth.device
+    if out is None:
+        out = (torch.empty_like(color), torch.empty_like(depth), torch.empty_like(sil))
+    if loss3 is None:
+        loss3 = torch.zeros(3, device=dev)
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_TRACKING_LOSS, 0), dtype=torch.uint8, device=dev)
+    _check(lib().csplat_tracking_loss(_ptr(color), _ptr(depth), _ptr(sil), _ptr(obs_color),
+                                      _ptr(obs_depth), W, H, lambda_depth, sil_gate,
+                                      _ptr(out[0]), _ptr(out[1]), _ptr(out[2]), _ptr(loss3),
+                                      _ptr(ws), ws.numel(), _stream(stream)),
+           "csplat_tracking_loss")
+    return out, loss3
 
 
 def rvq_assign(x, codes, idx_bytes=None, n_dev=None, idx=None, recon=None, want_recon=True,

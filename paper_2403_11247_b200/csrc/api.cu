@@ -146,6 +146,7 @@ size_t csplat_workspace_bytes(int op, int64_t n, int64_t pairs, const csplat_cam
     case CSPLAT_OP_BIN_TILES: return cam ? csplat::bin_workspace_bytes(n, pairs, *cam) : 0;
     case CSPLAT_OP_RENDER_BWD: return csplat::bwd_workspace_bytes(n);
     case CSPLAT_OP_MASK_PRUNE: return csplat::prune_workspace_bytes(n);
+    case CSPLAT_OP_TRACKING_LOSS: return 64;
     default: return 0;
   }
 }
@@ -257,6 +258,29 @@ int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
                                                d_depth, d_silhouette, flags, *out, ws,
                                                static_cast<cudaStream_t>(stream)),
                      "csplat_render_bwd");
+}
+
+int csplat_tracking_loss(const float *color, const float *depth, const float *silhouette,
+                         const float *obs_color, const float *obs_depth, int32_t width,
+                         int32_t height, float lambda_depth, float sil_gate, float *d_color,
+                         float *d_depth, float *d_silhouette, float *loss3_dev, void *ws,
+                         size_t ws_bytes, void *stream) {
+  if (width <= 0 || height <= 0) return invalid("width/height must be > 0");
+  if (!color || !depth || !silhouette || !obs_color || !obs_depth || !d_color || !d_depth ||
+      !d_silhouette)
+    return invalid("tracking_loss: NULL argument");
+  if (!std::isfinite(lambda_depth) || !std::isfinite(sil_gate))
+    return invalid("lambda_depth / sil_gate must be finite");
+  if (!ws || ws_bytes < 64) {
+    set_err("tracking_loss workspace too small");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_tracking_loss(color, depth, silhouette, obs_color, obs_depth,
+                                                  width, height, lambda_depth, sil_gate, d_color,
+                                                  d_depth, d_silhouette, loss3_dev, ws,
+                                                  static_cast<cudaStream_t>(stream)),
+                     "csplat_tracking_loss");
 }
 
 int csplat_rvq_assign(const float *x, int64_t n, const int64_t *n_dev, int32_t d,

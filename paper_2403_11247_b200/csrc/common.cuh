@@ -182,6 +182,11 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
 cudaError_t launch_rvq(const float *x, int64_t n, const int64_t *n_dev, int d, const float *codes,
                        int L, int P, void *idx, int idx_bytes, float *recon, cudaStream_t s);
 
+cudaError_t launch_tracking_loss(const float *color, const float *depth, const float *sil,
+                                 const float *obs_color, const float *obs_depth, int W, int H,
+                                 float lambda_d, float gate, float *d_color, float *d_depth,
+                                 float *d_sil, float *loss3, void *ws, cudaStream_t s);
+
 size_t prune_workspace_bytes(int64_t n);
 cudaError_t launch_prune(const csplat_gaussians &in, const DecodeArgs *idx, float tau,
                          float reset, const csplat_gaussians_out &out, void *out_sidx,

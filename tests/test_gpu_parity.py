@@ -331,6 +331,63 @@ def test_window_accumulate_matches_sum_of_views(env):
         assert torch.allclose(win.poses[k], poses[k], rtol=1e-4, atol=1e-4)
 
 
+# ------------------------------------------------------------------ NEXT-1 tracking
+
+def _observed(env, sc, view):
+    """Observed colour/depth = the GPU render of the scene at the true pose."""
+    cs, dev = env["cs"], env["dev"]
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec, cnt = cs.project(g, sc.cam, view)
+    b = cs.bin_tiles(rec, cnt, sc.cam, capacity=int(cnt.sum().item()) + 64)
+    out = cs.render_fwd(b["pair_rec"], b["tile_range"], sc.cam)
+    return out["color"].clone(), out["depth"].clone()
+
+
+def test_tracking_loss_parity(env):
+    """csplat_tracking_loss against the oracle on the same rendered images."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.mid_scene(8)
+    obs_c, obs_d = _observed(env, sc, sc.views[0])
+    obs_d[::7] = 0.0                             # some invalid-depth rays
+    view = synth.perturbed_view(np.random.default_rng(4), rot_deg=1.0, trans=0.02)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec, cnt = cs.project(g, sc.cam, view)
+    b = cs.bin_tiles(rec, cnt, sc.cam, capacity=int(cnt.sum().item()) + 64)
+    img = cs.render_fwd(b["pair_rec"], b["tile_range"], sc.cam)
+    (dC, dD, dS), loss3 = cs.tracking_loss(img, obs_c, obs_d, lambda_depth=0.5)
+    (rC, rD, rS), rl, flags = orc.tracking_loss(img["color"].double().cpu().numpy(),
+                                                img["depth"].double().cpu().numpy(),
+                                                img["sil"].double().cpu().numpy(),
+                                                obs_c.cpu().numpy(), obs_d.cpu().numpy(),
+                                                lambda_d=0.5)
+    assert np.allclose(loss3.cpu().numpy(), rl, rtol=1e-4)
+    for a, r in ((dC, rC), (dD, rD), (dS, rS)):
+        a = a.double().cpu().numpy()
+        assert np.abs(a - r).max() <= 1e-6 * max(1.0, np.abs(r).max()) + 1e-9
+
+
+def test_tracking_iterations_reduce_pose_error(env):
+    """Pose-only tracking (project -> bin -> fwd -> loss -> bwd POSE_ONLY ->
+    descent) from a perturbed pose moves towards the true pose."""
+    torch, cs, dev = env["torch"], env["cs"], env["dev"]
+    from paper_2403_11247_b200.pipeline import RenderStep
+    from paper_2403_11247_b200.tracking import Tracker, pose_error
+    sc = synth.mid_scene(9, n=4000)
+    sc.codebook = None
+    gt = sc.views[0]
+    obs_c, obs_d = _observed(env, sc, gt)
+    start = synth.perturbed_view(np.random.default_rng(2), rot_deg=1.0, trans=0.02)
+    st = RenderStep(sc.planes(), sc.cam, None, device=dev, flags=cs.POSE_ONLY)
+    st.size_pairs(start, views=[gt])
+    tr = Tracker(st, obs_c, obs_d)
+    e0 = pose_error(start, gt)
+    view, losses = tr.track(start, iters=60, lr_rot=5e-4, lr_trans=5e-4)
+    e1 = pose_error(view, gt)
+    assert losses[-1] < 0.6 * losses[0], losses[::10]
+    assert all(b <= a * 1.05 for a, b in zip(losses, losses[1:])), losses
+    assert e1[0] < e0[0] and e1[1] < e0[1], (e0, e1)
+
+
 # ------------------------------------------------------------------ configs C3, C4, C5
 
 @pytest.mark.slow

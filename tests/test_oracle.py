@@ -486,6 +486,41 @@ def test_rvq_special_cases(orc):
     assert (idx[0] == d.argmin(0)).all()
 
 
+# ---------------------------------------------------------------- tracking loss (NEXT-1)
+
+def test_tracking_loss_worked_example(orc):
+    g = GOLD["tracking_loss"]
+    C = np.zeros((3, 2, 2)); C[0] = g["color_r"]
+    (dC, dD, dS), loss, flags = orc.tracking_loss(C, np.array(g["depth"]), np.array(g["sil"]),
+                                                  np.zeros((3, 2, 2)), np.array(g["obs_depth"]))
+    assert np.allclose(loss, [g["L_t"], g["L_c"], g["L_d"]], rtol=1e-12)
+    assert np.allclose(dC[0], g["d_color_r"]) and not dC[1:].any()
+    assert np.allclose(dD, g["d_depth"]) and not dS.any() and not flags.any()
+
+
+def test_tracking_loss_gradient_fd(orc):
+    """The returned upstream gradient is the derivative of the returned loss."""
+    r = np.random.default_rng(5)
+    H, W = 6, 7
+    C, D = r.uniform(0, 1, (3, H, W)), r.uniform(0.5, 3, (H, W))
+    S = np.where(r.uniform(0, 1, (H, W)) < 0.7, 0.999, 0.5)
+    OC = r.uniform(0, 1, (3, H, W)).astype(np.float32)
+    OD = np.where(r.uniform(0, 1, (H, W)) < 0.8, r.uniform(0.5, 3, (H, W)), 0).astype(np.float32)
+    (dC, dD, _), loss, _ = orc.tracking_loss(C, D, S, OC, OD, lambda_d=0.7)
+    h = 1e-6
+    for arr, grad in ((C, dC), (D, dD)):
+        flat, gflat = arr.reshape(-1), grad.reshape(-1)
+        for i in r.choice(flat.size, 12, replace=False):
+            x0 = flat[i]
+            flat[i] = x0 + h; lp = orc.tracking_loss(C, D, S, OC, OD, lambda_d=0.7)[1][0]
+            flat[i] = x0 - h; lm = orc.tracking_loss(C, D, S, OC, OD, lambda_d=0.7)[1][0]
+            flat[i] = x0
+            assert abs((lp - lm) / (2 * h) - gflat[i]) < 1e-6
+    # flags mark silhouettes within 1e-5 of the gate
+    (_, _, _), _, fl = orc.tracking_loss(C, D, np.full((H, W), 0.990005), OC, OD)
+    assert fl.all()
+
+
 # ---------------------------------------------------------------- prune
 
 def test_prune_worked_example(orc):
