@@ -372,14 +372,8 @@ def main():
     if args.profile_stages:
         g = step.pruned
         stages = [
-            ("mask_prune", lambda: cs.mask_prune(step.g, None, step.prm.mask_eps, float("nan"),
-                                                 out=g, keep_map=step.keep_map,
-                                                 n_kept=step.n_kept, ws=step.ws_prune)),
-            ("rvq_assign", lambda: (cs.rvq_assign(g.log_scale, step.cb.scale_codes,
-                                                  n_dev=step.n_kept, idx=step.cb.scale_idx,
-                                                  want_recon=False),
-                                    cs.rvq_assign(g.quat, step.cb.rot_codes, n_dev=step.n_kept,
-                                                  idx=step.cb.rot_idx, want_recon=False))),
+            ("mask_prune", step.prune),
+            ("rvq_assign", step.assign_codes),
             ("project", lambda: cs.project(g, step.cam, view, step.prm, step.cb, rec=step.rec,
                                            count=step.count)),
             ("bin_tiles", lambda: cs.bin_tiles(step.rec, step.count, step.cam, step.capacity,

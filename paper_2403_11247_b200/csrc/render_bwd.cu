@@ -96,6 +96,50 @@ __device__ __forceinline__ bool bwd_pixel(BPix &p, int j, float dx, float dy, co
   return true;
 }
 
+// Branch-free form of bwd_pixel for the thread's two pixels: both dependency
+// chains are straight-line code (inactive pixels contribute exact zeros and
+// leave T and B unchanged: alpha = 0 gives rcp(1) = 1), so the compiler can
+// interleave them -- the replay is latency-bound, not issue-bound.
+__device__ __forceinline__ bool bwd_pixel_pair(BPix (&pp)[2], int j, float dx, float dy0,
+                                               float dy1, const float4 &r0, const float4 &r1,
+                                               const float4 &r2, float amax, float (&v)[kV]) {
+  const float dys[2] = {dy0, dy1};
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    BPix &p = pp[k];
+    const float dy = dys[k];
+    const float q = DFMA(DMUL(r0.z, dx), dx, DFMA(DMUL(r0.w, dx), dy, DMUL(DMUL(r1.x, dy), dy)));
+    const bool val = (j < p.last) & (q >= 0.0f) & (q <= r1.z);
+    any |= val;
+    const float G = ex2_approx_b(q * -0.72134752f);  // same expression as the forward
+    const float araw = r1.y * G;
+    const float alpha = val ? fminf(amax, araw) : 0.0f;
+    float rcp;  // alpha <= alpha_max < 1 (R1)
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(1.0f - alpha));
+    const float Tj = p.T * rcp;
+    const float w = alpha * Tj;
+    const float vv = fmaf(r2.x, p.gr, fmaf(r2.y, p.gg, fmaf(r2.z, p.gb, fmaf(r1.w, p.gd, p.gs))));
+    // R23: no gradient through a capped alpha
+    const float dLda = (val & (araw < amax)) ? Tj * (vv - p.B) : 0.0f;
+    v[7] = fmaf(p.gr, w, v[7]);
+    v[8] = fmaf(p.gg, w, v[8]);
+    v[9] = fmaf(p.gb, w, v[9]);
+    v[6] = fmaf(p.gd, w, v[6]);
+    v[5] = fmaf(G, dLda, v[5]);
+    const float dq = -0.5f * alpha * dLda;
+    const float dqdx = dq * dx, dqdy = dq * dy;
+    v[2] = fmaf(dqdx, dx, v[2]);
+    v[3] = fmaf(2.0f * dqdx, dy, v[3]);
+    v[4] = fmaf(dqdy, dy, v[4]);
+    v[0] -= fmaf(2.0f * r0.z, dqdx, r0.w * dqdy);
+    v[1] -= fmaf(r0.w, dqdx, 2.0f * r1.x * dqdy);
+    p.B = fmaf(alpha, vv, (1.0f - alpha) * p.B);
+    p.T = Tj;
+  }
+  return any;
+}
+
 __global__ void __launch_bounds__(kBwdThreads) k_render_bwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, const float *__restrict__ t_final,
@@ -220,8 +264,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_render_bwd(
 #pragma unroll
             for (int c = 0; c < kV; c++) v[c] = 0.f;
             const float dx = DSUB(fpx, r0.x);
-            bool a = bwd_pixel(pp[0], j, dx, DSUB(fpy0, r0.y), r0, r1, r2, amax, v);
-            a |= bwd_pixel(pp[1], j, dx, DSUB(fpy1, r0.y), r0, r1, r2, amax, v);
+            const bool a = bwd_pixel_pair(pp, j, dx, DSUB(fpy0, r0.y), DSUB(fpy1, r0.y), r0, r1,
+                                          r2, amax, v);
             any = __any_sync(0xffffffffu, a);
             if (any) {  // every lane writes its (possibly zero) partials
 #pragma unroll

@@ -52,6 +52,26 @@ __device__ __forceinline__ void composite(PixState &p, float q, float oh, float 
   p.last = idx;
 }
 
+// Predicated form of composite(): a pixel whose q test failed (h = false)
+// contributes w = 0 and keeps T, `last` and `done`.
+__device__ __forceinline__ void composite_pred(PixState &p, bool h, float q, float oh, float z,
+                                               const float4 &rgb, float amax, float tmin,
+                                               int idx) {
+  const float alpha = fminf(amax, oh * ex2_approx(q * -0.72134752f));  // exp(-q/2)
+  const float test = p.T * (1.0f - alpha);
+  const bool stop = test < tmin;          // R3: the triggering entry is not composited
+  const bool take = h & !stop;
+  const float w = take ? alpha * p.T : 0.0f;
+  p.r = fmaf(rgb.x, w, p.r);  // Eq 3
+  p.g = fmaf(rgb.y, w, p.g);
+  p.b = fmaf(rgb.z, w, p.b);
+  p.D = fmaf(z, w, p.D);      // Eq 4 (R8)
+  p.S += w;                   // Eq 5 (R9)
+  p.T = take ? test : p.T;
+  p.last = take ? idx : p.last;
+  p.done |= (h & stop) ? 1 : 0;
+}
+
 __global__ void __launch_bounds__(kFwdThreads) k_render_fwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, float tmin, float *__restrict__ color, float *__restrict__ depth,
@@ -116,8 +136,9 @@ __global__ void __launch_bounds__(kFwdThreads) k_render_fwd(
       if (!(h0 | h1)) continue;
       const float4 r2 = rb[e * 4 + 2];  // r, g, b, gid
       const int idx = b * kBatch + e + 1;
-      if (h0) composite(p0, q0, r1.y, r1.w, r2, amax, tmin, idx);
-      if (h1) composite(p1, q1, r1.y, r1.w, r2, amax, tmin, idx);
+      // both pixels as straight-line (predicated) code so their chains interleave
+      composite_pred(p0, h0, q0, r1.y, r1.w, r2, amax, tmin, idx);
+      composite_pred(p1, h1, q1, r1.y, r1.w, r2, amax, tmin, idx);
     }
   }
   // never leave the CTA with bulk copies in flight into its shared memory

@@ -67,6 +67,7 @@ class RenderStep:
                                   device=self.dev)
         self.upstream = None
         self.graph = None
+        self.side = torch.cuda.Stream(device=self.dev)
 
     def _alloc_pairs(self, cap):
         self.capacity = cap
@@ -93,15 +94,28 @@ class RenderStep:
     def prepare(self):
         """a9 (mask prune) -> a2 (R-VQ assignment of the survivors): once per
         iteration, shared by every view rendered from the same map."""
-        g = self.pruned
-        # the codebook indices are re-assigned below, so only attribute planes are compacted
-        cs.mask_prune(self.g, None, self.prm.mask_eps, float("nan"), out=g,
+        self.prune()
+        self.assign_codes()
+
+    def prune(self):
+        """a9: the codebook indices are re-assigned after, so only attribute planes
+        are compacted."""
+        cs.mask_prune(self.g, None, self.prm.mask_eps, float("nan"), out=self.pruned,
                       keep_map=self.keep_map, n_kept=self.n_kept, ws=self.ws_prune)
+
+    def assign_codes(self):
+        """a2 on the survivors (scale and rotation codebooks)."""
+        g = self.pruned
         if self.cb is not None:
+            # the scale and rotation assignments are independent: run them
+            # concurrently (fork/join on a side stream; preserved by graph capture)
+            main = torch.cuda.current_stream(self.dev)
+            self.side.wait_stream(main)
             cs.rvq_assign(g.log_scale, self.cb.scale_codes, n_dev=self.n_kept,
-                          idx=self.cb.scale_idx, want_recon=False)
+                          idx=self.cb.scale_idx, want_recon=False, stream=main)
             cs.rvq_assign(g.quat, self.cb.rot_codes, n_dev=self.n_kept, idx=self.cb.rot_idx,
-                          want_recon=False)
+                          want_recon=False, stream=self.side)
+            main.wait_stream(self.side)
 
     def render(self, view, flags=None, pose=None):
         """a3 -> a4/a5 -> a6 -> a7/a8 for one view of the prepared map."""
