@@ -15,7 +15,7 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libcsplat.so")
+LIB_PATH = os.environ.get("CSPLAT_LIB", os.path.join(_PKG, "libcsplat.so"))
 
 TILE = 16
 RECORD_BYTES = 64

@@ -24,12 +24,19 @@
 namespace csplat {
 
 constexpr int kBB = 32;           // records per TMA batch
-constexpr int kBS = 3;            // ring depth
+#ifndef KBS_OVERRIDE
+#define KBS_OVERRIDE 3
+#endif
+constexpr int kBS = KBS_OVERRIDE; // ring depth
 constexpr int kAcc = 12;          // accumulator floats per Gaussian
 constexpr int kCW = 4;            // pixel (consumer) warps: 4 x 32 lanes x 2 pixels = 16x16
 constexpr int kBwdThreads = (kCW + 1) * 32;  // + 1 producer warp
 constexpr int kG = 4;             // entries per transposed-reduction group (smem vs occupancy)
 constexpr int kV = 10;            // partials per (pixel, entry)
+#ifndef CSPLAT_BWD_MIN_BLOCKS
+#define CSPLAT_BWD_MIN_BLOCKS 5
+#endif
+constexpr int kBwdMinBlocks = CSPLAT_BWD_MIN_BLOCKS;  // CTAs per SM the register budget targets
 
 size_t bwd_workspace_bytes(int64_t n) { return (size_t)(n > 0 ? n : 1) * kAcc * sizeof(float); }
 
@@ -140,7 +147,7 @@ __device__ __forceinline__ bool bwd_pixel_pair(BPix (&pp)[2], int j, float dx, f
   return any;
 }
 
-__global__ void __launch_bounds__(kBwdThreads) k_render_bwd(
+__global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, const float *__restrict__ t_final,
     const int32_t *__restrict__ n_contrib, const float *__restrict__ dC,
