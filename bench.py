@@ -307,11 +307,22 @@ def main():
     from paper_2403_11247_b200.pipeline import RenderStep
     from scenes import synth
 
-    _build.build()
+    # one process per GPU; (local % device count) and CSPLAT_DIST_BACKEND=gloo only
+    # serve the single-GPU smoke test of the multi-rank code path
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("CSPLAT_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+        if local == 0:
+            _build.build()       # one rank (re)builds the in-tree library, the others wait
+        dist.barrier()
+    else:
+        _build.build()
     sc = synth.replica_scene(args.seed)
     H, W = sc.cam["height"], sc.cam["width"]
     # keyframe view of this rank: identity for rank 0, a nearby pose otherwise
@@ -533,6 +544,7 @@ def main():
             line["e2e"] = e2e
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()           # the other ranks wait for rank 0's CPU-side legs
         dist.destroy_process_group()
 
 
