@@ -196,11 +196,26 @@ int csplat_tracking_loss(const float *color, const float *depth, const float *si
                          float *d_depth, float *d_silhouette, float *loss3_dev, void *ws,
                          size_t ws_bytes, void *stream);
 
+/* NEXT-2: R-VQ codebook update (Eq 11; reading R28): one k-means
+ * M-step for the assignment idx [L][n] (from csplat_rvq_assign): with the
+ * residual r_n^l = x_n - S_hat_n^{l-1} (the DA stage-order sums of
+ * csplat_rvq_assign), codes_out[l][k] = mean of the r_n^l with idx[l][n] = k
+ * (codes with no member are copied), counts_out [L][P] (optional) = members,
+ * loss_out [L+1] (optional, device float) = per-stage sum ||r - C^l[i]||^2 and
+ * L_r = sum / (n P).  codes_out may alias codes.  Sums use float32 atomics
+ * (order-dependent rounding).  ws: csplat_workspace_bytes(CSPLAT_OP_RVQ_UPDATE,
+ * L * P, d, NULL). */
+int csplat_rvq_update(const float *x, int64_t n, const int64_t *n_dev, int32_t d,
+                      const float *codes, int32_t L, int32_t P, const void *idx, int32_t idx_bytes,
+                      float *codes_out, int32_t *counts_out, float *loss_out, void *ws,
+                      size_t ws_bytes, void *stream);
+
 enum csplat_op {
   CSPLAT_OP_BIN_TILES = 1,
   CSPLAT_OP_RENDER_BWD = 2,
   CSPLAT_OP_MASK_PRUNE = 3,
-  CSPLAT_OP_TRACKING_LOSS = 4
+  CSPLAT_OP_TRACKING_LOSS = 4,
+  CSPLAT_OP_RVQ_UPDATE = 5  /* n = L * P codes, pairs = d */
 };
 
 /* Scratch bytes needed by `op` for n Gaussians / pair_capacity pairs. */

@@ -317,6 +317,22 @@ def rvq_assign(x, codes):
     return idx, recon
 
 
+def rvq_update(x, codes, idx):
+    """NEXT-2: k-means M-step for a given assignment -> (new codes, counts, losses[L+1])."""
+    x = _f32(x)
+    codes = _f32(codes)
+    idx = np.ascontiguousarray(idx, dtype=np.uint16)
+    d, n = x.shape
+    L, P, _ = codes.shape
+    out = np.zeros_like(codes)
+    counts = np.zeros((L, P), dtype=np.int32)
+    loss = np.zeros(L + 1)
+    rc = lib().oracle_rvq_update(_p(x), C.c_int64(n), C.c_int32(d), _p(codes), C.c_int32(L),
+                                 C.c_int32(P), _p(idx), _p(out), _p(counts), _p(loss))
+    assert rc == 0
+    return out, counts, loss
+
+
 def mask_prune(planes: list, idx_planes: list, mask_plane: int, mask_eps=0.01,
                reset_mask=float("nan")):
     """a9: planes: list of float32 [n] arrays (one of them the mask logit)."""

@@ -110,6 +110,13 @@ int oracle_smooth_bwd(const or_gaussians *g, const or_camera *cam, const or_view
 int oracle_rvq_assign(const float *x, int64_t n, int32_t d, const float *codes, int32_t L,
                       int32_t P, uint16_t *idx, float *recon);
 
+/* NEXT-2: one k-means M-step of the R-VQ codebooks for a given assignment
+ * (Eq 11, reading R28).  codes_out [L][P][d], counts [L][P], loss_out [L+1]
+ * = per-stage squared errors and L_r. */
+int oracle_rvq_update(const float *x, int64_t n, int32_t d, const float *codes, int32_t L,
+                      int32_t P, const uint16_t *idx, float *codes_out, int32_t *counts,
+                      double *loss_out);
+
 /* Mask prune: order-preserving compaction of survivors of
  * m > tau.  in_planes: n_planes float planes [n] each; idx planes u16 [n].
  * reset_mask: if not NaN, the mask plane (plane index mask_plane) of

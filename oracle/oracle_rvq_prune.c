@@ -10,6 +10,7 @@
  *     Sig(m) <= eps (R12), keep the survivors' relative order.
  */
 #include "oracle_internal.h"
+#include <stdlib.h>
 
 int oracle_rvq_assign(const float *x, int64_t n, int32_t d, const float *codes, int32_t L,
                       int32_t P, uint16_t *idx, float *recon)
@@ -39,6 +40,51 @@ int oracle_rvq_assign(const float *x, int64_t n, int32_t d, const float *codes, 
         if (recon)
             for (int j = 0; j < d; j++) recon[(int64_t)j * n + i] = sh[j];
     }
+    return 0;
+}
+
+/* NEXT-2: one k-means M-step of the R-VQ codebooks given an assignment
+ * (Eq 11; SPEC rvq_train S:308-316 as the update rule, reading
+ * R28).  For every stage l and vector n: r_n = x_n - S_hat_n^{l-1} (float32,
+ * stage-order sum of the assigned codes, as in oracle_rvq_assign), then
+ *   sum_l[k] += r_n, cnt_l[k] += 1 for k = i_n^l,
+ *   err_l    += ||r_n - C^l[i_n^l]||^2          (float64)
+ * new C^l[k] = sum_l[k] / cnt_l[k] (unchanged when cnt = 0).
+ * loss_out[0..L-1] = err_l, loss_out[L] = L_r = sum_l err_l / (n P). */
+int oracle_rvq_update(const float *x, int64_t n, int32_t d, const float *codes, int32_t L,
+                      int32_t P, const uint16_t *idx, float *codes_out, int32_t *counts,
+                      double *loss_out)
+{
+    if (n < 0 || d < 1 || d > 8 || L < 1 || P < 1) return 1;
+    double *sum = (double *)calloc((size_t)L * P * d, sizeof(double));
+    for (int l = 0; l <= L; l++) loss_out[l] = 0.0;
+    for (int64_t k = 0; k < (int64_t)L * P; k++) counts[k] = 0;
+    for (int64_t i = 0; i < n; i++) {
+        float sh[8];
+        for (int j = 0; j < d; j++) sh[j] = 0.0f;
+        for (int l = 0; l < L; l++) {
+            const int k = idx[(int64_t)l * n + i];
+            const float *c = codes + ((int64_t)l * P + k) * d;
+            double e2 = 0.0;
+            for (int j = 0; j < d; j++) {
+                const float r = x[(int64_t)j * n + i] - sh[j];          /* S - S_hat^{l-1} */
+                sum[((int64_t)l * P + k) * d + j] += r;
+                const double e = (double)r - (double)c[j];
+                e2 += e * e;
+            }
+            counts[(int64_t)l * P + k] += 1;
+            loss_out[l] += e2;
+            for (int j = 0; j < d; j++) sh[j] = (l == 0) ? c[j] : sh[j] + c[j];
+        }
+    }
+    for (int64_t k = 0; k < (int64_t)L * P; k++)
+        for (int j = 0; j < d; j++)
+            codes_out[k * d + j] = counts[k] > 0 ? (float)(sum[k * d + j] / counts[k])
+                                                 : codes[k * d + j];
+    double tot = 0.0;
+    for (int l = 0; l < L; l++) tot += loss_out[l];
+    loss_out[L] = n > 0 ? tot / ((double)n * P) : 0.0;
+    free(sum);
     return 0;
 }
 

@@ -67,10 +67,11 @@ class Grads(C.Structure):
 
 
 EXPORTS = ["csplat_project", "csplat_bin_tiles", "csplat_render_fwd", "csplat_render_bwd",
-           "csplat_rvq_assign", "csplat_mask_prune", "csplat_tracking_loss",
+           "csplat_rvq_assign", "csplat_mask_prune", "csplat_tracking_loss", "csplat_rvq_update",
            "csplat_workspace_bytes", "csplat_last_error", "csplat_status_string",
            "csplat_version"]
 OP_TRACKING_LOSS = 4
+OP_RVQ_UPDATE = 5
 
 _lib = None
 
@@ -92,6 +93,8 @@ def lib():
                                         C.c_size_t, vp]
         L.csplat_tracking_loss.argtypes = [vp] * 5 + [i32, i32, C.c_float, C.c_float] + \
             [vp] * 5 + [C.c_size_t, vp]
+        L.csplat_rvq_update.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp, vp, vp,
+                                        C.c_size_t, vp]
         L.csplat_workspace_bytes.argtypes = [C.c_int, i64, i64, vp]
         L.csplat_workspace_bytes.restype = C.c_size_t
         L.csplat_last_error.argtypes = [C.c_char_p, C.c_size_t]
@@ -322,6 +325,25 @@ def rvq_assign(x, codes, idx_bytes=None, n_dev=None, idx=None, recon=None, want_
     _check(lib().csplat_rvq_assign(_ptr(x), n, _ptr(n_dev), d, _ptr(codes), L, P, _ptr(idx),
                                    idx_bytes, _ptr(recon), _stream(stream)), "csplat_rvq_assign")
     return idx, recon
+
+
+def rvq_update(x, codes, idx, n_dev=None, codes_out=None, want_counts=True, ws=None,
+               stream=None):
+    """NEXT-2 (Eq 11): k-means M-step of the codebooks for the assignment idx.
+    Returns (codes_out [L,P,d], counts [L,P] int32 or None, loss [L+1])."""
+    d, n = x.shape
+    L, P, _ = codes.shape
+    dev = x.device
+    if codes_out is None:
+        codes_out = torch.empty_like(codes)
+    counts = torch.empty((L, P), dtype=torch.int32, device=dev) if want_counts else None
+    loss = torch.zeros(L + 1, device=dev)
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_RVQ_UPDATE, L * P, d), dtype=torch.uint8, device=dev)
+    _check(lib().csplat_rvq_update(_ptr(x), n, _ptr(n_dev), d, _ptr(codes), L, P, _ptr(idx),
+                                   idx.element_size(), _ptr(codes_out), _ptr(counts), _ptr(loss),
+                                   _ptr(ws), ws.numel(), _stream(stream)), "csplat_rvq_update")
+    return codes_out, counts, loss
 
 
 def mask_prune(g: GaussianMap, cb: CodebookT | None = None, mask_eps=0.01,

@@ -147,6 +147,8 @@ size_t csplat_workspace_bytes(int op, int64_t n, int64_t pairs, const csplat_cam
     case CSPLAT_OP_RENDER_BWD: return csplat::bwd_workspace_bytes(n);
     case CSPLAT_OP_MASK_PRUNE: return csplat::prune_workspace_bytes(n);
     case CSPLAT_OP_TRACKING_LOSS: return 64;
+    case CSPLAT_OP_RVQ_UPDATE:  // n = L * P, pairs = d
+      return (size_t)n * (size_t)pairs * 4 + (size_t)n * 4 + 17 * 4 + 256;  // L <= 16
     default: return 0;
   }
 }
@@ -281,6 +283,27 @@ int csplat_tracking_loss(const float *color, const float *depth, const float *si
                                                   d_depth, d_silhouette, loss3_dev, ws,
                                                   static_cast<cudaStream_t>(stream)),
                      "csplat_tracking_loss");
+}
+
+int csplat_rvq_update(const float *x, int64_t n, const int64_t *n_dev, int32_t d,
+                      const float *codes, int32_t L, int32_t P, const void *idx, int32_t idx_bytes,
+                      float *codes_out, int32_t *counts_out, float *loss_out, void *ws,
+                      size_t ws_bytes, void *stream) {
+  if (n < 0) return invalid("n < 0");
+  if (d < 1 || d > 8) return invalid("d must be 1..8");
+  if (L < 1 || L > 16) return invalid("L must be 1..16");
+  if (P < 1 || P > 65536) return invalid("P must be 1..65536");
+  if (idx_bytes != 1 && idx_bytes != 2) return invalid("idx_bytes must be 1 or 2");
+  if (!codes || !codes_out || (n > 0 && (!x || !idx))) return invalid("rvq_update: NULL argument");
+  if (!ws || ws_bytes < csplat::rvq_update_workspace_bytes(L, P, d)) {
+    set_err("rvq_update workspace too small");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_rvq_update(x, n, n_dev, d, codes, L, P, idx, idx_bytes,
+                                               codes_out, counts_out, loss_out, ws,
+                                               static_cast<cudaStream_t>(stream)),
+                     "csplat_rvq_update");
 }
 
 int csplat_rvq_assign(const float *x, int64_t n, const int64_t *n_dev, int32_t d,

@@ -187,6 +187,12 @@ cudaError_t launch_tracking_loss(const float *color, const float *depth, const f
                                  float lambda_d, float gate, float *d_color, float *d_depth,
                                  float *d_sil, float *loss3, void *ws, cudaStream_t s);
 
+size_t rvq_update_workspace_bytes(int L, int P, int d);
+cudaError_t launch_rvq_update(const float *x, int64_t n, const int64_t *n_dev, int d,
+                              const float *codes, int L, int P, const void *idx, int idx_bytes,
+                              float *codes_out, int32_t *counts_out, float *loss_out, void *ws,
+                              cudaStream_t s);
+
 size_t prune_workspace_bytes(int64_t n);
 cudaError_t launch_prune(const csplat_gaussians &in, const DecodeArgs *idx, float tau,
                          float reset, const csplat_gaussians_out &out, void *out_sidx,

@@ -331,6 +331,32 @@ def test_window_accumulate_matches_sum_of_views(env):
         assert torch.allclose(win.poses[k], poses[k], rtol=1e-4, atol=1e-4)
 
 
+# ------------------------------------------------------------------ NEXT-2 R-VQ update
+
+@pytest.mark.parametrize("attr,LP", [("log_scale", (4, 256)), ("quat", (4, 256)),
+                                     ("log_scale", (2, 16))])
+def test_rvq_update_parity(env, attr, LP):
+    """csplat_rvq_update (one k-means M-step, Eq 11) against the oracle: counts
+    exact, codes and losses within float32 accumulation tolerance; n_dev honoured."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.room_scene(60_000, synth.CAMERAS["scannet"], 4, codebook_LP=LP)
+    x = getattr(sc, attr)
+    codes = sc.codebook["scale_codes" if attr == "log_scale" else "rot_codes"]
+    m = 50_000                                   # only the first m vectors exist (n_dev)
+    idx_o, _ = orc.rvq_assign(x[:, :m], codes)
+    new_o, cnt_o, loss_o = orc.rvq_update(x[:, :m], codes, idx_o)
+    xt = torch.tensor(x, device=dev)
+    ct = torch.tensor(codes, device=dev)
+    n_dev = torch.tensor([m], dtype=torch.int64, device=dev)
+    idx, _ = cs.rvq_assign(xt, ct, n_dev=n_dev, want_recon=False)
+    assert np.array_equal(idx.cpu().numpy()[:, :m].astype(np.uint16), idx_o)
+    new, cnt, loss = cs.rvq_update(xt, ct, idx, n_dev=n_dev)
+    assert np.array_equal(cnt.cpu().numpy(), cnt_o)
+    scale = np.abs(codes).max()
+    assert np.abs(new.cpu().numpy() - new_o).max() <= 2e-5 * scale
+    assert np.allclose(loss.double().cpu().numpy(), loss_o, rtol=1e-4)
+
+
 # ------------------------------------------------------------------ NEXT-1 tracking
 
 def _observed(env, sc, view):

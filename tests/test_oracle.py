@@ -486,6 +486,53 @@ def test_rvq_special_cases(orc):
     assert (idx[0] == d.argmin(0)).all()
 
 
+# ---------------------------------------------------------------- R-VQ update (NEXT-2)
+
+def test_rvq_update_degenerate_and_centroids(orc):
+    """N identical vectors, L = 1 -> the assigned code becomes
+    that vector and a second round has zero loss; two separated clusters with
+    P = 2 -> codes = the cluster centroids, loss = within-cluster scatter."""
+    v = np.float32([[0.3], [-1.2], [2.0]])
+    x = np.repeat(v, 8, axis=1)
+    codes = np.random.default_rng(0).standard_normal((1, 8, 3)).astype(np.float32)
+    idx, _ = orc.rvq_assign(x, codes)
+    new, cnt, loss = orc.rvq_update(x, codes, idx)
+    assert cnt.sum() == 8 and np.array_equal(new[0, idx[0, 0]], v[:, 0])
+    assert loss[0] > 0
+    new2, _, loss2 = orc.rvq_update(x, new, orc.rvq_assign(x, new)[0])
+    assert loss2[0] == 0.0 and loss2[1] == 0.0
+    r = np.random.default_rng(1)
+    a = r.normal(0, 0.1, (3, 50)) + np.array([[5.0], [0], [0]])
+    b = r.normal(0, 0.1, (3, 70)) - np.array([[5.0], [0], [0]])
+    x = np.concatenate([a, b], 1).astype(np.float32)
+    codes = np.float32([[[4.0, 0, 0], [-4.0, 0, 0]]])
+    idx, _ = orc.rvq_assign(x, codes)
+    new, cnt, loss = orc.rvq_update(x, codes, idx)
+    assert list(cnt[0]) == [50, 70]
+    assert np.allclose(new[0, 0], a.astype(np.float32).mean(1), atol=1e-6)
+    assert np.allclose(new[0, 1], b.astype(np.float32).mean(1), atol=1e-6)
+    scatter = sum(((c.astype(np.float32).astype(np.float64) - cc[:, None]) ** 2).sum()
+                  for c, cc in ((a, codes[0, 0]), (b, codes[0, 1])))
+    assert abs(loss[0] - scatter) < 1e-6 * scatter
+    assert abs(loss[1] - scatter / (120 * 2)) < 1e-9
+
+
+def test_rvq_update_decreases_reconstruction_error(orc):
+    """Lloyd iterations (assign, update) never increase the stage-1 error, and
+    the stage losses of a trained cascade decrease across stages."""
+    sc = synth.room_scene(3000, synth.CAMERAS["tum"], 2, codebook_LP=(3, 32))
+    x, codes = sc.log_scale, sc.codebook["scale_codes"].copy()
+    prev = np.inf
+    for _ in range(6):
+        idx, _ = orc.rvq_assign(x, codes)
+        codes, _, loss = orc.rvq_update(x, codes, idx)
+        assert loss[0] <= prev * (1 + 1e-9)
+        prev = loss[0]
+    idx, _ = orc.rvq_assign(x, codes)
+    _, _, loss = orc.rvq_update(x, codes, idx)
+    assert loss[0] > loss[1] > loss[2]
+
+
 # ---------------------------------------------------------------- tracking loss (NEXT-1)
 
 def test_tracking_loss_worked_example(orc):
