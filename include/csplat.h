@@ -210,12 +210,36 @@ int csplat_rvq_update(const float *x, int64_t n, const int64_t *n_dev, int32_t d
                       float *codes_out, int32_t *counts_out, float *loss_out, void *ws,
                       size_t ws_bytes, void *stream);
 
+/* NEXT-3 (sliding-window mask schedule):
+ * csplat_mask_loss: the mask sparsity loss of Eq 8, L_m = (1/N_a)
+ * sum Sig(m_n) over the Gaussians in the current frustum, taken as those the
+ * projection kept (count[n] > 0, from csplat_project; reading R29):
+ * d_mask[n] += lambda Sig'(m_n) / N_a for them (accumulates into the render
+ * gradient), loss_dev (optional, device float[1]) = L_m.
+ * ws: csplat_workspace_bytes(CSPLAT_OP_MASK_LOSS, 0, 0, NULL). */
+int csplat_mask_loss(const csplat_gaussians *g, const int32_t *count, float lambda,
+                     float *d_mask, float *loss_dev, void *ws, size_t ws_bytes, void *stream);
+
+/* csplat_keyframe_overlap: "tallying points within the frustum of each
+ * keyframe": every valid pixel (depth > 0) of the current depth map
+ * [H][W] (device) is back-projected with the current world->camera view `cur`
+ * and counted for keyframe k (views: HOST array of K <= 256 views, same
+ * camera) when its depth in k lies in (near, far) and it projects inside
+ * [0, W-1] x [0, H-1]; float32 decision arithmetic (reading R29), so the
+ * counts are exact.  counts_dev: device int64[K].
+ * ws: csplat_workspace_bytes(CSPLAT_OP_KEYFRAME_OVERLAP, K, 0, NULL). */
+int csplat_keyframe_overlap(const float *depth, const csplat_camera *cam, const csplat_view *cur,
+                            const csplat_view *views, int32_t K, int64_t *counts_dev, void *ws,
+                            size_t ws_bytes, void *stream);
+
 enum csplat_op {
   CSPLAT_OP_BIN_TILES = 1,
   CSPLAT_OP_RENDER_BWD = 2,
   CSPLAT_OP_MASK_PRUNE = 3,
   CSPLAT_OP_TRACKING_LOSS = 4,
-  CSPLAT_OP_RVQ_UPDATE = 5  /* n = L * P codes, pairs = d */
+  CSPLAT_OP_RVQ_UPDATE = 5,  /* n = L * P codes, pairs = d */
+  CSPLAT_OP_MASK_LOSS = 6,
+  CSPLAT_OP_KEYFRAME_OVERLAP = 7  /* n = K */
 };
 
 /* Scratch bytes needed by `op` for n Gaussians / pair_capacity pairs. */

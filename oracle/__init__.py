@@ -302,6 +302,29 @@ def tracking_loss(color, depth, sil, obs_color, obs_depth, lambda_d=1.0, gate=0.
     return (dC, dD, dS), loss, flags
 
 
+def mask_loss(mask, active, lam=1.0):
+    """NEXT-3: Eq 8 over the active (in-frustum) Gaussians -> (L_m, d_mask)."""
+    mask = _f32(mask)
+    act = np.ascontiguousarray(active, dtype=np.uint8)
+    d = np.zeros(mask.shape[0])
+    lib().oracle_mask_loss.restype = C.c_double
+    L = lib().oracle_mask_loss(_p(mask), _p(act), C.c_int64(mask.shape[0]), C.c_double(lam),
+                               _p(d))
+    return L, d
+
+
+def keyframe_overlap(depth, cam: dict, cur_view, views):
+    """NEXT-3: points of the current depth map inside each keyframe's frustum."""
+    depth = _f32(depth)
+    K = len(views)
+    arr = (View * max(K, 1))(*[view(v) for v in views])
+    counts = np.zeros(max(K, 1), dtype=np.int64)
+    rc = lib().oracle_keyframe_overlap(_p(depth), C.byref(camera(cam)), C.byref(view(cur_view)),
+                                       arr, C.c_int32(K), _p(counts))
+    assert rc == 0
+    return counts[:K]
+
+
 def rvq_assign(x, codes):
     """a2: x [d, n] float32, codes [L, P, d] -> idx [L, n] u16, recon [d, n]."""
     x = _f32(x)

@@ -126,6 +126,13 @@ int oracle_mask_prune(int64_t n, const float *mask, float mask_eps,
                       int32_t n_idx_planes, const uint16_t *const *in_idx, uint16_t *const *out_idx,
                       int32_t mask_plane, float reset_mask, int32_t *keep_map, int64_t *n_kept);
 
+/* NEXT-3: Eq 8 mask loss restricted to the frustum (d_mask accumulated) and
+ * the keyframe-overlap counts of the sliding-window selection (reading R29). */
+double oracle_mask_loss(const float *mask, const uint8_t *active, int64_t n, double lambda,
+                        double *d_mask);
+int oracle_keyframe_overlap(const float *depth, const or_camera *cam, const or_view *cur,
+                            const or_view *views, int32_t K, int64_t *counts);
+
 /* NEXT-1 tracking loss (Eq 12 gated by Eq 14, reading R27): upstream
  * gradients dL/d(colour, depth, silhouette) and loss3 = (L_t, L_c, L_d). */
 int oracle_tracking_loss(const double *color, const double *depth, const double *sil,

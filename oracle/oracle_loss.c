@@ -16,6 +16,65 @@
  */
 #include "oracle_internal.h"
 
+/* NEXT-3 (a): the mask sparsity loss of Eq 8, L_m = (1/N) sum_n
+ * Sig(m_n), restricted to the Gaussians inside the current viewing frustum
+ * ("optimize only the mask within the current viewing frustum"; reading
+ * R29: frustum membership = the Gaussian's projection touches the image,
+ * i.e. tile count > 0 or the mask is off but the centre is in the frustum --
+ * here: active[n] != 0 supplied by the caller).  d_mask[n] += lambda Sig'(m)/N_a
+ * for active n (N_a = number of active); returns L_m. */
+double oracle_mask_loss(const float *mask, const uint8_t *active, int64_t n, double lambda,
+                        double *d_mask)
+{
+    int64_t na = 0;
+    for (int64_t i = 0; i < n; i++) na += active[i] != 0;
+    if (na == 0) return 0.0;
+    double s = 0.0;
+    for (int64_t i = 0; i < n; i++) {
+        if (!active[i]) continue;
+        const double sg = 1.0 / (1.0 + exp(-(double)mask[i]));
+        s += sg;
+        d_mask[i] += lambda * sg * (1.0 - sg) / (double)na;
+    }
+    return s / (double)na;
+}
+
+/* NEXT-3 (b): keyframe overlap ("tallying points within the frustum of
+ * each keyframe"): every valid depth pixel of the current frame is
+ * back-projected, X = V_cur^-1 (D K^-1 [px, py, 1]), and counted for keyframe
+ * k when V_k X has near < z < far and projects inside [0, W-1] x [0, H-1]
+ * (reading R29).  counts[k] = number of such points. */
+int oracle_keyframe_overlap(const float *depth, const or_camera *cam, const or_view *cur,
+                            const or_view *views, int32_t K, int64_t *counts)
+{
+    /* float32 decision arithmetic in the written order (the counts are integers
+     * compared bit-exactly with the GPU) */
+    const int W = cam->width, H = cam->height;
+    const float *C = cur->m;
+    const float Wm1 = (float)W - 1.0f, Hm1 = (float)H - 1.0f;
+    for (int k = 0; k < K; k++) counts[k] = 0;
+    for (int py = 0; py < H; py++)
+        for (int px = 0; px < W; px++) {
+            const float d = depth[(int64_t)py * W + px];
+            if (!(d > 0.0f)) continue;
+            const float xn = ((float)px - cam->cx) / cam->fx, yn = ((float)py - cam->cy) / cam->fy;
+            const float qx = xn * d - C[3], qy = yn * d - C[7], qz = d - C[11];
+            float X[3];  /* R^T (p_c - t) */
+            for (int a = 0; a < 3; a++) X[a] = (C[a] * qx + C[4 + a] * qy) + C[8 + a] * qz;
+            for (int k = 0; k < K; k++) {
+                const float *V = views[k].m;
+                const float xc = ((V[0] * X[0] + V[1] * X[1]) + V[2] * X[2]) + V[3];
+                const float yc = ((V[4] * X[0] + V[5] * X[1]) + V[6] * X[2]) + V[7];
+                const float zc = ((V[8] * X[0] + V[9] * X[1]) + V[10] * X[2]) + V[11];
+                if (!(zc > cam->near_z) || !(zc < cam->far_z)) continue;
+                const float iz = 1.0f / zc;
+                const float u = cam->fx * (xc * iz) + cam->cx, v = cam->fy * (yc * iz) + cam->cy;
+                if (u >= 0.0f && u <= Wm1 && v >= 0.0f && v <= Hm1) counts[k]++;
+            }
+        }
+    return 0;
+}
+
 int oracle_tracking_loss(const double *color, const double *depth, const double *sil,
                          const float *obs_color, const float *obs_depth, int32_t width,
                          int32_t height, double lambda_d, double gate, double *d_color,

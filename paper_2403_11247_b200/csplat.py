@@ -68,10 +68,13 @@ class Grads(C.Structure):
 
 EXPORTS = ["csplat_project", "csplat_bin_tiles", "csplat_render_fwd", "csplat_render_bwd",
            "csplat_rvq_assign", "csplat_mask_prune", "csplat_tracking_loss", "csplat_rvq_update",
+           "csplat_mask_loss", "csplat_keyframe_overlap",
            "csplat_workspace_bytes", "csplat_last_error", "csplat_status_string",
            "csplat_version"]
 OP_TRACKING_LOSS = 4
 OP_RVQ_UPDATE = 5
+OP_MASK_LOSS = 6
+OP_KEYFRAME_OVERLAP = 7
 
 _lib = None
 
@@ -95,6 +98,8 @@ def lib():
             [vp] * 5 + [C.c_size_t, vp]
         L.csplat_rvq_update.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp, vp, vp,
                                         C.c_size_t, vp]
+        L.csplat_mask_loss.argtypes = [vp, vp, C.c_float, vp, vp, vp, C.c_size_t, vp]
+        L.csplat_keyframe_overlap.argtypes = [vp, vp, vp, vp, i32, vp, vp, C.c_size_t, vp]
         L.csplat_workspace_bytes.argtypes = [C.c_int, i64, i64, vp]
         L.csplat_workspace_bytes.restype = C.c_size_t
         L.csplat_last_error.argtypes = [C.c_char_p, C.c_size_t]
@@ -325,6 +330,46 @@ def rvq_assign(x, codes, idx_bytes=None, n_dev=None, idx=None, recon=None, want_
     _check(lib().csplat_rvq_assign(_ptr(x), n, _ptr(n_dev), d, _ptr(codes), L, P, _ptr(idx),
                                    idx_bytes, _ptr(recon), _stream(stream)), "csplat_rvq_assign")
     return idx, recon
+
+
+def mask_loss(g: GaussianMap, count, d_mask, lam=1.0, loss=None, ws=None, stream=None):
+    """NEXT-3 (Eq 8 over the in-frustum Gaussians, count > 0): d_mask += lam Sig'(m)/N_a.
+    Returns the device loss [1]."""
+    dev = g.opacity.device
+    if loss is None:
+        loss = torch.zeros(1, device=dev)
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_MASK_LOSS, 0), dtype=torch.uint8, device=dev)
+    gs = g.struct()
+    _check(lib().csplat_mask_loss(C.byref(gs), _ptr(count), lam, _ptr(d_mask), _ptr(loss),
+                                  _ptr(ws), ws.numel(), _stream(stream)), "csplat_mask_loss")
+    return loss
+
+
+def keyframe_overlap(depth, cam: dict, cur_view, views, counts=None, ws=None, stream=None):
+    """NEXT-3: per keyframe, the number of valid current-depth points inside
+    its frustum (device int64 [K])."""
+    K = len(views)
+    dev = depth.device
+    if counts is None:
+        counts = torch.zeros(max(K, 1), dtype=torch.int64, device=dev)
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_KEYFRAME_OVERLAP, K), dtype=torch.uint8, device=dev)
+    arr = (View * max(K, 1))(*[view(v) for v in views])
+    _check(lib().csplat_keyframe_overlap(_ptr(depth), C.byref(camera(cam)), C.byref(view(cur_view)),
+                                         arr, K, _ptr(counts), _ptr(ws), ws.numel(),
+                                         _stream(stream)), "csplat_keyframe_overlap")
+    return counts[:K]
+
+
+def select_window(overlap_counts, n: int, recency=None):
+    """P:138 sliding window: the most relevant keyframe plus the n-2 next by
+    overlap (ties -> more recent first); returns keyframe indices (host)."""
+    import numpy as np
+    c = np.asarray(overlap_counts.cpu() if hasattr(overlap_counts, "cpu") else overlap_counts)
+    rec = np.arange(len(c)) if recency is None else np.asarray(recency)
+    order = sorted(range(len(c)), key=lambda k: (-int(c[k]), -int(rec[k])))
+    return [k for k in order if c[k] > 0][:max(0, n - 1)]
 
 
 def rvq_update(x, codes, idx, n_dev=None, codes_out=None, want_counts=True, ws=None,

@@ -147,6 +147,8 @@ size_t csplat_workspace_bytes(int op, int64_t n, int64_t pairs, const csplat_cam
     case CSPLAT_OP_RENDER_BWD: return csplat::bwd_workspace_bytes(n);
     case CSPLAT_OP_MASK_PRUNE: return csplat::prune_workspace_bytes(n);
     case CSPLAT_OP_TRACKING_LOSS: return 64;
+    case CSPLAT_OP_MASK_LOSS: return 64;
+    case CSPLAT_OP_KEYFRAME_OVERLAP: return (size_t)(n > 0 ? n : 1) * 48 + 64;
     case CSPLAT_OP_RVQ_UPDATE:  // n = L * P, pairs = d
       return (size_t)n * (size_t)pairs * 4 + (size_t)n * 4 + 17 * 4 + 256;  // L <= 16
     default: return 0;
@@ -283,6 +285,42 @@ int csplat_tracking_loss(const float *color, const float *depth, const float *si
                                                   d_depth, d_silhouette, loss3_dev, ws,
                                                   static_cast<cudaStream_t>(stream)),
                      "csplat_tracking_loss");
+}
+
+int csplat_mask_loss(const csplat_gaussians *g, const int32_t *count, float lambda,
+                     float *d_mask, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
+  if (!g || g->n < 0) return invalid("gaussians NULL / n < 0");
+  if (g->n > 0 && (!g->mask || !count || !d_mask)) return invalid("mask_loss: NULL argument");
+  if (!std::isfinite(lambda)) return invalid("lambda must be finite");
+  if (!ws || ws_bytes < 64) {
+    set_err("mask_loss workspace too small");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_mask_loss(g->n, g->n_dev, g->mask, count, lambda, d_mask,
+                                              loss_dev, ws, static_cast<cudaStream_t>(stream)),
+                     "csplat_mask_loss");
+}
+
+int csplat_keyframe_overlap(const float *depth, const csplat_camera *cam, const csplat_view *cur,
+                            const csplat_view *views, int32_t K, int64_t *counts_dev, void *ws,
+                            size_t ws_bytes, void *stream) {
+  RET_IF(check_camera(cam));
+  if (K < 0 || K > 256) return invalid("K must be 0..256");
+  if (!depth || !cur || (K > 0 && (!views || !counts_dev))) return invalid("overlap: NULL argument");
+  if (!ws || ws_bytes < (size_t)(K > 0 ? K : 1) * 48 + 64) {
+    set_err("keyframe_overlap workspace too small");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  if (K == 0) return CSPLAT_OK;
+  RET_IF(check_device());
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float *vd = static_cast<float *>(ws);
+  RET_IF(cuda_status(cudaMemcpyAsync(vd, views, (size_t)K * 48, cudaMemcpyHostToDevice, s),
+                     "keyframe_overlap views upload"));
+  return cuda_status(csplat::launch_overlap(depth, *cam, *cur, vd, K,
+                                            reinterpret_cast<unsigned long long *>(counts_dev), s),
+                     "csplat_keyframe_overlap");
 }
 
 int csplat_rvq_update(const float *x, int64_t n, const int64_t *n_dev, int32_t d,

@@ -187,6 +187,13 @@ cudaError_t launch_tracking_loss(const float *color, const float *depth, const f
                                  float lambda_d, float gate, float *d_color, float *d_depth,
                                  float *d_sil, float *loss3, void *ws, cudaStream_t s);
 
+cudaError_t launch_mask_loss(int64_t n, const int64_t *n_dev, const float *mask,
+                             const int32_t *count, float lambda, float *d_mask, float *loss,
+                             void *ws, cudaStream_t s);
+cudaError_t launch_overlap(const float *depth, const csplat_camera &cam, const csplat_view &cur,
+                           const float *views_dev, int K, unsigned long long *counts,
+                           cudaStream_t s);
+
 size_t rvq_update_workspace_bytes(int L, int P, int d);
 cudaError_t launch_rvq_update(const float *x, int64_t n, const int64_t *n_dev, int d,
                               const float *codes, int L, int P, const void *idx, int idx_bytes,

@@ -64,6 +64,133 @@ __global__ void __launch_bounds__(kLossThreads) k_tracking_loss(
   }
 }
 
+// ---------------------------------------------------------------- NEXT-3
+
+__global__ void __launch_bounds__(kLossThreads) k_count_active(int64_t n,
+                                                               const int64_t *__restrict__ n_dev,
+                                                               const int32_t *__restrict__ count,
+                                                               unsigned long long *__restrict__ na) {
+  const int64_t ne = eff_n(n, n_dev);
+  unsigned c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += count[i] > 0 ? 1u : 0u;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(na, (unsigned long long)c);
+}
+
+// Eq 8 over the in-frustum Gaussians: d_mask += lambda Sig'(m)/N_a.
+__global__ void __launch_bounds__(kLossThreads) k_mask_loss(
+    int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mask,
+    const int32_t *__restrict__ count, float lambda, const unsigned long long *__restrict__ na,
+    float *__restrict__ d_mask, float *__restrict__ loss) {
+  __shared__ float red[kLossThreads / 32];
+  const int64_t ne = eff_n(n, n_dev);
+  const unsigned long long a = *na;
+  const float inv = a ? 1.0f / (float)a : 0.0f;
+  float s = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (count[i] <= 0) continue;
+    const float sg = 1.0f / (1.0f + __expf(-mask[i]));
+    s += sg;
+    d_mask[i] += lambda * sg * (1.0f - sg) * inv;
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0 && loss) {
+    float t = 0.f;
+    for (int w = 0; w < kLossThreads / 32; w++) t += red[w];
+    atomicAdd(loss, t * inv);
+  }
+}
+
+constexpr int kMaxOverlapViews = 256;
+
+struct OverlapConst {
+  float C[12];
+  float fx, fy, cx, cy, near_z, far_z, Wm1, Hm1;
+  int W, H, K;
+};
+
+// P:138 keyframe overlap, float32 decision arithmetic (bit-exact counts).
+__global__ void __launch_bounds__(kLossThreads) k_overlap(const float *__restrict__ depth,
+                                                          OverlapConst oc,
+                                                          const float *__restrict__ views,
+                                                          unsigned long long *__restrict__ counts) {
+  __shared__ float sv[kMaxOverlapViews * 12];
+  __shared__ unsigned sc[kMaxOverlapViews];
+  for (int t = threadIdx.x; t < oc.K * 12; t += blockDim.x) sv[t] = views[t];
+  for (int t = threadIdx.x; t < oc.K; t += blockDim.x) sc[t] = 0;
+  __syncthreads();
+  const int64_t HW = (int64_t)oc.W * oc.H;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const float d = depth[p];
+    if (!(d > 0.0f)) continue;
+    const int px = (int)(p % oc.W), py = (int)(p / oc.W);
+    const float xn = DDIV(DSUB((float)px, oc.cx), oc.fx), yn = DDIV(DSUB((float)py, oc.cy), oc.fy);
+    const float qx = DSUB(DMUL(xn, d), oc.C[3]), qy = DSUB(DMUL(yn, d), oc.C[7]);
+    const float qz = DSUB(d, oc.C[11]);
+    float X[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+      X[a] = DADD(DADD(DMUL(oc.C[a], qx), DMUL(oc.C[4 + a], qy)), DMUL(oc.C[8 + a], qz));
+    for (int k = 0; k < oc.K; k++) {
+      const float *V = sv + 12 * k;
+      const float xc = DADD(DADD(DADD(DMUL(V[0], X[0]), DMUL(V[1], X[1])), DMUL(V[2], X[2])), V[3]);
+      const float yc = DADD(DADD(DADD(DMUL(V[4], X[0]), DMUL(V[5], X[1])), DMUL(V[6], X[2])), V[7]);
+      const float zc = DADD(DADD(DADD(DMUL(V[8], X[0]), DMUL(V[9], X[1])), DMUL(V[10], X[2])), V[11]);
+      if (!(zc > oc.near_z) || !(zc < oc.far_z)) continue;
+      const float iz = DDIV(1.0f, zc);
+      const float u = DADD(DMUL(oc.fx, DMUL(xc, iz)), oc.cx);
+      const float v = DADD(DMUL(oc.fy, DMUL(yc, iz)), oc.cy);
+      if (u >= 0.0f && u <= oc.Wm1 && v >= 0.0f && v <= oc.Hm1) atomicAdd(sc + k, 1u);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < oc.K; t += blockDim.x)
+    if (sc[t]) atomicAdd(counts + t, (unsigned long long)sc[t]);
+}
+
+cudaError_t launch_mask_loss(int64_t n, const int64_t *n_dev, const float *mask,
+                             const int32_t *count, float lambda, float *d_mask, float *loss,
+                             void *ws, cudaStream_t s) {
+  unsigned long long *na = static_cast<unsigned long long *>(ws);
+  cudaError_t e = cudaMemsetAsync(na, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  if (loss) {
+    e = cudaMemsetAsync(loss, 0, sizeof(float), s);
+    if (e != cudaSuccess) return e;
+  }
+  if (n == 0) return cudaSuccess;
+  int64_t blocks = (n + kLossThreads - 1) / kLossThreads;
+  if (blocks > 1184) blocks = 1184;
+  k_count_active<<<(unsigned)blocks, kLossThreads, 0, s>>>(n, n_dev, count, na);
+  k_mask_loss<<<(unsigned)blocks, kLossThreads, 0, s>>>(n, n_dev, mask, count, lambda, na, d_mask,
+                                                        loss);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_overlap(const float *depth, const csplat_camera &cam, const csplat_view &cur,
+                           const float *views_dev, int K, unsigned long long *counts,
+                           cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)K * sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  OverlapConst oc;
+  for (int i = 0; i < 12; i++) oc.C[i] = cur.m[i];
+  oc.fx = cam.fx; oc.fy = cam.fy; oc.cx = cam.cx; oc.cy = cam.cy;
+  oc.near_z = cam.near_z; oc.far_z = cam.far_z;
+  oc.Wm1 = (float)cam.width - 1.0f; oc.Hm1 = (float)cam.height - 1.0f;
+  oc.W = cam.width; oc.H = cam.height; oc.K = K;
+  const int64_t HW = (int64_t)cam.width * cam.height;
+  int64_t blocks = (HW + kLossThreads - 1) / kLossThreads;
+  if (blocks > 1184) blocks = 1184;
+  k_overlap<<<(unsigned)blocks, kLossThreads, 0, s>>>(depth, oc, views_dev, counts);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tracking_loss(const float *color, const float *depth, const float *sil,
                                  const float *obs_color, const float *obs_depth, int W, int H,
                                  float lambda_d, float gate, float *d_color, float *d_depth,

@@ -331,6 +331,36 @@ def test_window_accumulate_matches_sum_of_views(env):
         assert torch.allclose(win.poses[k], poses[k], rtol=1e-4, atol=1e-4)
 
 
+# ------------------------------------------------------------------ NEXT-3 window mask schedule
+
+def test_mask_loss_parity(env):
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.mid_scene(10)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec, cnt = cs.project(g, sc.cam, sc.views[0])
+    d_mask = torch.full((g.n,), 0.5, device=dev)     # accumulates into an existing gradient
+    loss = cs.mask_loss(g, cnt, d_mask, lam=3.0)
+    L, d = orc.mask_loss(sc.mask, (cnt.cpu().numpy() > 0), lam=3.0)
+    assert abs(float(loss.item()) - L) < 1e-5 * max(1.0, L)
+    assert np.allclose(d_mask.double().cpu().numpy(), d + 0.5, rtol=1e-5, atol=1e-9)
+
+
+def test_keyframe_overlap_parity(env):
+    """Bit-exact overlap counts for the 64 C5 keyframes from keyframe 5's depth."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.window_scene(0, n=200_000, n_keyframes=64)
+    cur = sc.views[5]
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec, cnt = cs.project(g, sc.cam, cur)
+    b = cs.bin_tiles(rec, cnt, sc.cam, capacity=int(cnt.sum().item()) + 64)
+    depth = cs.render_fwd(b["pair_rec"], b["tile_range"], sc.cam)["depth"]
+    counts = cs.keyframe_overlap(depth, sc.cam, cur, sc.views)
+    ref = orc.keyframe_overlap(depth.cpu().numpy(), sc.cam, cur, sc.views)
+    assert np.array_equal(counts.cpu().numpy(), ref)
+    win = cs.select_window(counts, 5)
+    assert win[0] == 5 and len(win) == 4     # the current keyframe overlaps itself most
+
+
 # ------------------------------------------------------------------ NEXT-2 R-VQ update
 
 @pytest.mark.parametrize("attr,LP", [("log_scale", (4, 256)), ("quat", (4, 256)),

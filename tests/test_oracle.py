@@ -533,6 +533,37 @@ def test_rvq_update_decreases_reconstruction_error(orc):
     assert loss[0] > loss[1] > loss[2]
 
 
+# ---------------------------------------------------------------- window mask schedule (NEXT-3)
+
+def test_mask_loss_worked_examples(orc):
+    """SPEC S:219-221 (Eq 8): all m = 0 -> 0.5; m -> -inf -> 0; {0, 20} -> 0.75;
+    the gradient is Sig'(m)/N_a and only in-frustum Gaussians count."""
+    L, d = orc.mask_loss(np.zeros(6), np.ones(6))
+    assert abs(L - 0.5) < 1e-12 and np.allclose(d, 0.25 / 6)
+    L, _ = orc.mask_loss(np.full(3, -80.0), np.ones(3))
+    assert L < 1e-30
+    L, _ = orc.mask_loss(np.float32([0, 20]), np.ones(2))
+    assert abs(L - 0.75) < 1e-8
+    L, d = orc.mask_loss(np.float32([0, 20, -3]), np.uint8([1, 1, 0]), lam=2.0)
+    assert abs(L - 0.75) < 1e-8 and d[2] == 0.0 and abs(d[0] - 2 * 0.25 / 2) < 1e-12
+
+
+def test_keyframe_overlap_worked_examples(orc):
+    """candidate = current pose -> (almost) all points; facing the
+    opposite way -> 0; translated by half the scene -> strictly between."""
+    cam = dict(fx=60.0, fy=60.0, cx=39.5, cy=29.5, width=80, height=60, near=0.01, far=100.0)
+    depth = np.random.default_rng(0).uniform(2, 4, (60, 80)).astype(np.float32)
+    depth[::5] = 0.0                                  # invalid rows are not counted
+    valid = int((depth > 0).sum())
+    I = synth.IDENTITY_VIEW
+    back = synth.look_view((0, 0, 0), -np.pi / 2)      # looking along -z
+    shifted = I.copy(); shifted[0, 3] = -1.5           # camera moved +1.5 m in x
+    counts = orc.keyframe_overlap(depth, cam, I, [I, back, shifted])
+    assert counts[0] >= 0.99 * valid and counts[0] <= valid
+    assert counts[1] == 0
+    assert 0 < counts[2] < counts[0]
+
+
 # ---------------------------------------------------------------- tracking loss (NEXT-1)
 
 def test_tracking_loss_worked_example(orc):
