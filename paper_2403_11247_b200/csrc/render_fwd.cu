@@ -19,7 +19,6 @@ namespace csplat {
 
 constexpr int kBatch = 32;   // records per TMA batch (2 KB)
 constexpr int kStages = 4;   // ring depth
-constexpr int kFwdThreads = 128;
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -72,7 +71,10 @@ __device__ __forceinline__ void composite_pred(PixState &p, bool h, float q, flo
   p.done |= (h & stop) ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(kFwdThreads) k_render_fwd(
+// PPT = pixels per thread (a column of PPT vertically adjacent pixels): a warp
+// owns an 8 x (4 PPT) block, a CTA of 256/PPT threads one 16x16 tile.
+template <int PPT>
+__global__ void __launch_bounds__(256 / PPT) k_render_fwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, float tmin, float *__restrict__ color, float *__restrict__ depth,
     float *__restrict__ sil, float *__restrict__ t_final, int32_t *__restrict__ n_contrib) {
@@ -81,11 +83,12 @@ __global__ void __launch_bounds__(kFwdThreads) k_render_fwd(
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * 8;
-  const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * 2, py1 = py0 + 1;
+  constexpr int kBH = 4 * PPT;  // warp block height
+  const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * kBH;
+  const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * PPT;
   // warp block corners as u16x2 for the SWAR rectangle test
   const uint32_t wlo = (uint32_t)wx0 | ((uint32_t)wy0 << 16);
-  const uint32_t whi_x = ((uint32_t)(wx0 + 7) | ((uint32_t)(wy0 + 7) << 16)) | 0x80008000u;
+  const uint32_t whi_x = ((uint32_t)(wx0 + 7) | ((uint32_t)(wy0 + kBH - 1) << 16)) | 0x80008000u;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
   const int len = (int)(end - start);
   const int nb = (len + kBatch - 1) / kBatch;
@@ -107,12 +110,17 @@ __global__ void __launch_bounds__(kFwdThreads) k_render_fwd(
   if (tid == 0)
     for (; issued < min(kStages - 1, nb); issued++) issue(issued);
 
-  PixState p0{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, (px < W && py0 < H) ? 0 : 1};
-  PixState p1{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, (px < W && py1 < H) ? 0 : 1};
-  const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
+  PixState p[PPT];
+  int alldone = 1;
+#pragma unroll
+  for (int k = 0; k < PPT; k++) {
+    p[k] = PixState{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, (px < W && py0 + k < H) ? 0 : 1};
+    alldone &= p[k].done;
+  }
+  const float fpx = (float)px;
   int b = 0;
   for (; b < nb; b++) {
-    if (__syncthreads_and(p0.done & p1.done)) break;
+    if (__syncthreads_and(alldone)) break;
     if (tid == 0 && issued < nb && issued <= b + kStages - 1) issue(issued++);
     mbar_wait(&full[b % kStages], (uint32_t)(b / kStages) & 1u);
     const float4 *rb = buf[b % kStages];
@@ -120,7 +128,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_render_fwd(
 #pragma unroll 2
     for (int e = 0; e < cnt; e++) {
       const float4 r3 = rb[e * 4 + 3];
-      // warp-level cull: record rectangle [lo, hi] vs the warp's 8x8 block
+      // warp-level cull: record rectangle [lo, hi] vs the warp's block
       const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
       const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
       if ((t1 & t2 & 0x80008000u) != 0x80008000u) continue;
@@ -128,36 +136,45 @@ __global__ void __launch_bounds__(kFwdThreads) k_render_fwd(
       const float4 r1 = rb[e * 4 + 1];  // cc, o_hat, k2, z
       const float dx = DSUB(fpx, r0.x);
       const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
-      const float dy0 = DSUB(fpy0, r0.y), dy1 = DSUB(fpy1, r0.y);
-      const float q0 = DFMA(cadx, dx, DFMA(cbdx, dy0, DMUL(DMUL(r1.x, dy0), dy0)));
-      const float q1 = DFMA(cadx, dx, DFMA(cbdx, dy1, DMUL(DMUL(r1.x, dy1), dy1)));
-      const bool h0 = (p0.done == 0) & (q0 >= 0.0f) & (q0 <= r1.z);  // R2 (DA)
-      const bool h1 = (p1.done == 0) & (q1 >= 0.0f) & (q1 <= r1.z);
-      if (!(h0 | h1)) continue;
+      float q[PPT];
+      bool h[PPT];
+      bool anyh = false;
+#pragma unroll
+      for (int k = 0; k < PPT; k++) {
+        const float dy = DSUB((float)(py0 + k), r0.y);
+        q[k] = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
+        h[k] = (p[k].done == 0) & (q[k] >= 0.0f) & (q[k] <= r1.z);  // R2 (DA)
+        anyh |= h[k];
+      }
+      if (!anyh) continue;
       const float4 r2 = rb[e * 4 + 2];  // r, g, b, gid
       const int idx = b * kBatch + e + 1;
-      // both pixels as straight-line (predicated) code so their chains interleave
-      composite_pred(p0, h0, q0, r1.y, r1.w, r2, amax, tmin, idx);
-      composite_pred(p1, h1, q1, r1.y, r1.w, r2, amax, tmin, idx);
+      // the pixels as straight-line (predicated) code so their chains interleave
+#pragma unroll
+      for (int k = 0; k < PPT; k++) composite_pred(p[k], h[k], q[k], r1.y, r1.w, r2, amax, tmin, idx);
     }
+    alldone = 1;
+#pragma unroll
+    for (int k = 0; k < PPT; k++) alldone &= p[k].done;
   }
   // never leave the CTA with bulk copies in flight into its shared memory
   if (tid == 0)
     for (int bb = b; bb < issued; bb++) mbar_wait(&full[bb % kStages], (uint32_t)(bb / kStages) & 1u);
   const int64_t HW = (int64_t)W * H;
   if (px < W) {
-    if (py0 < H) {
-      const int64_t p = (int64_t)py0 * W + px;
-      color[p] = p0.r; color[HW + p] = p0.g; color[2 * HW + p] = p0.b;
-      depth[p] = p0.D; sil[p] = p0.S; t_final[p] = p0.T; n_contrib[p] = p0.last;
-    }
-    if (py1 < H) {
-      const int64_t p = (int64_t)py1 * W + px;
-      color[p] = p1.r; color[HW + p] = p1.g; color[2 * HW + p] = p1.b;
-      depth[p] = p1.D; sil[p] = p1.S; t_final[p] = p1.T; n_contrib[p] = p1.last;
+#pragma unroll
+    for (int k = 0; k < PPT; k++) {
+      if (py0 + k >= H) continue;
+      const int64_t o = (int64_t)(py0 + k) * W + px;
+      color[o] = p[k].r; color[HW + o] = p[k].g; color[2 * HW + o] = p[k].b;
+      depth[o] = p[k].D; sil[o] = p[k].S; t_final[o] = p[k].T; n_contrib[o] = p[k].last;
     }
   }
 }
+
+#ifndef CSPLAT_FWD_PPT
+#define CSPLAT_FWD_PPT 2
+#endif
 
 cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
@@ -165,9 +182,10 @@ cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               cudaStream_t s) {
   const CamInfo ci = cam_info(cam);
   const int T = ci.tiles_x * ci.tiles_y;
-  k_render_fwd<<<T, kFwdThreads, 0, s>>>(static_cast<const float4 *>(pair_rec), tile_range, ci.W,
-                                         ci.H, ci.tiles_x, prm.alpha_max, prm.t_min, color, depth,
-                                         sil, t_final, n_contrib);
+  constexpr int PPT = CSPLAT_FWD_PPT;
+  k_render_fwd<PPT><<<T, 256 / PPT, 0, s>>>(static_cast<const float4 *>(pair_rec), tile_range,
+                                            ci.W, ci.H, ci.tiles_x, prm.alpha_max, prm.t_min,
+                                            color, depth, sil, t_final, n_contrib);
   return cudaGetLastError();
 }
 
