@@ -132,8 +132,14 @@ __global__ void __launch_bounds__(kRvqThreads) k_rvq_chunked(
 #pragma unroll
         for (int j = 0; j < D; j++) {
           const float cf = cv[c * D + j];
+#ifdef CSPLAT_RVQ_SCALAR
+          // scalar FADD/FFMA on the two halves (same IEEE RN results as the packed ops)
+          const float ea = DSUB(cf, lo2(r[j])), eb = DSUB(cf, hi2(r[j]));
+          acc[c] = pk2(DFMA(ea, ea, lo2(acc[c])), DFMA(eb, eb, hi2(acc[c])));
+#else
           const f2_t e = sub2(pk2(cf, cf), r[j]);
           acc[c] = fma2(e, e, acc[c]);
+#endif
         }
       }
     };

@@ -12,6 +12,8 @@ the device (n_dev), so the step has no host synchronisation.
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import csplat as cs
@@ -68,6 +70,7 @@ class RenderStep:
         self.upstream = None
         self.graph = None
         self.side = torch.cuda.Stream(device=self.dev)
+        self.single_stream = os.environ.get("CSPLAT_SINGLE_STREAM", "0") == "1"
 
     def _alloc_pairs(self, cap):
         self.capacity = cap
@@ -110,6 +113,12 @@ class RenderStep:
             # the scale and rotation assignments are independent: run them
             # concurrently (fork/join on a side stream; preserved by graph capture)
             main = torch.cuda.current_stream(self.dev)
+            if self.single_stream:  # profilers serialise kernels: keep one stream
+                cs.rvq_assign(g.log_scale, self.cb.scale_codes, n_dev=self.n_kept,
+                              idx=self.cb.scale_idx, want_recon=False, stream=main)
+                cs.rvq_assign(g.quat, self.cb.rot_codes, n_dev=self.n_kept,
+                              idx=self.cb.rot_idx, want_recon=False, stream=main)
+                return
             self.side.wait_stream(main)
             cs.rvq_assign(g.log_scale, self.cb.scale_codes, n_dev=self.n_kept,
                           idx=self.cb.scale_idx, want_recon=False, stream=main)
