@@ -197,6 +197,49 @@ def bench_tracking(dev, flush, iters=40, frames=3):
             "note": "includes one 36-byte device->host read per iteration for the host pose step"}
 
 
+def bench_next_rows(step, sc, view, dev, flush, reps=20):
+    """Device times of the NEXT-2/3 kernels on the C2 map (CUDA events, cold L2):
+    R-VQ codebook update of both attributes over the survivors, the Eq 8 mask
+    loss, and keyframe overlap of a 1200x680 depth map against 64 keyframes."""
+    import torch
+    from paper_2403_11247_b200 import csplat as cs
+    from scenes import synth
+    stream = torch.cuda.current_stream(dev)
+    step.prepare()
+    step.project_bin(view)
+    step.forward()
+    g = step.pruned
+    d_mask = torch.zeros(step.n, device=dev)
+    win = synth.window_scene(0, n=1000, n_keyframes=64)
+    depth = step.img["depth"]
+    jobs = {
+        "rvq_update_scale_rot": lambda: (cs.rvq_update(g.log_scale, step.cb.scale_codes,
+                                                       step.cb.scale_idx, n_dev=step.n_kept),
+                                         cs.rvq_update(g.quat, step.cb.rot_codes,
+                                                       step.cb.rot_idx, n_dev=step.n_kept)),
+        "mask_loss": lambda: cs.mask_loss(g, step.count, d_mask),
+        "keyframe_overlap_64": lambda: cs.keyframe_overlap(depth, sc.cam, view, win.views),
+    }
+    out = {}
+    for name, fn in jobs.items():
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+        out[name + "_us"] = statistics.median(ts)
+    n_kept = int(step.n_kept.item())
+    L = step.cb.scale_codes.shape[0]
+    out["rvq_update_hbm_gbs"] = n_kept * (4 * 7 + 2 * L) / (out["rvq_update_scale_rot_us"] * 1e-6) / 1e9
+    out["keyframe_overlap_points"] = int((depth > 0).sum().item())
+    return out
+
+
 # ---------------------------------------------------------------- oracle (CPU) legs
 
 def oracle_step(sc, view, upstream, row_frac=1.0, rvq_frac=1.0):
@@ -453,6 +496,9 @@ def main():
     tracking = None
     if rank == 0 and not args.no_tracking:
         tracking = bench_tracking(dev, flush)
+    next_rows = None
+    if rank == 0 and not args.no_tracking:
+        next_rows = bench_next_rows(step, sc, view, dev, flush)
 
     if rank == 0:
         n_kept = int(step.n_kept.item())
@@ -536,6 +582,8 @@ def main():
                                                      peaks, step)
         if tracking:
             line["tracking_c3"] = tracking
+        if next_rows:
+            line["next_rows"] = next_rows
         if roof:
             line["roofline"] = roof
         if cpu:

@@ -67,9 +67,11 @@ int oracle_keyframe_overlap(const float *depth, const or_camera *cam, const or_v
                 const float yc = ((V[4] * X[0] + V[5] * X[1]) + V[6] * X[2]) + V[7];
                 const float zc = ((V[8] * X[0] + V[9] * X[1]) + V[10] * X[2]) + V[11];
                 if (!(zc > cam->near_z) || !(zc < cam->far_z)) continue;
-                const float iz = 1.0f / zc;
-                const float u = cam->fx * (xc * iz) + cam->cx, v = cam->fy * (yc * iz) + cam->cy;
-                if (u >= 0.0f && u <= Wm1 && v >= 0.0f && v <= Hm1) counts[k]++;
+                /* 0 <= fx xc/zc + cx <= W-1, multiplied through by zc > 0 */
+                const float ax = cam->fx * xc, ay = cam->fy * yc;
+                if (ax >= (-cam->cx) * zc && ax <= (Wm1 - cam->cx) * zc &&
+                    ay >= (-cam->cy) * zc && ay <= (Hm1 - cam->cy) * zc)
+                    counts[k]++;
             }
         }
     return 0;

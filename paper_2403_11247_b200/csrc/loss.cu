@@ -110,7 +110,7 @@ constexpr int kMaxOverlapViews = 256;
 
 struct OverlapConst {
   float C[12];
-  float fx, fy, cx, cy, near_z, far_z, Wm1, Hm1;
+  float fx, fy, cx, cy, near_z, far_z, Wm1, Hm1, wcx, hcy;  // wcx = (W-1) - cx, hcy alike
   int W, H, K;
 };
 
@@ -119,16 +119,19 @@ __global__ void __launch_bounds__(kLossThreads) k_overlap(const float *__restric
                                                           OverlapConst oc,
                                                           const float *__restrict__ views,
                                                           unsigned long long *__restrict__ counts) {
-  __shared__ float sv[kMaxOverlapViews * 12];
+  __shared__ __align__(16) float sv[kMaxOverlapViews * 12];
   __shared__ unsigned sc[kMaxOverlapViews];
   for (int t = threadIdx.x; t < oc.K * 12; t += blockDim.x) sv[t] = views[t];
   for (int t = threadIdx.x; t < oc.K; t += blockDim.x) sc[t] = 0;
   __syncthreads();
   const int64_t HW = (int64_t)oc.W * oc.H;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const float d = depth[p];
-    if (!(d > 0.0f)) continue;
+  const int lane = threadIdx.x & 31;
+  // uniform trip count, so each (point, keyframe) test is warp-aggregated by a ballot
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < HW;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = base + threadIdx.x;
+    const float d = p < HW ? depth[p] : 0.0f;
+    const bool valid = d > 0.0f;
     const int px = (int)(p % oc.W), py = (int)(p / oc.W);
     const float xn = DDIV(DSUB((float)px, oc.cx), oc.fx), yn = DDIV(DSUB((float)py, oc.cy), oc.fy);
     const float qx = DSUB(DMUL(xn, d), oc.C[3]), qy = DSUB(DMUL(yn, d), oc.C[7]);
@@ -137,16 +140,27 @@ __global__ void __launch_bounds__(kLossThreads) k_overlap(const float *__restric
 #pragma unroll
     for (int a = 0; a < 3; a++)
       X[a] = DADD(DADD(DMUL(oc.C[a], qx), DMUL(oc.C[4 + a], qy)), DMUL(oc.C[8 + a], qz));
-    for (int k = 0; k < oc.K; k++) {
-      const float *V = sv + 12 * k;
-      const float xc = DADD(DADD(DADD(DMUL(V[0], X[0]), DMUL(V[1], X[1])), DMUL(V[2], X[2])), V[3]);
-      const float yc = DADD(DADD(DADD(DMUL(V[4], X[0]), DMUL(V[5], X[1])), DMUL(V[6], X[2])), V[7]);
-      const float zc = DADD(DADD(DADD(DMUL(V[8], X[0]), DMUL(V[9], X[1])), DMUL(V[10], X[2])), V[11]);
-      if (!(zc > oc.near_z) || !(zc < oc.far_z)) continue;
-      const float iz = DDIV(1.0f, zc);
-      const float u = DADD(DMUL(oc.fx, DMUL(xc, iz)), oc.cx);
-      const float v = DADD(DMUL(oc.fy, DMUL(yc, iz)), oc.cy);
-      if (u >= 0.0f && u <= oc.Wm1 && v >= 0.0f && v <= oc.Hm1) atomicAdd(sc + k, 1u);
+    if (!__any_sync(0xffffffffu, valid)) continue;
+    // keyframes in chunks of 32: lane j keeps the warp's count for keyframe kb + j
+    // in a register, one shared atomic per (warp, 32 keyframes)
+    for (int kb = 0; kb < oc.K; kb += 32) {
+      const int kn = min(32, oc.K - kb);
+      unsigned cnt = 0;
+      for (int j = 0; j < kn; j++) {
+        const float4 *V = reinterpret_cast<const float4 *>(sv + 12 * (kb + j));
+        const float4 r0 = V[0], r1 = V[1], r2 = V[2];
+        const float xc = DADD(DADD(DADD(DMUL(r0.x, X[0]), DMUL(r0.y, X[1])), DMUL(r0.z, X[2])), r0.w);
+        const float yc = DADD(DADD(DADD(DMUL(r1.x, X[0]), DMUL(r1.y, X[1])), DMUL(r1.z, X[2])), r1.w);
+        const float zc = DADD(DADD(DADD(DMUL(r2.x, X[0]), DMUL(r2.y, X[1])), DMUL(r2.z, X[2])), r2.w);
+        // 0 <= fx xc/zc + cx <= W-1 multiplied through by zc > 0 (no division)
+        const float ax = DMUL(oc.fx, xc), ay = DMUL(oc.fy, yc);
+        const bool in = valid && (zc > oc.near_z) && (zc < oc.far_z) &&
+                        ax >= DMUL(-oc.cx, zc) && ax <= DMUL(oc.wcx, zc) &&
+                        ay >= DMUL(-oc.cy, zc) && ay <= DMUL(oc.hcy, zc);
+        const unsigned m = __ballot_sync(0xffffffffu, in);
+        if (lane == j) cnt += (unsigned)__popc(m);
+      }
+      if (lane < kn && cnt) atomicAdd(sc + kb + lane, cnt);
     }
   }
   __syncthreads();
@@ -184,6 +198,9 @@ cudaError_t launch_overlap(const float *depth, const csplat_camera &cam, const c
   oc.near_z = cam.near_z; oc.far_z = cam.far_z;
   oc.Wm1 = (float)cam.width - 1.0f; oc.Hm1 = (float)cam.height - 1.0f;
   oc.W = cam.width; oc.H = cam.height; oc.K = K;
+  volatile float wm1 = oc.Wm1, hm1 = oc.Hm1;  // one IEEE subtraction each, as in the oracle
+  oc.wcx = wm1 - cam.cx;
+  oc.hcy = hm1 - cam.cy;
   const int64_t HW = (int64_t)cam.width * cam.height;
   int64_t blocks = (HW + kLossThreads - 1) / kLossThreads;
   if (blocks > 1184) blocks = 1184;
