@@ -123,7 +123,11 @@ int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const c
  * Outputs, for n_pairs = sum(count) pairs:
  *   pair_gid[pair_capacity]   Gaussian index per pair, ordered by (tile, bits(z_c), index)
  *   pair_rec[pair_capacity]   the 64-byte record of each pair, same order (the
- *                             contiguous payload the renderer streams with TMA)
+ *                             contiguous payload the renderer streams with TMA);
+ *                             word 14 (0 in rec) carries the pair's cull mask:
+ *                             bit w set unless alpha < 1/255 provably holds over
+ *                             the whole 8x8 pixel block w (x half w&1, y half w>>1)
+ *                             of the pair's tile
  *   tile_range[T][2]          [start, end) of every tile, T = ceil(W/16)*ceil(H/16)
  *   n_pairs_dev               device int64: the total (may exceed the capacity)
  * Pairs beyond pair_capacity are dropped (ranges clamped); with CSPLAT_SYNC the

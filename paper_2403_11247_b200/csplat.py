@@ -348,18 +348,24 @@ def mask_loss(g: GaussianMap, count, d_mask, lam=1.0, loss=None, ws=None, stream
 
 def keyframe_overlap(depth, cam: dict, cur_view, views, counts=None, ws=None, stream=None):
     """NEXT-3: per keyframe, the number of valid current-depth points inside
-    its frustum (device int64 [K])."""
+    its frustum (device int64 [K]).  views: a list of 4x4/3x4 views, or the
+    ctypes array view_array() returns (marshalled once, reused per frame)."""
     K = len(views)
     dev = depth.device
     if counts is None:
         counts = torch.zeros(max(K, 1), dtype=torch.int64, device=dev)
     if ws is None:
         ws = torch.empty(workspace_bytes(OP_KEYFRAME_OVERLAP, K), dtype=torch.uint8, device=dev)
-    arr = (View * max(K, 1))(*[view(v) for v in views])
+    arr = views if isinstance(views, C.Array) else view_array(views)
     _check(lib().csplat_keyframe_overlap(_ptr(depth), C.byref(camera(cam)), C.byref(view(cur_view)),
                                          arr, K, _ptr(counts), _ptr(ws), ws.numel(),
                                          _stream(stream)), "csplat_keyframe_overlap")
     return counts[:K]
+
+
+def view_array(views):
+    """Marshal a list of views into the csplat_view[K] array keyframe_overlap takes."""
+    return (View * max(len(views), 1))(*[view(v) for v in views])
 
 
 def select_window(overlap_counts, n: int, recency=None):

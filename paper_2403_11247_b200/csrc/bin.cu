@@ -13,7 +13,8 @@
 //   4. sort:    one warp per tile sorts its bucket in shared memory (bitonic
 //               network, all-ascending form, so no padding is needed), then
 //               writes pair_gid and the pair-ordered 64-byte record payload
-//               that the renderer streams with TMA bulk copies.  Buckets longer
+//               that the renderer streams with TMA bulk copies (word 14 of the
+//               payload: the pair's 8x8-block cull mask, block_mask below).  Buckets longer
 //               than a warp's shared-memory slice go to a CTA-wide pass.
 // Keys are unique (the index is in the low word), so the order is unique and
 // bit-exact: (tile, bits(z_c), index) ascending.
@@ -211,16 +212,67 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long *a, int len, int
   }
 }
 
+// Cull hint for the renderers: bit w (w = 0..3, x half = w & 1, y half = w >> 1)
+// of the pair payload's word 14 is set unless the Gaussian provably has
+// alpha < 1/255 over the whole 8x8 pixel block w of the tile, i.e. unless the
+// minimum of q(dx, dy) = ca dx^2 + (2cb) dx dy + cc dy^2 over the block's
+// rectangle exceeds k^2 by more than a rounding margin (the renderers skip a
+// pixel when q > k^2).  The minimum of the convex q over a box
+// that does not contain the centre lies on a box edge that faces the centre,
+// so at most two 1-D clamped minimisations per block.  The margin covers the
+// float32 evaluation of q at any pixel of the block, so a
+// cleared bit never skips a pixel the per-pixel test would have composited.
+__device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1, const uint4 &v3,
+                                               int X0, int Y0) {
+  const float u = __uint_as_float(v0.x), v = __uint_as_float(v0.y);
+  const float ca = __uint_as_float(v0.z), cb2 = __uint_as_float(v0.w);
+  const float cc = __uint_as_float(v1.x), k2 = __uint_as_float(v1.z);
+  const int rx0 = (int)(v3.x & 0xffffu), ry0 = (int)(v3.x >> 16);
+  const int rx1 = (int)(v3.y & 0xffffu), ry1 = (int)(v3.y >> 16);
+  const bool conic_ok = ca > 0.0f && cc > 0.0f;
+  uint32_t m = 0;
+#pragma unroll
+  for (int w = 0; w < 4; w++) {
+    const int bx0 = X0 + (w & 1) * 8, by0 = Y0 + (w >> 1) * 8;
+    const int bx1 = bx0 + 7, by1 = by0 + 7;
+    if (rx1 < bx0 || rx0 > bx1 || ry1 < by0 || ry0 > by1) continue;  // rectangle cull
+    if (!conic_ok) { m |= 1u << w; continue; }
+    const float dx0 = (float)bx0 - u, dx1 = (float)bx1 - u;
+    const float dy0 = (float)by0 - v, dy1 = (float)by1 - v;
+    const bool ox = dx0 > 0.0f || dx1 < 0.0f, oy = dy0 > 0.0f || dy1 < 0.0f;
+    float qmin = 0.0f;
+    if (ox || oy) {
+      qmin = INFINITY;
+      if (ox) {  // near vertical edge, dy clamped to the block
+        const float ex = dx0 > 0.0f ? dx0 : dx1;
+        const float dy = fminf(fmaxf(-cb2 * ex / (2.0f * cc), dy0), dy1);
+        qmin = fminf(qmin, ca * ex * ex + cb2 * ex * dy + cc * dy * dy);
+      }
+      if (oy) {  // near horizontal edge
+        const float ey = dy0 > 0.0f ? dy0 : dy1;
+        const float dx = fminf(fmaxf(-cb2 * ey / (2.0f * ca), dx0), dx1);
+        qmin = fminf(qmin, ca * dx * dx + cb2 * dx * ey + cc * ey * ey);
+      }
+    }
+    const float DX = fmaxf(fabsf(dx0), fabsf(dx1)), DY = fmaxf(fabsf(dy0), fabsf(dy1));
+    const float margin = 0.01f + 2e-5f * (ca * DX * DX + fabsf(cb2) * DX * DY + cc * DY * DY);
+    if (!(qmin > k2 + margin)) m |= 1u << w;  // NaN keeps the block
+  }
+  return m;
+}
+
 __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len, uint32_t start,
                                             int tid, int nthr, const uint4 *__restrict__ rec4,
                                             uint32_t *__restrict__ pair_gid,
-                                            uint4 *__restrict__ pair_rec) {
+                                            uint4 *__restrict__ pair_rec, int X0, int Y0) {
   for (int k = tid; k < len; k += nthr) {
     const uint32_t gid = (uint32_t)(a[k] & 0xffffffffull);
     const int64_t pos = (int64_t)start + k;
     pair_gid[pos] = gid;
     const uint4 *src = rec4 + (int64_t)gid * 4;
-    const uint4 v0 = src[0], v1 = src[1], v2 = src[2], v3 = src[3];
+    const uint4 v0 = src[0], v1 = src[1], v2 = src[2];
+    uint4 v3 = src[3];
+    v3.z = block_mask(v0, v1, v3, X0, Y0);
     uint4 *dst = pair_rec + pos * 4;
     dst[0] = v0; dst[1] = v1; dst[2] = v2; dst[3] = v3;
   }
@@ -232,9 +284,10 @@ __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int64_t T, const uint32_t *__restrict__ range, const unsigned long long *__restrict__ keys,
     const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid, uint4 *__restrict__ pair_rec,
-    uint32_t *__restrict__ long_list, uint32_t *__restrict__ long_count) {
+    uint32_t *__restrict__ long_list, uint32_t *__restrict__ long_count, int tiles_x) {
   __shared__ unsigned long long sk[kCtaCap];
   const int64_t tile = blockIdx.x;
+  const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
   const int len = (int)(end - start);
   if (len == 0) return;
@@ -250,7 +303,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   } else {
     bitonic_sort(sk, len, threadIdx.x, kSortThreads, [] { __syncthreads(); });
   }
-  emit_sorted(sk, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, pair_rec);
+  emit_sorted(sk, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, pair_rec, X0, Y0);
 }
 
 __global__ void __launch_bounds__(1024) k_sort_long(const uint32_t *__restrict__ range,
@@ -259,7 +312,8 @@ __global__ void __launch_bounds__(1024) k_sort_long(const uint32_t *__restrict__
                                                     uint32_t *__restrict__ pair_gid,
                                                     uint4 *__restrict__ pair_rec,
                                                     const uint32_t *__restrict__ long_list,
-                                                    const uint32_t *__restrict__ long_count) {
+                                                    const uint32_t *__restrict__ long_count,
+                                                    int tiles_x) {
   extern __shared__ unsigned long long lk[];
   const uint32_t nl = *long_count;
   for (uint32_t li = blockIdx.x; li < nl; li += gridDim.x) {
@@ -267,14 +321,15 @@ __global__ void __launch_bounds__(1024) k_sort_long(const uint32_t *__restrict__
     const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
     const int len = (int)(end - start);
     unsigned long long *a = keys + start;
+    const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
     if (len <= kLongSmemKeys) {
       for (int k = threadIdx.x; k < len; k += blockDim.x) lk[k] = a[k];
       __syncthreads();
       bitonic_sort(lk, len, threadIdx.x, blockDim.x, [] { __syncthreads(); });
-      emit_sorted(lk, len, start, threadIdx.x, blockDim.x, rec4, pair_gid, pair_rec);
+      emit_sorted(lk, len, start, threadIdx.x, blockDim.x, rec4, pair_gid, pair_rec, X0, Y0);
     } else {  // slow path for pathological buckets: same network in global memory
       bitonic_sort(a, len, threadIdx.x, blockDim.x, [] { __syncthreads(); });
-      emit_sorted(a, len, start, threadIdx.x, blockDim.x, rec4, pair_gid, pair_rec);
+      emit_sorted(a, len, start, threadIdx.x, blockDim.x, rec4, pair_gid, pair_rec, X0, Y0);
     }
     __syncthreads();
   }
@@ -305,7 +360,7 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
                                                w.keys);
   k_sort_tiles<<<(unsigned)T, kSortThreads, 0, s>>>(
       T, tile_range, w.keys, rec4, pair_gid, static_cast<uint4 *>(pair_rec), w.long_list,
-      w.long_count);
+      w.long_count, ci.tiles_x);
   const size_t lsm = kLongSmemKeys * sizeof(unsigned long long);
   static bool attr_done = false;
   if (!attr_done) {
@@ -315,7 +370,7 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   }
   k_sort_long<<<(unsigned)sms, 1024, lsm, s>>>(tile_range, w.keys, rec4, pair_gid,
                                                static_cast<uint4 *>(pair_rec), w.long_list,
-                                               w.long_count);
+                                               w.long_count, ci.tiles_x);
   return cudaGetLastError();
 }
 

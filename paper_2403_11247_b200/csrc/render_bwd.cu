@@ -240,8 +240,6 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
   }
 
   // ---- pixel warps
-  const uint32_t wlo = (uint32_t)wx0 | ((uint32_t)wy0 << 16);
-  const uint32_t whi_x = ((uint32_t)(wx0 + 7) | ((uint32_t)(wy0 + 7) << 16)) | 0x80008000u;
   const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
   float(*red)[8 * 4] = reinterpret_cast<float(*)[8 * 4]>(sm.red[wid]);  // [kG*kV][32]
   for (int k = 0; k < nb; k++) {
@@ -257,13 +255,11 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
         for (int q = 0; q < ng; q++) {
           const int e = cnt - 1 - g0 - q;
           const int j = b * kBB + e;
-          const float4 r3 = rb[e * 4 + 3];
-          const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
-          const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
+          const uint32_t bm = __float_as_uint(rb[e * 4 + 3].z);
           bool any = false;
-          // warp-uniform: the record's rectangle meets this warp's 8x8 block and
-          // the entry is inside some lane's replay range
-          if ((t1 & t2 & 0x80008000u) == 0x80008000u && j < wmax) {
+          // warp-uniform: the pair's block mask (payload word 14, bin.cu) keeps
+          // this warp's 8x8 block and the entry is inside some lane's replay range
+          if (((bm >> wid) & 1u) && j < wmax) {
             const float4 r0 = rb[e * 4 + 0];
             const float4 r1 = rb[e * 4 + 1];
             const float4 r2 = rb[e * 4 + 2];

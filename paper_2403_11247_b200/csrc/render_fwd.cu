@@ -128,10 +128,15 @@ __global__ void __launch_bounds__(256 / PPT) k_render_fwd(
 #pragma unroll 2
     for (int e = 0; e < cnt; e++) {
       const float4 r3 = rb[e * 4 + 3];
-      // warp-level cull: record rectangle [lo, hi] vs the warp's block
-      const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
-      const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
-      if ((t1 & t2 & 0x80008000u) != 0x80008000u) continue;
+      if (PPT == 2) {
+        // warp-level cull: the pair's 8x8-block mask (payload word 14, bin.cu)
+        if (!((__float_as_uint(r3.z) >> wid) & 1u)) continue;
+      } else {
+        // record rectangle [lo, hi] vs the warp's block
+        const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
+        const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
+        if ((t1 & t2 & 0x80008000u) != 0x80008000u) continue;
+      }
       const float4 r0 = rb[e * 4 + 0];  // u, v, ca, cb+cb
       const float4 r1 = rb[e * 4 + 1];  // cc, o_hat, k2, z
       const float dx = DSUB(fpx, r0.x);

@@ -37,27 +37,36 @@ __global__ void __launch_bounds__(kRuThreads) k_rvq_accum(
     __syncthreads();
   }
   const int64_t ne = eff_n(n, n_dev);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  // uniform trip count: the Eq 11 error of each stage is warp-reduced before its
+  // (shared) atomic instead of one same-address atomic per vector
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ne;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool ok = i < ne;
     float sh[D];
 #pragma unroll
     for (int j = 0; j < D; j++) sh[j] = 0.0f;
     for (int l = 0; l < L; l++) {
-      const uint32_t k = ru_idx(idx, idx_bytes, (int64_t)l * n + i);
-      if (k >= (uint32_t)P) break;  // out-of-range index: the vector is skipped from here
-      const float *c = codes + ((int64_t)l * P + k) * D;
+      const uint32_t k = ok ? ru_idx(idx, idx_bytes, (int64_t)l * n + i) : (uint32_t)P;
+      ok = ok && k < (uint32_t)P;  // out-of-range index: the vector is skipped from here
       float e2 = 0.0f;
+      if (ok) {
+        const float *c = codes + ((int64_t)l * P + k) * D;
 #pragma unroll
-      for (int j = 0; j < D; j++) {
-        const float r = DSUB(x[(int64_t)j * n + i], sh[j]);  // S - S_hat^{l-1}
-        atomicAdd(ssum + ((int64_t)l * P + k) * D + j, r);
-        const float e = r - c[j];
-        e2 = fmaf(e, e, e2);
+        for (int j = 0; j < D; j++) {
+          const float r = DSUB(x[(int64_t)j * n + i], sh[j]);  // S - S_hat^{l-1}
+          atomicAdd(ssum + ((int64_t)l * P + k) * D + j, r);
+          const float e = r - c[j];
+          e2 = fmaf(e, e, e2);
+        }
+        atomicAdd(scnt + (int64_t)l * P + k, 1u);
+#pragma unroll
+        for (int j = 0; j < D; j++) sh[j] = l == 0 ? c[j] : DADD(sh[j], c[j]);
       }
-      atomicAdd(scnt + (int64_t)l * P + k, 1u);
-      atomicAdd(serr + l, e2);
-#pragma unroll
-      for (int j = 0; j < D; j++) sh[j] = l == 0 ? c[j] : DADD(sh[j], c[j]);
+      if (!__any_sync(0xffffffffu, ok)) break;
+      e2 = warp_sum(e2);
+      if (lane == 0 && e2 != 0.0f) atomicAdd(serr + l, e2);
     }
   }
   if (SMEM) {

@@ -43,6 +43,50 @@ def _codebooks(env, sc):
             dict(scale_codes=sco, rot_codes=rco, scale_idx=si_o, rot_idx=ri_o))
 
 
+def check_block_mask(prec, rec_o, gid_o, rng_o, cam):
+    """Payload word 14 (the renderers' 8x8-block cull mask): every
+    other word equals the oracle record bit-exactly; a bit may be set only where
+    the record's pixel rectangle meets the block, must be set wherever the
+    float64 minimum of q over the block's box is <= k^2 (a pixel the renderer
+    could composite), and must be clear where that minimum exceeds k^2 by far."""
+    other = [i for i in range(16) if i != 14]
+    assert np.array_equal(prec[:, other], rec_o[gid_o][:, other])
+    assert np.all(rec_o[:, 14] == 0)
+    T = rng_o.shape[0]
+    tiles_x = (cam["width"] + 15) // 16
+    tile = np.repeat(np.arange(T), (rng_o[:, 1] - rng_o[:, 0]).astype(np.int64))
+    f = prec.view(np.float32).astype(np.float64)
+    u, v, ca, cb2, cc, k2 = f[:, 0], f[:, 1], f[:, 2], f[:, 3], f[:, 4], f[:, 6]
+    rx0, ry0 = prec[:, 12] & 0xffff, prec[:, 12] >> 16
+    rx1, ry1 = prec[:, 13] & 0xffff, prec[:, 13] >> 16
+    bits = prec[:, 14]
+    assert np.all(bits < 16)
+    n_set = 0
+    for w in range(4):
+        bx0 = (tile % tiles_x) * 16 + (w & 1) * 8
+        by0 = (tile // tiles_x) * 16 + (w >> 1) * 8
+        bx1, by1 = bx0 + 7, by0 + 7
+        rect = ~((rx1 < bx0) | (rx0 > bx1) | (ry1 < by0) | (ry0 > by1))
+        dx0, dx1, dy0, dy1 = bx0 - u, bx1 - u, by0 - v, by1 - v
+        q = lambda dx, dy: ca * dx * dx + cb2 * dx * dy + cc * dy * dy
+        qmin = np.full(len(u), np.inf)
+        for ex in (dx0, dx1):
+            qmin = np.minimum(qmin, q(ex, np.clip(-cb2 * ex / (2 * cc), dy0, dy1)))
+        for ey in (dy0, dy1):
+            qmin = np.minimum(qmin, q(np.clip(-cb2 * ey / (2 * ca), dx0, dx1), ey))
+        inside = (dx0 <= 0) & (dx1 >= 0) & (dy0 <= 0) & (dy1 >= 0)
+        qmin[inside] = 0.0
+        b = ((bits >> w) & 1).astype(bool)
+        n_set += int(b.sum())
+        assert not np.any(b & ~rect), "mask bit outside the record rectangle"
+        must = rect & (qmin <= k2)
+        assert np.all(b[must]), f"block {w}: {int((must & ~b).sum())} needed bits cleared"
+        DX, DY = np.maximum(np.abs(dx0), np.abs(dx1)), np.maximum(np.abs(dy0), np.abs(dy1))
+        far = qmin > k2 + 1.0 + 1e-3 * (ca * DX * DX + np.abs(cb2) * DX * DY + cc * DY * DY)
+        assert not np.any(b & far), "mask bit set for a block far outside the ellipse"
+    return n_set
+
+
 def run_and_compare(env, sc, view=None, use_codebook=True, prm=None, bwd=True, seed=1,
                     flags=0):
     torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
@@ -70,7 +114,7 @@ def run_and_compare(env, sc, view=None, use_codebook=True, prm=None, bwd=True, s
     assert np.array_equal(gid_g, gid_o)
     assert np.array_equal(b["tile_range"].cpu().numpy().view(np.uint32), rng_o)
     prec = b["pair_rec"][:npairs].cpu().numpy().view(np.uint32)
-    assert np.array_equal(prec, rec_o[gid_o])
+    check_block_mask(prec, rec_o, gid_o, rng_o, cam)
     # a6
     out = cs.render_fwd(b["pair_rec"], b["tile_range"], cam, prm_c)
     fo = orc.render_fwd(rec_o, gid_o, rng_o, cam, prm_o)
