@@ -110,6 +110,30 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// try_wait with a suspend-time hint: the waiting warp is parked (it resumes when
+// the phase completes or after ~ns) instead of re-issuing the probe, so a warp
+// blocked on a slow partner does not take issue slots from the working warps.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+#ifndef CSPLAT_MBAR_SLEEP_NS
+#define CSPLAT_MBAR_SLEEP_NS 20000
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+  while (!mbar_try_wait_hint(bar, parity, CSPLAT_MBAR_SLEEP_NS)) {
+  }
+}
 // 1-D TMA bulk copy global -> shared, completion signalled on `bar`.
 __device__ __forceinline__ void tma_load_1d(void *dst_smem, const void *src_gmem, uint32_t bytes,
                                             uint64_t *bar) {

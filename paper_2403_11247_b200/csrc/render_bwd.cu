@@ -56,9 +56,6 @@ __device__ __forceinline__ float ex2_approx_b(float x) {
   return y;
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 struct BPix {
   float T, B, gr, gg, gb, gd, gs;
@@ -218,7 +215,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     for (int k = 0; k < nb; k++) {
       const int s = k % kBS;
       if (k >= kBS) {  // slot s held replay batch k - kBS: wait for all pixel warps
-        mbar_wait(&sm.empty[s], (uint32_t)((k / kBS) - 1) & 1u);
+        mbar_wait_sleep(&sm.empty[s], (uint32_t)((k / kBS) - 1) & 1u);
         flush(k - kBS, s);
         __syncwarp();  // every lane has read the slot's gids before it is overwritten
       }
@@ -233,7 +230,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     }
     for (int k = max(0, nb - kBS); k < nb; k++) {  // drain the last slots
       const int s = k % kBS;
-      mbar_wait(&sm.empty[s], (uint32_t)(k / kBS) & 1u);
+      mbar_wait_sleep(&sm.empty[s], (uint32_t)(k / kBS) & 1u);
       flush(k, s);
     }
     return;
@@ -246,7 +243,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     const int s = k % kBS;
     const int b = nb - 1 - k;
     const int cnt = batch_cnt(k);
-    mbar_wait(&sm.full[s], (uint32_t)(k / kBS) & 1u);
+    mbar_wait_sleep(&sm.full[s], (uint32_t)(k / kBS) & 1u);
     const bool work = b * kBB < wmax;  // warp-uniform: some lane replays into this batch
     if (work) {
       const float4 *rb = sm.buf[s];

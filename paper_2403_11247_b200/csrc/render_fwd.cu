@@ -6,11 +6,11 @@
 // 8x8 pixel block.  The tile's records are a contiguous slice of the
 // pair-ordered payload written by csplat_bin_tiles and are streamed into
 // shared memory by 1-D TMA bulk copies (cp.async.bulk + mbarrier complete_tx)
-// through a kStages-deep ring of kBatch-record batches; thread 0 is the
-// producer; every record is read from shared memory as a broadcast.  A warp
-// skips a record whose pixel rectangle misses its 8x8 block (two SWAR u16x2
-// subtractions; result-invariant).  The CTA stops once every pixel terminated
-// (T(1-alpha) < t_min, R3), checked once per batch.  The per-pixel q test is
+// through a kStages-deep ring of kBatch-record batches fed by a producer warp;
+// every record is read from shared memory as a broadcast.  A warp skips a
+// record whose 8x8-block cull bit (payload word 14, bin.cu) is clear
+// (result-invariant).  The tile's stream ends once every pixel terminated
+// (T(1-alpha) < t_min, R3), checked once per batch and warp.  The per-pixel q test is
 // the DA of DESIGN.md §3 (bit-exact with the oracle); alpha, T and the sums
 // are float32 with ex2.approx.
 #include "common.cuh"
@@ -71,100 +71,130 @@ __device__ __forceinline__ void composite_pred(PixState &p, bool h, float q, flo
   p.done |= (h & stop) ? 1 : 0;
 }
 
-// PPT = pixels per thread (a column of PPT vertically adjacent pixels): a warp
-// owns an 8 x (4 PPT) block, a CTA of 256/PPT threads one 16x16 tile.
+// PPT = pixels per thread (a column of PPT vertically adjacent pixels): a pixel
+// warp owns an 8 x (4 PPT) block, 256/PPT pixel threads one 16x16 tile, plus
+// one producer warp.  The producer streams the tile's batches into the ring
+// (mbarrier full[] with complete_tx) and refills a slot once every pixel warp
+// has released it (empty[], one arrival per warp); the pixel warps never
+// synchronise with each other, so a warp with a heavy block does not hold the
+// others at a CTA barrier.  A warp whose pixels all terminated counts itself
+// in done_cnt and from then on only releases slots; once all have, the
+// producer ends the stream by completing the next full[] phase without data
+// (end_b), and every pixel warp leaves at that batch.
 template <int PPT>
-__global__ void __launch_bounds__(256 / PPT) k_render_fwd(
+__global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, float tmin, float *__restrict__ color, float *__restrict__ depth,
     float *__restrict__ sil, float *__restrict__ t_final, int32_t *__restrict__ n_contrib) {
+  constexpr int kPW = 8 / PPT;  // pixel warps
   __shared__ __align__(128) float4 buf[kStages][kBatch * 4];
-  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ int done_cnt, end_b;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int tile = blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
-  constexpr int kBH = 4 * PPT;  // warp block height
-  const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * kBH;
-  const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * PPT;
-  // warp block corners as u16x2 for the SWAR rectangle test
-  const uint32_t wlo = (uint32_t)wx0 | ((uint32_t)wy0 << 16);
-  const uint32_t whi_x = ((uint32_t)(wx0 + 7) | ((uint32_t)(wy0 + kBH - 1) << 16)) | 0x80008000u;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
   const int len = (int)(end - start);
   const int nb = (len + kBatch - 1) / kBatch;
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; s++) mbar_init(&full[s], 1);
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kPW);
+    }
+    done_cnt = 0;
+    end_b = -1;
     fence_mbar_init();
   }
   __syncthreads();
-  int issued = 0;
-  auto issue = [&](int b) {
-    const int cnt = min(kBatch, len - b * kBatch);
-    const uint32_t bytes = (uint32_t)cnt * CSPLAT_RECORD_BYTES;
-    uint64_t *bar = &full[b % kStages];
-    mbar_arrive_expect_tx(bar, bytes);
-    tma_load_1d(&buf[b % kStages][0], pair_rec + ((int64_t)start + (int64_t)b * kBatch) * 4, bytes,
-                bar);
-  };
-  if (tid == 0)
-    for (; issued < min(kStages - 1, nb); issued++) issue(issued);
 
+  if (wid == kPW) {  // ---- producer warp (lane 0)
+    if (lane == 0) {
+      for (int b = 0; b < nb; b++) {
+        const int s = b % kStages;
+        if (b >= kStages) mbar_wait_sleep(&empty[s], (uint32_t)((b / kStages) - 1) & 1u);
+        if (*(volatile int *)&done_cnt == kPW) {  // every pixel terminated: end the stream
+          end_b = b;
+          mbar_arrive(&full[s]);
+          break;
+        }
+        const int cnt = min(kBatch, len - b * kBatch);
+        const uint32_t bytes = (uint32_t)cnt * CSPLAT_RECORD_BYTES;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        tma_load_1d(&buf[s][0], pair_rec + ((int64_t)start + (int64_t)b * kBatch) * 4, bytes,
+                    &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---- pixel warps
+  constexpr int kBH = 4 * PPT;  // warp block height
+  const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * kBH;
+  const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * PPT;
+  // warp block corners as u16x2 for the SWAR rectangle test (PPT != 2)
+  const uint32_t wlo = (uint32_t)wx0 | ((uint32_t)wy0 << 16);
+  const uint32_t whi_x = ((uint32_t)(wx0 + 7) | ((uint32_t)(wy0 + kBH - 1) << 16)) | 0x80008000u;
   PixState p[PPT];
-  int alldone = 1;
+  int mydone = 1;
 #pragma unroll
   for (int k = 0; k < PPT; k++) {
     p[k] = PixState{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, (px < W && py0 + k < H) ? 0 : 1};
-    alldone &= p[k].done;
+    mydone &= p[k].done;
   }
+  bool wdone = __all_sync(0xffffffffu, mydone);
+  if (wdone && lane == 0) atomicAdd(&done_cnt, 1);
   const float fpx = (float)px;
-  int b = 0;
-  for (; b < nb; b++) {
-    if (__syncthreads_and(alldone)) break;
-    if (tid == 0 && issued < nb && issued <= b + kStages - 1) issue(issued++);
-    mbar_wait(&full[b % kStages], (uint32_t)(b / kStages) & 1u);
-    const float4 *rb = buf[b % kStages];
-    const int cnt = min(kBatch, len - b * kBatch);
+  for (int b = 0; b < nb; b++) {
+    const int s = b % kStages;
+    mbar_wait_sleep(&full[s], (uint32_t)(b / kStages) & 1u);
+    if (*(volatile int *)&end_b == b) break;
+    if (!wdone) {
+      const float4 *rb = buf[s];
+      const int cnt = min(kBatch, len - b * kBatch);
 #pragma unroll 2
-    for (int e = 0; e < cnt; e++) {
-      const float4 r3 = rb[e * 4 + 3];
-      if (PPT == 2) {
-        // warp-level cull: the pair's 8x8-block mask (payload word 14, bin.cu)
-        if (!((__float_as_uint(r3.z) >> wid) & 1u)) continue;
-      } else {
-        // record rectangle [lo, hi] vs the warp's block
-        const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
-        const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
-        if ((t1 & t2 & 0x80008000u) != 0x80008000u) continue;
-      }
-      const float4 r0 = rb[e * 4 + 0];  // u, v, ca, cb+cb
-      const float4 r1 = rb[e * 4 + 1];  // cc, o_hat, k2, z
-      const float dx = DSUB(fpx, r0.x);
-      const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
-      float q[PPT];
-      bool h[PPT];
-      bool anyh = false;
+      for (int e = 0; e < cnt; e++) {
+        const float4 r3 = rb[e * 4 + 3];
+        if (PPT == 2) {
+          // warp-level cull: the pair's 8x8-block mask (payload word 14, bin.cu)
+          if (!((__float_as_uint(r3.z) >> wid) & 1u)) continue;
+        } else {
+          // record rectangle [lo, hi] vs the warp's block
+          const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
+          const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
+          if ((t1 & t2 & 0x80008000u) != 0x80008000u) continue;
+        }
+        const float4 r0 = rb[e * 4 + 0];  // u, v, ca, cb+cb
+        const float4 r1 = rb[e * 4 + 1];  // cc, o_hat, k2, z
+        const float dx = DSUB(fpx, r0.x);
+        const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
+        float q[PPT];
+        bool h[PPT];
+        bool anyh = false;
 #pragma unroll
-      for (int k = 0; k < PPT; k++) {
-        const float dy = DSUB((float)(py0 + k), r0.y);
-        q[k] = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
-        h[k] = (p[k].done == 0) & (q[k] >= 0.0f) & (q[k] <= r1.z);  // R2 (DA)
-        anyh |= h[k];
-      }
-      if (!anyh) continue;
-      const float4 r2 = rb[e * 4 + 2];  // r, g, b, gid
-      const int idx = b * kBatch + e + 1;
-      // the pixels as straight-line (predicated) code so their chains interleave
+        for (int k = 0; k < PPT; k++) {
+          const float dy = DSUB((float)(py0 + k), r0.y);
+          q[k] = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
+          h[k] = (p[k].done == 0) & (q[k] >= 0.0f) & (q[k] <= r1.z);  // R2 (DA)
+          anyh |= h[k];
+        }
+        if (!anyh) continue;
+        const float4 r2 = rb[e * 4 + 2];  // r, g, b, gid
+        const int idx = b * kBatch + e + 1;
+        // the pixels as straight-line (predicated) code so their chains interleave
 #pragma unroll
-      for (int k = 0; k < PPT; k++) composite_pred(p[k], h[k], q[k], r1.y, r1.w, r2, amax, tmin, idx);
+        for (int k = 0; k < PPT; k++)
+          composite_pred(p[k], h[k], q[k], r1.y, r1.w, r2, amax, tmin, idx);
+      }
+      mydone = 1;
+#pragma unroll
+      for (int k = 0; k < PPT; k++) mydone &= p[k].done;
+      wdone = __all_sync(0xffffffffu, mydone);
+      if (wdone && lane == 0) atomicAdd(&done_cnt, 1);  // before the release below
     }
-    alldone = 1;
-#pragma unroll
-    for (int k = 0; k < PPT; k++) alldone &= p[k].done;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // release the slot
   }
-  // never leave the CTA with bulk copies in flight into its shared memory
-  if (tid == 0)
-    for (int bb = b; bb < issued; bb++) mbar_wait(&full[bb % kStages], (uint32_t)(bb / kStages) & 1u);
   const int64_t HW = (int64_t)W * H;
   if (px < W) {
 #pragma unroll
@@ -188,7 +218,7 @@ cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
   const CamInfo ci = cam_info(cam);
   const int T = ci.tiles_x * ci.tiles_y;
   constexpr int PPT = CSPLAT_FWD_PPT;
-  k_render_fwd<PPT><<<T, 256 / PPT, 0, s>>>(static_cast<const float4 *>(pair_rec), tile_range,
+  k_render_fwd<PPT><<<T, 256 / PPT + 32, 0, s>>>(static_cast<const float4 *>(pair_rec), tile_range,
                                             ci.W, ci.H, ci.tiles_x, prm.alpha_max, prm.t_min,
                                             color, depth, sil, t_final, n_contrib);
   return cudaGetLastError();
