@@ -37,7 +37,14 @@ __global__ void __launch_bounds__(256) k_chain(
   if (i < ne) alive = rec4[i * 4 + 1].y != 0.0f;  // o_hat word is 0 iff culled
   if (alive) {
     const float4 a0 = acc4[i * 3 + 0], a1 = acc4[i * 3 + 1], a2 = acc4[i * 3 + 2];
-    const float gu = a0.x, gv = a0.y, gca = a0.z, gcb = a0.w, gcc = a1.x, goh = a1.y, gz = a1.z;
+    // k_render_bwd accumulates the raw moments Sx, Sy, Sxx, Sxy, Syy of
+    // a = alpha dL/dalpha; map them through the record's DA conic
+    // (q = ca dx^2 + (2cb) dx dy + cc dy^2; render_bwd.cu, bwd_pixel_pair)
+    const float4 rc0 = rec4[i * 4 + 0];
+    const float cca = rc0.z, ccb = 0.5f * rc0.w, ccc = rec4[i * 4 + 1].x;
+    const float gu = cca * a0.x + ccb * a0.y, gv = ccb * a0.x + ccc * a0.y;
+    const float gca = -0.5f * a0.z, gcb = -a0.w, gcc = -0.5f * a1.x;
+    const float goh = a1.y, gz = a1.z;
     g[4] = a1.w;  // rgb
     g[5] = a2.x;
     g[6] = a2.y;

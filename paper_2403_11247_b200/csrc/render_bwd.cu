@@ -15,7 +15,8 @@
 // Per pixel, from T_final and n_contrib: T_j = T_{j+1} / (1 - alpha_j),
 // v_j = <rgb_j, dL/dC> + z_j dL/dD + dL/dS, dL/dalpha_j = T_j (v_j - B_j),
 // B_{j-1} = alpha_j v_j + (1-alpha_j) B_j.  A thread adds its two pixels'
-// ten partials (u, v, ca, cb, cc, o_hat, z, r, g, b) in registers; the warp
+// ten partials (raw moments of the conic/mean gradient, o_hat, z, r, g, b;
+// bwd_pixel_pair) in registers; the warp
 // stores the lanes' partials of kG entries as shared-memory rows and each lane
 // sums whole rows with rotated LDS.128 (a transposed reduction: ~2
 // instructions per (entry, value) instead of a 10-instruction shuffle tree).
@@ -31,7 +32,7 @@ constexpr int kBS = KBS_OVERRIDE; // ring depth
 constexpr int kAcc = 12;          // accumulator floats per Gaussian
 constexpr int kCW = 4;            // pixel (consumer) warps: 4 x 32 lanes x 2 pixels = 16x16
 constexpr int kBwdThreads = (kCW + 1) * 32;  // + 1 producer warp
-constexpr int kG = 4;             // entries per transposed-reduction group (smem vs occupancy)
+constexpr int kG = 3;             // active entries per transposed reduction: kG*kV <= 32 rows = one pass
 constexpr int kV = 10;            // partials per (pixel, entry)
 #ifndef CSPLAT_BWD_MIN_BLOCKS
 #define CSPLAT_BWD_MIN_BLOCKS 5
@@ -45,8 +46,7 @@ struct BwdSmem {
   float4 red[kCW][kG * kV][8];          // per-warp rows of 32 lane partials
   float part[kBS][kCW][kBB][kAcc];      // per-slot, per-warp sums per batch entry
   uint64_t full[kBS], empty[kBS];
-  uint32_t pact[kBS][kCW];              // did warp w write part[slot][w]?
-  uint32_t act[kCW][kG];
+  uint32_t pmask[kBS][kCW];             // bit e: warp w wrote part[slot][w][e]
   int wmax[kCW];
 };
 
@@ -62,85 +62,62 @@ struct BPix {
   int last;
 };
 
-// One (pixel, entry) of the replay; adds its partials into v and returns
-// whether the entry contributed to this pixel.
-__device__ __forceinline__ bool bwd_pixel(BPix &p, int j, float dx, float dy, const float4 &r0,
-                                          const float4 &r1, const float4 &r2, float amax,
-                                          float (&v)[kV]) {
-  if (j >= p.last) return false;
-  // DA q, bit-identical to the forward's
-  const float q = DFMA(DMUL(r0.z, dx), dx, DFMA(DMUL(r0.w, dx), dy, DMUL(DMUL(r1.x, dy), dy)));
-  if (!(q >= 0.0f && q <= r1.z)) return false;
-  const float G = ex2_approx_b(q * -0.72134752f);  // exp(-q/2), same expression as the forward
-  const float araw = r1.y * G;
-  const bool capped = !(araw < amax);
-  const float alpha = fminf(amax, araw);
-  float rcp;  // 1 / (1 - alpha) with alpha <= alpha_max < 1 (R1): no range fix-up needed
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(1.0f - alpha));
-  const float Tj = p.T * rcp;
-  const float w = alpha * Tj;
-  const float vv = fmaf(r2.x, p.gr, fmaf(r2.y, p.gg, fmaf(r2.z, p.gb, fmaf(r1.w, p.gd, p.gs))));
-  const float dLda = Tj * (vv - p.B);
-  v[7] = fmaf(p.gr, w, v[7]);
-  v[8] = fmaf(p.gg, w, v[8]);
-  v[9] = fmaf(p.gb, w, v[9]);
-  v[6] = fmaf(p.gd, w, v[6]);
-  if (!capped) {  // R23: no gradient through a capped alpha
-    v[5] = fmaf(G, dLda, v[5]);
-    const float dq = -0.5f * alpha * dLda;
-    const float dqdx = dq * dx, dqdy = dq * dy;
-    v[2] = fmaf(dqdx, dx, v[2]);
-    v[3] = fmaf(2.0f * dqdx, dy, v[3]);
-    v[4] = fmaf(dqdy, dy, v[4]);
-    v[0] -= fmaf(2.0f * r0.z, dqdx, r0.w * dqdy);
-    v[1] -= fmaf(r0.w, dqdx, 2.0f * r1.x * dqdy);
-  }
-  p.B = fmaf(alpha, vv, (1.0f - alpha) * p.B);
-  p.T = Tj;
-  return true;
-}
-
-// Branch-free form of bwd_pixel for the thread's two pixels: both dependency
-// chains are straight-line code (inactive pixels contribute exact zeros and
-// leave T and B unchanged: alpha = 0 gives rcp(1) = 1), so the compiler can
-// interleave them -- the replay is latency-bound, not issue-bound.
+// One replay entry j for the thread's two pixels (same column: dx shared, dy0,
+// dy1), as straight-line predicated code so the two dependency chains
+// interleave (inactive pixels contribute exact zeros and leave T and B
+// unchanged: alpha = 0 gives rcp(1) = 1).  With a = alpha dL/dalpha the
+// partials are the raw moments
+//   v0..4 = sum a dx, sum a dy, sum a dx^2, sum a dx dy, sum a dy^2,
+//   v5 = sum G dL/dalpha, v6 = sum w gD, v7..9 = sum w gC
+// (w = alpha T_j); the conic's constants and the -1/2 of dalpha/dq are applied
+// once per Gaussian in k_chain (linear, so summing first is exact algebra):
+//   dL/du = ca Sx + cb Sy, dL/dv = cb Sx + cc Sy, dL/dca = -Sxx/2,
+//   dL/d(cb) = -Sxy, dL/dcc = -Syy/2   (q = ca dx^2 + 2cb dx dy + cc dy^2).
 __device__ __forceinline__ bool bwd_pixel_pair(BPix (&pp)[2], int j, float dx, float dy0,
                                                float dy1, const float4 &r0, const float4 &r1,
                                                const float4 &r2, float amax, float (&v)[kV]) {
   const float dys[2] = {dy0, dy1};
+  const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);  // shared by the column
+  float av[2], gd[2], w[2];
   bool any = false;
 #pragma unroll
   for (int k = 0; k < 2; k++) {
     BPix &p = pp[k];
     const float dy = dys[k];
-    const float q = DFMA(DMUL(r0.z, dx), dx, DFMA(DMUL(r0.w, dx), dy, DMUL(DMUL(r1.x, dy), dy)));
+    // DA q, bit-identical to the forward's
+    const float q = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
     const bool val = (j < p.last) & (q >= 0.0f) & (q <= r1.z);
     any |= val;
-    const float G = ex2_approx_b(q * -0.72134752f);  // same expression as the forward
+    const float G = ex2_approx_b(q * -0.72134752f);  // exp(-q/2), same expression as the forward
     const float araw = r1.y * G;
     const float alpha = val ? fminf(amax, araw) : 0.0f;
+    const float om = 1.0f - alpha;
     float rcp;  // alpha <= alpha_max < 1 (R1)
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(1.0f - alpha));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(om));
     const float Tj = p.T * rcp;
-    const float w = alpha * Tj;
+    w[k] = alpha * Tj;
     const float vv = fmaf(r2.x, p.gr, fmaf(r2.y, p.gg, fmaf(r2.z, p.gb, fmaf(r1.w, p.gd, p.gs))));
     // R23: no gradient through a capped alpha
     const float dLda = (val & (araw < amax)) ? Tj * (vv - p.B) : 0.0f;
-    v[7] = fmaf(p.gr, w, v[7]);
-    v[8] = fmaf(p.gg, w, v[8]);
-    v[9] = fmaf(p.gb, w, v[9]);
-    v[6] = fmaf(p.gd, w, v[6]);
-    v[5] = fmaf(G, dLda, v[5]);
-    const float dq = -0.5f * alpha * dLda;
-    const float dqdx = dq * dx, dqdy = dq * dy;
-    v[2] = fmaf(dqdx, dx, v[2]);
-    v[3] = fmaf(2.0f * dqdx, dy, v[3]);
-    v[4] = fmaf(dqdy, dy, v[4]);
-    v[0] -= fmaf(2.0f * r0.z, dqdx, r0.w * dqdy);
-    v[1] -= fmaf(r0.w, dqdx, 2.0f * r1.x * dqdy);
-    p.B = fmaf(alpha, vv, (1.0f - alpha) * p.B);
+    av[k] = alpha * dLda;
+    gd[k] = G * dLda;
+    p.B = fmaf(alpha, vv, om * p.B);
     p.T = Tj;
   }
+  // the entry's partials (written, not accumulated: v is per entry)
+  const float sx = dx * (av[0] + av[1]);
+  const float t0 = av[0] * dy0, t1 = av[1] * dy1;
+  const float sy = t0 + t1;
+  v[0] = sx;
+  v[1] = sy;
+  v[2] = dx * sx;
+  v[3] = dx * sy;
+  v[4] = fmaf(t0, dy0, t1 * dy1);
+  v[5] = gd[0] + gd[1];
+  v[6] = fmaf(pp[1].gd, w[1], pp[0].gd * w[0]);
+  v[7] = fmaf(pp[1].gr, w[1], pp[0].gr * w[0]);
+  v[8] = fmaf(pp[1].gg, w[1], pp[0].gg * w[0]);
+  v[9] = fmaf(pp[1].gb, w[1], pp[0].gb * w[0]);
   return any;
 }
 
@@ -194,22 +171,26 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
   if (producer) {
     // fold the pixel warps' partials of replay batch k (slot s) into the accumulator
     auto flush = [&](int k, int s) {
-      const int cnt = batch_cnt(k);
-      const float4 *rb = sm.buf[s];
-      for (int p = lane; p < cnt * 3; p += 32) {
-        const int e = p / 3, c = p - (p / 3) * 3;
-        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int e = lane;  // one batch entry per lane
+      if (e >= batch_cnt(k)) return;
+      float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0;
+      bool hit = false;
 #pragma unroll
-        for (int w = 0; w < kCW; w++) {
-          if (!sm.pact[s][w]) continue;
-          const float4 t4 = reinterpret_cast<const float4 *>(sm.part[s][w][e])[c];
-          s4.x += t4.x; s4.y += t4.y; s4.z += t4.z; s4.w += t4.w;
-        }
-        if (c == 2) { s4.z = 0.f; s4.w = 0.f; }  // padding slots
-        if (s4.x != 0.f || s4.y != 0.f || s4.z != 0.f || s4.w != 0.f) {
-          const uint32_t gid = __float_as_uint(rb[e * 4 + 2].w);
-          red_add_v4(acc + (int64_t)gid * kAcc + c * 4, s4.x, s4.y, s4.z, s4.w);
-        }
+      for (int w = 0; w < kCW; w++) {
+        if (!((sm.pmask[s][w] >> e) & 1u)) continue;
+        hit = true;
+        const float4 *t = reinterpret_cast<const float4 *>(sm.part[s][w][e]);
+        const float4 t0 = t[0], t1 = t[1], t2 = t[2];
+        s0.x += t0.x; s0.y += t0.y; s0.z += t0.z; s0.w += t0.w;
+        s1.x += t1.x; s1.y += t1.y; s1.z += t1.z; s1.w += t1.w;
+        s2.x += t2.x; s2.y += t2.y;
+      }
+      if (hit) {
+        const uint32_t gid = __float_as_uint(sm.buf[s][e * 4 + 2].w);
+        float *dst = acc + (int64_t)gid * kAcc;
+        red_add_v4(dst, s0.x, s0.y, s0.z, s0.w);
+        red_add_v4(dst + 4, s1.x, s1.y, s1.z, s1.w);
+        red_add_v4(dst + 8, s2.x, s2.y, 0.f, 0.f);
       }
     };
     for (int k = 0; k < nb; k++) {
@@ -245,63 +226,65 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     const int cnt = batch_cnt(k);
     mbar_wait_sleep(&sm.full[s], (uint32_t)(k / kBS) & 1u);
     const bool work = b * kBB < wmax;  // warp-uniform: some lane replays into this batch
+    uint32_t pm = 0;                   // entries of this batch with partials in part[s][wid]
     if (work) {
       const float4 *rb = sm.buf[s];
-      for (int g0 = 0; g0 < cnt; g0 += kG) {  // processing index g0 + q <-> entry cnt-1-g0-q
-        const int ng = min(kG, cnt - g0);
-        for (int q = 0; q < ng; q++) {
-          const int e = cnt - 1 - g0 - q;
-          const int j = b * kBB + e;
-          const uint32_t bm = __float_as_uint(rb[e * 4 + 3].z);
-          bool any = false;
-          // warp-uniform: the pair's block mask (payload word 14, bin.cu) keeps
-          // this warp's 8x8 block and the entry is inside some lane's replay range
-          if (((bm >> wid) & 1u) && j < wmax) {
-            const float4 r0 = rb[e * 4 + 0];
-            const float4 r1 = rb[e * 4 + 1];
-            const float4 r2 = rb[e * 4 + 2];
-            float v[kV];
+      // sum the rows of the nq pending entries (entry indices packed in ents) into
+      // part[s][wid]: lane r < nq*kV owns row r (one pass, kG*kV <= 32)
+      auto reduce = [&](int nq, uint32_t ents) {
+        __syncwarp();
+        if (lane < nq * kV) {
+          const int q = lane / kV, c = lane - q * kV;
+          // 32 partials as 8 rotated 16-byte chunks, summed on packed FADD2
+          const float4 *row = sm.red[wid][lane];
+          unsigned long long s01 = 0ull, s23 = 0ull;
 #pragma unroll
-            for (int c = 0; c < kV; c++) v[c] = 0.f;
-            const float dx = DSUB(fpx, r0.x);
-            const bool a = bwd_pixel_pair(pp, j, dx, DSUB(fpy0, r0.y), DSUB(fpy1, r0.y), r0, r1,
-                                          r2, amax, v);
-            any = __any_sync(0xffffffffu, a);
-            if (any) {  // every lane writes its (possibly zero) partials
-#pragma unroll
-              for (int c = 0; c < kV; c++) red[q * kV + c][lane] = v[c];
-            }
+          for (int t = 0; t < 8; t++) {
+            const float4 x = row[(t + lane) & 7];
+            unsigned long long a2, b2;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(a2) : "f"(x.x), "f"(x.y));
+            asm("mov.b64 %0, {%1, %2};" : "=l"(b2) : "f"(x.z), "f"(x.w));
+            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s01) : "l"(a2));
+            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s23) : "l"(b2));
           }
-          if (lane == 0) sm.act[wid][q] = any ? 1u : 0u;
+          asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s01) : "l"(s23));
+          const float sum = __uint_as_float((uint32_t)s01) + __uint_as_float((uint32_t)(s01 >> 32));
+          sm.part[s][wid][(ents >> (8 * q)) & 0xffu][c] = sum;
         }
         __syncwarp();
-        // transposed sums: lane l owns rows l, l+32 of the ng*kV rows
-        for (int r = lane; r < ng * kV; r += 32) {
-          const int q = r / kV, c = r - q * kV;
-          float sum = 0.f;
-          if (sm.act[wid][q]) {
-            // 32 partials as 8 rotated 16-byte chunks, summed on packed FADD2
-            const float4 *row = sm.red[wid][r];
-            unsigned long long s01 = 0ull, s23 = 0ull;
+      };
+      int nq = 0;
+      uint32_t ents = 0;
+      for (int i = 0; i < cnt; i++) {  // back to front
+        const int e = cnt - 1 - i;
+        const int j = b * kBB + e;
+        const uint32_t bm = __float_as_uint(rb[e * 4 + 3].z);
+        // warp-uniform: the pair's block mask (payload word 14, bin.cu) keeps this
+        // warp's 8x8 block and the entry is inside some lane's replay range
+        if (!((bm >> wid) & 1u) || j >= wmax) continue;
+        const float4 r0 = rb[e * 4 + 0];
+        const float4 r1 = rb[e * 4 + 1];
+        const float4 r2 = rb[e * 4 + 2];
+        float v[kV];
+        const float dx = DSUB(fpx, r0.x);
+        const bool a = bwd_pixel_pair(pp, j, dx, DSUB(fpy0, r0.y), DSUB(fpy1, r0.y), r0, r1, r2,
+                                      amax, v);
+        if (!__any_sync(0xffffffffu, a)) continue;
+        // every lane writes its (possibly zero) partials as row nq*kV + c
 #pragma unroll
-            for (int t = 0; t < 8; t++) {
-              const float4 x = row[(t + lane) & 7];
-              unsigned long long a, b;
-              asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "f"(x.x), "f"(x.y));
-              asm("mov.b64 %0, {%1, %2};" : "=l"(b) : "f"(x.z), "f"(x.w));
-              asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s01) : "l"(a));
-              asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s23) : "l"(b));
-            }
-            asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s01) : "l"(s23));
-            sum = __uint_as_float((uint32_t)s01) + __uint_as_float((uint32_t)(s01 >> 32));
-          }
-          sm.part[s][wid][cnt - 1 - g0 - q][c] = sum;
+        for (int c = 0; c < kV; c++) red[nq * kV + c][lane] = v[c];
+        ents |= (uint32_t)e << (8 * nq);
+        pm |= 1u << e;
+        if (++nq == kG) {
+          reduce(nq, ents);
+          nq = 0;
+          ents = 0;
         }
-        __syncwarp();
       }
+      if (nq) reduce(nq, ents);
     }
     if (lane == 0) {
-      sm.pact[s][wid] = work ? 1u : 0u;
+      sm.pmask[s][wid] = pm;
       mbar_arrive(&sm.empty[s]);  // release: part[s][wid] and the slot are done
     }
   }
