@@ -121,6 +121,65 @@ __device__ __forceinline__ bool bwd_pixel_pair(BPix (&pp)[2], int j, float dx, f
   return any;
 }
 
+// The thread's two pixels as packed float32 pairs (lo = upper pixel, hi =
+// lower): the same arithmetic as bwd_pixel_pair with every per-pixel add / mul
+// / fma issued once as an f32x2 instruction (each lane IEEE round-to-nearest,
+// so the DA q is still bit-identical to the forward's); the replay is
+// issue-bound, so this removes ~20 issue slots per (warp, entry).
+struct BPix2 {
+  f2_t T, B, gr, gg, gb, gd, gs;
+  int last0, last1;
+};
+
+__device__ __forceinline__ bool bwd_pair_packed(BPix2 &P, int j, float dx, f2_t DY,
+                                                const float4 &r0, const float4 &r1,
+                                                const float4 &r2, float amax, float (&v)[kV]) {
+  const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
+  const f2_t Y = mul2(mul2(pk2(r1.x, r1.x), DY), DY);  // DMUL(DMUL(cc, dy), dy)
+  const f2_t X = fma2(pk2(cbdx, cbdx), DY, Y);         // DFMA(cbdx, dy, .)
+  const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx), X); // DFMA(cadx, dx, .)
+  const float q0 = lo2(Q), q1 = hi2(Q);
+  const bool val0 = (j < P.last0) & (q0 >= 0.0f) & (q0 <= r1.z);
+  const bool val1 = (j < P.last1) & (q1 >= 0.0f) & (q1 <= r1.z);
+  const f2_t QE = mul2(Q, pk2(-0.72134752f, -0.72134752f));  // exp(-q/2) as in the forward
+  const f2_t G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
+  const f2_t AR = mul2(pk2(r1.y, r1.y), G);
+  const float ar0 = lo2(AR), ar1 = hi2(AR);
+  const f2_t AL = pk2(val0 ? fminf(amax, ar0) : 0.0f, val1 ? fminf(amax, ar1) : 0.0f);
+  const f2_t OM = sub2(pk2(1.0f, 1.0f), AL);
+  float rc0, rc1;  // alpha <= alpha_max < 1 (R1)
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc1) : "f"(hi2(OM)));
+  const f2_t TJ = mul2(P.T, pk2(rc0, rc1));
+  const f2_t W = mul2(AL, TJ);
+  const f2_t VV = fma2(pk2(r2.x, r2.x), P.gr,
+                       fma2(pk2(r2.y, r2.y), P.gg,
+                            fma2(pk2(r2.z, r2.z), P.gb, fma2(pk2(r1.w, r1.w), P.gd, P.gs))));
+  const f2_t D0 = mul2(TJ, sub2(VV, P.B));
+  // R23: no gradient through a capped alpha
+  const f2_t DL = pk2((val0 & (ar0 < amax)) ? lo2(D0) : 0.0f, (val1 & (ar1 < amax)) ? hi2(D0) : 0.0f);
+  const f2_t AV = mul2(AL, DL);
+  const f2_t GD = mul2(G, DL);
+  P.B = fma2(AL, VV, mul2(OM, P.B));
+  P.T = TJ;
+  const f2_t TT = mul2(AV, DY);   // a dy
+  const f2_t T2 = mul2(TT, DY);   // a dy^2
+  const f2_t WD = mul2(W, P.gd), WR = mul2(W, P.gr), WG = mul2(W, P.gg), WB = mul2(W, P.gb);
+  const float sx = dx * (lo2(AV) + hi2(AV));
+  const float sy = lo2(TT) + hi2(TT);
+  v[0] = sx;
+  v[1] = sy;
+  v[2] = dx * sx;
+  v[3] = dx * sy;
+  v[4] = lo2(T2) + hi2(T2);
+  v[5] = lo2(GD) + hi2(GD);
+  v[6] = lo2(WD) + hi2(WD);
+  v[7] = lo2(WR) + hi2(WR);
+  v[8] = lo2(WG) + hi2(WG);
+  v[9] = lo2(WB) + hi2(WB);
+  return val0 | val1;
+}
+
 __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, const float *__restrict__ t_final,
@@ -219,6 +278,14 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
 
   // ---- pixel warps
   const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
+#ifndef CSPLAT_BWD_SCALAR
+  BPix2 P;
+  P.T = pk2(pp[0].T, pp[1].T); P.B = pk2(pp[0].B, pp[1].B);
+  P.gr = pk2(pp[0].gr, pp[1].gr); P.gg = pk2(pp[0].gg, pp[1].gg); P.gb = pk2(pp[0].gb, pp[1].gb);
+  P.gd = pk2(pp[0].gd, pp[1].gd); P.gs = pk2(pp[0].gs, pp[1].gs);
+  P.last0 = pp[0].last; P.last1 = pp[1].last;
+  const f2_t FPY = pk2(fpy0, fpy1);
+#endif
   float(*red)[8 * 4] = reinterpret_cast<float(*)[8 * 4]>(sm.red[wid]);  // [kG*kV][32]
   for (int k = 0; k < nb; k++) {
     const int s = k % kBS;
@@ -255,20 +322,25 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
       };
       int nq = 0;
       uint32_t ents = 0;
-      for (int i = 0; i < cnt; i++) {  // back to front
-        const int e = cnt - 1 - i;
+      // the batch's entries this warp replays, one ballot: lane l tests entry l's
+      // block mask (payload word 14, bin.cu) and replay range (j < wmax)
+      const uint32_t bml = lane < cnt ? __float_as_uint(rb[lane * 4 + 3].z) : 0u;
+      uint32_t todo = __ballot_sync(0xffffffffu, ((bml >> wid) & 1u) && b * kBB + lane < wmax);
+      while (todo) {  // back to front
+        const int e = 31 - __clz(todo);
+        todo ^= 1u << e;
         const int j = b * kBB + e;
-        const uint32_t bm = __float_as_uint(rb[e * 4 + 3].z);
-        // warp-uniform: the pair's block mask (payload word 14, bin.cu) keeps this
-        // warp's 8x8 block and the entry is inside some lane's replay range
-        if (!((bm >> wid) & 1u) || j >= wmax) continue;
         const float4 r0 = rb[e * 4 + 0];
         const float4 r1 = rb[e * 4 + 1];
         const float4 r2 = rb[e * 4 + 2];
         float v[kV];
         const float dx = DSUB(fpx, r0.x);
+#ifdef CSPLAT_BWD_SCALAR
         const bool a = bwd_pixel_pair(pp, j, dx, DSUB(fpy0, r0.y), DSUB(fpy1, r0.y), r0, r1, r2,
                                       amax, v);
+#else
+        const bool a = bwd_pair_packed(P, j, dx, sub2(FPY, pk2(r0.y, r0.y)), r0, r1, r2, amax, v);
+#endif
         if (!__any_sync(0xffffffffu, a)) continue;
         // every lane writes its (possibly zero) partials as row nq*kV + c
 #pragma unroll

@@ -152,18 +152,23 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
     if (!wdone) {
       const float4 *rb = buf[s];
       const int cnt = min(kBatch, len - b * kBatch);
-#pragma unroll 2
-      for (int e = 0; e < cnt; e++) {
-        const float4 r3 = rb[e * 4 + 3];
+      // the batch's entries this warp composites, one ballot: lane l tests entry
+      // l's 8x8-block mask (payload word 14, bin.cu; the rectangle for PPT != 2)
+      bool mine = false;
+      if (lane < cnt) {
+        const float4 r3 = rb[lane * 4 + 3];
         if (PPT == 2) {
-          // warp-level cull: the pair's 8x8-block mask (payload word 14, bin.cu)
-          if (!((__float_as_uint(r3.z) >> wid) & 1u)) continue;
+          mine = (__float_as_uint(r3.z) >> wid) & 1u;
         } else {
-          // record rectangle [lo, hi] vs the warp's block
           const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
           const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
-          if ((t1 & t2 & 0x80008000u) != 0x80008000u) continue;
+          mine = (t1 & t2 & 0x80008000u) == 0x80008000u;
         }
+      }
+      uint32_t todo = __ballot_sync(0xffffffffu, mine);
+      while (todo) {  // front to back
+        const int e = __ffs(todo) - 1;
+        todo &= todo - 1u;
         const float4 r0 = rb[e * 4 + 0];  // u, v, ca, cb+cb
         const float4 r1 = rb[e * 4 + 1];  // cc, o_hat, k2, z
         const float dx = DSUB(fpx, r0.x);

@@ -18,26 +18,6 @@ namespace csplat {
 
 constexpr int kRvqThreads = 256;
 
-typedef unsigned long long f2_t;  // two packed float32 lanes (lo = vector a, hi = vector b)
-
-__device__ __forceinline__ f2_t pk2(float a, float b) {
-  f2_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float lo2(f2_t v) { return __uint_as_float((uint32_t)v); }
-__device__ __forceinline__ float hi2(f2_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
-__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) {
-  f2_t r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
-  f2_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-
 // Merge partial argmins over the S-lane group: (d, k) lexicographic minimum.
 template <int S>
 __device__ __forceinline__ void group_argmin(float &d, int &k) {

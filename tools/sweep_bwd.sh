@@ -1,0 +1,6 @@
+# A/B the bwd variants built by tools/variants.py (names as arguments)
+for v in "$@"; do
+  CSPLAT_LIB=variants/$v.so timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --no-e2e --no-tracking > gpurun_out/sw_$v.json 2>gpurun_out/sw_$v.err
+  python -c "
+import json,sys;d=json.load(open('gpurun_out/sw_$v.json'));print('$v', round(d['value'],1), {k:round(v*1000,1) for k,v in d['stage_ms'].items()})"
+done
