@@ -272,7 +272,11 @@ __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len
     const uint4 *src = rec4 + (int64_t)gid * 4;
     const uint4 v0 = src[0], v1 = src[1], v2 = src[2];
     uint4 v3 = src[3];
+#ifdef CSPLAT_BIN_NOMASK  // timing attribution only
+    v3.z = 0xfu;
+#else
     v3.z = block_mask(v0, v1, v3, X0, Y0);
+#endif
     uint4 *dst = pair_rec + pos * 4;
     dst[0] = v0; dst[1] = v1; dst[2] = v2; dst[3] = v3;
   }
@@ -297,7 +301,14 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   }
   for (int k = threadIdx.x; k < len; k += kSortThreads) sk[k] = keys[start + k];
   __syncthreads();
+#ifdef CSPLAT_BIN_NOSORT  // timing attribution only (wrong order)
+  if (len < 0) {
+  } else if (1) {
+    __syncthreads();
+  } else if (len <= 32) {
+#else
   if (len <= 32) {  // one warp sorts a short list; the others only help emit
+#endif
     if (threadIdx.x < 32) bitonic_sort(sk, len, threadIdx.x, 32, [] { __syncwarp(); });
     __syncthreads();
   } else {

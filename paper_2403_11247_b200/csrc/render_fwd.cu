@@ -71,6 +71,37 @@ __device__ __forceinline__ void composite_pred(PixState &p, bool h, float q, flo
   p.done |= (h & stop) ? 1 : 0;
 }
 
+// composite_pred for the thread's two pixels on packed f32x2 instructions
+// (FMUL2/FFMA2/FADD2: each lane IEEE round-to-nearest, the same values as the
+// scalar form); the compositing is issue-bound, so one slot does both pixels.
+__device__ __forceinline__ void composite_pair(PixState &p0, PixState &p1, bool h0, bool h1,
+                                               float q0, float q1, float oh, float z,
+                                               const float4 &rgb, float amax, float tmin,
+                                               int idx) {
+  const f2_t QE = mul2(pk2(q0, q1), pk2(-0.72134752f, -0.72134752f));  // exp(-q/2)
+  const f2_t AR = mul2(pk2(oh, oh), pk2(ex2_approx(lo2(QE)), ex2_approx(hi2(QE))));
+  const f2_t AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));
+  const f2_t T = pk2(p0.T, p1.T);
+  const f2_t TEST = mul2(T, sub2(pk2(1.0f, 1.0f), AL));
+  const bool stop0 = lo2(TEST) < tmin, stop1 = hi2(TEST) < tmin;  // R3
+  const bool take0 = h0 & !stop0, take1 = h1 & !stop1;
+  const f2_t WA = mul2(AL, T);
+  const f2_t W = pk2(take0 ? lo2(WA) : 0.0f, take1 ? hi2(WA) : 0.0f);
+  const f2_t R = fma2(pk2(rgb.x, rgb.x), W, pk2(p0.r, p1.r));  // Eq 3
+  const f2_t G = fma2(pk2(rgb.y, rgb.y), W, pk2(p0.g, p1.g));
+  const f2_t B = fma2(pk2(rgb.z, rgb.z), W, pk2(p0.b, p1.b));
+  const f2_t D = fma2(pk2(z, z), W, pk2(p0.D, p1.D));          // Eq 4 (R8)
+  const f2_t S = add2(pk2(p0.S, p1.S), W);                     // Eq 5 (R9)
+  p0.r = lo2(R); p1.r = hi2(R); p0.g = lo2(G); p1.g = hi2(G); p0.b = lo2(B); p1.b = hi2(B);
+  p0.D = lo2(D); p1.D = hi2(D); p0.S = lo2(S); p1.S = hi2(S);
+  p0.T = take0 ? lo2(TEST) : p0.T;
+  p1.T = take1 ? hi2(TEST) : p1.T;
+  p0.last = take0 ? idx : p0.last;
+  p1.last = take1 ? idx : p1.last;
+  p0.done |= (h0 & stop0) ? 1 : 0;
+  p1.done |= (h1 & stop1) ? 1 : 0;
+}
+
 // PPT = pixels per thread (a column of PPT vertically adjacent pixels): a pixel
 // warp owns an 8 x (4 PPT) block, 256/PPT pixel threads one 16x16 tile, plus
 // one producer warp.  The producer streams the tile's batches into the ring
@@ -176,16 +207,35 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
         float q[PPT];
         bool h[PPT];
         bool anyh = false;
+#ifndef CSPLAT_FWD_SCALAR
+        if constexpr (PPT == 2) {  // the DA q of both pixels on f32x2 (same roundings)
+          const f2_t DY = sub2(pk2((float)py0, (float)(py0 + 1)), pk2(r0.y, r0.y));
+          const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx),
+                              fma2(pk2(cbdx, cbdx), DY, mul2(mul2(pk2(r1.x, r1.x), DY), DY)));
+          q[0] = lo2(Q);
+          q[1] = hi2(Q);
+        }
+#endif
 #pragma unroll
         for (int k = 0; k < PPT; k++) {
-          const float dy = DSUB((float)(py0 + k), r0.y);
-          q[k] = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
+#ifndef CSPLAT_FWD_SCALAR
+          if constexpr (PPT != 2)
+#endif
+          {
+            const float dy = DSUB((float)(py0 + k), r0.y);
+            q[k] = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
+          }
           h[k] = (p[k].done == 0) & (q[k] >= 0.0f) & (q[k] <= r1.z);  // R2 (DA)
           anyh |= h[k];
         }
         if (!anyh) continue;
         const float4 r2 = rb[e * 4 + 2];  // r, g, b, gid
         const int idx = b * kBatch + e + 1;
+#ifndef CSPLAT_FWD_SCALAR
+        if constexpr (PPT == 2)
+          composite_pair(p[0], p[1], h[0], h[1], q[0], q[1], r1.y, r1.w, r2, amax, tmin, idx);
+        else
+#endif
         // the pixels as straight-line (predicated) code so their chains interleave
 #pragma unroll
         for (int k = 0; k < PPT; k++)
