@@ -3,47 +3,56 @@
 //
 // The (tile, depth) key sort is done as an MSD radix step on the tile digit
 // followed by a per-tile sort of the low digits:
-//   1. count:   warp-cooperative expansion of every Gaussian's tile rectangle
+//   1. bucket:  warp-cooperative expansion of every Gaussian's tile rectangle
 //               (a warp scans 32 counts and spreads the pairs over its lanes,
-//               so one big rectangle does not serialise a lane), one atomic
-//               increment of the tile's bucket per pair;
-//   2. scan:    exclusive scan of the T bucket sizes -> tile_range [start, end);
-//   3. scatter: the same expansion writes key = bits(z_c) << 32 | index into the
-//               tile's bucket (slot from an atomic cursor; order fixed in 4);
-//   4. sort:    one warp per tile sorts its bucket in shared memory (bitonic
-//               network, all-ascending form, so no padding is needed), then
+//               so one big rectangle does not serialise a lane); each pair's
+//               key = bits(z_c) << 32 | index goes into its tile's fixed-size
+//               bucket (slot from the tile's atomic cursor, order fixed in 3),
+//               or, once the bucket is full, into one shared overflow list;
+//   2. scan:    exclusive scan of the T cursor values -> tile_range [start, end);
+//   3. sort:    one CTA per tile gathers its bucket (+ its overflow entries),
+//               sorts it in shared memory (bitonic network, all-ascending form,
+//               no padding; warp-local stages synchronise only the warp), then
 //               writes pair_gid and the pair-ordered 64-byte record payload
 //               that the renderer streams with TMA bulk copies (word 14 of the
-//               payload: the pair's 8x8-block cull mask, block_mask below).  Buckets longer
-//               than a warp's shared-memory slice go to a CTA-wide pass.
+//               payload: the pair's 8x8-block cull mask, block_mask below).
+//               Buckets longer than the CTA's shared-memory slice are sorted in
+//               global memory (pathological inputs only).
 // Keys are unique (the index is in the low word), so the order is unique and
 // bit-exact: (tile, bits(z_c), index) ascending.
 #include "common.cuh"
 
 namespace csplat {
 
-constexpr int kCtaCap = 2048;         // keys per tile sorted by k_sort_tiles (16 KB smem)
-constexpr int kSortThreads = 128;     // threads per tile in k_sort_tiles
-constexpr int kLongSmemKeys = 12288;  // 96 KB: CTA-wide shared-memory sort limit
+constexpr int kCtaCap = 2048;      // keys per tile sorted in shared memory (16 KB)
+constexpr int kSortThreads = 128;  // threads per tile in k_sort_tiles
+constexpr int kBucketCap = 512;    // bucket slots per tile; later pairs go to the overflow list
 
 struct BinWs {
-  uint32_t *cnt, *cur, *long_list, *long_count;
-  unsigned long long *keys;
+  uint32_t *cur;                     // [T] pairs per tile (atomic cursor)
+  uint32_t *ovf_n;                   // overflow-list length
+  unsigned long long *bucket;        // [T][kBucketCap] keys
+  uint32_t *ovf_tile;                // [cap] tile of each overflow entry
+  unsigned long long *ovf_key;       // [cap] its key
+  unsigned long long *keys;          // [cap] global-memory sort scratch (tiles > kCtaCap)
 };
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 static BinWs carve(void *ws, int64_t cap, int64_t T) {
   char *p = static_cast<char *>(ws);
+  const size_t c = (size_t)(cap > 0 ? cap : 1);
   BinWs w;
-  w.cnt = reinterpret_cast<uint32_t *>(p);
-  p += align_up(T * 4);
   w.cur = reinterpret_cast<uint32_t *>(p);
   p += align_up(T * 4);
-  w.long_count = reinterpret_cast<uint32_t *>(p);
+  w.ovf_n = reinterpret_cast<uint32_t *>(p);
   p += align_up(4);
-  w.long_list = reinterpret_cast<uint32_t *>(p);
-  p += align_up(T * 4);
+  w.bucket = reinterpret_cast<unsigned long long *>(p);
+  p += align_up((size_t)T * kBucketCap * 8);
+  w.ovf_tile = reinterpret_cast<uint32_t *>(p);
+  p += align_up(c * 4);
+  w.ovf_key = reinterpret_cast<unsigned long long *>(p);
+  p += align_up(c * 8);
   w.keys = reinterpret_cast<unsigned long long *>(p);
   return w;
 }
@@ -52,7 +61,9 @@ size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam) {
   (void)n;
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
-  return 4 * align_up(T * 4) + align_up(4) + align_up((size_t)(cap > 0 ? cap : 1) * 8);
+  const size_t c = (size_t)(cap > 0 ? cap : 1);
+  return align_up(T * 4) + align_up(4) + align_up((size_t)T * kBucketCap * 8) + align_up(c * 4) +
+         2 * align_up(c * 8);
 }
 
 // Warp-cooperative expansion of 32 Gaussians' tile rectangles.  Calls
@@ -108,14 +119,27 @@ __device__ __forceinline__ void expand_warp(int64_t base, int64_t n, const int32
   }
 }
 
-__global__ void __launch_bounds__(256) k_count(int64_t n, const int32_t *__restrict__ count,
-                                               const uint4 *__restrict__ rec4, int tiles_x,
-                                               uint32_t *__restrict__ cnt) {
+// a4: every (Gaussian, tile) pair's key into the tile's bucket, or the
+// overflow list once the bucket holds kBucketCap keys.
+__global__ void __launch_bounds__(256) k_bucket(int64_t n, const int32_t *__restrict__ count,
+                                                const uint4 *__restrict__ rec4, int tiles_x,
+                                                int64_t cap, BinWs w) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = warp; w * 32 < n; w += nwarps)
-    expand_warp(w * 32, n, count, rec4, tiles_x,
-                [&](uint32_t, int tile, uint32_t) { atomicAdd(cnt + tile, 1u); });
+  for (int64_t i = warp; i * 32 < n; i += nwarps)
+    expand_warp(i * 32, n, count, rec4, tiles_x, [&](uint32_t gid, int tile, uint32_t zb) {
+      const unsigned long long key = ((unsigned long long)zb << 32) | (unsigned long long)gid;
+      const uint32_t slot = atomicAdd(w.cur + tile, 1u);
+      if (slot < (uint32_t)kBucketCap) {
+        w.bucket[(int64_t)tile * kBucketCap + slot] = key;
+      } else {
+        const uint32_t o = atomicAdd(w.ovf_n, 1u);
+        if ((int64_t)o < cap) {  // beyond cap the pairs exceed the capacity anyway
+          w.ovf_tile[o] = (uint32_t)tile;
+          w.ovf_key[o] = key;
+        }
+      }
+    });
 }
 
 // Single-CTA exclusive scan of the T bucket sizes (T is small: 3225 at 1200x680).
@@ -162,31 +186,23 @@ __global__ void __launch_bounds__(1024) k_scan(int64_t T, const uint32_t *__rest
   if (tid == 0) *n_pairs = (int64_t)carry;
 }
 
-__global__ void __launch_bounds__(256) k_scatter(int64_t n, const int32_t *__restrict__ count,
-                                                 const uint4 *__restrict__ rec4, int tiles_x,
-                                                 const uint32_t *__restrict__ range,
-                                                 uint32_t *__restrict__ cur,
-                                                 unsigned long long *__restrict__ keys) {
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = warp; w * 32 < n; w += nwarps)
-    expand_warp(w * 32, n, count, rec4, tiles_x, [&](uint32_t gid, int tile, uint32_t zb) {
-      const uint32_t slot = atomicAdd(cur + tile, 1u);
-      const uint32_t pos = range[2 * tile] + slot;
-      if (pos < range[2 * tile + 1])
-        keys[pos] = ((unsigned long long)zb << 32) | (unsigned long long)gid;
-    });
-}
-
 // All-ascending bitonic network over a[0..len) (virtual +inf padding), executed
-// by `nthr` cooperating threads with index `tid`; `sync` separates stages.
+// by `nthr` (a multiple of 32) cooperating threads with index `tid`.  Pair t of
+// a stage whose compare-exchange blocks span B <= 64 elements stays inside the
+// 64 elements [64 (t / 32), +64), which belong to t's warp in every such stage,
+// so consecutive stages with B <= 64 only synchronise the warp; `cta_sync`
+// separates the others (and ends the sort).
 template <typename Sync>
 __device__ __forceinline__ void bitonic_sort(unsigned long long *a, int len, int tid, int nthr,
-                                             Sync sync) {
+                                             Sync cta_sync) {
   int np2 = 1;
   while (np2 < len) np2 <<= 1;
   // index of the lower element of pair t in a block of 2j (j a power of two)
   auto lower = [](int t, int j) { return ((t & ~(j - 1)) << 1) | (t & (j - 1)); };
+  auto sync = [&](int b, int b_next) {
+    if (b <= 64 && b_next <= 64) __syncwarp();
+    else cta_sync();
+  };
   for (int k = 2; k <= np2; k <<= 1) {
     const int half = k >> 1;
     for (int t = tid; t < np2 / 2; t += nthr) {
@@ -197,7 +213,7 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long *a, int len, int
         if (y < x) { a[i] = y; a[p] = x; }
       }
     }
-    sync();
+    sync(k, half >= 2 ? half : 2 * k);
     for (int j = half >> 1; j > 0; j >>= 1) {
       for (int t = tid; t < np2 / 2; t += nthr) {
         const int i = lower(t, j);
@@ -207,9 +223,10 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long *a, int len, int
           if (y < x) { a[i] = y; a[p] = x; }
         }
       }
-      sync();
+      sync(2 * j, j >= 2 ? j : 2 * k);
     }
   }
+  cta_sync();
 }
 
 // Cull hint for the renderers: bit w (w = 0..3, x half = w & 1, y half = w >> 1)
@@ -283,67 +300,45 @@ __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len
 }
 
 // One 128-thread CTA per tile: enough warps in flight to hide the latency of
-// the record gathers in emit_sorted (one warp per tile left SMs at ~30%
-// occupancy: there are only ~3k tiles per view).
+// the record gathers in emit_sorted (there are only ~3k tiles per view).
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
-    int64_t T, const uint32_t *__restrict__ range, const unsigned long long *__restrict__ keys,
-    const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid, uint4 *__restrict__ pair_rec,
-    uint32_t *__restrict__ long_list, uint32_t *__restrict__ long_count, int tiles_x) {
+    const uint32_t *__restrict__ range, BinWs w, int64_t cap, const uint4 *__restrict__ rec4,
+    uint32_t *__restrict__ pair_gid, uint4 *__restrict__ pair_rec, int tiles_x) {
   __shared__ unsigned long long sk[kCtaCap];
+  __shared__ uint32_t fill;
   const int64_t tile = blockIdx.x;
   const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
-  const int len = (int)(end - start);
+  const int len = (int)(end - start);  // < the tile's pair count only beyond the capacity
   if (len == 0) return;
-  if (len > kCtaCap) {
-    if (threadIdx.x == 0) long_list[atomicAdd(long_count, 1u)] = (uint32_t)tile;
-    return;
+  unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
+  const int nb = min(len, kBucketCap);
+  const unsigned long long *bk = w.bucket + tile * kBucketCap;
+  for (int k = threadIdx.x; k < nb; k += kSortThreads) a[k] = bk[k];
+  if (len > kBucketCap) {  // the rest of the tile's keys are in the overflow list
+    if (threadIdx.x == 0) fill = kBucketCap;
+    // placeholders (Gaussian 0, sorted last) for keys lost beyond the capacity
+    for (int k = kBucketCap + threadIdx.x; k < len; k += kSortThreads) a[k] = ~0ull << 32;
+    __syncthreads();
+    const int64_t no = min((int64_t)*w.ovf_n, cap);
+    for (int64_t o = threadIdx.x; o < no; o += kSortThreads)
+      if (w.ovf_tile[o] == (uint32_t)tile) {
+        const uint32_t pos = atomicAdd(&fill, 1u);
+        if (pos < (uint32_t)len) a[pos] = w.ovf_key[o];
+      }
   }
-  for (int k = threadIdx.x; k < len; k += kSortThreads) sk[k] = keys[start + k];
   __syncthreads();
 #ifdef CSPLAT_BIN_NOSORT  // timing attribution only (wrong order)
   if (len < 0) {
-  } else if (1) {
-    __syncthreads();
-  } else if (len <= 32) {
 #else
   if (len <= 32) {  // one warp sorts a short list; the others only help emit
 #endif
-    if (threadIdx.x < 32) bitonic_sort(sk, len, threadIdx.x, 32, [] { __syncwarp(); });
+    if (threadIdx.x < 32) bitonic_sort(a, len, threadIdx.x, 32, [] { __syncwarp(); });
     __syncthreads();
   } else {
-    bitonic_sort(sk, len, threadIdx.x, kSortThreads, [] { __syncthreads(); });
+    bitonic_sort(a, len, threadIdx.x, kSortThreads, [] { __syncthreads(); });
   }
-  emit_sorted(sk, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, pair_rec, X0, Y0);
-}
-
-__global__ void __launch_bounds__(1024) k_sort_long(const uint32_t *__restrict__ range,
-                                                    unsigned long long *__restrict__ keys,
-                                                    const uint4 *__restrict__ rec4,
-                                                    uint32_t *__restrict__ pair_gid,
-                                                    uint4 *__restrict__ pair_rec,
-                                                    const uint32_t *__restrict__ long_list,
-                                                    const uint32_t *__restrict__ long_count,
-                                                    int tiles_x) {
-  extern __shared__ unsigned long long lk[];
-  const uint32_t nl = *long_count;
-  for (uint32_t li = blockIdx.x; li < nl; li += gridDim.x) {
-    const uint32_t tile = long_list[li];
-    const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
-    const int len = (int)(end - start);
-    unsigned long long *a = keys + start;
-    const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
-    if (len <= kLongSmemKeys) {
-      for (int k = threadIdx.x; k < len; k += blockDim.x) lk[k] = a[k];
-      __syncthreads();
-      bitonic_sort(lk, len, threadIdx.x, blockDim.x, [] { __syncthreads(); });
-      emit_sorted(lk, len, start, threadIdx.x, blockDim.x, rec4, pair_gid, pair_rec, X0, Y0);
-    } else {  // slow path for pathological buckets: same network in global memory
-      bitonic_sort(a, len, threadIdx.x, blockDim.x, [] { __syncthreads(); });
-      emit_sorted(a, len, start, threadIdx.x, blockDim.x, rec4, pair_gid, pair_rec, X0, Y0);
-    }
-    __syncthreads();
-  }
+  emit_sorted(a, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, pair_rec, X0, Y0);
 }
 
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
@@ -352,8 +347,8 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
   BinWs w = carve(ws, cap, T);
-  // cnt, cur, long_count are contiguous at the head of the workspace
-  cudaError_t e = cudaMemsetAsync(w.cnt, 0, 2 * align_up(T * 4) + align_up(4), s);
+  // cur and ovf_n are contiguous at the head of the workspace
+  cudaError_t e = cudaMemsetAsync(w.cur, 0, align_up(T * 4) + align_up(4), s);
   if (e != cudaSuccess) return e;
   const uint4 *rec4 = static_cast<const uint4 *>(rec);
   int dev = 0, sms = 148;
@@ -364,24 +359,10 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   const int64_t max_blocks = (int64_t)sms * 8;
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  if (n > 0) k_count<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, w.cnt);
-  k_scan<<<1, 1024, 0, s>>>(T, w.cnt, cap, tile_range, n_pairs_dev);
-  if (n > 0)
-    k_scatter<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, tile_range, w.cur,
-                                               w.keys);
-  k_sort_tiles<<<(unsigned)T, kSortThreads, 0, s>>>(
-      T, tile_range, w.keys, rec4, pair_gid, static_cast<uint4 *>(pair_rec), w.long_list,
-      w.long_count, ci.tiles_x);
-  const size_t lsm = kLongSmemKeys * sizeof(unsigned long long);
-  static bool attr_done = false;
-  if (!attr_done) {
-    e = cudaFuncSetAttribute(k_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
-  k_sort_long<<<(unsigned)sms, 1024, lsm, s>>>(tile_range, w.keys, rec4, pair_gid,
-                                               static_cast<uint4 *>(pair_rec), w.long_list,
-                                               w.long_count, ci.tiles_x);
+  if (n > 0) k_bucket<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, cap, w);
+  k_scan<<<1, 1024, 0, s>>>(T, w.cur, cap, tile_range, n_pairs_dev);
+  k_sort_tiles<<<(unsigned)T, kSortThreads, 0, s>>>(tile_range, w, cap, rec4, pair_gid,
+                                                    static_cast<uint4 *>(pair_rec), ci.tiles_x);
   return cudaGetLastError();
 }
 
