@@ -302,6 +302,40 @@ def tracking_loss(color, depth, sil, obs_color, obs_depth, lambda_d=1.0, gate=0.
     return (dC, dD, dS), loss, flags
 
 
+def ba_patch_loss(color, depth, obs_color, obs_depth, patches, n_rays, n_valid, lambda_d=1.0,
+                  lambda_s=0.2, c1=0.01 ** 2, c2=0.03 ** 2):
+    """NEXT-4 (reading R30): one keyframe's share of the patch BA loss.
+    Returns (dC, dD, dS) upstream gradients and loss3 = its parts of
+    (L_c, L_d, mean SSIM); L_ba = L_c + lambda_d L_d + lambda_s (1 - SSIM)."""
+    color = np.ascontiguousarray(color, dtype=np.float64)
+    depth = np.ascontiguousarray(depth, dtype=np.float64)
+    oc = _f32(obs_color)
+    od = _f32(obs_depth)
+    pt = np.ascontiguousarray(patches, dtype=np.int32)
+    H, W = depth.shape
+    dC = np.zeros_like(color); dD = np.zeros_like(depth); dS = np.zeros_like(depth)
+    loss = np.zeros(3)
+    rc = lib().oracle_ba_patch_loss(_p(color), _p(depth), _p(oc), _p(od), C.c_int32(W),
+                                    C.c_int32(H), _p(pt), C.c_int64(pt.shape[0]),
+                                    C.c_int64(n_rays), C.c_int64(n_valid), C.c_double(lambda_d),
+                                    C.c_double(lambda_s), C.c_double(c1), C.c_double(c2),
+                                    _p(dC), _p(dD), _p(dS), _p(loss))
+    assert rc == 0
+    return (dC, dD, dS), loss
+
+
+def ba_count_valid(obs_depths, patches_per_kf, width):
+    """|R| of Eq 12 over the sampled rays: patch pixels with a valid observed depth."""
+    bw = width // 8
+    n = 0
+    for od, pt in zip(obs_depths, patches_per_kf):
+        od = np.asarray(od, dtype=np.float32)
+        for b in np.asarray(pt).ravel():
+            by, bx = divmod(int(b), bw)
+            n += int((od[8 * by:8 * by + 8, 8 * bx:8 * bx + 8] > 0).sum())
+    return n
+
+
 def mask_loss(mask, active, lam=1.0):
     """NEXT-3: Eq 8 over the active (in-frustum) Gaussians -> (L_m, d_mask)."""
     mask = _f32(mask)

@@ -140,6 +140,16 @@ int oracle_tracking_loss(const double *color, const double *depth, const double 
                          int32_t height, double lambda_d, double gate, double *d_color,
                          double *d_depth, double *d_sil, double *loss3, uint8_t *flags);
 
+/* NEXT-4: random-ray (8x8 patch) global BA loss of one keyframe (
+ * reading R30): adds its share of (L_c, L_d, mean SSIM) to loss3 and writes
+ * the upstream gradients on the patch pixels (zero elsewhere). */
+int oracle_ba_patch_loss(const double *color, const double *depth, const float *obs_color,
+                         const float *obs_depth, int32_t width, int32_t height,
+                         const int32_t *patches, int64_t n_patches, int64_t n_rays,
+                         int64_t n_valid, double lambda_d, double lambda_s, double c1,
+                         double c2, double *d_color, double *d_depth, double *d_sil,
+                         double *loss3);
+
 /* Restrict oracle_render_fwd/bwd to pixel rows [row_lo, row_hi) (row_hi < 0:
  * all rows) -- used only to time a bounded CPU-baseline sample. */
 void oracle_set_row_window(int32_t row_lo, int32_t row_hi);

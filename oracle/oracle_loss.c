@@ -106,3 +106,86 @@ int oracle_tracking_loss(const double *color, const double *depth, const double 
     loss3[0] = loss3[1] + lambda_d * loss3[2];
     return 0;
 }
+
+/* NEXT-4: the loss of the random-ray global bundle adjustment (Sec 3.4 "Global
+ * Bundle Adjustment": "randomly sample a total number of N rays from
+ * our global keyframe database ... a loss similar to tracking loss, and we also
+ * add an SSIM loss to RGB rendering").  Reading R30: the N rays are
+ * drawn as N/64 random 8x8 pixel patches (block-aligned), so that the SSIM
+ * term has a window; no silhouette gate.  Over the whole sample:
+ *   L_c    = (1/N) sum_rays sum_c (C - C_obs)^2                     (Eq 12)
+ *   L_d    = (1/|R|) sum_{rays, D_obs > 0} (D - D_obs)^2             (Eq 12)
+ *   SSIM_b = mean over the patches b and channels c of
+ *            (2 mx my + C1)(2 sxy + C2) / ((mx^2 + my^2 + C1)(sx^2 + sy^2 + C2)),
+ *            m, s^2, sxy the patch mean, (population) variance, covariance
+ *   L_ba   = L_c + lambda_d L_d + lambda_s (1 - SSIM_b)
+ * This call handles the patches of ONE keyframe and ADDS its share:
+ *   loss3[0] += its part of L_c, loss3[1] += of L_d, loss3[2] += of SSIM_b,
+ * with the sample-wide normalisers n_rays (= N) and n_valid (= |R|) given.
+ * Gradients (written on the patch pixels, zero elsewhere):
+ *   dL/dC_i = 2 (C_i - C_obs_i)/N - lambda_s/(3P) dSSIM_c/dC_i,  P = N/64,
+ *   dSSIM/dx_i = (2S/64) [my/A1 + (y_i - my)/A2 - mx/B1 - (x_i - mx)/B2]
+ *   (A1, A2, B1, B2 the four factors above), dL/dD_i = 2 lambda_d v_i (D - D_obs)/|R|,
+ *   dL/dS = 0.  patches[b] = by * (W/8) + bx (block origin (8 bx, 8 by)). */
+int oracle_ba_patch_loss(const double *color, const double *depth, const float *obs_color,
+                         const float *obs_depth, int32_t width, int32_t height,
+                         const int32_t *patches, int64_t n_patches, int64_t n_rays,
+                         int64_t n_valid, double lambda_d, double lambda_s, double c1,
+                         double c2, double *d_color, double *d_depth, double *d_sil,
+                         double *loss3)
+{
+    const int64_t HW = (int64_t)width * height;
+    const int bw = width / 8;
+    const double N = (double)n_rays, R = (double)(n_valid > 0 ? n_valid : 1);
+    const double P = N / 64.0;
+    for (int64_t p = 0; p < HW; p++) {
+        d_depth[p] = 0.0;
+        d_sil[p] = 0.0;
+        for (int c = 0; c < 3; c++) d_color[c * HW + p] = 0.0;
+    }
+    for (int64_t b = 0; b < n_patches; b++) {
+        const int bx = patches[b] % bw, by = patches[b] / bw;
+        int64_t pix[64];
+        for (int k = 0; k < 64; k++) pix[k] = (int64_t)(8 * by + k / 8) * width + 8 * bx + k % 8;
+        for (int k = 0; k < 64; k++) {  /* Eq 12 depth term */
+            const int64_t p = pix[k];
+            if (obs_depth[p] > 0.0f) {
+                const double r = depth[p] - (double)obs_depth[p];
+                loss3[1] += r * r / R;
+                d_depth[p] = 2.0 * lambda_d * r / R;
+            }
+        }
+        for (int c = 0; c < 3; c++) {
+            const double *x = color + c * HW;
+            const float *y = obs_color + c * HW;
+            double mx = 0.0, my = 0.0;
+            for (int k = 0; k < 64; k++) { mx += x[pix[k]]; my += (double)y[pix[k]]; }
+            mx /= 64.0;
+            my /= 64.0;
+            double sxx = 0.0, syy = 0.0, sxy = 0.0;
+            for (int k = 0; k < 64; k++) {
+                const double dx = x[pix[k]] - mx, dy = (double)y[pix[k]] - my;
+                sxx += dx * dx;
+                syy += dy * dy;
+                sxy += dx * dy;
+            }
+            sxx /= 64.0;
+            syy /= 64.0;
+            sxy /= 64.0;
+            const double A1 = 2.0 * mx * my + c1, A2 = 2.0 * sxy + c2;
+            const double B1 = mx * mx + my * my + c1, B2 = sxx + syy + c2;
+            const double S = A1 * A2 / (B1 * B2);
+            loss3[2] += S / (3.0 * P);
+            for (int k = 0; k < 64; k++) {
+                const int64_t p = pix[k];
+                const double xi = x[p], yi = (double)y[p];
+                const double dS = 2.0 * S / 64.0 *
+                                  (my / A1 + (yi - my) / A2 - mx / B1 - (xi - mx) / B2);
+                const double r = xi - yi;
+                loss3[0] += r * r / N;
+                d_color[c * HW + p] = 2.0 * r / N - lambda_s / (3.0 * P) * dS;
+            }
+        }
+    }
+    return 0;
+}

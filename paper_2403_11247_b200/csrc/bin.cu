@@ -278,24 +278,88 @@ __device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1,
   return m;
 }
 
+// Pair `pos` of the sorted order: its Gaussian index and the pair-ordered
+// record payload with the pair's block cull mask in word 14.
+__device__ __forceinline__ void emit_pair(unsigned long long key, int64_t pos,
+                                          const uint4 *__restrict__ rec4,
+                                          uint32_t *__restrict__ pair_gid,
+                                          uint4 *__restrict__ pair_rec, int X0, int Y0) {
+  const uint32_t gid = (uint32_t)(key & 0xffffffffull);
+  pair_gid[pos] = gid;
+  const uint4 *src = rec4 + (int64_t)gid * 4;
+  const uint4 v0 = src[0], v1 = src[1], v2 = src[2];
+  uint4 v3 = src[3];
+#ifdef CSPLAT_BIN_NOMASK  // timing attribution only
+  v3.z = 0xfu;
+#else
+  v3.z = block_mask(v0, v1, v3, X0, Y0);
+#endif
+  uint4 *dst = pair_rec + pos * 4;
+  dst[0] = v0; dst[1] = v1; dst[2] = v2; dst[3] = v3;
+}
+
 __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len, uint32_t start,
                                             int tid, int nthr, const uint4 *__restrict__ rec4,
                                             uint32_t *__restrict__ pair_gid,
                                             uint4 *__restrict__ pair_rec, int X0, int Y0) {
-  for (int k = tid; k < len; k += nthr) {
-    const uint32_t gid = (uint32_t)(a[k] & 0xffffffffull);
-    const int64_t pos = (int64_t)start + k;
-    pair_gid[pos] = gid;
-    const uint4 *src = rec4 + (int64_t)gid * 4;
-    const uint4 v0 = src[0], v1 = src[1], v2 = src[2];
-    uint4 v3 = src[3];
-#ifdef CSPLAT_BIN_NOMASK  // timing attribution only
-    v3.z = 0xfu;
-#else
-    v3.z = block_mask(v0, v1, v3, X0, Y0);
-#endif
-    uint4 *dst = pair_rec + pos * 4;
-    dst[0] = v0; dst[1] = v1; dst[2] = v2; dst[3] = v3;
+  for (int k = tid; k < len; k += nthr) emit_pair(a[k], (int64_t)start + k, rec4, pair_gid,
+                                                  pair_rec, X0, Y0);
+}
+
+// Register-resident bitonic sort of up to 2 * kSortThreads = 256 keys: thread t
+// holds elements 2t (x0) and 2t+1 (x1); missing elements are +inf (~0, above
+// every key: bits(z_c) of a finite depth is below 0x7f800000).  Same
+// all-ascending network as bitonic_sort, run for blocks up to np2: the
+// compare-exchange partner is in the same thread (distance 1), in lane
+// t ^ (distance / 2) of the same warp (shuffles), or in another warp (one
+// double-buffered shared-memory exchange and one CTA barrier per stage; three
+// such stages at np2 = 256).
+__device__ __forceinline__ void cx2(unsigned long long &x, unsigned long long p, bool keep_min) {
+  x = keep_min ? (p < x ? p : x) : (p < x ? x : p);
+}
+
+__device__ __forceinline__ void sort_regs256(unsigned long long &x0, unsigned long long &x1,
+                                             int np2, unsigned long long (*xb)[2 * kSortThreads]) {
+  const int t = threadIdx.x;
+  int buf = 0;
+  // partner values of (x0, x1) from thread t ^ m; `swap` = the partner's elements
+  // in reverse order (the mirror stage pairs element 2t with 2(t^m)+1)
+  auto fetch = [&](int m, bool swap, unsigned long long &p0, unsigned long long &p1) {
+    if (m < 32) {
+      const unsigned long long a = __shfl_xor_sync(0xffffffffu, x0, m);
+      const unsigned long long b = __shfl_xor_sync(0xffffffffu, x1, m);
+      p0 = swap ? b : a;
+      p1 = swap ? a : b;
+    } else {
+      xb[buf][2 * t] = x0;
+      xb[buf][2 * t + 1] = x1;
+      __syncthreads();
+      const int u = t ^ m;
+      p0 = xb[buf][2 * u + (swap ? 1 : 0)];
+      p1 = xb[buf][2 * u + (swap ? 0 : 1)];
+      buf ^= 1;
+    }
+  };
+  for (int k = 2; k <= np2; k <<= 1) {
+    unsigned long long p0, p1;
+    if (k == 2) {  // mirror of the pair (2t, 2t+1): in-thread
+      p0 = x1; x1 = x0 < x1 ? x1 : x0; x0 = p0 < x0 ? p0 : x0;
+    } else {       // mirror stage: element e pairs with e ^ (k - 1)
+      fetch((k - 1) >> 1, true, p0, p1);
+      const bool lower = ((2 * t) & (k >> 1)) == 0;
+      cx2(x0, p0, lower);
+      cx2(x1, p1, lower);
+    }
+    for (int j = k >> 2; j >= 1; j >>= 1) {  // element e pairs with e ^ j
+      if (j == 1) {
+        p0 = x1; x1 = x0 < x1 ? x1 : x0; x0 = p0 < x0 ? p0 : x0;
+      } else {
+        fetch(j >> 1, false, p0, p1);
+        const bool lower = ((2 * t) & j) == 0;
+        cx2(x0, p0, lower);
+        cx2(x1, p1, lower);
+      }
+    }
   }
 }
 
@@ -304,13 +368,33 @@ __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     const uint32_t *__restrict__ range, BinWs w, int64_t cap, const uint4 *__restrict__ rec4,
     uint32_t *__restrict__ pair_gid, uint4 *__restrict__ pair_rec, int tiles_x) {
-  __shared__ unsigned long long sk[kCtaCap];
+  __shared__ __align__(16) unsigned long long sk[kCtaCap];
   __shared__ uint32_t fill;
   const int64_t tile = blockIdx.x;
   const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
   const int len = (int)(end - start);  // < the tile's pair count only beyond the capacity
   if (len == 0) return;
+#ifndef CSPLAT_BIN_SMEM_SORT
+  if (len <= 2 * kSortThreads) {  // the common case: the list fits the threads' registers
+    const int t = threadIdx.x;
+    const unsigned long long *bk = w.bucket + tile * kBucketCap;
+    unsigned long long x0 = ~0ull, x1 = ~0ull;
+    if (2 * t + 1 < len) {
+      const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(bk)[t];
+      x0 = v.x;
+      x1 = v.y;
+    } else if (2 * t < len) {
+      x0 = bk[2 * t];
+    }
+    int np2 = 2;
+    while (np2 < len) np2 <<= 1;
+    sort_regs256(x0, x1, np2, reinterpret_cast<unsigned long long(*)[2 * kSortThreads]>(sk));
+    if (2 * t < len) emit_pair(x0, (int64_t)start + 2 * t, rec4, pair_gid, pair_rec, X0, Y0);
+    if (2 * t + 1 < len) emit_pair(x1, (int64_t)start + 2 * t + 1, rec4, pair_gid, pair_rec, X0, Y0);
+    return;
+  }
+#endif
   unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
   const int nb = min(len, kBucketCap);
   const unsigned long long *bk = w.bucket + tile * kBucketCap;
@@ -328,11 +412,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
       }
   }
   __syncthreads();
-#ifdef CSPLAT_BIN_NOSORT  // timing attribution only (wrong order)
-  if (len < 0) {
-#else
   if (len <= 32) {  // one warp sorts a short list; the others only help emit
-#endif
     if (threadIdx.x < 32) bitonic_sort(a, len, threadIdx.x, 32, [] { __syncwarp(); });
     __syncthreads();
   } else {
