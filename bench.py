@@ -245,6 +245,50 @@ def bench_next_rows(step, sc, view, dev, flush, reps=20):
     return out
 
 
+def bench_ba(dev, n_rays=65536, iters=5):
+    """NEXT-4: one random-ray global-BA iteration (reading R30) over
+    the C5 keyframe database (64 Replica-shaped keyframes x 500k Gaussians,
+    R-VQ 4x256): n_rays rays as n_rays/64 random 8x8 patches; per keyframe
+    project -> active-tile bin -> fwd -> patch loss (Eq 12 + SSIM) -> bwd
+    ACCUMULATE.  Observed images: renders of the map at the keyframe views
+    (synthetic).  Device time per iteration (CUDA events, median)."""
+    import torch
+    from paper_2403_11247_b200 import csplat as cs
+    from paper_2403_11247_b200.ba import ba_loss_value, gpu_ba
+    from paper_2403_11247_b200.pipeline import RenderStep
+    from scenes import synth
+    sc = synth.window_scene(0)
+    st = RenderStep(sc.planes(), sc.cam, sc.codebook, device=dev)
+    st.size_pairs(sc.views[0], views=sc.views[1::8])
+    st.prepare()
+    oc, od = [], []
+    for v in sc.views:  # observations: the map rendered at the keyframe views
+        st.project_bin(v)
+        st.forward()
+        oc.append(st.img["color"].clone())
+        od.append(st.img["depth"].clone())
+    patches = synth.sample_patches(1, len(sc.views), sc.cam["width"], sc.cam["height"], n_rays)
+    ba = gpu_ba(st, sc.views, oc, od, patches, rank=0, world=1)
+    stream = torch.cuda.current_stream(dev)
+    ba.run()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ba.run()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    return {"workload": "C5 DB: 64 keyframes x 500k Gaussians, R-VQ 4x256, "
+                        f"{ba.n_rays} rays as {ba.n_rays // 64} random 8x8 patches",
+            "ms_per_iter": ms, "rays_per_s": ba.n_rays / (ms * 1e-3),
+            "n_valid": int(ba.n_valid.item()), "loss": ba_loss_value(ba.loss3),
+            "pairs_last_kf": int(st.n_pairs.item()),
+            "note": "includes the per-keyframe host loop (no graph capture)"}
+
+
 # ---------------------------------------------------------------- oracle (CPU) legs
 
 def oracle_step(sc, view, upstream, row_frac=1.0, rvq_frac=1.0):
@@ -551,6 +595,7 @@ def main():
     next_rows = None
     if rank == 0 and not args.no_tracking:
         next_rows = bench_next_rows(step, sc, view, dev, flush)
+        next_rows["global_ba"] = bench_ba(dev)
 
     if rank == 0:
         n_kept = int(step.n_kept.item())

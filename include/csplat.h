@@ -138,6 +138,17 @@ int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csp
                      uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
                      size_t ws_bytes, void *stream);
 
+/* csplat_bin_tiles restricted to the tiles whose bit is set in tile_active
+ * (device uint32[ceil(T/32)], bit t & 31 of word t >> 5; NULL = every tile):
+ * the pairs of the other tiles are not emitted and their ranges are empty, so
+ * the output is csplat_bin_tiles' with those tiles' lists removed.  NEXT-4 uses
+ * it to bin only the tiles that hold sampled rays (csplat_ba_patches). */
+int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
+                            const csplat_camera *cam, const uint32_t *tile_active,
+                            int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                            uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
+                            size_t ws_bytes, void *stream);
+
 /* a6: front-to-back compositing of colour, depth and silhouette (Eq 3-5,
  * P:98-109; R1-R3, R7-R10).  Outputs color [3][H][W], depth, silhouette,
  * t_final [H][W] float32 and n_contrib [H][W] int32 (local index + 1 of the
@@ -235,6 +246,39 @@ int csplat_mask_loss(const csplat_gaussians *g, const int32_t *count, float lamb
 int csplat_keyframe_overlap(const float *depth, const csplat_camera *cam, const csplat_view *cur,
                             const csplat_view *views, int32_t K, int64_t *counts_dev, void *ws,
                             size_t ws_bytes, void *stream);
+
+/* NEXT-4: random-ray global bundle adjustment (Sec 3.4; reading
+ * R30).  The N rays sampled from the keyframe database are N/64 random 8x8
+ * pixel patches aligned to the 8-pixel grid; patches[b] = by * (W/8) + bx
+ * names the block with origin (8 bx, 8 by) of one keyframe (device int32;
+ * ids outside the image's whole blocks are ignored).
+ *
+ * csplat_ba_patches: for the patches of one keyframe, clears and sets its
+ * active-tile mask (device uint32[ceil(T/32)], for csplat_bin_tiles_active)
+ * and ADDS the patch pixels with a valid observed depth (obs_depth > 0, the
+ * set R of Eq 12) to *n_valid_dev (device uint64; the caller zeroes it once
+ * per sample and sums it over the keyframes, and over ranks). */
+int csplat_ba_patches(const float *obs_depth, const csplat_camera *cam, const int32_t *patches,
+                      int64_t n_patches, uint32_t *tile_active, uint64_t *n_valid_dev,
+                      void *stream);
+
+/* csplat_ba_patch_loss: one keyframe's share of the BA objective over the
+ * whole sample (N = n_rays rays, |R| = *n_valid_dev, P = N/64 patches):
+ *   L_c  = (1/N) sum_rays sum_c (C - C_obs)^2,  L_d = (1/|R|) sum_R (D - D_obs)^2  (Eq 12)
+ *   SSIM = mean over patches and channels of the 8x8-window SSIM
+ *          (2 mx my + C1)(2 sxy + C2) / ((mx^2 + my^2 + C1)(sx^2 + sy^2 + C2)),
+ *          population moments, C1 = 0.01^2, C2 = 0.03^2
+ *   L_ba = L_c + lambda_depth L_d + lambda_ssim (1 - SSIM)      (no silhouette gate)
+ * Writes the upstream gradients of csplat_render_bwd on the whole image
+ * (d_color [3][H][W], d_depth, d_silhouette [H][W]; zero off the patches)
+ * and ADDS its shares of (L_c, L_d, SSIM) to loss3_dev[0..2] (device float;
+ * the caller zeroes it per sample).  Inputs: the rendered color / depth of
+ * csplat_render_fwd and the observed images, all device float32. */
+int csplat_ba_patch_loss(const float *color, const float *depth, const float *obs_color,
+                         const float *obs_depth, const csplat_camera *cam, const int32_t *patches,
+                         int64_t n_patches, int64_t n_rays, const uint64_t *n_valid_dev,
+                         float lambda_depth, float lambda_ssim, float *d_color, float *d_depth,
+                         float *d_silhouette, float *loss3_dev, void *stream);
 
 enum csplat_op {
   CSPLAT_OP_BIN_TILES = 1,

@@ -1,0 +1,112 @@
+"""NEXT-4: random-ray global bundle adjustment (Sec 3.4; reading R30).
+
+"We randomly sample a total number of N rays from our global keyframe database
+to optimize our scene representation as well as camera poses.  This phase
+optimizes a loss similar to tracking loss, and we also add an SSIM loss to RGB
+rendering."  The N rays are N/64 random 8x8 patches (the SSIM window), drawn
+over all keyframes (``scenes.synth.sample_patches``).  One BA iteration:
+
+    prepare the map (mask prune + R-VQ assignment, once)
+    per local keyframe:  csplat_ba_patches   -> active-tile mask, |R| share
+    [ranks > 1: SUM all-reduce of the 8-byte |R|: the Eq 12 normaliser is
+     sample-wide]
+    per local keyframe with patches:
+        project -> csplat_bin_tiles_active (only the sampled tiles)
+        -> render_fwd -> csplat_ba_patch_loss -> render_bwd(ACCUMULATE, own pose)
+    [ranks > 1: SUM all-reduce of the flat Gaussian gradient and the loss]
+
+Keyframes are sharded round-robin over ranks exactly as the mapping window
+(``window.shard``); poses stay rank-local.  Every stage is a libcsplat kernel;
+the loop, the sharding and the collectives are host plumbing.  The GPU backend
+is injected as in ``window.WindowStep`` so the gloo tests exercise the
+sharding and the two reductions without a GPU.
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from .window import shard
+
+
+class BAStep:
+    def __init__(self, n_keyframes: int, flat_grad: torch.Tensor, n_valid: torch.Tensor,
+                 loss3: torch.Tensor, count_fn: Callable[[int], None],
+                 render_fn: Callable[[int, torch.Tensor], None],
+                 prepare_fn: Callable[[], None] | None = None, rank: int | None = None,
+                 world: int | None = None, group=None):
+        self.world = world if world is not None else (dist.get_world_size(group)
+                                                      if dist.is_initialized() else 1)
+        self.rank = rank if rank is not None else (dist.get_rank(group)
+                                                   if dist.is_initialized() else 0)
+        self.group = group
+        self.local = shard(n_keyframes, self.rank, self.world)
+        self.flat, self.n_valid, self.loss3 = flat_grad, n_valid, loss3
+        self.count_fn, self.render_fn, self.prepare_fn = count_fn, render_fn, prepare_fn
+        self.poses = {k: torch.zeros(6, dtype=flat_grad.dtype, device=flat_grad.device)
+                      for k in self.local}
+
+    def run(self):
+        """One BA iteration; returns the (all-reduced) flat gradient buffer."""
+        self.flat.zero_()
+        self.n_valid.zero_()
+        self.loss3.zero_()
+        if self.prepare_fn is not None:
+            self.prepare_fn()
+        for k in self.local:
+            self.count_fn(k)
+        if self.world > 1:
+            dist.all_reduce(self.n_valid, op=dist.ReduceOp.SUM, group=self.group)
+        for k in self.local:
+            self.poses[k].zero_()
+            self.render_fn(k, self.poses[k])
+        if self.world > 1:
+            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
+            dist.all_reduce(self.loss3, op=dist.ReduceOp.SUM, group=self.group)
+        return self.flat
+
+
+def ba_loss_value(loss3, lambda_depth=1.0, lambda_ssim=0.2) -> float:
+    """L_ba = L_c + lambda_d L_d + lambda_s (1 - SSIM) from the reduced shares."""
+    l = [float(x) for x in loss3]
+    return l[0] + lambda_depth * l[1] + lambda_ssim * (1.0 - l[2])
+
+
+def gpu_ba(step, views, obs_color, obs_depth, patches, lambda_depth=1.0, lambda_ssim=0.2,
+           rank=None, world=None, group=None):
+    """BAStep over a RenderStep: keyframe k has view `views[k]`, observed images
+    obs_color[k] [3,H,W] / obs_depth[k] [H,W] (device; only local keyframes are
+    read) and patch ids `patches[k]` (int32, see scenes.synth.sample_patches)."""
+    from . import csplat as cs
+
+    dev = step.dev
+    n_rays = 64 * sum(int(len(p)) for p in patches)
+    n_valid = torch.zeros(1, dtype=torch.int64, device=dev)
+    loss3 = torch.zeros(3, dtype=torch.float32, device=dev)
+    up = (torch.empty_like(step.img["color"]), torch.empty_like(step.img["depth"]),
+          torch.empty_like(step.img["sil"]))
+    words = cs.tile_mask_words(step.cam)
+    pt, masks = {}, {}
+
+    def count(k):
+        if k not in pt:
+            pt[k] = torch.as_tensor(patches[k], dtype=torch.int32).to(dev)
+            masks[k] = torch.empty(words, dtype=torch.int32, device=dev)
+        cs.ba_patches(obs_depth[k], step.cam, pt[k], tile_active=masks[k], n_valid=n_valid)
+
+    def render(k, pose):
+        if pt[k].numel() == 0:
+            return
+        step.project_bin(views[k], tile_active=masks[k])
+        step.forward()
+        cs.ba_patch_loss(step.img, obs_color[k], obs_depth[k], step.cam, pt[k], n_rays, n_valid,
+                         lambda_depth, lambda_ssim, out=up, loss3=loss3)
+        step.set_upstream(*up)
+        step.backward(views[k], flags=cs.ACCUMULATE, pose=pose)
+
+    ba = BAStep(len(views), step.grads["flat"], n_valid, loss3, count, render, step.prepare,
+                rank, world, group)
+    ba.n_rays = n_rays
+    return ba

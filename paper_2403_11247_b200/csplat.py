@@ -68,7 +68,8 @@ class Grads(C.Structure):
 
 EXPORTS = ["csplat_project", "csplat_bin_tiles", "csplat_render_fwd", "csplat_render_bwd",
            "csplat_rvq_assign", "csplat_mask_prune", "csplat_tracking_loss", "csplat_rvq_update",
-           "csplat_mask_loss", "csplat_keyframe_overlap",
+           "csplat_mask_loss", "csplat_keyframe_overlap", "csplat_bin_tiles_active",
+           "csplat_ba_patches", "csplat_ba_patch_loss",
            "csplat_workspace_bytes", "csplat_last_error", "csplat_status_string",
            "csplat_version"]
 OP_TRACKING_LOSS = 4
@@ -89,6 +90,11 @@ def lib():
         vp, i64, i32, u32 = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32
         L.csplat_project.argtypes = [vp] * 8
         L.csplat_bin_tiles.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp, vp, u32, vp, C.c_size_t, vp]
+        L.csplat_bin_tiles_active.argtypes = [vp, vp, i64, vp, vp, i64, vp, vp, vp, vp, u32, vp,
+                                              C.c_size_t, vp]
+        L.csplat_ba_patches.argtypes = [vp, vp, vp, i64, vp, vp, vp]
+        L.csplat_ba_patch_loss.argtypes = [vp] * 6 + [i64, i64, vp, C.c_float, C.c_float] + \
+            [vp] * 5
         L.csplat_render_fwd.argtypes = [vp] * 10
         L.csplat_render_bwd.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_rvq_assign.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp]
@@ -213,8 +219,10 @@ def workspace_bytes(op: int, n: int, pairs: int = 0, cam: dict | None = None) ->
     return int(lib().csplat_workspace_bytes(op, n, pairs, _byref(c)))
 
 
-def bin_tiles(rec, count, cam: dict, capacity: int, ws=None, out=None, sync=True, stream=None):
-    """a4+a5.  Returns dict(pair_gid, pair_rec, tile_range, n_pairs_dev[, n_pairs])."""
+def bin_tiles(rec, count, cam: dict, capacity: int, ws=None, out=None, sync=True, stream=None,
+              tile_active=None):
+    """a4+a5.  Returns dict(pair_gid, pair_rec, tile_range, n_pairs_dev[, n_pairs]).
+    tile_active (device int32 bitmask, NEXT-4): bin only those tiles."""
     n = int(count.shape[0])
     dev = rec.device
     tx, ty = tiles(cam)
@@ -226,11 +234,19 @@ def bin_tiles(rec, count, cam: dict, capacity: int, ws=None, out=None, sync=True
     if ws is None:
         ws = torch.empty(workspace_bytes(OP_BIN_TILES, n, capacity, cam), dtype=torch.uint8,
                          device=dev)
-    st = lib().csplat_bin_tiles(_ptr(rec), _ptr(count), n, C.byref(camera(cam)), capacity,
-                                _ptr(out["pair_gid"]), _ptr(out["pair_rec"]),
-                                _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]),
-                                SYNC if sync else 0, _ptr(ws), ws.numel(), _stream(stream))
-    _check(st, "csplat_bin_tiles")
+    if tile_active is None:
+        st = lib().csplat_bin_tiles(_ptr(rec), _ptr(count), n, C.byref(camera(cam)), capacity,
+                                    _ptr(out["pair_gid"]), _ptr(out["pair_rec"]),
+                                    _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]),
+                                    SYNC if sync else 0, _ptr(ws), ws.numel(), _stream(stream))
+        _check(st, "csplat_bin_tiles")
+    else:
+        st = lib().csplat_bin_tiles_active(_ptr(rec), _ptr(count), n, C.byref(camera(cam)),
+                                           _ptr(tile_active), capacity, _ptr(out["pair_gid"]),
+                                           _ptr(out["pair_rec"]), _ptr(out["tile_range"]),
+                                           _ptr(out["n_pairs_dev"]), SYNC if sync else 0,
+                                           _ptr(ws), ws.numel(), _stream(stream))
+        _check(st, "csplat_bin_tiles_active")
     return out
 
 
@@ -310,6 +326,44 @@ def tracking_loss(img: dict, obs_color, obs_depth, lambda_depth=1.0, sil_gate=0.
                                       _ptr(out[0]), _ptr(out[1]), _ptr(out[2]), _ptr(loss3),
                                       _ptr(ws), ws.numel(), _stream(stream)),
            "csplat_tracking_loss")
+    return out, loss3
+
+
+def tile_mask_words(cam: dict) -> int:
+    tx, ty = tiles(cam)
+    return (tx * ty + 31) // 32
+
+
+def ba_patches(obs_depth, cam: dict, patches, tile_active=None, n_valid=None, stream=None):
+    """NEXT-4: one keyframe's active-tile mask (cleared, then set) and its
+    valid-depth rays ADDED to n_valid (device int64[1])."""
+    dev = obs_depth.device
+    if tile_active is None:
+        tile_active = torch.empty(tile_mask_words(cam), dtype=torch.int32, device=dev)
+    if n_valid is None:
+        n_valid = torch.zeros(1, dtype=torch.int64, device=dev)
+    _check(lib().csplat_ba_patches(_ptr(obs_depth), C.byref(camera(cam)), _ptr(patches),
+                                   int(patches.numel()), _ptr(tile_active), _ptr(n_valid),
+                                   _stream(stream)), "csplat_ba_patches")
+    return tile_active, n_valid
+
+
+def ba_patch_loss(img: dict, obs_color, obs_depth, cam: dict, patches, n_rays: int, n_valid,
+                  lambda_depth=1.0, lambda_ssim=0.2, out=None, loss3=None, stream=None):
+    """NEXT-4: upstream grads (d_color, d_depth, d_sil) of one keyframe's patches and
+    its shares of (L_c, L_d, SSIM) ADDED to loss3 (device float32[3])."""
+    color, depth = img["color"], img["depth"]
+    dev = depth.device
+    if out is None:
+        out = (torch.empty_like(color), torch.empty_like(depth), torch.empty_like(depth))
+    if loss3 is None:
+        loss3 = torch.zeros(3, device=dev)
+    _check(lib().csplat_ba_patch_loss(_ptr(color), _ptr(depth), _ptr(obs_color),
+                                      _ptr(obs_depth), C.byref(camera(cam)), _ptr(patches),
+                                      int(patches.numel()), int(n_rays), _ptr(n_valid),
+                                      lambda_depth, lambda_ssim, _ptr(out[0]), _ptr(out[1]),
+                                      _ptr(out[2]), _ptr(loss3), _stream(stream)),
+           "csplat_ba_patch_loss")
     return out, loss3
 
 

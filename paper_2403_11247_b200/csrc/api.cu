@@ -178,8 +178,9 @@ int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const c
                      "csplat_project");
 }
 
-int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csplat_camera *cam,
-                     int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
+                            const csplat_camera *cam, const uint32_t *tile_active,
+                            int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
                      uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
                      size_t ws_bytes, void *stream) {
   RET_IF(check_camera(cam));
@@ -198,7 +199,7 @@ int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csp
   }
   RET_IF(check_device());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  RET_IF(cuda_status(csplat::launch_bin(rec, count, n, *cam, pair_capacity, pair_gid, pair_rec,
+  RET_IF(cuda_status(csplat::launch_bin(rec, count, n, *cam, pair_capacity, tile_active, pair_gid, pair_rec,
                                         tile_range, n_pairs_dev, ws, s),
                      "csplat_bin_tiles"));
   if (flags & CSPLAT_SYNC) {
@@ -213,6 +214,52 @@ int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csp
     }
   }
   return CSPLAT_OK;
+}
+
+int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csplat_camera *cam,
+                     int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                     uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
+                     size_t ws_bytes, void *stream) {
+  return csplat_bin_tiles_active(rec, count, n, cam, nullptr, pair_capacity, pair_gid, pair_rec,
+                                 tile_range, n_pairs_dev, flags, ws, ws_bytes, stream);
+}
+
+int csplat_ba_patches(const float *obs_depth, const csplat_camera *cam, const int32_t *patches,
+                      int64_t n_patches, uint32_t *tile_active, uint64_t *n_valid_dev,
+                      void *stream) {
+  RET_IF(check_camera(cam));
+  if (n_patches < 0) return invalid("n_patches < 0");
+  if (!tile_active || !n_valid_dev || (n_patches > 0 && (!obs_depth || !patches)))
+    return invalid("ba_patches: NULL argument");
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_ba_patches(obs_depth, *cam, patches, n_patches, tile_active,
+                                               reinterpret_cast<unsigned long long *>(n_valid_dev),
+                                               static_cast<cudaStream_t>(stream)),
+                     "csplat_ba_patches");
+}
+
+int csplat_ba_patch_loss(const float *color, const float *depth, const float *obs_color,
+                         const float *obs_depth, const csplat_camera *cam, const int32_t *patches,
+                         int64_t n_patches, int64_t n_rays, const uint64_t *n_valid_dev,
+                         float lambda_depth, float lambda_ssim, float *d_color, float *d_depth,
+                         float *d_silhouette, float *loss3_dev, void *stream) {
+  RET_IF(check_camera(cam));
+  if (n_patches < 0 || n_rays < 64 * n_patches || (n_patches > 0 && n_rays <= 0))
+    return invalid("need 0 <= 64 n_patches <= n_rays");
+  if (!d_color || !d_depth || !d_silhouette)
+    return invalid("ba_patch_loss: NULL gradient output");
+  if (n_patches > 0 && (!color || !depth || !obs_color || !obs_depth || !patches ||
+                        !n_valid_dev || !loss3_dev))
+    return invalid("ba_patch_loss: NULL argument");
+  if (!std::isfinite(lambda_depth) || !std::isfinite(lambda_ssim))
+    return invalid("lambda_depth / lambda_ssim must be finite");
+  RET_IF(check_device());
+  return cuda_status(
+      csplat::launch_ba_loss(color, depth, obs_color, obs_depth, *cam, patches, n_patches,
+                             n_rays, reinterpret_cast<const unsigned long long *>(n_valid_dev),
+                             lambda_depth, lambda_ssim, d_color, d_depth, d_silhouette, loss3_dev,
+                             static_cast<cudaStream_t>(stream)),
+      "csplat_ba_patch_loss");
 }
 
 int csplat_render_fwd(const void *pair_rec, const uint32_t *tile_range, const csplat_camera *cam,

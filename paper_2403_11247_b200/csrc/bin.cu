@@ -120,14 +120,17 @@ __device__ __forceinline__ void expand_warp(int64_t base, int64_t n, const int32
 }
 
 // a4: every (Gaussian, tile) pair's key into the tile's bucket, or the
-// overflow list once the bucket holds kBucketCap keys.
+// overflow list once the bucket holds kBucketCap keys; with an active-tile
+// mask (NEXT-4, csplat_bin_tiles_active) only the pairs of active tiles.
 __global__ void __launch_bounds__(256) k_bucket(int64_t n, const int32_t *__restrict__ count,
                                                 const uint4 *__restrict__ rec4, int tiles_x,
-                                                int64_t cap, BinWs w) {
+                                                int64_t cap, const uint32_t *__restrict__ active,
+                                                BinWs w) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i * 32 < n; i += nwarps)
     expand_warp(i * 32, n, count, rec4, tiles_x, [&](uint32_t gid, int tile, uint32_t zb) {
+      if (active && !((active[tile >> 5] >> (tile & 31)) & 1u)) return;  // tile not sampled
       const unsigned long long key = ((unsigned long long)zb << 32) | (unsigned long long)gid;
       const uint32_t slot = atomicAdd(w.cur + tile, 1u);
       if (slot < (uint32_t)kBucketCap) {
@@ -422,8 +425,9 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
 }
 
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
-                       int64_t cap, uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
-                       int64_t *n_pairs_dev, void *ws, cudaStream_t s) {
+                       int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid,
+                       void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                       cudaStream_t s) {
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
   BinWs w = carve(ws, cap, T);
@@ -439,7 +443,8 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   const int64_t max_blocks = (int64_t)sms * 8;
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  if (n > 0) k_bucket<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, cap, w);
+  if (n > 0) k_bucket<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, cap,
+                                                      tile_active, w);
   k_scan<<<1, 1024, 0, s>>>(T, w.cur, cap, tile_range, n_pairs_dev);
   k_sort_tiles<<<(unsigned)T, kSortThreads, 0, s>>>(tile_range, w, cap, rec4, pair_gid,
                                                     static_cast<uint4 *>(pair_rec), ci.tiles_x);

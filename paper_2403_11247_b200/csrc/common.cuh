@@ -215,8 +215,19 @@ cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
 
 size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam);
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
-                       int64_t cap, uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
-                       int64_t *n_pairs_dev, void *ws, cudaStream_t s);
+                       int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid,
+                       void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                       cudaStream_t s);
+
+cudaError_t launch_ba_patches(const float *obs_depth, const csplat_camera &cam,
+                              const int32_t *patches, int64_t n_patches, uint32_t *tile_active,
+                              unsigned long long *n_valid, cudaStream_t s);
+cudaError_t launch_ba_loss(const float *color, const float *depth, const float *obs_color,
+                           const float *obs_depth, const csplat_camera &cam,
+                           const int32_t *patches, int64_t n_patches, int64_t n_rays,
+                           const unsigned long long *n_valid, float lambda_d, float lambda_s,
+                           float *d_color, float *d_depth, float *d_sil, float *loss3,
+                           cudaStream_t s);
 
 cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,

@@ -137,7 +137,7 @@ class RenderStep:
         self.prepare()
         self.project_bin(view, sync_probe)
 
-    def project_bin(self, view, sync_probe=False):
+    def project_bin(self, view, sync_probe=False, tile_active=None):
         g = self.pruned
         cs.project(g, self.cam, view, self.prm, self.cb, rec=self.rec, count=self.count)
         if sync_probe:
@@ -147,7 +147,7 @@ class RenderStep:
         cs.bin_tiles(self.rec, self.count, self.cam, self.capacity, ws=self.ws_bin,
                      out=dict(pair_gid=self.pair_gid, pair_rec=self.pair_rec,
                               tile_range=self.tile_range, n_pairs_dev=self.n_pairs),
-                     sync=sync_probe)
+                     sync=sync_probe, tile_active=tile_active)
 
     def forward(self):
         cs.render_fwd(self.pair_rec, self.tile_range, self.cam, self.prm, out=self.img)

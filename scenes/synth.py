@@ -281,3 +281,17 @@ def upstream(rng, H, W):
     return (rng.standard_normal((3, H, W)).astype(np.float32),
             rng.standard_normal((H, W)).astype(np.float32),
             rng.standard_normal((H, W)).astype(np.float32))
+
+
+def sample_patches(seed, n_keyframes, width, height, n_rays):
+    """NEXT-4 ray sample (P:212-215, reading R30): n_rays // 64 distinct 8x8
+    blocks drawn uniformly without replacement from all keyframes' whole
+    blocks.  Returns one sorted int32 array of block ids (by * (W//8) + bx)
+    per keyframe.  (The random draw of the method, passed in as an input.)"""
+    bw, bh = width // 8, height // 8
+    per = bw * bh
+    n = min(n_rays // 64, n_keyframes * per)
+    rng = np.random.default_rng(seed)
+    pick = np.sort(rng.choice(n_keyframes * per, size=n, replace=False))
+    kf = pick // per
+    return [np.ascontiguousarray(pick[kf == k] % per, dtype=np.int32) for k in range(n_keyframes)]
