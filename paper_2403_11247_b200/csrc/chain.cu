@@ -35,8 +35,16 @@ __global__ void __launch_bounds__(256) k_chain(
   for (int k = 0; k < 15; k++) g[k] = 0.f;
   bool alive = false;
   if (i < ne) alive = rec4[i * 4 + 1].y != 0.0f;  // o_hat word is 0 iff culled
+  float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
   if (alive) {
-    const float4 a0 = acc4[i * 3 + 0], a1 = acc4[i * 3 + 1], a2 = acc4[i * 3 + 2];
+    a0 = acc4[i * 3 + 0]; a1 = acc4[i * 3 + 1]; a2 = acc4[i * 3 + 2];
+    // no pixel reached this Gaussian: every gradient term is an exact zero
+    // (finite factors times a zero accumulator), so skip the chain -- and,
+    // when accumulating, the writes (sparse views: the NEXT-4 patch BA)
+    alive = (a0.x != 0.f) | (a0.y != 0.f) | (a0.z != 0.f) | (a0.w != 0.f) | (a1.x != 0.f) |
+            (a1.y != 0.f) | (a1.z != 0.f) | (a1.w != 0.f) | (a2.x != 0.f) | (a2.y != 0.f);
+  }
+  if (alive) {
     // k_render_bwd accumulates the raw moments Sx, Sy, Sxx, Sxy, Syy of
     // a = alpha dL/dalpha; map them through the record's DA conic
     // (q = ca dx^2 + (2cb) dx dy + cc dy^2; render_bwd.cu, bwd_pixel_pair)
@@ -209,8 +217,8 @@ __global__ void __launch_bounds__(256) k_chain(
     const float sm = 1.f / (1.f + __expf(-mask[i]));
     g[14] = gM * sm * (1.f - sm);
   }
-  if (!(flags & CSPLAT_POSE_ONLY) && i < n) {
-    const bool accu = (flags & CSPLAT_ACCUMULATE) != 0;
+  const bool accu = (flags & CSPLAT_ACCUMULATE) != 0;
+  if (!(flags & CSPLAT_POSE_ONLY) && i < n && (alive || !accu)) {
     auto put = [&](float *plane, int k, int64_t off) {
       if (!plane) return;
       if (accu) plane[off] += g[k];
