@@ -17,6 +17,9 @@
 namespace csplat {
 
 constexpr int kRvqThreads = 256;
+#ifndef CSPLAT_RVQ_VP
+#define CSPLAT_RVQ_VP 2
+#endif
 
 // Merge partial argmins over the S-lane group: (d, k) lexicographic minimum.
 template <int S>
@@ -45,9 +48,12 @@ __device__ __forceinline__ void block_argmin4(float d0, float d1, float d2, floa
 }
 
 // Chunked variant: group lane `sub` scans the contiguous code range
-// [sub*P/S, (sub+1)*P/S) of every stage (P % (4S) == 0), reading a padded,
+// [sub*P/S, (sub+1)*P/S) of every stage (P % (8S) == 0), reading a padded,
 // bank-conflict-free shared-memory copy of the codebook with 16-byte loads.
-template <int D, int S>
+// Each thread carries VP packed vector PAIRS (2 VP vectors), so every code
+// loaded from shared memory feeds VP FFMA2 chains (register blocking: the scan
+// is bound by shared-memory loads and their latency at VP = 1).
+template <int D, int S, int VP>
 __global__ void __launch_bounds__(kRvqThreads) k_rvq_chunked(
     const float *__restrict__ x, int64_t n, const int64_t *__restrict__ n_dev,
     const float *__restrict__ codes_g, int L, int P, void *__restrict__ idx, int idx_bytes,
@@ -73,117 +79,122 @@ __global__ void __launch_bounds__(kRvqThreads) k_rvq_chunked(
   mbar_wait(&bar, 0);
   const int64_t ne = eff_n(n, n_dev);
   const int sub = threadIdx.x % S;
-  const int64_t ia0 = 2 * (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / S);
-  const bool live = ia0 < ne;
+  // vectors i0 + 2v (lo) and i0 + 2v + 1 (hi) of pair v; groups of S lanes share them
+  const int64_t i0 = 2 * VP * (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / S);
   // only whole warps may leave (group shuffles need a converged warp); this
   // drops the work of the vectors beyond the device-side count n_dev
-  if (__all_sync(0xffffffffu, !live)) return;
-  const int64_t ia = live ? ia0 : 0;
-  const bool has_b = live && ia + 1 < ne;
-  const int64_t ib = has_b ? ia + 1 : ia;
-  float xa[D], xb[D], sa[D], sb[D];
+  if (__all_sync(0xffffffffu, !(i0 < ne))) return;
+  int64_t iv[2 * VP];
+  bool has[2 * VP];
+  float xv[2 * VP][D], sv[2 * VP][D];
 #pragma unroll
-  for (int j = 0; j < D; j++) {
-    xa[j] = x[(int64_t)j * n + ia];
-    xb[j] = x[(int64_t)j * n + ib];
-    sa[j] = sb[j] = 0.0f;
+  for (int u = 0; u < 2 * VP; u++) {
+    has[u] = i0 + u < ne;
+    iv[u] = has[u] ? i0 + u : 0;
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+      xv[u][j] = x[(int64_t)j * n + iv[u]];
+      sv[u][j] = 0.0f;
+    }
   }
+  constexpr int kBlk = 8 / VP;  // codes per block (VP * kBlk accumulators in flight)
   for (int l = 0; l < L; l++) {
-    f2_t r[D];
+    f2_t r[VP][D];
 #pragma unroll
-    for (int j = 0; j < D; j++) r[j] = pk2(DSUB(xa[j], sa[j]), DSUB(xb[j], sb[j]));  // S - S_hat
+    for (int v = 0; v < VP; v++)
+#pragma unroll
+      for (int j = 0; j < D; j++)  // S - S_hat
+        r[v][j] = pk2(DSUB(xv[2 * v][j], sv[2 * v][j]), DSUB(xv[2 * v + 1][j], sv[2 * v + 1][j]));
     const float4 *C4 = reinterpret_cast<const float4 *>(sc + l * lstride + sub * cstride);
     const int kbase = sub * chunk;
-    float da = __int_as_float(0x7f800000), db = da;  // +inf: NaN distances are never taken
-    int blka = 0, blkb = 0;                          // block (of kBlk codes) of the best
-    f2_t acc0 = 0ull;
-    constexpr int kBlk = 8;
-    // distances of the kBlk codes of block i (bit-identical whenever recomputed)
-    auto block_dist = [&](int i, f2_t (&acc)[kBlk]) {
+    float dmin[2 * VP];
+    int blk[2 * VP];
+    f2_t acc0[VP];
+#pragma unroll
+    for (int u = 0; u < 2 * VP; u++) {
+      dmin[u] = __int_as_float(0x7f800000);  // +inf: NaN distances are never taken
+      blk[u] = 0;                            // block (of kBlk codes) of the best
+    }
+    // distances of the kBlk codes of block i for pair v (bit-identical whenever recomputed)
+    auto block_dist = [&](int i, f2_t (&acc)[VP][kBlk]) {
       float cv[kBlk * D];
 #pragma unroll
-      for (int q = 0; q < 2 * D; q++) {  // kBlk * D floats = 2D float4 loads
-        const float4 v = C4[(i * D) / 4 + q];
-        cv[4 * q] = v.x; cv[4 * q + 1] = v.y; cv[4 * q + 2] = v.z; cv[4 * q + 3] = v.w;
+      for (int q = 0; q < kBlk * D / 4; q++) {  // kBlk * D floats as float4 loads
+        const float4 t = C4[(i * D) / 4 + q];
+        cv[4 * q] = t.x; cv[4 * q + 1] = t.y; cv[4 * q + 2] = t.z; cv[4 * q + 3] = t.w;
       }
 #pragma unroll
-      for (int c = 0; c < kBlk; c++) {
-        acc[c] = 0ull;  // (+0, +0): fma(e, e, 0) = e*e exactly
+      for (int c = 0; c < kBlk; c++)
 #pragma unroll
-        for (int j = 0; j < D; j++) {
-          const float cf = cv[c * D + j];
-#ifdef CSPLAT_RVQ_SCALAR
-          // scalar FADD/FFMA on the two halves (same IEEE RN results as the packed ops)
-          const float ea = DSUB(cf, lo2(r[j])), eb = DSUB(cf, hi2(r[j]));
-          acc[c] = pk2(DFMA(ea, ea, lo2(acc[c])), DFMA(eb, eb, hi2(acc[c])));
-#else
-          const f2_t e = sub2(pk2(cf, cf), r[j]);
-          acc[c] = fma2(e, e, acc[c]);
-#endif
+        for (int v = 0; v < VP; v++) {
+          acc[v][c] = 0ull;  // (+0, +0): fma(e, e, 0) = e*e exactly
+#pragma unroll
+          for (int j = 0; j < D; j++) {
+            const float cf = cv[c * D + j];
+            const f2_t e = sub2(pk2(cf, cf), r[v][j]);
+            acc[v][c] = fma2(e, e, acc[v][c]);
+          }
         }
-      }
     };
     // scan: track only the minimum and the block holding its first occurrence
     for (int i = 0; i < chunk; i += kBlk) {
-      f2_t acc[kBlk];
+      f2_t acc[VP][kBlk];
       block_dist(i, acc);
-      if (i == 0) acc0 = acc[0];
-      const float ma = fminf(fminf(fminf(lo2(acc[0]), lo2(acc[1])), fminf(lo2(acc[2]), lo2(acc[3]))),
-                             fminf(fminf(lo2(acc[4]), lo2(acc[5])), fminf(lo2(acc[6]), lo2(acc[7]))));
-      const float mb = fminf(fminf(fminf(hi2(acc[0]), hi2(acc[1])), fminf(hi2(acc[2]), hi2(acc[3]))),
-                             fminf(fminf(hi2(acc[4]), hi2(acc[5])), fminf(hi2(acc[6]), hi2(acc[7]))));
-      blka = ma < da ? i : blka;  // strict: an earlier block keeps a tie
-      blkb = mb < db ? i : blkb;
-      da = fminf(da, ma);
-      db = fminf(db, mb);
-    }
-    // resolve the first code of the winning blocks that attains the minimum
-    int besta = kbase + blka, bestb = kbase + blkb;
-    {
-      f2_t acc[kBlk];
-      block_dist(blka, acc);
 #pragma unroll
-      for (int c = kBlk - 1; c >= 0; c--)
-        if (lo2(acc[c]) == da) besta = kbase + blka + c;
-      block_dist(blkb, acc);
+      for (int v = 0; v < VP; v++) {
+        if (i == 0) acc0[v] = acc[v][0];
+        float ma = lo2(acc[v][0]), mb = hi2(acc[v][0]);
 #pragma unroll
-      for (int c = kBlk - 1; c >= 0; c--)
-        if (hi2(acc[c]) == db) bestb = kbase + blkb + c;
-    }
-    // the sequential scan keeps k = 0 when d_0 is NaN (no later d compares below it)
-    if (sub == 0) {
-      if (lo2(acc0) != lo2(acc0)) { da = -__int_as_float(0x7f800000); besta = 0; }
-      if (hi2(acc0) != hi2(acc0)) { db = -__int_as_float(0x7f800000); bestb = 0; }
-    }
-    group_argmin<S>(da, besta);
-    group_argmin<S>(db, bestb);
-    if (sub == 0 && live) {
-      if (idx_bytes == 1) {
-        uint8_t *o = static_cast<uint8_t *>(idx) + (int64_t)l * n;
-        o[ia] = (uint8_t)besta;
-        if (has_b) o[ib] = (uint8_t)bestb;
-      } else {
-        uint16_t *o = static_cast<uint16_t *>(idx) + (int64_t)l * n;
-        o[ia] = (uint16_t)besta;
-        if (has_b) o[ib] = (uint16_t)bestb;
+        for (int c = 1; c < kBlk; c++) {
+          ma = fminf(ma, lo2(acc[v][c]));
+          mb = fminf(mb, hi2(acc[v][c]));
+        }
+        blk[2 * v] = ma < dmin[2 * v] ? i : blk[2 * v];  // strict: an earlier block keeps a tie
+        blk[2 * v + 1] = mb < dmin[2 * v + 1] ? i : blk[2 * v + 1];
+        dmin[2 * v] = fminf(dmin[2 * v], ma);
+        dmin[2 * v + 1] = fminf(dmin[2 * v + 1], mb);
       }
     }
-    const float *Cl = sc + l * lstride;
-    const int sa_s = besta / chunk, sa_i = besta - sa_s * chunk;
-    const int sb_s = bestb / chunk, sb_i = bestb - sb_s * chunk;
+    // resolve the first code of the winning blocks that attains the minimum
+    int best[2 * VP];
 #pragma unroll
-    for (int j = 0; j < D; j++) {  // S_hat^l in stage order
-      const float ca = Cl[sa_s * cstride + sa_i * D + j], cb = Cl[sb_s * cstride + sb_i * D + j];
-      sa[j] = l == 0 ? ca : DADD(sa[j], ca);
-      sb[j] = l == 0 ? cb : DADD(sb[j], cb);
+    for (int u = 0; u < 2 * VP; u++) {
+      f2_t acc[VP][kBlk];
+      block_dist(blk[u], acc);
+      best[u] = kbase + blk[u];
+#pragma unroll
+      for (int c = kBlk - 1; c >= 0; c--) {
+        const float d = (u & 1) ? hi2(acc[u >> 1][c]) : lo2(acc[u >> 1][c]);
+        if (d == dmin[u]) best[u] = kbase + blk[u] + c;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2 * VP; u++) {
+      // the sequential scan keeps k = 0 when d_0 is NaN (no later d compares below it)
+      if (sub == 0) {
+        const float d0 = (u & 1) ? hi2(acc0[u >> 1]) : lo2(acc0[u >> 1]);
+        if (d0 != d0) { dmin[u] = -__int_as_float(0x7f800000); best[u] = 0; }
+      }
+      group_argmin<S>(dmin[u], best[u]);
+      if (sub == 0 && has[u]) {
+        if (idx_bytes == 1) static_cast<uint8_t *>(idx)[(int64_t)l * n + iv[u]] = (uint8_t)best[u];
+        else static_cast<uint16_t *>(idx)[(int64_t)l * n + iv[u]] = (uint16_t)best[u];
+      }
+      const float *Cl = sc + l * lstride;
+      const int bs = best[u] / chunk, bi = best[u] - bs * chunk;
+#pragma unroll
+      for (int j = 0; j < D; j++) {  // S_hat^l in stage order
+        const float c = Cl[bs * cstride + bi * D + j];
+        sv[u][j] = l == 0 ? c : DADD(sv[u][j], c);
+      }
     }
   }
-  if (recon && sub == 0 && live) {
+  if (recon && sub == 0) {
 #pragma unroll
-    for (int j = 0; j < D; j++) {
-      recon[(int64_t)j * n + ia] = sa[j];
-      if (has_b) recon[(int64_t)j * n + ib] = sb[j];
-    }
+    for (int u = 0; u < 2 * VP; u++)
+      if (has[u])
+#pragma unroll
+        for (int j = 0; j < D; j++) recon[(int64_t)j * n + iv[u]] = sv[u][j];
   }
 }
 
@@ -303,14 +314,15 @@ static cudaError_t run_rvq_d(const float *x, int64_t n, const int64_t *n_dev, co
   if (P % (8 * S) == 0 && chunked_bytes <= 200 * 1024 &&
       (reinterpret_cast<uintptr_t>(codes) & 15u) == 0) {
     if (chunked_bytes > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(k_rvq_chunked<D, S>,
+      cudaError_t e = cudaFuncSetAttribute(k_rvq_chunked<D, S, (D <= 4 ? CSPLAT_RVQ_VP : 1)>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)chunked_bytes);
       if (e != cudaSuccess) return e;
     }
-    const int64_t threads = (n + 1) / 2 * S;
+    constexpr int VP = D <= 4 ? CSPLAT_RVQ_VP : 1;  // vector pairs per thread
+    const int64_t threads = (n + 2 * VP - 1) / (2 * VP) * S;
     const int64_t blocks = (threads + kRvqThreads - 1) / kRvqThreads;
-    k_rvq_chunked<D, S><<<(unsigned)blocks, kRvqThreads, chunked_bytes, s>>>(
+    k_rvq_chunked<D, S, VP><<<(unsigned)blocks, kRvqThreads, chunked_bytes, s>>>(
         x, n, n_dev, codes, L, P, idx, idx_bytes, recon);
     return cudaGetLastError();
   }
