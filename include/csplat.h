@@ -119,6 +119,14 @@ int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const c
                    const csplat_view *view, const csplat_params *prm, void *rec, int32_t *count,
                    void *stream);
 
+/* csplat_project with the world->camera view read from DEVICE memory
+ * (view_dev: 12 floats, row-major [R|t]) when the kernel runs, so a pose
+ * updated on the device by csplat_pose_step is picked up inside a captured
+ * CUDA graph (NEXT-1 tracking).  Otherwise identical to csplat_project. */
+int csplat_project_dv(const csplat_gaussians *g, const csplat_codebook *cb,
+                      const csplat_camera *cam, const float *view_dev, const csplat_params *prm,
+                      void *rec, int32_t *count, void *stream);
+
 /* a4 + a5: tile binning and (tile, depth) ordering (R4, R11).
  * Outputs, for n_pairs = sum(count) pairs:
  *   pair_gid[pair_capacity]   Gaussian index per pair, ordered by (tile, bits(z_c), index)
@@ -171,6 +179,24 @@ int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
                       const float *t_final, const int32_t *n_contrib, const float *d_color,
                       const float *d_depth, const float *d_silhouette, uint32_t flags,
                       const csplat_grads *out, void *ws, size_t ws_bytes, void *stream);
+
+/* csplat_render_bwd with the view in DEVICE memory (see csplat_project_dv). */
+int csplat_render_bwd_dv(const csplat_gaussians *g, const csplat_codebook *cb,
+                         const csplat_camera *cam, const float *view_dev,
+                         const csplat_params *prm, const void *rec, const void *pair_rec,
+                         const uint32_t *tile_range, const float *t_final,
+                         const int32_t *n_contrib, const float *d_color, const float *d_depth,
+                         const float *d_silhouette, uint32_t flags, const csplat_grads *out,
+                         void *ws, size_t ws_bytes, void *stream);
+
+/* NEXT-1: the pose step of a tracking iteration on the device (Sec 3.4,
+ * the pose is optimised by minimising the tracking objective):
+ * view_dev (12 floats, world->camera [R|t]) <- Exp(xi) view_dev with
+ * xi = -(lr_rot * g[0..2], lr_trans * g[3..5]), g = pose_grad_dev (the 6-float
+ * pose gradient of csplat_render_bwd, left perturbation (omega, v), R22);
+ * Exp applied as p' = Rod(omega) p + v, evaluated in float64. */
+int csplat_pose_step(float *view_dev, const float *pose_grad_dev, float lr_rot, float lr_trans,
+                     void *stream);
 
 /* a2: greedy residual VQ assignment (Eq 10; R17): for each of the n
  * d-dimensional vectors x [d][n] and each stage l, idx[l][i] = argmin_k

@@ -69,7 +69,8 @@ class Grads(C.Structure):
 EXPORTS = ["csplat_project", "csplat_bin_tiles", "csplat_render_fwd", "csplat_render_bwd",
            "csplat_rvq_assign", "csplat_mask_prune", "csplat_tracking_loss", "csplat_rvq_update",
            "csplat_mask_loss", "csplat_keyframe_overlap", "csplat_bin_tiles_active",
-           "csplat_ba_patches", "csplat_ba_patch_loss",
+           "csplat_ba_patches", "csplat_ba_patch_loss", "csplat_project_dv",
+           "csplat_render_bwd_dv", "csplat_pose_step",
            "csplat_workspace_bytes", "csplat_last_error", "csplat_status_string",
            "csplat_version"]
 OP_TRACKING_LOSS = 4
@@ -95,6 +96,9 @@ def lib():
         L.csplat_ba_patches.argtypes = [vp, vp, vp, i64, vp, vp, vp]
         L.csplat_ba_patch_loss.argtypes = [vp] * 6 + [i64, i64, vp, C.c_float, C.c_float] + \
             [vp] * 5
+        L.csplat_project_dv.argtypes = [vp] * 8
+        L.csplat_render_bwd_dv.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
+        L.csplat_pose_step.argtypes = [vp, vp, C.c_float, C.c_float, vp]
         L.csplat_render_fwd.argtypes = [vp] * 10
         L.csplat_render_bwd.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_rvq_assign.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp]
@@ -208,10 +212,31 @@ def project(g: GaussianMap, cam: dict, v, prm: Params | None = None, cb: Codeboo
     rec = rec if rec is not None else torch.empty((max(n, 1), 16), dtype=torch.int32, device=dev)
     count = count if count is not None else torch.empty(max(n, 1), dtype=torch.int32, device=dev)
     gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    if _on_device(v):  # the view is read by the kernel (graph-captured pose updates)
+        _check(lib().csplat_project_dv(C.byref(gs), _byref(cbs), C.byref(camera(cam)), _ptr(v),
+                                       C.byref(prm or params()), _ptr(rec), _ptr(count),
+                                       _stream(stream)), "csplat_project_dv")
+        return rec[:n], count[:n]
     _check(lib().csplat_project(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
                                 C.byref(view(v)), C.byref(prm or params()), _ptr(rec),
                                 _ptr(count), _stream(stream)), "csplat_project")
     return rec[:n], count[:n]
+
+
+def _on_device(v) -> bool:
+    if isinstance(v, torch.Tensor) and v.is_cuda:
+        if v.dtype != torch.float32 or v.numel() != 12 or not v.is_contiguous():
+            raise CsplatError("a device view must be a contiguous float32 tensor of 12 values")
+        return True
+    return False
+
+
+def pose_step(view_dev, pose_grad, lr_rot: float, lr_trans: float, stream=None):
+    """NEXT-1: view_dev <- Exp(-(lr_rot g_omega, lr_trans g_v)) view_dev on the device."""
+    _on_device(view_dev)
+    _check(lib().csplat_pose_step(_ptr(view_dev), _ptr(pose_grad), lr_rot, lr_trans,
+                                  _stream(stream)), "csplat_pose_step")
+    return view_dev
 
 
 def workspace_bytes(op: int, n: int, pairs: int = 0, cam: dict | None = None) -> int:
@@ -299,6 +324,14 @@ def render_bwd(g: GaussianMap, cam: dict, v, rec, pair_rec, tile_range, t_final,
     gr = Grads(*[_ptr(grads.get(k)) for k in ("mean", "opacity", "rgb", "log_scale", "quat",
                                                "mask", "pose")])
     gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    if _on_device(v):
+        _check(lib().csplat_render_bwd_dv(C.byref(gs), _byref(cbs), C.byref(camera(cam)), _ptr(v),
+                                          C.byref(prm or params()), _ptr(rec), _ptr(pair_rec),
+                                          _ptr(tile_range), _ptr(t_final), _ptr(n_contrib),
+                                          _ptr(d_color), _ptr(d_depth), _ptr(d_sil), flags,
+                                          C.byref(gr), _ptr(ws), ws.numel(), _stream(stream)),
+               "csplat_render_bwd_dv")
+        return grads
     _check(lib().csplat_render_bwd(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
                                    C.byref(view(v)), C.byref(prm or params()), _ptr(rec),
                                    _ptr(pair_rec), _ptr(tile_range), _ptr(t_final),

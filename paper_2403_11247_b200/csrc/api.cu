@@ -155,13 +155,13 @@ size_t csplat_workspace_bytes(int op, int64_t n, int64_t pairs, const csplat_cam
   }
 }
 
-int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const csplat_camera *cam,
-                   const csplat_view *view, const csplat_params *prm, void *rec, int32_t *count,
-                   void *stream) {
+static int project_impl(const csplat_gaussians *g, const csplat_codebook *cb,
+                        const csplat_camera *cam, const csplat_view *view, const float *view_dev,
+                        const csplat_params *prm, void *rec, int32_t *count, void *stream) {
   RET_IF(check_gaussians(g));
   RET_IF(check_camera(cam));
   RET_IF(check_codebook(cb, true));
-  if (!view || !prm) return invalid("view/params NULL");
+  if ((!view && !view_dev) || !prm) return invalid("view/params NULL");
   if (g->n > 0 && (!rec || !count)) return invalid("rec/count NULL");
   if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
   if (!aligned16(rec)) {
@@ -172,10 +172,24 @@ int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const c
   RET_IF(check_device());
   csplat::DecodeArgs d;
   if (cb) d = decode_args(cb);
-  return cuda_status(csplat::launch_project(*g, cb ? &d : nullptr, *cam, *view,
+  return cuda_status(csplat::launch_project(*g, cb ? &d : nullptr, *cam, view ? *view : csplat_view{}, view_dev,
                                             mask_tau(prm->mask_eps), prm->dilation, rec, count,
                                             static_cast<cudaStream_t>(stream)),
                      "csplat_project");
+}
+
+int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const csplat_camera *cam,
+                   const csplat_view *view, const csplat_params *prm, void *rec, int32_t *count,
+                   void *stream) {
+  if (!view) return invalid("view NULL");
+  return project_impl(g, cb, cam, view, nullptr, prm, rec, count, stream);
+}
+
+int csplat_project_dv(const csplat_gaussians *g, const csplat_codebook *cb,
+                      const csplat_camera *cam, const float *view_dev, const csplat_params *prm,
+                      void *rec, int32_t *count, void *stream) {
+  if (!view_dev) return invalid("view_dev NULL");
+  return project_impl(g, cb, cam, nullptr, view_dev, prm, rec, count, stream);
 }
 
 int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
@@ -279,8 +293,9 @@ int csplat_render_fwd(const void *pair_rec, const uint32_t *tile_range, const cs
                      "csplat_render_fwd");
 }
 
-int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
-                      const csplat_camera *cam, const csplat_view *view, const csplat_params *prm,
+static int render_bwd_impl(const csplat_gaussians *g, const csplat_codebook *cb,
+                      const csplat_camera *cam, const csplat_view *view, const float *view_dev,
+                      const csplat_params *prm,
                       const void *rec, const void *pair_rec, const uint32_t *tile_range,
                       const float *t_final, const int32_t *n_contrib, const float *d_color,
                       const float *d_depth, const float *d_silhouette, uint32_t flags,
@@ -288,7 +303,7 @@ int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
   RET_IF(check_gaussians(g, false));
   RET_IF(check_camera(cam));
   RET_IF(check_codebook(cb, true));
-  if (!view || !prm || !out || !tile_range || !t_final || !n_contrib || !d_color || !d_depth ||
+  if ((!view && !view_dev) || !prm || !out || !tile_range || !t_final || !n_contrib || !d_color || !d_depth ||
       !d_silhouette)
     return invalid("render_bwd: NULL argument");
   if (g->n > 0 && !rec) return invalid("rec NULL");
@@ -304,11 +319,47 @@ int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
   RET_IF(check_device());
   csplat::DecodeArgs d;
   if (cb) d = decode_args(cb);
-  return cuda_status(csplat::launch_render_bwd(*g, cb ? &d : nullptr, *cam, *view, *prm, rec,
+  return cuda_status(csplat::launch_render_bwd(*g, cb ? &d : nullptr, *cam,
+                                               view ? *view : csplat_view{}, view_dev, *prm, rec,
                                                pair_rec, tile_range, t_final, n_contrib, d_color,
                                                d_depth, d_silhouette, flags, *out, ws,
                                                static_cast<cudaStream_t>(stream)),
                      "csplat_render_bwd");
+}
+
+int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
+                      const csplat_camera *cam, const csplat_view *view, const csplat_params *prm,
+                      const void *rec, const void *pair_rec, const uint32_t *tile_range,
+                      const float *t_final, const int32_t *n_contrib, const float *d_color,
+                      const float *d_depth, const float *d_silhouette, uint32_t flags,
+                      const csplat_grads *out, void *ws, size_t ws_bytes, void *stream) {
+  if (!view) return invalid("view NULL");
+  return render_bwd_impl(g, cb, cam, view, nullptr, prm, rec, pair_rec, tile_range, t_final,
+                         n_contrib, d_color, d_depth, d_silhouette, flags, out, ws, ws_bytes,
+                         stream);
+}
+
+int csplat_render_bwd_dv(const csplat_gaussians *g, const csplat_codebook *cb,
+                         const csplat_camera *cam, const float *view_dev,
+                         const csplat_params *prm, const void *rec, const void *pair_rec,
+                         const uint32_t *tile_range, const float *t_final,
+                         const int32_t *n_contrib, const float *d_color, const float *d_depth,
+                         const float *d_silhouette, uint32_t flags, const csplat_grads *out,
+                         void *ws, size_t ws_bytes, void *stream) {
+  if (!view_dev) return invalid("view_dev NULL");
+  return render_bwd_impl(g, cb, cam, nullptr, view_dev, prm, rec, pair_rec, tile_range, t_final,
+                         n_contrib, d_color, d_depth, d_silhouette, flags, out, ws, ws_bytes,
+                         stream);
+}
+
+int csplat_pose_step(float *view_dev, const float *pose_grad_dev, float lr_rot, float lr_trans,
+                     void *stream) {
+  if (!view_dev || !pose_grad_dev) return invalid("pose_step: NULL argument");
+  if (!std::isfinite(lr_rot) || !std::isfinite(lr_trans)) return invalid("lr must be finite");
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_pose_step(view_dev, pose_grad_dev, lr_rot, lr_trans,
+                                              static_cast<cudaStream_t>(stream)),
+                     "csplat_pose_step");
 }
 
 int csplat_tracking_loss(const float *color, const float *depth, const float *silhouette,

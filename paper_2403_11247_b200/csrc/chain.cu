@@ -25,7 +25,15 @@ __global__ void __launch_bounds__(256) k_chain(
     const float *__restrict__ opac, const float *__restrict__ lsc, const float *__restrict__ quat,
     const float *__restrict__ mask, DecodeArgs dec, int use_dec, ChainConst cc,
     const float4 *__restrict__ rec4, const float4 *__restrict__ acc4, uint32_t flags,
-    csplat_grads out) {
+    const float *__restrict__ view_dev, csplat_grads out) {
+  if (view_dev) {  // the view lives in device memory (graph-captured pose updates)
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+#pragma unroll
+      for (int b = 0; b < 3; b++) cc.W[3 * a + b] = __ldg(view_dev + 4 * a + b);
+      cc.t[a] = __ldg(view_dev + 4 * a + 3);
+    }
+  }
   __shared__ float red[8][6];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t ne = eff_n(n, n_dev);
@@ -249,8 +257,9 @@ __global__ void __launch_bounds__(256) k_chain(
 
 cudaError_t launch_chain(const csplat_gaussians &g, const DecodeArgs *dec,
                          const csplat_camera &cam, const csplat_view &view,
-                         const csplat_params &prm, const void *rec, const float *acc,
-                         uint32_t flags, const csplat_grads &out, cudaStream_t s) {
+                         const float *view_dev, const csplat_params &prm, const void *rec,
+                         const float *acc, uint32_t flags, const csplat_grads &out,
+                         cudaStream_t s) {
   ChainConst cc;
   for (int a = 0; a < 3; a++) {
     for (int b = 0; b < 3; b++) cc.W[3 * a + b] = view.m[4 * a + b];
@@ -270,7 +279,8 @@ cudaError_t launch_chain(const csplat_gaussians &g, const DecodeArgs *dec,
   k_chain<<<(unsigned)blocks, 256, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.log_scale, g.quat,
                                            g.mask, d, dec ? 1 : 0, cc,
                                            static_cast<const float4 *>(rec),
-                                           reinterpret_cast<const float4 *>(acc), flags, out);
+                                           reinterpret_cast<const float4 *>(acc), flags, view_dev,
+                                           out);
   return cudaGetLastError();
 }
 

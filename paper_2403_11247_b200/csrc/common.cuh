@@ -210,14 +210,18 @@ struct DecodeArgs {
 };
 
 cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
-                           const csplat_camera &cam, const csplat_view &view, float tau,
-                           float dilation, void *rec, int32_t *count, cudaStream_t s);
+                           const csplat_camera &cam, const csplat_view &view,
+                           const float *view_dev, float tau, float dilation, void *rec,
+                           int32_t *count, cudaStream_t s);
 
 size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam);
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
                        int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid,
                        void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                        cudaStream_t s);
+
+cudaError_t launch_pose_step(float *view_dev, const float *pose_grad, float lr_rot,
+                             float lr_trans, cudaStream_t s);
 
 cudaError_t launch_ba_patches(const float *obs_depth, const csplat_camera &cam,
                               const int32_t *patches, int64_t n_patches, uint32_t *tile_active,
@@ -237,11 +241,12 @@ cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
 size_t bwd_workspace_bytes(int64_t n);
 cudaError_t launch_chain(const csplat_gaussians &g, const DecodeArgs *dec,
                          const csplat_camera &cam, const csplat_view &view,
-                         const csplat_params &prm, const void *rec, const float *acc,
-                         uint32_t flags, const csplat_grads &out, cudaStream_t s);
+                         const float *view_dev, const csplat_params &prm, const void *rec,
+                         const float *acc, uint32_t flags, const csplat_grads &out,
+                         cudaStream_t s);
 cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                               const csplat_camera &cam, const csplat_view &view,
-                              const csplat_params &prm, const void *rec, const void *pair_rec,
+                              const float *view_dev, const csplat_params &prm, const void *rec, const void *pair_rec,
                               const uint32_t *tile_range, const float *t_final,
                               const int32_t *n_contrib, const float *d_color, const float *d_depth,
                               const float *d_sil, uint32_t flags, const csplat_grads &out,

@@ -64,6 +64,49 @@ __global__ void __launch_bounds__(kLossThreads) k_tracking_loss(
   }
 }
 
+// NEXT-1: the device-side pose update of a tracking iteration, so a frame's
+// iterations replay as one CUDA graph without a host round trip: V' = Exp(xi) V
+// with xi = -(lr_rot g_omega, lr_trans g_v), the left perturbation the pose
+// gradient of csplat_render_bwd is taken with (R22): p' = Rod(omega) p + v.
+// One thread, float64 (the host form of tracking.apply_left).
+__global__ void k_pose_step(float *__restrict__ V, const float *__restrict__ g, float lr_rot,
+                            float lr_trans) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double w0 = -(double)lr_rot * g[0], w1 = -(double)lr_rot * g[1],
+               w2 = -(double)lr_rot * g[2];
+  const double th = sqrt(w0 * w0 + w1 * w1 + w2 * w2);
+  const double K[3][3] = {{0, -w2, w1}, {w2, 0, -w0}, {-w1, w0, 0}};
+  double a = 1.0, b = 0.5;  // R = I + a K + b K^2 (Rodrigues); th -> 0: I + K
+  if (th >= 1e-12) {
+    a = sin(th) / th;
+    b = (1.0 - cos(th)) / (th * th);
+  } else {
+    b = 0.0;
+  }
+  double R[3][3];
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) {
+      double k2 = 0.0;
+      for (int k = 0; k < 3; k++) k2 += K[i][k] * K[k][j];
+      R[i][j] = (i == j ? 1.0 : 0.0) + a * K[i][j] + b * k2;
+    }
+  double out[12];
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 4; j++) {
+      double t = 0.0;
+      for (int k = 0; k < 3; k++) t += R[i][k] * (double)V[4 * k + j];
+      if (j == 3) t += -(double)lr_trans * g[3 + i];
+      out[4 * i + j] = t;
+    }
+  for (int k = 0; k < 12; k++) V[k] = (float)out[k];
+}
+
+cudaError_t launch_pose_step(float *view_dev, const float *pose_grad, float lr_rot,
+                             float lr_trans, cudaStream_t s) {
+  k_pose_step<<<1, 32, 0, s>>>(view_dev, pose_grad, lr_rot, lr_trans);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- NEXT-3
 
 __global__ void __launch_bounds__(kLossThreads) k_count_active(int64_t n,

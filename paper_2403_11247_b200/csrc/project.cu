@@ -25,9 +25,13 @@ __global__ void __launch_bounds__(256) k_project(
     const float *__restrict__ opac, const float *__restrict__ rgb,
     const float *__restrict__ lsc, const float *__restrict__ quat,
     const float *__restrict__ mask, DecodeArgs dec, int use_dec, ProjConst pc,
-    float4 *__restrict__ rec, int32_t *__restrict__ count) {
+    const float *__restrict__ view_dev, float4 *__restrict__ rec, int32_t *__restrict__ count) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (view_dev) {  // the view lives in device memory (graph-captured pose updates)
+#pragma unroll
+    for (int k = 0; k < 12; k++) pc.V[k] = __ldg(view_dev + k);
+  }
   const int64_t ne = eff_n(n, n_dev);
   float4 *r = rec + i * 4;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -165,8 +169,9 @@ __global__ void __launch_bounds__(256) k_project(
 }
 
 cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
-                           const csplat_camera &cam, const csplat_view &view, float tau,
-                           float dilation, void *rec, int32_t *count, cudaStream_t s) {
+                           const csplat_camera &cam, const csplat_view &view,
+                           const float *view_dev, float tau, float dilation, void *rec,
+                           int32_t *count, cudaStream_t s) {
   if (g.n == 0) return cudaSuccess;
   ProjConst pc;
   for (int k = 0; k < 12; k++) pc.V[k] = view.m[k];
@@ -191,7 +196,7 @@ cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
   const int64_t blocks = (g.n + threads - 1) / threads;
   k_project<<<(unsigned)blocks, threads, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.rgb,
                                                  g.log_scale, g.quat, g.mask, d, dec ? 1 : 0, pc,
-                                                 reinterpret_cast<float4 *>(rec), count);
+                                                 view_dev, reinterpret_cast<float4 *>(rec), count);
   return cudaGetLastError();
 }
 

@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
 
 cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                               const csplat_camera &cam, const csplat_view &view,
-                              const csplat_params &prm, const void *rec, const void *pair_rec,
+                              const float *view_dev, const csplat_params &prm, const void *rec, const void *pair_rec,
                               const uint32_t *tile_range, const float *t_final,
                               const int32_t *n_contrib, const float *d_color, const float *d_depth,
                               const float *d_sil, uint32_t flags, const csplat_grads &out,
@@ -390,7 +390,7 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                                             n_contrib, d_color, d_depth, d_sil, acc);
   e = cudaGetLastError();
   if (e != cudaSuccess || g.n == 0) return e;
-  return launch_chain(g, dec, cam, view, prm, rec, acc, flags, out, s);
+  return launch_chain(g, dec, cam, view, view_dev, prm, rec, acc, flags, out, s);
 }
 
 }  // namespace csplat

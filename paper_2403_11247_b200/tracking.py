@@ -3,8 +3,14 @@
 One iteration = project -> bin_tiles -> render_fwd -> tracking_loss (Eq 12 gated
 by Eq 14) -> render_bwd(POSE_ONLY) -> a fixed-step descent on the left
 perturbation xi = (omega, v) of the world->camera pose (R22).  Every stage is a
-libcsplat kernel; the 6-float pose update runs on the host (the view is a host
-argument of the ABI), so one iteration has one 32-byte device->host read.
+libcsplat kernel.  Two drivers:
+
+* ``track``: the pose update on the host (one 36-byte device->host read per
+  iteration, the view passed to the ABI by value);
+* ``track_graph``: the view lives in device memory (``csplat_project_dv`` /
+  ``csplat_render_bwd_dv`` read it when they run, ``csplat_pose_step`` updates
+  it), so one iteration is captured once as a CUDA graph and a frame's
+  iterations are graph replays with no host round trip.
 """
 from __future__ import annotations
 
@@ -89,3 +95,43 @@ class Tracker:
             view, loss = self.iteration(view, lr_rot, lr_trans)
             losses.append(loss)
         return view, losses
+
+    # ---- device-resident pose: a frame's iterations as CUDA-graph replays
+    def iteration_dv(self, view_dev, lr_rot, lr_trans):
+        """One iteration with the view in device memory (capturable)."""
+        st = self.step
+        g = st.pruned
+        cs.project(g, st.cam, view_dev, st.prm, st.cb, rec=st.rec, count=st.count)
+        cs.bin_tiles(st.rec, st.count, st.cam, st.capacity, ws=st.ws_bin,
+                     out=dict(pair_gid=st.pair_gid, pair_rec=st.pair_rec,
+                              tile_range=st.tile_range, n_pairs_dev=st.n_pairs), sync=False)
+        st.forward()
+        cs.tracking_loss(st.img, self.obs_color, self.obs_depth, self.lambda_depth,
+                         self.sil_gate, out=self.up, loss3=self.loss3, ws=self.ws)
+        st.set_upstream(*self.up)
+        st.backward(view_dev, flags=cs.POSE_ONLY, pose=self.pose)
+        cs.pose_step(view_dev, self.pose, lr_rot, lr_trans)
+
+    def capture(self, view, lr_rot=1e-4, lr_trans=1e-4):
+        """Capture one device-pose iteration as a CUDA graph (the pair buffers
+        must already be sized: RenderStep.size_pairs)."""
+        dev = self.step.dev
+        self.view_dev = torch.as_tensor(np.asarray(view, dtype=np.float32).reshape(12)).to(dev)
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):  # warm-up outside the capture
+            self.iteration_dv(self.view_dev.clone(), lr_rot, lr_trans)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.iteration_dv(self.view_dev, lr_rot, lr_trans)
+        return self.graph
+
+    def track_graph(self, view, iters=40):
+        """A frame's `iters` iterations as graph replays; returns the final view."""
+        self.view_dev.copy_(torch.as_tensor(np.asarray(view, dtype=np.float32).reshape(12)))
+        for _ in range(iters):
+            self.graph.replay()
+        return self.view_dev.view(3, 4).cpu().numpy()
+

@@ -488,6 +488,66 @@ def test_tracking_iterations_reduce_pose_error(env):
     assert e1[0] < e0[0] and e1[1] < e0[1], (e0, e1)
 
 
+def test_pose_step_matches_host_exp(env):
+    """csplat_pose_step == tracking.apply_left (float64 Rodrigues, then float32)."""
+    torch, cs, dev = env["torch"], env["cs"], env["dev"]
+    from paper_2403_11247_b200.tracking import apply_left
+    rng = np.random.default_rng(8)
+    for scale in (0.0, 1e-14, 1e-3, 0.3):
+        V = synth.perturbed_view(rng, rot_deg=20.0, trans=0.5)
+        g = np.float32(rng.standard_normal(6) * scale)
+        lr_r, lr_t = 0.7, 0.4
+        vd = torch.tensor(V.reshape(12), device=dev)
+        cs.pose_step(vd, torch.tensor(g, device=dev), lr_r, lr_t)
+        want = apply_left(V, np.concatenate([-lr_r * np.float64(g[:3]), -lr_t * np.float64(g[3:])]))
+        assert np.allclose(vd.cpu().numpy().reshape(3, 4), want, rtol=0, atol=2e-7), scale
+
+
+def test_device_view_paths_match_host_view(env):
+    """csplat_project_dv / csplat_render_bwd_dv read the same view from device
+    memory: records bit-identical, gradients equal up to atomic ordering."""
+    torch, cs, dev = env["torch"], env["cs"], env["dev"]
+    sc = synth.mid_scene(3)
+    v = synth.perturbed_view(np.random.default_rng(1), rot_deg=2.0, trans=0.03)
+    vd = torch.tensor(np.float32(v).reshape(12), device=dev)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec_h, cnt_h = cs.project(g, sc.cam, v)
+    rec_d, cnt_d = cs.project(g, sc.cam, vd)
+    assert torch.equal(rec_h, rec_d) and torch.equal(cnt_h, cnt_d)
+    b = cs.bin_tiles(rec_h, cnt_h, sc.cam, capacity=int(cnt_h.sum().item()) + 64)
+    img = cs.render_fwd(b["pair_rec"], b["tile_range"], sc.cam)
+    H, W = sc.cam["height"], sc.cam["width"]
+    up = [torch.tensor(a, device=dev) for a in synth.upstream(np.random.default_rng(2), H, W)]
+    args = (rec_h, b["pair_rec"], b["tile_range"], img["t_final"], img["n_contrib"], *up)
+    gh = cs.render_bwd(g, sc.cam, v, *args)
+    gd = cs.render_bwd(g, sc.cam, vd, *args)
+    for k in ("mean", "quat", "pose"):  # the RED order differs run to run: rounding only
+        assert (gh[k] - gd[k]).norm() <= 1e-5 * gh[k].norm(), k
+
+
+def test_tracking_graph_replays_match_host_loop(env):
+    """A frame's iterations as CUDA-graph replays with the device-resident pose
+    follow the host-loop tracker (same kernels; the pose step in float64 on
+    either side) and reduce the pose error."""
+    torch, cs, dev = env["torch"], env["cs"], env["dev"]
+    from paper_2403_11247_b200.pipeline import RenderStep
+    from paper_2403_11247_b200.tracking import Tracker, pose_error
+    sc = synth.mid_scene(9, n=4000)
+    gt = sc.views[0]
+    obs_c, obs_d = _observed(env, sc, gt)
+    start = synth.perturbed_view(np.random.default_rng(2), rot_deg=1.0, trans=0.02)
+    st = RenderStep(sc.planes(), sc.cam, None, device=dev, flags=cs.POSE_ONLY)
+    st.size_pairs(start, views=[gt])
+    tr = Tracker(st, obs_c, obs_d)
+    v_host, _ = tr.track(start, iters=20, lr_rot=5e-4, lr_trans=5e-4)
+    tr.capture(start, lr_rot=5e-4, lr_trans=5e-4)
+    v_graph = tr.track_graph(start, iters=20)
+    st.check_capacity()
+    assert np.abs(v_graph - v_host).max() < 1e-5, np.abs(v_graph - v_host).max()
+    e0, e1 = pose_error(start, gt), pose_error(v_graph, gt)
+    assert e1[0] < e0[0] and e1[1] < e0[1]
+
+
 # ------------------------------------------------------------------ configs C3, C4, C5
 
 @pytest.mark.slow
