@@ -228,7 +228,14 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
           h[k] = (p[k].done == 0) & (q[k] >= 0.0f) & (q[k] <= r1.z);  // R2 (DA)
           anyh |= h[k];
         }
+#ifdef CSPLAT_FWD_DIVERGENT
         if (!anyh) continue;
+#else
+        // warp-uniform skip: composite_pair / composite_pred are exact no-ops for
+        // pixels whose test failed, so lanes without a hit ride along predicated
+        // (no divergence / reconvergence; the issue slots are the same)
+        if (!__any_sync(0xffffffffu, anyh)) continue;
+#endif
         const float4 r2 = rb[e * 4 + 2];  // r, g, b, gid
         const int idx = b * kBatch + e + 1;
 #ifndef CSPLAT_FWD_SCALAR
