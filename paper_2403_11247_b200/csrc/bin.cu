@@ -9,8 +9,10 @@
 //               key = bits(z_c) << 32 | index goes into its tile's fixed-size
 //               bucket (slot from the tile's atomic cursor, order fixed in 3),
 //               or, once the bucket is full, into one shared overflow list;
-//   2. scan:    exclusive scan of the T cursor values -> tile_range [start, end);
-//   3. sort:    one CTA per tile gathers its bucket (+ its overflow entries),
+//   2. sort:    one CTA per tile finds its output offset (the exclusive scan of
+//               the T cursor values, by a decoupled look-back that never waits:
+//               every tile's count is already final) -> tile_range [start, end),
+//               gathers its bucket (+ its overflow entries),
 //               sorts it in shared memory (bitonic network, all-ascending form,
 //               no padding; warp-local stages synchronise only the warp), then
 //               writes pair_gid and the pair-ordered 64-byte record payload
@@ -31,6 +33,7 @@ constexpr int kBucketCap = 512;    // bucket slots per tile; later pairs go to t
 struct BinWs {
   uint32_t *cur;                     // [T] pairs per tile (atomic cursor)
   uint32_t *ovf_n;                   // overflow-list length
+  unsigned long long *status;        // [T] look-back words of the tile-range scan
   unsigned long long *bucket;        // [T][kBucketCap] keys
   uint32_t *ovf_tile;                // [cap] tile of each overflow entry
   unsigned long long *ovf_key;       // [cap] its key
@@ -47,6 +50,8 @@ static BinWs carve(void *ws, int64_t cap, int64_t T) {
   p += align_up(T * 4);
   w.ovf_n = reinterpret_cast<uint32_t *>(p);
   p += align_up(4);
+  w.status = reinterpret_cast<unsigned long long *>(p);
+  p += align_up(T * 8);
   w.bucket = reinterpret_cast<unsigned long long *>(p);
   p += align_up((size_t)T * kBucketCap * 8);
   w.ovf_tile = reinterpret_cast<uint32_t *>(p);
@@ -62,8 +67,8 @@ size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam) {
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
   const size_t c = (size_t)(cap > 0 ? cap : 1);
-  return align_up(T * 4) + align_up(4) + align_up((size_t)T * kBucketCap * 8) + align_up(c * 4) +
-         2 * align_up(c * 8);
+  return align_up(T * 4) + align_up(4) + align_up(T * 8) + align_up((size_t)T * kBucketCap * 8) +
+         align_up(c * 4) + 2 * align_up(c * 8);
 }
 
 // Warp-cooperative expansion of 32 Gaussians' tile rectangles.  Calls
@@ -145,49 +150,6 @@ __global__ void __launch_bounds__(256) k_bucket(int64_t n, const int32_t *__rest
     });
 }
 
-// Single-CTA exclusive scan of the T bucket sizes (T is small: 3225 at 1200x680).
-__global__ void __launch_bounds__(1024) k_scan(int64_t T, const uint32_t *__restrict__ cnt,
-                                               int64_t cap, uint32_t *__restrict__ range,
-                                               int64_t *__restrict__ n_pairs) {
-  __shared__ unsigned long long warp_tot[32];
-  __shared__ unsigned long long carry;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) carry = 0;
-  __syncthreads();
-  for (int64_t base = 0; base < T; base += 1024) {
-    const int64_t t = base + tid;
-    const unsigned long long c = t < T ? cnt[t] : 0ull;
-    unsigned long long incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    if (lane == 31) warp_tot[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      unsigned long long v = warp_tot[lane], s = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long u = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += u;
-      }
-      warp_tot[lane] = s - v;  // exclusive prefix of warp totals
-    }
-    __syncthreads();
-    const unsigned long long start = carry + warp_tot[wid] + incl - c;
-    if (t < T) {
-      const unsigned long long s0 = start < (unsigned long long)cap ? start : cap;
-      const unsigned long long e0 = start + c < (unsigned long long)cap ? start + c : cap;
-      range[2 * t] = (uint32_t)s0;
-      range[2 * t + 1] = (uint32_t)e0;
-    }
-    __syncthreads();
-    if (tid == 1023) carry = start + c;
-    __syncthreads();
-  }
-  if (tid == 0) *n_pairs = (int64_t)carry;
-}
 
 // All-ascending bitonic network over a[0..len) (virtual +inf padding), executed
 // by `nthr` (a multiple of 32) cooperating threads with index `tid`.  Pair t of
@@ -368,14 +330,53 @@ __device__ __forceinline__ void sort_regs256(unsigned long long &x0, unsigned lo
 
 // One 128-thread CTA per tile: enough warps in flight to hide the latency of
 // the record gathers in emit_sorted (there are only ~3k tiles per view).
+// Tile-range scan status words: bit 63 set = inclusive prefix through the tile
+// published (bits 0-62); the tiles' own counts are the bucket cursors, all known
+// when k_sort_tiles starts, so a tile never waits for a predecessor.
+constexpr unsigned long long kRangeP = 1ull << 63;
+
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
-    const uint32_t *__restrict__ range, BinWs w, int64_t cap, const uint4 *__restrict__ rec4,
-    uint32_t *__restrict__ pair_gid, uint4 *__restrict__ pair_rec, int tiles_x) {
+    int64_t T, uint32_t *__restrict__ range, int64_t *__restrict__ n_pairs, BinWs w,
+    int64_t cap, const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid,
+    uint4 *__restrict__ pair_rec, int tiles_x) {
   __shared__ __align__(16) unsigned long long sk[kCtaCap];
-  __shared__ uint32_t fill;
+  __shared__ uint32_t fill, s_start, s_end;
   const int64_t tile = blockIdx.x;
   const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
-  const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
+  if (threadIdx.x < 32) {  // the tile's output offset: a look-back over the preceding tiles
+    const int lane = threadIdx.x;
+    const unsigned long long cnt = w.cur[tile];
+    unsigned long long prefix = 0;
+    for (int64_t j = tile - 1; j >= 0; j -= 32) {
+      const int64_t jj = j - lane;
+      unsigned long long v = 0;  // before tile 0: an inclusive prefix of 0
+      bool pub = true;
+      if (jj >= 0) {
+        const unsigned long long st = *reinterpret_cast<volatile unsigned long long *>(w.status + jj);
+        pub = (st & kRangeP) != 0;
+        v = pub ? (st & ~kRangeP) : (unsigned long long)w.cur[jj];
+      }
+      const unsigned pm = __ballot_sync(0xffffffffu, pub);
+      const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest published prefix
+      unsigned long long add = lane <= stop ? v : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
+      prefix += add;
+      if (pm) break;
+    }
+    if (lane == 0) {
+      const unsigned long long tot = prefix + cnt;
+      atomicExch(w.status + tile, kRangeP | tot);
+      const unsigned long long c = (unsigned long long)cap;
+      s_start = (uint32_t)(prefix < c ? prefix : c);
+      s_end = (uint32_t)(tot < c ? tot : c);
+      range[2 * tile] = s_start;
+      range[2 * tile + 1] = s_end;
+      if (tile == T - 1) *n_pairs = (int64_t)tot;
+    }
+  }
+  __syncthreads();
+  const uint32_t start = s_start, end = s_end;
   const int len = (int)(end - start);  // < the tile's pair count only beyond the capacity
   if (len == 0) return;
 #ifndef CSPLAT_BIN_SMEM_SORT
@@ -431,8 +432,8 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
   BinWs w = carve(ws, cap, T);
-  // cur and ovf_n are contiguous at the head of the workspace
-  cudaError_t e = cudaMemsetAsync(w.cur, 0, align_up(T * 4) + align_up(4), s);
+  // cur, ovf_n and status are contiguous at the head of the workspace
+  cudaError_t e = cudaMemsetAsync(w.cur, 0, align_up(T * 4) + align_up(4) + align_up(T * 8), s);
   if (e != cudaSuccess) return e;
   const uint4 *rec4 = static_cast<const uint4 *>(rec);
   int dev = 0, sms = 148;
@@ -445,9 +446,9 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   if (blocks < 1) blocks = 1;
   if (n > 0) k_bucket<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, cap,
                                                       tile_active, w);
-  k_scan<<<1, 1024, 0, s>>>(T, w.cur, cap, tile_range, n_pairs_dev);
-  k_sort_tiles<<<(unsigned)T, kSortThreads, 0, s>>>(tile_range, w, cap, rec4, pair_gid,
-                                                    static_cast<uint4 *>(pair_rec), ci.tiles_x);
+  k_sort_tiles<<<(unsigned)T, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap, rec4,
+                                                    pair_gid, static_cast<uint4 *>(pair_rec),
+                                                    ci.tiles_x);
   return cudaGetLastError();
 }
 
