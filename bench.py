@@ -36,7 +36,7 @@ METRIC = "fwd+bwd renders/sec at 1200x680 (Replica-shaped, 200k Gaussians)"
 UNIT = "renders/s"
 KERNEL_LAUNCHES_PER_STEP = {
     # kernels of libcsplat launched by one RenderStep.step()
-    "mask_prune": 3, "rvq_assign": 2, "project": 1, "bin_tiles": 5, "render_fwd": 1,
+    "mask_prune": 1, "rvq_assign": 2, "project": 1, "bin_tiles": 2, "render_fwd": 1,
     "render_bwd": 2,
 }
 
@@ -327,6 +327,116 @@ def bench_ba(dev, n_rays=65536, iters=5):
             "n_valid": int(ba.n_valid.item()), "loss": ba_loss_value(ba.loss3),
             "pairs_last_kf": int(st.n_pairs.item()), "ms_per_iter_eager": ms_eager,
             "note": "graph replay of the whole iteration; eager = per-keyframe host loop"}
+
+
+def _timed(fn, stream, flush, reps):
+    import torch
+    fn()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    return statistics.median(ts)
+
+
+def bench_c4(dev, flush, reps=10):
+    """C4: ScanNet-shaped 1M unpruned Gaussians: csplat_mask_prune
+    over all 1M (keep 1/1.97) and csplat_rvq_assign 4 x 256 of scale and
+    rotation over all 1M.  Cold L2, CUDA events, median."""
+    import torch
+    from paper_2403_11247_b200 import csplat as cs
+    from scenes import synth
+    sc = synth.scannet_scene(0)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    n = g.n
+    out = cs.GaussianMap(**{k: torch.empty_like(getattr(g, k)) for k in
+                            ("mean", "opacity", "rgb", "log_scale", "quat", "mask")})
+    keep_map = torch.empty(n, dtype=torch.int32, device=dev)
+    n_kept = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(cs.workspace_bytes(cs.OP_MASK_PRUNE, n), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    t_prune = _timed(lambda: cs.mask_prune(g, out=out, keep_map=keep_map, n_kept=n_kept, ws=ws),
+                     stream, flush, reps)
+    k = int(n_kept.item())
+    sct = torch.tensor(sc.codebook["scale_codes"], device=dev)
+    rct = torch.tensor(sc.codebook["rot_codes"], device=dev)
+    L = sct.shape[0]
+    si = torch.empty((L, n), dtype=torch.uint8, device=dev)
+    ri = torch.empty((L, n), dtype=torch.uint8, device=dev)
+    t_rvq = _timed(lambda: (cs.rvq_assign(g.log_scale, sct, idx=si, want_recon=False),
+                            cs.rvq_assign(g.quat, rct, idx=ri, want_recon=False)),
+                   stream, flush, reps)
+    pbytes = n * (4 + 60) + k * (60 + 4)   # masks + planes read, planes + keep_map written
+    work = n * L * sct.shape[1] * (2 * 3 + 2 * 4)  # sub + fma per dimension (stage_rooflines)
+    return {"workload": "C4 ScanNet-shaped 1M Gaussians (mask keep 1/1.97), R-VQ 4x256",
+            "n": n, "n_kept": k, "prune_us": t_prune,
+            "prune_hbm_gbs": pbytes / (t_prune * 1e-6) / 1e9,
+            "rvq_scale_rot_us": t_rvq, "rvq_gaussians_per_s": n / (t_rvq * 1e-6),
+            "rvq_tlane_ops_per_s": work / (t_rvq * 1e-6) / 1e12}
+
+
+def bench_c5_window(dev, rank, world, iters=3):
+    """C5 (SURVEY §8(d,e)): the mapping window of 64 Replica-shaped keyframes x
+    500k Gaussians (R-VQ 4x256) sharded over the ranks (keyframe i -> rank
+    i mod G): each rank renders its keyframes fwd+bwd (ACCUMULATE, the local
+    part captured as one CUDA graph), then one NCCL all-reduce of the flat
+    gradient buffer.  Window iteration time = max over ranks (CUDA events)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2403_11247_b200.pipeline import RenderStep
+    from paper_2403_11247_b200.window import gpu_window
+    from scenes import synth
+    sc = synth.window_scene(0)
+    st = RenderStep(sc.planes(), sc.cam, sc.codebook, device=dev)
+    st.size_pairs(sc.views[rank], views=sc.views[rank::max(1, 8 * world)])
+    H, W = sc.cam["height"], sc.cam["width"]
+    st.set_upstream(*(torch.tensor(a, device=dev)
+                      for a in synth.upstream(np.random.default_rng(5), H, W)))
+    # the local part (the rank's keyframes); the all-reduce is issued below
+    win = gpu_window(st, sc.views, rank=rank, world=world, reduce=False)
+    stream = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(device=dev)
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        win.run()
+    stream.wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        win.run()
+
+    def one():
+        graph.replay()
+        if world > 1:
+            dist.all_reduce(st.grads["flat"])
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ts = []
+    for _ in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        one()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    st.check_capacity()
+    t = statistics.median(ts)
+    if world > 1:
+        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    return {"workload": "C5 window: 64 keyframes x 500k Gaussians, R-VQ 4x256, "
+                        f"keyframes sharded over {world} GPU(s) + NCCL all-reduce",
+            "n_gpus": world, "keyframes_per_rank": len(win.local), "ms_per_window_iter": t,
+            "window_iters_per_s": 1e3 / t, "keyframe_renders_per_s": 64e3 / t}
 
 
 # ---------------------------------------------------------------- oracle (CPU) legs
@@ -636,6 +746,9 @@ def main():
     if rank == 0 and not args.no_tracking:
         next_rows = bench_next_rows(step, sc, view, dev, flush)
         next_rows["global_ba"] = bench_ba(dev)
+    c4 = bench_c4(dev, flush) if rank == 0 and not args.no_tracking else None
+    # every rank takes part in the sharded C5 window (its collective is a real exchange)
+    c5 = None if args.no_tracking else bench_c5_window(dev, rank, world)
 
     if rank == 0:
         n_kept = int(step.n_kept.item())
@@ -717,6 +830,10 @@ def main():
                                                         + stage_ms["render_bwd"])
             line["stage_roofline"] = stage_rooflines(stage_ms, counts, n_kept, n_pairs, e_bwd,
                                                      peaks, step)
+        if c4:
+            line["c4_prune_rvq"] = c4
+        if c5:
+            line["c5_window"] = c5
         if tracking:
             line["tracking_c3"] = tracking
         if next_rows:

@@ -32,12 +32,13 @@ class WindowStep:
     def __init__(self, n_keyframes: int, flat_grad: torch.Tensor,
                  render_fn: Callable[[int, torch.Tensor], None],
                  prepare_fn: Callable[[], None] | None = None, rank: int | None = None,
-                 world: int | None = None, group=None):
+                 world: int | None = None, group=None, reduce: bool = True):
         self.world = world if world is not None else (dist.get_world_size(group)
                                                       if dist.is_initialized() else 1)
         self.rank = rank if rank is not None else (dist.get_rank(group)
                                                    if dist.is_initialized() else 0)
         self.group = group
+        self.reduce = reduce  # False: the caller issues the all-reduce (e.g. outside a graph)
         self.local = shard(n_keyframes, self.rank, self.world)
         self.flat = flat_grad
         self.render_fn = render_fn
@@ -53,7 +54,7 @@ class WindowStep:
         for k in self.local:
             self.poses[k].zero_()
             self.render_fn(k, self.poses[k])
-        if self.world > 1:
+        if self.world > 1 and self.reduce:
             dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
         return self.flat
 
@@ -65,11 +66,12 @@ def apply_sgd(params: Sequence[torch.Tensor], grads: Sequence[torch.Tensor], lr:
             p.sub_(lr * g)
 
 
-def gpu_window(step, views, rank=None, world=None, group=None):
+def gpu_window(step, views, rank=None, world=None, group=None, reduce=True):
     """WindowStep over a RenderStep: `views[i]` is keyframe i's world->camera view."""
     from . import csplat as cs
 
     def render(k, pose):
         step.render(views[k], flags=cs.ACCUMULATE, pose=pose)
 
-    return WindowStep(len(views), step.grads["flat"], render, step.prepare, rank, world, group)
+    return WindowStep(len(views), step.grads["flat"], render, step.prepare, rank, world, group,
+                      reduce)
