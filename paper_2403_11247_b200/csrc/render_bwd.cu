@@ -30,12 +30,19 @@ constexpr int kBB = 32;           // records per TMA batch
 #endif
 constexpr int kBS = KBS_OVERRIDE; // ring depth
 constexpr int kAcc = 12;          // accumulator floats per Gaussian
-constexpr int kCW = 4;            // pixel (consumer) warps: 4 x 32 lanes x 2 pixels = 16x16
+#ifndef CSPLAT_BWD_CW
+#define CSPLAT_BWD_CW 4
+#endif
+// pixel (consumer) warps per CTA, each an 8x8 block of the tile (32 lanes x 2
+// pixels): 4 = the whole 16x16 tile; 2 = half a tile (two CTAs per tile: twice
+// the CTAs, finer-grained waves, the tile's list streamed by both)
+constexpr int kCW = CSPLAT_BWD_CW;
+constexpr int kCtaPerTile = 4 / kCW;
 constexpr int kBwdThreads = (kCW + 1) * 32;  // + 1 producer warp
 constexpr int kG = 3;             // active entries per transposed reduction: kG*kV <= 32 rows = one pass
 constexpr int kV = 10;            // partials per (pixel, entry)
 #ifndef CSPLAT_BWD_MIN_BLOCKS
-#define CSPLAT_BWD_MIN_BLOCKS 5
+#define CSPLAT_BWD_MIN_BLOCKS (CSPLAT_BWD_CW == 4 ? 5 : 9)
 #endif
 constexpr int kBwdMinBlocks = CSPLAT_BWD_MIN_BLOCKS;  // CTAs per SM the register budget targets
 
@@ -188,13 +195,14 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tile = blockIdx.x;
+  const int tile = blockIdx.x / kCtaPerTile;
+  const int blk = (blockIdx.x % kCtaPerTile) * kCW + (tid >> 5);  // 8x8 block of the tile
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const uint32_t start = range[2 * tile];
   const bool producer = wid == kCW;
 
   // ---- pixel state (pixel warps only)
-  const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * 8;
+  const int wx0 = tx * kTile + (blk & 1) * 8, wy0 = ty * kTile + (blk >> 1) * 8;
   const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * 2, py1 = py0 + 1;
   BPix pp[2];
 #pragma unroll
@@ -325,7 +333,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
       // the batch's entries this warp replays, one ballot: lane l tests entry l's
       // block mask (payload word 14, bin.cu) and replay range (j < wmax)
       const uint32_t bml = lane < cnt ? __float_as_uint(rb[lane * 4 + 3].z) : 0u;
-      uint32_t todo = __ballot_sync(0xffffffffu, ((bml >> wid) & 1u) && b * kBB + lane < wmax);
+      uint32_t todo = __ballot_sync(0xffffffffu, ((bml >> blk) & 1u) && b * kBB + lane < wmax);
       while (todo) {  // back to front
         const int e = 31 - __clz(todo);
         todo ^= 1u << e;
@@ -385,7 +393,7 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
     attr_done = true;
   }
   const int T = ci.tiles_x * ci.tiles_y;
-  k_render_bwd<<<T, kBwdThreads, smem, s>>>(static_cast<const float4 *>(pair_rec), tile_range,
+  k_render_bwd<<<T * kCtaPerTile, kBwdThreads, smem, s>>>(static_cast<const float4 *>(pair_rec), tile_range,
                                             ci.W, ci.H, ci.tiles_x, prm.alpha_max, t_final,
                                             n_contrib, d_color, d_depth, d_sil, acc);
   e = cudaGetLastError();
