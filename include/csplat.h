@@ -189,6 +189,34 @@ int csplat_render_bwd_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                          const float *d_silhouette, uint32_t flags, const csplat_grads *out,
                          void *ws, size_t ws_bytes, void *stream);
 
+/* NEXT-1 loss-fused backward: csplat_render_bwd whose
+ * upstream gradients are those of the tracking objective, formed per pixel in
+ * the backward's prologue instead of read: Eq 12 gated by Eq 14
+ * (P:207-210), reading R27 -- g = 1[S > sil_gate], v = 1[D_obs > 0],
+ * dL/dC = 2 g (C - C_obs)/(W H), dL/dD = 2 lambda_depth g v (D - D_obs)/|R|,
+ * dL/dS = 0, with |R| = *n_valid_dev (csplat_count_valid_depth of the same
+ * obs_depth).  Pixels whose upstream is zero (gated out, or no valid depth and
+ * no colour residual) are not replayed; a warp or tile with none left is
+ * skipped.  color/depth/silhouette: csplat_render_fwd's outputs; obs_*: the
+ * observed frame (device).  loss3_dev (device float[3], may be NULL) receives
+ * (L_t, L_c, L_d), zeroed by the call.  Exactly one of view (host)
+ * / view_dev (device, see csplat_project_dv) is non-NULL.  Other arguments,
+ * flags (CSPLAT_POSE_ONLY for tracking) and ws as csplat_render_bwd. */
+int csplat_tracking_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
+                        const csplat_camera *cam, const csplat_view *view, const float *view_dev,
+                        const csplat_params *prm, const void *rec, const void *pair_rec,
+                        const uint32_t *tile_range, const float *t_final,
+                        const int32_t *n_contrib, const float *color, const float *depth,
+                        const float *silhouette, const float *obs_color, const float *obs_depth,
+                        const uint64_t *n_valid_dev, float lambda_depth, float sil_gate,
+                        uint32_t flags, const csplat_grads *out, float *loss3_dev, void *ws,
+                        size_t ws_bytes, void *stream);
+
+/* |R| of Eq 12 for a frame: *n_valid_dev (device uint64) = the number of
+ * pixels of obs_depth [H][W] (device) with a valid depth (> 0). */
+int csplat_count_valid_depth(const float *obs_depth, int32_t width, int32_t height,
+                             uint64_t *n_valid_dev, void *stream);
+
 /* NEXT-1: the pose step of a tracking iteration on the device (Sec 3.4,
  * the pose is optimised by minimising the tracking objective):
  * view_dev (12 floats, world->camera [R|t]) <- Exp(xi) view_dev with

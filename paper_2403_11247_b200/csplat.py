@@ -70,7 +70,8 @@ EXPORTS = ["csplat_project", "csplat_bin_tiles", "csplat_render_fwd", "csplat_re
            "csplat_rvq_assign", "csplat_mask_prune", "csplat_tracking_loss", "csplat_rvq_update",
            "csplat_mask_loss", "csplat_keyframe_overlap", "csplat_bin_tiles_active",
            "csplat_ba_patches", "csplat_ba_patch_loss", "csplat_project_dv",
-           "csplat_render_bwd_dv", "csplat_pose_step",
+           "csplat_render_bwd_dv", "csplat_pose_step", "csplat_tracking_bwd",
+           "csplat_count_valid_depth",
            "csplat_workspace_bytes", "csplat_last_error", "csplat_status_string",
            "csplat_version"]
 OP_TRACKING_LOSS = 4
@@ -99,6 +100,9 @@ def lib():
         L.csplat_project_dv.argtypes = [vp] * 8
         L.csplat_render_bwd_dv.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_pose_step.argtypes = [vp, vp, C.c_float, C.c_float, vp]
+        L.csplat_tracking_bwd.argtypes = [vp] * 17 + [C.c_float, C.c_float, u32, vp, vp, vp,
+                                                      C.c_size_t, vp]
+        L.csplat_count_valid_depth.argtypes = [vp, i32, i32, vp, vp]
         L.csplat_render_fwd.argtypes = [vp] * 10
         L.csplat_render_bwd.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_rvq_assign.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp]
@@ -229,6 +233,45 @@ def _on_device(v) -> bool:
             raise CsplatError("a device view must be a contiguous float32 tensor of 12 values")
         return True
     return False
+
+
+def count_valid_depth(obs_depth, n_valid=None, stream=None):
+    """|R| of Eq 12: pixels of obs_depth [H, W] with a valid depth -> device int64[1]."""
+    H, W = obs_depth.shape
+    if n_valid is None:
+        n_valid = torch.zeros(1, dtype=torch.int64, device=obs_depth.device)
+    _check(lib().csplat_count_valid_depth(_ptr(obs_depth), W, H, _ptr(n_valid), _stream(stream)),
+           "csplat_count_valid_depth")
+    return n_valid
+
+
+def tracking_bwd(g: GaussianMap, cam: dict, v, rec, pair_rec, tile_range, img: dict, obs_color,
+                 obs_depth, n_valid, prm: Params | None = None, cb: CodebookT | None = None,
+                 flags: int = POSE_ONLY, lambda_depth=1.0, sil_gate=0.99, grads=None, loss3=None,
+                 ws=None, stream=None):
+    """NEXT-1 loss-fused backward: render_bwd with the Eq 12 + Eq 14 upstream formed
+    in the kernel from the rendered `img` (render_fwd output) and the observed frame."""
+    n = g.n
+    dev = g.opacity.device
+    if grads is None:
+        grads = alloc_grads(n, dev, pose_only=bool(flags & POSE_ONLY))
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_RENDER_BWD, n), dtype=torch.uint8, device=dev)
+    gr = Grads(*[_ptr(grads.get(k)) for k in ("mean", "opacity", "rgb", "log_scale", "quat",
+                                               "mask", "pose")])
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    dv = _on_device(v)
+    hv = None if dv else view(v)
+    _check(lib().csplat_tracking_bwd(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
+                                     None if dv else C.byref(hv), _ptr(v) if dv else None,
+                                     C.byref(prm or params()), _ptr(rec), _ptr(pair_rec),
+                                     _ptr(tile_range), _ptr(img["t_final"]), _ptr(img["n_contrib"]),
+                                     _ptr(img["color"]), _ptr(img["depth"]), _ptr(img["sil"]),
+                                     _ptr(obs_color), _ptr(obs_depth), _ptr(n_valid),
+                                     lambda_depth, sil_gate, flags, C.byref(gr), _ptr(loss3),
+                                     _ptr(ws), ws.numel(), _stream(stream)),
+           "csplat_tracking_bwd")
+    return grads
 
 
 def pose_step(view_dev, pose_grad, lr_rot: float, lr_trans: float, stream=None):

@@ -299,12 +299,13 @@ static int render_bwd_impl(const csplat_gaussians *g, const csplat_codebook *cb,
                       const void *rec, const void *pair_rec, const uint32_t *tile_range,
                       const float *t_final, const int32_t *n_contrib, const float *d_color,
                       const float *d_depth, const float *d_silhouette, uint32_t flags,
-                      const csplat_grads *out, void *ws, size_t ws_bytes, void *stream) {
+                      const csplat_grads *out, void *ws, size_t ws_bytes, void *stream,
+                      const csplat::TrackingLoss *loss = nullptr) {
   RET_IF(check_gaussians(g, false));
   RET_IF(check_camera(cam));
   RET_IF(check_codebook(cb, true));
-  if ((!view && !view_dev) || !prm || !out || !tile_range || !t_final || !n_contrib || !d_color || !d_depth ||
-      !d_silhouette)
+  if ((!view && !view_dev) || !prm || !out || !tile_range || !t_final || !n_contrib ||
+      (!loss && (!d_color || !d_depth || !d_silhouette)))
     return invalid("render_bwd: NULL argument");
   if (g->n > 0 && !rec) return invalid("rec NULL");
   if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
@@ -320,7 +321,8 @@ static int render_bwd_impl(const csplat_gaussians *g, const csplat_codebook *cb,
   csplat::DecodeArgs d;
   if (cb) d = decode_args(cb);
   return cuda_status(csplat::launch_render_bwd(*g, cb ? &d : nullptr, *cam,
-                                               view ? *view : csplat_view{}, view_dev, *prm, rec,
+                                               view ? *view : csplat_view{}, view_dev, loss,
+                                               *prm, rec,
                                                pair_rec, tile_range, t_final, n_contrib, d_color,
                                                d_depth, d_silhouette, flags, *out, ws,
                                                static_cast<cudaStream_t>(stream)),
@@ -350,6 +352,39 @@ int csplat_render_bwd_dv(const csplat_gaussians *g, const csplat_codebook *cb,
   return render_bwd_impl(g, cb, cam, nullptr, view_dev, prm, rec, pair_rec, tile_range, t_final,
                          n_contrib, d_color, d_depth, d_silhouette, flags, out, ws, ws_bytes,
                          stream);
+}
+
+int csplat_count_valid_depth(const float *obs_depth, int32_t width, int32_t height,
+                             uint64_t *n_valid_dev, void *stream) {
+  if (width <= 0 || height <= 0) return invalid("width/height must be > 0");
+  if (!obs_depth || !n_valid_dev) return invalid("count_valid_depth: NULL argument");
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_count_valid(obs_depth, (int64_t)width * height,
+                                                reinterpret_cast<unsigned long long *>(n_valid_dev),
+                                                static_cast<cudaStream_t>(stream)),
+                     "csplat_count_valid_depth");
+}
+
+int csplat_tracking_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
+                        const csplat_camera *cam, const csplat_view *view, const float *view_dev,
+                        const csplat_params *prm, const void *rec, const void *pair_rec,
+                        const uint32_t *tile_range, const float *t_final,
+                        const int32_t *n_contrib, const float *color, const float *depth,
+                        const float *silhouette, const float *obs_color, const float *obs_depth,
+                        const uint64_t *n_valid_dev, float lambda_depth, float sil_gate,
+                        uint32_t flags, const csplat_grads *out, float *loss3_dev, void *ws,
+                        size_t ws_bytes, void *stream) {
+  if ((view == nullptr) == (view_dev == nullptr)) return invalid("give exactly one of view / view_dev");
+  if (!color || !depth || !silhouette || !obs_color || !obs_depth || !n_valid_dev)
+    return invalid("tracking_bwd: NULL image argument");
+  if (!std::isfinite(lambda_depth) || !std::isfinite(sil_gate))
+    return invalid("lambda_depth / sil_gate must be finite");
+  csplat::TrackingLoss tl{color, depth, silhouette, obs_color, obs_depth,
+                          reinterpret_cast<const unsigned long long *>(n_valid_dev), lambda_depth,
+                          sil_gate, loss3_dev};
+  return render_bwd_impl(g, cb, cam, view, view_dev, prm, rec, pair_rec, tile_range, t_final,
+                         n_contrib, nullptr, nullptr, nullptr, flags, out, ws, ws_bytes, stream,
+                         &tl);
 }
 
 int csplat_pose_step(float *view_dev, const float *pose_grad_dev, float lr_rot, float lr_trans,

@@ -244,9 +244,18 @@ cudaError_t launch_chain(const csplat_gaussians &g, const DecodeArgs *dec,
                          const float *view_dev, const csplat_params &prm, const void *rec,
                          const float *acc, uint32_t flags, const csplat_grads &out,
                          cudaStream_t s);
+struct TrackingLoss {  // NEXT-1 loss-fused backward (render_bwd.cu)
+  const float *color, *depth, *sil, *obs_color, *obs_depth;
+  const unsigned long long *n_valid;
+  float lambda_d, gate;
+  float *loss3;
+};
+cudaError_t launch_count_valid(const float *obs_depth, int64_t HW, unsigned long long *n_valid,
+                               cudaStream_t s);
 cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                               const csplat_camera &cam, const csplat_view &view,
-                              const float *view_dev, const csplat_params &prm, const void *rec, const void *pair_rec,
+                              const float *view_dev, const TrackingLoss *loss,
+                              const csplat_params &prm, const void *rec, const void *pair_rec,
                               const uint32_t *tile_range, const float *t_final,
                               const int32_t *n_contrib, const float *d_color, const float *d_depth,
                               const float *d_sil, uint32_t flags, const csplat_grads &out,

@@ -251,6 +251,19 @@ cudaError_t launch_overlap(const float *depth, const csplat_camera &cam, const c
   return cudaGetLastError();
 }
 
+cudaError_t launch_count_valid(const float *obs_depth, int64_t HW, unsigned long long *n_valid,
+                               cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(n_valid, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess || HW == 0) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t blocks = (HW + kLossThreads - 1) / kLossThreads;
+  if (blocks > 4LL * sms) blocks = 4LL * sms;
+  k_count_valid<<<(unsigned)blocks, kLossThreads, 0, s>>>(HW, obs_depth, n_valid);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tracking_loss(const float *color, const float *depth, const float *sil,
                                  const float *obs_color, const float *obs_depth, int W, int H,
                                  float lambda_d, float gate, float *d_color, float *d_depth,

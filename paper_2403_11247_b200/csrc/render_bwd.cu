@@ -187,11 +187,23 @@ __device__ __forceinline__ bool bwd_pair_packed(BPix2 &P, int j, float dx, f2_t 
   return val0 | val1;
 }
 
+// NEXT-1 loss-fused mode: the upstream gradients are
+// the tracking objective's (Eq 12 gated by Eq 14, reading R27), formed per
+// pixel in the prologue from the rendered and observed images instead of read.
+struct LossArgs {
+  const float *color, *depth, *sil, *obs_color, *obs_depth;
+  const unsigned long long *n_valid;  // |R|: pixels with a valid observed depth
+  float lambda_d, gate, inv_n;
+  float *loss3;                       // (L_t, L_c, L_d) added
+};
+
+template <bool LOSS>
 __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, const float *__restrict__ t_final,
     const int32_t *__restrict__ n_contrib, const float *__restrict__ dC,
-    const float *__restrict__ dD, const float *__restrict__ dS, float *__restrict__ acc) {
+    const float *__restrict__ dD, const float *__restrict__ dS, float *__restrict__ acc,
+    LossArgs la) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -205,6 +217,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
   const int wx0 = tx * kTile + (blk & 1) * 8, wy0 = ty * kTile + (blk >> 1) * 8;
   const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * 2, py1 = py0 + 1;
   BPix pp[2];
+  float lc = 0.f, ld = 0.f;  // LOSS: this thread's shares of the Eq 12 sums
 #pragma unroll
   for (int k = 0; k < 2; k++) {
     const int py = k ? py1 : py0;
@@ -214,8 +227,42 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
       const int64_t HW = (int64_t)W * H, q = (int64_t)py * W + px;
       p.T = t_final[q];
       p.last = n_contrib[q];
-      p.gr = dC[q]; p.gg = dC[HW + q]; p.gb = dC[2 * HW + q];
-      p.gd = dD[q]; p.gs = dS[q];
+      if constexpr (LOSS) {
+        // Eq 14 gate (no gradient through it), R_i of Eq 12: valid observed depth
+        const unsigned long long nv = *la.n_valid;
+        const float inv_r = 1.0f / (float)(nv > 0 ? nv : 1ull);
+        const float g = la.sil[q] > la.gate ? 1.0f : 0.0f;
+        const float obd = la.obs_depth[q];
+        const float v = obd > 0.0f ? 1.0f : 0.0f;
+        const float r0 = la.color[q] - la.obs_color[q];
+        const float r1 = la.color[HW + q] - la.obs_color[HW + q];
+        const float r2 = la.color[2 * HW + q] - la.obs_color[2 * HW + q];
+        const float rd = la.depth[q] - obd;
+        lc += g * (r0 * r0 + r1 * r1 + r2 * r2);
+        ld += g * v * rd * rd;
+        const float sc = 2.0f * g * la.inv_n;
+        p.gr = sc * r0; p.gg = sc * r1; p.gb = sc * r2;
+        p.gd = 2.0f * la.lambda_d * g * v * rd * inv_r;
+        p.gs = 0.0f;
+      } else {
+        p.gr = dC[q]; p.gg = dC[HW + q]; p.gb = dC[2 * HW + q];
+        p.gd = dD[q]; p.gs = dS[q];
+      }
+      // a pixel with an all-zero upstream contributes exact zeros to every
+      // partial (v_j = 0, so B = 0 and dL/dalpha = 0): no replay (gated-out
+      // tracking pixels, the unsampled pixels of the NEXT-4 patch BA)
+      if (p.gr == 0.f && p.gg == 0.f && p.gb == 0.f && p.gd == 0.f && p.gs == 0.f) p.last = 0;
+    }
+  }
+  if constexpr (LOSS) {
+    lc = warp_sum(lc);
+    ld = warp_sum(ld);
+    if (!producer && lane == 0 && (lc != 0.f || ld != 0.f)) {
+      const unsigned long long nv = *la.n_valid;
+      const float a = lc * la.inv_n, b = ld / (float)(nv > 0 ? nv : 1ull);
+      atomicAdd(la.loss3 + 0, a + la.lambda_d * b);
+      atomicAdd(la.loss3 + 1, a);
+      atomicAdd(la.loss3 + 2, b);
     }
   }
   const int mylast = max(pp[0].last, pp[1].last);
@@ -372,7 +419,8 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
 
 cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                               const csplat_camera &cam, const csplat_view &view,
-                              const float *view_dev, const csplat_params &prm, const void *rec, const void *pair_rec,
+                              const float *view_dev, const TrackingLoss *loss,
+                              const csplat_params &prm, const void *rec, const void *pair_rec,
                               const uint32_t *tile_range, const float *t_final,
                               const int32_t *n_contrib, const float *d_color, const float *d_depth,
                               const float *d_sil, uint32_t flags, const csplat_grads &out,
@@ -388,14 +436,34 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
   static bool attr_done = false;
   const size_t smem = sizeof(BwdSmem);
   if (!attr_done) {
-    e = cudaFuncSetAttribute(k_render_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_render_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_render_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
   const int T = ci.tiles_x * ci.tiles_y;
-  k_render_bwd<<<T * kCtaPerTile, kBwdThreads, smem, s>>>(static_cast<const float4 *>(pair_rec), tile_range,
-                                            ci.W, ci.H, ci.tiles_x, prm.alpha_max, t_final,
-                                            n_contrib, d_color, d_depth, d_sil, acc);
+  LossArgs la{};
+  if (loss) {
+    la.color = loss->color; la.depth = loss->depth; la.sil = loss->sil;
+    la.obs_color = loss->obs_color; la.obs_depth = loss->obs_depth;
+    la.n_valid = loss->n_valid; la.lambda_d = loss->lambda_d; la.gate = loss->gate;
+    la.inv_n = 1.0f / (float)((int64_t)ci.W * ci.H);
+    la.loss3 = loss->loss3;
+    if (la.loss3) {
+      e = cudaMemsetAsync(la.loss3, 0, 3 * sizeof(float), s);
+      if (e != cudaSuccess) return e;
+    }
+    k_render_bwd<true><<<T * kCtaPerTile, kBwdThreads, smem, s>>>(
+        static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
+        t_final, n_contrib, nullptr, nullptr, nullptr, acc, la);
+  } else {
+    k_render_bwd<false><<<T * kCtaPerTile, kBwdThreads, smem, s>>>(
+        static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
+        t_final, n_contrib, d_color, d_depth, d_sil, acc, la);
+  }
   e = cudaGetLastError();
   if (e != cudaSuccess || g.n == 0) return e;
   return launch_chain(g, dec, cam, view, view_dev, prm, rec, acc, flags, out, s);

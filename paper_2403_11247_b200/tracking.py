@@ -8,9 +8,11 @@ libcsplat kernel.  Two drivers:
 * ``track``: the pose update on the host (one 36-byte device->host read per
   iteration, the view passed to the ABI by value);
 * ``track_graph``: the view lives in device memory (``csplat_project_dv`` /
-  ``csplat_render_bwd_dv`` read it when they run, ``csplat_pose_step`` updates
-  it), so one iteration is captured once as a CUDA graph and a frame's
-  iterations are graph replays with no host round trip.
+  ``csplat_tracking_bwd`` read it when they run, ``csplat_pose_step`` updates
+  it) and the loss is fused into the backward (``csplat_tracking_bwd``: the
+  Eq 12 + Eq 14 upstream formed in its prologue, gated-out pixels skipped), so
+  one iteration is captured once as a CUDA graph and a frame's iterations are
+  graph replays with no host round trip.
 """
 from __future__ import annotations
 
@@ -68,6 +70,7 @@ class Tracker:
         self.ws = torch.empty(cs.workspace_bytes(cs.OP_TRACKING_LOSS, 0), dtype=torch.uint8,
                               device=dev)
         self.host = torch.empty(9, pin_memory=True)
+        self.n_valid = cs.count_valid_depth(obs_depth)  # |R| of the frame (Eq 12), once
         self.step.prepare()   # mask prune + R-VQ of the (fixed) map, once per frame
 
     def iteration_device(self, view):
@@ -98,7 +101,9 @@ class Tracker:
 
     # ---- device-resident pose: a frame's iterations as CUDA-graph replays
     def iteration_dv(self, view_dev, lr_rot, lr_trans):
-        """One iteration with the view in device memory (capturable)."""
+        """One iteration with the view in device memory (capturable): project ->
+        bin -> fwd -> loss-fused backward (Eq 12 + Eq 14 formed in the backward's
+        prologue, gated-out pixels not replayed) -> device pose step."""
         st = self.step
         g = st.pruned
         cs.project(g, st.cam, view_dev, st.prm, st.cb, rec=st.rec, count=st.count)
@@ -106,10 +111,11 @@ class Tracker:
                      out=dict(pair_gid=st.pair_gid, pair_rec=st.pair_rec,
                               tile_range=st.tile_range, n_pairs_dev=st.n_pairs), sync=False)
         st.forward()
-        cs.tracking_loss(st.img, self.obs_color, self.obs_depth, self.lambda_depth,
-                         self.sil_gate, out=self.up, loss3=self.loss3, ws=self.ws)
-        st.set_upstream(*self.up)
-        st.backward(view_dev, flags=cs.POSE_ONLY, pose=self.pose)
+        cs.tracking_bwd(g, st.cam, view_dev, st.rec, st.pair_rec, st.tile_range, st.img,
+                        self.obs_color, self.obs_depth, self.n_valid, st.prm, st.cb,
+                        flags=cs.POSE_ONLY, lambda_depth=self.lambda_depth,
+                        sil_gate=self.sil_gate, grads=dict(st.grads, pose=self.pose),
+                        loss3=self.loss3, ws=st.ws_bwd)
         cs.pose_step(view_dev, self.pose, lr_rot, lr_trans)
 
     def capture(self, view, lr_rot=1e-4, lr_trans=1e-4):

@@ -525,6 +525,50 @@ def test_device_view_paths_match_host_view(env):
         assert (gh[k] - gd[k]).norm() <= 1e-5 * gh[k].norm(), k
 
 
+@pytest.mark.parametrize("pose_only", [True, False])
+def test_loss_fused_backward_matches_separate_kernels(env, pose_only):
+    """csplat_tracking_bwd (Eq 12 + Eq 14 upstream formed in the backward) ==
+    csplat_tracking_loss + csplat_render_bwd, and both == the oracle."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.mid_scene(8)
+    obs_c, obs_d = _observed(env, sc, sc.views[0])
+    obs_d[::7] = 0.0
+    view = synth.perturbed_view(np.random.default_rng(4), rot_deg=1.0, trans=0.02)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec, cnt = cs.project(g, sc.cam, view)
+    b = cs.bin_tiles(rec, cnt, sc.cam, capacity=int(cnt.sum().item()) + 64)
+    img = cs.render_fwd(b["pair_rec"], b["tile_range"], sc.cam)
+    flags = cs.POSE_ONLY if pose_only else 0
+    (dC, dD, dS), l_sep = cs.tracking_loss(img, obs_c, obs_d, lambda_depth=0.5)
+    g_sep = cs.render_bwd(g, sc.cam, view, rec, b["pair_rec"], b["tile_range"], img["t_final"],
+                          img["n_contrib"], dC, dD, dS, flags=flags)
+    nv = cs.count_valid_depth(obs_d)
+    assert int(nv.item()) == int((obs_d > 0).sum().item())
+    l_fus = torch.zeros(3, device=dev)
+    g_fus = cs.tracking_bwd(g, sc.cam, view, rec, b["pair_rec"], b["tile_range"], img, obs_c,
+                            obs_d, nv, flags=flags, lambda_depth=0.5, loss3=l_fus)
+    assert torch.allclose(l_fus, l_sep, rtol=1e-5)
+    names = ["pose"] if pose_only else GROUPS
+    for k in names:
+        assert (g_fus[k] - g_sep[k]).norm() <= 1e-5 * g_sep[k].norm(), k
+    # the oracle: Eq 12 + 14 upstream of the GPU-rendered images, then its backward
+    (rC, rD, rS), _, flg = orc.tracking_loss(img["color"].double().cpu().numpy(),
+                                              img["depth"].double().cpu().numpy(),
+                                              img["sil"].double().cpu().numpy(),
+                                              obs_c.cpu().numpy(), obs_d.cpu().numpy(),
+                                              lambda_d=0.5)
+    S = orc.Scene(**sc.planes())
+    rec_o, cnt_o = orc.project(S, sc.cam, view)
+    gid_o, rng_o = orc.bin_tiles(rec_o, cnt_o, sc.cam)
+    fo = orc.render_fwd(rec_o, gid_o, rng_o, sc.cam)
+    assert (fo["flags"] | flg).sum() <= 5   # a few float32-vs-float64 ambiguous pixels
+    go = orc.render_bwd(S, sc.cam, view, rec_o, gid_o, rng_o, rC, rD, rS)
+    for k in names:
+        a = g_fus[k].double().cpu().numpy().reshape(-1)
+        r = go[k].reshape(-1)
+        assert np.linalg.norm(a - r) / np.linalg.norm(r) <= GRAD_TOL, k
+
+
 def test_tracking_graph_replays_match_host_loop(env):
     """A frame's iterations as CUDA-graph replays with the device-resident pose
     follow the host-loop tracker (same kernels; the pose step in float64 on
