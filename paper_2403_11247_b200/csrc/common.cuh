@@ -72,6 +72,15 @@ __device__ __forceinline__ float da_q(float px, float py, float u, float v, floa
   return DFMA(DMUL(ca, dx), dx, DFMA(DMUL(cb2, dx), dy, DMUL(DMUL(cc, dy), dy)));
 }
 
+// The DA contribution test 0 <= q <= k2 as ONE unsigned
+// compare of the bit patterns: for k2 >= +0 finite, non-negative floats order
+// like their bits, a negative q or a NaN has bits above k2's, and the DA q is
+// never -0 (its last term (cc dy) dy is >= +0 and an exact-zero sum rounds to
+// +0), so this equals the two float comparisons bit for bit.
+__device__ __forceinline__ bool da_in_range(float q, float k2) {
+  return __float_as_uint(q) <= __float_as_uint(k2);
+}
+
 __device__ __forceinline__ int64_t eff_n(int64_t n, const int64_t *n_dev) {
   if (!n_dev) return n;
   const int64_t m = *n_dev;

@@ -93,7 +93,7 @@ __device__ __forceinline__ bool bwd_pixel_pair(BPix (&pp)[2], int j, float dx, f
     const float dy = dys[k];
     // DA q, bit-identical to the forward's
     const float q = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
-    const bool val = (j < p.last) & (q >= 0.0f) & (q <= r1.z);
+    const bool val = (j < p.last) & da_in_range(q, r1.z);
     any |= val;
     const float G = ex2_approx_b(q * -0.72134752f);  // exp(-q/2), same expression as the forward
     const float araw = r1.y * G;
@@ -146,8 +146,8 @@ __device__ __forceinline__ bool bwd_pair_packed(BPix2 &P, int j, float dx, f2_t 
   const f2_t X = fma2(pk2(cbdx, cbdx), DY, Y);         // DFMA(cbdx, dy, .)
   const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx), X); // DFMA(cadx, dx, .)
   const float q0 = lo2(Q), q1 = hi2(Q);
-  const bool val0 = (j < P.last0) & (q0 >= 0.0f) & (q0 <= r1.z);
-  const bool val1 = (j < P.last1) & (q1 >= 0.0f) & (q1 <= r1.z);
+  const bool val0 = (j < P.last0) & da_in_range(q0, r1.z);
+  const bool val1 = (j < P.last1) & da_in_range(q1, r1.z);
   const f2_t QE = mul2(Q, pk2(-0.72134752f, -0.72134752f));  // exp(-q/2) as in the forward
   const f2_t G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
   const f2_t AR = mul2(pk2(r1.y, r1.y), G);

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
             const float dy = DSUB((float)(py0 + k), r0.y);
             q[k] = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
           }
-          h[k] = (p[k].done == 0) & (q[k] >= 0.0f) & (q[k] <= r1.z);  // R2 (DA)
+          h[k] = (p[k].done == 0) & da_in_range(q[k], r1.z);  // R2 (DA): 0 <= q <= k2
           anyh |= h[k];
         }
 #ifdef CSPLAT_FWD_DIVERGENT
