@@ -148,11 +148,15 @@ __device__ __forceinline__ bool bwd_pair_packed(BPix2 &P, int j, float dx, f2_t 
   const float q0 = lo2(Q), q1 = hi2(Q);
   const bool val0 = (j < P.last0) & da_in_range(q0, r1.z);
   const bool val1 = (j < P.last1) & da_in_range(q1, r1.z);
-  const f2_t QE = mul2(Q, pk2(-0.72134752f, -0.72134752f));  // exp(-q/2) as in the forward
+  // exp(-q/2) as in the forward; a pixel that does not composite entry j gets
+  // q = +inf here, so G = ex2(-inf) = +0 and alpha = 0: it leaves T and B
+  // unchanged (rcp(1 - 0) = 1) and adds exact zeros to every partial
+  const f2_t QM = pk2(val0 ? q0 : __int_as_float(0x7f800000), val1 ? q1 : __int_as_float(0x7f800000));
+  const f2_t QE = mul2(QM, pk2(-0.72134752f, -0.72134752f));
   const f2_t G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
   const f2_t AR = mul2(pk2(r1.y, r1.y), G);
   const float ar0 = lo2(AR), ar1 = hi2(AR);
-  const f2_t AL = pk2(val0 ? fminf(amax, ar0) : 0.0f, val1 ? fminf(amax, ar1) : 0.0f);
+  const f2_t AL = pk2(fminf(amax, ar0), fminf(amax, ar1));
   const f2_t OM = sub2(pk2(1.0f, 1.0f), AL);
   float rc0, rc1;  // alpha <= alpha_max < 1 (R1)
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));
@@ -163,8 +167,9 @@ __device__ __forceinline__ bool bwd_pair_packed(BPix2 &P, int j, float dx, f2_t 
                        fma2(pk2(r2.y, r2.y), P.gg,
                             fma2(pk2(r2.z, r2.z), P.gb, fma2(pk2(r1.w, r1.w), P.gd, P.gs))));
   const f2_t D0 = mul2(TJ, sub2(VV, P.B));
-  // R23: no gradient through a capped alpha
-  const f2_t DL = pk2((val0 & (ar0 < amax)) ? lo2(D0) : 0.0f, (val1 & (ar1 < amax)) ? hi2(D0) : 0.0f);
+  // R23: no gradient through a capped alpha (a non-compositing pixel has
+  // alpha = G = 0, so its dL/dalpha only ever meets zero factors)
+  const f2_t DL = pk2(ar0 < amax ? lo2(D0) : 0.0f, ar1 < amax ? hi2(D0) : 0.0f);
   const f2_t AV = mul2(AL, DL);
   const f2_t GD = mul2(G, DL);
   P.B = fma2(AL, VV, mul2(OM, P.B));
