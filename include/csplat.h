@@ -317,7 +317,8 @@ int csplat_ba_patches(const float *obs_depth, const csplat_camera *cam, const in
                       void *stream);
 
 /* csplat_ba_patch_loss: one keyframe's share of the BA objective over the
- * whole sample (N = n_rays rays, |R| = *n_valid_dev, P = N/64 patches):
+ * whole sample (N = n_rays > 0 rays over all keyframes, |R| = *n_valid_dev,
+ * P = N/64 patches):
  *   L_c  = (1/N) sum_rays sum_c (C - C_obs)^2,  L_d = (1/|R|) sum_R (D - D_obs)^2  (Eq 12)
  *   SSIM = mean over patches and channels of the 8x8-window SSIM
  *          (2 mx my + C1)(2 sxy + C2) / ((mx^2 + my^2 + C1)(sx^2 + sy^2 + C2)),

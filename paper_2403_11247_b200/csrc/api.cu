@@ -258,8 +258,8 @@ int csplat_ba_patch_loss(const float *color, const float *depth, const float *ob
                          float lambda_depth, float lambda_ssim, float *d_color, float *d_depth,
                          float *d_silhouette, float *loss3_dev, void *stream) {
   RET_IF(check_camera(cam));
-  if (n_patches < 0 || n_rays < 64 * n_patches || (n_patches > 0 && n_rays <= 0))
-    return invalid("need 0 <= 64 n_patches <= n_rays");
+  if (n_patches < 0 || (n_patches > 0 && n_rays <= 0))
+    return invalid("need n_patches >= 0 and n_rays > 0");
   if (!d_color || !d_depth || !d_silhouette)
     return invalid("ba_patch_loss: NULL gradient output");
   if (n_patches > 0 && (!color || !depth || !obs_color || !obs_depth || !patches ||

@@ -166,3 +166,40 @@ def test_ba_iteration_parity(env, seed):
     for k in range(len(views)):
         a = ba.poses[k].double().cpu().numpy()
         assert np.linalg.norm(a - poses_o[k]) / np.linalg.norm(poses_o[k]) <= GRAD_TOL
+
+
+def test_ba_edge_cases(env):
+    """Keyframes without patches, patch ids outside the image's whole blocks
+    (ignored), an image whose width / height are not multiples of 8, and an
+    empty sample."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.mid_scene(13, width=150, height=100)     # 18 x 12 whole 8x8 blocks
+    cam = sc.cam
+    oc, od = _observed(env, sc, sc.views[0], 3)
+    ocd, odd = torch.tensor(oc, device=dev), torch.tensor(od, device=dev)
+    bw, bh = cam["width"] // 8, cam["height"] // 8
+    good = np.array([0, bw - 1, bw * (bh - 1), bw * bh - 1, 37], np.int32)
+    bad = np.array([-1, bw * bh, 10 ** 6], np.int32)
+    pt = torch.tensor(np.concatenate([good, bad]), device=dev)
+    mask, nv = cs.ba_patches(odd, cam, pt)
+    assert int(nv.item()) == orc.ba_count_valid([od], [good], cam["width"])
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec, cnt = cs.project(g, cam, sc.views[0])
+    b = cs.bin_tiles(rec, cnt, cam, capacity=int(cnt.sum().item()) + 64, tile_active=mask)
+    img = cs.render_fwd(b["pair_rec"], b["tile_range"], cam)
+    n_rays = 64 * len(good)
+    (dC, dD, dS), l3 = cs.ba_patch_loss(img, ocd, odd, cam, pt, n_rays, nv)
+    (rC, rD, rS), rl = orc.ba_patch_loss(img["color"].double().cpu().numpy(),
+                                         img["depth"].double().cpu().numpy(), oc, od, good,
+                                         n_rays, int(nv.item()))
+    np.testing.assert_allclose(l3.cpu().numpy(), rl, rtol=2e-5, atol=1e-7)
+    assert np.abs(dC.double().cpu().numpy() - rC).max() <= 1e-5 * max(np.abs(rC).max(), 1e-6)
+    # an empty sample: zero upstream, untouched loss, an all-clear tile mask
+    l0 = torch.zeros(3, device=dev)
+    empty = torch.zeros(0, dtype=torch.int32, device=dev)
+    m0, nv0 = cs.ba_patches(odd, cam, empty)
+    assert int(nv0.item()) == 0 and int(m0.abs().sum().item()) == 0
+    (eC, eD, eS), l0 = cs.ba_patch_loss(img, ocd, odd, cam, empty, 64, nv0, loss3=l0)
+    assert float(eC.abs().sum()) == 0 and float(eD.abs().sum()) == 0 and float(l0.abs().sum()) == 0
+    b0 = cs.bin_tiles(rec, cnt, cam, capacity=64, tile_active=m0)
+    assert int(b0["n_pairs_dev"].item()) == 0
