@@ -16,11 +16,8 @@ struct ChainConst {
   float fx, fy, lx_lo, lx_hi, ly_lo, ly_hi, dil;
 };
 
-__device__ __forceinline__ uint32_t load_idx2(const void *p, int bytes, int64_t off) {
-  return bytes == 1 ? (uint32_t)((const uint8_t *)p)[off] : (uint32_t)((const uint16_t *)p)[off];
-}
-
-__global__ void __launch_bounds__(256) k_chain(
+template <int LF>
+__global__ void __launch_bounds__(256, 3) k_chain(
     int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
     const float *__restrict__ opac, const float *__restrict__ lsc, const float *__restrict__ quat,
     const float *__restrict__ mask, DecodeArgs dec, int use_dec, ChainConst cc,
@@ -41,23 +38,23 @@ __global__ void __launch_bounds__(256) k_chain(
   float g[15];
 #pragma unroll
   for (int k = 0; k < 15; k++) g[k] = 0.f;
-  bool alive = false;
-  if (i < ne) alive = rec4[i * 4 + 1].y != 0.0f;  // o_hat word is 0 iff culled
-  float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0;
-  if (alive) {
-    a0 = acc4[i * 3 + 0]; a1 = acc4[i * 3 + 1]; a2 = acc4[i * 3 + 2];
-    // no pixel reached this Gaussian: every gradient term is an exact zero
-    // (finite factors times a zero accumulator), so skip the chain -- and,
-    // when accumulating, the writes (sparse views: the NEXT-4 patch BA)
-    alive = (a0.x != 0.f) | (a0.y != 0.f) | (a0.z != 0.f) | (a0.w != 0.f) | (a1.x != 0.f) |
-            (a1.y != 0.f) | (a1.z != 0.f) | (a1.w != 0.f) | (a2.x != 0.f) | (a2.y != 0.f);
-  }
+  // the record and the accumulator in one round of loads (a culled Gaussian
+  // has an all-zero record, so its o_hat word is 0)
+  const int64_t j = i < ne ? i : 0;
+  const float4 rc0 = rec4[j * 4 + 0], rc1 = rec4[j * 4 + 1];
+  const float4 a0 = acc4[j * 3 + 0], a1 = acc4[j * 3 + 1], a2 = acc4[j * 3 + 2];
+  // no pixel reached this Gaussian: every gradient term is an exact zero
+  // (finite factors times a zero accumulator), so skip the chain -- and,
+  // when accumulating, the writes (sparse views: the NEXT-4 patch BA)
+  const bool alive = i < ne && rc1.y != 0.0f &&
+                     ((a0.x != 0.f) | (a0.y != 0.f) | (a0.z != 0.f) | (a0.w != 0.f) |
+                      (a1.x != 0.f) | (a1.y != 0.f) | (a1.z != 0.f) | (a1.w != 0.f) |
+                      (a2.x != 0.f) | (a2.y != 0.f));
   if (alive) {
     // k_render_bwd accumulates the raw moments Sx, Sy, Sxx, Sxy, Syy of
     // a = alpha dL/dalpha; map them through the record's DA conic
     // (q = ca dx^2 + (2cb) dx dy + cc dy^2; render_bwd.cu, bwd_pixel_pair)
-    const float4 rc0 = rec4[i * 4 + 0];
-    const float cca = rc0.z, ccb = 0.5f * rc0.w, ccc = rec4[i * 4 + 1].x;
+    const float cca = rc0.z, ccb = 0.5f * rc0.w, ccc = rc1.x;
     const float gu = cca * a0.x + ccb * a0.y, gv = ccb * a0.x + ccc * a0.y;
     const float gca = -0.5f * a0.z, gcb = -a0.w, gcc = -0.5f * a1.x;
     const float goh = a1.y, gz = a1.z;
@@ -66,14 +63,7 @@ __global__ void __launch_bounds__(256) k_chain(
     g[6] = a2.y;
     float ls[3], qv[4];
     if (use_dec) {
-      for (int l = 0; l < dec.L; l++) {
-        const uint32_t si = load_idx2(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i);
-        const uint32_t ri = load_idx2(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i);
-        const float *sc = dec.scale_codes + ((int64_t)l * dec.P + si) * 3;
-        const float *rc = dec.rot_codes + ((int64_t)l * dec.P + ri) * 4;
-        for (int k = 0; k < 3; k++) ls[k] = l ? DADD(ls[k], sc[k]) : sc[k];
-        for (int k = 0; k < 4; k++) qv[k] = l ? DADD(qv[k], rc[k]) : rc[k];
-      }
+      rvq_decode<LF>(dec, n, i, ls, qv);  // the decoded geometry the renderer saw (R20)
     } else {
       for (int k = 0; k < 3; k++) ls[k] = lsc[k * n + i];
       for (int k = 0; k < 4; k++) qv[k] = quat[k * n + i];
@@ -276,7 +266,13 @@ cudaError_t launch_chain(const csplat_gaussians &g, const DecodeArgs *dec,
   DecodeArgs d{};
   if (dec) d = *dec;
   const int64_t blocks = (g.n + 255) / 256;
-  k_chain<<<(unsigned)blocks, 256, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.log_scale, g.quat,
+  auto kern = k_chain<0>;
+  switch (rvq_lf(dec)) {
+    case 4: kern = k_chain<4>; break;
+    case 2: kern = k_chain<2>; break;
+    default: break;
+  }
+  kern<<<(unsigned)blocks, 256, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.log_scale, g.quat,
                                            g.mask, d, dec ? 1 : 0, cc,
                                            static_cast<const float4 *>(rec),
                                            reinterpret_cast<const float4 *>(acc), flags, view_dev,

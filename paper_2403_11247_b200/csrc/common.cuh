@@ -218,6 +218,69 @@ struct DecodeArgs {
   const void *scale_idx, *rot_idx;
 };
 
+// a codebook index (precondition: < P; clamped to P - 1 so that a violating
+// index cannot read outside the codebook)
+__device__ __forceinline__ uint32_t load_rvq_idx(const void *p, int bytes, int64_t off, int P) {
+  const uint32_t k = bytes == 1 ? (uint32_t)__ldg((const uint8_t *)p + off)
+                                : (uint32_t)__ldg((const uint16_t *)p + off);
+  return min(k, (uint32_t)(P - 1));
+}
+
+// Eq 10 decode (R17, R20): S_hat^L = sum_l C^l[i^l], summed in stage order, of
+// Gaussian i's log-scale and quaternion.  LF > 0 = the stage count known at
+// compile time: all 2 LF index loads are issued first, then all code gathers,
+// so a thread waits for two memory round trips instead of 2 L dependent ones.
+template <int LF>
+__device__ __forceinline__ void rvq_decode(const DecodeArgs &dec, int64_t n, int64_t i,
+                                           float (&ls)[3], float (&qv)[4]) {
+  const float4 *rot4 = reinterpret_cast<const float4 *>(dec.rot_codes);
+  if constexpr (LF > 0) {
+    uint32_t si[LF], ri[LF];
+#pragma unroll
+    for (int l = 0; l < LF; l++) {
+      si[l] = load_rvq_idx(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i, dec.P);
+      ri[l] = load_rvq_idx(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i, dec.P);
+    }
+    float s[LF][3];
+    float4 r[LF];
+#pragma unroll
+    for (int l = 0; l < LF; l++) {
+      const float *sc = dec.scale_codes + ((int64_t)l * dec.P + si[l]) * 3;
+      s[l][0] = __ldg(sc); s[l][1] = __ldg(sc + 1); s[l][2] = __ldg(sc + 2);
+      r[l] = __ldg(rot4 + ((int64_t)l * dec.P + ri[l]));
+    }
+    ls[0] = s[0][0]; ls[1] = s[0][1]; ls[2] = s[0][2];
+    qv[0] = r[0].x; qv[1] = r[0].y; qv[2] = r[0].z; qv[3] = r[0].w;
+#pragma unroll
+    for (int l = 1; l < LF; l++) {
+      ls[0] = DADD(ls[0], s[l][0]); ls[1] = DADD(ls[1], s[l][1]); ls[2] = DADD(ls[2], s[l][2]);
+      qv[0] = DADD(qv[0], r[l].x); qv[1] = DADD(qv[1], r[l].y);
+      qv[2] = DADD(qv[2], r[l].z); qv[3] = DADD(qv[3], r[l].w);
+    }
+  } else {
+    for (int l = 0; l < dec.L; l++) {
+      const uint32_t si = load_rvq_idx(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i, dec.P);
+      const uint32_t ri = load_rvq_idx(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i, dec.P);
+      const float *sc = dec.scale_codes + ((int64_t)l * dec.P + si) * 3;
+      const float4 rc = __ldg(rot4 + ((int64_t)l * dec.P + ri));
+      const float s0 = __ldg(sc), s1 = __ldg(sc + 1), s2 = __ldg(sc + 2);
+      if (l == 0) {
+        ls[0] = s0; ls[1] = s1; ls[2] = s2;
+        qv[0] = rc.x; qv[1] = rc.y; qv[2] = rc.z; qv[3] = rc.w;
+      } else {
+        ls[0] = DADD(ls[0], s0); ls[1] = DADD(ls[1], s1); ls[2] = DADD(ls[2], s2);
+        qv[0] = DADD(qv[0], rc.x); qv[1] = DADD(qv[1], rc.y);
+        qv[2] = DADD(qv[2], rc.z); qv[3] = DADD(qv[3], rc.w);
+      }
+    }
+  }
+}
+
+// the compile-time stage count for rvq_decode (0 = a runtime loop)
+inline int rvq_lf(const DecodeArgs *dec) {
+  return dec ? (dec->L == 4 ? 4 : (dec->L == 2 ? 2 : 0)) : 0;
+}
+
 cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
                            const csplat_camera &cam, const csplat_view &view,
                            const float *view_dev, float tau, float dilation, void *rec,

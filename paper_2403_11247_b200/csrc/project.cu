@@ -16,10 +16,7 @@ struct ProjConst {
   float tau, dil;
 };
 
-__device__ __forceinline__ uint32_t load_idx(const void *p, int bytes, int64_t off) {
-  return bytes == 1 ? (uint32_t)((const uint8_t *)p)[off] : (uint32_t)((const uint16_t *)p)[off];
-}
-
+template <int LF>
 __global__ void __launch_bounds__(256) k_project(
     int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
     const float *__restrict__ opac, const float *__restrict__ rgb,
@@ -36,39 +33,27 @@ __global__ void __launch_bounds__(256) k_project(
   float4 *r = rec + i * 4;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   bool ok = i < ne;
-  float m = ok ? mask[i] : 0.f;
-  ok = ok && (m > pc.tau);  // Eq 6: M = 1[Sig(m) > eps]  <=>  m > tau (R12)
-  float ls0 = 0, ls1 = 0, ls2 = 0, qw = 0, qx = 0, qy = 0, qz = 0;
-  float mx = 0, my = 0, mz = 0, o = 0, cr = 0, cg = 0, cb = 0;
-  if (ok) {
-    if (use_dec) {
-      // Eq 10: S_hat^L = sum_l C^l[i^l], summed in stage order (R17, R20)
-      for (int l = 0; l < dec.L; l++) {
-        const uint32_t si = load_idx(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i);
-        const uint32_t ri = load_idx(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i);
-        const float *sc = dec.scale_codes + ((int64_t)l * dec.P + si) * 3;
-        const float4 rc = __ldg(reinterpret_cast<const float4 *>(dec.rot_codes) +
-                                ((int64_t)l * dec.P + ri));
-        const float s0 = __ldg(sc), s1 = __ldg(sc + 1), s2 = __ldg(sc + 2);
-        if (l == 0) {
-          ls0 = s0; ls1 = s1; ls2 = s2;
-          qw = rc.x; qx = rc.y; qy = rc.z; qz = rc.w;
-        } else {
-          ls0 = DADD(ls0, s0); ls1 = DADD(ls1, s1); ls2 = DADD(ls2, s2);
-          qw = DADD(qw, rc.x); qx = DADD(qx, rc.y); qy = DADD(qy, rc.z); qz = DADD(qz, rc.w);
-        }
-      }
-    } else {
-      ls0 = lsc[i]; ls1 = lsc[n + i]; ls2 = lsc[2 * n + i];
-      qw = quat[i]; qx = quat[n + i]; qy = quat[2 * n + i]; qz = quat[3 * n + i];
-    }
-    mx = mean[i]; my = mean[n + i]; mz = mean[2 * n + i];
-    o = opac[i];
-    cr = rgb[i]; cg = rgb[n + i]; cb = rgb[2 * n + i];
-    ok = isfinite(mx) && isfinite(my) && isfinite(mz) && isfinite(o) && isfinite(ls0) &&
-         isfinite(ls1) && isfinite(ls2) && isfinite(qw) && isfinite(qx) && isfinite(qy) &&
-         isfinite(qz) && isfinite(cr) && isfinite(cg) && isfinite(cb);
+  // every attribute load is independent of the mask test: issue them all at
+  // once (the Gaussian's planes, then the R-VQ codes), one memory round trip
+  // each, and cull afterwards
+  const int64_t j = ok ? i : 0;
+  const float m = mask[j];
+  float ls[3], qv[4];
+  if (use_dec) {
+    rvq_decode<LF>(dec, n, j, ls, qv);  // Eq 10: S_hat^L = sum_l C^l[i^l] (R17, R20)
+  } else {
+    ls[0] = lsc[j]; ls[1] = lsc[n + j]; ls[2] = lsc[2 * n + j];
+    qv[0] = quat[j]; qv[1] = quat[n + j]; qv[2] = quat[2 * n + j]; qv[3] = quat[3 * n + j];
   }
+  const float mx = mean[j], my = mean[n + j], mz = mean[2 * n + j];
+  const float o = opac[j];
+  const float cr = rgb[j], cg = rgb[n + j], cb = rgb[2 * n + j];
+  const float ls0 = ls[0], ls1 = ls[1], ls2 = ls[2];
+  const float qw = qv[0], qx = qv[1], qy = qv[2], qz = qv[3];
+  ok = ok && (m > pc.tau);  // Eq 6: M = 1[Sig(m) > eps]  <=>  m > tau (R12)
+  ok = ok && isfinite(mx) && isfinite(my) && isfinite(mz) && isfinite(o) && isfinite(ls0) &&
+       isfinite(ls1) && isfinite(ls2) && isfinite(qw) && isfinite(qx) && isfinite(qy) &&
+       isfinite(qz) && isfinite(cr) && isfinite(cg) && isfinite(cb);
   float oh = 0, k2 = 0, xc = 0, yc = 0, zc = 0;
   if (ok) {
     oh = da_sigm(o);
@@ -194,9 +179,15 @@ cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
   if (dec) d = *dec;
   const int threads = 256;
   const int64_t blocks = (g.n + threads - 1) / threads;
-  k_project<<<(unsigned)blocks, threads, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.rgb,
-                                                 g.log_scale, g.quat, g.mask, d, dec ? 1 : 0, pc,
-                                                 view_dev, reinterpret_cast<float4 *>(rec), count);
+  auto kern = k_project<0>;
+  switch (rvq_lf(dec)) {
+    case 4: kern = k_project<4>; break;
+    case 2: kern = k_project<2>; break;
+    default: break;
+  }
+  kern<<<(unsigned)blocks, threads, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.rgb, g.log_scale,
+                                            g.quat, g.mask, d, dec ? 1 : 0, pc, view_dev,
+                                            reinterpret_cast<float4 *>(rec), count);
   return cudaGetLastError();
 }
 
