@@ -176,7 +176,13 @@ __global__ void __launch_bounds__(kPT) k_prune_onepass(int64_t n, const int64_t 
     wr[k] = __popc(bal & ((1u << lane) - 1u));
     if (lane == 0) wpre[k][wid] = __popc(bal);
 #pragma unroll
+#ifdef CSPLAT_PRUNE_LOAD_KEPT
     for (int p = 0; p < 15; p++) v[k][p] = keep[k] ? pp.in[p][i] : 0.0f;  // in flight early
+#else
+    // not predicated on the mask test: the plane loads go out with the mask load
+    // (one memory round trip instead of two; the masked ones are read in vain)
+    for (int p = 0; p < 15; p++) v[k][p] = i < ne ? pp.in[p][i] : 0.0f;
+#endif
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // exclusive warp offsets of every round; the tile total
