@@ -53,8 +53,11 @@ __device__ __forceinline__ void block_argmin4(float d0, float d1, float d2, floa
 // Each thread carries VP packed vector PAIRS (2 VP vectors), so every code
 // loaded from shared memory feeds VP FFMA2 chains (register blocking: the scan
 // is bound by shared-memory loads and their latency at VP = 1).
+#ifndef CSPLAT_RVQ_MINB
+#define CSPLAT_RVQ_MINB 3  // 3 CTAs (24 warps) per SM: 80 registers, a few spills (114.8 vs 121 us)
+#endif
 template <int D, int S, int VP>
-__global__ void __launch_bounds__(kRvqThreads) k_rvq_chunked(
+__global__ void __launch_bounds__(kRvqThreads, CSPLAT_RVQ_MINB) k_rvq_chunked(
     const float *__restrict__ x, int64_t n, const int64_t *__restrict__ n_dev,
     const float *__restrict__ codes_g, int L, int P, void *__restrict__ idx, int idx_bytes,
     float *__restrict__ recon) {
@@ -155,8 +158,10 @@ __global__ void __launch_bounds__(kRvqThreads) k_rvq_chunked(
         dmin[2 * v + 1] = fminf(dmin[2 * v + 1], mb);
       }
     }
-    // resolve the first code of the winning blocks that attains the minimum
+    // resolve the first code of the winning blocks that attains the minimum:
+    // re-evaluate only vector u's pair in its block (bit-identical distances)
     int best[2 * VP];
+#ifdef CSPLAT_RVQ_RES_BOTH
 #pragma unroll
     for (int u = 0; u < 2 * VP; u++) {
       f2_t acc[VP][kBlk];
@@ -168,6 +173,31 @@ __global__ void __launch_bounds__(kRvqThreads) k_rvq_chunked(
         if (d == dmin[u]) best[u] = kbase + blk[u] + c;
       }
     }
+#else
+#pragma unroll
+    for (int u = 0; u < 2 * VP; u++) {
+      const int v = u >> 1;
+      float cv[kBlk * D];
+#pragma unroll
+      for (int q = 0; q < kBlk * D / 4; q++) {
+        const float4 t = C4[(blk[u] * D) / 4 + q];
+        cv[4 * q] = t.x; cv[4 * q + 1] = t.y; cv[4 * q + 2] = t.z; cv[4 * q + 3] = t.w;
+      }
+      best[u] = kbase + blk[u];
+#pragma unroll
+      for (int c = kBlk - 1; c >= 0; c--) {
+        f2_t a = 0ull;
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+          const float cf = cv[c * D + j];
+          const f2_t e = sub2(pk2(cf, cf), r[v][j]);
+          a = fma2(e, e, a);
+        }
+        const float d = (u & 1) ? hi2(a) : lo2(a);
+        if (d == dmin[u]) best[u] = kbase + blk[u] + c;
+      }
+    }
+#endif
 #pragma unroll
     for (int u = 0; u < 2 * VP; u++) {
       // the sequential scan keeps k = 0 when d_0 is NaN (no later d compares below it)
