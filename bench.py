@@ -329,6 +329,17 @@ def bench_ba(dev, n_rays=65536, iters=5):
             "note": "graph replay of the whole iteration; eager = per-keyframe host loop"}
 
 
+def cpu_model() -> str:
+    """The host CPU (lscpu 'Model name'), for the oracle baselines."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def _timed(fn, stream, flush, reps):
     import torch
     fn()
@@ -429,14 +440,22 @@ def bench_c5_window(dev, rank, world, iters=3):
         ts.append(a.elapsed_time(b))
     st.check_capacity()
     t = statistics.median(ts)
+    # every rank must hold the identical reduced gradient (the replicas stay in step)
+    chk = st.grads["flat"].double().sum().reshape(1)
+    same = True
     if world > 1:
         tt = torch.tensor([t], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
+        lo, hi = chk.clone(), chk.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        same = bool(torch.equal(lo, hi))
     return {"workload": "C5 window: 64 keyframes x 500k Gaussians, R-VQ 4x256, "
                         f"keyframes sharded over {world} GPU(s) + NCCL all-reduce",
             "n_gpus": world, "keyframes_per_rank": len(win.local), "ms_per_window_iter": t,
-            "window_iters_per_s": 1e3 / t, "keyframe_renders_per_s": 64e3 / t}
+            "window_iters_per_s": 1e3 / t, "keyframe_renders_per_s": 64e3 / t,
+            "reduced_grad_checksum": float(chk.item()), "replicas_identical": same}
 
 
 # ---------------------------------------------------------------- oracle (CPU) legs
@@ -526,6 +545,7 @@ def run_reference(args, rank, world):
                        "sample": f"{frac:.4f} of a render per step (first {frac:.4f} of pixel "
                                  f"rows, R-VQ on {frac:.4f} of survivors; full prune/project/bin)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "cpu_model": cpu_model(),
                              "sample": f"{frac:.4f} of one render per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -769,6 +789,7 @@ def main():
                 units += u
                 nst += 1
             cpu = {"value": units / tot, "unit": UNIT, "cores": ncores, "kind": "oracle",
+                   "cpu_model": cpu_model(),
                    "sample": f"{nst} full step(s) of the C2 workload (prune, R-VQ 2x4x256 on "
                              f"all survivors, project, bin, fwd+bwd over all 1200x680 pixels), "
                              f"1 thread, {tot:.1f} s"}
