@@ -212,6 +212,11 @@ __device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1,
   const int rx0 = (int)(v3.x & 0xffffu), ry0 = (int)(v3.x >> 16);
   const int rx1 = (int)(v3.y & 0xffffu), ry1 = (int)(v3.y >> 16);
   const bool conic_ok = ca > 0.0f && cc > 0.0f;
+  // the edge minimisers' slopes, once per pair: on a vertical edge at dx = ex the
+  // convex q is least at dy = -cb2 ex / (2 cc) (horizontal edges alike); any
+  // rounding of this location only moves the probe along the edge, which can
+  // raise q by at most cc * (location error)^2 -- far below the margin
+  const float sy = conic_ok ? -cb2 / (2.0f * cc) : 0.0f, sx = conic_ok ? -cb2 / (2.0f * ca) : 0.0f;
   uint32_t m = 0;
 #pragma unroll
   for (int w = 0; w < 4; w++) {
@@ -227,12 +232,12 @@ __device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1,
       qmin = INFINITY;
       if (ox) {  // near vertical edge, dy clamped to the block
         const float ex = dx0 > 0.0f ? dx0 : dx1;
-        const float dy = fminf(fmaxf(-cb2 * ex / (2.0f * cc), dy0), dy1);
+        const float dy = fminf(fmaxf(sy * ex, dy0), dy1);
         qmin = fminf(qmin, ca * ex * ex + cb2 * ex * dy + cc * dy * dy);
       }
       if (oy) {  // near horizontal edge
         const float ey = dy0 > 0.0f ? dy0 : dy1;
-        const float dx = fminf(fmaxf(-cb2 * ey / (2.0f * ca), dx0), dx1);
+        const float dx = fminf(fmaxf(sx * ey, dx0), dx1);
         qmin = fminf(qmin, ca * dx * dx + cb2 * dx * ey + cc * ey * ey);
       }
     }
