@@ -173,6 +173,55 @@ def test_rvq_parity(env, LPd):
     assert np.array_equal(rec.cpu().numpy(), rec_o)
 
 
+@pytest.mark.parametrize("d", [3, 4, 7])
+def test_rvq_near_ties_and_nonfinite(env, d):
+    """The filtered scan (rvq.cu k_rvq_filter) must give the sequential DA
+    argmin bit-exactly where its float32 candidate filter cannot decide:
+    codes 1 ulp apart, vectors equal to a code (distance 0), several codes at
+    the same distance, magnitudes from 1e-20 to 1e17, NaN/inf inputs, and a
+    stage whose codebook holds an inf (the whole stage takes the exact scan)."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    rng = np.random.default_rng(77 + d)
+    L, P, n = 4, 256, 12_000
+    x = (rng.standard_normal((d, n)) * 0.3 - 5.0).astype(np.float32)
+    codes = np.zeros((L, P, d), dtype=np.float32)
+    codes[0] = x[:, rng.choice(n, P, replace=False)].T
+    for l in range(1, L):
+        codes[l] = rng.standard_normal((P, d)) * 0.3 * 0.35 ** l
+    # near-duplicates one ulp apart at both ends of the chunk layout
+    for a, b in [(3, 200), (70, 71), (64, 127), (5, 250)]:
+        codes[0, b] = np.nextafter(codes[0, a], np.float32(np.inf))
+    codes[1, 9] = codes[1, 140]          # exact duplicate in a later stage
+    # vectors sitting exactly on a code, and midway between two codes
+    x[:, :300] = codes[0, rng.integers(0, P, 300)].T
+    mid = 0.5 * (codes[0, 10] + codes[0, 11])
+    x[:, 300:340] = mid[:, None]
+    # magnitude extremes (each on its own codebook scale)
+    x[:, 400:500] *= np.float32(1e-20)
+    x[:, 500:600] *= np.float32(1e17)
+    x[0, 600] = np.nan
+    x[1, 601] = np.inf
+    x[:, 602] = -np.inf
+    idx_o, rec_o = orc.rvq_assign(x, codes)
+    idx, rec = cs.rvq_assign(torch.tensor(x, device=dev), torch.tensor(codes, device=dev))
+    assert np.array_equal(idx.cpu().numpy().astype(np.uint16), idx_o)
+    assert np.array_equal(rec.cpu().numpy(), rec_o, equal_nan=True)
+    # a non-finite code: that stage is decided by the exact scan
+    codes2 = codes.copy()
+    codes2[2, 17, 0] = np.inf
+    idx_o, rec_o = orc.rvq_assign(x, codes2)
+    idx, rec = cs.rvq_assign(torch.tensor(x, device=dev), torch.tensor(codes2, device=dev))
+    assert np.array_equal(idx.cpu().numpy().astype(np.uint16), idx_o)
+    assert np.array_equal(rec.cpu().numpy(), rec_o, equal_nan=True)
+    # tiny-scale codebook (values ~1e-20: M is floored, ties go to the exact scan)
+    small = (codes * np.float32(1e-20)).astype(np.float32)
+    xs = (x[:, :2000] * np.float32(1e-20)).astype(np.float32)
+    idx_o, rec_o = orc.rvq_assign(xs, small)
+    idx, rec = cs.rvq_assign(torch.tensor(xs, device=dev), torch.tensor(small, device=dev))
+    assert np.array_equal(idx.cpu().numpy().astype(np.uint16), idx_o)
+    assert np.array_equal(rec.cpu().numpy(), rec_o, equal_nan=True)
+
+
 def test_rvq_parity_c4_sample(env):
     """C4 codebook shape (4 x 256, log-scale and quaternion) on 100k Gaussians."""
     sc = synth.scannet_scene(0, n=100_000)
