@@ -161,19 +161,22 @@ __device__ __forceinline__ bool bwd_pair_packed(BPix2 &P, int j, float dx, f2_t 
   float rc0, rc1;  // alpha <= alpha_max < 1 (R1)
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc1) : "f"(hi2(OM)));
-  const f2_t TJ = mul2(P.T, pk2(rc0, rc1));
-  const f2_t W = mul2(AL, TJ);
+  // T_j = T_{j+1} / (1 - alpha_j), updated in place (P.T is T_j from here on;
+  // "+l" keeps the loop-carried pair in its registers: no copies per entry)
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(P.T) : "l"(pk2(rc0, rc1)));
+  const f2_t W = mul2(AL, P.T);
   const f2_t VV = fma2(pk2(r2.x, r2.x), P.gr,
                        fma2(pk2(r2.y, r2.y), P.gg,
                             fma2(pk2(r2.z, r2.z), P.gb, fma2(pk2(r1.w, r1.w), P.gd, P.gs))));
-  const f2_t D0 = mul2(TJ, sub2(VV, P.B));
+  const f2_t D0 = mul2(P.T, sub2(VV, P.B));
   // R23: no gradient through a capped alpha (a non-compositing pixel has
   // alpha = G = 0, so its dL/dalpha only ever meets zero factors)
   const f2_t DL = pk2(ar0 < amax ? lo2(D0) : 0.0f, ar1 < amax ? hi2(D0) : 0.0f);
   const f2_t AV = mul2(AL, DL);
   const f2_t GD = mul2(G, DL);
-  P.B = fma2(AL, VV, mul2(OM, P.B));
-  P.T = TJ;
+  // B_{j-1} = alpha v + (1 - alpha) B_j, in place (same roundings as fma2(AL, VV, mul2(OM, B)))
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(P.B) : "l"(OM));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(P.B) : "l"(AL), "l"(VV));
   const f2_t TT = mul2(AV, DY);   // a dy
   const f2_t T2 = mul2(TT, DY);   // a dy^2
   const f2_t WD = mul2(W, P.gd), WR = mul2(W, P.gr), WG = mul2(W, P.gg), WB = mul2(W, P.gb);
@@ -387,8 +390,11 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
       const uint32_t bml = lane < cnt ? __float_as_uint(rb[lane * 4 + 3].z) : 0u;
       uint32_t todo = __ballot_sync(0xffffffffu, ((bml >> blk) & 1u) && b * kBB + lane < wmax);
       while (todo) {  // back to front
-        const int e = 31 - __clz(todo);
-        todo ^= 1u << e;
+        int e;  // the highest set bit (bfind = 31 - clz in one instruction)
+        asm("bfind.u32 %0, %1;" : "=r"(e) : "r"(todo));
+        uint32_t below;  // bits 0 .. e-1
+        asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(e));
+        todo &= below;
         const int j = b * kBB + e;
         const float4 r0 = rb[e * 4 + 0];
         const float4 r1 = rb[e * 4 + 1];
