@@ -359,7 +359,8 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     uint32_t pm = 0;                   // entries of this batch with partials in part[s][wid]
     if (work) {
       const float4 *rb = sm.buf[s];
-      // sum the rows of the nq pending entries (entry indices packed in ents) into
+      // sum the rows of the nq pending entries (entry indices packed in ents, the
+      // first entry in the highest used byte) into
       // part[s][wid]: lane r < nq*kV owns row r (one pass, kG*kV <= 32)
       auto reduce = [&](int nq, uint32_t ents) {
         __syncwarp();
@@ -379,7 +380,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
           }
           asm("add.rn.f32x2 %0, %0, %1;" : "+l"(s01) : "l"(s23));
           const float sum = __uint_as_float((uint32_t)s01) + __uint_as_float((uint32_t)(s01 >> 32));
-          sm.part[s][wid][(ents >> (8 * q)) & 0xffu][c] = sum;
+          sm.part[s][wid][(ents >> (8 * (nq - 1 - q))) & 0xffu][c] = sum;
         }
         __syncwarp();
       };
@@ -411,8 +412,10 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
         // every lane writes its (possibly zero) partials as row nq*kV + c
 #pragma unroll
         for (int c = 0; c < kV; c++) red[nq * kV + c][lane] = v[c];
-        ents |= (uint32_t)e << (8 * nq);
-        pm |= 1u << e;
+        ents = ents * 256u + (uint32_t)e;  // entry q of the group in byte nq - 1 - q
+        uint32_t bit;
+        asm("bmsk.clamp.b32 %0, %1, 1;" : "=r"(bit) : "r"(e));
+        pm |= bit;
         if (++nq == kG) {
           reduce(nq, ents);
           nq = 0;

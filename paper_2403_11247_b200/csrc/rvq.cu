@@ -334,28 +334,51 @@ static cudaError_t run_rvq(const float *x, int64_t n, const int64_t *n_dev, cons
   return cudaGetLastError();
 }
 
+// k_rvq_chunked with S lanes per vector group; false if the shape does not fit
+// (P % (8 S), shared memory, 16-byte aligned codebook for the TMA copies)
+template <int D, int S>
+static bool try_chunked(const float *x, int64_t n, const int64_t *n_dev, const float *codes,
+                        int L, int P, void *idx, int idx_bytes, float *recon, cudaStream_t s,
+                        cudaError_t &err) {
+  constexpr int VP = D <= 4 ? CSPLAT_RVQ_VP : 1;  // vector pairs per thread
+  const size_t chunked_bytes = (size_t)L * S * ((P / S) * D + 4) * sizeof(float);
+  if (!(P % (8 * S) == 0 && chunked_bytes <= 200 * 1024 &&
+        (reinterpret_cast<uintptr_t>(codes) & 15u) == 0))
+    return false;
+  if (chunked_bytes > 48 * 1024) {
+    err = cudaFuncSetAttribute(k_rvq_chunked<D, S, VP>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chunked_bytes);
+    if (err != cudaSuccess) return true;
+  }
+  const int64_t threads = (n + 2 * VP - 1) / (2 * VP) * S;
+  const int64_t blocks = (threads + kRvqThreads - 1) / kRvqThreads;
+  k_rvq_chunked<D, S, VP><<<(unsigned)blocks, kRvqThreads, chunked_bytes, s>>>(
+      x, n, n_dev, codes, L, P, idx, idx_bytes, recon);
+  err = cudaGetLastError();
+  return true;
+}
+
+// Lanes per vector group: splitting a stage's code scan over S lanes buys
+// warps for latency hiding but costs a log2(S)-level merge per vector and
+// stage.  Measured (B200, 4 x 256, scale / rotation): at C2's 150k vectors S = 2
+// beats S = 4 (50.9 / 60.0 vs 56.4 / 65.9 us) and S = 1 (52.6 / 68.7); at C4's
+// 1M, with warps to spare, S = 1 wins (259 / 329 vs 280 / 343 us at S = 2).
+#ifndef CSPLAT_RVQ_S1_MIN_N
+#define CSPLAT_RVQ_S1_MIN_N 400000
+#endif
 template <int D>
 static cudaError_t run_rvq_d(const float *x, int64_t n, const int64_t *n_dev, const float *codes,
                              int L, int P, void *idx, int idx_bytes, float *recon,
                              cudaStream_t s) {
-  constexpr int S = 4;
-  const size_t chunked_bytes = (size_t)L * S * ((P / S) * D + 4) * sizeof(float);
-  // TMA chunk copies need 16-byte aligned sources and sizes
-  if (P % (8 * S) == 0 && chunked_bytes <= 200 * 1024 &&
-      (reinterpret_cast<uintptr_t>(codes) & 15u) == 0) {
-    if (chunked_bytes > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(k_rvq_chunked<D, S, (D <= 4 ? CSPLAT_RVQ_VP : 1)>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)chunked_bytes);
-      if (e != cudaSuccess) return e;
-    }
-    constexpr int VP = D <= 4 ? CSPLAT_RVQ_VP : 1;  // vector pairs per thread
-    const int64_t threads = (n + 2 * VP - 1) / (2 * VP) * S;
-    const int64_t blocks = (threads + kRvqThreads - 1) / kRvqThreads;
-    k_rvq_chunked<D, S, VP><<<(unsigned)blocks, kRvqThreads, chunked_bytes, s>>>(
-        x, n, n_dev, codes, L, P, idx, idx_bytes, recon);
-    return cudaGetLastError();
-  }
+  cudaError_t e = cudaSuccess;
+#ifdef CSPLAT_RVQ_S  // tuning builds: one fixed group size
+  if (try_chunked<D, CSPLAT_RVQ_S>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s, e)) return e;
+#else
+  if (n >= CSPLAT_RVQ_S1_MIN_N &&
+      try_chunked<D, 1>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s, e))
+    return e;
+  if (try_chunked<D, 2>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s, e)) return e;
+#endif
   if (P >= 16) return run_rvq<D, 4>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s);
   return run_rvq<D, 1>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s);
 }
