@@ -56,8 +56,11 @@ __device__ __forceinline__ void block_argmin4(float d0, float d1, float d2, floa
 #ifndef CSPLAT_RVQ_MINB
 #define CSPLAT_RVQ_MINB 3  // 3 CTAs (24 warps) per SM: 80 registers, a few spills (114.8 vs 121 us)
 #endif
+#ifndef CSPLAT_RVQ_MINB_S2
+#define CSPLAT_RVQ_MINB_S2 2  // S = 2 (C2-sized inputs): 128 registers, in-step 106.5 -> 104.4 us
+#endif
 template <int D, int S, int VP>
-__global__ void __launch_bounds__(kRvqThreads, CSPLAT_RVQ_MINB) k_rvq_chunked(
+__global__ void __launch_bounds__(kRvqThreads, S == 2 ? CSPLAT_RVQ_MINB_S2 : CSPLAT_RVQ_MINB) k_rvq_chunked(
     const float *__restrict__ x, int64_t n, const int64_t *__restrict__ n_dev,
     const float *__restrict__ codes_g, int L, int P, void *__restrict__ idx, int idx_bytes,
     float *__restrict__ recon) {
@@ -340,7 +343,10 @@ template <int D, int S>
 static bool try_chunked(const float *x, int64_t n, const int64_t *n_dev, const float *codes,
                         int L, int P, void *idx, int idx_bytes, float *recon, cudaStream_t s,
                         cudaError_t &err) {
-  constexpr int VP = D <= 4 ? CSPLAT_RVQ_VP : 1;  // vector pairs per thread
+#ifndef CSPLAT_RVQ_VP3
+#define CSPLAT_RVQ_VP3 CSPLAT_RVQ_VP
+#endif
+  constexpr int VP = D == 3 ? CSPLAT_RVQ_VP3 : (D <= 4 ? CSPLAT_RVQ_VP : 1);  // vector pairs per thread
   const size_t chunked_bytes = (size_t)L * S * ((P / S) * D + 4) * sizeof(float);
   if (!(P % (8 * S) == 0 && chunked_bytes <= 200 * 1024 &&
         (reinterpret_cast<uintptr_t>(codes) & 15u) == 0))
