@@ -348,6 +348,29 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   __shared__ uint32_t fill, s_start, s_end;
   const int64_t tile = blockIdx.x;
   const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
+#ifndef CSPLAT_BIN_SMEM_SORT
+  // the common case first: a list that fits the threads' registers is sorted
+  // BEFORE the look-back (the sort needs only the tile's own count), so by the
+  // time the look-back runs the preceding tiles have mostly published and the
+  // CTA does not idle at a barrier behind it
+  const uint32_t cnt_t = w.cur[tile];
+  const bool reg_path = cnt_t <= 2u * kSortThreads;  // block-uniform
+  unsigned long long x0 = ~0ull, x1 = ~0ull;
+  if (reg_path && cnt_t > 0) {
+    const int t = threadIdx.x, n0 = (int)cnt_t;
+    const unsigned long long *bk = w.bucket + tile * kBucketCap;
+    if (2 * t + 1 < n0) {
+      const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(bk)[t];
+      x0 = v.x;
+      x1 = v.y;
+    } else if (2 * t < n0) {
+      x0 = bk[2 * t];
+    }
+    int np2 = 2;
+    while (np2 < n0) np2 <<= 1;
+    sort_regs256(x0, x1, np2, reinterpret_cast<unsigned long long(*)[2 * kSortThreads]>(sk));
+  }
+#endif
   if (threadIdx.x < 32) {  // the tile's output offset: a look-back over the preceding tiles
     const int lane = threadIdx.x;
     const unsigned long long cnt = w.cur[tile];
@@ -385,20 +408,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   const int len = (int)(end - start);  // < the tile's pair count only beyond the capacity
   if (len == 0) return;
 #ifndef CSPLAT_BIN_SMEM_SORT
-  if (len <= 2 * kSortThreads) {  // the common case: the list fits the threads' registers
+  if (reg_path) {  // sorted above; len < cnt_t only beyond the capacity (reported)
     const int t = threadIdx.x;
-    const unsigned long long *bk = w.bucket + tile * kBucketCap;
-    unsigned long long x0 = ~0ull, x1 = ~0ull;
-    if (2 * t + 1 < len) {
-      const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(bk)[t];
-      x0 = v.x;
-      x1 = v.y;
-    } else if (2 * t < len) {
-      x0 = bk[2 * t];
-    }
-    int np2 = 2;
-    while (np2 < len) np2 <<= 1;
-    sort_regs256(x0, x1, np2, reinterpret_cast<unsigned long long(*)[2 * kSortThreads]>(sk));
     if (2 * t < len) emit_pair(x0, (int64_t)start + 2 * t, rec4, pair_gid, pair_rec, X0, Y0);
     if (2 * t + 1 < len) emit_pair(x1, (int64_t)start + 2 * t + 1, rec4, pair_gid, pair_rec, X0, Y0);
     return;
