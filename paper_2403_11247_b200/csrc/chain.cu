@@ -217,10 +217,23 @@ __global__ void __launch_bounds__(256, 3) k_chain(
   }
   const bool accu = (flags & CSPLAT_ACCUMULATE) != 0;
   if (!(flags & CSPLAT_POSE_ONLY) && i < n && (alive || !accu)) {
+    if (accu) {
+      // all 15 old values first: the planes may alias as far as the compiler
+      // knows, so interleaved += would serialise 15 load -> store round trips
+      // (the C5 window accumulates 64 views: 50 -> ~20 us per view)
+      float old[15];
+      auto get = [&](const float *plane, int k, int64_t off) { old[k] = plane ? plane[off] : 0.f; };
+      for (int k = 0; k < 3; k++) get(out.mean, k, (int64_t)k * n + i);
+      get(out.opacity, 3, i);
+      for (int k = 0; k < 3; k++) get(out.rgb, 4 + k, (int64_t)k * n + i);
+      for (int k = 0; k < 3; k++) get(out.log_scale, 7 + k, (int64_t)k * n + i);
+      for (int k = 0; k < 4; k++) get(out.quat, 10 + k, (int64_t)k * n + i);
+      get(out.mask, 14, i);
+#pragma unroll
+      for (int k = 0; k < 15; k++) g[k] += old[k];
+    }
     auto put = [&](float *plane, int k, int64_t off) {
-      if (!plane) return;
-      if (accu) plane[off] += g[k];
-      else plane[off] = g[k];
+      if (plane) plane[off] = g[k];
     };
     for (int k = 0; k < 3; k++) put(out.mean, k, (int64_t)k * n + i);
     put(out.opacity, 3, i);
