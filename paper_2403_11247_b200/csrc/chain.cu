@@ -50,6 +50,20 @@ __global__ void __launch_bounds__(256, 3) k_chain(
                      ((a0.x != 0.f) | (a0.y != 0.f) | (a0.z != 0.f) | (a0.w != 0.f) |
                       (a1.x != 0.f) | (a1.y != 0.f) | (a1.z != 0.f) | (a1.w != 0.f) |
                       (a2.x != 0.f) | (a2.y != 0.f));
+  // ACCUMULATE: all 15 old gradient values are loaded up front -- the planes
+  // may alias as far as the compiler knows, so an interleaved += would
+  // serialise 15 load -> store round trips (C5: 50 -> ~28 us per view), and
+  // issued here they overlap the R-VQ decode and the chain arithmetic
+  float old[15];
+  if (alive && (flags & CSPLAT_ACCUMULATE) && !(flags & CSPLAT_POSE_ONLY)) {
+    auto get = [&](const float *plane, int k, int64_t off) { old[k] = plane ? plane[off] : 0.f; };
+    for (int k = 0; k < 3; k++) get(out.mean, k, (int64_t)k * n + i);
+    get(out.opacity, 3, i);
+    for (int k = 0; k < 3; k++) get(out.rgb, 4 + k, (int64_t)k * n + i);
+    for (int k = 0; k < 3; k++) get(out.log_scale, 7 + k, (int64_t)k * n + i);
+    for (int k = 0; k < 4; k++) get(out.quat, 10 + k, (int64_t)k * n + i);
+    get(out.mask, 14, i);
+  }
   if (alive) {
     // k_render_bwd accumulates the raw moments Sx, Sy, Sxx, Sxy, Syy of
     // a = alpha dL/dalpha; map them through the record's DA conic
@@ -218,17 +232,6 @@ __global__ void __launch_bounds__(256, 3) k_chain(
   const bool accu = (flags & CSPLAT_ACCUMULATE) != 0;
   if (!(flags & CSPLAT_POSE_ONLY) && i < n && (alive || !accu)) {
     if (accu) {
-      // all 15 old values first: the planes may alias as far as the compiler
-      // knows, so interleaved += would serialise 15 load -> store round trips
-      // (the C5 window accumulates 64 views: 50 -> ~20 us per view)
-      float old[15];
-      auto get = [&](const float *plane, int k, int64_t off) { old[k] = plane ? plane[off] : 0.f; };
-      for (int k = 0; k < 3; k++) get(out.mean, k, (int64_t)k * n + i);
-      get(out.opacity, 3, i);
-      for (int k = 0; k < 3; k++) get(out.rgb, 4 + k, (int64_t)k * n + i);
-      for (int k = 0; k < 3; k++) get(out.log_scale, 7 + k, (int64_t)k * n + i);
-      for (int k = 0; k < 4; k++) get(out.quat, 10 + k, (int64_t)k * n + i);
-      get(out.mask, 14, i);
 #pragma unroll
       for (int k = 0; k < 15; k++) g[k] += old[k];
     }
