@@ -146,6 +146,31 @@ int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csp
                      uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
                      size_t ws_bytes, void *stream);
 
+/* a1 + a2-decode + a3 + a4 + a5 in one call: csplat_project followed by
+ * csplat_bin_tiles_active, with the bucket pass of the binning (the
+ * warp-cooperative expansion of each Gaussian's tile rectangle into the tile
+ * buckets) fused into the projection kernel while the records are still in
+ * registers.  Outputs are bit-identical to the two calls: rec and count as
+ * csplat_project (same layout, ownership and alignment), pair_gid, pair_rec,
+ * tile_range and n_pairs_dev as csplat_bin_tiles_active (tile_active may be
+ * NULL = every tile).  n = g->n; ws: csplat_workspace_bytes(CSPLAT_OP_BIN_TILES,
+ * g->n, pair_capacity, cam).  flags: CSPLAT_SYNC as csplat_bin_tiles.
+ * Errors as the two calls. */
+int csplat_project_bin(const csplat_gaussians *g, const csplat_codebook *cb,
+                       const csplat_camera *cam, const csplat_view *view,
+                       const csplat_params *prm, void *rec, int32_t *count,
+                       const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid,
+                       void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                       uint32_t flags, void *ws, size_t ws_bytes, void *stream);
+
+/* csplat_project_bin with the view in DEVICE memory (see csplat_project_dv). */
+int csplat_project_bin_dv(const csplat_gaussians *g, const csplat_codebook *cb,
+                          const csplat_camera *cam, const float *view_dev,
+                          const csplat_params *prm, void *rec, int32_t *count,
+                          const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid,
+                          void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                          uint32_t flags, void *ws, size_t ws_bytes, void *stream);
+
 /* csplat_bin_tiles restricted to the tiles whose bit is set in tile_active
  * (device uint32[ceil(T/32)], bit t & 31 of word t >> 5; NULL = every tile):
  * the pairs of the other tiles are not emitted and their ranges are empty, so

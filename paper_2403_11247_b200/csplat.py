@@ -98,6 +98,9 @@ def lib():
         L.csplat_ba_patch_loss.argtypes = [vp] * 6 + [i64, i64, vp, C.c_float, C.c_float] + \
             [vp] * 5
         L.csplat_project_dv.argtypes = [vp] * 8
+        L.csplat_project_bin.argtypes = [vp] * 8 + [i64, vp, vp, vp, vp, u32, vp, C.c_size_t, vp]
+        L.csplat_project_bin_dv.argtypes = [vp] * 8 + [i64, vp, vp, vp, vp, u32, vp, C.c_size_t,
+                                                        vp]
         L.csplat_render_bwd_dv.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_pose_step.argtypes = [vp, vp, C.c_float, C.c_float, vp]
         L.csplat_tracking_bwd.argtypes = [vp] * 17 + [C.c_float, C.c_float, u32, vp, vp, vp,
@@ -225,6 +228,39 @@ def project(g: GaussianMap, cam: dict, v, prm: Params | None = None, cb: Codeboo
                                 C.byref(view(v)), C.byref(prm or params()), _ptr(rec),
                                 _ptr(count), _stream(stream)), "csplat_project")
     return rec[:n], count[:n]
+
+
+def project_bin(g: GaussianMap, cam: dict, v, capacity: int, prm: Params | None = None,
+                cb: CodebookT | None = None, rec=None, count=None, ws=None, out=None, sync=True,
+                stream=None, tile_active=None):
+    """a1+a2(decode)+a3+a4+a5 in one call (the bucket pass fused into the projection):
+    the outputs of project() and bin_tiles().  Returns (rec, count, bin dict)."""
+    n = g.n
+    dev = g.opacity.device
+    rec = rec if rec is not None else torch.empty((max(n, 1), 16), dtype=torch.int32, device=dev)
+    count = count if count is not None else torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    tx, ty = tiles(cam)
+    if out is None:
+        out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
+                   pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
+                   tile_range=torch.empty((tx * ty, 2), dtype=torch.int32, device=dev),
+                   n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_BIN_TILES, n, capacity, cam), dtype=torch.uint8,
+                         device=dev)
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    tail = (_ptr(tile_active), capacity, _ptr(out["pair_gid"]), _ptr(out["pair_rec"]),
+            _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]), SYNC if sync else 0, _ptr(ws),
+            ws.numel(), _stream(stream))
+    if _on_device(v):
+        _check(lib().csplat_project_bin_dv(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
+                                           _ptr(v), C.byref(prm or params()), _ptr(rec),
+                                           _ptr(count), *tail), "csplat_project_bin_dv")
+    else:
+        _check(lib().csplat_project_bin(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
+                                        C.byref(view(v)), C.byref(prm or params()), _ptr(rec),
+                                        _ptr(count), *tail), "csplat_project_bin")
+    return rec[:n], count[:n], out
 
 
 def _on_device(v) -> bool:

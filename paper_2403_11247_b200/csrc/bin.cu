@@ -22,27 +22,15 @@
 //               global memory (pathological inputs only).
 // Keys are unique (the index is in the low word), so the order is unique and
 // bit-exact: (tile, bits(z_c), index) ascending.
-#include "common.cuh"
+#include "bin_dev.cuh"
 
 namespace csplat {
 
 constexpr int kCtaCap = 2048;      // keys per tile sorted in shared memory (16 KB)
 constexpr int kSortThreads = 128;  // threads per tile in k_sort_tiles
-constexpr int kBucketCap = 512;    // bucket slots per tile; later pairs go to the overflow list
-
-struct BinWs {
-  uint32_t *cur;                     // [T] pairs per tile (atomic cursor)
-  uint32_t *ovf_n;                   // overflow-list length
-  unsigned long long *status;        // [T] look-back words of the tile-range scan
-  unsigned long long *bucket;        // [T][kBucketCap] keys
-  uint32_t *ovf_tile;                // [cap] tile of each overflow entry
-  unsigned long long *ovf_key;       // [cap] its key
-  unsigned long long *keys;          // [cap] global-memory sort scratch (tiles > kCtaCap)
-};
-
 static inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-static BinWs carve(void *ws, int64_t cap, int64_t T) {
+BinWs bin_carve(void *ws, int64_t cap, int64_t T) {
   char *p = static_cast<char *>(ws);
   const size_t c = (size_t)(cap > 0 ? cap : 1);
   BinWs w;
@@ -62,6 +50,11 @@ static BinWs carve(void *ws, int64_t cap, int64_t T) {
   return w;
 }
 
+cudaError_t bin_reset(const BinWs &w, int64_t T, cudaStream_t s) {
+  // cur, ovf_n and status are contiguous at the head of the workspace
+  return cudaMemsetAsync(w.cur, 0, align_up(T * 4) + align_up(4) + align_up(T * 8), s);
+}
+
 size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam) {
   (void)n;
   const CamInfo ci = cam_info(cam);
@@ -69,59 +62,6 @@ size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam) {
   const size_t c = (size_t)(cap > 0 ? cap : 1);
   return align_up(T * 4) + align_up(4) + align_up(T * 8) + align_up((size_t)T * kBucketCap * 8) +
          align_up(c * 4) + 2 * align_up(c * 8);
-}
-
-// Warp-cooperative expansion of 32 Gaussians' tile rectangles.  Calls
-// f(gid, tile, lane_owner_zbits) once per (Gaussian, tile) pair; all 32 lanes
-// must be converged on entry.
-template <typename F>
-__device__ __forceinline__ void expand_warp(int64_t base, int64_t n, const int32_t *count,
-                                            const uint4 *rec4, int tiles_x, F f) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i = base + lane;
-  int c = 0;
-  uint32_t rx = 0, ry = 0, zb = 0;
-  if (i < n) {
-    c = count[i];
-    if (c > 0) {
-      const uint4 r1 = rec4[i * 4 + 1];
-      const uint4 r3 = rec4[i * 4 + 3];
-      zb = r1.w;
-      rx = r3.x;
-      ry = r3.y;
-    }
-  }
-  int incl = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const int excl = incl - c;
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  for (int kb = 0; kb < total; kb += 32) {
-    const int k = kb + lane;
-    int owner = 0;
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-      const int cand = owner + step;
-      const int e = __shfl_sync(0xffffffffu, excl, cand & 31);
-      if (cand < 32 && e <= k) owner = cand;
-    }
-    const int oe = __shfl_sync(0xffffffffu, excl, owner);
-    const uint32_t orx = __shfl_sync(0xffffffffu, rx, owner);
-    const uint32_t ory = __shfl_sync(0xffffffffu, ry, owner);
-    const uint32_t ozb = __shfl_sync(0xffffffffu, zb, owner);
-    if (k < total) {
-      // rx = px0 | py0 << 16 (low corner), ry = px1 | py1 << 16 (high corner)
-      const int tx0 = (int)(orx & 0xffffu) / kTile, tx1 = (int)(ory & 0xffffu) / kTile;
-      const int ty0 = (int)(orx >> 16) / kTile;
-      const int w = tx1 - tx0 + 1;
-      const int li = k - oe;
-      const int tile = (ty0 + li / w) * tiles_x + tx0 + li % w;
-      f((uint32_t)(base + owner), tile, ozb);
-    }
-  }
 }
 
 // a4: every (Gaussian, tile) pair's key into the tile's bucket, or the
@@ -133,21 +73,25 @@ __global__ void __launch_bounds__(256) k_bucket(int64_t n, const int32_t *__rest
                                                 BinWs w) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i * 32 < n; i += nwarps)
-    expand_warp(i * 32, n, count, rec4, tiles_x, [&](uint32_t gid, int tile, uint32_t zb) {
-      if (active && !((active[tile >> 5] >> (tile & 31)) & 1u)) return;  // tile not sampled
-      const unsigned long long key = ((unsigned long long)zb << 32) | (unsigned long long)gid;
-      const uint32_t slot = atomicAdd(w.cur + tile, 1u);
-      if (slot < (uint32_t)kBucketCap) {
-        w.bucket[(int64_t)tile * kBucketCap + slot] = key;
-      } else {
-        const uint32_t o = atomicAdd(w.ovf_n, 1u);
-        if ((int64_t)o < cap) {  // beyond cap the pairs exceed the capacity anyway
-          w.ovf_tile[o] = (uint32_t)tile;
-          w.ovf_key[o] = key;
-        }
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = warp; b * 32 < n; b += nwarps) {
+    const int64_t i = b * 32 + lane;
+    int c = 0;
+    uint32_t rx = 0, ry = 0, zb = 0;
+    if (i < n) {
+      c = count[i];
+      if (c > 0) {
+        const uint4 r1 = rec4[i * 4 + 1];
+        const uint4 r3 = rec4[i * 4 + 3];
+        zb = r1.w;
+        rx = r3.x;
+        ry = r3.y;
       }
+    }
+    expand_warp_regs(b * 32, c, rx, ry, zb, tiles_x, [&](uint32_t gid, int tile, uint32_t z) {
+      bucket_put(w, cap, active, gid, tile, z);
     });
+  }
 }
 
 
@@ -441,15 +385,23 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   emit_sorted(a, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, pair_rec, X0, Y0);
 }
 
+cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
+                              const void *rec, uint32_t *pair_gid, void *pair_rec,
+                              uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s) {
+  k_sort_tiles<<<(unsigned)T, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
+                                                    static_cast<const uint4 *>(rec), pair_gid,
+                                                    static_cast<uint4 *>(pair_rec), tiles_x);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
                        int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid,
                        void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                        cudaStream_t s) {
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
-  BinWs w = carve(ws, cap, T);
-  // cur, ovf_n and status are contiguous at the head of the workspace
-  cudaError_t e = cudaMemsetAsync(w.cur, 0, align_up(T * 4) + align_up(4) + align_up(T * 8), s);
+  BinWs w = bin_carve(ws, cap, T);
+  cudaError_t e = bin_reset(w, T, s);
   if (e != cudaSuccess) return e;
   const uint4 *rec4 = static_cast<const uint4 *>(rec);
   int dev = 0, sms = 148;
@@ -462,10 +414,10 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   if (blocks < 1) blocks = 1;
   if (n > 0) k_bucket<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, cap,
                                                       tile_active, w);
-  k_sort_tiles<<<(unsigned)T, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap, rec4,
-                                                    pair_gid, static_cast<uint4 *>(pair_rec),
-                                                    ci.tiles_x);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
+                           n_pairs_dev, s);
 }
 
 }  // namespace csplat

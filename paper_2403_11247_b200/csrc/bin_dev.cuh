@@ -1,0 +1,91 @@
+// bin_dev.cuh -- the a4 bucket pass's device pieces, shared by the stand-alone
+// bucket kernel (bin.cu) and the fused projection + bucket kernel (project.cu,
+// csplat_project_bin): the workspace layout, the warp-cooperative expansion of
+// 32 Gaussians' tile rectangles and the bucket insert.  See bin.cu.
+#pragma once
+#include "common.cuh"
+
+namespace csplat {
+
+constexpr int kBucketCap = 512;    // bucket slots per tile; later pairs go to the overflow list
+
+struct BinWs {
+  uint32_t *cur;                     // [T] pairs per tile (atomic cursor)
+  uint32_t *ovf_n;                   // overflow-list length
+  unsigned long long *status;        // [T] look-back words of the tile-range scan
+  unsigned long long *bucket;        // [T][kBucketCap] keys
+  uint32_t *ovf_tile;                // [cap] tile of each overflow entry
+  unsigned long long *ovf_key;       // [cap] its key
+  unsigned long long *keys;          // [cap] global-memory sort scratch (tiles > kCtaCap)
+};
+
+BinWs bin_carve(void *ws, int64_t cap, int64_t T);
+// zero the cursors, the overflow length and the look-back words (one memset)
+cudaError_t bin_reset(const BinWs &w, int64_t T, cudaStream_t s);
+// a5: k_sort_tiles over the buckets filled by k_bucket or the fused projection
+cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
+                              const void *rec, uint32_t *pair_gid, void *pair_rec,
+                              uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s);
+
+// Warp-cooperative expansion of 32 Gaussians' tile rectangles.  Lane l holds
+// Gaussian base + l's pair count c, its pixel rectangle corners rx, ry (record
+// words 12, 13) and bits(z_c) zb.  Calls f(gid, tile, zb) once per (Gaussian,
+// tile) pair; all 32 lanes must be converged on entry.
+template <typename F>
+__device__ __forceinline__ void expand_warp_regs(int64_t base, int c, uint32_t rx, uint32_t ry,
+                                                 uint32_t zb, int tiles_x, F f) {
+  const int lane = threadIdx.x & 31;
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int excl = incl - c;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int kb = 0; kb < total; kb += 32) {
+    const int k = kb + lane;
+    int owner = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int cand = owner + step;
+      const int e = __shfl_sync(0xffffffffu, excl, cand & 31);
+      if (cand < 32 && e <= k) owner = cand;
+    }
+    const int oe = __shfl_sync(0xffffffffu, excl, owner);
+    const uint32_t orx = __shfl_sync(0xffffffffu, rx, owner);
+    const uint32_t ory = __shfl_sync(0xffffffffu, ry, owner);
+    const uint32_t ozb = __shfl_sync(0xffffffffu, zb, owner);
+    if (k < total) {
+      // rx = px0 | py0 << 16 (low corner), ry = px1 | py1 << 16 (high corner)
+      const int tx0 = (int)(orx & 0xffffu) / kTile, tx1 = (int)(ory & 0xffffu) / kTile;
+      const int ty0 = (int)(orx >> 16) / kTile;
+      const int w = tx1 - tx0 + 1;
+      const int li = k - oe;
+      const int tile = (ty0 + li / w) * tiles_x + tx0 + li % w;
+      f((uint32_t)(base + owner), tile, ozb);
+    }
+  }
+}
+
+// the pair's key into its tile's bucket (slot from the tile's atomic cursor),
+// or into the overflow list once the bucket is full; with an active-tile mask
+// (NEXT-4) only the pairs of active tiles
+__device__ __forceinline__ void bucket_put(const BinWs &w, int64_t cap,
+                                           const uint32_t *__restrict__ active, uint32_t gid,
+                                           int tile, uint32_t zb) {
+  if (active && !((active[tile >> 5] >> (tile & 31)) & 1u)) return;  // tile not sampled
+  const unsigned long long key = ((unsigned long long)zb << 32) | (unsigned long long)gid;
+  const uint32_t slot = atomicAdd(w.cur + tile, 1u);
+  if (slot < (uint32_t)kBucketCap) {
+    w.bucket[(int64_t)tile * kBucketCap + slot] = key;
+  } else {
+    const uint32_t o = atomicAdd(w.ovf_n, 1u);
+    if ((int64_t)o < cap) {  // beyond cap the pairs exceed the capacity anyway
+      w.ovf_tile[o] = (uint32_t)tile;
+      w.ovf_key[o] = key;
+    }
+  }
+}
+
+}  // namespace csplat

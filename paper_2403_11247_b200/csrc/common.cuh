@@ -286,6 +286,15 @@ cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
                            const float *view_dev, float tau, float dilation, void *rec,
                            int32_t *count, cudaStream_t s);
 
+// csplat_project_bin: the projection with the bucket pass fused in, then the
+// per-tile sort (same outputs as launch_project + launch_bin)
+cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
+                               const csplat_camera &cam, const csplat_view &view,
+                               const float *view_dev, float tau, float dilation, void *rec,
+                               int32_t *count, int64_t cap, const uint32_t *tile_active,
+                               uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                               int64_t *n_pairs_dev, void *ws, cudaStream_t s);
+
 size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam);
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
                        int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid,

@@ -5,7 +5,7 @@
 // the R-VQ decode gathers from the (L1/L2-resident) codebooks, and one 64-byte
 // record written as four 16-byte stores.  HBM-bound: 60 B in + 64 B + 4 B out
 // per Gaussian (raw geometry); DA keeps it at ~300 instructions per Gaussian.
-#include "common.cuh"
+#include "bin_dev.cuh"
 
 namespace csplat {
 
@@ -16,15 +16,16 @@ struct ProjConst {
   float tau, dil;
 };
 
+// Gaussian i (< n): its 64-byte record and pair count; for the fused bucket
+// pass also the count, the pixel-rectangle words and bits(z_c) (0 if culled).
 template <int LF>
-__global__ void __launch_bounds__(256) k_project(
-    int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
+__device__ __forceinline__ void project_one(
+    int64_t i, int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
     const float *__restrict__ opac, const float *__restrict__ rgb,
     const float *__restrict__ lsc, const float *__restrict__ quat,
-    const float *__restrict__ mask, DecodeArgs dec, int use_dec, ProjConst pc,
-    const float *__restrict__ view_dev, float4 *__restrict__ rec, int32_t *__restrict__ count) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+    const float *__restrict__ mask, const DecodeArgs &dec, int use_dec, ProjConst &pc,
+    const float *__restrict__ view_dev, float4 *__restrict__ rec, int32_t *__restrict__ count,
+    int &c_out, uint32_t &rx_out, uint32_t &ry_out, uint32_t &zb_out) {
   if (view_dev) {  // the view lives in device memory (graph-captured pose updates)
 #pragma unroll
     for (int k = 0; k < 12; k++) pc.V[k] = __ldg(view_dev + k);
@@ -150,13 +151,44 @@ __global__ void __launch_bounds__(256) k_project(
   // inclusive pixel rectangle as two u16x2 corners (low | high), DESIGN.md §4
   r[3] = make_float4(__uint_as_float((uint32_t)px0 | ((uint32_t)py0 << 16)),
                      __uint_as_float((uint32_t)px1 | ((uint32_t)py1 << 16)), 0.f, 0.f);
-  count[i] = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+  c_out = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+  rx_out = (uint32_t)px0 | ((uint32_t)py0 << 16);
+  ry_out = (uint32_t)px1 | ((uint32_t)py1 << 16);
+  zb_out = __float_as_uint(zc);
+  count[i] = c_out;
 }
 
-cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
-                           const csplat_camera &cam, const csplat_view &view,
-                           const float *view_dev, float tau, float dilation, void *rec,
-                           int32_t *count, cudaStream_t s) {
+// a1 + a2-decode + a3 (+ a4, BIN): one thread per Gaussian; with BIN the warp
+// then spreads its 32 Gaussians' (tile, Gaussian) pairs into the tile buckets
+// (bin_dev.cuh) while the records are still in registers -- the stand-alone
+// bucket pass's re-read of count and record and its launch go away.
+template <int LF, bool BIN>
+__global__ void __launch_bounds__(256) k_project(
+    int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
+    const float *__restrict__ opac, const float *__restrict__ rgb,
+    const float *__restrict__ lsc, const float *__restrict__ quat,
+    const float *__restrict__ mask, DecodeArgs dec, int use_dec, ProjConst pc,
+    const float *__restrict__ view_dev, float4 *__restrict__ rec, int32_t *__restrict__ count,
+    BinWs w, int tiles_x, int64_t cap, const uint32_t *__restrict__ active) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int c = 0;
+  uint32_t rx = 0, ry = 0, zb = 0;
+  if (i < n)
+    project_one<LF>(i, n, n_dev, mean, opac, rgb, lsc, quat, mask, dec, use_dec, pc, view_dev,
+                    rec, count, c, rx, ry, zb);
+  if constexpr (BIN) {
+    expand_warp_regs(i - (threadIdx.x & 31), c, rx, ry, zb, tiles_x,
+                     [&](uint32_t gid, int tile, uint32_t z) {
+                       bucket_put(w, cap, active, gid, tile, z);
+                     });
+  }
+}
+
+static cudaError_t launch_project_impl(const csplat_gaussians &g, const DecodeArgs *dec,
+                                      const csplat_camera &cam, const csplat_view &view,
+                                      const float *view_dev, float tau, float dilation,
+                                      void *rec, int32_t *count, const BinWs *bw, int tiles_x,
+                                      int64_t cap, const uint32_t *active, cudaStream_t s) {
   if (g.n == 0) return cudaSuccess;
   ProjConst pc;
   for (int k = 0; k < 12; k++) pc.V[k] = view.m[k];
@@ -179,16 +211,44 @@ cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
   if (dec) d = *dec;
   const int threads = 256;
   const int64_t blocks = (g.n + threads - 1) / threads;
-  auto kern = k_project<0>;
+  const bool bin = bw != nullptr;
+  auto kern = bin ? k_project<0, true> : k_project<0, false>;
   switch (rvq_lf(dec)) {
-    case 4: kern = k_project<4>; break;
-    case 2: kern = k_project<2>; break;
+    case 4: kern = bin ? k_project<4, true> : k_project<4, false>; break;
+    case 2: kern = bin ? k_project<2, true> : k_project<2, false>; break;
     default: break;
   }
   kern<<<(unsigned)blocks, threads, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.rgb, g.log_scale,
                                             g.quat, g.mask, d, dec ? 1 : 0, pc, view_dev,
-                                            reinterpret_cast<float4 *>(rec), count);
+                                            reinterpret_cast<float4 *>(rec), count,
+                                            bin ? *bw : BinWs{}, tiles_x, cap, active);
   return cudaGetLastError();
+}
+
+cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
+                           const csplat_camera &cam, const csplat_view &view,
+                           const float *view_dev, float tau, float dilation, void *rec,
+                           int32_t *count, cudaStream_t s) {
+  return launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, nullptr, 0,
+                             0, nullptr, s);
+}
+
+cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
+                               const csplat_camera &cam, const csplat_view &view,
+                               const float *view_dev, float tau, float dilation, void *rec,
+                               int32_t *count, int64_t cap, const uint32_t *tile_active,
+                               uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                               int64_t *n_pairs_dev, void *ws, cudaStream_t s) {
+  const CamInfo ci = cam_info(cam);
+  const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
+  BinWs w = bin_carve(ws, cap, T);
+  cudaError_t e = bin_reset(w, T, s);
+  if (e != cudaSuccess) return e;
+  e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
+                          ci.tiles_x, cap, tile_active, s);
+  if (e != cudaSuccess) return e;
+  return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
+                           n_pairs_dev, s);
 }
 
 }  // namespace csplat

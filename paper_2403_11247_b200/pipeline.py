@@ -19,6 +19,10 @@ import torch
 from . import csplat as cs
 
 
+# csplat_project_bin (projection with the bucket pass fused in) on the step's
+# path; CSPLAT_FUSED_BIN=0 selects the separate csplat_project + csplat_bin_tiles
+FUSED_BIN = os.environ.get("CSPLAT_FUSED_BIN", "1") == "1"
+
 class RenderStep:
     def __init__(self, planes: dict, cam: dict, codebook: dict | None, device="cuda",
                  prm: cs.Params | None = None, pair_capacity: int | None = None,
@@ -139,6 +143,13 @@ class RenderStep:
 
     def project_bin(self, view, sync_probe=False, tile_active=None):
         g = self.pruned
+        if FUSED_BIN and not sync_probe:  # the bucket pass inside the projection kernel
+            cs.project_bin(g, self.cam, view, self.capacity, self.prm, self.cb, rec=self.rec,
+                           count=self.count, ws=self.ws_bin,
+                           out=dict(pair_gid=self.pair_gid, pair_rec=self.pair_rec,
+                                    tile_range=self.tile_range, n_pairs_dev=self.n_pairs),
+                           sync=False, tile_active=tile_active)
+            return
         cs.project(g, self.cam, view, self.prm, self.cb, rec=self.rec, count=self.count)
         if sync_probe:
             big = max(self.capacity, 64 * self.n + 4096)

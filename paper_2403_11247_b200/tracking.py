@@ -106,10 +106,7 @@ class Tracker:
         prologue, gated-out pixels not replayed) -> device pose step."""
         st = self.step
         g = st.pruned
-        cs.project(g, st.cam, view_dev, st.prm, st.cb, rec=st.rec, count=st.count)
-        cs.bin_tiles(st.rec, st.count, st.cam, st.capacity, ws=st.ws_bin,
-                     out=dict(pair_gid=st.pair_gid, pair_rec=st.pair_rec,
-                              tile_range=st.tile_range, n_pairs_dev=st.n_pairs), sync=False)
+        st.project_bin(view_dev)
         st.forward()
         cs.tracking_bwd(g, st.cam, view_dev, st.rec, st.pair_rec, st.tile_range, st.img,
                         self.obs_color, self.obs_depth, self.n_valid, st.prm, st.cb,

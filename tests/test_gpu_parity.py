@@ -335,6 +335,62 @@ def test_capacity_overflow_reported(env):
         cs.bin_tiles(rec, cnt, sc.cam, capacity=5, sync=True)
 
 
+@pytest.mark.parametrize("which", ["tiny", "mid", "replica", "window"])
+def test_project_bin_fused_matches_separate_calls(env, which):
+    """csplat_project_bin (the bucket pass fused into the projection kernel) is
+    bit-identical to csplat_project + csplat_bin_tiles(_active): records, counts,
+    pair list, pair payload, tile ranges, pair total; host and device views; with
+    an active-tile mask; and both match the oracle's list on the small scenes."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = {"tiny": lambda: synth.tiny_scene(1), "mid": lambda: synth.mid_scene(3),
+          "replica": lambda: synth.replica_scene(0),
+          "window": lambda: synth.window_scene(0, n=200_000, n_keyframes=8)}[which]()
+    v = sc.views[min(3, len(sc.views) - 1)]
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec, cnt = cs.project(g, sc.cam, v)
+    cap = int(cnt.sum().item()) + 64
+    ref = cs.bin_tiles(rec, cnt, sc.cam, capacity=cap)
+    vd = torch.tensor(np.asarray(v, dtype=np.float32).reshape(-1)[:12], device=dev)
+    for view_arg in (v, vd):
+        rec2, cnt2, out = cs.project_bin(g, sc.cam, view_arg, cap, sync=True)
+        torch.cuda.synchronize()
+        assert torch.equal(rec2, rec) and torch.equal(cnt2, cnt)
+        n = int(out["n_pairs_dev"].item())
+        assert n == int(ref["n_pairs_dev"].item())
+        assert torch.equal(out["pair_gid"][:n], ref["pair_gid"][:n])
+        assert torch.equal(out["pair_rec"][:n], ref["pair_rec"][:n])
+        assert torch.equal(out["tile_range"], ref["tile_range"])
+    # active tiles: every third tile
+    tx, ty = cs.tiles(sc.cam)
+    T = tx * ty
+    bits = np.zeros((T + 31) // 32, dtype=np.uint32)
+    for t in range(0, T, 3):
+        bits[t >> 5] |= np.uint32(1 << (t & 31))
+    act = torch.tensor(bits.view(np.int32), device=dev)
+    ref_a = cs.bin_tiles(rec, cnt, sc.cam, capacity=cap, tile_active=act)
+    _, _, out_a = cs.project_bin(g, sc.cam, v, cap, sync=True, tile_active=act)
+    torch.cuda.synchronize()
+    n = int(out_a["n_pairs_dev"].item())
+    assert n == int(ref_a["n_pairs_dev"].item())
+    assert torch.equal(out_a["pair_gid"][:n], ref_a["pair_gid"][:n])
+    assert torch.equal(out_a["tile_range"], ref_a["tile_range"])
+    if which in ("tiny", "mid"):
+        rec_o, cnt_o = orc.project(orc.Scene(**sc.planes()), sc.cam, v)
+        gid_o, rng_o = orc.bin_tiles(rec_o, cnt_o, sc.cam)
+        rec2, _, out = cs.project_bin(g, sc.cam, v, cap, sync=True)
+        assert np.array_equal(rec2.cpu().numpy().view(np.uint32), rec_o)
+        assert np.array_equal(out["pair_gid"][:len(gid_o)].cpu().numpy().view(np.uint32), gid_o)
+        assert np.array_equal(out["tile_range"].cpu().numpy().view(np.uint32), rng_o)
+
+
+def test_project_bin_capacity_overflow_reported(env):
+    torch, cs, dev = env["torch"], env["cs"], env["dev"]
+    sc = synth.tiny_scene(0)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    with pytest.raises(cs.CsplatError, match="capacity"):
+        cs.project_bin(g, sc.cam, sc.views[0], 5, sync=True)
+
+
 def test_pipeline_step_matches_stages(env):
     """The graph-capturable RenderStep (prune -> R-VQ -> project -> bin -> fwd ->
     bwd) reproduces the oracle on the pruned, decoded map."""
