@@ -94,6 +94,25 @@ class RenderStep:
             self._alloc_pairs(cap)
         return worst
 
+    def view_slot(self):
+        """A second set of per-view buffers (records, pairs, images, workspaces)
+        over the SAME prepared map, codebook indices, upstream and gradient
+        buffers: two slots let one view's projection / binning / forward run
+        while the previous view's backward accumulates (window.py)."""
+        import copy
+        sl = copy.copy(self)
+        n, dev = self.n, self.dev
+        sl.rec = torch.empty_like(self.rec)
+        sl.count = torch.empty_like(self.count)
+        sl.tile_range = torch.empty_like(self.tile_range)
+        sl.n_pairs = torch.zeros_like(self.n_pairs)
+        sl._alloc_pairs(self.capacity)
+        sl.img = {k: torch.empty_like(v) for k, v in self.img.items()}
+        sl.ws_bwd = torch.empty_like(self.ws_bwd)
+        sl.graph = None
+        assert sl.n == n and sl.dev == dev
+        return sl
+
     def set_upstream(self, d_color, d_depth, d_sil):
         self.upstream = (d_color, d_depth, d_sil)
 

@@ -66,12 +66,64 @@ def apply_sgd(params: Sequence[torch.Tensor], grads: Sequence[torch.Tensor], lr:
             p.sub_(lr * g)
 
 
-def gpu_window(step, views, rank=None, world=None, group=None, reduce=True):
-    """WindowStep over a RenderStep: `views[i]` is keyframe i's world->camera view."""
+def gpu_window(step, views, rank=None, world=None, group=None, reduce=True,
+               pipelined=True):
+    """WindowStep over a RenderStep: `views[i]` is keyframe i's world->camera view.
+
+    pipelined: the rank's keyframes alternate between two view slots
+    (RenderStep.view_slot) on two streams -- keyframe q+1's projection, binning
+    and forward run while keyframe q's backward accumulates.  The backwards
+    (and their read-modify-write of the shared gradient buffer) stay in order on
+    one stream, so the result equals the sequential loop's up to the
+    nondeterministic order of the backward's float atomics."""
     from . import csplat as cs
 
-    def render(k, pose):
-        step.render(views[k], flags=cs.ACCUMULATE, pose=pose)
+    if not pipelined:
+        def render(k, pose):
+            step.render(views[k], flags=cs.ACCUMULATE, pose=pose)
 
-    return WindowStep(len(views), step.grads["flat"], render, step.prepare, rank, world, group,
-                      reduce)
+        return WindowStep(len(views), step.grads["flat"], render, step.prepare, rank, world,
+                          group, reduce)
+    return PipelinedWindow(step, views, rank, world, group, reduce)
+
+
+class PipelinedWindow(WindowStep):
+    """WindowStep whose local renders are software-pipelined over two view slots."""
+
+    def __init__(self, step, views, rank=None, world=None, group=None, reduce=True):
+        super().__init__(len(views), step.grads["flat"], None, step.prepare, rank, world, group,
+                         reduce)
+        self.views = views
+        self.slots = [step, step.view_slot()]
+        dev = step.dev
+        self.s_front = torch.cuda.Stream(device=dev)
+        self.s_back = torch.cuda.Stream(device=dev)
+        self.front_done = [torch.cuda.Event() for _ in range(2)]
+        self.slot_free = [torch.cuda.Event() for _ in range(2)]
+
+    def run(self):
+        from . import csplat as cs
+        main = torch.cuda.current_stream(self.flat.device)
+        self.flat.zero_()
+        self.prepare_fn()
+        self.s_front.wait_stream(main)
+        self.s_back.wait_stream(main)
+        for q, k in enumerate(self.local):
+            b = q % 2
+            sl = self.slots[b]
+            with torch.cuda.stream(self.s_front):
+                if q >= 2:  # keyframe q-2's backward has finished with this slot
+                    self.s_front.wait_event(self.slot_free[b])
+                sl.project_bin(self.views[k])
+                sl.forward()
+                self.front_done[b].record(self.s_front)
+            with torch.cuda.stream(self.s_back):
+                self.s_back.wait_event(self.front_done[b])
+                self.poses[k].zero_()
+                sl.backward(self.views[k], cs.ACCUMULATE, self.poses[k])
+                self.slot_free[b].record(self.s_back)
+        main.wait_stream(self.s_front)
+        main.wait_stream(self.s_back)
+        if self.world > 1 and self.reduce:
+            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
+        return self.flat

@@ -449,10 +449,12 @@ def test_replica_c2_full_parity(env):
     assert fo["e_pix"] > 10_000_000
 
 
-def test_window_accumulate_matches_sum_of_views(env):
+@pytest.mark.parametrize("mode", ["sequential", "pipelined", "pipelined_graph"])
+def test_window_accumulate_matches_sum_of_views(env, mode):
     """§8(e) on one GPU: a window iteration over 3 keyframes (ACCUMULATE into the
     flat buffer) equals the sum of the 3 single-view backward passes; each
-    keyframe's pose gradient equals its own single-view pose gradient."""
+    keyframe's pose gradient equals its own single-view pose gradient -- for the
+    sequential loop, the two-slot pipelined loop and its CUDA-graph capture."""
     torch, cs, dev = env["torch"], env["cs"], env["dev"]
     from paper_2403_11247_b200.pipeline import RenderStep
     from paper_2403_11247_b200.window import gpu_window
@@ -469,8 +471,22 @@ def test_window_accumulate_matches_sum_of_views(env):
         st.render(v)
         singles.append(st.grads["flat"].clone())
         poses.append(st.grads["pose"].clone())
-    win = gpu_window(st, views, rank=0, world=1)
-    flat = win.run().clone()
+    win = gpu_window(st, views, rank=0, world=1, pipelined=mode != "sequential")
+    if mode == "pipelined_graph":
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            win.run()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            win.run()
+        st.grads["flat"].fill_(123.0)   # the replay must start from zero again
+        graph.replay()
+    else:
+        win.run()
+    flat = st.grads["flat"].clone()
     torch.cuda.synchronize()
     ref = sum(s.double() for s in singles)
     n = st.n
