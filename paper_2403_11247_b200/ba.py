@@ -59,9 +59,29 @@ class BAStep:
             self.count_fn(k)
         if self.world > 1:
             dist.all_reduce(self.n_valid, op=dist.ReduceOp.SUM, group=self.group)
-        for k in self.local:
-            self.poses[k].zero_()
-            self.render_fn(k, self.poses[k])
+        if getattr(self, "pipe", None) is None:
+            for k in self.local:
+                self.poses[k].zero_()
+                self.render_fn(k, self.poses[k])
+        else:  # two view slots on two streams: keyframe q+1's front under q's backward
+            front_fn, back_fn, s_front, s_back, front_done, slot_free = self.pipe
+            main = torch.cuda.current_stream(self.flat.device)
+            s_front.wait_stream(main)
+            s_back.wait_stream(main)
+            for q, k in enumerate(self.local):
+                b = q % 2
+                with torch.cuda.stream(s_front):
+                    if q >= 2:
+                        s_front.wait_event(slot_free[b])
+                    front_fn(k, b)
+                    front_done[b].record(s_front)
+                with torch.cuda.stream(s_back):
+                    s_back.wait_event(front_done[b])
+                    self.poses[k].zero_()
+                    back_fn(k, b, self.poses[k])
+                    slot_free[b].record(s_back)
+            main.wait_stream(s_front)
+            main.wait_stream(s_back)
         if self.world > 1:
             dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group)
             dist.all_reduce(self.loss3, op=dist.ReduceOp.SUM, group=self.group)
@@ -75,7 +95,7 @@ def ba_loss_value(loss3, lambda_depth=1.0, lambda_ssim=0.2) -> float:
 
 
 def gpu_ba(step, views, obs_color, obs_depth, patches, lambda_depth=1.0, lambda_ssim=0.2,
-           rank=None, world=None, group=None):
+           rank=None, world=None, group=None, pipelined=True):
     """BAStep over a RenderStep: keyframe k has view `views[k]`, observed images
     obs_color[k] [3,H,W] / obs_depth[k] [H,W] (device; only local keyframes are
     read) and patch ids `patches[k]` (int32, see scenes.synth.sample_patches)."""
@@ -109,4 +129,27 @@ def gpu_ba(step, views, obs_color, obs_depth, patches, lambda_depth=1.0, lambda_
     ba = BAStep(len(views), step.grads["flat"], n_valid, loss3, count, render, step.prepare,
                 rank, world, group)
     ba.n_rays = n_rays
+    ba.pipe = None
+    if pipelined:  # window.py's two-slot pipeline: per-slot buffers and upstream
+        slots = [step, step.view_slot()]
+        ups = [up, tuple(torch.empty_like(t) for t in up)]
+
+        def front(k, b):
+            if pt[k].numel() == 0:
+                return
+            sl = slots[b]
+            sl.project_bin(views[k], tile_active=masks[k])
+            sl.forward()
+            cs.ba_patch_loss(sl.img, obs_color[k], obs_depth[k], sl.cam, pt[k], n_rays, n_valid,
+                             lambda_depth, lambda_ssim, out=ups[b], loss3=loss3)
+
+        def back(k, b, pose):
+            if pt[k].numel() == 0:
+                return
+            sl = slots[b]
+            sl.set_upstream(*ups[b])
+            sl.backward(views[k], flags=cs.ACCUMULATE, pose=pose)
+
+        ba.pipe = (front, back, torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev),
+                   [torch.cuda.Event() for _ in range(2)], [torch.cuda.Event() for _ in range(2)])
     return ba
