@@ -35,8 +35,9 @@ import numpy as np  # noqa: E402
 METRIC = "fwd+bwd renders/sec at 1200x680 (Replica-shaped, 200k Gaussians)"
 UNIT = "renders/s"
 KERNEL_LAUNCHES_PER_STEP = {
-    # kernels of libcsplat launched by one RenderStep.step()
-    "mask_prune": 1, "rvq_assign": 2, "project": 1, "bin_tiles": 2, "render_fwd": 1,
+    # kernels of libcsplat launched by one RenderStep.step(): the projection
+    # carries the bucket pass (csplat_project_bin), so binning adds the sort only
+    "mask_prune": 1, "rvq_assign": 2, "project": 1, "bin_tiles": 1, "render_fwd": 1,
     "render_bwd": 2,
 }
 
