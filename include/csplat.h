@@ -171,6 +171,34 @@ int csplat_project_bin_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                           void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
                           uint32_t flags, void *ws, size_t ws_bytes, void *stream);
 
+/* a1 + a2-decode + a3 + a4 + a5 + a6 in one call: csplat_project_bin (every
+ * tile active) followed by csplat_render_fwd, with the per-tile sort and the
+ * forward split into tile chunks that run as a pipeline on two library-owned
+ * streams forked from and joined back into `stream` (capturable in a CUDA
+ * graph): the latency-bound sort of chunk c+1 overlaps the issue-bound forward
+ * of chunk c.  Outputs are bit-identical to those calls (tested): rec, count,
+ * pair_gid, pair_rec, tile_range, n_pairs_dev as csplat_project_bin; color
+ * [3][H][W], depth, silhouette, t_final [H][W] and n_contrib [H][W] as
+ * csplat_render_fwd.  Pairs beyond pair_capacity are dropped (ranges clamped;
+ * no CSPLAT_SYNC check here: read n_pairs_dev).  ws: csplat_workspace_bytes(
+ * CSPLAT_OP_BIN_TILES, g->n, pair_capacity, cam).  Errors as those calls. */
+int csplat_project_bin_render(const csplat_gaussians *g, const csplat_codebook *cb,
+                              const csplat_camera *cam, const csplat_view *view,
+                              const csplat_params *prm, void *rec, int32_t *count,
+                              int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                              uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                              size_t ws_bytes, float *color, float *depth, float *silhouette,
+                              float *t_final, int32_t *n_contrib, void *stream);
+
+/* csplat_project_bin_render with the view in DEVICE memory (csplat_project_dv). */
+int csplat_project_bin_render_dv(const csplat_gaussians *g, const csplat_codebook *cb,
+                                 const csplat_camera *cam, const float *view_dev,
+                                 const csplat_params *prm, void *rec, int32_t *count,
+                                 int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                                 uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                                 size_t ws_bytes, float *color, float *depth, float *silhouette,
+                                 float *t_final, int32_t *n_contrib, void *stream);
+
 /* csplat_bin_tiles restricted to the tiles whose bit is set in tile_active
  * (device uint32[ceil(T/32)], bit t & 31 of word t >> 5; NULL = every tile):
  * the pairs of the other tiles are not emitted and their ranges are empty, so

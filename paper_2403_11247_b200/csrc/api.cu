@@ -265,6 +265,72 @@ int csplat_project_bin_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                           ws_bytes, stream);
 }
 
+static int project_bin_render_impl(const csplat_gaussians *g, const csplat_codebook *cb,
+                                   const csplat_camera *cam, const csplat_view *view,
+                                   const float *view_dev, const csplat_params *prm, void *rec,
+                                   int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
+                                   void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                                   void *ws, size_t ws_bytes, float *color, float *depth,
+                                   float *silhouette, float *t_final, int32_t *n_contrib,
+                                   void *stream) {
+  RET_IF(check_gaussians(g));
+  RET_IF(check_camera(cam));
+  RET_IF(check_codebook(cb, true));
+  if ((!view && !view_dev) || !prm) return invalid("view/params NULL");
+  if (g->n > 0 && (!rec || !count)) return invalid("rec/count NULL");
+  if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
+  if (!(prm->mask_eps > 0.f) || !(prm->mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
+  if (pair_capacity < 0 || pair_capacity > 0xffffffffLL) return invalid("capacity out of range");
+  if (!tile_range || !n_pairs_dev) return invalid("tile_range/n_pairs NULL");
+  if (pair_capacity > 0 && (!pair_gid || !pair_rec)) return invalid("pair_gid/pair_rec NULL");
+  if (!color || !depth || !silhouette || !t_final || !n_contrib)
+    return invalid("project_bin_render: image NULL");
+  if (!aligned16(rec) || !aligned16(pair_rec)) {
+    set_err("rec/pair_rec must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  const size_t need = csplat::bin_workspace_bytes(g->n, pair_capacity, *cam);
+  if (!ws || ws_bytes < need) {
+    set_err("project_bin_render workspace too small");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  RET_IF(check_device());
+  csplat::DecodeArgs d;
+  if (cb) d = decode_args(cb);
+  return cuda_status(csplat::launch_project_bin_render(
+                         *g, cb ? &d : nullptr, *cam, view ? *view : csplat_view{}, view_dev,
+                         mask_tau(prm->mask_eps), prm->dilation, *prm, rec, count, pair_capacity,
+                         pair_gid, pair_rec, tile_range, n_pairs_dev, ws, color, depth,
+                         silhouette, t_final, n_contrib, static_cast<cudaStream_t>(stream)),
+                     "csplat_project_bin_render");
+}
+
+int csplat_project_bin_render(const csplat_gaussians *g, const csplat_codebook *cb,
+                              const csplat_camera *cam, const csplat_view *view,
+                              const csplat_params *prm, void *rec, int32_t *count,
+                              int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                              uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                              size_t ws_bytes, float *color, float *depth, float *silhouette,
+                              float *t_final, int32_t *n_contrib, void *stream) {
+  if (!view) return invalid("view NULL");
+  return project_bin_render_impl(g, cb, cam, view, nullptr, prm, rec, count, pair_capacity,
+                                 pair_gid, pair_rec, tile_range, n_pairs_dev, ws, ws_bytes, color,
+                                 depth, silhouette, t_final, n_contrib, stream);
+}
+
+int csplat_project_bin_render_dv(const csplat_gaussians *g, const csplat_codebook *cb,
+                                 const csplat_camera *cam, const float *view_dev,
+                                 const csplat_params *prm, void *rec, int32_t *count,
+                                 int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                                 uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                                 size_t ws_bytes, float *color, float *depth, float *silhouette,
+                                 float *t_final, int32_t *n_contrib, void *stream) {
+  if (!view_dev) return invalid("view_dev NULL");
+  return project_bin_render_impl(g, cb, cam, nullptr, view_dev, prm, rec, count, pair_capacity,
+                                 pair_gid, pair_rec, tile_range, n_pairs_dev, ws, ws_bytes, color,
+                                 depth, silhouette, t_final, n_contrib, stream);
+}
+
 int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
                             const csplat_camera *cam, const uint32_t *tile_active,
                             int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,

@@ -23,9 +23,12 @@ BinWs bin_carve(void *ws, int64_t cap, int64_t T);
 // zero the cursors, the overflow length and the look-back words (one memset)
 cudaError_t bin_reset(const BinWs &w, int64_t T, cudaStream_t s);
 // a5: k_sort_tiles over the buckets filled by k_bucket or the fused projection
+// (tiles [tile0, tile0 + ntiles) only, ntiles < 0 = to the end: the tile-range
+// look-back never waits, so any split of the tiles into launches is valid)
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
                               const void *rec, uint32_t *pair_gid, void *pair_rec,
-                              uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s);
+                              uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,
+                              int64_t tile0 = 0, int64_t ntiles = -1);
 
 // Warp-cooperative expansion of 32 Gaussians' tile rectangles.  Lane l holds
 // Gaussian base + l's pair count c, its pixel rectangle corners rx, ry (record

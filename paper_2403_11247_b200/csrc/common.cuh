@@ -314,10 +314,23 @@ cudaError_t launch_ba_loss(const float *color, const float *depth, const float *
                            float *d_color, float *d_depth, float *d_sil, float *loss3,
                            cudaStream_t s);
 
+// tiles [tile0, tile0 + ntiles) only (ntiles < 0: to the last tile)
 cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
                               float *depth, float *sil, float *t_final, int32_t *n_contrib,
-                              cudaStream_t s);
+                              cudaStream_t s, int tile0 = 0, int ntiles = -1);
+
+// csplat_project_bin_render: projection + bucket, then the per-tile sort and
+// the forward in tile chunks, the sort of chunk c+1 overlapping the forward
+// of chunk c on two library streams forked from / joined into s
+cudaError_t launch_project_bin_render(const csplat_gaussians &g, const DecodeArgs *dec,
+                                      const csplat_camera &cam, const csplat_view &view,
+                                      const float *view_dev, float tau, float dilation,
+                                      const csplat_params &prm, void *rec, int32_t *count,
+                                      int64_t cap, uint32_t *pair_gid, void *pair_rec,
+                                      uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                                      float *color, float *depth, float *sil, float *t_final,
+                                      int32_t *n_contrib, cudaStream_t s);
 
 size_t bwd_workspace_bytes(int64_t n);
 cudaError_t launch_chain(const csplat_gaussians &g, const DecodeArgs *dec,

@@ -9,6 +9,13 @@
 
 namespace csplat {
 
+#ifndef CSPLAT_FWD_CHUNKS
+#define CSPLAT_FWD_CHUNKS 2
+#endif
+constexpr int kFwdChunks = CSPLAT_FWD_CHUNKS;  // sort / forward pipeline chunks
+constexpr int kFwdChunksMax = 16;
+static_assert(kFwdChunks >= 1 && kFwdChunks <= kFwdChunksMax, "CSPLAT_FWD_CHUNKS");
+
 struct ProjConst {
   float V[12];
   float fx, fy, cx, cy, Wf, Hf, near_z, far_z;
@@ -249,6 +256,78 @@ cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
   if (e != cudaSuccess) return e;
   return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
                            n_pairs_dev, s);
+}
+
+// library-owned fork streams and events (per device), created on first use
+struct ForkRes {
+  cudaStream_t st[kFwdChunksMax] = {};
+  cudaEvent_t start = nullptr, done[kFwdChunksMax] = {};
+};
+
+static cudaError_t fork_res(ForkRes *&out) {
+  static ForkRes res[16];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  ForkRes &r = res[dev];
+  if (!r.start) {
+    const unsigned fl = cudaEventDisableTiming;
+    for (int c = 0; c < kFwdChunksMax; c++) {
+      if ((e = cudaStreamCreateWithFlags(&r.st[c], cudaStreamNonBlocking)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&r.done[c], fl)) != cudaSuccess) return e;
+    }
+    if ((e = cudaEventCreateWithFlags(&r.start, fl)) != cudaSuccess) return e;
+  }
+  out = &r;
+  return cudaSuccess;
+}
+
+cudaError_t launch_project_bin_render(const csplat_gaussians &g, const DecodeArgs *dec,
+                                      const csplat_camera &cam, const csplat_view &view,
+                                      const float *view_dev, float tau, float dilation,
+                                      const csplat_params &prm, void *rec, int32_t *count,
+                                      int64_t cap, uint32_t *pair_gid, void *pair_rec,
+                                      uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                                      float *color, float *depth, float *sil, float *t_final,
+                                      int32_t *n_contrib, cudaStream_t s) {
+  const CamInfo ci = cam_info(cam);
+  const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
+  BinWs w = bin_carve(ws, cap, T);
+  cudaError_t e = bin_reset(w, T, s);
+  if (e != cudaSuccess) return e;
+  e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
+                          ci.tiles_x, cap, nullptr, s);
+  if (e != cudaSuccess) return e;
+  // fork into K streams, one tile chunk each: sort the chunk, then render it;
+  // the chunks run concurrently, so a chunk's forward (issue-bound) overlaps
+  // the other chunks' sorts (latency-bound) instead of waiting for all tiles
+  const int K = kFwdChunks;
+  if (K == 1) {
+    e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
+                          n_pairs_dev, s);
+    if (e != cudaSuccess) return e;
+    return launch_render_fwd(pair_rec, tile_range, cam, prm, color, depth, sil, t_final,
+                             n_contrib, s);
+  }
+  ForkRes *r = nullptr;
+  if ((e = fork_res(r)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(r->start, s)) != cudaSuccess) return e;
+  for (int c = 0; c < K; c++) {
+    const int64_t t0 = T * c / K, t1 = T * (c + 1) / K;
+    cudaStream_t sc = r->st[c];
+    if ((e = cudaStreamWaitEvent(sc, r->start, 0)) != cudaSuccess) return e;
+    e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
+                          n_pairs_dev, sc, t0, t1 - t0);
+    if (e != cudaSuccess) return e;
+    e = launch_render_fwd(pair_rec, tile_range, cam, prm, color, depth, sil, t_final, n_contrib,
+                          sc, (int)t0, (int)(t1 - t0));
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(r->done[c], sc)) != cudaSuccess) return e;
+  }
+  for (int c = 0; c < K; c++)
+    if ((e = cudaStreamWaitEvent(s, r->done[c], 0)) != cudaSuccess) return e;
+  return cudaSuccess;
 }
 
 }  // namespace csplat

@@ -151,8 +151,7 @@ class RenderStep:
 
     def render(self, view, flags=None, pose=None):
         """a3 -> a4/a5 -> a6 -> a7/a8 for one view of the prepared map."""
-        self.project_bin(view)
-        self.forward()
+        self.project_bin_forward(view)
         self.backward(view, flags, pose)
 
     def front(self, view, sync_probe=False):
@@ -190,9 +189,22 @@ class RenderStep:
                       self.flags if flags is None else flags, grads=grads, ws=self.ws_bwd)
 
     def step(self, view):
-        self.front(view)
-        self.forward()
+        self.prepare()
+        self.project_bin_forward(view)
         self.backward(view)
+
+    def project_bin_forward(self, view):
+        """a3 -> a4/a5 -> a6: one csplat_project_bin_render call (the per-tile
+        sort and the forward pipelined in tile chunks) unless CSPLAT_FUSED_BIN=0."""
+        if FUSED_BIN:
+            cs.project_bin_render(self.pruned, self.cam, view, self.capacity, self.prm, self.cb,
+                                  rec=self.rec, count=self.count, ws=self.ws_bin,
+                                  out=dict(pair_gid=self.pair_gid, pair_rec=self.pair_rec,
+                                           tile_range=self.tile_range, n_pairs_dev=self.n_pairs),
+                                  img=self.img)
+        else:
+            self.project_bin(view)
+            self.forward()
 
     def check_capacity(self):
         n = int(self.n_pairs.item())

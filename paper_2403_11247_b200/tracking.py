@@ -106,8 +106,7 @@ class Tracker:
         prologue, gated-out pixels not replayed) -> device pose step."""
         st = self.step
         g = st.pruned
-        st.project_bin(view_dev)
-        st.forward()
+        st.project_bin_forward(view_dev)
         cs.tracking_bwd(g, st.cam, view_dev, st.rec, st.pair_rec, st.tile_range, st.img,
                         self.obs_color, self.obs_depth, self.n_valid, st.prm, st.cb,
                         flags=cs.POSE_ONLY, lambda_depth=self.lambda_depth,

@@ -114,8 +114,7 @@ class PipelinedWindow(WindowStep):
             with torch.cuda.stream(self.s_front):
                 if q >= 2:  # keyframe q-2's backward has finished with this slot
                     self.s_front.wait_event(self.slot_free[b])
-                sl.project_bin(self.views[k])
-                sl.forward()
+                sl.project_bin_forward(self.views[k])
                 self.front_done[b].record(self.s_front)
             with torch.cuda.stream(self.s_back):
                 self.s_back.wait_event(self.front_done[b])

@@ -360,6 +360,19 @@ def test_project_bin_fused_matches_separate_calls(env, which):
         assert torch.equal(out["pair_gid"][:n], ref["pair_gid"][:n])
         assert torch.equal(out["pair_rec"][:n], ref["pair_rec"][:n])
         assert torch.equal(out["tile_range"], ref["tile_range"])
+    # projection + binning + forward in one call (sort / forward chunk pipeline)
+    img_ref = cs.render_fwd(ref["pair_rec"], ref["tile_range"], sc.cam)
+    for view_arg in (v, vd):
+        rec3, cnt3, out3, img3 = cs.project_bin_render(g, sc.cam, view_arg, cap)
+        torch.cuda.synchronize()
+        assert torch.equal(rec3, rec) and torch.equal(cnt3, cnt)
+        n = int(out3["n_pairs_dev"].item())
+        assert n == int(ref["n_pairs_dev"].item())
+        assert torch.equal(out3["pair_gid"][:n], ref["pair_gid"][:n])
+        assert torch.equal(out3["pair_rec"][:n], ref["pair_rec"][:n])
+        assert torch.equal(out3["tile_range"], ref["tile_range"])
+        for k in ("color", "depth", "sil", "t_final", "n_contrib"):
+            assert torch.equal(img3[k], img_ref[k]), k
     # active tiles: every third tile
     tx, ty = cs.tiles(sc.cam)
     T = tx * ty
