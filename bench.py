@@ -36,10 +36,10 @@ METRIC = "fwd+bwd renders/sec at 1200x680 (Replica-shaped, 200k Gaussians)"
 UNIT = "renders/s"
 KERNEL_LAUNCHES_PER_STEP = {
     # kernels of libcsplat launched by one RenderStep.step(): the projection
-    # carries the bucket pass, and the per-tile sort and the forward run as 2
-    # tile chunks each (csplat_project_bin_render)
+    # carries the bucket pass, and the per-tile sort, the forward and the
+    # backward kernel run as 2 tile chunks each, then the chain (csplat_render_step)
     "mask_prune": 1, "rvq_assign": 2, "project": 1, "bin_tiles": 2, "render_fwd": 2,
-    "render_bwd": 2,
+    "render_bwd": 3,
 }
 
 

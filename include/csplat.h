@@ -199,6 +199,27 @@ int csplat_project_bin_render_dv(const csplat_gaussians *g, const csplat_codeboo
                                  size_t ws_bytes, float *color, float *depth, float *silhouette,
                                  float *t_final, int32_t *n_contrib, void *stream);
 
+/* a1 + a2-decode + a3 .. a8 for one view in one call (the C2 step after the
+ * prune and the R-VQ assignment): csplat_project_bin_render followed by
+ * csplat_render_bwd, with the backward kernel joining each tile chunk's
+ * pipeline (sort -> forward -> backward on one library stream per chunk,
+ * forked from / joined into `stream`), then the per-Gaussian chain on
+ * `stream`.  Arguments as those calls (ws_bin: CSPLAT_OP_BIN_TILES
+ * workspace; ws_bwd: CSPLAT_OP_RENDER_BWD workspace; flags: CSPLAT_ACCUMULATE,
+ * CSPLAT_POSE_ONLY is rejected).  Outputs equal the separate calls: the
+ * discrete ones and the images bit for bit, the gradients up to the order of
+ * the backward's float atomics. */
+int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
+                       const csplat_camera *cam, const csplat_view *view,
+                       const csplat_params *prm, void *rec, int32_t *count,
+                       int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                       uint32_t *tile_range, int64_t *n_pairs_dev, void *ws_bin,
+                       size_t ws_bin_bytes, float *color, float *depth, float *silhouette,
+                       float *t_final, int32_t *n_contrib, const float *d_color,
+                       const float *d_depth, const float *d_silhouette, uint32_t flags,
+                       const csplat_grads *out, void *ws_bwd, size_t ws_bwd_bytes,
+                       void *stream);
+
 /* csplat_bin_tiles restricted to the tiles whose bit is set in tile_active
  * (device uint32[ceil(T/32)], bit t & 31 of word t >> 5; NULL = every tile):
  * the pairs of the other tiles are not emitted and their ranges are empty, so

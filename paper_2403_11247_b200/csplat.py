@@ -102,6 +102,8 @@ def lib():
         L.csplat_project_bin_render.argtypes = [vp] * 7 + [i64, vp, vp, vp, vp, vp, C.c_size_t] + \
             [vp] * 6
         L.csplat_project_bin_render_dv.argtypes = L.csplat_project_bin_render.argtypes
+        L.csplat_render_step.argtypes = [vp] * 7 + [i64, vp, vp, vp, vp, vp, C.c_size_t] + \
+            [vp] * 8 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_project_bin_dv.argtypes = [vp] * 8 + [i64, vp, vp, vp, vp, u32, vp, C.c_size_t,
                                                         vp]
         L.csplat_render_bwd_dv.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
@@ -303,6 +305,48 @@ def project_bin_render(g: GaussianMap, cam: dict, v, capacity: int, prm: Params 
                                                C.byref(view(v)), C.byref(prm or params()), *tail),
                "csplat_project_bin_render")
     return rec[:n], count[:n], out, img
+
+
+def render_step(g: GaussianMap, cam: dict, v, capacity: int, d_color, d_depth, d_sil,
+                prm: Params | None = None, cb: CodebookT | None = None, flags: int = 0,
+                rec=None, count=None, ws=None, out=None, img=None, grads=None, ws_bwd=None,
+                stream=None):
+    """a3 .. a8 for one view in one call (csplat_render_step: per tile chunk the
+    sort, the forward and the backward kernel on a library stream, then the
+    chain).  Returns (rec, count, bin dict, img dict, grads dict)."""
+    n = g.n
+    dev = g.opacity.device
+    H, W = cam["height"], cam["width"]
+    rec = rec if rec is not None else torch.empty((max(n, 1), 16), dtype=torch.int32, device=dev)
+    count = count if count is not None else torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    tx, ty = tiles(cam)
+    if out is None:
+        out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
+                   pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
+                   tile_range=torch.empty((tx * ty, 2), dtype=torch.int32, device=dev),
+                   n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
+    if img is None:
+        img = dict(color=torch.empty((3, H, W), device=dev), depth=torch.empty((H, W), device=dev),
+                   sil=torch.empty((H, W), device=dev), t_final=torch.empty((H, W), device=dev),
+                   n_contrib=torch.empty((H, W), dtype=torch.int32, device=dev))
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_BIN_TILES, n, capacity, cam), dtype=torch.uint8,
+                         device=dev)
+    if grads is None:
+        grads = alloc_grads(n, dev)
+    if ws_bwd is None:
+        ws_bwd = torch.empty(workspace_bytes(OP_RENDER_BWD, n), dtype=torch.uint8, device=dev)
+    gr = Grads(*[_ptr(grads.get(k)) for k in ("mean", "opacity", "rgb", "log_scale", "quat",
+                                               "mask", "pose")])
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    _check(lib().csplat_render_step(
+        C.byref(gs), _byref(cbs), C.byref(camera(cam)), C.byref(view(v)),
+        C.byref(prm or params()), _ptr(rec), _ptr(count), capacity, _ptr(out["pair_gid"]),
+        _ptr(out["pair_rec"]), _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]), _ptr(ws),
+        ws.numel(), _ptr(img["color"]), _ptr(img["depth"]), _ptr(img["sil"]),
+        _ptr(img["t_final"]), _ptr(img["n_contrib"]), _ptr(d_color), _ptr(d_depth), _ptr(d_sil),
+        flags, C.byref(gr), _ptr(ws_bwd), ws_bwd.numel(), _stream(stream)), "csplat_render_step")
+    return rec[:n], count[:n], out, img, grads
 
 
 def _on_device(v) -> bool:

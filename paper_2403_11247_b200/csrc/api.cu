@@ -331,6 +331,55 @@ int csplat_project_bin_render_dv(const csplat_gaussians *g, const csplat_codeboo
                                  depth, silhouette, t_final, n_contrib, stream);
 }
 
+int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
+                       const csplat_camera *cam, const csplat_view *view,
+                       const csplat_params *prm, void *rec, int32_t *count,
+                       int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                       uint32_t *tile_range, int64_t *n_pairs_dev, void *ws_bin,
+                       size_t ws_bin_bytes, float *color, float *depth, float *silhouette,
+                       float *t_final, int32_t *n_contrib, const float *d_color,
+                       const float *d_depth, const float *d_silhouette, uint32_t flags,
+                       const csplat_grads *out, void *ws_bwd, size_t ws_bwd_bytes,
+                       void *stream) {
+  RET_IF(check_gaussians(g));
+  RET_IF(check_camera(cam));
+  RET_IF(check_codebook(cb, true));
+  if (!view || !prm || !out) return invalid("view/params/grads NULL");
+  if (g->n > 0 && (!rec || !count)) return invalid("rec/count NULL");
+  if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
+  if (!(prm->mask_eps > 0.f) || !(prm->mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
+  if (pair_capacity < 0 || pair_capacity > 0xffffffffLL) return invalid("capacity out of range");
+  if (!tile_range || !n_pairs_dev) return invalid("tile_range/n_pairs NULL");
+  if (pair_capacity > 0 && (!pair_gid || !pair_rec)) return invalid("pair_gid/pair_rec NULL");
+  if (!color || !depth || !silhouette || !t_final || !n_contrib)
+    return invalid("render_step: image NULL");
+  if (!d_color || !d_depth || !d_silhouette) return invalid("render_step: upstream NULL");
+  if (flags & CSPLAT_POSE_ONLY) return invalid("render_step: CSPLAT_POSE_ONLY not supported");
+  if (!aligned16(rec) || !aligned16(pair_rec)) {
+    set_err("rec/pair_rec must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  if (!ws_bin || ws_bin_bytes < csplat::bin_workspace_bytes(g->n, pair_capacity, *cam)) {
+    set_err("render_step binning workspace too small");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  if (!ws_bwd || ws_bwd_bytes < csplat::bwd_workspace_bytes(g->n) || !aligned16(ws_bwd)) {
+    set_err("render_step backward workspace too small or misaligned");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  RET_IF(check_device());
+  csplat::DecodeArgs d;
+  if (cb) d = decode_args(cb);
+  const csplat::StepBwd b{d_color, d_depth, d_silhouette, flags, *out, ws_bwd};
+  return cuda_status(csplat::launch_render_step(*g, cb ? &d : nullptr, *cam, *view, nullptr,
+                                                mask_tau(prm->mask_eps), prm->dilation, *prm, rec,
+                                                count, pair_capacity, pair_gid, pair_rec,
+                                                tile_range, n_pairs_dev, ws_bin, color, depth,
+                                                silhouette, t_final, n_contrib, &b,
+                                                static_cast<cudaStream_t>(stream)),
+                     "csplat_render_step");
+}
+
 int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
                             const csplat_camera *cam, const uint32_t *tile_active,
                             int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,

@@ -333,6 +333,33 @@ cudaError_t launch_project_bin_render(const csplat_gaussians &g, const DecodeArg
                                       int32_t *n_contrib, cudaStream_t s);
 
 size_t bwd_workspace_bytes(int64_t n);
+struct TrackingLoss;
+cudaError_t bwd_prep(const csplat_gaussians &g, uint32_t flags, const csplat_grads &out,
+                     void *ws, const TrackingLoss *loss, cudaStream_t s);
+cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss *loss,
+                                    const csplat_params &prm, const void *pair_rec,
+                                    const uint32_t *tile_range, const float *t_final,
+                                    const int32_t *n_contrib, const float *d_color,
+                                    const float *d_depth, const float *d_sil, void *ws,
+                                    cudaStream_t s, int tile0, int ntiles);
+
+// csplat_render_step: a3 .. a8 for one view -- projection + bucket, then per
+// tile chunk (on its own library stream) the sort, the forward and the
+// backward kernel, joined, then the per-Gaussian chain
+struct StepBwd {
+  const float *d_color, *d_depth, *d_sil;
+  uint32_t flags;
+  csplat_grads out;
+  void *ws;
+};
+cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
+                               const csplat_camera &cam, const csplat_view &view,
+                               const float *view_dev, float tau, float dilation,
+                               const csplat_params &prm, void *rec, int32_t *count, int64_t cap,
+                               uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                               int64_t *n_pairs_dev, void *ws, float *color, float *depth,
+                               float *sil, float *t_final, int32_t *n_contrib,
+                               const StepBwd *bwd, cudaStream_t s);
 cudaError_t launch_chain(const csplat_gaussians &g, const DecodeArgs *dec,
                          const csplat_camera &cam, const csplat_view &view,
                          const float *view_dev, const csplat_params &prm, const void *rec,

@@ -283,6 +283,59 @@ static cudaError_t fork_res(ForkRes *&out) {
   return cudaSuccess;
 }
 
+cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
+                               const csplat_camera &cam, const csplat_view &view,
+                               const float *view_dev, float tau, float dilation,
+                               const csplat_params &prm, void *rec, int32_t *count, int64_t cap,
+                               uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                               int64_t *n_pairs_dev, void *ws, float *color, float *depth,
+                               float *sil, float *t_final, int32_t *n_contrib,
+                               const StepBwd *bwd, cudaStream_t s) {
+  const CamInfo ci = cam_info(cam);
+  const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
+  BinWs w = bin_carve(ws, cap, T);
+  cudaError_t e = bin_reset(w, T, s);
+  if (e != cudaSuccess) return e;
+  if (bwd && (e = bwd_prep(g, bwd->flags, bwd->out, bwd->ws, nullptr, s)) != cudaSuccess) return e;
+  e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
+                          ci.tiles_x, cap, nullptr, s);
+  if (e != cudaSuccess) return e;
+  // fork into K streams, one tile chunk each: sort the chunk, render it (and
+  // run its backward); the chunks run concurrently, so one chunk's issue-bound
+  // forward / backward overlaps the other's latency-bound sort and the
+  // kernels' tails overlap each other
+  const int K = kFwdChunks;
+  ForkRes *r = nullptr;
+  if (K > 1) {
+    if ((e = fork_res(r)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(r->start, s)) != cudaSuccess) return e;
+  }
+  for (int c = 0; c < K; c++) {
+    const int64_t t0 = T * c / K, t1 = T * (c + 1) / K;
+    cudaStream_t sc = K > 1 ? r->st[c] : s;
+    if (K > 1 && (e = cudaStreamWaitEvent(sc, r->start, 0)) != cudaSuccess) return e;
+    e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
+                          n_pairs_dev, sc, t0, t1 - t0);
+    if (e != cudaSuccess) return e;
+    e = launch_render_fwd(pair_rec, tile_range, cam, prm, color, depth, sil, t_final, n_contrib,
+                          sc, (int)t0, (int)(t1 - t0));
+    if (e != cudaSuccess) return e;
+    if (bwd) {
+      e = launch_render_bwd_tiles(cam, nullptr, prm, pair_rec, tile_range, t_final, n_contrib,
+                                  bwd->d_color, bwd->d_depth, bwd->d_sil, bwd->ws, sc, (int)t0,
+                                  (int)(t1 - t0));
+      if (e != cudaSuccess) return e;
+    }
+    if (K > 1 && (e = cudaEventRecord(r->done[c], sc)) != cudaSuccess) return e;
+  }
+  if (K > 1)
+    for (int c = 0; c < K; c++)
+      if ((e = cudaStreamWaitEvent(s, r->done[c], 0)) != cudaSuccess) return e;
+  if (!bwd || g.n == 0) return cudaSuccess;
+  return launch_chain(g, dec, cam, view, view_dev, prm, rec, static_cast<float *>(bwd->ws),
+                      bwd->flags, bwd->out, s);
+}
+
 cudaError_t launch_project_bin_render(const csplat_gaussians &g, const DecodeArgs *dec,
                                       const csplat_camera &cam, const csplat_view &view,
                                       const float *view_dev, float tau, float dilation,
@@ -291,43 +344,9 @@ cudaError_t launch_project_bin_render(const csplat_gaussians &g, const DecodeArg
                                       uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                                       float *color, float *depth, float *sil, float *t_final,
                                       int32_t *n_contrib, cudaStream_t s) {
-  const CamInfo ci = cam_info(cam);
-  const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
-  BinWs w = bin_carve(ws, cap, T);
-  cudaError_t e = bin_reset(w, T, s);
-  if (e != cudaSuccess) return e;
-  e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
-                          ci.tiles_x, cap, nullptr, s);
-  if (e != cudaSuccess) return e;
-  // fork into K streams, one tile chunk each: sort the chunk, then render it;
-  // the chunks run concurrently, so a chunk's forward (issue-bound) overlaps
-  // the other chunks' sorts (latency-bound) instead of waiting for all tiles
-  const int K = kFwdChunks;
-  if (K == 1) {
-    e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
-                          n_pairs_dev, s);
-    if (e != cudaSuccess) return e;
-    return launch_render_fwd(pair_rec, tile_range, cam, prm, color, depth, sil, t_final,
-                             n_contrib, s);
-  }
-  ForkRes *r = nullptr;
-  if ((e = fork_res(r)) != cudaSuccess) return e;
-  if ((e = cudaEventRecord(r->start, s)) != cudaSuccess) return e;
-  for (int c = 0; c < K; c++) {
-    const int64_t t0 = T * c / K, t1 = T * (c + 1) / K;
-    cudaStream_t sc = r->st[c];
-    if ((e = cudaStreamWaitEvent(sc, r->start, 0)) != cudaSuccess) return e;
-    e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
-                          n_pairs_dev, sc, t0, t1 - t0);
-    if (e != cudaSuccess) return e;
-    e = launch_render_fwd(pair_rec, tile_range, cam, prm, color, depth, sil, t_final, n_contrib,
-                          sc, (int)t0, (int)(t1 - t0));
-    if (e != cudaSuccess) return e;
-    if ((e = cudaEventRecord(r->done[c], sc)) != cudaSuccess) return e;
-  }
-  for (int c = 0; c < K; c++)
-    if ((e = cudaStreamWaitEvent(s, r->done[c], 0)) != cudaSuccess) return e;
-  return cudaSuccess;
+  return launch_render_step(g, dec, cam, view, view_dev, tau, dilation, prm, rec, count, cap,
+                            pair_gid, pair_rec, tile_range, n_pairs_dev, ws, color, depth, sil,
+                            t_final, n_contrib, nullptr, s);
 }
 
 }  // namespace csplat

@@ -211,11 +211,11 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     int tiles_x, float amax, const float *__restrict__ t_final,
     const int32_t *__restrict__ n_contrib, const float *__restrict__ dC,
     const float *__restrict__ dD, const float *__restrict__ dS, float *__restrict__ acc,
-    LossArgs la) {
+    LossArgs la, int tile0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tile = blockIdx.x / kCtaPerTile;
+  const int tile = tile0 + (int)(blockIdx.x / kCtaPerTile);
   const int blk = (blockIdx.x % kCtaPerTile) * kCW + (tid >> 5);  // 8x8 block of the tile
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const uint32_t start = range[2 * tile];
@@ -431,24 +431,33 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
   }
 }
 
-cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
-                              const csplat_camera &cam, const csplat_view &view,
-                              const float *view_dev, const TrackingLoss *loss,
-                              const csplat_params &prm, const void *rec, const void *pair_rec,
-                              const uint32_t *tile_range, const float *t_final,
-                              const int32_t *n_contrib, const float *d_color, const float *d_depth,
-                              const float *d_sil, uint32_t flags, const csplat_grads &out,
-                              void *ws, cudaStream_t s) {
-  const CamInfo ci = cam_info(cam);
-  float *acc = static_cast<float *>(ws);
-  cudaError_t e = cudaMemsetAsync(acc, 0, bwd_workspace_bytes(g.n), s);
+// zero the accumulator (and the pose gradient unless accumulating)
+cudaError_t bwd_prep(const csplat_gaussians &g, uint32_t flags, const csplat_grads &out,
+                     void *ws, const TrackingLoss *loss, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(ws, 0, bwd_workspace_bytes(g.n), s);
   if (e != cudaSuccess) return e;
   if (out.pose && !(flags & CSPLAT_ACCUMULATE)) {
     e = cudaMemsetAsync(out.pose, 0, 6 * sizeof(float), s);
     if (e != cudaSuccess) return e;
   }
+  if (loss && loss->loss3) e = cudaMemsetAsync(loss->loss3, 0, 3 * sizeof(float), s);
+  return e;
+}
+
+// the backward kernel over tiles [tile0, tile0 + ntiles) (ntiles < 0: to the
+// end); the per-Gaussian accumulation is by atomics, so tile chunks may run in
+// any order or concurrently
+cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss *loss,
+                                    const csplat_params &prm, const void *pair_rec,
+                                    const uint32_t *tile_range, const float *t_final,
+                                    const int32_t *n_contrib, const float *d_color,
+                                    const float *d_depth, const float *d_sil, void *ws,
+                                    cudaStream_t s, int tile0, int ntiles) {
+  const CamInfo ci = cam_info(cam);
+  float *acc = static_cast<float *>(ws);
   static bool attr_done = false;
   const size_t smem = sizeof(BwdSmem);
+  cudaError_t e = cudaSuccess;
   if (!attr_done) {
     e = cudaFuncSetAttribute(k_render_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
@@ -459,6 +468,8 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
     attr_done = true;
   }
   const int T = ci.tiles_x * ci.tiles_y;
+  if (ntiles < 0) ntiles = T - tile0;
+  if (ntiles <= 0) return cudaSuccess;
   LossArgs la{};
   if (loss) {
     la.color = loss->color; la.depth = loss->depth; la.sil = loss->sil;
@@ -466,21 +477,32 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
     la.n_valid = loss->n_valid; la.lambda_d = loss->lambda_d; la.gate = loss->gate;
     la.inv_n = 1.0f / (float)((int64_t)ci.W * ci.H);
     la.loss3 = loss->loss3;
-    if (la.loss3) {
-      e = cudaMemsetAsync(la.loss3, 0, 3 * sizeof(float), s);
-      if (e != cudaSuccess) return e;
-    }
-    k_render_bwd<true><<<T * kCtaPerTile, kBwdThreads, smem, s>>>(
+    k_render_bwd<true><<<ntiles * kCtaPerTile, kBwdThreads, smem, s>>>(
         static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, nullptr, nullptr, nullptr, acc, la);
+        t_final, n_contrib, nullptr, nullptr, nullptr, acc, la, tile0);
   } else {
-    k_render_bwd<false><<<T * kCtaPerTile, kBwdThreads, smem, s>>>(
+    k_render_bwd<false><<<ntiles * kCtaPerTile, kBwdThreads, smem, s>>>(
         static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, d_color, d_depth, d_sil, acc, la);
+        t_final, n_contrib, d_color, d_depth, d_sil, acc, la, tile0);
   }
-  e = cudaGetLastError();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
+                              const csplat_camera &cam, const csplat_view &view,
+                              const float *view_dev, const TrackingLoss *loss,
+                              const csplat_params &prm, const void *rec, const void *pair_rec,
+                              const uint32_t *tile_range, const float *t_final,
+                              const int32_t *n_contrib, const float *d_color, const float *d_depth,
+                              const float *d_sil, uint32_t flags, const csplat_grads &out,
+                              void *ws, cudaStream_t s) {
+  cudaError_t e = bwd_prep(g, flags, out, ws, loss, s);
+  if (e != cudaSuccess) return e;
+  e = launch_render_bwd_tiles(cam, loss, prm, pair_rec, tile_range, t_final, n_contrib, d_color,
+                              d_depth, d_sil, ws, s, 0, -1);
   if (e != cudaSuccess || g.n == 0) return e;
-  return launch_chain(g, dec, cam, view, view_dev, prm, rec, acc, flags, out, s);
+  return launch_chain(g, dec, cam, view, view_dev, prm, rec, static_cast<float *>(ws), flags,
+                      out, s);
 }
 
 }  // namespace csplat

@@ -23,6 +23,10 @@ from . import csplat as cs
 # path; CSPLAT_FUSED_BIN=0 selects the separate csplat_project + csplat_bin_tiles
 FUSED_BIN = os.environ.get("CSPLAT_FUSED_BIN", "1") == "1"
 
+
+def _on_device(v) -> bool:
+    return isinstance(v, torch.Tensor) and v.is_cuda
+
 class RenderStep:
     def __init__(self, planes: dict, cam: dict, codebook: dict | None, device="cuda",
                  prm: cs.Params | None = None, pair_capacity: int | None = None,
@@ -190,6 +194,15 @@ class RenderStep:
 
     def step(self, view):
         self.prepare()
+        if FUSED_BIN and not (self.flags & cs.POSE_ONLY) and not _on_device(view):
+            # a3 .. a8 in one library call (per tile chunk: sort -> fwd -> bwd)
+            dC, dD, dS = self.upstream
+            cs.render_step(self.pruned, self.cam, view, self.capacity, dC, dD, dS, self.prm,
+                           self.cb, self.flags, rec=self.rec, count=self.count, ws=self.ws_bin,
+                           out=dict(pair_gid=self.pair_gid, pair_rec=self.pair_rec,
+                                    tile_range=self.tile_range, n_pairs_dev=self.n_pairs),
+                           img=self.img, grads=self.grads, ws_bwd=self.ws_bwd)
+            return
         self.project_bin_forward(view)
         self.backward(view)
 
