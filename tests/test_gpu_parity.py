@@ -305,6 +305,19 @@ def test_empty_and_all_culled(env):
     res = run_and_compare(env, sc)
     assert res["npairs"] == 0
     assert float(res["out"]["sil"].abs().max()) == 0.0
+    # the one-call paths on the all-culled map and on an empty map (n = 0)
+    H, W = sc.cam["height"], sc.cam["width"]
+    up = [torch.ones((3, H, W), device=dev), torch.ones((H, W), device=dev),
+          torch.ones((H, W), device=dev)]
+    for planes in (sc.planes(), {k: v[..., :0] for k, v in sc.planes().items()}):
+        g = cs.GaussianMap.from_numpy(planes, device=dev)
+        _, _, b, img, gr = cs.render_step(g, sc.cam, sc.views[0], 16, *up)
+        _, _, b2, img2 = cs.project_bin_render(g, sc.cam, sc.views[0], 16)
+        torch.cuda.synchronize()
+        assert int(b["n_pairs_dev"].item()) == 0 and int(b2["n_pairs_dev"].item()) == 0
+        assert float(img["sil"].abs().max()) == 0.0 and float(img2["sil"].abs().max()) == 0.0
+        assert float(img["t_final"].min()) == 1.0
+        assert float(gr["flat"].abs().max()) == 0.0
 
 
 def test_long_tile_lists(env):
