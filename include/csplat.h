@@ -220,6 +220,26 @@ int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
                        const csplat_grads *out, void *ws_bwd, size_t ws_bwd_bytes,
                        void *stream);
 
+/* NEXT-1: one tracking iteration's render in one call -- csplat_render_step
+ * with the loss-fused backward of csplat_tracking_bwd (Eq 12 + Eq 14 formed
+ * per pixel from the images this call renders and obs_color / obs_depth;
+ * |R| = *n_valid_dev from csplat_count_valid_depth) in each tile chunk, then
+ * the chain.  Exactly one of view / view_dev (device, as csplat_project_dv).
+ * flags: CSPLAT_POSE_ONLY for tracking.  loss3_dev (L_t, L_c, L_d) is
+ * overwritten.  Other arguments, outputs and errors as csplat_render_step and
+ * csplat_tracking_bwd. */
+int csplat_tracking_step(const csplat_gaussians *g, const csplat_codebook *cb,
+                         const csplat_camera *cam, const csplat_view *view,
+                         const float *view_dev, const csplat_params *prm, void *rec,
+                         int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
+                         void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                         void *ws_bin, size_t ws_bin_bytes, float *color, float *depth,
+                         float *silhouette, float *t_final, int32_t *n_contrib,
+                         const float *obs_color, const float *obs_depth,
+                         const uint64_t *n_valid_dev, float lambda_depth, float sil_gate,
+                         uint32_t flags, const csplat_grads *out, float *loss3_dev,
+                         void *ws_bwd, size_t ws_bwd_bytes, void *stream);
+
 /* csplat_bin_tiles restricted to the tiles whose bit is set in tile_active
  * (device uint32[ceil(T/32)], bit t & 31 of word t >> 5; NULL = every tile):
  * the pairs of the other tiles are not emitted and their ranges are empty, so

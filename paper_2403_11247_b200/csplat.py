@@ -104,6 +104,8 @@ def lib():
         L.csplat_project_bin_render_dv.argtypes = L.csplat_project_bin_render.argtypes
         L.csplat_render_step.argtypes = [vp] * 7 + [i64, vp, vp, vp, vp, vp, C.c_size_t] + \
             [vp] * 8 + [u32, vp, vp, C.c_size_t, vp]
+        L.csplat_tracking_step.argtypes = [vp] * 8 + [i64, vp, vp, vp, vp, vp, C.c_size_t] + \
+            [vp] * 8 + [C.c_float, C.c_float, u32, vp, vp, vp, C.c_size_t, vp]
         L.csplat_project_bin_dv.argtypes = [vp] * 8 + [i64, vp, vp, vp, vp, u32, vp, C.c_size_t,
                                                         vp]
         L.csplat_render_bwd_dv.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
@@ -347,6 +349,40 @@ def render_step(g: GaussianMap, cam: dict, v, capacity: int, d_color, d_depth, d
         _ptr(img["t_final"]), _ptr(img["n_contrib"]), _ptr(d_color), _ptr(d_depth), _ptr(d_sil),
         flags, C.byref(gr), _ptr(ws_bwd), ws_bwd.numel(), _stream(stream)), "csplat_render_step")
     return rec[:n], count[:n], out, img, grads
+
+
+def tracking_step(g: GaussianMap, cam: dict, v, capacity: int, obs_color, obs_depth, n_valid,
+                  prm: Params | None = None, cb: CodebookT | None = None,
+                  flags: int = POSE_ONLY, lambda_depth=1.0, sil_gate=0.99, rec=None, count=None,
+                  ws=None, out=None, img=None, grads=None, loss3=None, ws_bwd=None, stream=None):
+    """NEXT-1: one tracking iteration's render in one call (csplat_tracking_step):
+    project + bin + fwd + the loss-fused backward per tile chunk, then the chain.
+    Returns (grads, loss3)."""
+    n = g.n
+    dev = g.opacity.device
+    if grads is None:
+        grads = alloc_grads(n, dev, pose_only=bool(flags & POSE_ONLY))
+    if loss3 is None:
+        loss3 = torch.zeros(3, device=dev)
+    if ws_bwd is None:
+        ws_bwd = torch.empty(workspace_bytes(OP_RENDER_BWD, n), dtype=torch.uint8, device=dev)
+    if ws is None:
+        ws = torch.empty(workspace_bytes(OP_BIN_TILES, n, capacity, cam), dtype=torch.uint8,
+                         device=dev)
+    gr = Grads(*[_ptr(grads.get(k)) for k in ("mean", "opacity", "rgb", "log_scale", "quat",
+                                               "mask", "pose")])
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    dv = _on_device(v)
+    hv = None if dv else view(v)
+    _check(lib().csplat_tracking_step(
+        C.byref(gs), _byref(cbs), C.byref(camera(cam)), None if dv else C.byref(hv),
+        _ptr(v) if dv else None, C.byref(prm or params()), _ptr(rec), _ptr(count), capacity,
+        _ptr(out["pair_gid"]), _ptr(out["pair_rec"]), _ptr(out["tile_range"]),
+        _ptr(out["n_pairs_dev"]), _ptr(ws), ws.numel(), _ptr(img["color"]), _ptr(img["depth"]),
+        _ptr(img["sil"]), _ptr(img["t_final"]), _ptr(img["n_contrib"]), _ptr(obs_color),
+        _ptr(obs_depth), _ptr(n_valid), lambda_depth, sil_gate, flags, C.byref(gr), _ptr(loss3),
+        _ptr(ws_bwd), ws_bwd.numel(), _stream(stream)), "csplat_tracking_step")
+    return grads, loss3
 
 
 def _on_device(v) -> bool:

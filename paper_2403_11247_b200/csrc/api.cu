@@ -331,20 +331,21 @@ int csplat_project_bin_render_dv(const csplat_gaussians *g, const csplat_codeboo
                                  depth, silhouette, t_final, n_contrib, stream);
 }
 
-int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
-                       const csplat_camera *cam, const csplat_view *view,
-                       const csplat_params *prm, void *rec, int32_t *count,
-                       int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
-                       uint32_t *tile_range, int64_t *n_pairs_dev, void *ws_bin,
-                       size_t ws_bin_bytes, float *color, float *depth, float *silhouette,
-                       float *t_final, int32_t *n_contrib, const float *d_color,
-                       const float *d_depth, const float *d_silhouette, uint32_t flags,
-                       const csplat_grads *out, void *ws_bwd, size_t ws_bwd_bytes,
-                       void *stream) {
+static int render_step_impl(const csplat_gaussians *g, const csplat_codebook *cb,
+                            const csplat_camera *cam, const csplat_view *view,
+                            const float *view_dev, const csplat_params *prm, void *rec,
+                            int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
+                            void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                            void *ws_bin, size_t ws_bin_bytes, float *color, float *depth,
+                            float *silhouette, float *t_final, int32_t *n_contrib,
+                            const float *d_color, const float *d_depth,
+                            const float *d_silhouette, const csplat::TrackingLoss *loss,
+                            uint32_t flags, const csplat_grads *out, void *ws_bwd,
+                            size_t ws_bwd_bytes, void *stream) {
   RET_IF(check_gaussians(g));
   RET_IF(check_camera(cam));
   RET_IF(check_codebook(cb, true));
-  if (!view || !prm || !out) return invalid("view/params/grads NULL");
+  if ((!view && !view_dev) || !prm || !out) return invalid("view/params/grads NULL");
   if (g->n > 0 && (!rec || !count)) return invalid("rec/count NULL");
   if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
   if (!(prm->mask_eps > 0.f) || !(prm->mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
@@ -353,8 +354,8 @@ int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
   if (pair_capacity > 0 && (!pair_gid || !pair_rec)) return invalid("pair_gid/pair_rec NULL");
   if (!color || !depth || !silhouette || !t_final || !n_contrib)
     return invalid("render_step: image NULL");
-  if (!d_color || !d_depth || !d_silhouette) return invalid("render_step: upstream NULL");
-  if (flags & CSPLAT_POSE_ONLY) return invalid("render_step: CSPLAT_POSE_ONLY not supported");
+  if (!loss && (!d_color || !d_depth || !d_silhouette)) return invalid("render_step: upstream NULL");
+  if (!loss && (flags & CSPLAT_POSE_ONLY)) return invalid("render_step: CSPLAT_POSE_ONLY not supported");
   if (!aligned16(rec) || !aligned16(pair_rec)) {
     set_err("rec/pair_rec must be 16-byte aligned");
     return CSPLAT_ERR_ALIGNMENT;
@@ -370,14 +371,57 @@ int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
   RET_IF(check_device());
   csplat::DecodeArgs d;
   if (cb) d = decode_args(cb);
-  const csplat::StepBwd b{d_color, d_depth, d_silhouette, flags, *out, ws_bwd};
-  return cuda_status(csplat::launch_render_step(*g, cb ? &d : nullptr, *cam, *view, nullptr,
+  const csplat::StepBwd b{d_color, d_depth, d_silhouette, flags, *out, ws_bwd, loss};
+  return cuda_status(csplat::launch_render_step(*g, cb ? &d : nullptr, *cam,
+                                                view ? *view : csplat_view{}, view_dev,
                                                 mask_tau(prm->mask_eps), prm->dilation, *prm, rec,
                                                 count, pair_capacity, pair_gid, pair_rec,
                                                 tile_range, n_pairs_dev, ws_bin, color, depth,
                                                 silhouette, t_final, n_contrib, &b,
                                                 static_cast<cudaStream_t>(stream)),
                      "csplat_render_step");
+}
+
+int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
+                       const csplat_camera *cam, const csplat_view *view,
+                       const csplat_params *prm, void *rec, int32_t *count,
+                       int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                       uint32_t *tile_range, int64_t *n_pairs_dev, void *ws_bin,
+                       size_t ws_bin_bytes, float *color, float *depth, float *silhouette,
+                       float *t_final, int32_t *n_contrib, const float *d_color,
+                       const float *d_depth, const float *d_silhouette, uint32_t flags,
+                       const csplat_grads *out, void *ws_bwd, size_t ws_bwd_bytes,
+                       void *stream) {
+  if (!view) return invalid("view NULL");
+  return render_step_impl(g, cb, cam, view, nullptr, prm, rec, count, pair_capacity, pair_gid,
+                          pair_rec, tile_range, n_pairs_dev, ws_bin, ws_bin_bytes, color, depth,
+                          silhouette, t_final, n_contrib, d_color, d_depth, d_silhouette, nullptr,
+                          flags, out, ws_bwd, ws_bwd_bytes, stream);
+}
+
+int csplat_tracking_step(const csplat_gaussians *g, const csplat_codebook *cb,
+                         const csplat_camera *cam, const csplat_view *view,
+                         const float *view_dev, const csplat_params *prm, void *rec,
+                         int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
+                         void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                         void *ws_bin, size_t ws_bin_bytes, float *color, float *depth,
+                         float *silhouette, float *t_final, int32_t *n_contrib,
+                         const float *obs_color, const float *obs_depth,
+                         const uint64_t *n_valid_dev, float lambda_depth, float sil_gate,
+                         uint32_t flags, const csplat_grads *out, float *loss3_dev,
+                         void *ws_bwd, size_t ws_bwd_bytes, void *stream) {
+  if ((view == nullptr) == (view_dev == nullptr)) return invalid("give exactly one of view / view_dev");
+  if (!obs_color || !obs_depth || !n_valid_dev || !loss3_dev)
+    return invalid("tracking_step: NULL observation argument");
+  if (!std::isfinite(lambda_depth) || !std::isfinite(sil_gate))
+    return invalid("lambda_depth / sil_gate must be finite");
+  const csplat::TrackingLoss tl{color, depth, silhouette, obs_color, obs_depth,
+                                reinterpret_cast<const unsigned long long *>(n_valid_dev),
+                                lambda_depth, sil_gate, loss3_dev};
+  return render_step_impl(g, cb, cam, view, view_dev, prm, rec, count, pair_capacity, pair_gid,
+                          pair_rec, tile_range, n_pairs_dev, ws_bin, ws_bin_bytes, color, depth,
+                          silhouette, t_final, n_contrib, nullptr, nullptr, nullptr, &tl, flags,
+                          out, ws_bwd, ws_bwd_bytes, stream);
 }
 
 int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,

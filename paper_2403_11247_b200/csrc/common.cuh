@@ -347,10 +347,11 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
 // tile chunk (on its own library stream) the sort, the forward and the
 // backward kernel, joined, then the per-Gaussian chain
 struct StepBwd {
-  const float *d_color, *d_depth, *d_sil;
+  const float *d_color, *d_depth, *d_sil;  // upstream (loss == nullptr)
   uint32_t flags;
   csplat_grads out;
   void *ws;
+  const TrackingLoss *loss;                // NEXT-1: upstream formed in the backward
 };
 cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
                                const csplat_camera &cam, const csplat_view &view,

@@ -296,7 +296,8 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
   BinWs w = bin_carve(ws, cap, T);
   cudaError_t e = bin_reset(w, T, s);
   if (e != cudaSuccess) return e;
-  if (bwd && (e = bwd_prep(g, bwd->flags, bwd->out, bwd->ws, nullptr, s)) != cudaSuccess) return e;
+  if (bwd && (e = bwd_prep(g, bwd->flags, bwd->out, bwd->ws, bwd->loss, s)) != cudaSuccess)
+    return e;
   e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
                           ci.tiles_x, cap, nullptr, s);
   if (e != cudaSuccess) return e;
@@ -321,7 +322,7 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
                           sc, (int)t0, (int)(t1 - t0));
     if (e != cudaSuccess) return e;
     if (bwd) {
-      e = launch_render_bwd_tiles(cam, nullptr, prm, pair_rec, tile_range, t_final, n_contrib,
+      e = launch_render_bwd_tiles(cam, bwd->loss, prm, pair_rec, tile_range, t_final, n_contrib,
                                   bwd->d_color, bwd->d_depth, bwd->d_sil, bwd->ws, sc, (int)t0,
                                   (int)(t1 - t0));
       if (e != cudaSuccess) return e;

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import csplat as cs
-from .pipeline import RenderStep
+from .pipeline import FUSED_BIN, RenderStep
 
 
 def rodrigues(w):
@@ -106,12 +106,22 @@ class Tracker:
         prologue, gated-out pixels not replayed) -> device pose step."""
         st = self.step
         g = st.pruned
-        st.project_bin_forward(view_dev)
-        cs.tracking_bwd(g, st.cam, view_dev, st.rec, st.pair_rec, st.tile_range, st.img,
-                        self.obs_color, self.obs_depth, self.n_valid, st.prm, st.cb,
-                        flags=cs.POSE_ONLY, lambda_depth=self.lambda_depth,
-                        sil_gate=self.sil_gate, grads=dict(st.grads, pose=self.pose),
-                        loss3=self.loss3, ws=st.ws_bwd)
+        if FUSED_BIN:  # project + bin + fwd + loss-fused bwd per tile chunk, one call
+            cs.tracking_step(g, st.cam, view_dev, st.capacity, self.obs_color, self.obs_depth,
+                             self.n_valid, st.prm, st.cb, flags=cs.POSE_ONLY,
+                             lambda_depth=self.lambda_depth, sil_gate=self.sil_gate,
+                             rec=st.rec, count=st.count, ws=st.ws_bin,
+                             out=dict(pair_gid=st.pair_gid, pair_rec=st.pair_rec,
+                                      tile_range=st.tile_range, n_pairs_dev=st.n_pairs),
+                             img=st.img, grads=dict(st.grads, pose=self.pose),
+                             loss3=self.loss3, ws_bwd=st.ws_bwd)
+        else:
+            st.project_bin_forward(view_dev)
+            cs.tracking_bwd(g, st.cam, view_dev, st.rec, st.pair_rec, st.tile_range, st.img,
+                            self.obs_color, self.obs_depth, self.n_valid, st.prm, st.cb,
+                            flags=cs.POSE_ONLY, lambda_depth=self.lambda_depth,
+                            sil_gate=self.sil_gate, grads=dict(st.grads, pose=self.pose),
+                            loss3=self.loss3, ws=st.ws_bwd)
         cs.pose_step(view_dev, self.pose, lr_rot, lr_trans)
 
     def capture(self, view, lr_rot=1e-4, lr_trans=1e-4):

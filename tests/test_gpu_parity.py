@@ -738,6 +738,21 @@ def test_loss_fused_backward_matches_separate_kernels(env, pose_only):
     names = ["pose"] if pose_only else GROUPS
     for k in names:
         assert (g_fus[k] - g_sep[k]).norm() <= 1e-5 * g_sep[k].norm(), k
+    # csplat_tracking_step: the same iteration in one call (chunked, host and device view)
+    cap = int(cnt.sum().item()) + 64
+    vd = torch.tensor(np.asarray(view, dtype=np.float32).reshape(-1)[:12], device=dev)
+    for v_arg in (view, vd):
+        _, _, out, img2 = cs.project_bin_render(g, sc.cam, view, cap)   # buffers
+        l_st = torch.full((3,), 7.0, device=dev)                         # overwritten
+        g_st, _ = cs.tracking_step(g, sc.cam, v_arg, cap, obs_c, obs_d, nv, flags=flags,
+                                   lambda_depth=0.5, rec=torch.empty_like(rec),
+                                   count=torch.empty_like(cnt), out=out, img=img2, loss3=l_st)
+        torch.cuda.synchronize()
+        for k in ("color", "depth", "sil", "t_final", "n_contrib"):
+            assert torch.equal(img2[k], img[k]), k
+        assert torch.allclose(l_st, l_fus, rtol=1e-5)
+        for k in names:
+            assert (g_st[k] - g_fus[k]).norm() <= 1e-5 * g_fus[k].norm(), k
     # the oracle: Eq 12 + 14 upstream of the GPU-rendered images, then its backward
     (rC, rD, rS), _, flg = orc.tracking_loss(img["color"].double().cpu().numpy(),
                                               img["depth"].double().cpu().numpy(),
