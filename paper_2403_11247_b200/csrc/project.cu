@@ -5,6 +5,8 @@
 // the R-VQ decode gathers from the (L1/L2-resident) codebooks, and one 64-byte
 // record written as four 16-byte stores.  HBM-bound: 60 B in + 64 B + 4 B out
 // per Gaussian (raw geometry); DA keeps it at ~300 instructions per Gaussian.
+#include <mutex>
+
 #include "bin_dev.cuh"
 
 namespace csplat {
@@ -266,10 +268,12 @@ struct ForkRes {
 
 static cudaError_t fork_res(ForkRes *&out) {
   static ForkRes res[16];
+  static std::mutex mu;  // first use per device may race between host threads
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lock(mu);
   ForkRes &r = res[dev];
   if (!r.start) {
     const unsigned fl = cudaEventDisableTiming;
