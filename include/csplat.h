@@ -181,7 +181,11 @@ int csplat_project_bin_dv(const csplat_gaussians *g, const csplat_codebook *cb,
  * [3][H][W], depth, silhouette, t_final [H][W] and n_contrib [H][W] as
  * csplat_render_fwd.  Pairs beyond pair_capacity are dropped (ranges clamped;
  * no CSPLAT_SYNC check here: read n_pairs_dev).  ws: csplat_workspace_bytes(
- * CSPLAT_OP_BIN_TILES, g->n, pair_capacity, cam).  Errors as those calls. */
+ * CSPLAT_OP_BIN_TILES, g->n, pair_capacity, cam).  Errors as those calls.
+ * The library's fork streams and events are per device and shared by
+ * csplat_project_bin_render, csplat_render_step and csplat_tracking_step:
+ * calls from several host threads onto one device must be serialised by the
+ * caller (enqueueing order defines the fork/join order). */
 int csplat_project_bin_render(const csplat_gaussians *g, const csplat_codebook *cb,
                               const csplat_camera *cam, const csplat_view *view,
                               const csplat_params *prm, void *rec, int32_t *count,
