@@ -17,7 +17,10 @@
 namespace csplat {
 
 constexpr int kPT = 256;         // threads per CTA
-constexpr int kPItems = 2;       // rounds per CTA (keeps >= 2 waves of CTAs at 200k)
+#ifndef CSPLAT_PRUNE_ITEMS
+#define CSPLAT_PRUNE_ITEMS 2
+#endif
+constexpr int kPItems = CSPLAT_PRUNE_ITEMS;  // rounds per CTA (keeps >= 2 waves of CTAs at 200k)
 constexpr int kPTile = kPT * kPItems;
 
 size_t prune_workspace_bytes(int64_t n) {
