@@ -89,3 +89,51 @@ def test_invalid_arguments_rejected_without_device(cs):
     assert L.csplat_workspace_bytes(3, 100, 0, None) > 0
     buf = C.create_string_buffer(256)
     assert L.csplat_last_error(buf, 256) > 0
+
+
+def test_composed_entry_points_reject_invalid_arguments_without_device(cs):
+    """csplat_project_bin(_dv), csplat_project_bin_render(_dv), csplat_render_step and
+    csplat_tracking_step validate their arguments before touching the device."""
+    L = cs.lib()
+    cam = cs.camera(dict(fx=10, fy=10, cx=5, cy=5, width=16, height=16))
+    v, p = cs.view([1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0]), cs.params()
+    gbad = cs.Gaussians(-1, None, None, None, None, None, None, None)
+    g0 = cs.Gaussians(0, None, None, None, None, None, None, None)
+    x = C.c_void_p(16)  # a non-NULL, 16-byte aligned placeholder (never dereferenced)
+    gr = cs.Grads(*([None] * 7))
+    # bad map / NULL view / NULL tile_range / small workspace
+    assert L.csplat_project_bin(C.byref(gbad), None, C.byref(cam), C.byref(v), C.byref(p), x, x,
+                                None, 0, None, None, x, x, 0, x, 1 << 20, None) == 1
+    assert L.csplat_project_bin(C.byref(g0), None, C.byref(cam), None, C.byref(p), x, x,
+                                None, 0, None, None, x, x, 0, x, 1 << 20, None) == 1
+    assert L.csplat_project_bin_dv(C.byref(g0), None, C.byref(cam), None, C.byref(p), x, x,
+                                   None, 0, None, None, x, x, 0, x, 1 << 20, None) == 1
+    assert L.csplat_project_bin(C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p), x, x,
+                                None, 0, None, None, None, x, 0, x, 1 << 20, None) == 1
+    assert L.csplat_project_bin(C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p), x, x,
+                                None, 0, None, None, x, x, 0, x, 0, None) == 4
+    # misaligned pair payload
+    assert L.csplat_project_bin(C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p), x, x,
+                                None, 4, x, C.c_void_p(8), x, x, 0, x, 1 << 20, None) == 2
+    # render: NULL image
+    assert L.csplat_project_bin_render(C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p),
+                                       x, x, 0, None, None, x, x, x, 1 << 20, None, x, x, x, x,
+                                       None) == 1
+    assert L.csplat_project_bin_render_dv(C.byref(g0), None, C.byref(cam), None, C.byref(p),
+                                          x, x, 0, None, None, x, x, x, 1 << 20, x, x, x, x, x,
+                                          None) == 1
+    # step: NULL upstream, POSE_ONLY rejected, small backward workspace
+    step = lambda dC, flags, wsb: L.csplat_render_step(  # noqa: E731
+        C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p), x, x, 0, None, None, x, x, x,
+        1 << 20, x, x, x, x, x, dC, x, x, flags, C.byref(gr), x, wsb, None)
+    assert step(None, 0, 1 << 20) == 1
+    assert step(x, cs.POSE_ONLY, 1 << 20) == 1
+    assert step(x, 0, 0) == 4
+    # tracking step: both / neither view, NULL observations
+    track = lambda hv, dv, obs: L.csplat_tracking_step(  # noqa: E731
+        C.byref(g0), None, C.byref(cam), hv, dv, C.byref(p), x, x, 0, None, None, x, x, x,
+        1 << 20, x, x, x, x, x, obs, x, x, 1.0, 0.99, cs.POSE_ONLY, C.byref(gr), x, x, 1 << 20,
+        None)
+    assert track(C.byref(v), x, x) == 1
+    assert track(None, None, x) == 1
+    assert track(C.byref(v), None, None) == 1
