@@ -287,10 +287,11 @@ constexpr unsigned long long kRangeP = 1ull << 63;
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int64_t T, uint32_t *__restrict__ range, int64_t *__restrict__ n_pairs, BinWs w,
     int64_t cap, const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid,
-    uint4 *__restrict__ pair_rec, int tiles_x, int64_t tile0) {
+    uint4 *__restrict__ pair_rec, int tiles_x, int64_t tile0, int row_step) {
   __shared__ __align__(16) unsigned long long sk[kCtaCap];
   __shared__ uint32_t fill, s_start, s_end;
-  const int64_t tile = tile0 + blockIdx.x;
+  const int64_t tile = row_step ? tile0 + (int64_t)(blockIdx.x / tiles_x) * row_step + blockIdx.x % tiles_x
+                                : tile0 + blockIdx.x;
   const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
 #ifndef CSPLAT_BIN_SMEM_SORT
   // the common case first: a list that fits the threads' registers is sorted
@@ -388,13 +389,13 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
                               const void *rec, uint32_t *pair_gid, void *pair_rec,
                               uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,
-                              int64_t tile0, int64_t ntiles) {
+                              int64_t tile0, int64_t ntiles, int row_step) {
   if (ntiles < 0) ntiles = T - tile0;
   if (ntiles <= 0) return cudaSuccess;
   k_sort_tiles<<<(unsigned)ntiles, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
                                                          static_cast<const uint4 *>(rec), pair_gid,
                                                          static_cast<uint4 *>(pair_rec), tiles_x,
-                                                         tile0);
+                                                         tile0, row_step);
   return cudaGetLastError();
 }
 

@@ -318,7 +318,7 @@ cudaError_t launch_ba_loss(const float *color, const float *depth, const float *
 cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
                               float *depth, float *sil, float *t_final, int32_t *n_contrib,
-                              cudaStream_t s, int tile0 = 0, int ntiles = -1);
+                              cudaStream_t s, int tile0 = 0, int ntiles = -1, int row_step = 0);
 
 // csplat_project_bin_render: projection + bucket, then the per-tile sort and
 // the forward in tile chunks, the sort of chunk c+1 overlapping the forward
@@ -341,7 +341,7 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
                                     const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
-                                    cudaStream_t s, int tile0, int ntiles);
+                                    cudaStream_t s, int tile0, int ntiles, int row_step = 0);
 
 // csplat_render_step: a3 .. a8 for one view -- projection + bucket, then per
 // tile chunk (on its own library stream) the sort, the forward and the

@@ -16,6 +16,10 @@ namespace csplat {
 #endif
 constexpr int kFwdChunks = CSPLAT_FWD_CHUNKS;  // sort / forward pipeline chunks
 constexpr int kFwdChunksMax = 16;
+#ifndef CSPLAT_CHUNK_ROWS
+#define CSPLAT_CHUNK_ROWS 0
+#endif
+constexpr bool kChunkRows = CSPLAT_CHUNK_ROWS != 0;  // chunks of interleaved tile rows
 static_assert(kFwdChunks >= 1 && kFwdChunks <= kFwdChunksMax, "CSPLAT_FWD_CHUNKS");
 
 struct ProjConst {
@@ -316,19 +320,27 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
     if ((e = cudaEventRecord(r->start, s)) != cudaSuccess) return e;
   }
   for (int c = 0; c < K; c++) {
-    const int64_t t0 = T * c / K, t1 = T * (c + 1) / K;
+    // contiguous tile ranges, or (CSPLAT_CHUNK_ROWS) every K-th tile row
+    int64_t t0 = T * c / K, nt = T * (c + 1) / K - t0;
+    int rs = 0;
+    if (kChunkRows && K > 1) {
+      const int64_t rows = ((int64_t)ci.tiles_y - c + K - 1) / K;
+      t0 = (int64_t)c * ci.tiles_x;
+      nt = rows * ci.tiles_x;
+      rs = K * ci.tiles_x;
+    }
     cudaStream_t sc = K > 1 ? r->st[c] : s;
     if (K > 1 && (e = cudaStreamWaitEvent(sc, r->start, 0)) != cudaSuccess) return e;
     e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
-                          n_pairs_dev, sc, t0, t1 - t0);
+                          n_pairs_dev, sc, t0, nt, rs);
     if (e != cudaSuccess) return e;
     e = launch_render_fwd(pair_rec, tile_range, cam, prm, color, depth, sil, t_final, n_contrib,
-                          sc, (int)t0, (int)(t1 - t0));
+                          sc, (int)t0, (int)nt, rs);
     if (e != cudaSuccess) return e;
     if (bwd) {
       e = launch_render_bwd_tiles(cam, bwd->loss, prm, pair_rec, tile_range, t_final, n_contrib,
                                   bwd->d_color, bwd->d_depth, bwd->d_sil, bwd->ws, sc, (int)t0,
-                                  (int)(t1 - t0));
+                                  (int)nt, rs);
       if (e != cudaSuccess) return e;
     }
     if (K > 1 && (e = cudaEventRecord(r->done[c], sc)) != cudaSuccess) return e;

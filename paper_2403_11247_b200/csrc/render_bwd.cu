@@ -211,11 +211,12 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     int tiles_x, float amax, const float *__restrict__ t_final,
     const int32_t *__restrict__ n_contrib, const float *__restrict__ dC,
     const float *__restrict__ dD, const float *__restrict__ dS, float *__restrict__ acc,
-    LossArgs la, int tile0) {
+    LossArgs la, int tile0, int row_step) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tile = tile0 + (int)(blockIdx.x / kCtaPerTile);
+  const int tb = (int)(blockIdx.x / kCtaPerTile);
+  const int tile = row_step ? tile0 + (tb / tiles_x) * row_step + tb % tiles_x : tile0 + tb;
   const int blk = (blockIdx.x % kCtaPerTile) * kCW + (tid >> 5);  // 8x8 block of the tile
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const uint32_t start = range[2 * tile];
@@ -452,7 +453,7 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
                                     const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
-                                    cudaStream_t s, int tile0, int ntiles) {
+                                    cudaStream_t s, int tile0, int ntiles, int row_step) {
   const CamInfo ci = cam_info(cam);
   float *acc = static_cast<float *>(ws);
   static bool attr_done = false;
@@ -479,11 +480,11 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
     la.loss3 = loss->loss3;
     k_render_bwd<true><<<ntiles * kCtaPerTile, kBwdThreads, smem, s>>>(
         static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, nullptr, nullptr, nullptr, acc, la, tile0);
+        t_final, n_contrib, nullptr, nullptr, nullptr, acc, la, tile0, row_step);
   } else {
     k_render_bwd<false><<<ntiles * kCtaPerTile, kBwdThreads, smem, s>>>(
         static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, d_color, d_depth, d_sil, acc, la, tile0);
+        t_final, n_contrib, d_color, d_depth, d_sil, acc, la, tile0, row_step);
   }
   return cudaGetLastError();
 }
@@ -499,7 +500,7 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
   cudaError_t e = bwd_prep(g, flags, out, ws, loss, s);
   if (e != cudaSuccess) return e;
   e = launch_render_bwd_tiles(cam, loss, prm, pair_rec, tile_range, t_final, n_contrib, d_color,
-                              d_depth, d_sil, ws, s, 0, -1);
+                              d_depth, d_sil, ws, s, 0, -1, 0);
   if (e != cudaSuccess || g.n == 0) return e;
   return launch_chain(g, dec, cam, view, view_dev, prm, rec, static_cast<float *>(ws), flags,
                       out, s);

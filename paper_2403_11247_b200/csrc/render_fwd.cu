@@ -117,13 +117,14 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, float tmin, float *__restrict__ color, float *__restrict__ depth,
     float *__restrict__ sil, float *__restrict__ t_final, int32_t *__restrict__ n_contrib,
-    int tile0) {
+    int tile0, int row_step) {
   constexpr int kPW = 8 / PPT;  // pixel warps
   __shared__ __align__(128) float4 buf[kStages][kBatch * 4];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ int done_cnt, end_b;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tile = tile0 + (int)blockIdx.x;
+  const int tile = row_step ? tile0 + (int)(blockIdx.x / tiles_x) * row_step + (int)(blockIdx.x % tiles_x)
+                           : tile0 + (int)blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
   const int len = (int)(end - start);
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
 cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
                               float *depth, float *sil, float *t_final, int32_t *n_contrib,
-                              cudaStream_t s, int tile0, int ntiles) {
+                              cudaStream_t s, int tile0, int ntiles, int row_step) {
   const CamInfo ci = cam_info(cam);
   const int T = ci.tiles_x * ci.tiles_y;
   if (ntiles < 0) ntiles = T - tile0;
@@ -285,7 +286,7 @@ cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
   constexpr int PPT = CSPLAT_FWD_PPT;
   k_render_fwd<PPT><<<ntiles, 256 / PPT + 32, 0, s>>>(
       static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-      prm.t_min, color, depth, sil, t_final, n_contrib, tile0);
+      prm.t_min, color, depth, sil, t_final, n_contrib, tile0, row_step);
   return cudaGetLastError();
 }
 
