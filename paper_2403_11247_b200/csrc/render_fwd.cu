@@ -19,6 +19,11 @@ namespace csplat {
 
 constexpr int kBatch = 32;   // records per TMA batch (2 KB)
 constexpr int kStages = 4;   // ring depth
+#ifdef CSPLAT_FWD_SCALAR
+constexpr bool kFwdScalar = true;
+#else
+constexpr bool kFwdScalar = false;
+#endif
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -74,10 +79,16 @@ __device__ __forceinline__ void composite_pred(PixState &p, bool h, float q, flo
 // composite_pred for the thread's two pixels on packed f32x2 instructions
 // (FMUL2/FFMA2/FADD2: each lane IEEE round-to-nearest, the same values as the
 // scalar form); the compositing is issue-bound, so one slot does both pixels.
+// FPY (CSPLAT_FWD_NANDONE): the pixels' row coordinates, NaN once a pixel has
+// terminated -- its DA q is then NaN and the range test fails, so the q test
+// needs no separate "done" check and termination is one select per pixel
+#ifndef CSPLAT_FWD_NANDONE
+#define CSPLAT_FWD_NANDONE 0  // measured slower: 84.9 vs 82.3 us at C2
+#endif
 __device__ __forceinline__ void composite_pair(PixState &p0, PixState &p1, bool h0, bool h1,
                                                float q0, float q1, float oh, float z,
                                                const float4 &rgb, float amax, float tmin,
-                                               int idx) {
+                                               int idx, f2_t &FPY) {
   const f2_t QE = mul2(pk2(q0, q1), pk2(-0.72134752f, -0.72134752f));  // exp(-q/2)
   const f2_t AR = mul2(pk2(oh, oh), pk2(ex2_approx(lo2(QE)), ex2_approx(hi2(QE))));
   const f2_t AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));
@@ -98,8 +109,14 @@ __device__ __forceinline__ void composite_pair(PixState &p0, PixState &p1, bool 
   p1.T = take1 ? hi2(TEST) : p1.T;
   p0.last = take0 ? idx : p0.last;
   p1.last = take1 ? idx : p1.last;
+#if CSPLAT_FWD_NANDONE
+  const float nan = __int_as_float(0x7fc00000);
+  FPY = pk2((h0 & stop0) ? nan : lo2(FPY), (h1 & stop1) ? nan : hi2(FPY));
+#else
+  (void)FPY;
   p0.done |= (h0 & stop0) ? 1 : 0;
   p1.done |= (h1 & stop1) ? 1 : 0;
+#endif
 }
 
 // PPT = pixels per thread (a column of PPT vertically adjacent pixels): a pixel
@@ -178,6 +195,9 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
   bool wdone = __all_sync(0xffffffffu, mydone);
   if (wdone && lane == 0) atomicAdd(&done_cnt, 1);
   const float fpx = (float)px;
+  f2_t FPY = pk2(p[0].done ? __int_as_float(0x7fc00000) : (float)py0,
+                 (PPT > 1 && p[PPT > 1 ? 1 : 0].done) ? __int_as_float(0x7fc00000)
+                                                      : (float)(py0 + 1));
   for (int b = 0; b < nb; b++) {
     const int s = b % kStages;
     mbar_wait_sleep(&full[s], (uint32_t)(b / kStages) & 1u);
@@ -211,7 +231,11 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
         bool anyh = false;
 #ifndef CSPLAT_FWD_SCALAR
         if constexpr (PPT == 2) {  // the DA q of both pixels on f32x2 (same roundings)
+#if CSPLAT_FWD_NANDONE
+          const f2_t DY = sub2(FPY, pk2(r0.y, r0.y));
+#else
           const f2_t DY = sub2(pk2((float)py0, (float)(py0 + 1)), pk2(r0.y, r0.y));
+#endif
           const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx),
                               fma2(pk2(cbdx, cbdx), DY, mul2(mul2(pk2(r1.x, r1.x), DY), DY)));
           q[0] = lo2(Q);
@@ -227,7 +251,11 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
             const float dy = DSUB((float)(py0 + k), r0.y);
             q[k] = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
           }
-          h[k] = (p[k].done == 0) & da_in_range(q[k], r1.z);  // R2 (DA): 0 <= q <= k2
+          // R2 (DA): 0 <= q <= k2 (a terminated pixel's NaN q fails it, NANDONE)
+          if constexpr (PPT == 2 && CSPLAT_FWD_NANDONE && !kFwdScalar)
+            h[k] = da_in_range(q[k], r1.z);
+          else
+            h[k] = (p[k].done == 0) & da_in_range(q[k], r1.z);
           anyh |= h[k];
         }
 #ifdef CSPLAT_FWD_DIVERGENT
@@ -242,7 +270,8 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
         const int idx = b * kBatch + e + 1;
 #ifndef CSPLAT_FWD_SCALAR
         if constexpr (PPT == 2)
-          composite_pair(p[0], p[1], h[0], h[1], q[0], q[1], r1.y, r1.w, r2, amax, tmin, idx);
+          composite_pair(p[0], p[1], h[0], h[1], q[0], q[1], r1.y, r1.w, r2, amax, tmin, idx,
+                         FPY);
         else
 #endif
         // the pixels as straight-line (predicated) code so their chains interleave
@@ -251,8 +280,12 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
           composite_pred(p[k], h[k], q[k], r1.y, r1.w, r2, amax, tmin, idx);
       }
       mydone = 1;
+      if constexpr (PPT == 2 && CSPLAT_FWD_NANDONE && !kFwdScalar) {
+        mydone = (lo2(FPY) != lo2(FPY)) & (hi2(FPY) != hi2(FPY));
+      } else {
 #pragma unroll
-      for (int k = 0; k < PPT; k++) mydone &= p[k].done;
+        for (int k = 0; k < PPT; k++) mydone &= p[k].done;
+      }
       wdone = __all_sync(0xffffffffu, mydone);
       if (wdone && lane == 0) atomicAdd(&done_cnt, 1);  // before the release below
     }
