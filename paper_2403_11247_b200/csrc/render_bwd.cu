@@ -30,6 +30,12 @@ constexpr int kBB = 32;           // records per TMA batch
 #endif
 constexpr int kBS = KBS_OVERRIDE; // ring depth
 constexpr int kAcc = 12;          // accumulator floats per Gaussian
+#ifndef CSPLAT_BWD_PART10
+#define CSPLAT_BWD_PART10 1  // C5 window 12.69 -> 12.43 ms, C2 bwd 195.4 -> 194.7 us
+#endif
+// shared-memory row of an entry's warp sums: 12 floats (three 16-byte loads)
+// or, CSPLAT_BWD_PART10, the 10 used ones (five 8-byte loads, 3 KB less per CTA)
+constexpr int kPartW = CSPLAT_BWD_PART10 ? 10 : kAcc;
 #ifndef CSPLAT_BWD_CW
 #define CSPLAT_BWD_CW 4
 #endif
@@ -51,7 +57,7 @@ size_t bwd_workspace_bytes(int64_t n) { return (size_t)(n > 0 ? n : 1) * kAcc * 
 struct BwdSmem {
   float4 buf[kBS][kBB * 4];             // staged records
   float4 red[kCW][kG * kV][8];          // per-warp rows of 32 lane partials
-  float part[kBS][kCW][kBB][kAcc];      // per-slot, per-warp sums per batch entry
+  float part[kBS][kCW][kBB][kPartW];    // per-slot, per-warp sums per batch entry
   uint64_t full[kBS], empty[kBS];
   uint32_t pmask[kBS][kCW];             // bit e: warp w wrote part[slot][w][e]
   int wmax[kCW];
@@ -302,11 +308,19 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
       for (int w = 0; w < kCW; w++) {
         if (!((sm.pmask[s][w] >> e) & 1u)) continue;
         hit = true;
+#if CSPLAT_BWD_PART10
+        const float2 *t = reinterpret_cast<const float2 *>(sm.part[s][w][e]);
+        const float2 t0 = t[0], t1 = t[1], t2 = t[2], t3 = t[3], t4 = t[4];
+        s0.x += t0.x; s0.y += t0.y; s0.z += t1.x; s0.w += t1.y;
+        s1.x += t2.x; s1.y += t2.y; s1.z += t3.x; s1.w += t3.y;
+        s2.x += t4.x; s2.y += t4.y;
+#else
         const float4 *t = reinterpret_cast<const float4 *>(sm.part[s][w][e]);
         const float4 t0 = t[0], t1 = t[1], t2 = t[2];
         s0.x += t0.x; s0.y += t0.y; s0.z += t0.z; s0.w += t0.w;
         s1.x += t1.x; s1.y += t1.y; s1.z += t1.z; s1.w += t1.w;
         s2.x += t2.x; s2.y += t2.y;
+#endif
       }
       if (hit) {
         const uint32_t gid = __float_as_uint(sm.buf[s][e * 4 + 2].w);
