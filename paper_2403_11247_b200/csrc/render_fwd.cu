@@ -18,7 +18,10 @@
 namespace csplat {
 
 constexpr int kBatch = 32;   // records per TMA batch (2 KB)
-constexpr int kStages = 4;   // ring depth
+#ifndef CSPLAT_FWD_STAGES
+#define CSPLAT_FWD_STAGES 4
+#endif
+constexpr int kStages = CSPLAT_FWD_STAGES;  // ring depth
 #ifdef CSPLAT_FWD_SCALAR
 constexpr bool kFwdScalar = true;
 #else
