@@ -138,6 +138,11 @@ def params(mask_eps=0.01, alpha_max=0.99, t_min=1e-4, dilation=0.3) -> Params:
     return Params(mask_eps, alpha_max, t_min, dilation)
 
 
+def set_flag_window(t_rel: float = 1e-5, cap_abs: float = 1e-6):
+    """Ambiguity window of the forward's pixel flags."""
+    lib().oracle_set_flag_window(C.c_double(t_rel), C.c_double(cap_abs))
+
+
 def set_row_window(row_lo: int = 0, row_hi: int = -1):
     """Restrict render_fwd/render_bwd to pixel rows [row_lo, row_hi) (timing samples)."""
     lib().oracle_set_row_window(C.c_int32(row_lo), C.c_int32(row_hi))

@@ -153,6 +153,8 @@ int oracle_ba_patch_loss(const double *color, const double *depth, const float *
 /* Restrict oracle_render_fwd/bwd to pixel rows [row_lo, row_hi) (row_hi < 0:
  * all rows) -- used only to time a bounded CPU-baseline sample. */
 void oracle_set_row_window(int32_t row_lo, int32_t row_hi);
+/* Flagging window of oracle_render_fwd; defaults 1e-5, 1e-6. */
+void oracle_set_flag_window(double t_rel, double cap_abs);
 
 /* DA helpers exported for pins. */
 float oracle_pexp(float x);

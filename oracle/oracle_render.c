@@ -93,10 +93,16 @@ typedef struct {
     int capped;
 } or_entry;
 
-/* Ambiguity windows: a float32 evaluation of T(1-alpha) drifts
- * from float64 by ~1e-7 per composited entry; o_hat*G by ~2e-7 (ex2.approx). */
-#define FLAG_T_REL 2e-5
-#define FLAG_CAP_ABS 1e-6
+/* Ambiguity windows (SURVEY §8(c) policy 2): a pixel is flagged
+ * when a termination test T(1-alpha) lies within FLAG_T_REL (relative) of
+ * t_min, or o_hat*G within FLAG_CAP_ABS of alpha_max, because there a float32
+ * evaluation may decide the other way than this float64 one.  Defaults are
+ * the §8(c) values; oracle_set_flag_window() lets a test measure how many
+ * pixels a wider or narrower window would flag (it does not change any
+ * rendered value). */
+static double FLAG_T_REL = 1e-5;
+static double FLAG_CAP_ABS = 1e-6;
+void oracle_set_flag_window(double t_rel, double cap_abs) { FLAG_T_REL = t_rel; FLAG_CAP_ABS = cap_abs; }
 
 /* Composite one pixel over an ordered candidate list (Eq 3-5).  Returns the
  * number of composited entries; fills out6 = (C rgb, D, S, T_final), the

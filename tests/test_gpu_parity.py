@@ -5,6 +5,9 @@ Bit-exact: records, counts, pair lists/order, tile ranges, R-VQ indices and
 reconstructions, survivors, keep_map.  Images: max |diff| <= 1e-4 off the
 oracle-flagged pixels, n_contrib exact there.  Gradients: rel-L2 <= 1e-3 per
 group with flagged pixels' upstream zeroed on both sides."""
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -15,6 +18,16 @@ pytestmark = pytest.mark.gpu
 IMG_TOL = 1e-4
 GRAD_TOL = 1e-3
 GROUPS = ["mean", "opacity", "rgb", "log_scale", "quat", "mask", "pose"]
+FLAG_BUDGET = 1e-4      # SURVEY §8(c) policy 2: flagged pixels <= 1e-4 x pixels
+
+
+def record_stat(name, **kw):
+    """Append a measured parity statistic (flagged-pixel counts, error maxima)
+    to gpurun_out/parity_stats.jsonl so the margins are visible."""
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, "parity_stats.jsonl"), "a") as f:
+        f.write(json.dumps(dict(test=name, **kw)) + "\n")
 
 
 @pytest.fixture(scope="module")
@@ -119,13 +132,20 @@ def run_and_compare(env, sc, view=None, use_codebook=True, prm=None, bwd=True, s
     out = cs.render_fwd(b["pair_rec"], b["tile_range"], cam, prm_c)
     fo = orc.render_fwd(rec_o, gid_o, rng_o, cam, prm_o)
     ok = fo["flags"] == 0
-    assert (~ok).sum() <= max(2, 2e-4 * H * W), (~ok).sum()
+    n_flag = int((~ok).sum())
+    errs_img = {}
     for k in ("depth", "sil", "t_final"):
         err = np.abs(out[k].cpu().numpy() - fo[k])[ok]
-        assert err.size == 0 or err.max() <= IMG_TOL, (k, err.max())
+        errs_img[k] = float(err.max()) if err.size else 0.0
     cerr = np.abs(out["color"].cpu().numpy() - fo["color"])[:, ok]
-    assert cerr.size == 0 or cerr.max() <= IMG_TOL
-    assert np.array_equal(out["n_contrib"].cpu().numpy()[ok], fo["n_contrib"][ok])
+    errs_img["color"] = float(cerr.max()) if cerr.size else 0.0
+    n_nc = int((out["n_contrib"].cpu().numpy()[ok] != fo["n_contrib"][ok]).sum())
+    record_stat(f"{H}x{W}/{sc.n}", flagged=n_flag, budget=max(2, FLAG_BUDGET * H * W),
+                n_contrib_mismatch_unflagged=n_nc, **{f"maxerr_{k}": v for k, v in errs_img.items()})
+    assert n_flag <= max(2, FLAG_BUDGET * H * W), f"{n_flag} flagged pixels of {H * W}"
+    for k, e in errs_img.items():
+        assert e <= IMG_TOL, (k, e)
+    assert n_nc == 0, f"{n_nc} unflagged pixels with a different n_contrib"
     res = dict(fo=fo, out=out, npairs=npairs)
     if not bwd:
         return res
@@ -513,6 +533,40 @@ def test_replica_c2_full_parity(env):
     fo = res["fo"]
     assert res["npairs"] > 100_000
     assert fo["e_pix"] > 10_000_000
+
+
+@pytest.mark.slow
+def test_replica_c2_flag_window_sweep(env):
+    """Measures the §8(c) flagging policy at C2: for oracle flag windows
+    (relative distance of a termination test from t_min) from 0 to 4e-5, how
+    many pixels are flagged and how many unflagged pixels still disagree with
+    the GPU on n_contrib.  The policy window (1e-5) must leave none."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.replica_scene(0)
+    cam, v = sc.cam, sc.views[0]
+    cb, cbo = _codebooks(env, sc)
+    S = orc.Scene(**sc.planes())
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec_o, cnt_o = orc.project(S, cam, v, codebook=cbo)
+    gid_o, rng_o = orc.bin_tiles(rec_o, cnt_o, cam)
+    rec, cnt = cs.project(g, cam, v, cs.params(), cb=cb)
+    b = cs.bin_tiles(rec, cnt, cam, capacity=len(gid_o) + 128)
+    out = cs.render_fwd(b["pair_rec"], b["tile_range"], cam, cs.params())
+    ncg = out["n_contrib"].cpu().numpy()
+    sweep = {}
+    try:
+        for w in (0.0, 2.5e-6, 5e-6, 1e-5, 2e-5, 4e-5):
+            orc.set_flag_window(w, 1e-6)
+            fo = orc.render_fwd(rec_o, gid_o, rng_o, cam)
+            ok = fo["flags"] == 0
+            sweep[str(w)] = dict(flagged=int((~ok).sum()),
+                                 mismatch_unflagged=int((ncg[ok] != fo["n_contrib"][ok]).sum()))
+    finally:
+        orc.set_flag_window()
+    record_stat("c2_flag_window_sweep", pixels=cam["width"] * cam["height"], sweep=sweep)
+    pol = sweep["1e-05"]
+    assert pol["mismatch_unflagged"] == 0, sweep
+    assert pol["flagged"] <= FLAG_BUDGET * cam["width"] * cam["height"], sweep
 
 
 @pytest.mark.parametrize("mode", ["sequential", "pipelined", "pipelined_graph"])

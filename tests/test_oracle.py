@@ -638,3 +638,108 @@ def test_prune_render_invariance(orc):
     b = render_all(orc, S2, sc.cam)[-1]
     for key in ("color", "depth", "sil", "t_final", "n_contrib"):
         assert np.array_equal(a[key], b[key])
+
+
+# ---------------------------------------------------------------- round-2 pins
+# (early termination / n_contrib, the DA J-clamp branch, keyframe
+# overlap under a non-identity current pose)
+
+def _gauss_list(orc, gs):
+    means = np.array([g["mean"] for g in gs], dtype=np.float64)
+    n = len(gs)
+    return orc.Scene(mean=np.float32(means.T),
+                     opacity=np.float32([math.log(g["o_hat"] / (1 - g["o_hat"])) for g in gs]),
+                     rgb=np.float32(np.array([g["rgb"] for g in gs]).T),
+                     log_scale=np.float32(np.array([[math.log(g["sigma"])] * 3 for g in gs]).T),
+                     quat=np.float32(np.tile([[1.0], [0], [0], [0]], (1, n))),
+                     mask=np.full(n, 3.0, dtype=np.float32))
+
+
+def _check_pixel(out, px, py, ref, tol):
+    assert np.allclose(out["color"][:, py, px], ref["color"], atol=tol), out["color"][:, py, px]
+    assert abs(out["depth"][py, px] - ref["depth"]) < tol
+    assert abs(out["sil"][py, px] - ref["sil"]) < tol
+    assert abs(out["t_final"][py, px] - ref["t_final"]) < tol
+    assert out["n_contrib"][py, px] == ref["n_contrib"]
+
+
+def test_termination_alpha_max_one_drops_back_gaussian(orc):
+    """SPEC S:147 with alpha_max = 1 and t_min = 1e-4 (R3): the back Gaussian's
+    alpha is exactly 1, so T(1 - alpha) = 0 < t_min and it is NOT composited."""
+    ref = GOLD["termination"]["alpha_max_1"]
+    S = orc.Scene(mean=np.float32([[0, 0], [0, 0], [1, 2]]), opacity=np.float32([0.0, 20.0]),
+                  rgb=np.float32([[1, 0], [0, 1], [0, 0]]),
+                  log_scale=np.float32(np.full((3, 2), math.log(0.05))),
+                  quat=np.float32([[1, 1], [0, 0], [0, 0], [0, 0]]), mask=np.float32([3, 3]))
+    prm = orc.params(alpha_max=ref["alpha_max"], t_min=ref["t_min"])
+    rec, cnt, gid, rng_, out = render_all(orc, S, CF_CAM, prm=prm)
+    px, py = ref["pixel"]
+    _check_pixel(out, px, py, ref, 1e-7)
+    o6, ncomp = orc.render_pixel(rec, cnt, CF_CAM, px, py, prm)   # untiled form agrees
+    assert ncomp == 1 and abs(o6[5] - ref["t_final"]) < 1e-7 and abs(o6[1]) < 1e-12
+
+
+def test_termination_mid_list_n_contrib(orc):
+    """R3 mid-list: a non-covering entry between two composited ones, then the
+    terminating entry, then one never examined.  n_contrib counts list
+    positions (last composited index + 1), not composited entries."""
+    ref = GOLD["termination"]["mid_list"]
+    S = _gauss_list(orc, ref["gaussians"])
+    prm = orc.params(alpha_max=ref["alpha_max"], t_min=ref["t_min"])
+    rec, cnt, gid, rng_, out = render_all(orc, S, CF_CAM, prm=prm)
+    px, py = ref["pixel"]
+    t = (py // 16) * ((64 + 15) // 16) + px // 16
+    assert list(gid[rng_[t, 0]:rng_[t, 1]]) == [0, 1, 2, 3, 4]      # depth order
+    _check_pixel(out, px, py, ref, ref["tolerance"])
+    o6, ncomp = orc.render_pixel(rec, cnt, CF_CAM, px, py, prm)
+    assert ncomp == ref["n_composited"]
+    assert np.allclose(o6, list(ref["color"]) + [ref["depth"], ref["sil"], ref["t_final"]],
+                       atol=ref["tolerance"])
+    # without the terminating Gaussian, the fifth one is composited instead
+    S2 = _gauss_list(orc, [g for i, g in enumerate(ref["gaussians"]) if i != 3])
+    out2 = render_all(orc, S2, CF_CAM, prm=prm)[-1]
+    assert out2["n_contrib"][py, px] == 4
+    assert abs(out2["t_final"][py, px] - 0.001) < 1e-6
+
+
+@pytest.mark.parametrize("case", ["x_clamped", "y_clamped"])
+def test_projection_jacobian_clamp_closed_form(orc, case):
+    """R6 in the DA projection (oracle_project): an off-FOV Gaussian's Sigma' is
+    built from the clamped x/z (or y/z), its mean from the unclamped one."""
+    g = GOLD["jacobian_clamp"]
+    c = g[case]
+    S = one_gaussian_scene(orc, [c["mean"]], sigma=g["sigma"], o_hat=g["o_hat"])
+    rec, cnt = orc.project(S, CF_CAM, IDV)
+    assert cnt[0] > 0
+    f = rec[0].view(np.float32)
+    assert abs(f[0] - c["uv"][0]) < 1e-4 and abs(f[1] - c["uv"][1]) < 1e-4
+    Sp = sigma_prime_from_rec(rec[0], dil=0.0)          # Sigma' incl. the 0.3 I dilation
+    ref = np.array(c["sigma_prime"])
+    assert np.allclose(Sp, ref, rtol=g["tolerance_rel"], atol=1e-3), Sp
+    px0, py0, px1, py1 = rec[0, 12] & 0xffff, rec[0, 12] >> 16, rec[0, 13] & 0xffff, rec[0, 13] >> 16
+    assert [px0, px1] == c["pixel_rect"]["x"] and [py0, py1] == c["pixel_rect"]["y"]
+
+
+def test_keyframe_overlap_plane_non_identity_pose(orc):
+    """P:138 overlap count against closed-form counts on a fronto-parallel
+    plane seen from a rotated and translated current camera."""
+    from scipy.spatial.transform import Rotation
+    k = GOLD["keyframe_overlap_plane"]
+    cam = dict(k["camera"], near=0.01, far=100.0)
+    R = Rotation.from_rotvec([0.3, -0.5, 0.2]).as_matrix()
+    t = np.array([0.4, -0.7, 1.1])
+    cur = np.concatenate([R, t[:, None]], 1).astype(np.float32)
+    depth = np.full((cam["height"], cam["width"]), k["depth"], dtype=np.float32)
+    names = ["shift_x", "shift_y", "forward", "behind"]
+    views = []
+    for nm in names:
+        v = cur.astype(np.float64).copy()
+        v[:, 3] += k["shifts"][nm]
+        views.append(v.astype(np.float32))
+    counts = orc.keyframe_overlap(depth, cam, cur, views + [cur])
+    for i, nm in enumerate(names):
+        assert counts[i] == k["counts"][nm], (nm, counts[i])
+    # the current view itself: every interior pixel maps to itself; the border
+    # pixels land exactly on the frustum boundary, where float32 rounding decides
+    H, W = depth.shape
+    assert (H - 2) * (W - 2) <= counts[-1] <= H * W
