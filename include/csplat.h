@@ -53,6 +53,18 @@ enum csplat_status {
 #define CSPLAT_TILE 16           /* screen tile edge in pixels (R4) */
 #define CSPLAT_RECORD_BYTES 64   /* projected record size */
 
+/* Device status bits.  A status word is a caller-owned device uint32 that
+ * library kernels OR these bits into and NEVER clear (the caller zeroes it,
+ * e.g. once per window iteration, and reads it whenever it likes -- one word
+ * can collect the status of many asynchronous calls, CUDA-graph replays
+ * included).  SURVEY §8(b): "overflow is written to a device status word and
+ * downstream kernels early-out"; "out-of-range codebook indices are culled
+ * and set a device status bit". */
+#define CSPLAT_STATUS_CAPACITY 1u    /* a tile's (tile, Gaussian) pairs did not fit the pair
+                                        capacity: that tile's range is left EMPTY, so the
+                                        renderers treat it as background (early-out) */
+#define CSPLAT_STATUS_CODE_INDEX 2u  /* a codebook index >= P: that Gaussian is culled */
+
 /* Flags */
 #define CSPLAT_SYNC 1u           /* bin_tiles: read n_pairs back, return CAPACITY if it exceeds the capacity */
 #define CSPLAT_POSE_ONLY 2u      /* render_bwd: only the pose gradient (tracking) */
@@ -102,6 +114,9 @@ typedef struct {
     const float *rot_codes;    /* [L][P][4] */
     const void *scale_idx;     /* [L][n] uint8/uint16 */
     const void *rot_idx;       /* [L][n] uint8/uint16 */
+    uint32_t *status;          /* optional device status word (NULL = not reported):
+                                  CSPLAT_STATUS_CODE_INDEX is OR-ed in when a decoded
+                                  Gaussian has an index >= P (that Gaussian is culled) */
 } csplat_codebook;
 
 /* Gradients: planes [k][n] like csplat_gaussians (any may be NULL to skip),
@@ -136,10 +151,20 @@ int csplat_project_dv(const csplat_gaussians *g, const csplat_codebook *cb,
  *                             bit w set unless alpha < 1/255 provably holds over
  *                             the whole 8x8 pixel block w (x half w&1, y half w>>1)
  *                             of the pair's tile
- *   tile_range[T][2]          [start, end) of every tile, T = ceil(W/16)*ceil(H/16)
+ *   tile_range[T+1][2]        [start, end) of every tile, T = ceil(W/16)*ceil(H/16);
+ *                             entry T is the view's STATUS slot {status word, max
+ *                             n_pairs}: the library ORs CSPLAT_STATUS_CAPACITY into
+ *                             tile_range[2T] and atomically maxes the total pair
+ *                             count (clamped to 2^32-1) into tile_range[2T+1]; it
+ *                             never clears them (the caller zeroes the slot once,
+ *                             then reads it after any number of calls)
  *   n_pairs_dev               device int64: the total (may exceed the capacity)
- * Pairs beyond pair_capacity are dropped (ranges clamped); with CSPLAT_SYNC the
- * call synchronises and returns CSPLAT_ERR_CAPACITY in that case.
+ * Capacity overflow: a tile whose pairs do not all fit (its prefix + count
+ * exceeds pair_capacity, or its bucket spill was lost) gets an EMPTY range and
+ * sets CSPLAT_STATUS_CAPACITY, so every downstream kernel treats it as
+ * background (early-out) instead of rendering a truncated list; tiles that fit
+ * are exact.  With CSPLAT_SYNC the call also synchronises and returns
+ * CSPLAT_ERR_CAPACITY.
  * ws: csplat_workspace_bytes(CSPLAT_OP_BIN_TILES, n, pair_capacity, cam). */
 int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csplat_camera *cam,
                      int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
@@ -451,6 +476,16 @@ int csplat_last_error(char *buf, size_t len);
 const char *csplat_status_string(int status);
 /* ABI version (major << 16 | minor). */
 int csplat_version(void);
+
+/* The composed entry points (csplat_project_bin_render, csplat_render_step,
+ * csplat_tracking_step) fork their tile chunks onto library streams: one set
+ * of streams and events per (calling host thread, device), created on that
+ * thread's first composed call and destroyed at thread exit or by this call.
+ * Per-thread sets mean concurrent callers never share a fork/join event.
+ * These are the only resources the library keeps between calls (it never
+ * retains caller memory).  Call only when the thread has no composed call in
+ * flight (e.g. after synchronising its streams).  Returns CSPLAT_OK. */
+int csplat_release_thread_resources(void);
 
 #ifdef __cplusplus
 }

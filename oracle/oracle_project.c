@@ -69,6 +69,15 @@ void or_geometry(const or_gaussians *g, const or_codebook *cb, int64_t i, float 
         for (int k = 0; k < 4; k++) q[k] = g->quat[k * n + i];
         return;
     }
+    /* a Gaussian with any index outside [0, P) is culled --
+     * reported as a NaN log-scale, which every user of the geometry culls. */
+    for (int l = 0; l < cb->stages; l++)
+        if (cb->scale_idx[(int64_t)l * n + i] >= (uint32_t)cb->size ||
+            cb->rot_idx[(int64_t)l * n + i] >= (uint32_t)cb->size) {
+            ls[0] = ls[1] = ls[2] = NAN;
+            q[0] = 1.0f; q[1] = q[2] = q[3] = 0.0f;
+            return;
+        }
     /* S_hat^L = sum_{k=1..L} C^k[i^k], summed in stage order (R17). */
     for (int l = 0; l < cb->stages; l++) {
         uint32_t si = cb->scale_idx[(int64_t)l * n + i];

@@ -130,8 +130,12 @@ def gpu_ba(step, views, obs_color, obs_depth, patches, lambda_depth=1.0, lambda_
                 rank, world, group)
     ba.n_rays = n_rays
     ba.pipe = None
+    slots = [step]
+    # pair capacity over every keyframe since the last check (all view slots'
+    # status words, one host read; pipeline.RenderStep.check_capacity)
+    ba.check_capacity = lambda: slots[0].check_capacity(slots[1:])
     if pipelined:  # window.py's two-slot pipeline: per-slot buffers and upstream
-        slots = [step, step.view_slot()]
+        slots.append(step.view_slot())
         ups = [up, tuple(torch.empty_like(t) for t in up)]
 
         def front(k, b):

@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("CSPLAT_LIB", os.path.join(_PKG, "libcsplat.so"))
 TILE = 16
 RECORD_BYTES = 64
 SYNC, POSE_ONLY, ACCUMULATE = 1, 2, 4
+STATUS_CAPACITY, STATUS_CODE_INDEX = 1, 2  # device status bits (csplat.h)
 OP_BIN_TILES, OP_RENDER_BWD, OP_MASK_PRUNE = 1, 2, 3
 
 
@@ -57,7 +58,7 @@ class GaussiansOut(C.Structure):
 class Codebook(C.Structure):
     _fields_ = [("stages", C.c_int32), ("size", C.c_int32), ("idx_bytes", C.c_int32),
                 ("reserved", C.c_int32), ("scale_codes", C.c_void_p), ("rot_codes", C.c_void_p),
-                ("scale_idx", C.c_void_p), ("rot_idx", C.c_void_p)]
+                ("scale_idx", C.c_void_p), ("rot_idx", C.c_void_p), ("status", C.c_void_p)]
 
 
 class Grads(C.Structure):
@@ -206,12 +207,35 @@ class CodebookT:
     rot_codes: torch.Tensor    # [L, P, 4]
     scale_idx: torch.Tensor    # [L, n] uint8/int16
     rot_idx: torch.Tensor
+    status: torch.Tensor | None = None  # [1] int32 device status word (STATUS_CODE_INDEX)
 
     def struct(self) -> Codebook:
         L, P = self.scale_codes.shape[:2]
         ib = self.scale_idx.element_size()
         return Codebook(L, P, ib, 0, _ptr(self.scale_codes), _ptr(self.rot_codes),
-                        _ptr(self.scale_idx), _ptr(self.rot_idx))
+                        _ptr(self.scale_idx), _ptr(self.rot_idx), _ptr(self.status))
+
+
+def release_thread_resources():
+    """csplat_release_thread_resources: free this thread's fork streams / events."""
+    _check(lib().csplat_release_thread_resources(), "csplat_release_thread_resources")
+
+
+def alloc_tile_range(cam: dict, device) -> torch.Tensor:
+    """tile_range [T + 1, 2] int32: the T tile ranges plus the view's status slot
+    {status word, max n_pairs} (csplat.h), zeroed here; the library only ORs /
+    maxes into the slot, so it collects every call until the caller clears it."""
+    tx, ty = tiles(cam)
+    return torch.zeros((tx * ty + 1, 2), dtype=torch.int32, device=device)
+
+
+def range_status(tile_range: torch.Tensor) -> torch.Tensor:
+    """The status slot of tile_range (device tensor [2]: status bits, max n_pairs)."""
+    return tile_range[-1]
+
+
+def clear_status(tile_range: torch.Tensor):
+    tile_range[-1].zero_()
 
 
 def _byref(x):
@@ -250,7 +274,7 @@ def project_bin(g: GaussianMap, cam: dict, v, capacity: int, prm: Params | None 
     if out is None:
         out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
                    pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
-                   tile_range=torch.empty((tx * ty, 2), dtype=torch.int32, device=dev),
+                   tile_range=alloc_tile_range(cam, dev),
                    n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
     if ws is None:
         ws = torch.empty(workspace_bytes(OP_BIN_TILES, n, capacity, cam), dtype=torch.uint8,
@@ -284,7 +308,7 @@ def project_bin_render(g: GaussianMap, cam: dict, v, capacity: int, prm: Params 
     if out is None:
         out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
                    pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
-                   tile_range=torch.empty((tx * ty, 2), dtype=torch.int32, device=dev),
+                   tile_range=alloc_tile_range(cam, dev),
                    n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
     if img is None:
         img = dict(color=torch.empty((3, H, W), device=dev), depth=torch.empty((H, W), device=dev),
@@ -325,7 +349,7 @@ def render_step(g: GaussianMap, cam: dict, v, capacity: int, d_color, d_depth, d
     if out is None:
         out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
                    pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
-                   tile_range=torch.empty((tx * ty, 2), dtype=torch.int32, device=dev),
+                   tile_range=alloc_tile_range(cam, dev),
                    n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
     if img is None:
         img = dict(color=torch.empty((3, H, W), device=dev), depth=torch.empty((H, W), device=dev),
@@ -455,7 +479,7 @@ def bin_tiles(rec, count, cam: dict, capacity: int, ws=None, out=None, sync=True
     if out is None:
         out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
                    pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
-                   tile_range=torch.empty((tx * ty, 2), dtype=torch.int32, device=dev),
+                   tile_range=alloc_tile_range(cam, dev),
                    n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
     if ws is None:
         ws = torch.empty(workspace_bytes(OP_BIN_TILES, n, capacity, cam), dtype=torch.uint8,

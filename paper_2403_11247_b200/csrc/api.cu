@@ -98,6 +98,7 @@ csplat::DecodeArgs decode_args(const csplat_codebook *cb) {
   d.rot_codes = cb->rot_codes;
   d.scale_idx = cb->scale_idx;
   d.rot_idx = cb->rot_idx;
+  d.status = cb->status;
   return d;
 }
 
@@ -117,7 +118,12 @@ float mask_tau(float eps) {
 
 extern "C" {
 
-int csplat_version(void) { return (1 << 16) | 0; }
+int csplat_version(void) { return (2 << 16) | 0; }  // 2.0: tile_range status slot, codebook status
+
+int csplat_release_thread_resources(void) {
+  csplat::release_thread_fork_resources();
+  return CSPLAT_OK;
+}
 
 const char *csplat_status_string(int s) {
   switch (s) {

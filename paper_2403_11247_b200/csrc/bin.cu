@@ -203,11 +203,7 @@ __device__ __forceinline__ void emit_pair(unsigned long long key, int64_t pos,
   const uint4 *src = rec4 + (int64_t)gid * 4;
   const uint4 v0 = src[0], v1 = src[1], v2 = src[2];
   uint4 v3 = src[3];
-#ifdef CSPLAT_BIN_NOMASK  // timing attribution only
-  v3.z = 0xfu;
-#else
   v3.z = block_mask(v0, v1, v3, X0, Y0);
-#endif
   uint4 *dst = pair_rec + pos * 4;
   dst[0] = v0; dst[1] = v1; dst[2] = v2; dst[3] = v3;
 }
@@ -287,13 +283,11 @@ constexpr unsigned long long kRangeP = 1ull << 63;
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int64_t T, uint32_t *__restrict__ range, int64_t *__restrict__ n_pairs, BinWs w,
     int64_t cap, const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid,
-    uint4 *__restrict__ pair_rec, int tiles_x, int64_t tile0, int row_step) {
+    uint4 *__restrict__ pair_rec, int tiles_x, int64_t tile0) {
   __shared__ __align__(16) unsigned long long sk[kCtaCap];
   __shared__ uint32_t fill, s_start, s_end;
-  const int64_t tile = row_step ? tile0 + (int64_t)(blockIdx.x / tiles_x) * row_step + blockIdx.x % tiles_x
-                                : tile0 + blockIdx.x;
+  const int64_t tile = tile0 + blockIdx.x;
   const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
-#ifndef CSPLAT_BIN_SMEM_SORT
   // the common case first: a list that fits the threads' registers is sorted
   // BEFORE the look-back (the sort needs only the tile's own count), so by the
   // time the look-back runs the preceding tiles have mostly published and the
@@ -315,7 +309,6 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     while (np2 < n0) np2 <<= 1;
     sort_regs256(x0, x1, np2, reinterpret_cast<unsigned long long(*)[2 * kSortThreads]>(sk));
   }
-#endif
   if (threadIdx.x < 32) {  // the tile's output offset: a look-back over the preceding tiles
     const int lane = threadIdx.x;
     const unsigned long long cnt = w.cur[tile];
@@ -341,33 +334,38 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
       const unsigned long long tot = prefix + cnt;
       atomicExch(w.status + tile, kRangeP | tot);
       const unsigned long long c = (unsigned long long)cap;
+      // capacity overflow (csplat.h): a tile whose pairs do not all fit -- past
+      // the capacity, or with bucket spill lost from a full overflow list --
+      // gets an EMPTY range (the renderers treat it as background) and sets
+      // the status bit; every other tile's list is exact
+      const bool cut = tot > c || (cnt > (unsigned long long)kBucketCap && (int64_t)*w.ovf_n > cap);
       s_start = (uint32_t)(prefix < c ? prefix : c);
-      s_end = (uint32_t)(tot < c ? tot : c);
+      s_end = cut ? s_start : (uint32_t)tot;
       range[2 * tile] = s_start;
       range[2 * tile + 1] = s_end;
-      if (tile == T - 1) *n_pairs = (int64_t)tot;
+      if (cut) atomicOr(range + 2 * T, CSPLAT_STATUS_CAPACITY);
+      if (tile == T - 1) {
+        *n_pairs = (int64_t)tot;
+        atomicMax(range + 2 * T + 1, (uint32_t)(tot < 0xffffffffull ? tot : 0xffffffffull));
+      }
     }
   }
   __syncthreads();
   const uint32_t start = s_start, end = s_end;
-  const int len = (int)(end - start);  // < the tile's pair count only beyond the capacity
+  const int len = (int)(end - start);  // the tile's pair count, or 0 (empty or cut)
   if (len == 0) return;
-#ifndef CSPLAT_BIN_SMEM_SORT
   if (reg_path) {  // sorted above; len < cnt_t only beyond the capacity (reported)
     const int t = threadIdx.x;
     if (2 * t < len) emit_pair(x0, (int64_t)start + 2 * t, rec4, pair_gid, pair_rec, X0, Y0);
     if (2 * t + 1 < len) emit_pair(x1, (int64_t)start + 2 * t + 1, rec4, pair_gid, pair_rec, X0, Y0);
     return;
   }
-#endif
   unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
   const int nb = min(len, kBucketCap);
   const unsigned long long *bk = w.bucket + tile * kBucketCap;
   for (int k = threadIdx.x; k < nb; k += kSortThreads) a[k] = bk[k];
-  if (len > kBucketCap) {  // the rest of the tile's keys are in the overflow list
+  if (len > kBucketCap) {  // the rest of the tile's keys are in the overflow list (all kept)
     if (threadIdx.x == 0) fill = kBucketCap;
-    // placeholders (Gaussian 0, sorted last) for keys lost beyond the capacity
-    for (int k = kBucketCap + threadIdx.x; k < len; k += kSortThreads) a[k] = ~0ull << 32;
     __syncthreads();
     const int64_t no = min((int64_t)*w.ovf_n, cap);
     for (int64_t o = threadIdx.x; o < no; o += kSortThreads)
@@ -389,13 +387,13 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
                               const void *rec, uint32_t *pair_gid, void *pair_rec,
                               uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,
-                              int64_t tile0, int64_t ntiles, int row_step) {
+                              int64_t tile0, int64_t ntiles) {
   if (ntiles < 0) ntiles = T - tile0;
   if (ntiles <= 0) return cudaSuccess;
   k_sort_tiles<<<(unsigned)ntiles, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
                                                          static_cast<const uint4 *>(rec), pair_gid,
                                                          static_cast<uint4 *>(pair_rec), tiles_x,
-                                                         tile0, row_step);
+                                                         tile0);
   return cudaGetLastError();
 }
 

@@ -28,7 +28,7 @@ cudaError_t bin_reset(const BinWs &w, int64_t T, cudaStream_t s);
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
                               const void *rec, uint32_t *pair_gid, void *pair_rec,
                               uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,
-                              int64_t tile0 = 0, int64_t ntiles = -1, int row_step = 0);
+                              int64_t tile0 = 0, int64_t ntiles = -1);
 
 // Warp-cooperative expansion of 32 Gaussians' tile rectangles.  Lane l holds
 // Gaussian base + l's pair count c, its pixel rectangle corners rx, ry (record

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256, 3) k_chain(
     g[6] = a2.y;
     float ls[3], qv[4];
     if (use_dec) {
-      rvq_decode<LF>(dec, n, i, ls, qv);  // the decoded geometry the renderer saw (R20)
+      rvq_decode<LF>(dec, n, i, ls, qv, false);  // the decoded geometry the renderer saw (R20)
     } else {
       for (int k = 0; k < 3; k++) ls[k] = lsc[k * n + i];
       for (int k = 0; k < 4; k++) qv[k] = quat[k * n + i];

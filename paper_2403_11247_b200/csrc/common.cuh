@@ -136,11 +136,9 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parit
       : "memory");
   return ok != 0;
 }
-#ifndef CSPLAT_MBAR_SLEEP_NS
-#define CSPLAT_MBAR_SLEEP_NS 20000
-#endif
+constexpr uint32_t kMbarSleepNs = 20000;  // suspend-time hint (an upper bound)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
-  while (!mbar_try_wait_hint(bar, parity, CSPLAT_MBAR_SLEEP_NS)) {
+  while (!mbar_try_wait_hint(bar, parity, kMbarSleepNs)) {
   }
 }
 // 1-D TMA bulk copy global -> shared, completion signalled on `bar`.
@@ -216,14 +214,26 @@ struct DecodeArgs {
   int L, P, idx_bytes;
   const float *scale_codes, *rot_codes;
   const void *scale_idx, *rot_idx;
+  uint32_t *status;  // optional: CSPLAT_STATUS_CODE_INDEX is OR-ed in (csplat.h)
 };
 
-// a codebook index (precondition: < P; clamped to P - 1 so that a violating
-// index cannot read outside the codebook)
-__device__ __forceinline__ uint32_t load_rvq_idx(const void *p, int bytes, int64_t off, int P) {
-  const uint32_t k = bytes == 1 ? (uint32_t)__ldg((const uint8_t *)p + off)
-                                : (uint32_t)__ldg((const uint16_t *)p + off);
-  return min(k, (uint32_t)(P - 1));
+__device__ __forceinline__ uint32_t load_rvq_idx(const void *p, int bytes, int64_t off) {
+  return bytes == 1 ? (uint32_t)__ldg((const uint8_t *)p + off)
+                    : (uint32_t)__ldg((const uint16_t *)p + off);
+}
+
+// a Gaussian with a codebook index >= P is culled (its decoded
+// log-scale becomes NaN, which the projection's non-finite test culls, as
+// the oracle does) and the codebook's status word gets CSPLAT_STATUS_CODE_INDEX;
+// the gathers use a clamped index so nothing is read outside the codebook.
+// Only a live Gaussian (i < n, mask on: `report`) sets the bit; index planes
+// beyond the live count may hold anything.
+__device__ __forceinline__ void rvq_flag_bad(const DecodeArgs &dec, bool bad, bool report,
+                                             float (&ls)[3]) {
+  if (bad) {
+    ls[0] = __int_as_float(0x7fc00000);
+    if (report && dec.status) atomicOr(dec.status, CSPLAT_STATUS_CODE_INDEX);
+  }
 }
 
 // Eq 10 decode (R17, R20): S_hat^L = sum_l C^l[i^l], summed in stage order, of
@@ -232,22 +242,26 @@ __device__ __forceinline__ uint32_t load_rvq_idx(const void *p, int bytes, int64
 // so a thread waits for two memory round trips instead of 2 L dependent ones.
 template <int LF>
 __device__ __forceinline__ void rvq_decode(const DecodeArgs &dec, int64_t n, int64_t i,
-                                           float (&ls)[3], float (&qv)[4]) {
+                                           float (&ls)[3], float (&qv)[4], bool report) {
   const float4 *rot4 = reinterpret_cast<const float4 *>(dec.rot_codes);
+  const uint32_t Pm1 = (uint32_t)(dec.P - 1);
   if constexpr (LF > 0) {
     uint32_t si[LF], ri[LF];
 #pragma unroll
     for (int l = 0; l < LF; l++) {
-      si[l] = load_rvq_idx(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i, dec.P);
-      ri[l] = load_rvq_idx(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i, dec.P);
+      si[l] = load_rvq_idx(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i);
+      ri[l] = load_rvq_idx(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i);
     }
+    uint32_t mx = 0;
+#pragma unroll
+    for (int l = 0; l < LF; l++) mx = max(mx, max(si[l], ri[l]));
     float s[LF][3];
     float4 r[LF];
 #pragma unroll
     for (int l = 0; l < LF; l++) {
-      const float *sc = dec.scale_codes + ((int64_t)l * dec.P + si[l]) * 3;
+      const float *sc = dec.scale_codes + ((int64_t)l * dec.P + min(si[l], Pm1)) * 3;
       s[l][0] = __ldg(sc); s[l][1] = __ldg(sc + 1); s[l][2] = __ldg(sc + 2);
-      r[l] = __ldg(rot4 + ((int64_t)l * dec.P + ri[l]));
+      r[l] = __ldg(rot4 + ((int64_t)l * dec.P + min(ri[l], Pm1)));
     }
     ls[0] = s[0][0]; ls[1] = s[0][1]; ls[2] = s[0][2];
     qv[0] = r[0].x; qv[1] = r[0].y; qv[2] = r[0].z; qv[3] = r[0].w;
@@ -257,12 +271,15 @@ __device__ __forceinline__ void rvq_decode(const DecodeArgs &dec, int64_t n, int
       qv[0] = DADD(qv[0], r[l].x); qv[1] = DADD(qv[1], r[l].y);
       qv[2] = DADD(qv[2], r[l].z); qv[3] = DADD(qv[3], r[l].w);
     }
+    rvq_flag_bad(dec, mx > Pm1, report, ls);
   } else {
+    bool bad = false;
     for (int l = 0; l < dec.L; l++) {
-      const uint32_t si = load_rvq_idx(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i, dec.P);
-      const uint32_t ri = load_rvq_idx(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i, dec.P);
-      const float *sc = dec.scale_codes + ((int64_t)l * dec.P + si) * 3;
-      const float4 rc = __ldg(rot4 + ((int64_t)l * dec.P + ri));
+      const uint32_t si = load_rvq_idx(dec.scale_idx, dec.idx_bytes, (int64_t)l * n + i);
+      const uint32_t ri = load_rvq_idx(dec.rot_idx, dec.idx_bytes, (int64_t)l * n + i);
+      bad |= (si > Pm1) | (ri > Pm1);
+      const float *sc = dec.scale_codes + ((int64_t)l * dec.P + min(si, Pm1)) * 3;
+      const float4 rc = __ldg(rot4 + ((int64_t)l * dec.P + min(ri, Pm1)));
       const float s0 = __ldg(sc), s1 = __ldg(sc + 1), s2 = __ldg(sc + 2);
       if (l == 0) {
         ls[0] = s0; ls[1] = s1; ls[2] = s2;
@@ -273,6 +290,7 @@ __device__ __forceinline__ void rvq_decode(const DecodeArgs &dec, int64_t n, int
         qv[2] = DADD(qv[2], rc.z); qv[3] = DADD(qv[3], rc.w);
       }
     }
+    rvq_flag_bad(dec, bad, report, ls);
   }
 }
 
@@ -296,6 +314,8 @@ cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
                                int64_t *n_pairs_dev, void *ws, cudaStream_t s);
 
 size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam);
+// the calling thread's fork streams / events of the composed calls (project.cu)
+void release_thread_fork_resources();
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
                        int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid,
                        void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
@@ -318,7 +338,7 @@ cudaError_t launch_ba_loss(const float *color, const float *depth, const float *
 cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
                               float *depth, float *sil, float *t_final, int32_t *n_contrib,
-                              cudaStream_t s, int tile0 = 0, int ntiles = -1, int row_step = 0);
+                              cudaStream_t s, int tile0 = 0, int ntiles = -1);
 
 // csplat_project_bin_render: projection + bucket, then the per-tile sort and
 // the forward in tile chunks, the sort of chunk c+1 overlapping the forward
@@ -341,7 +361,7 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
                                     const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
-                                    cudaStream_t s, int tile0, int ntiles, int row_step = 0);
+                                    cudaStream_t s, int tile0, int ntiles);
 
 // csplat_render_step: a3 .. a8 for one view -- projection + bucket, then per
 // tile chunk (on its own library stream) the sort, the forward and the

@@ -11,16 +11,11 @@
 
 namespace csplat {
 
-#ifndef CSPLAT_FWD_CHUNKS
-#define CSPLAT_FWD_CHUNKS 2
-#endif
-constexpr int kFwdChunks = CSPLAT_FWD_CHUNKS;  // sort / forward pipeline chunks
-constexpr int kFwdChunksMax = 16;
-#ifndef CSPLAT_CHUNK_ROWS
-#define CSPLAT_CHUNK_ROWS 0
-#endif
-constexpr bool kChunkRows = CSPLAT_CHUNK_ROWS != 0;  // chunks of interleaved tile rows
-static_assert(kFwdChunks >= 1 && kFwdChunks <= kFwdChunksMax, "CSPLAT_FWD_CHUNKS");
+// sort / forward / backward pipeline chunks of contiguous tile ranges (C2:
+// 2 chunks 2324/s, 3-4 the same within noise, 8 chunks 2113/s; chunks of
+// interleaved tile rows 2335 vs 2371/s: a tile's look-back then walks over the
+// other chunk's unpublished rows)
+constexpr int kFwdChunks = 2;
 
 struct ProjConst {
   float V[12];
@@ -54,7 +49,8 @@ __device__ __forceinline__ void project_one(
   const float m = mask[j];
   float ls[3], qv[4];
   if (use_dec) {
-    rvq_decode<LF>(dec, n, j, ls, qv);  // Eq 10: S_hat^L = sum_l C^l[i^l] (R17, R20)
+    // Eq 10: S_hat^L = sum_l C^l[i^l] (R17, R20); a bad index culls (NaN)
+    rvq_decode<LF>(dec, n, j, ls, qv, ok && (m > pc.tau));
   } else {
     ls[0] = lsc[j]; ls[1] = lsc[n + j]; ls[2] = lsc[2 * n + j];
     qv[0] = quat[j]; qv[1] = quat[n + j]; qv[2] = quat[2 * n + j]; qv[3] = quat[3 * n + j];
@@ -264,28 +260,60 @@ cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
                            n_pairs_dev, s);
 }
 
-// library-owned fork streams and events (per device), created on first use
+// Fork streams and events of the composed entry points: one set per (host
+// thread, device), created on the thread's first composed call on that device
+// and destroyed when the thread exits or calls csplat_release_thread_resources.
+// Per-thread sets mean concurrent callers (a tracking and a mapping thread on
+// one GPU) never share a start / done event, so one caller's join can never
+// wait on the other's work.  These are the only resources the library keeps
+// between calls; it never retains caller memory.
 struct ForkRes {
-  cudaStream_t st[kFwdChunksMax] = {};
-  cudaEvent_t start = nullptr, done[kFwdChunksMax] = {};
+  cudaStream_t st[kFwdChunks] = {};
+  cudaEvent_t start = nullptr, done[kFwdChunks] = {};
+  bool ready = false;
+  void release() {
+    for (int c = 0; c < kFwdChunks; c++) {
+      if (st[c]) cudaStreamDestroy(st[c]);
+      if (done[c]) cudaEventDestroy(done[c]);
+      st[c] = nullptr;
+      done[c] = nullptr;
+    }
+    if (start) cudaEventDestroy(start);
+    start = nullptr;
+    ready = false;
+  }
 };
 
+struct ThreadForkRes {
+  ForkRes dev[16];
+  ~ThreadForkRes() { release(); }
+  void release() {
+    for (auto &r : dev) r.release();
+  }
+};
+
+static thread_local ThreadForkRes t_fork;
+
+void release_thread_fork_resources() { t_fork.release(); }
+
 static cudaError_t fork_res(ForkRes *&out) {
-  static ForkRes res[16];
-  static std::mutex mu;  // first use per device may race between host threads
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
-  std::lock_guard<std::mutex> lock(mu);
-  ForkRes &r = res[dev];
-  if (!r.start) {
+  ForkRes &r = t_fork.dev[dev];
+  if (!r.ready) {
     const unsigned fl = cudaEventDisableTiming;
-    for (int c = 0; c < kFwdChunksMax; c++) {
-      if ((e = cudaStreamCreateWithFlags(&r.st[c], cudaStreamNonBlocking)) != cudaSuccess) return e;
-      if ((e = cudaEventCreateWithFlags(&r.done[c], fl)) != cudaSuccess) return e;
+    for (int c = 0; c < kFwdChunks; c++) {
+      if ((e = cudaStreamCreateWithFlags(&r.st[c], cudaStreamNonBlocking)) != cudaSuccess) break;
+      if ((e = cudaEventCreateWithFlags(&r.done[c], fl)) != cudaSuccess) break;
     }
-    if ((e = cudaEventCreateWithFlags(&r.start, fl)) != cudaSuccess) return e;
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.start, fl);
+    if (e != cudaSuccess) {
+      r.release();
+      return e;
+    }
+    r.ready = true;
   }
   out = &r;
   return cudaSuccess;
@@ -313,41 +341,35 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
   // run its backward); the chunks run concurrently, so one chunk's issue-bound
   // forward / backward overlaps the other's latency-bound sort and the
   // kernels' tails overlap each other
-  const int K = kFwdChunks;
+  constexpr int K = kFwdChunks;
   ForkRes *r = nullptr;
-  if (K > 1) {
-    if ((e = fork_res(r)) != cudaSuccess) return e;
-    if ((e = cudaEventRecord(r->start, s)) != cudaSuccess) return e;
-  }
-  for (int c = 0; c < K; c++) {
-    // contiguous tile ranges, or (CSPLAT_CHUNK_ROWS) every K-th tile row
-    int64_t t0 = T * c / K, nt = T * (c + 1) / K - t0;
-    int rs = 0;
-    if (kChunkRows && K > 1) {
-      const int64_t rows = ((int64_t)ci.tiles_y - c + K - 1) / K;
-      t0 = (int64_t)c * ci.tiles_x;
-      nt = rows * ci.tiles_x;
-      rs = K * ci.tiles_x;
-    }
-    cudaStream_t sc = K > 1 ? r->st[c] : s;
-    if (K > 1 && (e = cudaStreamWaitEvent(sc, r->start, 0)) != cudaSuccess) return e;
+  if ((e = fork_res(r)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(r->start, s)) != cudaSuccess) return e;
+  int forked = 0;  // chunk streams that wait on `start` (must be joined, even on error)
+  for (int c = 0; c < K && e == cudaSuccess; c++) {
+    const int64_t t0 = T * c / K, nt = T * (c + 1) / K - t0;
+    cudaStream_t sc = r->st[c];
+    if ((e = cudaStreamWaitEvent(sc, r->start, 0)) != cudaSuccess) break;
+    forked = c + 1;
     e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
-                          n_pairs_dev, sc, t0, nt, rs);
-    if (e != cudaSuccess) return e;
-    e = launch_render_fwd(pair_rec, tile_range, cam, prm, color, depth, sil, t_final, n_contrib,
-                          sc, (int)t0, (int)nt, rs);
-    if (e != cudaSuccess) return e;
-    if (bwd) {
+                          n_pairs_dev, sc, t0, nt);
+    if (e == cudaSuccess)
+      e = launch_render_fwd(pair_rec, tile_range, cam, prm, color, depth, sil, t_final,
+                            n_contrib, sc, (int)t0, (int)nt);
+    if (e == cudaSuccess && bwd)
       e = launch_render_bwd_tiles(cam, bwd->loss, prm, pair_rec, tile_range, t_final, n_contrib,
                                   bwd->d_color, bwd->d_depth, bwd->d_sil, bwd->ws, sc, (int)t0,
-                                  (int)nt, rs);
-      if (e != cudaSuccess) return e;
-    }
-    if (K > 1 && (e = cudaEventRecord(r->done[c], sc)) != cudaSuccess) return e;
+                                  (int)nt);
   }
-  if (K > 1)
-    for (int c = 0; c < K; c++)
-      if ((e = cudaStreamWaitEvent(s, r->done[c], 0)) != cudaSuccess) return e;
+  // join every forked stream back into the caller's stream before returning --
+  // also after an error, so a capture is never left with unjoined work and
+  // later work on `s` stays ordered after the chunks already enqueued
+  for (int c = 0; c < forked; c++) {
+    cudaError_t ej = cudaEventRecord(r->done[c], r->st[c]);
+    if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s, r->done[c], 0);
+    if (e == cudaSuccess) e = ej;
+  }
+  if (e != cudaSuccess) return e;
   if (!bwd || g.n == 0) return cudaSuccess;
   return launch_chain(g, dec, cam, view, view_dev, prm, rec, static_cast<float *>(bwd->ws),
                       bwd->flags, bwd->out, s);

@@ -16,41 +16,30 @@
 // v_j = <rgb_j, dL/dC> + z_j dL/dD + dL/dS, dL/dalpha_j = T_j (v_j - B_j),
 // B_{j-1} = alpha_j v_j + (1-alpha_j) B_j.  A thread adds its two pixels'
 // ten partials (raw moments of the conic/mean gradient, o_hat, z, r, g, b;
-// bwd_pixel_pair) in registers; the warp
+// bwd_pair) in registers; the warp
 // stores the lanes' partials of kG entries as shared-memory rows and each lane
 // sums whole rows with rotated LDS.128 (a transposed reduction: ~2
 // instructions per (entry, value) instead of a 10-instruction shuffle tree).
+#include <atomic>
+
 #include "common.cuh"
 
 namespace csplat {
 
 constexpr int kBB = 32;           // records per TMA batch
-#ifndef KBS_OVERRIDE
-#define KBS_OVERRIDE 3
-#endif
-constexpr int kBS = KBS_OVERRIDE; // ring depth
+constexpr int kBS = 3;            // ring depth
 constexpr int kAcc = 12;          // accumulator floats per Gaussian
-#ifndef CSPLAT_BWD_PART10
-#define CSPLAT_BWD_PART10 1  // C5 window 12.69 -> 12.43 ms, C2 bwd 195.4 -> 194.7 us
-#endif
-// shared-memory row of an entry's warp sums: 12 floats (three 16-byte loads)
-// or, CSPLAT_BWD_PART10, the 10 used ones (five 8-byte loads, 3 KB less per CTA)
-constexpr int kPartW = CSPLAT_BWD_PART10 ? 10 : kAcc;
-#ifndef CSPLAT_BWD_CW
-#define CSPLAT_BWD_CW 4
-#endif
+// shared-memory row of an entry's warp sums: the 10 used floats (five 8-byte
+// loads in the fold; 12 floats = three 16-byte loads measured slower: C5
+// window 12.69 vs 12.43 ms, C2 backward 195.4 vs 194.7 us)
+constexpr int kPartW = 10;
 // pixel (consumer) warps per CTA, each an 8x8 block of the tile (32 lanes x 2
-// pixels): 4 = the whole 16x16 tile; 2 = half a tile (two CTAs per tile: twice
-// the CTAs, finer-grained waves, the tile's list streamed by both)
-constexpr int kCW = CSPLAT_BWD_CW;
-constexpr int kCtaPerTile = 4 / kCW;
+// pixels): 4 = the whole 16x16 tile (half-tile CTAs measured slower)
+constexpr int kCW = 4;
 constexpr int kBwdThreads = (kCW + 1) * 32;  // + 1 producer warp
 constexpr int kG = 3;             // active entries per transposed reduction: kG*kV <= 32 rows = one pass
 constexpr int kV = 10;            // partials per (pixel, entry)
-#ifndef CSPLAT_BWD_MIN_BLOCKS
-#define CSPLAT_BWD_MIN_BLOCKS (CSPLAT_BWD_CW == 4 ? 5 : 9)
-#endif
-constexpr int kBwdMinBlocks = CSPLAT_BWD_MIN_BLOCKS;  // CTAs per SM the register budget targets
+constexpr int kBwdMinBlocks = 5;  // CTAs per SM the register budget targets (6-7 measured slower)
 
 size_t bwd_workspace_bytes(int64_t n) { return (size_t)(n > 0 ? n : 1) * kAcc * sizeof(float); }
 
@@ -75,116 +64,59 @@ struct BPix {
   int last;
 };
 
-// One replay entry j for the thread's two pixels (same column: dx shared, dy0,
-// dy1), as straight-line predicated code so the two dependency chains
-// interleave (inactive pixels contribute exact zeros and leave T and B
-// unchanged: alpha = 0 gives rcp(1) = 1).  With a = alpha dL/dalpha the
-// partials are the raw moments
+// One replay entry j for the thread's two pixels (same column: dx shared; lo =
+// upper pixel, hi = lower) as packed float32 pairs: every per-pixel add / mul
+// / fma is one f32x2 instruction (each lane IEEE round-to-nearest, so the DA q
+// is bit-identical to the forward's).  With a = alpha dL/dalpha the partials
+// are the raw moments
 //   v0..4 = sum a dx, sum a dy, sum a dx^2, sum a dx dy, sum a dy^2,
 //   v5 = sum G dL/dalpha, v6 = sum w gD, v7..9 = sum w gC
 // (w = alpha T_j); the conic's constants and the -1/2 of dalpha/dq are applied
 // once per Gaussian in k_chain (linear, so summing first is exact algebra):
 //   dL/du = ca Sx + cb Sy, dL/dv = cb Sx + cc Sy, dL/dca = -Sxx/2,
 //   dL/d(cb) = -Sxy, dL/dcc = -Syy/2   (q = ca dx^2 + 2cb dx dy + cc dy^2).
-__device__ __forceinline__ bool bwd_pixel_pair(BPix (&pp)[2], int j, float dx, float dy0,
-                                               float dy1, const float4 &r0, const float4 &r1,
-                                               const float4 &r2, float amax, float (&v)[kV]) {
-  const float dys[2] = {dy0, dy1};
-  const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);  // shared by the column
-  float av[2], gd[2], w[2];
-  bool any = false;
-#pragma unroll
-  for (int k = 0; k < 2; k++) {
-    BPix &p = pp[k];
-    const float dy = dys[k];
-    // DA q, bit-identical to the forward's
-    const float q = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
-    const bool val = (j < p.last) & da_in_range(q, r1.z);
-    any |= val;
-    const float G = ex2_approx_b(q * -0.72134752f);  // exp(-q/2), same expression as the forward
-    const float araw = r1.y * G;
-    const float alpha = val ? fminf(amax, araw) : 0.0f;
-    const float om = 1.0f - alpha;
-    float rcp;  // alpha <= alpha_max < 1 (R1)
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(om));
-    const float Tj = p.T * rcp;
-    w[k] = alpha * Tj;
-    const float vv = fmaf(r2.x, p.gr, fmaf(r2.y, p.gg, fmaf(r2.z, p.gb, fmaf(r1.w, p.gd, p.gs))));
-    // R23: no gradient through a capped alpha
-    const float dLda = (val & (araw < amax)) ? Tj * (vv - p.B) : 0.0f;
-    av[k] = alpha * dLda;
-    gd[k] = G * dLda;
-    p.B = fmaf(alpha, vv, om * p.B);
-    p.T = Tj;
-  }
-  // the entry's partials (written, not accumulated: v is per entry)
-  const float sx = dx * (av[0] + av[1]);
-  const float t0 = av[0] * dy0, t1 = av[1] * dy1;
-  const float sy = t0 + t1;
-  v[0] = sx;
-  v[1] = sy;
-  v[2] = dx * sx;
-  v[3] = dx * sy;
-  v[4] = fmaf(t0, dy0, t1 * dy1);
-  v[5] = gd[0] + gd[1];
-  v[6] = fmaf(pp[1].gd, w[1], pp[0].gd * w[0]);
-  v[7] = fmaf(pp[1].gr, w[1], pp[0].gr * w[0]);
-  v[8] = fmaf(pp[1].gg, w[1], pp[0].gg * w[0]);
-  v[9] = fmaf(pp[1].gb, w[1], pp[0].gb * w[0]);
-  return any;
-}
-
-// The thread's two pixels as packed float32 pairs (lo = upper pixel, hi =
-// lower): the same arithmetic as bwd_pixel_pair with every per-pixel add / mul
-// / fma issued once as an f32x2 instruction (each lane IEEE round-to-nearest,
-// so the DA q is still bit-identical to the forward's); the replay is
-// issue-bound, so this removes ~20 issue slots per (warp, entry).
+// T_j = T_{j+1} / (1 - alpha_j) and B_{j-1} = B_j + alpha_j (v_j - B_j) are
+// updated in place (the (v - B) is shared with dL/dalpha).  A pixel that does
+// not composite entry j gets q = +inf, so G = ex2(-inf) = +0 and alpha = 0:
+// T and B unchanged (rcp(1) = 1), exact zeros in every partial.
 struct BPix2 {
   f2_t T, B, gr, gg, gb, gd, gs;
   int last0, last1;
 };
 
-__device__ __forceinline__ bool bwd_pair_packed(BPix2 &P, int j, float dx, f2_t DY,
-                                                const float4 &r0, const float4 &r1,
-                                                const float4 &r2, float amax, float (&v)[kV]) {
+__device__ __forceinline__ bool bwd_pair(BPix2 &P, int j, float dx, f2_t DY, const float4 &r0,
+                                         const float4 &r1, const float4 &r2, float amax,
+                                         float (&v)[kV]) {
   const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
-  const f2_t Y = mul2(mul2(pk2(r1.x, r1.x), DY), DY);  // DMUL(DMUL(cc, dy), dy)
-  const f2_t X = fma2(pk2(cbdx, cbdx), DY, Y);         // DFMA(cbdx, dy, .)
-  const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx), X); // DFMA(cadx, dx, .)
+  const f2_t Y = mul2(mul2(pk2(r1.x, r1.x), DY), DY);
+  const f2_t X = fma2(pk2(cbdx, cbdx), DY, Y);
+  const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx), X);
   const float q0 = lo2(Q), q1 = hi2(Q);
   const bool val0 = (j < P.last0) & da_in_range(q0, r1.z);
   const bool val1 = (j < P.last1) & da_in_range(q1, r1.z);
-  // exp(-q/2) as in the forward; a pixel that does not composite entry j gets
-  // q = +inf here, so G = ex2(-inf) = +0 and alpha = 0: it leaves T and B
-  // unchanged (rcp(1 - 0) = 1) and adds exact zeros to every partial
   const f2_t QM = pk2(val0 ? q0 : __int_as_float(0x7f800000), val1 ? q1 : __int_as_float(0x7f800000));
   const f2_t QE = mul2(QM, pk2(-0.72134752f, -0.72134752f));
   const f2_t G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
   const f2_t AR = mul2(pk2(r1.y, r1.y), G);
-  const float ar0 = lo2(AR), ar1 = hi2(AR);
-  const f2_t AL = pk2(fminf(amax, ar0), fminf(amax, ar1));
+  const f2_t AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));  // R1
   const f2_t OM = sub2(pk2(1.0f, 1.0f), AL);
-  float rc0, rc1;  // alpha <= alpha_max < 1 (R1)
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));
+  float rc0, rc1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));  // alpha <= alpha_max < 1
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc1) : "f"(hi2(OM)));
-  // T_j = T_{j+1} / (1 - alpha_j), updated in place (P.T is T_j from here on;
-  // "+l" keeps the loop-carried pair in its registers: no copies per entry)
   asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(P.T) : "l"(pk2(rc0, rc1)));
   const f2_t W = mul2(AL, P.T);
   const f2_t VV = fma2(pk2(r2.x, r2.x), P.gr,
                        fma2(pk2(r2.y, r2.y), P.gg,
                             fma2(pk2(r2.z, r2.z), P.gb, fma2(pk2(r1.w, r1.w), P.gd, P.gs))));
-  const f2_t D0 = mul2(P.T, sub2(VV, P.B));
-  // R23: no gradient through a capped alpha (a non-compositing pixel has
-  // alpha = G = 0, so its dL/dalpha only ever meets zero factors)
-  const f2_t DL = pk2(ar0 < amax ? lo2(D0) : 0.0f, ar1 < amax ? hi2(D0) : 0.0f);
+  const f2_t VB = sub2(VV, P.B);
+  const f2_t D0 = mul2(P.T, VB);
+  // R23: no gradient through a capped alpha
+  const f2_t DL = pk2(lo2(AR) < amax ? lo2(D0) : 0.0f, hi2(AR) < amax ? hi2(D0) : 0.0f);
   const f2_t AV = mul2(AL, DL);
   const f2_t GD = mul2(G, DL);
-  // B_{j-1} = alpha v + (1 - alpha) B_j, in place (same roundings as fma2(AL, VV, mul2(OM, B)))
-  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(P.B) : "l"(OM));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(P.B) : "l"(AL), "l"(VV));
-  const f2_t TT = mul2(AV, DY);   // a dy
-  const f2_t T2 = mul2(TT, DY);   // a dy^2
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(P.B) : "l"(AL), "l"(VB));
+  const f2_t TT = mul2(AV, DY);
+  const f2_t T2 = mul2(TT, DY);
   const f2_t WD = mul2(W, P.gd), WR = mul2(W, P.gr), WG = mul2(W, P.gg), WB = mul2(W, P.gb);
   const float sx = dx * (lo2(AV) + hi2(AV));
   const float sy = lo2(TT) + hi2(TT);
@@ -217,13 +149,13 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     int tiles_x, float amax, const float *__restrict__ t_final,
     const int32_t *__restrict__ n_contrib, const float *__restrict__ dC,
     const float *__restrict__ dD, const float *__restrict__ dS, float *__restrict__ acc,
-    LossArgs la, int tile0, int row_step) {
+    LossArgs la, int tile0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tb = (int)(blockIdx.x / kCtaPerTile);
-  const int tile = row_step ? tile0 + (tb / tiles_x) * row_step + tb % tiles_x : tile0 + tb;
-  const int blk = (blockIdx.x % kCtaPerTile) * kCW + (tid >> 5);  // 8x8 block of the tile
+  const int tb = (int)blockIdx.x;
+  const int tile = tile0 + tb;
+  const int blk = wid;  // the warp's 8x8 block of the tile
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const uint32_t start = range[2 * tile];
   const bool producer = wid == kCW;
@@ -308,19 +240,11 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
       for (int w = 0; w < kCW; w++) {
         if (!((sm.pmask[s][w] >> e) & 1u)) continue;
         hit = true;
-#if CSPLAT_BWD_PART10
         const float2 *t = reinterpret_cast<const float2 *>(sm.part[s][w][e]);
         const float2 t0 = t[0], t1 = t[1], t2 = t[2], t3 = t[3], t4 = t[4];
         s0.x += t0.x; s0.y += t0.y; s0.z += t1.x; s0.w += t1.y;
         s1.x += t2.x; s1.y += t2.y; s1.z += t3.x; s1.w += t3.y;
         s2.x += t4.x; s2.y += t4.y;
-#else
-        const float4 *t = reinterpret_cast<const float4 *>(sm.part[s][w][e]);
-        const float4 t0 = t[0], t1 = t[1], t2 = t[2];
-        s0.x += t0.x; s0.y += t0.y; s0.z += t0.z; s0.w += t0.w;
-        s1.x += t1.x; s1.y += t1.y; s1.z += t1.z; s1.w += t1.w;
-        s2.x += t2.x; s2.y += t2.y;
-#endif
       }
       if (hit) {
         const uint32_t gid = __float_as_uint(sm.buf[s][e * 4 + 2].w);
@@ -355,15 +279,13 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
   }
 
   // ---- pixel warps
-  const float fpx = (float)px, fpy0 = (float)py0, fpy1 = (float)py1;
-#ifndef CSPLAT_BWD_SCALAR
+  const float fpx = (float)px;
   BPix2 P;
   P.T = pk2(pp[0].T, pp[1].T); P.B = pk2(pp[0].B, pp[1].B);
   P.gr = pk2(pp[0].gr, pp[1].gr); P.gg = pk2(pp[0].gg, pp[1].gg); P.gb = pk2(pp[0].gb, pp[1].gb);
   P.gd = pk2(pp[0].gd, pp[1].gd); P.gs = pk2(pp[0].gs, pp[1].gs);
   P.last0 = pp[0].last; P.last1 = pp[1].last;
-  const f2_t FPY = pk2(fpy0, fpy1);
-#endif
+  const f2_t FPY = pk2((float)py0, (float)py1);
   float(*red)[8 * 4] = reinterpret_cast<float(*)[8 * 4]>(sm.red[wid]);  // [kG*kV][32]
   for (int k = 0; k < nb; k++) {
     const int s = k % kBS;
@@ -416,13 +338,8 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
         const float4 r1 = rb[e * 4 + 1];
         const float4 r2 = rb[e * 4 + 2];
         float v[kV];
-        const float dx = DSUB(fpx, r0.x);
-#ifdef CSPLAT_BWD_SCALAR
-        const bool a = bwd_pixel_pair(pp, j, dx, DSUB(fpy0, r0.y), DSUB(fpy1, r0.y), r0, r1, r2,
-                                      amax, v);
-#else
-        const bool a = bwd_pair_packed(P, j, dx, sub2(FPY, pk2(r0.y, r0.y)), r0, r1, r2, amax, v);
-#endif
+        const bool a = bwd_pair(P, j, DSUB(fpx, r0.x), sub2(FPY, pk2(r0.y, r0.y)), r0, r1, r2,
+                                amax, v);
         if (!__any_sync(0xffffffffu, a)) continue;
         // every lane writes its (possibly zero) partials as row nq*kV + c
 #pragma unroll
@@ -467,20 +384,25 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
                                     const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
-                                    cudaStream_t s, int tile0, int ntiles, int row_step) {
+                                    cudaStream_t s, int tile0, int ntiles) {
   const CamInfo ci = cam_info(cam);
   float *acc = static_cast<float *>(ws);
-  static bool attr_done = false;
   const size_t smem = sizeof(BwdSmem);
-  cudaError_t e = cudaSuccess;
-  if (!attr_done) {
+  // the opt-in shared-memory size: set once per device (a race between host
+  // threads only repeats the idempotent call)
+  static std::atomic<unsigned long long> attr_done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_done.load(std::memory_order_acquire) & bit)) {
     e = cudaFuncSetAttribute(k_render_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_render_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    attr_done.fetch_or(bit, std::memory_order_release);
   }
   const int T = ci.tiles_x * ci.tiles_y;
   if (ntiles < 0) ntiles = T - tile0;
@@ -492,13 +414,13 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
     la.n_valid = loss->n_valid; la.lambda_d = loss->lambda_d; la.gate = loss->gate;
     la.inv_n = 1.0f / (float)((int64_t)ci.W * ci.H);
     la.loss3 = loss->loss3;
-    k_render_bwd<true><<<ntiles * kCtaPerTile, kBwdThreads, smem, s>>>(
+    k_render_bwd<true><<<ntiles, kBwdThreads, smem, s>>>(
         static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, nullptr, nullptr, nullptr, acc, la, tile0, row_step);
+        t_final, n_contrib, nullptr, nullptr, nullptr, acc, la, tile0);
   } else {
-    k_render_bwd<false><<<ntiles * kCtaPerTile, kBwdThreads, smem, s>>>(
+    k_render_bwd<false><<<ntiles, kBwdThreads, smem, s>>>(
         static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, d_color, d_depth, d_sil, acc, la, tile0, row_step);
+        t_final, n_contrib, d_color, d_depth, d_sil, acc, la, tile0);
   }
   return cudaGetLastError();
 }
@@ -514,7 +436,7 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
   cudaError_t e = bwd_prep(g, flags, out, ws, loss, s);
   if (e != cudaSuccess) return e;
   e = launch_render_bwd_tiles(cam, loss, prm, pair_rec, tile_range, t_final, n_contrib, d_color,
-                              d_depth, d_sil, ws, s, 0, -1, 0);
+                              d_depth, d_sil, ws, s, 0, -1);
   if (e != cudaSuccess || g.n == 0) return e;
   return launch_chain(g, dec, cam, view, view_dev, prm, rec, static_cast<float *>(ws), flags,
                       out, s);

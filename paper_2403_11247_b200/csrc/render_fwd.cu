@@ -18,15 +18,8 @@
 namespace csplat {
 
 constexpr int kBatch = 32;   // records per TMA batch (2 KB)
-#ifndef CSPLAT_FWD_STAGES
-#define CSPLAT_FWD_STAGES 4
-#endif
-constexpr int kStages = CSPLAT_FWD_STAGES;  // ring depth
-#ifdef CSPLAT_FWD_SCALAR
-constexpr bool kFwdScalar = true;
-#else
-constexpr bool kFwdScalar = false;
-#endif
+constexpr int kStages = 4;   // ring depth (2: 85.7 us at C2; 3, 4, 6: 82.6-83.1 us)
+constexpr int kPW = 4;       // pixel warps: 8x8 pixels each, two per thread
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -40,58 +33,15 @@ struct PixState {
   int done;  // 0 = still compositing
 };
 
-// Composite one record into one pixel whose DA q test passed (Eq 3-5).
-__device__ __forceinline__ void composite(PixState &p, float q, float oh, float z,
-                                          const float4 &rgb, float amax, float tmin, int idx) {
-  const float alpha = fminf(amax, oh * ex2_approx(q * -0.72134752f));  // exp(-q/2)
-  const float test = p.T * (1.0f - alpha);
-  if (test < tmin) {  // R3: the triggering entry is not composited
-    p.done = 1;
-    return;
-  }
-  const float w = alpha * p.T;
-  p.r = fmaf(rgb.x, w, p.r);  // Eq 3
-  p.g = fmaf(rgb.y, w, p.g);
-  p.b = fmaf(rgb.z, w, p.b);
-  p.D = fmaf(z, w, p.D);      // Eq 4 (R8)
-  p.S += w;                   // Eq 5 (R9)
-  p.T = test;
-  p.last = idx;
-}
-
-// Predicated form of composite(): a pixel whose q test failed (h = false)
-// contributes w = 0 and keeps T, `last` and `done`.
-__device__ __forceinline__ void composite_pred(PixState &p, bool h, float q, float oh, float z,
-                                               const float4 &rgb, float amax, float tmin,
-                                               int idx) {
-  const float alpha = fminf(amax, oh * ex2_approx(q * -0.72134752f));  // exp(-q/2)
-  const float test = p.T * (1.0f - alpha);
-  const bool stop = test < tmin;          // R3: the triggering entry is not composited
-  const bool take = h & !stop;
-  const float w = take ? alpha * p.T : 0.0f;
-  p.r = fmaf(rgb.x, w, p.r);  // Eq 3
-  p.g = fmaf(rgb.y, w, p.g);
-  p.b = fmaf(rgb.z, w, p.b);
-  p.D = fmaf(z, w, p.D);      // Eq 4 (R8)
-  p.S += w;                   // Eq 5 (R9)
-  p.T = take ? test : p.T;
-  p.last = take ? idx : p.last;
-  p.done |= (h & stop) ? 1 : 0;
-}
-
-// composite_pred for the thread's two pixels on packed f32x2 instructions
-// (FMUL2/FFMA2/FADD2: each lane IEEE round-to-nearest, the same values as the
-// scalar form); the compositing is issue-bound, so one slot does both pixels.
-// FPY (CSPLAT_FWD_NANDONE): the pixels' row coordinates, NaN once a pixel has
-// terminated -- its DA q is then NaN and the range test fails, so the q test
-// needs no separate "done" check and termination is one select per pixel
-#ifndef CSPLAT_FWD_NANDONE
-#define CSPLAT_FWD_NANDONE 0  // measured slower: 84.9 vs 82.3 us at C2
-#endif
+// Composite one record into the thread's two pixels (Eq 3-5) on packed f32x2
+// instructions (FMUL2/FFMA2/FADD2: each lane IEEE round-to-nearest); the
+// compositing is issue-bound, so one slot does both pixels.  A pixel whose
+// DA q test failed (h = false) contributes w = 0 and keeps T, `last` and
+// `done`; R3: the entry that would take T below t_min is not composited.
 __device__ __forceinline__ void composite_pair(PixState &p0, PixState &p1, bool h0, bool h1,
                                                float q0, float q1, float oh, float z,
                                                const float4 &rgb, float amax, float tmin,
-                                               int idx, f2_t &FPY) {
+                                               int idx) {
   const f2_t QE = mul2(pk2(q0, q1), pk2(-0.72134752f, -0.72134752f));  // exp(-q/2)
   const f2_t AR = mul2(pk2(oh, oh), pk2(ex2_approx(lo2(QE)), ex2_approx(hi2(QE))));
   const f2_t AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));
@@ -112,19 +62,12 @@ __device__ __forceinline__ void composite_pair(PixState &p0, PixState &p1, bool 
   p1.T = take1 ? hi2(TEST) : p1.T;
   p0.last = take0 ? idx : p0.last;
   p1.last = take1 ? idx : p1.last;
-#if CSPLAT_FWD_NANDONE
-  const float nan = __int_as_float(0x7fc00000);
-  FPY = pk2((h0 & stop0) ? nan : lo2(FPY), (h1 & stop1) ? nan : hi2(FPY));
-#else
-  (void)FPY;
   p0.done |= (h0 & stop0) ? 1 : 0;
   p1.done |= (h1 & stop1) ? 1 : 0;
-#endif
 }
 
-// PPT = pixels per thread (a column of PPT vertically adjacent pixels): a pixel
-// warp owns an 8 x (4 PPT) block, 256/PPT pixel threads one 16x16 tile, plus
-// one producer warp.  The producer streams the tile's batches into the ring
+// Each thread owns a column of two vertically adjacent pixels: a pixel warp
+// owns an 8x8 block, four pixel warps one 16x16 tile, plus one producer warp.  The producer streams the tile's batches into the ring
 // (mbarrier full[] with complete_tx) and refills a slot once every pixel warp
 // has released it (empty[], one arrival per warp); the pixel warps never
 // synchronise with each other, so a warp with a heavy block does not hold the
@@ -132,19 +75,16 @@ __device__ __forceinline__ void composite_pair(PixState &p0, PixState &p1, bool 
 // in done_cnt and from then on only releases slots; once all have, the
 // producer ends the stream by completing the next full[] phase without data
 // (end_b), and every pixel warp leaves at that batch.
-template <int PPT>
-__global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
+__global__ void __launch_bounds__((kPW + 1) * 32) k_render_fwd(
     const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, float tmin, float *__restrict__ color, float *__restrict__ depth,
     float *__restrict__ sil, float *__restrict__ t_final, int32_t *__restrict__ n_contrib,
-    int tile0, int row_step) {
-  constexpr int kPW = 8 / PPT;  // pixel warps
+    int tile0) {
   __shared__ __align__(128) float4 buf[kStages][kBatch * 4];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ int done_cnt, end_b;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tile = row_step ? tile0 + (int)(blockIdx.x / tiles_x) * row_step + (int)(blockIdx.x % tiles_x)
-                           : tile0 + (int)blockIdx.x;
+  const int tile = tile0 + (int)blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
   const int len = (int)(end - start);
@@ -182,25 +122,19 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
   }
 
   // ---- pixel warps
-  constexpr int kBH = 4 * PPT;  // warp block height
-  const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * kBH;
-  const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * PPT;
-  // warp block corners as u16x2 for the SWAR rectangle test (PPT != 2)
-  const uint32_t wlo = (uint32_t)wx0 | ((uint32_t)wy0 << 16);
-  const uint32_t whi_x = ((uint32_t)(wx0 + 7) | ((uint32_t)(wy0 + kBH - 1) << 16)) | 0x80008000u;
-  PixState p[PPT];
+  const int wx0 = tx * kTile + (wid & 1) * 8, wy0 = ty * kTile + (wid >> 1) * 8;
+  const int px = wx0 + (lane & 7), py0 = wy0 + (lane >> 3) * 2;
+  PixState p[2];
   int mydone = 1;
 #pragma unroll
-  for (int k = 0; k < PPT; k++) {
+  for (int k = 0; k < 2; k++) {
     p[k] = PixState{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0, (px < W && py0 + k < H) ? 0 : 1};
     mydone &= p[k].done;
   }
   bool wdone = __all_sync(0xffffffffu, mydone);
   if (wdone && lane == 0) atomicAdd(&done_cnt, 1);
   const float fpx = (float)px;
-  f2_t FPY = pk2(p[0].done ? __int_as_float(0x7fc00000) : (float)py0,
-                 (PPT > 1 && p[PPT > 1 ? 1 : 0].done) ? __int_as_float(0x7fc00000)
-                                                      : (float)(py0 + 1));
+  const f2_t FPY = pk2((float)py0, (float)(py0 + 1));
   for (int b = 0; b < nb; b++) {
     const int s = b % kStages;
     mbar_wait_sleep(&full[s], (uint32_t)(b / kStages) & 1u);
@@ -209,18 +143,8 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
       const float4 *rb = buf[s];
       const int cnt = min(kBatch, len - b * kBatch);
       // the batch's entries this warp composites, one ballot: lane l tests entry
-      // l's 8x8-block mask (payload word 14, bin.cu; the rectangle for PPT != 2)
-      bool mine = false;
-      if (lane < cnt) {
-        const float4 r3 = rb[lane * 4 + 3];
-        if (PPT == 2) {
-          mine = (__float_as_uint(r3.z) >> wid) & 1u;
-        } else {
-          const uint32_t lo = __float_as_uint(r3.x), hi = __float_as_uint(r3.y);
-          const uint32_t t1 = (hi | 0x80008000u) - wlo, t2 = whi_x - lo;
-          mine = (t1 & t2 & 0x80008000u) == 0x80008000u;
-        }
-      }
+      // l's 8x8-block mask (payload word 14, bin.cu)
+      const bool mine = lane < cnt && ((__float_as_uint(rb[lane * 4 + 3].z) >> wid) & 1u);
       uint32_t todo = __ballot_sync(0xffffffffu, mine);
       while (todo) {  // front to back
         const int e = __ffs(todo) - 1;
@@ -229,66 +153,21 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
         const float4 r1 = rb[e * 4 + 1];  // cc, o_hat, k2, z
         const float dx = DSUB(fpx, r0.x);
         const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
-        float q[PPT];
-        bool h[PPT];
-        bool anyh = false;
-#ifndef CSPLAT_FWD_SCALAR
-        if constexpr (PPT == 2) {  // the DA q of both pixels on f32x2 (same roundings)
-#if CSPLAT_FWD_NANDONE
-          const f2_t DY = sub2(FPY, pk2(r0.y, r0.y));
-#else
-          const f2_t DY = sub2(pk2((float)py0, (float)(py0 + 1)), pk2(r0.y, r0.y));
-#endif
-          const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx),
-                              fma2(pk2(cbdx, cbdx), DY, mul2(mul2(pk2(r1.x, r1.x), DY), DY)));
-          q[0] = lo2(Q);
-          q[1] = hi2(Q);
-        }
-#endif
-#pragma unroll
-        for (int k = 0; k < PPT; k++) {
-#ifndef CSPLAT_FWD_SCALAR
-          if constexpr (PPT != 2)
-#endif
-          {
-            const float dy = DSUB((float)(py0 + k), r0.y);
-            q[k] = DFMA(cadx, dx, DFMA(cbdx, dy, DMUL(DMUL(r1.x, dy), dy)));
-          }
-          // R2 (DA): 0 <= q <= k2 (a terminated pixel's NaN q fails it, NANDONE)
-          if constexpr (PPT == 2 && CSPLAT_FWD_NANDONE && !kFwdScalar)
-            h[k] = da_in_range(q[k], r1.z);
-          else
-            h[k] = (p[k].done == 0) & da_in_range(q[k], r1.z);
-          anyh |= h[k];
-        }
-#ifdef CSPLAT_FWD_DIVERGENT
-        if (!anyh) continue;
-#else
-        // warp-uniform skip: composite_pair / composite_pred are exact no-ops for
-        // pixels whose test failed, so lanes without a hit ride along predicated
-        // (no divergence / reconvergence; the issue slots are the same)
-        if (!__any_sync(0xffffffffu, anyh)) continue;
-#endif
+        // the DA q of both pixels on f32x2 (same roundings as the scalar DA form)
+        const f2_t DY = sub2(FPY, pk2(r0.y, r0.y));
+        const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx),
+                            fma2(pk2(cbdx, cbdx), DY, mul2(mul2(pk2(r1.x, r1.x), DY), DY)));
+        const float q0 = lo2(Q), q1 = hi2(Q);
+        // R2 (DA): 0 <= q <= k2
+        const bool h0 = (p[0].done == 0) & da_in_range(q0, r1.z);
+        const bool h1 = (p[1].done == 0) & da_in_range(q1, r1.z);
+        // warp-uniform skip: composite_pair is an exact no-op for pixels whose
+        // test failed, so lanes without a hit ride along predicated
+        if (!__any_sync(0xffffffffu, h0 | h1)) continue;
         const float4 r2 = rb[e * 4 + 2];  // r, g, b, gid
-        const int idx = b * kBatch + e + 1;
-#ifndef CSPLAT_FWD_SCALAR
-        if constexpr (PPT == 2)
-          composite_pair(p[0], p[1], h[0], h[1], q[0], q[1], r1.y, r1.w, r2, amax, tmin, idx,
-                         FPY);
-        else
-#endif
-        // the pixels as straight-line (predicated) code so their chains interleave
-#pragma unroll
-        for (int k = 0; k < PPT; k++)
-          composite_pred(p[k], h[k], q[k], r1.y, r1.w, r2, amax, tmin, idx);
+        composite_pair(p[0], p[1], h0, h1, q0, q1, r1.y, r1.w, r2, amax, tmin, b * kBatch + e + 1);
       }
-      mydone = 1;
-      if constexpr (PPT == 2 && CSPLAT_FWD_NANDONE && !kFwdScalar) {
-        mydone = (lo2(FPY) != lo2(FPY)) & (hi2(FPY) != hi2(FPY));
-      } else {
-#pragma unroll
-        for (int k = 0; k < PPT; k++) mydone &= p[k].done;
-      }
+      mydone = p[0].done & p[1].done;
       wdone = __all_sync(0xffffffffu, mydone);
       if (wdone && lane == 0) atomicAdd(&done_cnt, 1);  // before the release below
     }
@@ -298,7 +177,7 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
   const int64_t HW = (int64_t)W * H;
   if (px < W) {
 #pragma unroll
-    for (int k = 0; k < PPT; k++) {
+    for (int k = 0; k < 2; k++) {
       if (py0 + k >= H) continue;
       const int64_t o = (int64_t)(py0 + k) * W + px;
       color[o] = p[k].r; color[HW + o] = p[k].g; color[2 * HW + o] = p[k].b;
@@ -307,22 +186,17 @@ __global__ void __launch_bounds__(256 / PPT + 32) k_render_fwd(
   }
 }
 
-#ifndef CSPLAT_FWD_PPT
-#define CSPLAT_FWD_PPT 2
-#endif
-
 cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
                               float *depth, float *sil, float *t_final, int32_t *n_contrib,
-                              cudaStream_t s, int tile0, int ntiles, int row_step) {
+                              cudaStream_t s, int tile0, int ntiles) {
   const CamInfo ci = cam_info(cam);
   const int T = ci.tiles_x * ci.tiles_y;
   if (ntiles < 0) ntiles = T - tile0;
   if (ntiles <= 0) return cudaSuccess;
-  constexpr int PPT = CSPLAT_FWD_PPT;
-  k_render_fwd<PPT><<<ntiles, 256 / PPT + 32, 0, s>>>(
+  k_render_fwd<<<ntiles, (kPW + 1) * 32, 0, s>>>(
       static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-      prm.t_min, color, depth, sil, t_final, n_contrib, tile0, row_step);
+      prm.t_min, color, depth, sil, t_final, n_contrib, tile0);
   return cudaGetLastError();
 }
 

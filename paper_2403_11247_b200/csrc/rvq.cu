@@ -17,9 +17,7 @@
 namespace csplat {
 
 constexpr int kRvqThreads = 256;
-#ifndef CSPLAT_RVQ_VP
-#define CSPLAT_RVQ_VP 2
-#endif
+constexpr int kRvqVP = 2;  // vector pairs per thread (D <= 4): each 16-byte code load feeds 2 FFMA2 chains
 
 // Merge partial argmins over the S-lane group: (d, k) lexicographic minimum.
 template <int S>
@@ -53,14 +51,10 @@ __device__ __forceinline__ void block_argmin4(float d0, float d1, float d2, floa
 // Each thread carries VP packed vector PAIRS (2 VP vectors), so every code
 // loaded from shared memory feeds VP FFMA2 chains (register blocking: the scan
 // is bound by shared-memory loads and their latency at VP = 1).
-#ifndef CSPLAT_RVQ_MINB
-#define CSPLAT_RVQ_MINB 3  // 3 CTAs (24 warps) per SM: 80 registers, a few spills (114.8 vs 121 us)
-#endif
-#ifndef CSPLAT_RVQ_MINB_S2
-#define CSPLAT_RVQ_MINB_S2 2  // S = 2 (C2-sized inputs): 128 registers, in-step 106.5 -> 104.4 us
-#endif
+constexpr int kRvqMinB = 3;    // 3 CTAs (24 warps) per SM: 80 registers, a few spills (114.8 vs 121 us)
+constexpr int kRvqMinBS2 = 2;  // S = 2 (C2-sized inputs): 128 registers, in-step 106.5 -> 104.4 us
 template <int D, int S, int VP>
-__global__ void __launch_bounds__(kRvqThreads, S == 2 ? CSPLAT_RVQ_MINB_S2 : CSPLAT_RVQ_MINB) k_rvq_chunked(
+__global__ void __launch_bounds__(kRvqThreads, S == 2 ? kRvqMinBS2 : kRvqMinB) k_rvq_chunked(
     const float *__restrict__ x, int64_t n, const int64_t *__restrict__ n_dev,
     const float *__restrict__ codes_g, int L, int P, void *__restrict__ idx, int idx_bytes,
     float *__restrict__ recon) {
@@ -164,19 +158,6 @@ __global__ void __launch_bounds__(kRvqThreads, S == 2 ? CSPLAT_RVQ_MINB_S2 : CSP
     // resolve the first code of the winning blocks that attains the minimum:
     // re-evaluate only vector u's pair in its block (bit-identical distances)
     int best[2 * VP];
-#ifdef CSPLAT_RVQ_RES_BOTH
-#pragma unroll
-    for (int u = 0; u < 2 * VP; u++) {
-      f2_t acc[VP][kBlk];
-      block_dist(blk[u], acc);
-      best[u] = kbase + blk[u];
-#pragma unroll
-      for (int c = kBlk - 1; c >= 0; c--) {
-        const float d = (u & 1) ? hi2(acc[u >> 1][c]) : lo2(acc[u >> 1][c]);
-        if (d == dmin[u]) best[u] = kbase + blk[u] + c;
-      }
-    }
-#else
 #pragma unroll
     for (int u = 0; u < 2 * VP; u++) {
       const int v = u >> 1;
@@ -200,7 +181,6 @@ __global__ void __launch_bounds__(kRvqThreads, S == 2 ? CSPLAT_RVQ_MINB_S2 : CSP
         if (d == dmin[u]) best[u] = kbase + blk[u] + c;
       }
     }
-#endif
 #pragma unroll
     for (int u = 0; u < 2 * VP; u++) {
       // the sequential scan keeps k = 0 when d_0 is NaN (no later d compares below it)
@@ -343,10 +323,7 @@ template <int D, int S>
 static bool try_chunked(const float *x, int64_t n, const int64_t *n_dev, const float *codes,
                         int L, int P, void *idx, int idx_bytes, float *recon, cudaStream_t s,
                         cudaError_t &err) {
-#ifndef CSPLAT_RVQ_VP3
-#define CSPLAT_RVQ_VP3 CSPLAT_RVQ_VP
-#endif
-  constexpr int VP = D == 3 ? CSPLAT_RVQ_VP3 : (D <= 4 ? CSPLAT_RVQ_VP : 1);  // vector pairs per thread
+  constexpr int VP = D <= 4 ? kRvqVP : 1;  // vector pairs per thread
   const size_t chunked_bytes = (size_t)L * S * ((P / S) * D + 4) * sizeof(float);
   if (!(P % (8 * S) == 0 && chunked_bytes <= 200 * 1024 &&
         (reinterpret_cast<uintptr_t>(codes) & 15u) == 0))
@@ -369,22 +346,15 @@ static bool try_chunked(const float *x, int64_t n, const int64_t *n_dev, const f
 // stage.  Measured (B200, 4 x 256, scale / rotation): at C2's 150k vectors S = 2
 // beats S = 4 (50.9 / 60.0 vs 56.4 / 65.9 us) and S = 1 (52.6 / 68.7); at C4's
 // 1M, with warps to spare, S = 1 wins (259 / 329 vs 280 / 343 us at S = 2).
-#ifndef CSPLAT_RVQ_S1_MIN_N
-#define CSPLAT_RVQ_S1_MIN_N 400000
-#endif
+constexpr int64_t kRvqS1MinN = 400000;
 template <int D>
 static cudaError_t run_rvq_d(const float *x, int64_t n, const int64_t *n_dev, const float *codes,
                              int L, int P, void *idx, int idx_bytes, float *recon,
                              cudaStream_t s) {
   cudaError_t e = cudaSuccess;
-#ifdef CSPLAT_RVQ_S  // tuning builds: one fixed group size
-  if (try_chunked<D, CSPLAT_RVQ_S>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s, e)) return e;
-#else
-  if (n >= CSPLAT_RVQ_S1_MIN_N &&
-      try_chunked<D, 1>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s, e))
+  if (n >= kRvqS1MinN && try_chunked<D, 1>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s, e))
     return e;
   if (try_chunked<D, 2>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s, e)) return e;
-#endif
   if (P >= 16) return run_rvq<D, 4>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s);
   return run_rvq<D, 1>(x, n, n_dev, codes, L, P, idx, idx_bytes, recon, s);
 }

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import os
 
+import numpy as np
 import torch
 
 from . import csplat as cs
@@ -60,8 +61,7 @@ class RenderStep:
         self.rec = torch.empty((n, 16), dtype=torch.int32, device=self.dev)
         self.count = torch.empty(n, dtype=torch.int32, device=self.dev)
         # a4/a5: size the pair buffers from a probe bin of this scene at the first view
-        tx, ty = cs.tiles(cam)
-        self.tile_range = torch.empty((tx * ty, 2), dtype=torch.int32, device=self.dev)
+        self.tile_range = cs.alloc_tile_range(cam, self.dev)
         self.n_pairs = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.capacity = pair_capacity or 1
         self._alloc_pairs(self.capacity)
@@ -88,14 +88,15 @@ class RenderStep:
                                   dtype=torch.uint8, device=self.dev)
 
     def size_pairs(self, view, margin=1.25, views=()):
-        """Run the front of the path once (synchronously) to size the pair buffers."""
+        """Size the pair buffers: run the front of the path once per given view
+        (synchronously, into a generous probe buffer) and keep the worst count
+        x margin -- shrinking the probe buffer again.  Returns the worst count."""
         worst = 0
         for v in [view, *views]:
             self.front(v, sync_probe=True)
             worst = max(worst, int(self.n_pairs.item()))
-        cap = int(worst * margin) + 4096
-        if cap > self.capacity:
-            self._alloc_pairs(cap)
+        self._alloc_pairs(int(worst * margin) + 4096)
+        cs.clear_status(self.tile_range)
         return worst
 
     def view_slot(self):
@@ -108,7 +109,7 @@ class RenderStep:
         n, dev = self.n, self.dev
         sl.rec = torch.empty_like(self.rec)
         sl.count = torch.empty_like(self.count)
-        sl.tile_range = torch.empty_like(self.tile_range)
+        sl.tile_range = torch.zeros_like(self.tile_range)
         sl.n_pairs = torch.zeros_like(self.n_pairs)
         sl._alloc_pairs(self.capacity)
         sl.img = {k: torch.empty_like(v) for k, v in self.img.items()}
@@ -219,11 +220,22 @@ class RenderStep:
             self.project_bin(view)
             self.forward()
 
-    def check_capacity(self):
-        n = int(self.n_pairs.item())
-        if n > self.capacity:
-            raise cs.CsplatError(f"{n} pairs exceed the capacity {self.capacity}")
-        return n
+    def check_capacity(self, slots=()):
+        """One host read of the status slots (csplat.h) of this view buffer and
+        of `slots` (e.g. the window's second view slot): raises if ANY call since
+        the last clear overflowed its pair capacity, returns the largest pair
+        count seen, and clears the slots."""
+        allsl = [self, *[s for s in slots if s is not self]]
+        st = torch.stack([cs.range_status(s.tile_range) for s in allsl]).cpu()
+        for s in allsl:
+            cs.clear_status(s.tile_range)
+        bits = int(np.bitwise_or.reduce(st[:, 0].numpy()))
+        worst = int(st[:, 1].numpy().view(np.uint32).max())
+        cap = min(s.capacity for s in allsl)
+        if bits & cs.STATUS_CAPACITY or worst > cap:
+            raise cs.CsplatError(f"{worst} pairs exceed the capacity {cap} "
+                                 f"(CSPLAT_STATUS_CAPACITY: those tiles were left empty)")
+        return worst
 
     # ---- CUDA graph ------------------------------------------------------
     def capture(self, view):

@@ -90,6 +90,11 @@ def gpu_window(step, views, rank=None, world=None, group=None, reduce=True,
 class PipelinedWindow(WindowStep):
     """WindowStep whose local renders are software-pipelined over two view slots."""
 
+    def check_capacity(self):
+        """Pair capacity over every keyframe rendered since the last check (both
+        view slots' status words; one host read): raises on any overflow."""
+        return self.slots[0].check_capacity(self.slots[1:])
+
     def __init__(self, step, views, rank=None, world=None, group=None, reduce=True):
         super().__init__(len(views), step.grads["flat"], None, step.prepare, rank, world, group,
                          reduce)

@@ -56,7 +56,7 @@ def test_library_is_sm100a(cs):
 
 def test_version_and_strings(cs):
     L = cs.lib()
-    assert L.csplat_version() >> 16 == 1
+    assert L.csplat_version() >> 16 == 2
     assert L.csplat_status_string(0) == b"ok"
     assert L.csplat_status_string(3) == b"pair capacity exceeded"
 

@@ -743,3 +743,32 @@ def test_keyframe_overlap_plane_non_identity_pose(orc):
     # pixels land exactly on the frustum boundary, where float32 rounding decides
     H, W = depth.shape
     assert (H - 2) * (W - 2) <= counts[-1] <= H * W
+
+
+def test_out_of_range_code_index_culls(orc):
+    """a Gaussian whose codebook index is >= P is culled -- its
+    record is all zero, count 0 -- and nothing else changes: the render equals
+    the render of the map without it (bit for bit)."""
+    sc = synth.tiny_scene(2)
+    cb = dict(sc.codebook)
+    si, _ = orc.rvq_assign(sc.log_scale, cb["scale_codes"])
+    ri, _ = orc.rvq_assign(sc.quat, cb["rot_codes"])
+    P = cb["scale_codes"].shape[1]
+    S = orc.Scene(**sc.planes())
+    rec0, cnt0 = orc.project(S, sc.cam, IDV, codebook=dict(cb, scale_idx=si, rot_idx=ri))
+    live = np.nonzero(cnt0 > 0)[0]
+    bad = [int(live[0]), int(live[1])]
+    si2, ri2 = si.copy(), ri.copy()
+    si2[1, bad[0]] = P           # a later stage out of range
+    ri2[0, bad[1]] = P + 7       # a rotation index out of range
+    rec, cnt = orc.project(S, sc.cam, IDV, codebook=dict(cb, scale_idx=si2, rot_idx=ri2))
+    assert (cnt[bad] == 0).all() and not rec[bad].any()
+    others = np.setdiff1d(np.arange(sc.n), bad)
+    assert np.array_equal(rec[others], rec0[others]) and np.array_equal(cnt[others], cnt0[others])
+    keep = np.ones(sc.n, bool); keep[bad] = False
+    S2 = orc.Scene(**{k: v[..., keep] for k, v in sc.planes().items()})
+    cb2 = dict(cb, scale_idx=si[:, keep], rot_idx=ri[:, keep])
+    a = render_all(orc, S, sc.cam, codebook=dict(cb, scale_idx=si2, rot_idx=ri2))[-1]
+    b = render_all(orc, S2, sc.cam, codebook=cb2)[-1]
+    for k in ("color", "depth", "sil", "t_final", "n_contrib"):
+        assert np.array_equal(a[k], b[k])
