@@ -34,6 +34,14 @@ import numpy as np  # noqa: E402
 
 METRIC = "fwd+bwd renders/sec at 1200x680 (Replica-shaped, 200k Gaussians)"
 UNIT = "renders/s"
+def c2_config(world: int) -> dict:
+    """The workload both arms report (the GPU step and the oracle reference)."""
+    return {"workload": "C2 replica 1200x680, 200k Gaussians (75% kept), R-VQ 4x256, "
+                        "step = prune+rvq+project+bin+fwd+bwd"
+                        + (" + grad all-reduce" if world > 1 else ""),
+            "l2": "512 MB flush write between timed steps",
+            "views": "rank r renders its own keyframe (rank 0 identity)",
+            "parallelism": f"dp{world} keyframe window"}
 KERNEL_LAUNCHES_PER_STEP = {
     # kernels of libcsplat launched by one RenderStep.step(): the projection
     # carries the bucket pass, and the per-tile sort, the forward and the
@@ -143,14 +151,30 @@ def stage_rooflines(stage_ms, counts, n_kept, n_pairs, e_bwd, peaks, step):
             out[name] = {"bound": "alu", "achieved": a, "peak": fp, "unit": "T FP32-lane-op/s",
                          "frac": a / fp, "work": work}
 
-    hb("mask_prune", 4 * n + 60 * n_kept + 60 * n_kept + 4 * n)
+    # SURVEY §8(d) "algorithmic work per unit" (what the method must move / issue);
+    # "impl_bytes" = what this implementation moves by design, for comparison
+    hb("mask_prune", n * (4 + 60 + 2 * L) + n_kept * (60 + 2 * L))
     if L:
         al("rvq_assign", n_kept * L * P * (2 * 3 + 2 * 4))  # sub + fma per dimension
-    hb("project", 4 * n + n_kept * (32 + 2 * L) + 68 * n)
-    hb("bin_tiles", 24 * n + 148 * n_pairs)
+    hb("project", n_kept * (40 + 60) if L else n_kept * 120)
+    if "project" in out:
+        out["project"]["impl_bytes"] = 4 * n + n_kept * (32 + 2 * L) + 68 * n
+    hb("bin_tiles", 12 * n_kept + (12 + 28) * n_pairs)   # a4 12 B/G + 12 B/pair; a5 28 B/pair
+    if "bin_tiles" in out:
+        b = 24 * n + 148 * n_pairs  # keys, cursors, pair_gid, 64-B payload gather + write
+        out["bin_tiles"]["impl_bytes"] = b
+        out["bin_tiles"]["impl_gbs"] = b / (stage_ms["bin_tiles"] * 1e-3) / 1e9
     if counts:
         al("render_fwd", 10.0 * counts["e_pix"] + 11.0 * counts["e_contrib"])
-        al("render_bwd", 10.0 * e_bwd + 35.0 * counts["e_contrib"])
+        al("render_bwd_kernel", 10.0 * e_bwd + 35.0 * counts["e_contrib"])
+    if "render_bwd" in stage_ms and "render_bwd_kernel" in stage_ms:
+        hb("chain", 160 * n_kept)  # a8: 160 B/G
+        ch = stage_ms["render_bwd"] - stage_ms["render_bwd_kernel"]
+        if ch > 0:
+            a = 160 * n_kept / (ch * 1e-3) / 1e9
+            out["chain"] = {"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s",
+                            "frac": a / hbm, "bytes": 160 * n_kept,
+                            "ms": ch, "note": "render_bwd - render_bwd_kernel"}
     return out
 
 
@@ -424,25 +448,29 @@ def bench_c5_window(dev, rank, world, iters=3):
     with torch.cuda.graph(graph):
         win.run()
 
-    def one():
+    def one(ev=None):
         graph.replay()
         if world > 1:
+            if ev is not None:
+                ev.record(stream)
             dist.all_reduce(st.grads["flat"])
 
     one()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ts = []
+    ts, ars = [], []
     for _ in range(iters):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a, b, m = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a.record(stream)
-        one()
+        one(m)
         b.record(stream)
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
+        ars.append(m.elapsed_time(b) if world > 1 else 0.0)
     win.check_capacity()  # every keyframe of every timed iteration, both view slots
     t = statistics.median(ts)
+    t_local = t - statistics.median(ars)
     # every rank must hold the identical reduced gradient (the replicas stay in step)
     chk = st.grads["flat"].double().sum().reshape(1)
     same = True
@@ -454,102 +482,276 @@ def bench_c5_window(dev, rank, world, iters=3):
         dist.all_reduce(lo, op=dist.ReduceOp.MIN)
         dist.all_reduce(hi, op=dist.ReduceOp.MAX)
         same = bool(torch.equal(lo, hi))
+        mine = torch.tensor([t_local, statistics.median(ars)], device=dev, dtype=torch.float64)
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per = [tuple(float(x) for x in a_.cpu()) for a_ in allr]
+    else:
+        per = [(t_local, 0.0)]
     return {"workload": "C5 window: 64 keyframes x 500k Gaussians, R-VQ 4x256, "
                         f"keyframes sharded over {world} GPU(s) + NCCL all-reduce",
             "n_gpus": world, "keyframes_per_rank": len(win.local), "ms_per_window_iter": t,
             "window_iters_per_s": 1e3 / t, "keyframe_renders_per_s": 64e3 / t,
-            "reduced_grad_checksum": float(chk.item()), "replicas_identical": same}
+            "reduced_grad_checksum": float(chk.item()), "replicas_identical": same,
+            "per_rank_local_ms": [round(p[0], 4) for p in per],
+            "per_rank_allreduce_ms": [round(p[1], 4) for p in per],
+            "allreduce_share": max(p[1] for p in per) / t,
+            "allreduce_bytes": st.grads["flat"].numel() * 4,
+            "note": "local part = the rank's keyframes as one CUDA graph; then one SUM "
+                    "all-reduce of the flat [15n+8] gradient buffer (time = max over ranks)"}
 
 
 # ---------------------------------------------------------------- oracle (CPU) legs
 
-def oracle_step(sc, view, upstream, row_frac=1.0, rvq_frac=1.0):
-    """The CPU oracle as it stands, over one (sampled) step of the same
-    workload: prune, R-VQ on a fraction of the survivors, project, bin, and
-    forward + backward on a band of pixel rows.  Returns (seconds, units,
-    counters); units = fraction of one render the sample covers."""
-    import oracle
-    oracle.build()
-    H = sc.cam["height"]
+def nccl_info(rank: int) -> dict | None:
+    """What NCCL chose on this rank (from its INIT/TUNING log): NVLS or not."""
+    p = os.path.join(ROOT, "gpurun_out", f"nccl_rank{rank}.log")
+    if not os.path.exists(p):
+        return None
+    txt = open(p, errors="replace").read()
+    lines = txt.splitlines()
+    pick = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines
+            if "NVLS" in ln or "NCCL version" in ln or "comm " in ln and "nRanks" in ln]
+    return {"log": os.path.relpath(p, ROOT), "nvls_mentioned": "NVLS" in txt,
+            "nvls_enabled": any("NVLS" in ln and ("enabled" in ln.lower() or "support" in
+                                                  ln.lower()) for ln in lines),
+            "lines": pick[:8]}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _planes_of(outs, k):
     names = ["mean", "opacity", "rgb", "log_scale", "quat", "mask"]
-    t0 = time.perf_counter()
-    planes = []
-    for k in names:
-        planes += list(getattr(sc, k).reshape(-1, sc.n))
-    outs, _, keep_map, k = oracle.mask_prune(planes, [], mask_plane=14)
     pl, off = {}, 0
     for name, c in zip(names, (3, 1, 3, 3, 4, 1)):
         pl[name] = np.stack(outs[off:off + c]).reshape((c, k) if c > 1 else (k,))
         off += c
-    m = max(1, int(k * rvq_frac))
-    si, _ = oracle.rvq_assign(pl["log_scale"][:, :m], sc.codebook["scale_codes"])
-    ri, _ = oracle.rvq_assign(pl["quat"][:, :m], sc.codebook["rot_codes"])
-    if m < k:   # the rest of the indices for the render (untimed-equivalent reuse)
-        si = np.concatenate([si, np.zeros((si.shape[0], k - m), np.uint16)], 1)
-        ri = np.concatenate([ri, np.zeros((ri.shape[0], k - m), np.uint16)], 1)
+    return pl
+
+
+def _flat_planes(sc):
+    planes = []
+    for k in ["mean", "opacity", "rgb", "log_scale", "quat", "mask"]:
+        planes += list(getattr(sc, k).reshape(-1, sc.n))
+    return planes
+
+
+def oracle_step(sc, view, upstream, row_frac=1.0):
+    """One step of the C2 workload through the CPU oracle as it stands: prune,
+    R-VQ (scale + rotation) of every survivor, project, bin, and forward +
+    backward (incl. the chain) over the first row_frac of the pixel rows.
+    Returns (seconds, render-equivalent seconds, counters): every component
+    is timed on its own and charged by the share of one render it covered
+    (prune / R-VQ / project / bin / chain: all of it; the per-pixel forward and
+    backward: row_frac), so a row-sampled step is not charged a full render's
+    prune, projection and binning for a fraction of the pixels."""
+    import oracle
+    oracle.build()
+    H = sc.cam["height"]
+    T = {}
+    t = time.perf_counter()
+    outs, _, _, k = oracle.mask_prune(_flat_planes(sc), [], mask_plane=14)
+    pl = _planes_of(outs, k)
+    T["prune"] = time.perf_counter() - t
+    t = time.perf_counter()
+    si, _ = oracle.rvq_assign(pl["log_scale"], sc.codebook["scale_codes"])
+    ri, _ = oracle.rvq_assign(pl["quat"], sc.codebook["rot_codes"])
+    T["rvq"] = time.perf_counter() - t
     cbo = dict(scale_codes=sc.codebook["scale_codes"], rot_codes=sc.codebook["rot_codes"],
                scale_idx=si, rot_idx=ri)
     S = oracle.Scene(**pl)
+    t = time.perf_counter()
     rec, cnt = oracle.project(S, sc.cam, view, codebook=cbo)
+    T["project"] = time.perf_counter() - t
+    t = time.perf_counter()
     gid, rng = oracle.bin_tiles(rec, cnt, sc.cam)
+    T["bin"] = time.perf_counter() - t
     rows = max(1, int(round(H * row_frac)))
+    frac = rows / H
     oracle.set_row_window(0, rows)
     try:
+        t = time.perf_counter()
         fo = oracle.render_fwd(rec, gid, rng, sc.cam)
+        T["fwd"] = time.perf_counter() - t
         dC, dD, dS = upstream
+        t = time.perf_counter()
         oracle.render_bwd(S, sc.cam, view, rec, gid, rng, dC, dD, dS, codebook=cbo)
+        T["bwd"] = time.perf_counter() - t
     finally:
         oracle.set_row_window(0, -1)
-    dt = time.perf_counter() - t0
-    units = min(rows / H, rvq_frac)
-    return dt, units, fo
+    total = sum(T.values())
+    equiv = total - T["fwd"] - T["bwd"] + (T["fwd"] + T["bwd"]) / frac
+    return total, equiv, dict(fo=fo, parts=T, row_frac=frac)
+
+
+def _oracle_render(orc, S, cam, view, up=None, cbo=None):
+    rec, cnt = orc.project(S, cam, view, codebook=cbo)
+    gid, rng = orc.bin_tiles(rec, cnt, cam)
+    fo = orc.render_fwd(rec, gid, rng, cam)
+    if up is not None:
+        orc.render_bwd(S, cam, view, rec, gid, rng, *up, codebook=cbo)
+    return fo
+
+
+def cpu_configs(threads):
+    """SURVEY §8(d) "Oracle timing beside it": the CPU oracle as it stands on
+    `threads` host threads, one bounded run per config (extrapolations
+    labelled).  Returns {config: {...}}."""
+    import oracle
+    from scenes import synth
+    oracle.build()
+    oracle.set_threads(threads)
+    out = {}
+    try:
+        # C1: the whole tiny step (R-VQ 2x16, prune, project, bin, fwd, bwd)
+        sc = synth.tiny_scene(0)
+        up = synth.upstream(np.random.default_rng(1), sc.cam["height"], sc.cam["width"])
+        t = time.perf_counter()
+        reps = 20
+        for _ in range(reps):
+            oracle_step(sc, sc.views[0], up)
+        dt = (time.perf_counter() - t) / reps
+        out["C1"] = {"ms_per_step": 1e3 * dt, "steps_per_s": 1 / dt, "sample": "20 whole steps"}
+        # C2: one whole step (row sampling only if it would take too long)
+        sc = synth.replica_scene(0)
+        up = synth.upstream(np.random.default_rng(1), sc.cam["height"], sc.cam["width"])
+        wall, equiv, info = oracle_step(sc, sc.views[0], up)
+        out["C2"] = {"ms_per_render": 1e3 * equiv, "renders_per_s": 1 / equiv,
+                     "parts_ms": {k: round(1e3 * v, 1) for k, v in info["parts"].items()},
+                     "sample": "1 whole step (prune, R-VQ 2x4x256 of all survivors, project, "
+                               "bin, fwd+bwd over all 1200x680 pixels)"}
+        # C3: one tracking iteration (project, bin, fwd, Eq 12+14 loss, bwd) x 40
+        sc = synth.tum_scene(0)
+        keep = sc.mask > oracle.mask_tau(0.01)
+        pl = {k: v[..., keep] for k, v in sc.planes().items()}
+        si, _ = oracle.rvq_assign(pl["log_scale"], sc.codebook["scale_codes"])
+        ri, _ = oracle.rvq_assign(pl["quat"], sc.codebook["rot_codes"])
+        cbo = dict(scale_codes=sc.codebook["scale_codes"], rot_codes=sc.codebook["rot_codes"],
+                   scale_idx=si, rot_idx=ri)
+        S = oracle.Scene(**pl)
+        obs = _oracle_render(oracle, S, sc.cam, sc.views[0], cbo=cbo)
+        start = synth.perturbed_view(np.random.default_rng(11), rot_deg=1.0, trans=0.02)
+        t = time.perf_counter()
+        rec, cnt = oracle.project(S, sc.cam, start, codebook=cbo)
+        gid, rng = oracle.bin_tiles(rec, cnt, sc.cam)
+        fo = oracle.render_fwd(rec, gid, rng, sc.cam)
+        up, _, _ = oracle.tracking_loss(fo["color"], fo["depth"], fo["sil"], obs["color"],
+                                        obs["depth"])
+        oracle.render_bwd(S, sc.cam, start, rec, gid, rng, *up, codebook=cbo)
+        dt = time.perf_counter() - t
+        out["C3"] = {"ms_per_iter": 1e3 * dt, "ms_per_frame_extrapolated": 40e3 * dt,
+                     "sample": "1 tracking iteration; per frame = x40 (extrapolation)"}
+        # C4: prune over all 1M + R-VQ 4x256 (scale, rotation) over 1/16 of them x 16
+        sc = synth.scannet_scene(0)
+        t = time.perf_counter()
+        oracle.mask_prune(_flat_planes(sc), [], mask_plane=14)
+        t_prune = time.perf_counter() - t
+        m = sc.n // 16
+        t = time.perf_counter()
+        oracle.rvq_assign(np.ascontiguousarray(sc.log_scale[:, :m]), sc.codebook["scale_codes"])
+        oracle.rvq_assign(np.ascontiguousarray(sc.quat[:, :m]), sc.codebook["rot_codes"])
+        t_rvq = (time.perf_counter() - t) * sc.n / m
+        out["C4"] = {"prune_ms": 1e3 * t_prune, "rvq_ms_extrapolated": 1e3 * t_rvq,
+                     "sample": f"prune of all {sc.n}; R-VQ of the first {m} (1/16), x16"}
+        # C5: one keyframe fwd+bwd of the 500k map; a window = 64/G keyframes
+        sc = synth.window_scene(0)
+        keep = sc.mask > oracle.mask_tau(0.01)
+        pl = {k: v[..., keep] for k, v in sc.planes().items()}
+        si, _ = oracle.rvq_assign(pl["log_scale"], sc.codebook["scale_codes"])
+        ri, _ = oracle.rvq_assign(pl["quat"], sc.codebook["rot_codes"])
+        cbo = dict(scale_codes=sc.codebook["scale_codes"], rot_codes=sc.codebook["rot_codes"],
+                   scale_idx=si, rot_idx=ri)
+        S = oracle.Scene(**pl)
+        up = synth.upstream(np.random.default_rng(5), sc.cam["height"], sc.cam["width"])
+        t = time.perf_counter()
+        _oracle_render(oracle, S, sc.cam, sc.views[0], up=up, cbo=cbo)
+        dt = time.perf_counter() - t
+        out["C5"] = {"ms_per_keyframe": 1e3 * dt,
+                     "ms_per_window_iter_extrapolated_G1": 64e3 * dt,
+                     "sample": "1 keyframe fwd+bwd (project, bin, fwd, bwd with chain); "
+                               "window = x64/G keyframes (extrapolation, no all-reduce)"}
+    finally:
+        oracle.set_threads(1)
+    return out
 
 
 def oracle_counts(sc, view):
     """E_pix / E_contrib of the exact scene, counted by the oracle (§8(d))."""
     import oracle
     oracle.build()
-    keep = sc.mask > oracle.mask_tau(0.01)
-    pl = {k: v[..., keep] for k, v in sc.planes().items()}
-    si, _ = oracle.rvq_assign(pl["log_scale"], sc.codebook["scale_codes"])
-    ri, _ = oracle.rvq_assign(pl["quat"], sc.codebook["rot_codes"])
-    cbo = dict(scale_codes=sc.codebook["scale_codes"], rot_codes=sc.codebook["rot_codes"],
-               scale_idx=si, rot_idx=ri)
-    rec, cnt = oracle.project(oracle.Scene(**pl), sc.cam, view, codebook=cbo)
-    gid, rng = oracle.bin_tiles(rec, cnt, sc.cam)
-    fo = oracle.render_fwd(rec, gid, rng, sc.cam)
+    oracle.set_threads(host_cores())
+    try:
+        keep = sc.mask > oracle.mask_tau(0.01)
+        pl = {k: v[..., keep] for k, v in sc.planes().items()}
+        si, _ = oracle.rvq_assign(pl["log_scale"], sc.codebook["scale_codes"])
+        ri, _ = oracle.rvq_assign(pl["quat"], sc.codebook["rot_codes"])
+        cbo = dict(scale_codes=sc.codebook["scale_codes"], rot_codes=sc.codebook["rot_codes"],
+                   scale_idx=si, rot_idx=ri)
+        rec, cnt = oracle.project(oracle.Scene(**pl), sc.cam, view, codebook=cbo)
+        gid, rng = oracle.bin_tiles(rec, cnt, sc.cam)
+        fo = oracle.render_fwd(rec, gid, rng, sc.cam)
+    finally:
+        oracle.set_threads(1)
     return dict(e_pix=fo["e_pix"], e_contrib=fo["e_contrib"], n_pairs=len(gid),
                 n_active=int((cnt > 0).sum()), n_kept=int(keep.sum()))
 
 
+def cpu_baseline_block():
+    """cpu_baseline of the GPU arm: the oracle on 1 thread and on all host cores."""
+    n = host_cores()
+    one = cpu_configs(1)
+    alln = cpu_configs(n) if n > 1 else one
+    return {"value": alln["C2"]["renders_per_s"], "unit": UNIT, "cores": n, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": alln["C2"]["sample"] + f", OpenMP {n} threads",
+            "single_thread": {"value": one["C2"]["renders_per_s"], "cores": 1},
+            "configs": {"threads_1": one, f"threads_{n}": alln}}
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the oracle, as it stands, on the host cores."""
+    """--impl reference: the oracle, as it stands, on all the host's cores, on
+    this arm's config / metric / unit.  A step is one C2 render; if whole steps
+    would not fit a few minutes, each step renders a band of pixel rows and is
+    charged per component (oracle_step)."""
+    import oracle
     from scenes import synth
     if rank != 0:
         return
+    n = host_cores()
+    oracle.build()
+    oracle.set_threads(n)
     sc = synth.replica_scene(args.seed)
     view = sc.views[0]
     H, W = sc.cam["height"], sc.cam["width"]
     up = synth.upstream(np.random.default_rng(args.seed + 1), H, W)
-    frac = 1.0 / 16
-    times, units = [], 0.0
+    wall0, eq0, _ = oracle_step(sc, view, up)
+    budget = 150.0
+    frac = 1.0
+    if (args.steps + args.warmup) * wall0 > budget:
+        frac = max(1.0 / 64, budget / ((args.steps + args.warmup) * wall0))
+    walls, eqs = [], []
     for i in range(args.warmup + args.steps):
-        dt, u, _ = oracle_step(sc, view, up, row_frac=frac, rvq_frac=frac)
+        w, e, _ = oracle_step(sc, view, up, row_frac=frac)
         if i >= args.warmup:
-            times.append(dt)
-            units += u
-    total = sum(times)
-    value = units / total
+            walls.append(w)
+            eqs.append(e)
+    oracle.set_threads(1)
+    value = len(eqs) / sum(eqs)
+    sample = ("whole C2 steps" if frac == 1.0 else
+              f"each step: prune, R-VQ, project, bin over the whole map and fwd+bwd over "
+              f"{frac:.3f} of the pixel rows, charged per component")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C2 replica 1200x680, 200k Gaussians (75% kept), R-VQ 4x256",
-                       "sample": f"{frac:.4f} of a render per step (first {frac:.4f} of pixel "
-                                 f"rows, R-VQ on {frac:.4f} of survivors; full prune/project/bin)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "cpu_model": cpu_model(),
-                             "sample": f"{frac:.4f} of one render per step"},
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.mean(walls), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": c2_config(world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": n, "kind": "oracle",
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -577,9 +779,18 @@ def main():
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = None
     if world > 1:
         backend = os.environ.get("CSPLAT_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator setup per rank (NVLS / channels / algorithms) into
+            # gpurun_out/nccl_rank<r>.log; INIT + TUNING only (no per-op logging)
+            if os.environ.get("CSPLAT_NCCL_LOG", "1") == "1":
+                os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING,NVLS")
+                os.environ.setdefault("NCCL_DEBUG_FILE",
+                                      os.path.join(ROOT, "gpurun_out", f"nccl_rank{rank}.log"))
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
@@ -606,6 +817,8 @@ def main():
             timed_events[0].record(stream)
         graph.replay()
         if world > 1:
+            if timed_events is not None:
+                timed_events[2].record(stream)
             dist.all_reduce(step.grads["flat"])
         if timed_events is not None:
             timed_events[1].record(stream)
@@ -623,7 +836,7 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
                for _ in range(args.steps)]
         for e in evs:
             flush.fill_(1.0)
@@ -633,7 +846,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
     step.check_capacity()
-    ms = [a.elapsed_time(b) for a, b in evs]
+    ms = [e[0].elapsed_time(e[1]) for e in evs]
+    ar_ms = [e[2].elapsed_time(e[1]) for e in evs] if world > 1 else [0.0] * len(evs)
     t_rank = sum(ms) / 1e3
     if world > 1:
         t = torch.tensor([t_rank], device=dev, dtype=torch.float64)
@@ -642,6 +856,23 @@ def main():
     else:
         t_max = t_rank
     value = world * args.steps / t_max
+    multi = None
+    if world > 1:
+        # per-rank step time and all-reduce time (device events), gathered to rank 0
+        mine = torch.tensor([t_rank * 1e3 / args.steps, statistics.median(ar_ms)],
+                            device=dev, dtype=torch.float64)
+        allr = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allr, mine)
+        per = [tuple(float(x) for x in a.cpu()) for a in allr]
+        flat_bytes = step.grads["flat"].numel() * step.grads["flat"].element_size()
+        multi = {"backend": backend, "world": world,
+                 "per_rank_step_ms": [round(p[0], 4) for p in per],
+                 "allreduce_ms_median_per_rank": [round(p[1], 4) for p in per],
+                 "allreduce_share": max(p[1] for p in per) / max(p[0] for p in per),
+                 "allreduce_bytes": flat_bytes,
+                 "allreduce_busbw_gbs": 2 * (world - 1) / world * flat_bytes /
+                 (max(p[1] for p in per) * 1e-3) / 1e9 if max(p[1] for p in per) > 0 else None,
+                 "nccl": nccl_info(rank) if backend == "nccl" else None}
 
     # ---- per-stage device times (same stream, non-graph launches, flushed L2)
     stage_ms = {}
@@ -661,6 +892,9 @@ def main():
                                                sync=False)),
             ("render_fwd", step.forward),
             ("render_bwd", lambda: step.backward(view)),
+            # the compositing backward alone (k_render_bwd, CSPLAT_SKIP_CHAIN): the
+            # dominant kernel the roofline line reports
+            ("render_bwd_kernel", lambda: step.backward(view, flags=cs.SKIP_CHAIN)),
         ]
         acc = {k: [] for k, _ in stages}
         for _ in range(max(5, min(args.steps, 30))):
@@ -674,6 +908,39 @@ def main():
             for i, (k, _) in enumerate(stages):
                 acc[k].append(ev[2 * i].elapsed_time(ev[2 * i + 1]))
         stage_ms = {k: statistics.mean(v) for k, v in acc.items()}
+
+    # ---- SURVEY §8(d) metric: one view's project -> bin -> fwd -> bwd (incl. the
+    # chain), no prune / R-VQ, captured as a CUDA graph: 20 warm-up + 200 timed
+    # replays, median with p10 / p90; warm L2 (no flush, as §8(d) states) and,
+    # separately, with the 512 MB flush before each replay
+    render_only = None
+    if rank == 0:
+        g_r = step.capture(view, render_only=True)
+        for _ in range(20):
+            g_r.replay()
+        torch.cuda.synchronize()
+
+        def replays(flush_each):
+            out = []
+            for _ in range(200):
+                if flush_each:
+                    flush.fill_(1.0)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                g_r.replay()
+                b.record(stream)
+                out.append((a, b))
+            torch.cuda.synchronize()
+            return sorted(x.elapsed_time(y) for x, y in out)
+
+        warm, cold = replays(False), replays(True)
+        q = lambda v, f: v[min(len(v) - 1, int(f * len(v)))]
+        render_only = {"renders_per_s": 1e3 / q(warm, 0.5), "ms_median": q(warm, 0.5),
+                       "ms_p10": q(warm, 0.1), "ms_p90": q(warm, 0.9),
+                       "cold_l2_ms_median": q(cold, 0.5),
+                       "cold_l2_renders_per_s": 1e3 / q(cold, 0.5),
+                       "note": "csplat_render_step (project+bucket, per-tile sort, fwd, bwd, "
+                               "chain) as one CUDA graph, 200 replays; warm L2 unless 'cold'"}
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -821,58 +1088,33 @@ def main():
         cpu = None
         if not args.no_cpu_baseline:
             counts = oracle_counts(sc, view)
-            ncores = 1
-            # whole steps of the same workload until >= 10 s of single-thread CPU work
-            tot, units, nst = 0.0, 0.0, 0
-            while tot < 10.0 and nst < 8:
-                dt, u, _ = oracle_step(sc, view, up, row_frac=1.0, rvq_frac=1.0)
-                tot += dt
-                units += u
-                nst += 1
-            cpu = {"value": units / tot, "unit": UNIT, "cores": ncores, "kind": "oracle",
-                   "cpu_model": cpu_model(),
-                   "sample": f"{nst} full step(s) of the C2 workload (prune, R-VQ 2x4x256 on "
-                             f"all survivors, project, bin, fwd+bwd over all 1200x680 pixels), "
-                             f"1 thread, {tot:.1f} s"}
-        # roofline of the dominant kernel stage
+            cpu = cpu_baseline_block()
+        # roofline of the dominant kernel (k_render_bwd: the largest share of the
+        # step's kernel time in the ncu launch list, profiles/)
         roof = None
-        if stage_ms:
-            dom = max(stage_ms, key=stage_ms.get)
+        if stage_ms and counts is not None and "render_bwd_kernel" in stage_ms:
             sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-            if dom in ("render_bwd", "render_fwd") and counts is not None:
-                if dom == "render_bwd":
-                    # §8(d): ~10 lane-instr per replayed entry + ~35 per contributing entry
-                    work = 10.0 * e_bwd + 35.0 * counts["e_contrib"]
-                else:
-                    # §8(d): ~10 per examined entry + ~11 per contributing entry
-                    work = 10.0 * counts["e_pix"] + 11.0 * counts["e_contrib"]
-                ach = work / (stage_ms[dom] * 1e-3) / 1e12
-                peak = fp32_peak_tinstr(sm_mhz)
-                roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak,
-                        "unit": "T FP32-lane-instr/s", "frac": ach / peak,
-                        "traffic": None,
-                        "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz "
-                                       f"(sm_max_mhz of {peak_src} MEASURED_PEAKS.json)"}
-            else:
-                rb = n_pairs * (8 + 4 + 64) * 2 + n_kept * 72
-                ach = rb / (stage_ms[dom] * 1e-3) / 1e9
-                roof = {"bound": "hbm", "kernel": dom, "achieved": ach,
-                        "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                        "frac": ach / peaks["hbm_gbs"], "traffic": None}
+            # §8(d): ~10 lane-instr per replayed entry (E_bwd = sum n_contrib)
+            # + ~35 per contributing entry (E_contrib, counted by the oracle)
+            work = 10.0 * e_bwd + 35.0 * counts["e_contrib"]
+            t_k = stage_ms["render_bwd_kernel"]
+            ach = work / (t_k * 1e-3) / 1e12
+            peak = fp32_peak_tinstr(sm_mhz)
+            roof = {"bound": "alu", "kernel": "k_render_bwd", "achieved": ach, "peak": peak,
+                    "unit": "T FP32-lane-instr/s", "frac": ach / peak, "traffic": None,
+                    "work_per_launch": work, "ms_per_launch": t_k,
+                    "peak_source": f"148 SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz "
+                                   f"(sm_max_mhz of {peak_src} MEASURED_PEAKS.json; "
+                                   f"DESIGN.md §8)"}
             tr = os.path.join(ROOT, "profiles", "traffic.json")
             if os.path.exists(tr):
-                roof["traffic"] = json.load(open(tr)).get(dom)
+                roof["traffic"] = json.load(open(tr)).get("render_bwd")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": "C2 replica 1200x680, 200k Gaussians (75% kept), R-VQ 4x256, "
-                                   "step = prune+rvq+project+bin+fwd+bwd"
-                                   + (" + NCCL grad all-reduce" if world > 1 else ""),
-                       "l2": "512 MB flush write between timed steps",
-                       "views": "rank r renders its own keyframe (rank 0 identity)",
-                       "parallelism": f"dp{world} keyframe window"},
+            "config": c2_config(world),
             "gpu_launches": sum(KERNEL_LAUNCHES_PER_STEP.values()) * args.steps,
             "stage_ms": stage_ms,
             "n_kept": n_kept, "n_pairs": n_pairs, "e_bwd": e_bwd,
@@ -906,6 +1148,10 @@ def main():
             line["cpu_baseline"] = cpu
         if e2e:
             line["e2e"] = e2e
+        if multi:
+            line["multi_gpu"] = multi
+        if render_only:
+            line["render_only_graph"] = render_only
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()           # the other ranks wait for rank 0's CPU-side legs

@@ -69,6 +69,11 @@ enum csplat_status {
 #define CSPLAT_SYNC 1u           /* bin_tiles: read n_pairs back, return CAPACITY if it exceeds the capacity */
 #define CSPLAT_POSE_ONLY 2u      /* render_bwd: only the pose gradient (tracking) */
 #define CSPLAT_ACCUMULATE 4u     /* render_bwd: add into the outputs instead of overwriting */
+#define CSPLAT_SKIP_CHAIN 8u     /* render_bwd: stop after the compositing backward (a7): the
+                                    per-Gaussian screen-space gradient is left in ws as
+                                    [n][12] float32 (raw moments Sx, Sy, Sxx, Sxy, Syy of
+                                    alpha dL/dalpha, dL/do_hat, dL/dz, dL/drgb, 2 pad;
+                                    DESIGN.md §7); `out` is not touched */
 
 /* Pinhole intrinsics K ("known camera intrinsic K"), image size
  * (1..32767 pixels per side), clip (R21). */
@@ -388,6 +393,35 @@ int csplat_tracking_loss(const float *color, const float *depth, const float *si
                          float *d_depth, float *d_silhouette, float *loss3_dev, void *ws,
                          size_t ws_bytes, void *stream);
 
+/* NEXT-2: the straight-through gradient of the R-VQ decode (Eq 10 first
+ * line: S_hat = sum_l C^l[i^l]; reading R31).  d_shat [d][n] (device) =
+ * dL/dS_hat, the decoded-geometry gradient csplat_render_bwd writes into
+ * grads.log_scale (d = 3) or grads.quat (d = 4).  d_codes [L][P][d] (device,
+ * 16-byte aligned for d = 4) gets, for every stage l and code k, the sum of
+ * dL/dS_hat_n over the vectors with idx[l][n] = k (S_hat is linear in every
+ * code: each stage's chosen code receives the full gradient); overwritten
+ * unless flags has CSPLAT_ACCUMULATE.  The STE gradient of the raw vector S
+ * itself is d_shat (no call needed).  Indices >= P are skipped.  Sums use
+ * float32 vector reductions (order-dependent rounding).  n_dev as in
+ * csplat_gaussians. */
+int csplat_rvq_code_grad(const float *d_shat, int64_t n, const int64_t *n_dev, int32_t d,
+                         const void *idx, int32_t idx_bytes, int32_t L, int32_t P,
+                         float *d_codes, uint32_t flags, void *stream);
+
+/* NEXT-2: Fig 4 codebook initialisation of one stage ("randomly select
+ * codebook initialization with the closest code"; reading R32).  codes
+ * [L][P][d] (device): stage `stage` is overwritten with C[k] = the stage
+ * residual x_s - S_hat_s^{stage-1} of the sampled vector s = sample[k]
+ * (device int64[P], each in [0, n); the random draw is the caller's), S_hat
+ * the decision-arithmetic stage-order sum of the codes of the earlier stages
+ * at idx [L][n] (from csplat_rvq_assign over those stages; unused for stage
+ * 0).  The closest-code assignment that follows is csplat_rvq_assign.  Calls
+ * for stages 0..L-1 in order, each followed by an assignment over stages
+ * 0..stage, initialise the whole codebook (paper_2403_11247_b200.rvq_init). */
+int csplat_rvq_init_stage(const float *x, int64_t n, int32_t d, float *codes, int32_t L,
+                          int32_t P, int32_t stage, const void *idx, int32_t idx_bytes,
+                          const int64_t *sample, void *stream);
+
 /* NEXT-2: R-VQ codebook update (Eq 11; reading R28): one k-means
  * M-step for the assignment idx [L][n] (from csplat_rvq_assign): with the
  * residual r_n^l = x_n - S_hat_n^{l-1} (the DA stage-order sums of
@@ -428,7 +462,10 @@ int csplat_keyframe_overlap(const float *depth, const csplat_camera *cam, const 
  * R30).  The N rays sampled from the keyframe database are N/64 random 8x8
  * pixel patches aligned to the 8-pixel grid; patches[b] = by * (W/8) + bx
  * names the block with origin (8 bx, 8 by) of one keyframe (device int32;
- * ids outside the image's whole blocks are ignored).
+ * ids outside the image's whole blocks are ignored).  Precondition: the ids of
+ * one keyframe are DISTINCT (a sample without replacement, as the reading
+ * states): a repeated id would count its rays twice in the loss and |R| but
+ * write its upstream gradient once.  Not checked on the device.
  *
  * csplat_ba_patches: for the patches of one keyframe, clears and sets its
  * active-tile mask (device uint32[ceil(T/32)], for csplat_bin_tiles_active)

@@ -34,7 +34,7 @@ def build(force: bool = False) -> str:
         if all(os.path.getmtime(s) <= so_t for s in srcs + hdrs):
             return _SO
     cmd = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-           "-Wall", "-o", _SO] + srcs + ["-lm"]
+           "-fopenmp", "-Wall", "-o", _SO] + srcs + ["-lm"]
     subprocess.check_call(cmd)
     return _SO
 
@@ -136,6 +136,11 @@ def view(v) -> View:
 
 def params(mask_eps=0.01, alpha_max=0.99, t_min=1e-4, dilation=0.3) -> Params:
     return Params(mask_eps, alpha_max, t_min, dilation)
+
+
+def set_threads(n: int = 1):
+    """OpenMP threads of the oracle's loops (timed CPU baseline only; default 1)."""
+    lib().oracle_set_threads(C.c_int32(n))
 
 
 def set_flag_window(t_rel: float = 1e-5, cap_abs: float = 1e-6):
@@ -377,6 +382,35 @@ def rvq_assign(x, codes):
                                  C.c_int32(P), _p(idx), _p(recon))
     assert rc == 0
     return idx, recon
+
+
+def rvq_code_grad(d_shat, idx, L, P, d_codes=None):
+    """NEXT-2 STE: dL/dC^l[k] = sum of dL/dS_hat_n over i_n^l = k -> [L, P, d] float64."""
+    g = np.ascontiguousarray(d_shat, dtype=np.float64)
+    d, n = g.shape
+    idx = np.ascontiguousarray(idx, dtype=np.uint16)
+    acc = d_codes is not None
+    out = np.ascontiguousarray(d_codes, dtype=np.float64) if acc else np.zeros((L, P, d))
+    rc = lib().oracle_rvq_code_grad(_p(g), C.c_int64(n), C.c_int32(d), _p(idx), C.c_int32(L),
+                                    C.c_int32(P), _p(out), C.c_int32(1 if acc else 0))
+    assert rc == 0
+    return out
+
+
+def rvq_init_stage(x, codes, l, idx, sample):
+    """NEXT-2 Fig 4: stage l of codes [L, P, d] := the stage-l residuals of x[:, sample]."""
+    x = _f32(x)
+    d, n = x.shape
+    codes = np.array(codes, dtype=np.float32, copy=True)
+    L, P = codes.shape[:2]
+    idx = np.ascontiguousarray(idx, dtype=np.uint16) if idx is not None else \
+        np.zeros((L, n), np.uint16)
+    sample = np.ascontiguousarray(sample, dtype=np.int64)
+    assert sample.shape == (P,)
+    rc = lib().oracle_rvq_init_stage(_p(x), C.c_int64(n), C.c_int32(d), _p(codes), C.c_int32(L),
+                                     C.c_int32(P), C.c_int32(l), _p(idx), _p(sample))
+    assert rc == 0
+    return codes
 
 
 def rvq_update(x, codes, idx):

@@ -117,6 +117,24 @@ int oracle_rvq_update(const float *x, int64_t n, int32_t d, const float *codes, 
                       int32_t P, const uint16_t *idx, float *codes_out, int32_t *counts,
                       double *loss_out);
 
+/* NEXT-2: straight-through gradient of the R-VQ decode (Eq 10 first line,
+ * P:164, S_hat = sum_l C^l[i^l]; reading R31).  d_shat [d][n] = dL/dS_hat
+ * (the renderer's decoded-geometry gradient); d_codes [L][P][d] (float64) =
+ * sum over n with i_n^l = k of d_shat_n, for every stage l; with accumulate
+ * = 0 it is overwritten.  (The STE gradient of the raw vector S is d_shat
+ * itself.) */
+int oracle_rvq_code_grad(const double *d_shat, int64_t n, int32_t d, const uint16_t *idx,
+                         int32_t L, int32_t P, double *d_codes, int32_t accumulate);
+
+/* NEXT-2: Fig 4 codebook initialisation of stage l ("randomly select
+ * codebook initialization"; reading R32): C^l[k] = the stage-l residual
+ * S_s - S_hat_s^{l-1} of the sampled vector s = sample[k] (k < P), with
+ * S_hat^{l-1} the stage-order float32 sum of the codes of stages < l at the
+ * indices idx[0..l-1][s] (from oracle_rvq_assign with l stages).  codes is
+ * [L][P][d]; only stage l is written. */
+int oracle_rvq_init_stage(const float *x, int64_t n, int32_t d, float *codes, int32_t L,
+                          int32_t P, int32_t l, const uint16_t *idx, const int64_t *sample);
+
 /* Mask prune: order-preserving compaction of survivors of
  * m > tau.  in_planes: n_planes float planes [n] each; idx planes u16 [n].
  * reset_mask: if not NaN, the mask plane (plane index mask_plane) of
@@ -153,6 +171,11 @@ int oracle_ba_patch_loss(const double *color, const double *depth, const float *
 /* Restrict oracle_render_fwd/bwd to pixel rows [row_lo, row_hi) (row_hi < 0:
  * all rows) -- used only to time a bounded CPU-baseline sample. */
 void oracle_set_row_window(int32_t row_lo, int32_t row_hi);
+/* OpenMP threads of the per-Gaussian, per-vector and per-pixel loops (default
+ * 1).  Used ONLY by bench.py's timed CPU baseline (1 thread and
+ * all cores).  Results do not depend on it except for the summation order of
+ * the backward's per-thread partial sums (float64, reduced in thread order). */
+void oracle_set_threads(int32_t n);
 /* Flagging window of oracle_render_fwd; defaults 1e-5, 1e-6. */
 void oracle_set_flag_window(double t_rel, double cap_abs);
 

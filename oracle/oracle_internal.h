@@ -10,6 +10,9 @@
 static inline float or_u2f(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
 static inline uint32_t or_f2u(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
 
+/* OpenMP thread count of the timed baseline (oracle_set_threads; 1 = serial). */
+int or_threads(void);
+
 /* DA transcendentals. */
 float or_sigm(float x);
 

@@ -109,6 +109,7 @@ int oracle_project(const or_gaussians *g, const or_codebook *cb, const or_camera
     const float ly_hi = ((Hf - cy) + 0.15f * Hf) / fy;
     const float dil = prm->dilation;
 
+#pragma omp parallel for num_threads(or_threads()) schedule(static)
     for (int64_t i = 0; i < n; i++) {
         uint32_t *r = rec + i * OR_REC_WORDS;
         put_rec_zero(r);

@@ -19,10 +19,16 @@
  */
 #include "oracle_internal.h"
 #include <stdlib.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 /* Optional pixel-row window for the tiled forward/backward: the timed CPU
  * baseline renders a bounded sample of rows (bench.py); default = all rows. */
 static int g_row_lo = 0, g_row_hi = -1;
+static int g_threads = 1;
+void oracle_set_threads(int32_t n) { g_threads = n < 1 ? 1 : n; }
+int or_threads(void) { return g_threads; }
 void oracle_set_row_window(int32_t row_lo, int32_t row_hi) { g_row_lo = row_lo; g_row_hi = row_hi; }
 static int or_row_lo(int H) { return g_row_lo < 0 ? 0 : (g_row_lo > H ? H : g_row_lo); }
 static int or_row_hi(int H) { return (g_row_hi < 0 || g_row_hi > H) ? H : g_row_hi; }
@@ -172,6 +178,7 @@ int oracle_render_fwd(const uint32_t *rec, const uint32_t *pair_gid, const uint3
     const int tiles_x = (W + OR_TILE - 1) / OR_TILE;
     const int64_t HW = (int64_t)W * H;
     int64_t e_pix = 0, e_con = 0;
+#pragma omp parallel for num_threads(g_threads) schedule(dynamic, 1) reduction(+ : e_pix, e_con)
     for (int py = or_row_lo(H); py < or_row_hi(H); py++)
         for (int px = 0; px < W; px++) {
             int64_t t = (int64_t)(py / OR_TILE) * tiles_x + px / OR_TILE;
@@ -282,48 +289,78 @@ int oracle_render_bwd(const or_gaussians *g, const or_codebook *cb, const or_cam
     const int W = cam->width, H = cam->height;
     const int tiles_x = (W + OR_TILE - 1) / OR_TILE;
     const int64_t HW = (int64_t)W * H;
-    double *acc2d = (double *)calloc((size_t)(n ? n : 1) * 10, sizeof(double));
     int64_t maxlen = 0;
     const int64_t T_tiles = (int64_t)tiles_x * ((H + OR_TILE - 1) / OR_TILE);
     for (int64_t t = 0; t < T_tiles; t++) {
         int64_t l = (int64_t)tile_range[2 * t + 1] - tile_range[2 * t];
         if (l > maxlen) maxlen = l;
     }
-    or_entry *ent = (or_entry *)malloc((size_t)(maxlen ? maxlen : 1) * sizeof(or_entry));
-    for (int py = or_row_lo(H); py < or_row_hi(H); py++)
-        for (int px = 0; px < W; px++) {
-            int64_t p = (int64_t)py * W + px;
-            if (pixel_weight_zero && pixel_weight_zero[p]) continue;
-            int64_t t = (int64_t)(py / OR_TILE) * tiles_x + px / OR_TILE;
-            uint32_t s = tile_range[2 * t], e = tile_range[2 * t + 1];
-            double out6[6];
-            int64_t ex;
-            int flag;
-            int32_t lp1;
-            int ne = composite(rec, pair_gid + s, (int64_t)e - s, px, py, prm, out6, &ex, &flag,
-                               &lp1, ent);
-            double gC[3] = {d_color[p], d_color[HW + p], d_color[2 * HW + p]};
-            accumulate_pixel(ent, ne, gC, d_depth[p], d_sil[p], acc2d);
-        }
-    free(ent);
+    /* per-thread 2D accumulators (one with 1 thread), summed in thread order */
+    const int nth = g_threads;
+    double *accs = (double *)calloc((size_t)nth * (size_t)(n ? n : 1) * 10, sizeof(double));
+#pragma omp parallel num_threads(nth)
+    {
+#ifdef _OPENMP
+        const int tid = omp_get_thread_num();
+#else
+        const int tid = 0;
+#endif
+        double *acc_t = accs + (size_t)tid * (size_t)(n ? n : 1) * 10;
+        or_entry *ent = (or_entry *)malloc((size_t)(maxlen ? maxlen : 1) * sizeof(or_entry));
+#pragma omp for schedule(dynamic, 1)
+        for (int py = or_row_lo(H); py < or_row_hi(H); py++)
+            for (int px = 0; px < W; px++) {
+                int64_t p = (int64_t)py * W + px;
+                if (pixel_weight_zero && pixel_weight_zero[p]) continue;
+                int64_t t = (int64_t)(py / OR_TILE) * tiles_x + px / OR_TILE;
+                uint32_t s = tile_range[2 * t], e = tile_range[2 * t + 1];
+                double out6[6];
+                int64_t ex;
+                int flag;
+                int32_t lp1;
+                int ne = composite(rec, pair_gid + s, (int64_t)e - s, px, py, prm, out6, &ex,
+                                   &flag, &lp1, ent);
+                double gC[3] = {d_color[p], d_color[HW + p], d_color[2 * HW + p]};
+                accumulate_pixel(ent, ne, gC, d_depth[p], d_sil[p], acc_t);
+            }
+        free(ent);
+    }
+    double *acc2d = accs;
+    for (int th = 1; th < nth; th++) {
+        const double *a = accs + (size_t)th * (size_t)(n ? n : 1) * 10;
+        for (int64_t k = 0; k < n * 10; k++) acc2d[k] += a[k];
+    }
     double Wd[3][3], td[3];
     view_to_d(view, Wd, td);
     for (int k = 0; k < 6; k++) pose[k] = 0.0;
-    for (int64_t i = 0; i < n; i++) {
-        double g15[15] = {0};
-        const uint32_t *r = rec + i * OR_REC_WORDS;
-        int alive = r[5] != 0u;                                  /* o_hat word is 0 iff culled */
-        if (alive) {
-            or_proj64 pj;
-            or_project64(g, cb, cam, Wd, td, prm, i, OR_MODE_CLAMP, &pj);
-            or_chain(&pj, acc2d + i * 10, g15, pose);
-            double sm = sigd((double)g->mask[i]);
-            g15[14] *= sm * (1.0 - sm);                          /* Eq 6 STE */
+    double *pose_t = (double *)calloc((size_t)nth * 6, sizeof(double));
+#pragma omp parallel num_threads(nth)
+    {
+#ifdef _OPENMP
+        const int tid = omp_get_thread_num();
+#else
+        const int tid = 0;
+#endif
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < n; i++) {
+            double g15[15] = {0};
+            const uint32_t *r = rec + i * OR_REC_WORDS;
+            int alive = r[5] != 0u;                              /* o_hat word is 0 iff culled */
+            if (alive) {
+                or_proj64 pj;
+                or_project64(g, cb, cam, Wd, td, prm, i, OR_MODE_CLAMP, &pj);
+                or_chain(&pj, acc2d + i * 10, g15, pose_t + 6 * tid);
+                double sm = sigd((double)g->mask[i]);
+                g15[14] *= sm * (1.0 - sm);                      /* Eq 6 STE */
+            }
+            for (int k = 0; k < 15; k++) grads[k * n + i] = g15[k];
         }
-        for (int k = 0; k < 15; k++) grads[k * n + i] = g15[k];
     }
+    for (int th = 0; th < nth; th++)
+        for (int k = 0; k < 6; k++) pose[k] += pose_t[6 * th + k];
+    free(pose_t);
     if (acc2d_out) memcpy(acc2d_out, acc2d, (size_t)n * 10 * sizeof(double));
-    free(acc2d);
+    free(accs);
     return 0;
 }
 

@@ -16,6 +16,7 @@ int oracle_rvq_assign(const float *x, int64_t n, int32_t d, const float *codes, 
                       int32_t P, uint16_t *idx, float *recon)
 {
     if (n < 0 || d < 1 || d > 8 || L < 1 || P < 1 || P > 65536) return 1;
+#pragma omp parallel for num_threads(or_threads()) schedule(static)
     for (int64_t i = 0; i < n; i++) {
         float xi[8], sh[8];
         for (int j = 0; j < d; j++) { xi[j] = x[(int64_t)j * n + i]; sh[j] = 0.0f; }
@@ -85,6 +86,48 @@ int oracle_rvq_update(const float *x, int64_t n, int32_t d, const float *codes, 
     for (int l = 0; l < L; l++) tot += loss_out[l];
     loss_out[L] = n > 0 ? tot / ((double)n * P) : 0.0;
     free(sum);
+    return 0;
+}
+
+/* NEXT-2 STE (reading R31): Eq 10 decodes S_hat = sum_l C^l[i^l]; the
+ * straight-through estimator passes dL/dS_hat to the raw vector unchanged,
+ * and since S_hat is linear in every code, dL/dC^l[k] = sum of dL/dS_hat_n
+ * over the vectors with i_n^l = k (each stage's chosen code receives the full
+ * gradient). */
+int oracle_rvq_code_grad(const double *d_shat, int64_t n, int32_t d, const uint16_t *idx,
+                         int32_t L, int32_t P, double *d_codes, int32_t accumulate)
+{
+    if (n < 0 || d < 1 || d > 8 || L < 1 || P < 1) return 1;
+    if (!accumulate)
+        for (int64_t k = 0; k < (int64_t)L * P * d; k++) d_codes[k] = 0.0;
+    for (int64_t i = 0; i < n; i++)
+        for (int l = 0; l < L; l++) {
+            const int k = idx[(int64_t)l * n + i];
+            if (k >= P) continue;                         /* culled */
+            for (int j = 0; j < d; j++)
+                d_codes[((int64_t)l * P + k) * d + j] += d_shat[(int64_t)j * n + i];
+        }
+    return 0;
+}
+
+/* NEXT-2 Fig 4 (reading R32): stage l's codebook starts as the stage-l
+ * residuals of P randomly sampled vectors (the sample is an input). */
+int oracle_rvq_init_stage(const float *x, int64_t n, int32_t d, float *codes, int32_t L,
+                          int32_t P, int32_t l, const uint16_t *idx, const int64_t *sample)
+{
+    if (n < 1 || d < 1 || d > 8 || L < 1 || P < 1 || l < 0 || l >= L) return 1;
+    for (int k = 0; k < P; k++) {
+        const int64_t s = sample[k];
+        if (s < 0 || s >= n) return 1;
+        float sh[8];
+        for (int j = 0; j < d; j++) sh[j] = 0.0f;
+        for (int m = 0; m < l; m++) {                     /* S_hat^{l-1}, stage order */
+            const float *c = codes + ((int64_t)m * P + idx[(int64_t)m * n + s]) * d;
+            for (int j = 0; j < d; j++) sh[j] = (m == 0) ? c[j] : sh[j] + c[j];
+        }
+        for (int j = 0; j < d; j++)
+            codes[((int64_t)l * P + k) * d + j] = x[(int64_t)j * n + s] - sh[j];
+    }
     return 0;
 }
 

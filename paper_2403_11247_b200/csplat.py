@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("CSPLAT_LIB", os.path.join(_PKG, "libcsplat.so"))
 
 TILE = 16
 RECORD_BYTES = 64
-SYNC, POSE_ONLY, ACCUMULATE = 1, 2, 4
+SYNC, POSE_ONLY, ACCUMULATE, SKIP_CHAIN = 1, 2, 4, 8
 STATUS_CAPACITY, STATUS_CODE_INDEX = 1, 2  # device status bits (csplat.h)
 OP_BIN_TILES, OP_RENDER_BWD, OP_MASK_PRUNE = 1, 2, 3
 
@@ -117,6 +117,8 @@ def lib():
         L.csplat_render_fwd.argtypes = [vp] * 10
         L.csplat_render_bwd.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_rvq_assign.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp]
+        L.csplat_rvq_code_grad.argtypes = [vp, i64, vp, i32, vp, i32, i32, i32, vp, u32, vp]
+        L.csplat_rvq_init_stage.argtypes = [vp, i64, i32, vp, i32, i32, i32, vp, i32, vp, vp]
         L.csplat_mask_prune.argtypes = [vp, vp, C.c_float, C.c_float, vp, vp, vp, vp, vp, vp,
                                         C.c_size_t, vp]
         L.csplat_tracking_loss.argtypes = [vp] * 5 + [i32, i32, C.c_float, C.c_float] + \
@@ -642,6 +644,45 @@ def rvq_assign(x, codes, idx_bytes=None, n_dev=None, idx=None, recon=None, want_
     _check(lib().csplat_rvq_assign(_ptr(x), n, _ptr(n_dev), d, _ptr(codes), L, P, _ptr(idx),
                                    idx_bytes, _ptr(recon), _stream(stream)), "csplat_rvq_assign")
     return idx, recon
+
+
+def rvq_code_grad(d_shat, idx, P: int, n_dev=None, d_codes=None, accumulate=False, stream=None):
+    """NEXT-2 STE (reading R31): d_shat [d, n] = dL/dS_hat -> dL/dcodes [L, P, d]."""
+    d, n = d_shat.shape
+    L = idx.shape[0]
+    if d_codes is None:
+        d_codes = torch.empty((L, P, d), device=d_shat.device)
+    _check(lib().csplat_rvq_code_grad(_ptr(d_shat), n, _ptr(n_dev), d, _ptr(idx),
+                                      idx.element_size(), L, P, _ptr(d_codes),
+                                      ACCUMULATE if accumulate else 0, _stream(stream)),
+           "csplat_rvq_code_grad")
+    return d_codes
+
+
+def rvq_init_stage(x, codes, stage: int, idx, sample, stream=None):
+    """NEXT-2 Fig 4 (reading R32): codes[stage] := the stage residuals of x[:, sample]."""
+    d, n = x.shape
+    L, P = codes.shape[:2]
+    ib = idx.element_size() if idx is not None else 1
+    _check(lib().csplat_rvq_init_stage(_ptr(x), n, d, _ptr(codes), L, P, stage, _ptr(idx), ib,
+                                       _ptr(sample), _stream(stream)), "csplat_rvq_init_stage")
+    return codes
+
+
+def rvq_init(x, L: int, P: int, rng, stream=None):
+    """Fig 4: initialise an L-stage, P-code residual codebook on x [d, n]:
+    per stage, P vectors drawn without replacement (host rng: the caller's random
+    draw) seed the codes with their stage residuals, then the closest-code
+    assignment (Eq 10) gives the next stage's residuals.  Returns (codes, idx)."""
+    d, n = x.shape
+    dev = x.device
+    codes = torch.zeros((L, P, d), device=dev)
+    idx = torch.zeros((L, n), dtype=torch.uint8 if P <= 256 else torch.int16, device=dev)
+    for l in range(L):
+        sample = torch.tensor(rng.choice(n, P, replace=False), dtype=torch.int64, device=dev)
+        rvq_init_stage(x, codes, l, idx, sample, stream=stream)
+        rvq_assign(x, codes[:l + 1], idx=idx[:l + 1], want_recon=False, stream=stream)
+    return codes, idx
 
 
 def mask_loss(g: GaussianMap, count, d_mask, lam=1.0, loss=None, ws=None, stream=None):

@@ -715,6 +715,42 @@ int csplat_rvq_update(const float *x, int64_t n, const int64_t *n_dev, int32_t d
                      "csplat_rvq_update");
 }
 
+int csplat_rvq_code_grad(const float *d_shat, int64_t n, const int64_t *n_dev, int32_t d,
+                         const void *idx, int32_t idx_bytes, int32_t L, int32_t P,
+                         float *d_codes, uint32_t flags, void *stream) {
+  if (n < 0) return invalid("n < 0");
+  if (d < 1 || d > 8) return invalid("d must be 1..8");
+  if (L < 1 || L > 16) return invalid("L must be 1..16");
+  if (P < 1 || P > 65536) return invalid("P must be 1..65536");
+  if (idx_bytes != 1 && idx_bytes != 2) return invalid("idx_bytes must be 1 or 2");
+  if (!d_codes || (n > 0 && (!d_shat || !idx))) return invalid("rvq_code_grad: NULL argument");
+  if (d == 4 && (reinterpret_cast<uintptr_t>(d_codes) & 15u)) {
+    set_err("rvq_code_grad: d_codes must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_rvq_code_grad(d_shat, n, n_dev, d, L, P, idx, idx_bytes,
+                                                  d_codes, (flags & CSPLAT_ACCUMULATE) != 0,
+                                                  static_cast<cudaStream_t>(stream)),
+                     "csplat_rvq_code_grad");
+}
+
+int csplat_rvq_init_stage(const float *x, int64_t n, int32_t d, float *codes, int32_t L,
+                          int32_t P, int32_t stage, const void *idx, int32_t idx_bytes,
+                          const int64_t *sample, void *stream) {
+  if (n < 1) return invalid("n must be >= 1");
+  if (d < 1 || d > 8) return invalid("d must be 1..8");
+  if (L < 1 || L > 16) return invalid("L must be 1..16");
+  if (P < 1 || P > 65536) return invalid("P must be 1..65536");
+  if (stage < 0 || stage >= L) return invalid("stage must be 0..L-1");
+  if (idx_bytes != 1 && idx_bytes != 2) return invalid("idx_bytes must be 1 or 2");
+  if (!x || !codes || !sample || (stage > 0 && !idx)) return invalid("rvq_init_stage: NULL argument");
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_rvq_init_stage(x, n, d, codes, P, stage, idx, idx_bytes, sample,
+                                                   static_cast<cudaStream_t>(stream)),
+                     "csplat_rvq_init_stage");
+}
+
 int csplat_rvq_assign(const float *x, int64_t n, const int64_t *n_dev, int32_t d,
                       const float *codes, int32_t L, int32_t P, void *idx_out, int32_t idx_bytes,
                       float *recon_out, void *stream) {

@@ -314,6 +314,13 @@ cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
                                int64_t *n_pairs_dev, void *ws, cudaStream_t s);
 
 size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam);
+// NEXT-2 (rvq_update.cu): the STE code gradient and the Fig 4 stage init
+cudaError_t launch_rvq_code_grad(const float *g, int64_t n, const int64_t *n_dev, int d, int L,
+                                 int P, const void *idx, int idx_bytes, float *dcodes,
+                                 bool accumulate, cudaStream_t s);
+cudaError_t launch_rvq_init_stage(const float *x, int64_t n, int d, float *codes, int P, int l,
+                                  const void *idx, int idx_bytes, const int64_t *sample,
+                                  cudaStream_t s);
 // the calling thread's fork streams / events of the composed calls (project.cu)
 void release_thread_fork_resources();
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,

@@ -368,7 +368,7 @@ cudaError_t bwd_prep(const csplat_gaussians &g, uint32_t flags, const csplat_gra
                      void *ws, const TrackingLoss *loss, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(ws, 0, bwd_workspace_bytes(g.n), s);
   if (e != cudaSuccess) return e;
-  if (out.pose && !(flags & CSPLAT_ACCUMULATE)) {
+  if (out.pose && !(flags & (CSPLAT_ACCUMULATE | CSPLAT_SKIP_CHAIN))) {
     e = cudaMemsetAsync(out.pose, 0, 6 * sizeof(float), s);
     if (e != cudaSuccess) return e;
   }
@@ -437,7 +437,7 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
   if (e != cudaSuccess) return e;
   e = launch_render_bwd_tiles(cam, loss, prm, pair_rec, tile_range, t_final, n_contrib, d_color,
                               d_depth, d_sil, ws, s, 0, -1);
-  if (e != cudaSuccess || g.n == 0) return e;
+  if (e != cudaSuccess || g.n == 0 || (flags & CSPLAT_SKIP_CHAIN)) return e;
   return launch_chain(g, dec, cam, view, view_dev, prm, rec, static_cast<float *>(ws), flags,
                       out, s);
 }

@@ -9,6 +9,8 @@
 // counts and per-stage errors in shared memory (privatised, so the global
 // atomics are one per (CTA, code component)), then a tiny finalise kernel
 // divides.  HBM-bound: (4 d + 2 L) bytes per vector.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace csplat {
@@ -153,6 +155,110 @@ cudaError_t launch_rvq_update(const float *x, int64_t n, const int64_t *n_dev, i
     case 6: return run_update<6>(x, n, n_dev, codes, L, P, idx, idx_bytes, codes_out, counts_out, loss_out, ws, s);
     case 7: return run_update<7>(x, n, n_dev, codes, L, P, idx, idx_bytes, codes_out, counts_out, loss_out, ws, s);
     case 8: return run_update<8>(x, n, n_dev, codes, L, P, idx, idx_bytes, codes_out, counts_out, loss_out, ws, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ---- NEXT-2 STE (reading R31): dL/dC^l[k] += sum over i_n^l = k of dL/dS_hat_n.
+// One thread per vector: its d-vector gradient goes to every stage's chosen
+// code with global vector reductions (red.global.add.v4 / .v2 / scalar), the
+// L2 doing the per-code sums (C2: 150k vectors x 4 stages into 4 x 256 codes).
+// HBM-bound: 4 d + L idx_bytes bytes per vector.
+template <int D>
+__global__ void __launch_bounds__(kRuThreads) k_rvq_code_grad(
+    const float *__restrict__ g, int64_t n, const int64_t *__restrict__ n_dev, int L, int P,
+    const void *__restrict__ idx, int idx_bytes, float *__restrict__ dcodes) {
+  const int64_t ne = eff_n(n, n_dev);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v[D];
+    bool nz = false;
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+      v[j] = g[(int64_t)j * n + i];
+      nz |= v[j] != 0.0f;
+    }
+    if (!nz) continue;  // exact zeros add nothing (Gaussians no pixel reached)
+    for (int l = 0; l < L; l++) {
+      const uint32_t k = ru_idx(idx, idx_bytes, (int64_t)l * n + i);
+      if (k >= (uint32_t)P) continue;  // culled Gaussian
+      float *dst = dcodes + ((int64_t)l * P + k) * D;
+      if constexpr (D == 4) {
+        red_add_v4(dst, v[0], v[1], v[2], v[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < D; j++) atomicAdd(dst + j, v[j]);
+      }
+    }
+  }
+}
+
+// ---- NEXT-2 Fig 4 initialisation of stage l (reading R32): C^l[k] = the
+// stage-l residual of the sampled vector s_k, with the same DA stage-order sum
+// S_hat^{l-1} as csplat_rvq_assign.  One thread per code.
+template <int D>
+__global__ void k_rvq_init_stage(const float *__restrict__ x, int64_t n, float *__restrict__ codes,
+                                 int P, int l, const void *__restrict__ idx, int idx_bytes,
+                                 const int64_t *__restrict__ sample) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P) return;
+  const int64_t s = sample[k];
+  float sh[D];
+#pragma unroll
+  for (int j = 0; j < D; j++) sh[j] = 0.0f;
+  for (int m = 0; m < l; m++) {
+    const uint32_t c = min(ru_idx(idx, idx_bytes, (int64_t)m * n + s), (uint32_t)(P - 1));
+    const float *cp = codes + ((int64_t)m * P + c) * D;
+#pragma unroll
+    for (int j = 0; j < D; j++) sh[j] = m == 0 ? cp[j] : DADD(sh[j], cp[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < D; j++) codes[((int64_t)l * P + k) * D + j] = DSUB(x[(int64_t)j * n + s], sh[j]);
+}
+
+template <int D>
+static cudaError_t run_code_grad(const float *g, int64_t n, const int64_t *n_dev, int L, int P,
+                                 const void *idx, int idx_bytes, float *dcodes, bool accumulate,
+                                 cudaStream_t s) {
+  if (!accumulate) {
+    cudaError_t e = cudaMemsetAsync(dcodes, 0, (size_t)L * P * D * sizeof(float), s);
+    if (e != cudaSuccess) return e;
+  }
+  if (n == 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + kRuThreads - 1) / kRuThreads, 148 * 8);
+  k_rvq_code_grad<D><<<(unsigned)blocks, kRuThreads, 0, s>>>(g, n, n_dev, L, P, idx, idx_bytes,
+                                                             dcodes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rvq_code_grad(const float *g, int64_t n, const int64_t *n_dev, int d, int L,
+                                 int P, const void *idx, int idx_bytes, float *dcodes,
+                                 bool accumulate, cudaStream_t s) {
+  switch (d) {
+    case 1: return run_code_grad<1>(g, n, n_dev, L, P, idx, idx_bytes, dcodes, accumulate, s);
+    case 2: return run_code_grad<2>(g, n, n_dev, L, P, idx, idx_bytes, dcodes, accumulate, s);
+    case 3: return run_code_grad<3>(g, n, n_dev, L, P, idx, idx_bytes, dcodes, accumulate, s);
+    case 4: return run_code_grad<4>(g, n, n_dev, L, P, idx, idx_bytes, dcodes, accumulate, s);
+    case 5: return run_code_grad<5>(g, n, n_dev, L, P, idx, idx_bytes, dcodes, accumulate, s);
+    case 6: return run_code_grad<6>(g, n, n_dev, L, P, idx, idx_bytes, dcodes, accumulate, s);
+    case 7: return run_code_grad<7>(g, n, n_dev, L, P, idx, idx_bytes, dcodes, accumulate, s);
+    case 8: return run_code_grad<8>(g, n, n_dev, L, P, idx, idx_bytes, dcodes, accumulate, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_rvq_init_stage(const float *x, int64_t n, int d, float *codes, int P, int l,
+                                  const void *idx, int idx_bytes, const int64_t *sample,
+                                  cudaStream_t s) {
+  const unsigned blocks = (unsigned)((P + 127) / 128);
+  switch (d) {
+#define CSPLAT_INIT_CASE(D)                                                                   \
+  case D:                                                                                     \
+    k_rvq_init_stage<D><<<blocks, 128, 0, s>>>(x, n, codes, P, l, idx, idx_bytes, sample);  \
+    return cudaGetLastError();
+    CSPLAT_INIT_CASE(1) CSPLAT_INIT_CASE(2) CSPLAT_INIT_CASE(3) CSPLAT_INIT_CASE(4)
+    CSPLAT_INIT_CASE(5) CSPLAT_INIT_CASE(6) CSPLAT_INIT_CASE(7) CSPLAT_INIT_CASE(8)
+#undef CSPLAT_INIT_CASE
     default: return cudaErrorInvalidValue;
   }
 }

@@ -195,6 +195,10 @@ class RenderStep:
 
     def step(self, view):
         self.prepare()
+        self.render_view(view)
+
+    def render_view(self, view):
+        """a3 .. a8 of one view of the prepared map (no prune / R-VQ)."""
         if FUSED_BIN and not (self.flags & cs.POSE_ONLY) and not _on_device(view):
             # a3 .. a8 in one library call (per tile chunk: sort -> fwd -> bwd)
             dC, dD, dS = self.upstream
@@ -238,15 +242,21 @@ class RenderStep:
         return worst
 
     # ---- CUDA graph ------------------------------------------------------
-    def capture(self, view):
+    def capture(self, view, render_only=False):
+        """One step (or, render_only, one view's project -> bin -> fwd -> bwd
+        incl. the chain, no prune / R-VQ) captured as a CUDA graph."""
+        fn = self.render_view if render_only else self.step
         s = torch.cuda.Stream(device=self.dev)
         s.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(s):
-            self.step(view)          # warm (and any lazy attribute setup) outside capture
+            if render_only:
+                self.prepare()
+            fn(view)                 # warm (and any lazy attribute setup) outside capture
         torch.cuda.current_stream(self.dev).wait_stream(s)
         torch.cuda.synchronize(self.dev)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.step(view)
-        self.graph = g
+            fn(view)
+        if not render_only:
+            self.graph = g
         return g

@@ -894,3 +894,83 @@ def test_c5_window_keyframe_parity(env, kf):
     R-VQ 4x256: full fwd + bwd parity of one keyframe render."""
     sc = synth.window_scene(0)
     run_and_compare(env, sc, view=sc.views[kf])
+
+
+# ------------------------------------------------------------------ NEXT-2 STE + Fig 4 init
+
+@pytest.mark.parametrize("d,LP", [(3, (4, 256)), (4, (4, 256)), (4, (2, 16)), (3, (3, 1000))])
+def test_rvq_code_grad_parity(env, d, LP):
+    """STE code gradient (reading R31) vs the oracle's scatter-add: rel-L2
+    <= 1e-5 (float32 vector reductions, order-dependent), out-of-range indices
+    skipped, ACCUMULATE adds, empty codes get exact zeros."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    L, P = LP
+    r = np.random.default_rng(d + P)
+    n = 150_000
+    g = np.float32(r.standard_normal((d, n)))
+    idx = r.integers(0, P, (L, n)).astype(np.uint16)
+    if P + 3 < 256 or P > 256:
+        idx[0, :7] = P + 3                              # culled: skipped on both sides
+    ref = orc.rvq_code_grad(g.astype(np.float64), idx, L, P)
+    it = torch.tensor(idx.astype(np.int16 if P > 256 else np.uint8), device=dev)
+    out = cs.rvq_code_grad(torch.tensor(g, device=dev), it, P)
+    a = out.double().cpu().numpy()
+    assert np.linalg.norm(a - ref) / np.linalg.norm(ref) <= 1e-5
+    empty = np.ones((L, P), bool)
+    for l in range(L):
+        empty[l, idx[l][idx[l] < P]] = False
+    assert not a[empty].any()
+    out2 = cs.rvq_code_grad(torch.tensor(g, device=dev), it, P, d_codes=out.clone(),
+                            accumulate=True)
+    assert np.allclose(out2.double().cpu().numpy(), 2 * a, rtol=1e-6, atol=1e-3)
+
+
+def test_rvq_code_grad_from_render_bwd(env):
+    """The STE chain end to end: render_bwd's decoded-geometry gradient (C1,
+    R-VQ 2x16) routed to the codes matches the oracle's render_bwd + scatter."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.tiny_scene(0)
+    res = run_and_compare(env, sc)
+    cb, cbo = _codebooks(env, sc)
+    H, W = sc.cam["height"], sc.cam["width"]
+    S = orc.Scene(**sc.planes())
+    rec_o, cnt_o = orc.project(S, sc.cam, sc.views[0], codebook=cbo)
+    gid_o, rng_o = orc.bin_tiles(rec_o, cnt_o, sc.cam)
+    r = np.random.default_rng(1)
+    dC, dD, dS = synth.upstream(r, H, W)
+    go = orc.render_bwd(S, sc.cam, sc.views[0], rec_o, gid_o, rng_o, dC, dD, dS, codebook=cbo)
+    P = sc.codebook["scale_codes"].shape[1]
+    L = sc.codebook["scale_codes"].shape[0]
+    for name, key in (("log_scale", "scale_idx"), ("quat", "rot_idx")):
+        ref = orc.rvq_code_grad(go[name], cbo[key], L, P)
+        gpu = cs.rvq_code_grad(torch.tensor(np.float32(go[name]), device=dev),
+                               cb.scale_idx if key == "scale_idx" else cb.rot_idx, P)
+        a = gpu.double().cpu().numpy()
+        assert np.linalg.norm(a - ref) / max(np.linalg.norm(ref), 1e-30) <= 1e-5, name
+    assert res["grad_err"]["log_scale"] <= GRAD_TOL
+
+
+@pytest.mark.parametrize("d", [3, 4])
+def test_rvq_init_parity(env, d):
+    """Fig 4 init (reading R32), stage by stage with the closest-code
+    assignment in between: codes and indices bit-exact vs the oracle on the
+    same random draws."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.replica_scene(0)
+    x = sc.log_scale if d == 3 else sc.quat
+    L, P = 4, 256
+    n = x.shape[1]
+    draws = [np.random.default_rng(100 + l).choice(n, P, replace=False) for l in range(L)]
+    codes_o = np.zeros((L, P, d), np.float32)
+    idx_o = np.zeros((L, n), np.uint16)
+    xt = torch.tensor(x, device=dev)
+    codes = torch.zeros((L, P, d), device=dev)
+    idx = torch.zeros((L, n), dtype=torch.uint8, device=dev)
+    for l in range(L):
+        codes_o = orc.rvq_init_stage(x, codes_o, l, idx_o, draws[l])
+        io, _ = orc.rvq_assign(x, codes_o[:l + 1])
+        idx_o[:l + 1] = io
+        cs.rvq_init_stage(xt, codes, l, idx, torch.tensor(draws[l], device=dev))
+        cs.rvq_assign(xt, codes[:l + 1], idx=idx[:l + 1], want_recon=False)
+        assert np.array_equal(codes.cpu().numpy(), codes_o), l
+        assert np.array_equal(idx.cpu().numpy().astype(np.uint16), idx_o), l

@@ -772,3 +772,100 @@ def test_out_of_range_code_index_culls(orc):
     b = render_all(orc, S2, sc.cam, codebook=cb2)[-1]
     for k in ("color", "depth", "sil", "t_final", "n_contrib"):
         assert np.array_equal(a[k], b[k])
+
+
+def test_threads_do_not_change_results(orc):
+    """The OpenMP build of the timed baseline: the forward, the
+    projection and R-VQ are bit-identical at any thread count; the backward's
+    per-thread float64 partials change only the summation order."""
+    sc = synth.mid_scene(1)
+    S = orc.Scene(**sc.planes())
+    H, W = sc.cam["height"], sc.cam["width"]
+    r = np.random.default_rng(3)
+    up = r.standard_normal((3, H, W)), r.standard_normal((H, W)), r.standard_normal((H, W))
+    res = []
+    try:
+        for th in (1, 4):
+            orc.set_threads(th)
+            rec, cnt, gid, rng_, out = render_all(orc, S, sc.cam)
+            gr = orc.render_bwd(S, sc.cam, sc.views[0], rec, gid, rng_, *up)
+            idx, rc = orc.rvq_assign(sc.log_scale, sc.codebook["scale_codes"])
+            res.append((rec, out, gr, idx, rc))
+    finally:
+        orc.set_threads(1)
+    (r1, o1, g1, i1, c1), (r4, o4, g4, i4, c4) = res
+    assert np.array_equal(r1, r4) and np.array_equal(i1, i4) and np.array_equal(c1, c4)
+    for k in ("color", "depth", "sil", "t_final", "n_contrib", "flags"):
+        assert np.array_equal(o1[k], o4[k])
+    for k in g1:
+        assert np.allclose(g1[k], g4[k], rtol=1e-12, atol=1e-14), k
+
+
+# ---------------------------------------------------------------- NEXT-2 (R-VQ training side)
+
+def test_rvq_code_grad_closed_form_and_fd(orc):
+    """STE (reading R31): S_hat = sum_l C^l[i^l] is linear in every code, so
+    dL/dC^l[k] = sum of dL/dS_hat over the vectors whose stage-l index is k.
+    Pinned by a hand example and by float64 central differences of
+    L(C) = sum_n <w_n, S_hat_n(C)> with numpy's own decode."""
+    # hand example: 3 vectors, L = 2, P = 2, d = 2
+    idx = np.array([[0, 1, 0], [1, 1, 0]], np.uint16)
+    g = np.array([[1.0, 2.0, 4.0], [10.0, 20.0, 40.0]])
+    out = orc.rvq_code_grad(g, idx, 2, 2)
+    assert np.array_equal(out[0], [[5.0, 50.0], [2.0, 20.0]])   # stage 0: {0,2} -> 0, {1} -> 1
+    assert np.array_equal(out[1], [[4.0, 40.0], [3.0, 30.0]])   # stage 1: {2} -> 0, {0,1} -> 1
+    # accumulate adds onto the given buffer
+    out2 = orc.rvq_code_grad(g, idx, 2, 2, d_codes=out.copy())
+    assert np.array_equal(out2, 2 * out)
+    # FD on a random problem
+    r = np.random.default_rng(4)
+    L, P, d, n = 3, 8, 4, 200
+    codes = r.standard_normal((L, P, d))
+    idx = r.integers(0, P, (L, n)).astype(np.uint16)
+    w = r.standard_normal((d, n))
+
+    def loss(c):
+        shat = sum(c[l][idx[l]] for l in range(L))       # [n, d]
+        return float((shat.T * w).sum())
+    an = orc.rvq_code_grad(w, idx, L, P)
+    h = 1e-3
+    fd = np.zeros_like(codes)
+    for l in range(L):
+        for k in range(P):
+            for j in range(d):
+                cp, cm = codes.copy(), codes.copy()
+                cp[l, k, j] += h
+                cm[l, k, j] -= h
+                fd[l, k, j] = (loss(cp) - loss(cm)) / (2 * h)
+    assert np.allclose(an, fd, rtol=1e-9, atol=1e-9)
+
+
+def test_rvq_init_stage_fig4(orc):
+    """Fig 4 (reading R32): stage 0's codes are the sampled vectors
+    themselves; stage l's codes are the sampled vectors' stage-l residuals, so
+    after the closest-code assignment every sampled vector sits at distance
+    exactly 0 from its stage-l code (checked in numpy float32 from the
+    oracle's codes and indices)."""
+    r = np.random.default_rng(9)
+    d, n, L, P = 4, 3000, 3, 32
+    x = np.float32(r.standard_normal((d, n)) * [[1.0], [0.5], [0.25], [2.0]])
+    codes = np.zeros((L, P, d), np.float32)
+    idx = None
+    samples = []
+    for l in range(L):
+        s = r.choice(n, P, replace=False)
+        samples.append(s)
+        codes = orc.rvq_init_stage(x, codes, l, idx, s)
+        if l == 0:
+            assert np.array_equal(codes[0], x[:, s].T)
+        idx, _ = orc.rvq_assign(x, codes[:l + 1])
+        idx = np.concatenate([idx, np.zeros((L - l - 1, n), np.uint16)])
+    for l in range(L):
+        s = samples[l]
+        sh = np.zeros((d, P), np.float32)
+        for m in range(l):
+            sh = codes[m][idx[m, s]].T if m == 0 else np.float32(sh + codes[m][idx[m, s]].T)
+        res = np.float32(x[:, s] - sh)                       # stage-l residuals (float32)
+        assert np.array_equal(codes[l].T, res)             # the init copies them bit for bit
+        c = codes[l][idx[l, s]].T
+        assert not np.any(c - res), l                      # distance exactly 0

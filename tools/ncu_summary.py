@@ -80,6 +80,50 @@ def launches(path):
     return agg
 
 
+def counters(path):
+    """counters_<tag>.csv (ncu --metrics ... --csv): {kernel: {metric: (value, unit)}},
+    the first launch of each kernel."""
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hi]
+    ki, ni, vi, ui = (hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"),
+                      hdr.index("Metric Unit"))
+    idi = hdr.index("ID")
+    out = collections.OrderedDict()
+    first = {}
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        k = r[ki].split("(")[0].replace("void ", "").replace("csplat::", "")
+        first.setdefault(k, r[idi])
+        if r[idi] != first[k]:
+            continue
+        out.setdefault(k, {})[r[ni]] = (r[vi], r[ui])
+    return out
+
+
+COUNTER_ROWS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("lts__t_bytes.sum", "L2 (LTS) bytes"),
+    ("lts__t_requests_op_red.sum", "L2 RED requests"),
+    ("lts__t_sectors_op_red.sum", "L2 RED sectors"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+     "smem utilisation %"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem bank conflicts (ld)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "smem bank conflicts (st)"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("smsp__thread_inst_executed.sum", "thread (lane) instructions"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+]
+
+
 def main():
     tag = sys.argv[1]
     src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
@@ -89,7 +133,7 @@ def main():
              "Cold-cache, serialised per-launch times of one C2 step (tools/prof_step.py);",
              "compare SHARES with bench.py's stage times, not absolutes.", "",
              "| kernel | launches | mean us | share |", "|---|---|---|---|"]
-    for lf in sorted(glob.glob(os.path.join(src, "launches*.csv"))):
+    for lf in sorted(glob.glob(os.path.join(src, f"launches_{tag}.csv"))):
         agg = launches(lf)
         tot = sum(sum(v) for v in agg.values())
         for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
@@ -131,6 +175,18 @@ def main():
             traffic[stage] = rd + wr
         except (KeyError, ValueError):
             pass
+    for cf in sorted(glob.glob(os.path.join(src, f"counters_{tag}.csv"))):
+        cs_ = counters(cf)
+        kl.append(f"## SURVEY §8(d) counters (ncu --metrics, one launch per kernel; "
+                  f"{os.path.basename(cf)})\n")
+        names = list(cs_)
+        kl.append("| metric | " + " | ".join(names) + " |")
+        kl.append("|---|" + "---|" * len(names))
+        for key, label in COUNTER_ROWS:
+            vals = [cs_[k].get(key, ("-", ""))[0] + " " + cs_[k].get(key, ("", ""))[1]
+                    for k in names]
+            kl.append(f"| {label} (`{key}`) | " + " | ".join(v.strip() for v in vals) + " |")
+        kl.append("")
     open(os.path.join(prof, f"{tag}_kernels.md"), "w").write("\n".join(kl) + "\n")
     json.dump(traffic, open(tpath, "w"), indent=1)
     print("\n".join(lines[:40]))
