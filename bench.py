@@ -886,7 +886,7 @@ def main():
             ("bin_tiles", lambda: cs.bin_tiles(step.rec, step.count, step.cam, step.capacity,
                                                ws=step.ws_bin,
                                                out=dict(pair_gid=step.pair_gid,
-                                                        pair_rec=step.pair_rec,
+                                                        
                                                         tile_range=step.tile_range,
                                                         n_pairs_dev=step.n_pairs),
                                                sync=False)),

@@ -149,13 +149,13 @@ int csplat_project_dv(const csplat_gaussians *g, const csplat_codebook *cb,
 
 /* a4 + a5: tile binning and (tile, depth) ordering (R4, R11).
  * Outputs, for n_pairs = sum(count) pairs:
- *   pair_gid[pair_capacity]   Gaussian index per pair, ordered by (tile, bits(z_c), index)
- *   pair_rec[pair_capacity]   the 64-byte record of each pair, same order (the
- *                             contiguous payload the renderer streams with TMA);
- *                             word 14 (0 in rec) carries the pair's cull mask:
- *                             bit w set unless alpha < 1/255 provably holds over
- *                             the whole 8x8 pixel block w (x half w&1, y half w>>1)
- *                             of the pair's tile
+ *   pair_gid[pair_capacity]   one entry per pair, ordered by (tile, bits(z_c), index):
+ *                             bits 0-27 the Gaussian index (n < 2^28), bits 28-31
+ *                             the pair's 8x8-block cull mask: bit w (x half w & 1,
+ *                             y half w >> 1 of the tile) set unless alpha < 1/255
+ *                             provably holds over that whole block.
+ *                             The renderers gather each listed record from rec
+ *                             (one 64-byte TMA bulk copy per entry).
  *   tile_range[T+1][2]        [start, end) of every tile, T = ceil(W/16)*ceil(H/16);
  *                             entry T is the view's STATUS slot {status word, max
  *                             n_pairs}: the library ORs CSPLAT_STATUS_CAPACITY into
@@ -172,7 +172,7 @@ int csplat_project_dv(const csplat_gaussians *g, const csplat_codebook *cb,
  * CSPLAT_ERR_CAPACITY.
  * ws: csplat_workspace_bytes(CSPLAT_OP_BIN_TILES, n, pair_capacity, cam). */
 int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csplat_camera *cam,
-                     int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                     int64_t pair_capacity, uint32_t *pair_gid,
                      uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
                      size_t ws_bytes, void *stream);
 
@@ -181,7 +181,7 @@ int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csp
  * warp-cooperative expansion of each Gaussian's tile rectangle into the tile
  * buckets) fused into the projection kernel while the records are still in
  * registers.  Outputs are bit-identical to the two calls: rec and count as
- * csplat_project (same layout, ownership and alignment), pair_gid, pair_rec,
+ * csplat_project (same layout, ownership and alignment), pair_gid,
  * tile_range and n_pairs_dev as csplat_bin_tiles_active (tile_active may be
  * NULL = every tile).  n = g->n; ws: csplat_workspace_bytes(CSPLAT_OP_BIN_TILES,
  * g->n, pair_capacity, cam).  flags: CSPLAT_SYNC as csplat_bin_tiles.
@@ -189,16 +189,14 @@ int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csp
 int csplat_project_bin(const csplat_gaussians *g, const csplat_codebook *cb,
                        const csplat_camera *cam, const csplat_view *view,
                        const csplat_params *prm, void *rec, int32_t *count,
-                       const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid,
-                       void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                       const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                        uint32_t flags, void *ws, size_t ws_bytes, void *stream);
 
 /* csplat_project_bin with the view in DEVICE memory (see csplat_project_dv). */
 int csplat_project_bin_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                           const csplat_camera *cam, const float *view_dev,
                           const csplat_params *prm, void *rec, int32_t *count,
-                          const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid,
-                          void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                          const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                           uint32_t flags, void *ws, size_t ws_bytes, void *stream);
 
 /* a1 + a2-decode + a3 + a4 + a5 + a6 in one call: csplat_project_bin (every
@@ -207,7 +205,7 @@ int csplat_project_bin_dv(const csplat_gaussians *g, const csplat_codebook *cb,
  * streams forked from and joined back into `stream` (capturable in a CUDA
  * graph): the latency-bound sort of chunk c+1 overlaps the issue-bound forward
  * of chunk c.  Outputs are bit-identical to those calls (tested): rec, count,
- * pair_gid, pair_rec, tile_range, n_pairs_dev as csplat_project_bin; color
+ * pair_gid, tile_range, n_pairs_dev as csplat_project_bin; color
  * [3][H][W], depth, silhouette, t_final [H][W] and n_contrib [H][W] as
  * csplat_render_fwd.  Pairs beyond pair_capacity are dropped (ranges clamped;
  * no CSPLAT_SYNC check here: read n_pairs_dev).  ws: csplat_workspace_bytes(
@@ -219,7 +217,7 @@ int csplat_project_bin_dv(const csplat_gaussians *g, const csplat_codebook *cb,
 int csplat_project_bin_render(const csplat_gaussians *g, const csplat_codebook *cb,
                               const csplat_camera *cam, const csplat_view *view,
                               const csplat_params *prm, void *rec, int32_t *count,
-                              int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                              int64_t pair_capacity, uint32_t *pair_gid,
                               uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                               size_t ws_bytes, float *color, float *depth, float *silhouette,
                               float *t_final, int32_t *n_contrib, void *stream);
@@ -228,7 +226,7 @@ int csplat_project_bin_render(const csplat_gaussians *g, const csplat_codebook *
 int csplat_project_bin_render_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                                  const csplat_camera *cam, const float *view_dev,
                                  const csplat_params *prm, void *rec, int32_t *count,
-                                 int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                                 int64_t pair_capacity, uint32_t *pair_gid,
                                  uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                                  size_t ws_bytes, float *color, float *depth, float *silhouette,
                                  float *t_final, int32_t *n_contrib, void *stream);
@@ -246,7 +244,7 @@ int csplat_project_bin_render_dv(const csplat_gaussians *g, const csplat_codeboo
 int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
                        const csplat_camera *cam, const csplat_view *view,
                        const csplat_params *prm, void *rec, int32_t *count,
-                       int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                       int64_t pair_capacity, uint32_t *pair_gid,
                        uint32_t *tile_range, int64_t *n_pairs_dev, void *ws_bin,
                        size_t ws_bin_bytes, float *color, float *depth, float *silhouette,
                        float *t_final, int32_t *n_contrib, const float *d_color,
@@ -265,8 +263,7 @@ int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
 int csplat_tracking_step(const csplat_gaussians *g, const csplat_codebook *cb,
                          const csplat_camera *cam, const csplat_view *view,
                          const float *view_dev, const csplat_params *prm, void *rec,
-                         int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
-                         void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                         int32_t *count, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                          void *ws_bin, size_t ws_bin_bytes, float *color, float *depth,
                          float *silhouette, float *t_final, int32_t *n_contrib,
                          const float *obs_color, const float *obs_depth,
@@ -281,29 +278,32 @@ int csplat_tracking_step(const csplat_gaussians *g, const csplat_codebook *cb,
  * it to bin only the tiles that hold sampled rays (csplat_ba_patches). */
 int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
                             const csplat_camera *cam, const uint32_t *tile_active,
-                            int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                            int64_t pair_capacity, uint32_t *pair_gid,
                             uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
                             size_t ws_bytes, void *stream);
 
 /* a6: front-to-back compositing of colour, depth and silhouette (Eq 3-5,
  * P:98-109; R1-R3, R7-R10).  Outputs color [3][H][W], depth, silhouette,
  * t_final [H][W] float32 and n_contrib [H][W] int32 (local index + 1 of the
- * last composited entry of the pixel's tile list; the backward's replay bound). */
-int csplat_render_fwd(const void *pair_rec, const uint32_t *tile_range, const csplat_camera *cam,
-                      const csplat_params *prm, float *color, float *depth, float *silhouette,
-                      float *t_final, int32_t *n_contrib, void *stream);
+ * last composited entry of the pixel's tile list; the backward's replay bound).
+ * Inputs: rec (csplat_project) and the pair lists pair_gid / tile_range
+ * (csplat_bin_tiles). */
+int csplat_render_fwd(const void *rec, const uint32_t *pair_gid, const uint32_t *tile_range,
+                      const csplat_camera *cam, const csplat_params *prm, float *color,
+                      float *depth, float *silhouette, float *t_final, int32_t *n_contrib,
+                      void *stream);
 
 /* a7 + a8: backward of a6 through a3, a2-decode and the STE mask (Eq 6), with
  * the pose gradient (R14, R20, R22, R23).  d_color [3][H][W], d_depth,
  * d_silhouette [H][W] are dL/d(outputs).  The forward-state arguments (rec,
- * pair_rec, tile_range, t_final, n_contrib) must come from csplat_project /
+ * pair_gid, tile_range, t_final, n_contrib) must come from csplat_project /
  * csplat_bin_tiles / csplat_render_fwd on the same inputs (not verified).
  * Gradients are w.r.t. mean, opacity logit, rgb, (decoded) log-scale, (decoded)
  * quaternion, mask logit and pose.  flags: CSPLAT_POSE_ONLY, CSPLAT_ACCUMULATE.
  * ws: csplat_workspace_bytes(CSPLAT_OP_RENDER_BWD, n, 0, cam). */
 int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
                       const csplat_camera *cam, const csplat_view *view, const csplat_params *prm,
-                      const void *rec, const void *pair_rec, const uint32_t *tile_range,
+                      const void *rec, const uint32_t *pair_gid, const uint32_t *tile_range,
                       const float *t_final, const int32_t *n_contrib, const float *d_color,
                       const float *d_depth, const float *d_silhouette, uint32_t flags,
                       const csplat_grads *out, void *ws, size_t ws_bytes, void *stream);
@@ -311,7 +311,7 @@ int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
 /* csplat_render_bwd with the view in DEVICE memory (see csplat_project_dv). */
 int csplat_render_bwd_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                          const csplat_camera *cam, const float *view_dev,
-                         const csplat_params *prm, const void *rec, const void *pair_rec,
+                         const csplat_params *prm, const void *rec, const uint32_t *pair_gid,
                          const uint32_t *tile_range, const float *t_final,
                          const int32_t *n_contrib, const float *d_color, const float *d_depth,
                          const float *d_silhouette, uint32_t flags, const csplat_grads *out,
@@ -332,7 +332,7 @@ int csplat_render_bwd_dv(const csplat_gaussians *g, const csplat_codebook *cb,
  * flags (CSPLAT_POSE_ONLY for tracking) and ws as csplat_render_bwd. */
 int csplat_tracking_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
                         const csplat_camera *cam, const csplat_view *view, const float *view_dev,
-                        const csplat_params *prm, const void *rec, const void *pair_rec,
+                        const csplat_params *prm, const void *rec, const uint32_t *pair_gid,
                         const uint32_t *tile_range, const float *t_final,
                         const int32_t *n_contrib, const float *color, const float *depth,
                         const float *silhouette, const float *obs_color, const float *obs_depth,

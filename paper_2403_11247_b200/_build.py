@@ -9,7 +9,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libcsplat.so")
 SOURCES = ["api.cu", "project.cu", "bin.cu", "render_fwd.cu", "render_bwd.cu", "chain.cu", "rvq.cu",
-           "prune.cu", "loss.cu", "rvq_update.cu", "ba.cu"]
+           "prune.cu", "loss.cu", "rvq_update.cu", "ba.cu", "record_tmap.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

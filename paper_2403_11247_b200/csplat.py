@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("CSPLAT_LIB", os.path.join(_PKG, "libcsplat.so"))
 TILE = 16
 RECORD_BYTES = 64
 SYNC, POSE_ONLY, ACCUMULATE, SKIP_CHAIN = 1, 2, 4, 8
+PAIR_GID_MASK, PAIR_MASK_SHIFT = (1 << 28) - 1, 28  # pair_gid: index | block mask << 28
 STATUS_CAPACITY, STATUS_CODE_INDEX = 1, 2  # device status bits (csplat.h)
 OP_BIN_TILES, OP_RENDER_BWD, OP_MASK_PRUNE = 1, 2, 3
 
@@ -92,29 +93,29 @@ def lib():
         L = C.CDLL(LIB_PATH)
         vp, i64, i32, u32 = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32
         L.csplat_project.argtypes = [vp] * 8
-        L.csplat_bin_tiles.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp, vp, u32, vp, C.c_size_t, vp]
-        L.csplat_bin_tiles_active.argtypes = [vp, vp, i64, vp, vp, i64, vp, vp, vp, vp, u32, vp,
+        L.csplat_bin_tiles.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp, u32, vp, C.c_size_t, vp]
+        L.csplat_bin_tiles_active.argtypes = [vp, vp, i64, vp, vp, i64, vp, vp, vp, u32, vp,
                                               C.c_size_t, vp]
         L.csplat_ba_patches.argtypes = [vp, vp, vp, i64, vp, vp, vp]
         L.csplat_ba_patch_loss.argtypes = [vp] * 6 + [i64, i64, vp, C.c_float, C.c_float] + \
             [vp] * 5
         L.csplat_project_dv.argtypes = [vp] * 8
-        L.csplat_project_bin.argtypes = [vp] * 8 + [i64, vp, vp, vp, vp, u32, vp, C.c_size_t, vp]
-        L.csplat_project_bin_render.argtypes = [vp] * 7 + [i64, vp, vp, vp, vp, vp, C.c_size_t] + \
+        L.csplat_project_bin.argtypes = [vp] * 8 + [i64, vp, vp, vp, u32, vp, C.c_size_t, vp]
+        L.csplat_project_bin_render.argtypes = [vp] * 7 + [i64, vp, vp, vp, vp, C.c_size_t] + \
             [vp] * 6
         L.csplat_project_bin_render_dv.argtypes = L.csplat_project_bin_render.argtypes
-        L.csplat_render_step.argtypes = [vp] * 7 + [i64, vp, vp, vp, vp, vp, C.c_size_t] + \
+        L.csplat_render_step.argtypes = [vp] * 7 + [i64, vp, vp, vp, vp, C.c_size_t] + \
             [vp] * 8 + [u32, vp, vp, C.c_size_t, vp]
-        L.csplat_tracking_step.argtypes = [vp] * 8 + [i64, vp, vp, vp, vp, vp, C.c_size_t] + \
+        L.csplat_tracking_step.argtypes = [vp] * 8 + [i64, vp, vp, vp, vp, C.c_size_t] + \
             [vp] * 8 + [C.c_float, C.c_float, u32, vp, vp, vp, C.c_size_t, vp]
-        L.csplat_project_bin_dv.argtypes = [vp] * 8 + [i64, vp, vp, vp, vp, u32, vp, C.c_size_t,
+        L.csplat_project_bin_dv.argtypes = [vp] * 8 + [i64, vp, vp, vp, u32, vp, C.c_size_t,
                                                         vp]
         L.csplat_render_bwd_dv.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_pose_step.argtypes = [vp, vp, C.c_float, C.c_float, vp]
         L.csplat_tracking_bwd.argtypes = [vp] * 17 + [C.c_float, C.c_float, u32, vp, vp, vp,
                                                       C.c_size_t, vp]
         L.csplat_count_valid_depth.argtypes = [vp, i32, i32, vp, vp]
-        L.csplat_render_fwd.argtypes = [vp] * 10
+        L.csplat_render_fwd.argtypes = [vp] * 11
         L.csplat_render_bwd.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_rvq_assign.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp]
         L.csplat_rvq_code_grad.argtypes = [vp, i64, vp, i32, vp, i32, i32, i32, vp, u32, vp]
@@ -275,14 +276,13 @@ def project_bin(g: GaussianMap, cam: dict, v, capacity: int, prm: Params | None 
     tx, ty = tiles(cam)
     if out is None:
         out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
-                   pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
                    tile_range=alloc_tile_range(cam, dev),
                    n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
     if ws is None:
         ws = torch.empty(workspace_bytes(OP_BIN_TILES, n, capacity, cam), dtype=torch.uint8,
                          device=dev)
     gs, cbs = g.struct(), cb.struct() if cb is not None else None
-    tail = (_ptr(tile_active), capacity, _ptr(out["pair_gid"]), _ptr(out["pair_rec"]),
+    tail = (_ptr(tile_active), capacity, _ptr(out["pair_gid"]),
             _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]), SYNC if sync else 0, _ptr(ws),
             ws.numel(), _stream(stream))
     if _on_device(v):
@@ -309,7 +309,6 @@ def project_bin_render(g: GaussianMap, cam: dict, v, capacity: int, prm: Params 
     tx, ty = tiles(cam)
     if out is None:
         out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
-                   pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
                    tile_range=alloc_tile_range(cam, dev),
                    n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
     if img is None:
@@ -320,7 +319,7 @@ def project_bin_render(g: GaussianMap, cam: dict, v, capacity: int, prm: Params 
         ws = torch.empty(workspace_bytes(OP_BIN_TILES, n, capacity, cam), dtype=torch.uint8,
                          device=dev)
     gs, cbs = g.struct(), cb.struct() if cb is not None else None
-    tail = (_ptr(rec), _ptr(count), capacity, _ptr(out["pair_gid"]), _ptr(out["pair_rec"]),
+    tail = (_ptr(rec), _ptr(count), capacity, _ptr(out["pair_gid"]),
             _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]), _ptr(ws), ws.numel(),
             _ptr(img["color"]), _ptr(img["depth"]), _ptr(img["sil"]), _ptr(img["t_final"]),
             _ptr(img["n_contrib"]), _stream(stream))
@@ -350,7 +349,6 @@ def render_step(g: GaussianMap, cam: dict, v, capacity: int, d_color, d_depth, d
     tx, ty = tiles(cam)
     if out is None:
         out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
-                   pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
                    tile_range=alloc_tile_range(cam, dev),
                    n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
     if img is None:
@@ -370,7 +368,7 @@ def render_step(g: GaussianMap, cam: dict, v, capacity: int, d_color, d_depth, d
     _check(lib().csplat_render_step(
         C.byref(gs), _byref(cbs), C.byref(camera(cam)), C.byref(view(v)),
         C.byref(prm or params()), _ptr(rec), _ptr(count), capacity, _ptr(out["pair_gid"]),
-        _ptr(out["pair_rec"]), _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]), _ptr(ws),
+        _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]), _ptr(ws),
         ws.numel(), _ptr(img["color"]), _ptr(img["depth"]), _ptr(img["sil"]),
         _ptr(img["t_final"]), _ptr(img["n_contrib"]), _ptr(d_color), _ptr(d_depth), _ptr(d_sil),
         flags, C.byref(gr), _ptr(ws_bwd), ws_bwd.numel(), _stream(stream)), "csplat_render_step")
@@ -403,7 +401,7 @@ def tracking_step(g: GaussianMap, cam: dict, v, capacity: int, obs_color, obs_de
     _check(lib().csplat_tracking_step(
         C.byref(gs), _byref(cbs), C.byref(camera(cam)), None if dv else C.byref(hv),
         _ptr(v) if dv else None, C.byref(prm or params()), _ptr(rec), _ptr(count), capacity,
-        _ptr(out["pair_gid"]), _ptr(out["pair_rec"]), _ptr(out["tile_range"]),
+        _ptr(out["pair_gid"]), _ptr(out["tile_range"]),
         _ptr(out["n_pairs_dev"]), _ptr(ws), ws.numel(), _ptr(img["color"]), _ptr(img["depth"]),
         _ptr(img["sil"]), _ptr(img["t_final"]), _ptr(img["n_contrib"]), _ptr(obs_color),
         _ptr(obs_depth), _ptr(n_valid), lambda_depth, sil_gate, flags, C.byref(gr), _ptr(loss3),
@@ -429,7 +427,7 @@ def count_valid_depth(obs_depth, n_valid=None, stream=None):
     return n_valid
 
 
-def tracking_bwd(g: GaussianMap, cam: dict, v, rec, pair_rec, tile_range, img: dict, obs_color,
+def tracking_bwd(g: GaussianMap, cam: dict, v, rec, pair_gid, tile_range, img: dict, obs_color,
                  obs_depth, n_valid, prm: Params | None = None, cb: CodebookT | None = None,
                  flags: int = POSE_ONLY, lambda_depth=1.0, sil_gate=0.99, grads=None, loss3=None,
                  ws=None, stream=None):
@@ -448,7 +446,7 @@ def tracking_bwd(g: GaussianMap, cam: dict, v, rec, pair_rec, tile_range, img: d
     hv = None if dv else view(v)
     _check(lib().csplat_tracking_bwd(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
                                      None if dv else C.byref(hv), _ptr(v) if dv else None,
-                                     C.byref(prm or params()), _ptr(rec), _ptr(pair_rec),
+                                     C.byref(prm or params()), _ptr(rec), _ptr(pair_gid),
                                      _ptr(tile_range), _ptr(img["t_final"]), _ptr(img["n_contrib"]),
                                      _ptr(img["color"]), _ptr(img["depth"]), _ptr(img["sil"]),
                                      _ptr(obs_color), _ptr(obs_depth), _ptr(n_valid),
@@ -473,14 +471,13 @@ def workspace_bytes(op: int, n: int, pairs: int = 0, cam: dict | None = None) ->
 
 def bin_tiles(rec, count, cam: dict, capacity: int, ws=None, out=None, sync=True, stream=None,
               tile_active=None):
-    """a4+a5.  Returns dict(pair_gid, pair_rec, tile_range, n_pairs_dev[, n_pairs]).
+    """a4+a5.  Returns dict(pair_gid, tile_range, n_pairs_dev).
     tile_active (device int32 bitmask, NEXT-4): bin only those tiles."""
     n = int(count.shape[0])
     dev = rec.device
     tx, ty = tiles(cam)
     if out is None:
         out = dict(pair_gid=torch.empty(max(capacity, 1), dtype=torch.int32, device=dev),
-                   pair_rec=torch.empty((max(capacity, 1), 16), dtype=torch.int32, device=dev),
                    tile_range=alloc_tile_range(cam, dev),
                    n_pairs_dev=torch.zeros(1, dtype=torch.int64, device=dev))
     if ws is None:
@@ -488,21 +485,21 @@ def bin_tiles(rec, count, cam: dict, capacity: int, ws=None, out=None, sync=True
                          device=dev)
     if tile_active is None:
         st = lib().csplat_bin_tiles(_ptr(rec), _ptr(count), n, C.byref(camera(cam)), capacity,
-                                    _ptr(out["pair_gid"]), _ptr(out["pair_rec"]),
+                                    _ptr(out["pair_gid"]),
                                     _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]),
                                     SYNC if sync else 0, _ptr(ws), ws.numel(), _stream(stream))
         _check(st, "csplat_bin_tiles")
     else:
         st = lib().csplat_bin_tiles_active(_ptr(rec), _ptr(count), n, C.byref(camera(cam)),
                                            _ptr(tile_active), capacity, _ptr(out["pair_gid"]),
-                                           _ptr(out["pair_rec"]), _ptr(out["tile_range"]),
+                                           _ptr(out["tile_range"]),
                                            _ptr(out["n_pairs_dev"]), SYNC if sync else 0,
                                            _ptr(ws), ws.numel(), _stream(stream))
         _check(st, "csplat_bin_tiles_active")
     return out
 
 
-def render_fwd(pair_rec, tile_range, cam: dict, prm: Params | None = None, out=None,
+def render_fwd(rec, pair_gid, tile_range, cam: dict, prm: Params | None = None, out=None,
                stream=None):
     """a6.  Returns dict(color [3,H,W], depth, sil, t_final [H,W], n_contrib [H,W])."""
     H, W = cam["height"], cam["width"]
@@ -512,7 +509,7 @@ def render_fwd(pair_rec, tile_range, cam: dict, prm: Params | None = None, out=N
                    depth=torch.empty((H, W), device=dev), sil=torch.empty((H, W), device=dev),
                    t_final=torch.empty((H, W), device=dev),
                    n_contrib=torch.empty((H, W), dtype=torch.int32, device=dev))
-    _check(lib().csplat_render_fwd(_ptr(pair_rec), _ptr(tile_range), C.byref(camera(cam)),
+    _check(lib().csplat_render_fwd(_ptr(rec), _ptr(pair_gid), _ptr(tile_range), C.byref(camera(cam)),
                                    C.byref(prm or params()), _ptr(out["color"]),
                                    _ptr(out["depth"]), _ptr(out["sil"]), _ptr(out["t_final"]),
                                    _ptr(out["n_contrib"]), _stream(stream)), "csplat_render_fwd")
@@ -538,7 +535,7 @@ def alloc_grads(n: int, device="cuda", pose_only=False):
     return g
 
 
-def render_bwd(g: GaussianMap, cam: dict, v, rec, pair_rec, tile_range, t_final, n_contrib,
+def render_bwd(g: GaussianMap, cam: dict, v, rec, pair_gid, tile_range, t_final, n_contrib,
                d_color, d_depth, d_sil, prm: Params | None = None, cb: CodebookT | None = None,
                flags: int = 0, grads=None, ws=None, stream=None):
     """a7+a8.  Returns the grads dict (mean, opacity, rgb, log_scale, quat, mask, pose)."""
@@ -553,7 +550,7 @@ def render_bwd(g: GaussianMap, cam: dict, v, rec, pair_rec, tile_range, t_final,
     gs, cbs = g.struct(), cb.struct() if cb is not None else None
     if _on_device(v):
         _check(lib().csplat_render_bwd_dv(C.byref(gs), _byref(cbs), C.byref(camera(cam)), _ptr(v),
-                                          C.byref(prm or params()), _ptr(rec), _ptr(pair_rec),
+                                          C.byref(prm or params()), _ptr(rec), _ptr(pair_gid),
                                           _ptr(tile_range), _ptr(t_final), _ptr(n_contrib),
                                           _ptr(d_color), _ptr(d_depth), _ptr(d_sil), flags,
                                           C.byref(gr), _ptr(ws), ws.numel(), _stream(stream)),
@@ -561,7 +558,7 @@ def render_bwd(g: GaussianMap, cam: dict, v, rec, pair_rec, tile_range, t_final,
         return grads
     _check(lib().csplat_render_bwd(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
                                    C.byref(view(v)), C.byref(prm or params()), _ptr(rec),
-                                   _ptr(pair_rec), _ptr(tile_range), _ptr(t_final),
+                                   _ptr(pair_gid), _ptr(tile_range), _ptr(t_final),
                                    _ptr(n_contrib), _ptr(d_color), _ptr(d_depth), _ptr(d_sil),
                                    flags, C.byref(gr), _ptr(ws), ws.numel(), _stream(stream)),
            "csplat_render_bwd")

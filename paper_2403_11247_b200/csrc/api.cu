@@ -202,7 +202,7 @@ static int project_bin_impl(const csplat_gaussians *g, const csplat_codebook *cb
                             const csplat_camera *cam, const csplat_view *view,
                             const float *view_dev, const csplat_params *prm, void *rec,
                             int32_t *count, const uint32_t *tile_active, int64_t pair_capacity,
-                            uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                            uint32_t *pair_gid, uint32_t *tile_range,
                             int64_t *n_pairs_dev, uint32_t flags, void *ws, size_t ws_bytes,
                             void *stream) {
   RET_IF(check_gaussians(g));
@@ -213,10 +213,11 @@ static int project_bin_impl(const csplat_gaussians *g, const csplat_codebook *cb
   if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
   if (!(prm->mask_eps > 0.f) || !(prm->mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
   if (pair_capacity < 0 || pair_capacity > 0xffffffffLL) return invalid("capacity out of range");
+  if (g->n > (int64_t)csplat::kPairGidMask + 1) return invalid("n must be < 2^28 for binning");
   if (!tile_range || !n_pairs_dev) return invalid("tile_range/n_pairs NULL");
-  if (pair_capacity > 0 && (!pair_gid || !pair_rec)) return invalid("pair_gid/pair_rec NULL");
-  if (!aligned16(rec) || !aligned16(pair_rec)) {
-    set_err("rec/pair_rec must be 16-byte aligned");
+  if (pair_capacity > 0 && !pair_gid) return invalid("pair_gid NULL");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
     return CSPLAT_ERR_ALIGNMENT;
   }
   const size_t need = csplat::bin_workspace_bytes(g->n, pair_capacity, *cam);
@@ -231,7 +232,7 @@ static int project_bin_impl(const csplat_gaussians *g, const csplat_codebook *cb
   RET_IF(cuda_status(csplat::launch_project_bin(*g, cb ? &d : nullptr, *cam,
                                                 view ? *view : csplat_view{}, view_dev,
                                                 mask_tau(prm->mask_eps), prm->dilation, rec, count,
-                                                pair_capacity, tile_active, pair_gid, pair_rec,
+                                                pair_capacity, tile_active, pair_gid,
                                                 tile_range, n_pairs_dev, ws, s),
                      "csplat_project_bin"));
   if (flags & CSPLAT_SYNC) {
@@ -251,31 +252,28 @@ static int project_bin_impl(const csplat_gaussians *g, const csplat_codebook *cb
 int csplat_project_bin(const csplat_gaussians *g, const csplat_codebook *cb,
                        const csplat_camera *cam, const csplat_view *view,
                        const csplat_params *prm, void *rec, int32_t *count,
-                       const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid,
-                       void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                       const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                        uint32_t flags, void *ws, size_t ws_bytes, void *stream) {
   if (!view) return invalid("view NULL");
   return project_bin_impl(g, cb, cam, view, nullptr, prm, rec, count, tile_active, pair_capacity,
-                          pair_gid, pair_rec, tile_range, n_pairs_dev, flags, ws, ws_bytes, stream);
+                          pair_gid, tile_range, n_pairs_dev, flags, ws, ws_bytes, stream);
 }
 
 int csplat_project_bin_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                           const csplat_camera *cam, const float *view_dev,
                           const csplat_params *prm, void *rec, int32_t *count,
-                          const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid,
-                          void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                          const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                           uint32_t flags, void *ws, size_t ws_bytes, void *stream) {
   if (!view_dev) return invalid("view_dev NULL");
   return project_bin_impl(g, cb, cam, nullptr, view_dev, prm, rec, count, tile_active,
-                          pair_capacity, pair_gid, pair_rec, tile_range, n_pairs_dev, flags, ws,
+                          pair_capacity, pair_gid, tile_range, n_pairs_dev, flags, ws,
                           ws_bytes, stream);
 }
 
 static int project_bin_render_impl(const csplat_gaussians *g, const csplat_codebook *cb,
                                    const csplat_camera *cam, const csplat_view *view,
                                    const float *view_dev, const csplat_params *prm, void *rec,
-                                   int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
-                                   void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                                   int32_t *count, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                                    void *ws, size_t ws_bytes, float *color, float *depth,
                                    float *silhouette, float *t_final, int32_t *n_contrib,
                                    void *stream) {
@@ -287,12 +285,13 @@ static int project_bin_render_impl(const csplat_gaussians *g, const csplat_codeb
   if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
   if (!(prm->mask_eps > 0.f) || !(prm->mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
   if (pair_capacity < 0 || pair_capacity > 0xffffffffLL) return invalid("capacity out of range");
+  if (g->n > (int64_t)csplat::kPairGidMask + 1) return invalid("n must be < 2^28 for binning");
   if (!tile_range || !n_pairs_dev) return invalid("tile_range/n_pairs NULL");
-  if (pair_capacity > 0 && (!pair_gid || !pair_rec)) return invalid("pair_gid/pair_rec NULL");
+  if (pair_capacity > 0 && !pair_gid) return invalid("pair_gid NULL");
   if (!color || !depth || !silhouette || !t_final || !n_contrib)
     return invalid("project_bin_render: image NULL");
-  if (!aligned16(rec) || !aligned16(pair_rec)) {
-    set_err("rec/pair_rec must be 16-byte aligned");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
     return CSPLAT_ERR_ALIGNMENT;
   }
   const size_t need = csplat::bin_workspace_bytes(g->n, pair_capacity, *cam);
@@ -306,7 +305,7 @@ static int project_bin_render_impl(const csplat_gaussians *g, const csplat_codeb
   return cuda_status(csplat::launch_project_bin_render(
                          *g, cb ? &d : nullptr, *cam, view ? *view : csplat_view{}, view_dev,
                          mask_tau(prm->mask_eps), prm->dilation, *prm, rec, count, pair_capacity,
-                         pair_gid, pair_rec, tile_range, n_pairs_dev, ws, color, depth,
+                         pair_gid, tile_range, n_pairs_dev, ws, color, depth,
                          silhouette, t_final, n_contrib, static_cast<cudaStream_t>(stream)),
                      "csplat_project_bin_render");
 }
@@ -314,34 +313,33 @@ static int project_bin_render_impl(const csplat_gaussians *g, const csplat_codeb
 int csplat_project_bin_render(const csplat_gaussians *g, const csplat_codebook *cb,
                               const csplat_camera *cam, const csplat_view *view,
                               const csplat_params *prm, void *rec, int32_t *count,
-                              int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                              int64_t pair_capacity, uint32_t *pair_gid,
                               uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                               size_t ws_bytes, float *color, float *depth, float *silhouette,
                               float *t_final, int32_t *n_contrib, void *stream) {
   if (!view) return invalid("view NULL");
   return project_bin_render_impl(g, cb, cam, view, nullptr, prm, rec, count, pair_capacity,
-                                 pair_gid, pair_rec, tile_range, n_pairs_dev, ws, ws_bytes, color,
+                                 pair_gid, tile_range, n_pairs_dev, ws, ws_bytes, color,
                                  depth, silhouette, t_final, n_contrib, stream);
 }
 
 int csplat_project_bin_render_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                                  const csplat_camera *cam, const float *view_dev,
                                  const csplat_params *prm, void *rec, int32_t *count,
-                                 int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                                 int64_t pair_capacity, uint32_t *pair_gid,
                                  uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                                  size_t ws_bytes, float *color, float *depth, float *silhouette,
                                  float *t_final, int32_t *n_contrib, void *stream) {
   if (!view_dev) return invalid("view_dev NULL");
   return project_bin_render_impl(g, cb, cam, nullptr, view_dev, prm, rec, count, pair_capacity,
-                                 pair_gid, pair_rec, tile_range, n_pairs_dev, ws, ws_bytes, color,
+                                 pair_gid, tile_range, n_pairs_dev, ws, ws_bytes, color,
                                  depth, silhouette, t_final, n_contrib, stream);
 }
 
 static int render_step_impl(const csplat_gaussians *g, const csplat_codebook *cb,
                             const csplat_camera *cam, const csplat_view *view,
                             const float *view_dev, const csplat_params *prm, void *rec,
-                            int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
-                            void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                            int32_t *count, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                             void *ws_bin, size_t ws_bin_bytes, float *color, float *depth,
                             float *silhouette, float *t_final, int32_t *n_contrib,
                             const float *d_color, const float *d_depth,
@@ -356,14 +354,15 @@ static int render_step_impl(const csplat_gaussians *g, const csplat_codebook *cb
   if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
   if (!(prm->mask_eps > 0.f) || !(prm->mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
   if (pair_capacity < 0 || pair_capacity > 0xffffffffLL) return invalid("capacity out of range");
+  if (g->n > (int64_t)csplat::kPairGidMask + 1) return invalid("n must be < 2^28 for binning");
   if (!tile_range || !n_pairs_dev) return invalid("tile_range/n_pairs NULL");
-  if (pair_capacity > 0 && (!pair_gid || !pair_rec)) return invalid("pair_gid/pair_rec NULL");
+  if (pair_capacity > 0 && !pair_gid) return invalid("pair_gid NULL");
   if (!color || !depth || !silhouette || !t_final || !n_contrib)
     return invalid("render_step: image NULL");
   if (!loss && (!d_color || !d_depth || !d_silhouette)) return invalid("render_step: upstream NULL");
   if (!loss && (flags & CSPLAT_POSE_ONLY)) return invalid("render_step: CSPLAT_POSE_ONLY not supported");
-  if (!aligned16(rec) || !aligned16(pair_rec)) {
-    set_err("rec/pair_rec must be 16-byte aligned");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
     return CSPLAT_ERR_ALIGNMENT;
   }
   if (!ws_bin || ws_bin_bytes < csplat::bin_workspace_bytes(g->n, pair_capacity, *cam)) {
@@ -381,7 +380,7 @@ static int render_step_impl(const csplat_gaussians *g, const csplat_codebook *cb
   return cuda_status(csplat::launch_render_step(*g, cb ? &d : nullptr, *cam,
                                                 view ? *view : csplat_view{}, view_dev,
                                                 mask_tau(prm->mask_eps), prm->dilation, *prm, rec,
-                                                count, pair_capacity, pair_gid, pair_rec,
+                                                count, pair_capacity, pair_gid,
                                                 tile_range, n_pairs_dev, ws_bin, color, depth,
                                                 silhouette, t_final, n_contrib, &b,
                                                 static_cast<cudaStream_t>(stream)),
@@ -391,7 +390,7 @@ static int render_step_impl(const csplat_gaussians *g, const csplat_codebook *cb
 int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
                        const csplat_camera *cam, const csplat_view *view,
                        const csplat_params *prm, void *rec, int32_t *count,
-                       int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                       int64_t pair_capacity, uint32_t *pair_gid,
                        uint32_t *tile_range, int64_t *n_pairs_dev, void *ws_bin,
                        size_t ws_bin_bytes, float *color, float *depth, float *silhouette,
                        float *t_final, int32_t *n_contrib, const float *d_color,
@@ -400,7 +399,7 @@ int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
                        void *stream) {
   if (!view) return invalid("view NULL");
   return render_step_impl(g, cb, cam, view, nullptr, prm, rec, count, pair_capacity, pair_gid,
-                          pair_rec, tile_range, n_pairs_dev, ws_bin, ws_bin_bytes, color, depth,
+                          tile_range, n_pairs_dev, ws_bin, ws_bin_bytes, color, depth,
                           silhouette, t_final, n_contrib, d_color, d_depth, d_silhouette, nullptr,
                           flags, out, ws_bwd, ws_bwd_bytes, stream);
 }
@@ -408,8 +407,7 @@ int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
 int csplat_tracking_step(const csplat_gaussians *g, const csplat_codebook *cb,
                          const csplat_camera *cam, const csplat_view *view,
                          const float *view_dev, const csplat_params *prm, void *rec,
-                         int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
-                         void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev,
+                         int32_t *count, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                          void *ws_bin, size_t ws_bin_bytes, float *color, float *depth,
                          float *silhouette, float *t_final, int32_t *n_contrib,
                          const float *obs_color, const float *obs_depth,
@@ -425,23 +423,25 @@ int csplat_tracking_step(const csplat_gaussians *g, const csplat_codebook *cb,
                                 reinterpret_cast<const unsigned long long *>(n_valid_dev),
                                 lambda_depth, sil_gate, loss3_dev};
   return render_step_impl(g, cb, cam, view, view_dev, prm, rec, count, pair_capacity, pair_gid,
-                          pair_rec, tile_range, n_pairs_dev, ws_bin, ws_bin_bytes, color, depth,
+                          tile_range, n_pairs_dev, ws_bin, ws_bin_bytes, color, depth,
                           silhouette, t_final, n_contrib, nullptr, nullptr, nullptr, &tl, flags,
                           out, ws_bwd, ws_bwd_bytes, stream);
 }
 
 int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
                             const csplat_camera *cam, const uint32_t *tile_active,
-                            int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                            int64_t pair_capacity, uint32_t *pair_gid,
                      uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
                      size_t ws_bytes, void *stream) {
   RET_IF(check_camera(cam));
-  if (n < 0 || pair_capacity < 0 || pair_capacity > 0xffffffffLL) return invalid("n/capacity out of range");
+  if (n < 0 || n > (int64_t)csplat::kPairGidMask + 1 || pair_capacity < 0 ||
+      pair_capacity > 0xffffffffLL)
+    return invalid("n (< 2^28 for binning) / capacity out of range");
   if (!tile_range || !n_pairs_dev) return invalid("tile_range/n_pairs NULL");
   if (n > 0 && (!rec || !count)) return invalid("rec/count NULL");
-  if (pair_capacity > 0 && (!pair_gid || !pair_rec)) return invalid("pair_gid/pair_rec NULL");
-  if (!aligned16(rec) || !aligned16(pair_rec)) {
-    set_err("rec/pair_rec must be 16-byte aligned");
+  if (pair_capacity > 0 && !pair_gid) return invalid("pair_gid NULL");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
     return CSPLAT_ERR_ALIGNMENT;
   }
   const size_t need = csplat::bin_workspace_bytes(n, pair_capacity, *cam);
@@ -451,7 +451,7 @@ int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
   }
   RET_IF(check_device());
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  RET_IF(cuda_status(csplat::launch_bin(rec, count, n, *cam, pair_capacity, tile_active, pair_gid, pair_rec,
+  RET_IF(cuda_status(csplat::launch_bin(rec, count, n, *cam, pair_capacity, tile_active, pair_gid,
                                         tile_range, n_pairs_dev, ws, s),
                      "csplat_bin_tiles"));
   if (flags & CSPLAT_SYNC) {
@@ -469,10 +469,10 @@ int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
 }
 
 int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csplat_camera *cam,
-                     int64_t pair_capacity, uint32_t *pair_gid, void *pair_rec,
+                     int64_t pair_capacity, uint32_t *pair_gid,
                      uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
                      size_t ws_bytes, void *stream) {
-  return csplat_bin_tiles_active(rec, count, n, cam, nullptr, pair_capacity, pair_gid, pair_rec,
+  return csplat_bin_tiles_active(rec, count, n, cam, nullptr, pair_capacity, pair_gid,
                                  tile_range, n_pairs_dev, flags, ws, ws_bytes, stream);
 }
 
@@ -514,18 +514,19 @@ int csplat_ba_patch_loss(const float *color, const float *depth, const float *ob
       "csplat_ba_patch_loss");
 }
 
-int csplat_render_fwd(const void *pair_rec, const uint32_t *tile_range, const csplat_camera *cam,
-                      const csplat_params *prm, float *color, float *depth, float *silhouette,
-                      float *t_final, int32_t *n_contrib, void *stream) {
+int csplat_render_fwd(const void *rec, const uint32_t *pair_gid, const uint32_t *tile_range,
+                      const csplat_camera *cam, const csplat_params *prm, float *color,
+                      float *depth, float *silhouette, float *t_final, int32_t *n_contrib,
+                      void *stream) {
   RET_IF(check_camera(cam));
   if (!prm || !tile_range || !color || !depth || !silhouette || !t_final || !n_contrib)
     return invalid("render_fwd: NULL argument");
-  if (!aligned16(pair_rec)) {
-    set_err("pair_rec must be 16-byte aligned");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
     return CSPLAT_ERR_ALIGNMENT;
   }
   RET_IF(check_device());
-  return cuda_status(csplat::launch_render_fwd(pair_rec, tile_range, *cam, *prm, color, depth,
+  return cuda_status(csplat::launch_render_fwd(rec, pair_gid, tile_range, *cam, *prm, color, depth,
                                                silhouette, t_final, n_contrib,
                                                static_cast<cudaStream_t>(stream)),
                      "csplat_render_fwd");
@@ -534,7 +535,7 @@ int csplat_render_fwd(const void *pair_rec, const uint32_t *tile_range, const cs
 static int render_bwd_impl(const csplat_gaussians *g, const csplat_codebook *cb,
                       const csplat_camera *cam, const csplat_view *view, const float *view_dev,
                       const csplat_params *prm,
-                      const void *rec, const void *pair_rec, const uint32_t *tile_range,
+                      const void *rec, const uint32_t *pair_gid, const uint32_t *tile_range,
                       const float *t_final, const int32_t *n_contrib, const float *d_color,
                       const float *d_depth, const float *d_silhouette, uint32_t flags,
                       const csplat_grads *out, void *ws, size_t ws_bytes, void *stream,
@@ -547,8 +548,8 @@ static int render_bwd_impl(const csplat_gaussians *g, const csplat_codebook *cb,
     return invalid("render_bwd: NULL argument");
   if (g->n > 0 && !rec) return invalid("rec NULL");
   if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
-  if (!aligned16(rec) || !aligned16(pair_rec)) {
-    set_err("rec/pair_rec must be 16-byte aligned");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
     return CSPLAT_ERR_ALIGNMENT;
   }
   if (!ws || ws_bytes < csplat::bwd_workspace_bytes(g->n) || !aligned16(ws)) {
@@ -561,7 +562,7 @@ static int render_bwd_impl(const csplat_gaussians *g, const csplat_codebook *cb,
   return cuda_status(csplat::launch_render_bwd(*g, cb ? &d : nullptr, *cam,
                                                view ? *view : csplat_view{}, view_dev, loss,
                                                *prm, rec,
-                                               pair_rec, tile_range, t_final, n_contrib, d_color,
+                                               pair_gid, tile_range, t_final, n_contrib, d_color,
                                                d_depth, d_silhouette, flags, *out, ws,
                                                static_cast<cudaStream_t>(stream)),
                      "csplat_render_bwd");
@@ -569,25 +570,25 @@ static int render_bwd_impl(const csplat_gaussians *g, const csplat_codebook *cb,
 
 int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
                       const csplat_camera *cam, const csplat_view *view, const csplat_params *prm,
-                      const void *rec, const void *pair_rec, const uint32_t *tile_range,
+                      const void *rec, const uint32_t *pair_gid, const uint32_t *tile_range,
                       const float *t_final, const int32_t *n_contrib, const float *d_color,
                       const float *d_depth, const float *d_silhouette, uint32_t flags,
                       const csplat_grads *out, void *ws, size_t ws_bytes, void *stream) {
   if (!view) return invalid("view NULL");
-  return render_bwd_impl(g, cb, cam, view, nullptr, prm, rec, pair_rec, tile_range, t_final,
+  return render_bwd_impl(g, cb, cam, view, nullptr, prm, rec, pair_gid, tile_range, t_final,
                          n_contrib, d_color, d_depth, d_silhouette, flags, out, ws, ws_bytes,
                          stream);
 }
 
 int csplat_render_bwd_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                          const csplat_camera *cam, const float *view_dev,
-                         const csplat_params *prm, const void *rec, const void *pair_rec,
+                         const csplat_params *prm, const void *rec, const uint32_t *pair_gid,
                          const uint32_t *tile_range, const float *t_final,
                          const int32_t *n_contrib, const float *d_color, const float *d_depth,
                          const float *d_silhouette, uint32_t flags, const csplat_grads *out,
                          void *ws, size_t ws_bytes, void *stream) {
   if (!view_dev) return invalid("view_dev NULL");
-  return render_bwd_impl(g, cb, cam, nullptr, view_dev, prm, rec, pair_rec, tile_range, t_final,
+  return render_bwd_impl(g, cb, cam, nullptr, view_dev, prm, rec, pair_gid, tile_range, t_final,
                          n_contrib, d_color, d_depth, d_silhouette, flags, out, ws, ws_bytes,
                          stream);
 }
@@ -605,7 +606,7 @@ int csplat_count_valid_depth(const float *obs_depth, int32_t width, int32_t heig
 
 int csplat_tracking_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
                         const csplat_camera *cam, const csplat_view *view, const float *view_dev,
-                        const csplat_params *prm, const void *rec, const void *pair_rec,
+                        const csplat_params *prm, const void *rec, const uint32_t *pair_gid,
                         const uint32_t *tile_range, const float *t_final,
                         const int32_t *n_contrib, const float *color, const float *depth,
                         const float *silhouette, const float *obs_color, const float *obs_depth,
@@ -620,7 +621,7 @@ int csplat_tracking_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
   csplat::TrackingLoss tl{color, depth, silhouette, obs_color, obs_depth,
                           reinterpret_cast<const unsigned long long *>(n_valid_dev), lambda_depth,
                           sil_gate, loss3_dev};
-  return render_bwd_impl(g, cb, cam, view, view_dev, prm, rec, pair_rec, tile_range, t_final,
+  return render_bwd_impl(g, cb, cam, view, view_dev, prm, rec, pair_gid, tile_range, t_final,
                          n_contrib, nullptr, nullptr, nullptr, flags, out, ws, ws_bytes, stream,
                          &tl);
 }

@@ -138,82 +138,22 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long *a, int len, int
   cta_sync();
 }
 
-// Cull hint for the renderers: bit w (w = 0..3, x half = w & 1, y half = w >> 1)
-// of the pair payload's word 14 is set unless the Gaussian provably has
-// alpha < 1/255 over the whole 8x8 pixel block w of the tile, i.e. unless the
-// minimum of q(dx, dy) = ca dx^2 + (2cb) dx dy + cc dy^2 over the block's
-// rectangle exceeds k^2 by more than a rounding margin (the renderers skip a
-// pixel when q > k^2).  The minimum of the convex q over a box
-// that does not contain the centre lies on a box edge that faces the centre,
-// so at most two 1-D clamped minimisations per block.  The margin covers the
-// float32 evaluation of q at any pixel of the block, so a
-// cleared bit never skips a pixel the per-pixel test would have composited.
-__device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1, const uint4 &v3,
-                                               int X0, int Y0) {
-  const float u = __uint_as_float(v0.x), v = __uint_as_float(v0.y);
-  const float ca = __uint_as_float(v0.z), cb2 = __uint_as_float(v0.w);
-  const float cc = __uint_as_float(v1.x), k2 = __uint_as_float(v1.z);
-  const int rx0 = (int)(v3.x & 0xffffu), ry0 = (int)(v3.x >> 16);
-  const int rx1 = (int)(v3.y & 0xffffu), ry1 = (int)(v3.y >> 16);
-  const bool conic_ok = ca > 0.0f && cc > 0.0f;
-  // the edge minimisers' slopes, once per pair: on a vertical edge at dx = ex the
-  // convex q is least at dy = -cb2 ex / (2 cc) (horizontal edges alike); any
-  // rounding of this location only moves the probe along the edge, which can
-  // raise q by at most cc * (location error)^2 -- far below the margin
-  const float sy = conic_ok ? -cb2 / (2.0f * cc) : 0.0f, sx = conic_ok ? -cb2 / (2.0f * ca) : 0.0f;
-  uint32_t m = 0;
-#pragma unroll
-  for (int w = 0; w < 4; w++) {
-    const int bx0 = X0 + (w & 1) * 8, by0 = Y0 + (w >> 1) * 8;
-    const int bx1 = bx0 + 7, by1 = by0 + 7;
-    if (rx1 < bx0 || rx0 > bx1 || ry1 < by0 || ry0 > by1) continue;  // rectangle cull
-    if (!conic_ok) { m |= 1u << w; continue; }
-    const float dx0 = (float)bx0 - u, dx1 = (float)bx1 - u;
-    const float dy0 = (float)by0 - v, dy1 = (float)by1 - v;
-    const bool ox = dx0 > 0.0f || dx1 < 0.0f, oy = dy0 > 0.0f || dy1 < 0.0f;
-    float qmin = 0.0f;
-    if (ox || oy) {
-      qmin = INFINITY;
-      if (ox) {  // near vertical edge, dy clamped to the block
-        const float ex = dx0 > 0.0f ? dx0 : dx1;
-        const float dy = fminf(fmaxf(sy * ex, dy0), dy1);
-        qmin = fminf(qmin, ca * ex * ex + cb2 * ex * dy + cc * dy * dy);
-      }
-      if (oy) {  // near horizontal edge
-        const float ey = dy0 > 0.0f ? dy0 : dy1;
-        const float dx = fminf(fmaxf(sx * ey, dx0), dx1);
-        qmin = fminf(qmin, ca * dx * dx + cb2 * dx * ey + cc * ey * ey);
-      }
-    }
-    const float DX = fmaxf(fabsf(dx0), fabsf(dx1)), DY = fmaxf(fabsf(dy0), fabsf(dy1));
-    const float margin = 0.01f + 2e-5f * (ca * DX * DX + fabsf(cb2) * DX * DY + cc * DY * DY);
-    if (!(qmin > k2 + margin)) m |= 1u << w;  // NaN keeps the block
-  }
-  return m;
-}
-
-// Pair `pos` of the sorted order: its Gaussian index and the pair-ordered
-// record payload with the pair's block cull mask in word 14.
-__device__ __forceinline__ void emit_pair(unsigned long long key, int64_t pos,
-                                          const uint4 *__restrict__ rec4,
-                                          uint32_t *__restrict__ pair_gid,
-                                          uint4 *__restrict__ pair_rec, int X0, int Y0) {
+// Pair entry `pos` of the sorted order: the Gaussian index (key low word) in
+// bits 0-27 and the pair's 8x8-block cull mask (block_mask, from the record's
+// words 0-7 and 12-13) in bits 28-31 -- what the renderers need per entry,
+// so they gather the record itself from rec and compute nothing per entry.
+__device__ __forceinline__ void emit_entry(unsigned long long key, int64_t pos,
+                                           const uint4 *__restrict__ rec4,
+                                           uint32_t *__restrict__ pair_gid, int X0, int Y0) {
   const uint32_t gid = (uint32_t)(key & 0xffffffffull);
-  pair_gid[pos] = gid;
-  const uint4 *src = rec4 + (int64_t)gid * 4;
-  const uint4 v0 = src[0], v1 = src[1], v2 = src[2];
-  uint4 v3 = src[3];
-  v3.z = block_mask(v0, v1, v3, X0, Y0);
-  uint4 *dst = pair_rec + pos * 4;
-  dst[0] = v0; dst[1] = v1; dst[2] = v2; dst[3] = v3;
+  const uint4 *r = rec4 + (int64_t)gid * 4;
+  pair_gid[pos] = gid | (block_mask(r[0], r[1], r[3], X0, Y0) << kPairMaskShift);
 }
 
 __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len, uint32_t start,
                                             int tid, int nthr, const uint4 *__restrict__ rec4,
-                                            uint32_t *__restrict__ pair_gid,
-                                            uint4 *__restrict__ pair_rec, int X0, int Y0) {
-  for (int k = tid; k < len; k += nthr) emit_pair(a[k], (int64_t)start + k, rec4, pair_gid,
-                                                  pair_rec, X0, Y0);
+                                            uint32_t *__restrict__ pair_gid, int X0, int Y0) {
+  for (int k = tid; k < len; k += nthr) emit_entry(a[k], (int64_t)start + k, rec4, pair_gid, X0, Y0);
 }
 
 // Register-resident bitonic sort of up to 2 * kSortThreads = 256 keys: thread t
@@ -282,8 +222,8 @@ constexpr unsigned long long kRangeP = 1ull << 63;
 
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int64_t T, uint32_t *__restrict__ range, int64_t *__restrict__ n_pairs, BinWs w,
-    int64_t cap, const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid,
-    uint4 *__restrict__ pair_rec, int tiles_x, int64_t tile0) {
+    int64_t cap, const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid, int tiles_x,
+    int64_t tile0) {
   __shared__ __align__(16) unsigned long long sk[kCtaCap];
   __shared__ uint32_t fill, s_start, s_end;
   const int64_t tile = tile0 + blockIdx.x;
@@ -356,8 +296,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   if (len == 0) return;
   if (reg_path) {  // sorted above; len < cnt_t only beyond the capacity (reported)
     const int t = threadIdx.x;
-    if (2 * t < len) emit_pair(x0, (int64_t)start + 2 * t, rec4, pair_gid, pair_rec, X0, Y0);
-    if (2 * t + 1 < len) emit_pair(x1, (int64_t)start + 2 * t + 1, rec4, pair_gid, pair_rec, X0, Y0);
+    if (2 * t < len) emit_entry(x0, (int64_t)start + 2 * t, rec4, pair_gid, X0, Y0);
+    if (2 * t + 1 < len) emit_entry(x1, (int64_t)start + 2 * t + 1, rec4, pair_gid, X0, Y0);
     return;
   }
   unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
@@ -381,25 +321,23 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   } else {
     bitonic_sort(a, len, threadIdx.x, kSortThreads, [] { __syncthreads(); });
   }
-  emit_sorted(a, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, pair_rec, X0, Y0);
+  emit_sorted(a, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, X0, Y0);
 }
 
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
-                              const void *rec, uint32_t *pair_gid, void *pair_rec,
+                              const void *rec, uint32_t *pair_gid,
                               uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,
                               int64_t tile0, int64_t ntiles) {
   if (ntiles < 0) ntiles = T - tile0;
   if (ntiles <= 0) return cudaSuccess;
   k_sort_tiles<<<(unsigned)ntiles, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
-                                                         static_cast<const uint4 *>(rec), pair_gid,
-                                                         static_cast<uint4 *>(pair_rec), tiles_x,
-                                                         tile0);
+                                                         static_cast<const uint4 *>(rec),
+                                                         pair_gid, tiles_x, tile0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
-                       int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid,
-                       void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                       int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                        cudaStream_t s) {
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
@@ -419,7 +357,7 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
                                                       tile_active, w);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
+  return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range,
                            n_pairs_dev, s);
 }
 

@@ -26,7 +26,7 @@ cudaError_t bin_reset(const BinWs &w, int64_t T, cudaStream_t s);
 // (tiles [tile0, tile0 + ntiles) only, ntiles < 0 = to the end: the tile-range
 // look-back never waits, so any split of the tiles into launches is valid)
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
-                              const void *rec, uint32_t *pair_gid, void *pair_rec,
+                              const void *rec, uint32_t *pair_gid,
                               uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,
                               int64_t tile0 = 0, int64_t ntiles = -1);
 

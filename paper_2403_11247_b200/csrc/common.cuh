@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include "csplat.h"
+#include <cuda.h>
 
 namespace csplat {
 
@@ -149,6 +150,51 @@ __device__ __forceinline__ void tma_load_1d(void *dst_smem, const void *src_gmem
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// generic-proxy shared-memory writes ordered before later async-proxy (TMA)
+// accesses of the same locations
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+
+// pair_gid entries: the Gaussian index in bits 0-27, the pair's 8x8-block
+// cull mask (block_mask) in bits 28-31 (csplat.h, csplat_bin_tiles)
+constexpr int kPairMaskShift = 28;
+constexpr uint32_t kPairGidMask = (1u << kPairMaskShift) - 1u;
+
+// The record table as a 2-D TMA tensor for tile::gather4 loads: rows of 16
+// u32 words (one 64-byte record per Gaussian), 2^28 rows (every index a pair
+// entry can name; the entries only name Gaussians < n), box = 16 x 1.  Encoded
+// on the host per call (rec_tensor_map, record_tmap.cu).
+cudaError_t rec_tensor_map(const void *rec, CUtensorMap *out);
+
+// The renderers' producer warp, one batch of a tile's list into ring slot
+// `slot` (128-byte aligned): lane l holds entry l (Gaussian index | block mask
+// << 28) and stores its mask into msk[l]; lanes j < ceil(cnt / 4) each gather
+// the records of entries 4j .. 4j+3 with one tile::gather4 TMA load (4 rows x
+// 64 B, rows past the batch repeat its last entry); all 32 lanes arrive on
+// `full` (init count 32; lane 0 arms it with the bytes), so the phase
+// completes once every mask is stored and every record has landed.
+__device__ __forceinline__ void gather_batch(float4 *slot, uint32_t *msk, const CUtensorMap *tmap,
+                                             uint32_t entry, int lane, int cnt, uint64_t *full) {
+  const int last = cnt - 1;
+  const uint32_t gid = entry & kPairGidMask;
+  uint32_t r[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) r[q] = __shfl_sync(0xffffffffu, gid, min(4 * (lane & 7) + q, last));
+  const int nreq = (cnt + 3) >> 2;
+  if (lane < cnt) msk[lane] = entry >> kPairMaskShift;
+  if (lane < nreq) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(slot + lane * 16)),
+        "l"(tmap), "r"(0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(smem_u32(full))
+        : "memory");
+  }
+  if (lane == 0) mbar_arrive_expect_tx(full, (uint32_t)nreq * 4u * CSPLAT_RECORD_BYTES);
+  else mbar_arrive(full);
 }
 
 __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
@@ -310,10 +356,64 @@ cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
                                const csplat_camera &cam, const csplat_view &view,
                                const float *view_dev, float tau, float dilation, void *rec,
                                int32_t *count, int64_t cap, const uint32_t *tile_active,
-                               uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                               uint32_t *pair_gid, uint32_t *tile_range,
                                int64_t *n_pairs_dev, void *ws, cudaStream_t s);
 
 size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam);
+// Cull hint for the renderers: bit w (w = 0..3, x half = w & 1, y half = w >> 1)
+// of a (tile, Gaussian) pair's block mask is set unless the Gaussian provably has
+// alpha < 1/255 over the whole 8x8 pixel block w of the tile, i.e. unless the
+// minimum of q(dx, dy) = ca dx^2 + (2cb) dx dy + cc dy^2 over the block's
+// rectangle exceeds k^2 by more than a rounding margin (the renderers skip a
+// pixel when q > k^2).  The minimum of the convex q over a box
+// that does not contain the centre lies on a box edge that faces the centre,
+// so at most two 1-D clamped minimisations per block.  The margin covers the
+// float32 evaluation of q at any pixel of the block, so a
+// cleared bit never skips a pixel the per-pixel test would have composited.
+__device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1, const uint4 &v3,
+                                               int X0, int Y0) {
+  const float u = __uint_as_float(v0.x), v = __uint_as_float(v0.y);
+  const float ca = __uint_as_float(v0.z), cb2 = __uint_as_float(v0.w);
+  const float cc = __uint_as_float(v1.x), k2 = __uint_as_float(v1.z);
+  const int rx0 = (int)(v3.x & 0xffffu), ry0 = (int)(v3.x >> 16);
+  const int rx1 = (int)(v3.y & 0xffffu), ry1 = (int)(v3.y >> 16);
+  const bool conic_ok = ca > 0.0f && cc > 0.0f;
+  // the edge minimisers' slopes, once per pair: on a vertical edge at dx = ex the
+  // convex q is least at dy = -cb2 ex / (2 cc) (horizontal edges alike); any
+  // rounding of this location only moves the probe along the edge, which can
+  // raise q by at most cc * (location error)^2 -- far below the margin
+  const float sy = conic_ok ? -cb2 / (2.0f * cc) : 0.0f, sx = conic_ok ? -cb2 / (2.0f * ca) : 0.0f;
+  uint32_t m = 0;
+#pragma unroll
+  for (int w = 0; w < 4; w++) {
+    const int bx0 = X0 + (w & 1) * 8, by0 = Y0 + (w >> 1) * 8;
+    const int bx1 = bx0 + 7, by1 = by0 + 7;
+    if (rx1 < bx0 || rx0 > bx1 || ry1 < by0 || ry0 > by1) continue;  // rectangle cull
+    if (!conic_ok) { m |= 1u << w; continue; }
+    const float dx0 = (float)bx0 - u, dx1 = (float)bx1 - u;
+    const float dy0 = (float)by0 - v, dy1 = (float)by1 - v;
+    const bool ox = dx0 > 0.0f || dx1 < 0.0f, oy = dy0 > 0.0f || dy1 < 0.0f;
+    float qmin = 0.0f;
+    if (ox || oy) {
+      qmin = INFINITY;
+      if (ox) {  // near vertical edge, dy clamped to the block
+        const float ex = dx0 > 0.0f ? dx0 : dx1;
+        const float dy = fminf(fmaxf(sy * ex, dy0), dy1);
+        qmin = fminf(qmin, ca * ex * ex + cb2 * ex * dy + cc * dy * dy);
+      }
+      if (oy) {  // near horizontal edge
+        const float ey = dy0 > 0.0f ? dy0 : dy1;
+        const float dx = fminf(fmaxf(sx * ey, dx0), dx1);
+        qmin = fminf(qmin, ca * dx * dx + cb2 * dx * ey + cc * ey * ey);
+      }
+    }
+    const float DX = fmaxf(fabsf(dx0), fabsf(dx1)), DY = fmaxf(fabsf(dy0), fabsf(dy1));
+    const float margin = 0.01f + 2e-5f * (ca * DX * DX + fabsf(cb2) * DX * DY + cc * DY * DY);
+    if (!(qmin > k2 + margin)) m |= 1u << w;  // NaN keeps the block
+  }
+  return m;
+}
+
 // NEXT-2 (rvq_update.cu): the STE code gradient and the Fig 4 stage init
 cudaError_t launch_rvq_code_grad(const float *g, int64_t n, const int64_t *n_dev, int d, int L,
                                  int P, const void *idx, int idx_bytes, float *dcodes,
@@ -324,8 +424,7 @@ cudaError_t launch_rvq_init_stage(const float *x, int64_t n, int d, float *codes
 // the calling thread's fork streams / events of the composed calls (project.cu)
 void release_thread_fork_resources();
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
-                       int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid,
-                       void *pair_rec, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                       int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                        cudaStream_t s);
 
 cudaError_t launch_pose_step(float *view_dev, const float *pose_grad, float lr_rot,
@@ -342,7 +441,8 @@ cudaError_t launch_ba_loss(const float *color, const float *depth, const float *
                            cudaStream_t s);
 
 // tiles [tile0, tile0 + ntiles) only (ntiles < 0: to the last tile)
-cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
+cudaError_t launch_render_fwd(const void *rec, const uint32_t *pair_gid,
+                              const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
                               float *depth, float *sil, float *t_final, int32_t *n_contrib,
                               cudaStream_t s, int tile0 = 0, int ntiles = -1);
@@ -354,7 +454,7 @@ cudaError_t launch_project_bin_render(const csplat_gaussians &g, const DecodeArg
                                       const csplat_camera &cam, const csplat_view &view,
                                       const float *view_dev, float tau, float dilation,
                                       const csplat_params &prm, void *rec, int32_t *count,
-                                      int64_t cap, uint32_t *pair_gid, void *pair_rec,
+                                      int64_t cap, uint32_t *pair_gid,
                                       uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                                       float *color, float *depth, float *sil, float *t_final,
                                       int32_t *n_contrib, cudaStream_t s);
@@ -364,8 +464,8 @@ struct TrackingLoss;
 cudaError_t bwd_prep(const csplat_gaussians &g, uint32_t flags, const csplat_grads &out,
                      void *ws, const TrackingLoss *loss, cudaStream_t s);
 cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss *loss,
-                                    const csplat_params &prm, const void *pair_rec,
-                                    const uint32_t *tile_range, const float *t_final,
+                                    const csplat_params &prm, const void *rec,
+                                    const uint32_t *pair_gid, const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
                                     cudaStream_t s, int tile0, int ntiles);
@@ -384,7 +484,7 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
                                const csplat_camera &cam, const csplat_view &view,
                                const float *view_dev, float tau, float dilation,
                                const csplat_params &prm, void *rec, int32_t *count, int64_t cap,
-                               uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                               uint32_t *pair_gid, uint32_t *tile_range,
                                int64_t *n_pairs_dev, void *ws, float *color, float *depth,
                                float *sil, float *t_final, int32_t *n_contrib,
                                const StepBwd *bwd, cudaStream_t s);
@@ -404,7 +504,7 @@ cudaError_t launch_count_valid(const float *obs_depth, int64_t HW, unsigned long
 cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                               const csplat_camera &cam, const csplat_view &view,
                               const float *view_dev, const TrackingLoss *loss,
-                              const csplat_params &prm, const void *rec, const void *pair_rec,
+                              const csplat_params &prm, const void *rec, const uint32_t *pair_gid,
                               const uint32_t *tile_range, const float *t_final,
                               const int32_t *n_contrib, const float *d_color, const float *d_depth,
                               const float *d_sil, uint32_t flags, const csplat_grads &out,

@@ -246,7 +246,7 @@ cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
                                const csplat_camera &cam, const csplat_view &view,
                                const float *view_dev, float tau, float dilation, void *rec,
                                int32_t *count, int64_t cap, const uint32_t *tile_active,
-                               uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                               uint32_t *pair_gid, uint32_t *tile_range,
                                int64_t *n_pairs_dev, void *ws, cudaStream_t s) {
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
@@ -256,7 +256,7 @@ cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
   e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
                           ci.tiles_x, cap, tile_active, s);
   if (e != cudaSuccess) return e;
-  return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
+  return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range,
                            n_pairs_dev, s);
 }
 
@@ -323,7 +323,7 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
                                const csplat_camera &cam, const csplat_view &view,
                                const float *view_dev, float tau, float dilation,
                                const csplat_params &prm, void *rec, int32_t *count, int64_t cap,
-                               uint32_t *pair_gid, void *pair_rec, uint32_t *tile_range,
+                               uint32_t *pair_gid, uint32_t *tile_range,
                                int64_t *n_pairs_dev, void *ws, float *color, float *depth,
                                float *sil, float *t_final, int32_t *n_contrib,
                                const StepBwd *bwd, cudaStream_t s) {
@@ -351,13 +351,13 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
     cudaStream_t sc = r->st[c];
     if ((e = cudaStreamWaitEvent(sc, r->start, 0)) != cudaSuccess) break;
     forked = c + 1;
-    e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, pair_rec, tile_range,
+    e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range,
                           n_pairs_dev, sc, t0, nt);
     if (e == cudaSuccess)
-      e = launch_render_fwd(pair_rec, tile_range, cam, prm, color, depth, sil, t_final,
+      e = launch_render_fwd(rec, pair_gid, tile_range, cam, prm, color, depth, sil, t_final,
                             n_contrib, sc, (int)t0, (int)nt);
     if (e == cudaSuccess && bwd)
-      e = launch_render_bwd_tiles(cam, bwd->loss, prm, pair_rec, tile_range, t_final, n_contrib,
+      e = launch_render_bwd_tiles(cam, bwd->loss, prm, rec, pair_gid, tile_range, t_final, n_contrib,
                                   bwd->d_color, bwd->d_depth, bwd->d_sil, bwd->ws, sc, (int)t0,
                                   (int)nt);
   }
@@ -379,12 +379,12 @@ cudaError_t launch_project_bin_render(const csplat_gaussians &g, const DecodeArg
                                       const csplat_camera &cam, const csplat_view &view,
                                       const float *view_dev, float tau, float dilation,
                                       const csplat_params &prm, void *rec, int32_t *count,
-                                      int64_t cap, uint32_t *pair_gid, void *pair_rec,
+                                      int64_t cap, uint32_t *pair_gid,
                                       uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                                       float *color, float *depth, float *sil, float *t_final,
                                       int32_t *n_contrib, cudaStream_t s) {
   return launch_render_step(g, dec, cam, view, view_dev, tau, dilation, prm, rec, count, cap,
-                            pair_gid, pair_rec, tile_range, n_pairs_dev, ws, color, depth, sil,
+                            pair_gid, tile_range, n_pairs_dev, ws, color, depth, sil,
                             t_final, n_contrib, nullptr, s);
 }
 

@@ -48,6 +48,7 @@ struct BwdSmem {
   float4 red[kCW][kG * kV][8];          // per-warp rows of 32 lane partials
   float part[kBS][kCW][kBB][kPartW];    // per-slot, per-warp sums per batch entry
   uint64_t full[kBS], empty[kBS];
+  uint32_t msk[kBS][kBB];               // the batch entries' 8x8-block cull masks
   uint32_t pmask[kBS][kCW];             // bit e: warp w wrote part[slot][w][e]
   int wmax[kCW];
 };
@@ -145,7 +146,8 @@ struct LossArgs {
 
 template <bool LOSS>
 __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
-    const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
+    const __grid_constant__ CUtensorMap tmap, const uint32_t *__restrict__ pair_gid,
+    const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, const float *__restrict__ t_final,
     const int32_t *__restrict__ n_contrib, const float *__restrict__ dC,
     const float *__restrict__ dD, const float *__restrict__ dS, float *__restrict__ acc,
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
   if (!producer && lane == 0) sm.wmax[wid] = wmax;
   if (tid == kCW * 32) {
     for (int s = 0; s < kBS; s++) {
-      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.full[s], 32);  // the producer warp's 32 lanes (+ the batch's TMA bytes)
       mbar_init(&sm.empty[s], kCW);
     }
     fence_mbar_init();
@@ -254,6 +256,14 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
         red_add_v4(dst + 8, s2.x, s2.y, 0.f, 0.f);
       }
     };
+    // replay batch k = list batch b = nb - 1 - k: lane l takes list entry
+    // b*kBB + l (pair_gid: Gaussian index | block mask << 28, loaded one batch
+    // ahead), stores its mask into msk[s] and gathers its record with one
+    // 64-byte TMA bulk copy (gather_batch)
+    auto entry_of = [&](int k) {
+      return lane < batch_cnt(k) ? pair_gid[start + (nb - 1 - k) * kBB + lane] : 0u;
+    };
+    uint32_t entry = nb > 0 ? entry_of(0) : 0u;
     for (int k = 0; k < nb; k++) {
       const int s = k % kBS;
       if (k >= kBS) {  // slot s held replay batch k - kBS: wait for all pixel warps
@@ -261,14 +271,9 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
         flush(k - kBS, s);
         __syncwarp();  // every lane has read the slot's gids before it is overwritten
       }
-      if (lane == 0) {
-        const int b = nb - 1 - k;
-        const uint32_t bytes = (uint32_t)batch_cnt(k) * CSPLAT_RECORD_BYTES;
-        mbar_arrive_expect_tx(&sm.full[s], bytes);
-        tma_load_1d(&sm.buf[s][0], pair_rec + ((int64_t)start + (int64_t)b * kBB) * 4, bytes,
-                    &sm.full[s]);
-      }
-      __syncwarp();
+      const uint32_t e = entry;
+      if (k + 1 < nb) entry = entry_of(k + 1);
+      gather_batch(&sm.buf[s][0], sm.msk[s], &tmap, e, lane, batch_cnt(k), &sm.full[s]);
     }
     for (int k = max(0, nb - kBS); k < nb; k++) {  // drain the last slots
       const int s = k % kBS;
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
       uint32_t ents = 0;
       // the batch's entries this warp replays, one ballot: lane l tests entry l's
       // block mask (payload word 14, bin.cu) and replay range (j < wmax)
-      const uint32_t bml = lane < cnt ? __float_as_uint(rb[lane * 4 + 3].z) : 0u;
+      const uint32_t bml = lane < cnt ? sm.msk[s][lane] : 0u;
       uint32_t todo = __ballot_sync(0xffffffffu, ((bml >> blk) & 1u) && b * kBB + lane < wmax);
       while (todo) {  // back to front
         int e;  // the highest set bit (bfind = 31 - clz in one instruction)
@@ -380,8 +385,8 @@ cudaError_t bwd_prep(const csplat_gaussians &g, uint32_t flags, const csplat_gra
 // end); the per-Gaussian accumulation is by atomics, so tile chunks may run in
 // any order or concurrently
 cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss *loss,
-                                    const csplat_params &prm, const void *pair_rec,
-                                    const uint32_t *tile_range, const float *t_final,
+                                    const csplat_params &prm, const void *rec,
+                                    const uint32_t *pair_gid, const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
                                     cudaStream_t s, int tile0, int ntiles) {
@@ -407,6 +412,8 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
   const int T = ci.tiles_x * ci.tiles_y;
   if (ntiles < 0) ntiles = T - tile0;
   if (ntiles <= 0) return cudaSuccess;
+  CUtensorMap tmap;
+  if ((e = rec_tensor_map(rec, &tmap)) != cudaSuccess) return e;
   LossArgs la{};
   if (loss) {
     la.color = loss->color; la.depth = loss->depth; la.sil = loss->sil;
@@ -415,11 +422,11 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
     la.inv_n = 1.0f / (float)((int64_t)ci.W * ci.H);
     la.loss3 = loss->loss3;
     k_render_bwd<true><<<ntiles, kBwdThreads, smem, s>>>(
-        static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
+        tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
         t_final, n_contrib, nullptr, nullptr, nullptr, acc, la, tile0);
   } else {
     k_render_bwd<false><<<ntiles, kBwdThreads, smem, s>>>(
-        static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
+        tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
         t_final, n_contrib, d_color, d_depth, d_sil, acc, la, tile0);
   }
   return cudaGetLastError();
@@ -428,14 +435,14 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
 cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                               const csplat_camera &cam, const csplat_view &view,
                               const float *view_dev, const TrackingLoss *loss,
-                              const csplat_params &prm, const void *rec, const void *pair_rec,
+                              const csplat_params &prm, const void *rec, const uint32_t *pair_gid,
                               const uint32_t *tile_range, const float *t_final,
                               const int32_t *n_contrib, const float *d_color, const float *d_depth,
                               const float *d_sil, uint32_t flags, const csplat_grads &out,
                               void *ws, cudaStream_t s) {
   cudaError_t e = bwd_prep(g, flags, out, ws, loss, s);
   if (e != cudaSuccess) return e;
-  e = launch_render_bwd_tiles(cam, loss, prm, pair_rec, tile_range, t_final, n_contrib, d_color,
+  e = launch_render_bwd_tiles(cam, loss, prm, rec, pair_gid, tile_range, t_final, n_contrib, d_color,
                               d_depth, d_sil, ws, s, 0, -1);
   if (e != cudaSuccess || g.n == 0 || (flags & CSPLAT_SKIP_CHAIN)) return e;
   return launch_chain(g, dec, cam, view, view_dev, prm, rec, static_cast<float *>(ws), flags,

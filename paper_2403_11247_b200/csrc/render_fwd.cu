@@ -76,12 +76,14 @@ __device__ __forceinline__ void composite_pair(PixState &p0, PixState &p1, bool 
 // producer ends the stream by completing the next full[] phase without data
 // (end_b), and every pixel warp leaves at that batch.
 __global__ void __launch_bounds__((kPW + 1) * 32) k_render_fwd(
-    const float4 *__restrict__ pair_rec, const uint32_t *__restrict__ range, int W, int H,
+    const __grid_constant__ CUtensorMap tmap, const uint32_t *__restrict__ pair_gid,
+    const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, float tmin, float *__restrict__ color, float *__restrict__ depth,
     float *__restrict__ sil, float *__restrict__ t_final, int32_t *__restrict__ n_contrib,
     int tile0) {
   __shared__ __align__(128) float4 buf[kStages][kBatch * 4];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ uint32_t msk[kStages][kBatch];  // the entries' 8x8-block cull masks
   __shared__ int done_cnt, end_b;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int tile = tile0 + (int)blockIdx.x;
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__((kPW + 1) * 32) k_render_fwd(
 
   if (tid == 0) {
     for (int s = 0; s < kStages; s++) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 32);  // the producer warp's 32 lanes (+ the batch's TMA bytes)
       mbar_init(&empty[s], kPW);
     }
     done_cnt = 0;
@@ -101,22 +103,24 @@ __global__ void __launch_bounds__((kPW + 1) * 32) k_render_fwd(
   }
   __syncthreads();
 
-  if (wid == kPW) {  // ---- producer warp (lane 0)
-    if (lane == 0) {
-      for (int b = 0; b < nb; b++) {
-        const int s = b % kStages;
-        if (b >= kStages) mbar_wait_sleep(&empty[s], (uint32_t)((b / kStages) - 1) & 1u);
-        if (*(volatile int *)&done_cnt == kPW) {  // every pixel terminated: end the stream
-          end_b = b;
-          mbar_arrive(&full[s]);
-          break;
-        }
-        const int cnt = min(kBatch, len - b * kBatch);
-        const uint32_t bytes = (uint32_t)cnt * CSPLAT_RECORD_BYTES;
-        mbar_arrive_expect_tx(&full[s], bytes);
-        tma_load_1d(&buf[s][0], pair_rec + ((int64_t)start + (int64_t)b * kBatch) * 4, bytes,
-                    &full[s]);
+  if (wid == kPW) {  // ---- producer warp
+    // batch b: lane l takes list entry b*kBatch + l (pair_gid: Gaussian index |
+    // block mask << 28, loaded one batch ahead), stores its mask into msk[s]
+    // and gathers its record with one 64-byte TMA bulk copy (gather_batch)
+    uint32_t entry = lane < len ? pair_gid[start + lane] : 0u;
+    for (int b = 0; b < nb; b++) {
+      const int s = b % kStages;
+      if (b >= kStages) mbar_wait_sleep(&empty[s], (uint32_t)((b / kStages) - 1) & 1u);
+      // every pixel terminated: end the stream (one lane reads, all agree)
+      if (__shfl_sync(0xffffffffu, lane == 0 ? *(volatile int *)&done_cnt : 0, 0) == kPW) {
+        if (lane == 0) end_b = b;
+        mbar_arrive(&full[s]);  // 32 arrivals, no bytes: the phase completes empty
+        break;
       }
+      const int cnt = min(kBatch, len - b * kBatch);
+      const uint32_t e = entry;
+      if (b * kBatch + lane + kBatch < len) entry = pair_gid[start + b * kBatch + lane + kBatch];
+      gather_batch(&buf[s][0], msk[s], &tmap, e, lane, cnt, &full[s]);
     }
     return;
   }
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__((kPW + 1) * 32) k_render_fwd(
       const int cnt = min(kBatch, len - b * kBatch);
       // the batch's entries this warp composites, one ballot: lane l tests entry
       // l's 8x8-block mask (payload word 14, bin.cu)
-      const bool mine = lane < cnt && ((__float_as_uint(rb[lane * 4 + 3].z) >> wid) & 1u);
+      const bool mine = lane < cnt && ((msk[s][lane] >> wid) & 1u);
       uint32_t todo = __ballot_sync(0xffffffffu, mine);
       while (todo) {  // front to back
         const int e = __ffs(todo) - 1;
@@ -186,7 +190,8 @@ __global__ void __launch_bounds__((kPW + 1) * 32) k_render_fwd(
   }
 }
 
-cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
+cudaError_t launch_render_fwd(const void *rec, const uint32_t *pair_gid,
+                              const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
                               float *depth, float *sil, float *t_final, int32_t *n_contrib,
                               cudaStream_t s, int tile0, int ntiles) {
@@ -194,8 +199,11 @@ cudaError_t launch_render_fwd(const void *pair_rec, const uint32_t *tile_range,
   const int T = ci.tiles_x * ci.tiles_y;
   if (ntiles < 0) ntiles = T - tile0;
   if (ntiles <= 0) return cudaSuccess;
+  CUtensorMap tmap;
+  cudaError_t e = rec_tensor_map(rec, &tmap);
+  if (e != cudaSuccess) return e;
   k_render_fwd<<<ntiles, (kPW + 1) * 32, 0, s>>>(
-      static_cast<const float4 *>(pair_rec), tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
+      tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
       prm.t_min, color, depth, sil, t_final, n_contrib, tile0);
   return cudaGetLastError();
 }

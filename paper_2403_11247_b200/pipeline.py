@@ -83,7 +83,6 @@ class RenderStep:
     def _alloc_pairs(self, cap):
         self.capacity = cap
         self.pair_gid = torch.empty(cap, dtype=torch.int32, device=self.dev)
-        self.pair_rec = torch.empty((cap, 16), dtype=torch.int32, device=self.dev)
         self.ws_bin = torch.empty(cs.workspace_bytes(cs.OP_BIN_TILES, self.n, cap, self.cam),
                                   dtype=torch.uint8, device=self.dev)
 
@@ -169,7 +168,7 @@ class RenderStep:
         if FUSED_BIN and not sync_probe:  # the bucket pass inside the projection kernel
             cs.project_bin(g, self.cam, view, self.capacity, self.prm, self.cb, rec=self.rec,
                            count=self.count, ws=self.ws_bin,
-                           out=dict(pair_gid=self.pair_gid, pair_rec=self.pair_rec,
+                           out=dict(pair_gid=self.pair_gid,
                                     tile_range=self.tile_range, n_pairs_dev=self.n_pairs),
                            sync=False, tile_active=tile_active)
             return
@@ -179,17 +178,17 @@ class RenderStep:
             if big > self.capacity:
                 self._alloc_pairs(big)
         cs.bin_tiles(self.rec, self.count, self.cam, self.capacity, ws=self.ws_bin,
-                     out=dict(pair_gid=self.pair_gid, pair_rec=self.pair_rec,
+                     out=dict(pair_gid=self.pair_gid,
                               tile_range=self.tile_range, n_pairs_dev=self.n_pairs),
                      sync=sync_probe, tile_active=tile_active)
 
     def forward(self):
-        cs.render_fwd(self.pair_rec, self.tile_range, self.cam, self.prm, out=self.img)
+        cs.render_fwd(self.rec, self.pair_gid, self.tile_range, self.cam, self.prm, out=self.img)
 
     def backward(self, view, flags=None, pose=None):
         dC, dD, dS = self.upstream
         grads = self.grads if pose is None else dict(self.grads, pose=pose)
-        cs.render_bwd(self.pruned, self.cam, view, self.rec, self.pair_rec, self.tile_range,
+        cs.render_bwd(self.pruned, self.cam, view, self.rec, self.pair_gid, self.tile_range,
                       self.img["t_final"], self.img["n_contrib"], dC, dD, dS, self.prm, self.cb,
                       self.flags if flags is None else flags, grads=grads, ws=self.ws_bwd)
 
@@ -204,7 +203,7 @@ class RenderStep:
             dC, dD, dS = self.upstream
             cs.render_step(self.pruned, self.cam, view, self.capacity, dC, dD, dS, self.prm,
                            self.cb, self.flags, rec=self.rec, count=self.count, ws=self.ws_bin,
-                           out=dict(pair_gid=self.pair_gid, pair_rec=self.pair_rec,
+                           out=dict(pair_gid=self.pair_gid,
                                     tile_range=self.tile_range, n_pairs_dev=self.n_pairs),
                            img=self.img, grads=self.grads, ws_bwd=self.ws_bwd)
             return
@@ -217,7 +216,7 @@ class RenderStep:
         if FUSED_BIN:
             cs.project_bin_render(self.pruned, self.cam, view, self.capacity, self.prm, self.cb,
                                   rec=self.rec, count=self.count, ws=self.ws_bin,
-                                  out=dict(pair_gid=self.pair_gid, pair_rec=self.pair_rec,
+                                  out=dict(pair_gid=self.pair_gid,
                                            tile_range=self.tile_range, n_pairs_dev=self.n_pairs),
                                   img=self.img)
         else:

@@ -111,13 +111,13 @@ class Tracker:
                              self.n_valid, st.prm, st.cb, flags=cs.POSE_ONLY,
                              lambda_depth=self.lambda_depth, sil_gate=self.sil_gate,
                              rec=st.rec, count=st.count, ws=st.ws_bin,
-                             out=dict(pair_gid=st.pair_gid, pair_rec=st.pair_rec,
+                             out=dict(pair_gid=st.pair_gid,
                                       tile_range=st.tile_range, n_pairs_dev=st.n_pairs),
                              img=st.img, grads=dict(st.grads, pose=self.pose),
                              loss3=self.loss3, ws_bwd=st.ws_bwd)
         else:
             st.project_bin_forward(view_dev)
-            cs.tracking_bwd(g, st.cam, view_dev, st.rec, st.pair_rec, st.tile_range, st.img,
+            cs.tracking_bwd(g, st.cam, view_dev, st.rec, st.pair_gid, st.tile_range, st.img,
                             self.obs_color, self.obs_depth, self.n_valid, st.prm, st.cb,
                             flags=cs.POSE_ONLY, lambda_depth=self.lambda_depth,
                             sil_gate=self.sil_gate, grads=dict(st.grads, pose=self.pose),

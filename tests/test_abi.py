@@ -50,7 +50,8 @@ def test_library_is_sm100a(cs):
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", cs.LIB_PATH], capture_output=True,
                           text=True).stdout
-    assert "UBLKCP" in sass            # TMA bulk copies in the renderer
+    assert "UBLKCP" in sass            # TMA bulk copies (R-VQ codebook staging)
+    assert "UTMALDG.2D.GATHER4" in sass  # the renderers' tile::gather4 record loads
     assert "REDG.E.ADD.F32x4" in sass  # vector reductions in the backward
 
 
@@ -81,7 +82,7 @@ def test_invalid_arguments_rejected_without_device(cs):
     assert L.csplat_project(C.byref(g1), None, C.byref(cam), C.byref(v), C.byref(p),
                             C.c_void_p(8), C.c_void_p(16), None) == 2
     # workspace too small
-    assert L.csplat_bin_tiles(None, None, 0, C.byref(cam), 0, None, None, C.c_void_p(16),
+    assert L.csplat_bin_tiles(None, None, 0, C.byref(cam), 0, None, C.c_void_p(16),
                               C.c_void_p(16), 0, None, 0, None) == 4
     need = L.csplat_workspace_bytes(1, 100, 1000, C.byref(cam))
     assert need >= 8 * 1000
@@ -103,35 +104,35 @@ def test_composed_entry_points_reject_invalid_arguments_without_device(cs):
     gr = cs.Grads(*([None] * 7))
     # bad map / NULL view / NULL tile_range / small workspace
     assert L.csplat_project_bin(C.byref(gbad), None, C.byref(cam), C.byref(v), C.byref(p), x, x,
-                                None, 0, None, None, x, x, 0, x, 1 << 20, None) == 1
+                                None, 0, None, x, x, 0, x, 1 << 20, None) == 1
     assert L.csplat_project_bin(C.byref(g0), None, C.byref(cam), None, C.byref(p), x, x,
-                                None, 0, None, None, x, x, 0, x, 1 << 20, None) == 1
+                                None, 0, None, x, x, 0, x, 1 << 20, None) == 1
     assert L.csplat_project_bin_dv(C.byref(g0), None, C.byref(cam), None, C.byref(p), x, x,
-                                   None, 0, None, None, x, x, 0, x, 1 << 20, None) == 1
+                                   None, 0, None, x, x, 0, x, 1 << 20, None) == 1
     assert L.csplat_project_bin(C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p), x, x,
-                                None, 0, None, None, None, x, 0, x, 1 << 20, None) == 1
+                                None, 0, None, None, x, 0, x, 1 << 20, None) == 1
     assert L.csplat_project_bin(C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p), x, x,
-                                None, 0, None, None, x, x, 0, x, 0, None) == 4
-    # misaligned pair payload
-    assert L.csplat_project_bin(C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p), x, x,
-                                None, 4, x, C.c_void_p(8), x, x, 0, x, 1 << 20, None) == 2
+                                None, 0, None, x, x, 0, x, 0, None) == 4
+    # misaligned record buffer
+    assert L.csplat_project_bin(C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p),
+                                C.c_void_p(8), x, None, 4, x, x, x, 0, x, 1 << 20, None) == 2
     # render: NULL image
     assert L.csplat_project_bin_render(C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p),
-                                       x, x, 0, None, None, x, x, x, 1 << 20, None, x, x, x, x,
+                                       x, x, 0, None, x, x, x, 1 << 20, None, x, x, x, x,
                                        None) == 1
     assert L.csplat_project_bin_render_dv(C.byref(g0), None, C.byref(cam), None, C.byref(p),
-                                          x, x, 0, None, None, x, x, x, 1 << 20, x, x, x, x, x,
+                                          x, x, 0, None, x, x, x, 1 << 20, x, x, x, x, x,
                                           None) == 1
     # step: NULL upstream, POSE_ONLY rejected, small backward workspace
     step = lambda dC, flags, wsb: L.csplat_render_step(  # noqa: E731
-        C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p), x, x, 0, None, None, x, x, x,
+        C.byref(g0), None, C.byref(cam), C.byref(v), C.byref(p), x, x, 0, None, x, x, x,
         1 << 20, x, x, x, x, x, dC, x, x, flags, C.byref(gr), x, wsb, None)
     assert step(None, 0, 1 << 20) == 1
     assert step(x, cs.POSE_ONLY, 1 << 20) == 1
     assert step(x, 0, 0) == 4
     # tracking step: both / neither view, NULL observations
     track = lambda hv, dv, obs: L.csplat_tracking_step(  # noqa: E731
-        C.byref(g0), None, C.byref(cam), hv, dv, C.byref(p), x, x, 0, None, None, x, x, x,
+        C.byref(g0), None, C.byref(cam), hv, dv, C.byref(p), x, x, 0, None, x, x, x,
         1 << 20, x, x, x, x, x, obs, x, x, 1.0, 0.99, cs.POSE_ONLY, C.byref(gr), x, x, 1 << 20,
         None)
     assert track(C.byref(v), x, x) == 1

@@ -72,7 +72,8 @@ def test_ba_patches_and_active_binning(env):
     b = cs.bin_tiles(rec, cnt, cam, capacity=len(gid_o) + 64, tile_active=mask)
     n = int(b["n_pairs_dev"].item())
     assert n == len(keep_gid) and n < len(gid_o)
-    assert np.array_equal(b["pair_gid"][:n].cpu().numpy().view(np.uint32), keep_gid)
+    assert np.array_equal(b["pair_gid"][:n].cpu().numpy().view(np.uint32) & cs.PAIR_GID_MASK,
+                          keep_gid)
     assert np.array_equal(b["tile_range"][:-1].cpu().numpy().view(np.uint32), keep_rng)
 
 
@@ -85,7 +86,7 @@ def test_ba_patch_loss_parity(env):
     g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
     rec, cnt = cs.project(g, cam, view)
     b = cs.bin_tiles(rec, cnt, cam, capacity=int(cnt.sum().item()) + 64)
-    img = cs.render_fwd(b["pair_rec"], b["tile_range"], cam)
+    img = cs.render_fwd(rec, b["pair_gid"], b["tile_range"], cam)
     pt = synth.sample_patches(4, 2, cam["width"], cam["height"], 64 * 60)[0]
     n_rays = 64 * 60                        # this keyframe holds part of the sample
     ocd, odd = torch.tensor(oc, device=dev), torch.tensor(od, device=dev)
@@ -186,7 +187,7 @@ def test_ba_edge_cases(env):
     g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
     rec, cnt = cs.project(g, cam, sc.views[0])
     b = cs.bin_tiles(rec, cnt, cam, capacity=int(cnt.sum().item()) + 64, tile_active=mask)
-    img = cs.render_fwd(b["pair_rec"], b["tile_range"], cam)
+    img = cs.render_fwd(rec, b["pair_gid"], b["tile_range"], cam)
     n_rays = 64 * len(good)
     (dC, dD, dS), l3 = cs.ba_patch_loss(img, ocd, odd, cam, pt, n_rays, nv)
     (rC, rD, rS), rl = orc.ba_patch_loss(img["color"].double().cpu().numpy(),

@@ -34,11 +34,11 @@ def test_empty_map_full_path(env):
     b = cs.bin_tiles(rec, cnt, cam, capacity=0)
     assert int(b["n_pairs_dev"].item()) == 0
     assert not b["tile_range"].any()
-    out = cs.render_fwd(b["pair_rec"], b["tile_range"], cam)
+    out = cs.render_fwd(rec, b["pair_gid"], b["tile_range"], cam)
     assert not out["color"].any() and not out["sil"].any() and not out["n_contrib"].any()
     assert bool((out["t_final"] == 1).all())
     H, W = cam["height"], cam["width"]
-    gr = cs.render_bwd(g, cam, synth.IDENTITY_VIEW, rec, b["pair_rec"], b["tile_range"],
+    gr = cs.render_bwd(g, cam, synth.IDENTITY_VIEW, rec, b["pair_gid"], b["tile_range"],
                        out["t_final"], out["n_contrib"], torch.ones((3, H, W), device=dev),
                        torch.ones((H, W), device=dev), torch.ones((H, W), device=dev))
     assert not gr["pose"].any()
@@ -79,7 +79,7 @@ def test_one_pixel_image(env):
     assert np.array_equal(rec.cpu().numpy().view(np.uint32), rec_o)
     gid_o, rng_o = orc.bin_tiles(rec_o, cnt_o, cam)
     b = cs.bin_tiles(rec, cnt, cam, capacity=16)
-    out = cs.render_fwd(b["pair_rec"], b["tile_range"], cam)
+    out = cs.render_fwd(rec, b["pair_gid"], b["tile_range"], cam)
     fo = orc.render_fwd(rec_o, gid_o, rng_o, cam)
     assert abs(float(out["sil"][0, 0]) - fo["sil"][0, 0]) < 1e-5
 

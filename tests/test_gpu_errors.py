@@ -56,11 +56,11 @@ def test_capacity_overflow_status_word(env, fused):
     assert fits.any() and (~fits).any()
     assert np.array_equal(rng[fits], rng_o[fits])
     assert np.all(rng[~fits, 0] == rng[~fits, 1])         # cut tiles: empty
-    gid = b["pair_gid"].cpu().numpy().view(np.uint32)
+    gid = b["pair_gid"].cpu().numpy().view(np.uint32) & cs.PAIR_GID_MASK
     for t in np.nonzero(fits)[0]:
         s, e = rng_o[t]
         assert np.array_equal(gid[s:e], gid_o[s:e])
-    out = cs.render_fwd(b["pair_rec"], b["tile_range"], cam)
+    out = cs.render_fwd(rec, b["pair_gid"], b["tile_range"], cam)
     fo = orc.render_fwd(rec_o, gid_o, rng_o, cam)
     tx, ty = cs.tiles(cam)
     H, W = cam["height"], cam["width"]
@@ -85,8 +85,7 @@ def test_status_slot_collects_calls(env):
     out = None
     for cap in (total + 100, total // 3, total + 100):       # one overflowing call of three
         out = cs.bin_tiles(rec, cnt, sc.cam, capacity=cap, sync=False, out=None if out is None else
-                           dict(out, pair_gid=torch.empty(cap, dtype=torch.int32, device=dev),
-                                pair_rec=torch.empty((cap, 16), dtype=torch.int32, device=dev)))
+                           dict(out, pair_gid=torch.empty(cap, dtype=torch.int32, device=dev)))
     slot = cs.range_status(out["tile_range"]).cpu().numpy().view(np.uint32)
     assert slot[0] == cs.STATUS_CAPACITY and slot[1] == total
     cs.clear_status(out["tile_range"])

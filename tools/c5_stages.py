@@ -35,7 +35,7 @@ g = st.pruned
 stages = [
     ("project", lambda: cs.project(g, st.cam, v, st.prm, st.cb, rec=st.rec, count=st.count)),
     ("bin_tiles", lambda: cs.bin_tiles(st.rec, st.count, st.cam, st.capacity, ws=st.ws_bin,
-                                       out=dict(pair_gid=st.pair_gid, pair_rec=st.pair_rec,
+                                       out=dict(pair_gid=st.pair_gid,
                                                 tile_range=st.tile_range, n_pairs_dev=st.n_pairs),
                                        sync=False)),
     ("render_fwd", st.forward),

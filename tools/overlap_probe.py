@@ -30,7 +30,7 @@ main = torch.cuda.current_stream(dev)
 
 def bin_a():
     cs.bin_tiles(A.rec, A.count, A.cam, A.capacity, ws=A.ws_bin,
-                 out=dict(pair_gid=A.pair_gid, pair_rec=A.pair_rec, tile_range=A.tile_range,
+                 out=dict(pair_gid=A.pair_gid, tile_range=A.tile_range,
                           n_pairs_dev=A.n_pairs), sync=False)
 
 
