@@ -435,8 +435,9 @@ def bench_c5_window(dev, rank, world, iters=3):
     H, W = sc.cam["height"], sc.cam["width"]
     st.set_upstream(*(torch.tensor(a, device=dev)
                       for a in synth.upstream(np.random.default_rng(5), H, W)))
-    # the local part (the rank's keyframes); the all-reduce is issued below
-    win = gpu_window(st, sc.views, rank=rank, world=world, reduce=False)
+    # the local part (the rank's keyframes, multi-view front: one projection
+    # read per Gaussian for all of them); the all-reduce is issued below
+    win = gpu_window(st, sc.views, rank=rank, world=world, reduce=False, batched=True)
     stream = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(device=dev)
     side.wait_stream(stream)

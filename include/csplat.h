@@ -69,11 +69,16 @@ enum csplat_status {
 #define CSPLAT_SYNC 1u           /* bin_tiles: read n_pairs back, return CAPACITY if it exceeds the capacity */
 #define CSPLAT_POSE_ONLY 2u      /* render_bwd: only the pose gradient (tracking) */
 #define CSPLAT_ACCUMULATE 4u     /* render_bwd: add into the outputs instead of overwriting */
+#define CSPLAT_WS_ZEROED 16u     /* render_bwd: the caller guarantees ws's accumulator is all
+                                    zero (no memset); csplat_chain_views: clear every
+                                    accumulator entry it consumed, so it stays zero */
 #define CSPLAT_SKIP_CHAIN 8u     /* render_bwd: stop after the compositing backward (a7): the
                                     per-Gaussian screen-space gradient is left in ws as
                                     [n][12] float32 (raw moments Sx, Sy, Sxx, Sxy, Syy of
                                     alpha dL/dalpha, dL/do_hat, dL/dz, dL/drgb, 2 pad;
-                                    DESIGN.md §7); `out` is not touched */
+                                    DESIGN.md §7) followed (256-byte aligned) by a
+                                    ceil(n/32)-word bitmap of the Gaussians that got a
+                                    partial; `out` is not touched */
 
 /* Pinhole intrinsics K ("known camera intrinsic K"), image size
  * (1..32767 pixels per side), clip (R21). */
@@ -146,6 +151,49 @@ int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const c
 int csplat_project_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                       const csplat_camera *cam, const float *view_dev, const csplat_params *prm,
                       void *rec, int32_t *count, void *stream);
+
+/* a1 + a2-decode + a3 over n_views views at once (SURVEY §8(b) n_views, §8(e)
+ * "multi-view projection that reads each Gaussian once"): each Gaussian is
+ * read, decoded and its Sigma (Eq 1) formed once, then projected into every
+ * view.  views: host array [n_views]; rec [n_views][n] records, count
+ * [n_views][n]: view v's outputs are bit-identical to csplat_project(views[v]). */
+int csplat_project_views(const csplat_gaussians *g, const csplat_codebook *cb,
+                         const csplat_camera *cam, const csplat_view *views, int32_t n_views,
+                         const csplat_params *prm, void *rec, int32_t *count, void *stream);
+
+/* csplat_project_bin over n_views views at once: the multi-view projection
+ * above with the bucket pass fused in per view, then one batched per-tile
+ * sort of every view.  Per view v (same capacity for every view): rec + v n,
+ * count + v n, pair_gid + v pair_capacity, tile_range + v (T+1) (entry T = the
+ * view's status slot, see csplat_bin_tiles), n_pairs_dev + v, its binning
+ * workspace at ws + v ws_bytes_per_view (>= csplat_workspace_bytes(
+ * CSPLAT_OP_BIN_TILES, n, pair_capacity, cam), a multiple of 256; ws 256-byte
+ * aligned), tile_active (optional) + v ceil(T/32) words.  Outputs bit-identical
+ * to csplat_project_bin per view.  No host synchronisation (overflow: the
+ * status slots). */
+int csplat_project_bin_views(const csplat_gaussians *g, const csplat_codebook *cb,
+                             const csplat_camera *cam, const csplat_view *views, int32_t n_views,
+                             const csplat_params *prm, const uint32_t *tile_active, void *rec,
+                             int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
+                             uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                             size_t ws_bytes_per_view, void *stream);
+
+/* a8 summed over n_views views (the window's ACCUMULATE of csplat_render_bwd's
+ * chain, in one pass): ws = n_views consecutive csplat_render_bwd workspaces
+ * (each csplat_workspace_bytes(CSPLAT_OP_RENDER_BWD, n, 0, cam) bytes, 256-byte
+ * aligned), each left by csplat_render_bwd with CSPLAT_SKIP_CHAIN (the
+ * screen-space accumulator and the bitmap of the Gaussians it reached);
+ * rec [n_views][n] the views' records.  The Gaussian is read and decoded once; the view-dependent
+ * chain (mean, J, Sigma', pose) runs per view that reached it and the rest
+ * (Sigma -> rotation / scale, opacity, STE mask) once on the per-view sum.
+ * out: the 15 gradient planes (overwritten, or added with CSPLAT_ACCUMULATE);
+ * out->pose (optional) = [n_views][6] per-view pose gradients.  With
+ * CSPLAT_WS_ZEROED every consumed accumulator entry is cleared (so csplat_render_bwd
+ * may skip its memset next time).  POSE_ONLY is not supported. */
+int csplat_chain_views(const csplat_gaussians *g, const csplat_codebook *cb,
+                       const csplat_camera *cam, const csplat_view *views, int32_t n_views,
+                       const csplat_params *prm, const void *rec, void *ws, uint32_t flags,
+                       const csplat_grads *out, void *stream);
 
 /* a4 + a5: tile binning and (tile, depth) ordering (R4, R11).
  * Outputs, for n_pairs = sum(count) pairs:

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("CSPLAT_LIB", os.path.join(_PKG, "libcsplat.so"))
 
 TILE = 16
 RECORD_BYTES = 64
-SYNC, POSE_ONLY, ACCUMULATE, SKIP_CHAIN = 1, 2, 4, 8
+SYNC, POSE_ONLY, ACCUMULATE, SKIP_CHAIN, WS_ZEROED = 1, 2, 4, 8, 16
 PAIR_GID_MASK, PAIR_MASK_SHIFT = (1 << 28) - 1, 28  # pair_gid: index | block mask << 28
 STATUS_CAPACITY, STATUS_CODE_INDEX = 1, 2  # device status bits (csplat.h)
 OP_BIN_TILES, OP_RENDER_BWD, OP_MASK_PRUNE = 1, 2, 3
@@ -118,6 +118,10 @@ def lib():
         L.csplat_render_fwd.argtypes = [vp] * 11
         L.csplat_render_bwd.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_rvq_assign.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp]
+        L.csplat_project_views.argtypes = [vp] * 4 + [i32, vp, vp, vp, vp]
+        L.csplat_project_bin_views.argtypes = [vp] * 4 + [i32] + [vp] * 4 + [i64] + \
+            [vp] * 4 + [C.c_size_t, vp]
+        L.csplat_chain_views.argtypes = [vp] * 4 + [i32, vp, vp, vp, u32, vp, vp]
         L.csplat_rvq_code_grad.argtypes = [vp, i64, vp, i32, vp, i32, i32, i32, vp, u32, vp]
         L.csplat_rvq_init_stage.argtypes = [vp, i64, i32, vp, i32, i32, i32, vp, i32, vp, vp]
         L.csplat_mask_prune.argtypes = [vp, vp, C.c_float, C.c_float, vp, vp, vp, vp, vp, vp,
@@ -517,6 +521,79 @@ def render_fwd(rec, pair_gid, tile_range, cam: dict, prm: Params | None = None, 
 
 
 GRAD_SHAPES = dict(mean=3, opacity=1, rgb=3, log_scale=3, quat=4, mask=1)
+
+
+def _views_arr(views):
+    arr = (View * max(len(views), 1))(*[view(v) for v in views])
+    return arr
+
+
+def project_views(g: GaussianMap, cam: dict, views, prm: Params | None = None,
+                  cb: CodebookT | None = None, rec=None, count=None, stream=None):
+    """a1-a3 over V views reading each Gaussian once: rec [V, n, 16], count [V, n]."""
+    n, V = g.n, len(views)
+    dev = g.opacity.device
+    rec = rec if rec is not None else torch.empty((V, max(n, 1), 16), dtype=torch.int32, device=dev)
+    count = count if count is not None else torch.empty((V, max(n, 1)), dtype=torch.int32,
+                                                        device=dev)
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    _check(lib().csplat_project_views(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
+                                      _views_arr(views), V, C.byref(prm or params()), _ptr(rec),
+                                      _ptr(count), _stream(stream)), "csplat_project_views")
+    return rec, count
+
+
+def ws_bin_per_view(n: int, capacity: int, cam: dict) -> int:
+    """csplat_project_bin_views' workspace bytes per view (a multiple of 256)."""
+    b = workspace_bytes(OP_BIN_TILES, n, capacity, cam)
+    return (b + 255) // 256 * 256
+
+
+def alloc_views(n: int, V: int, capacity: int, cam: dict, device):
+    """Per-view buffers of csplat_project_bin_views for V views."""
+    tx, ty = tiles(cam)
+    wsv = ws_bin_per_view(n, capacity, cam)
+    return dict(rec=torch.empty((V, max(n, 1), 16), dtype=torch.int32, device=device),
+                count=torch.empty((V, max(n, 1)), dtype=torch.int32, device=device),
+                pair_gid=torch.empty((V, max(capacity, 1)), dtype=torch.int32, device=device),
+                tile_range=torch.zeros((V, tx * ty + 1, 2), dtype=torch.int32, device=device),
+                n_pairs_dev=torch.zeros(V, dtype=torch.int64, device=device),
+                ws=torch.empty(V * wsv + 256, dtype=torch.uint8, device=device), ws_per_view=wsv,
+                capacity=capacity)
+
+
+def project_bin_views(g: GaussianMap, cam: dict, views, out: dict, prm: Params | None = None,
+                      cb: CodebookT | None = None, tile_active=None, stream=None):
+    """a1-a5 over V views (projection once per Gaussian + per-view bucket + one
+    batched sort) into the per-view buffers of alloc_views."""
+    V = len(views)
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    ws = out["ws"]
+    base = ws.data_ptr()
+    off = (-base) % 256                     # 256-byte aligned workspace base
+    _check(lib().csplat_project_bin_views(
+        C.byref(gs), _byref(cbs), C.byref(camera(cam)), _views_arr(views), V,
+        C.byref(prm or params()), _ptr(tile_active), _ptr(out["rec"]), _ptr(out["count"]),
+        out["capacity"], _ptr(out["pair_gid"]), _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]),
+        C.c_void_p(base + off), out["ws_per_view"], _stream(stream)), "csplat_project_bin_views")
+    return out
+
+
+def chain_views(g: GaussianMap, cam: dict, views, rec, ws, grads: dict, pose=None,
+                prm: Params | None = None, cb: CodebookT | None = None, flags: int = 0,
+                stream=None):
+    """a8 summed over V views: ws [V, OP_RENDER_BWD bytes] (render_bwd SKIP_CHAIN
+    workspaces, 256-byte aligned), grads planes (overwritten unless ACCUMULATE),
+    pose [V, 6] (optional)."""
+    V = len(views)
+    gr = Grads(*[_ptr(grads.get(k)) for k in ("mean", "opacity", "rgb", "log_scale", "quat",
+                                               "mask")], _ptr(pose))
+    gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    _check(lib().csplat_chain_views(C.byref(gs), _byref(cbs), C.byref(camera(cam)),
+                                    _views_arr(views), V, C.byref(prm or params()), _ptr(rec),
+                                    _ptr(ws), flags, C.byref(gr), _stream(stream)),
+           "csplat_chain_views")
+    return grads
 
 
 def alloc_grads(n: int, device="cuda", pose_only=False):

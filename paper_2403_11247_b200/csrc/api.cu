@@ -198,6 +198,102 @@ int csplat_project_dv(const csplat_gaussians *g, const csplat_codebook *cb,
   return project_impl(g, cb, cam, nullptr, view_dev, prm, rec, count, stream);
 }
 
+int csplat_project_views(const csplat_gaussians *g, const csplat_codebook *cb,
+                         const csplat_camera *cam, const csplat_view *views, int32_t n_views,
+                         const csplat_params *prm, void *rec, int32_t *count, void *stream) {
+  RET_IF(check_gaussians(g));
+  RET_IF(check_camera(cam));
+  RET_IF(check_codebook(cb, true));
+  if (n_views < 0) return invalid("n_views < 0");
+  if ((n_views > 0 && !views) || !prm) return invalid("views/params NULL");
+  if (g->n > 0 && n_views > 0 && (!rec || !count)) return invalid("rec/count NULL");
+  if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  if (!(prm->mask_eps > 0.f) || !(prm->mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
+  if (n_views == 0) return CSPLAT_OK;
+  RET_IF(check_device());
+  csplat::DecodeArgs d;
+  if (cb) d = decode_args(cb);
+  return cuda_status(csplat::launch_project_views(*g, cb ? &d : nullptr, *cam, views, n_views,
+                                                  mask_tau(prm->mask_eps), prm->dilation, rec,
+                                                  count, nullptr, 0, 0, nullptr, 0, nullptr,
+                                                  nullptr, nullptr,
+                                                  static_cast<cudaStream_t>(stream)),
+                     "csplat_project_views");
+}
+
+int csplat_project_bin_views(const csplat_gaussians *g, const csplat_codebook *cb,
+                             const csplat_camera *cam, const csplat_view *views, int32_t n_views,
+                             const csplat_params *prm, const uint32_t *tile_active, void *rec,
+                             int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
+                             uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
+                             size_t ws_bytes_per_view, void *stream) {
+  RET_IF(check_gaussians(g));
+  RET_IF(check_camera(cam));
+  RET_IF(check_codebook(cb, true));
+  if (n_views < 0) return invalid("n_views < 0");
+  if ((n_views > 0 && !views) || !prm) return invalid("views/params NULL");
+  if (g->n > 0 && n_views > 0 && (!rec || !count)) return invalid("rec/count NULL");
+  if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
+  if (!(prm->mask_eps > 0.f) || !(prm->mask_eps < 1.f)) return invalid("mask_eps must be in (0,1)");
+  if (pair_capacity < 0 || pair_capacity > 0xffffffffLL) return invalid("capacity out of range");
+  if (g->n > (int64_t)csplat::kPairGidMask + 1) return invalid("n must be < 2^28 for binning");
+  if (n_views > 0 && (!tile_range || !n_pairs_dev)) return invalid("tile_range/n_pairs NULL");
+  if (pair_capacity > 0 && n_views > 0 && !pair_gid) return invalid("pair_gid NULL");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  const size_t need = csplat::bin_workspace_bytes(g->n, pair_capacity, *cam);
+  if (n_views > 0 && (!ws || ws_bytes_per_view < need || (ws_bytes_per_view & 255u) ||
+                      (reinterpret_cast<uintptr_t>(ws) & 255u))) {
+    set_err("project_bin_views: workspace per view too small, or not a multiple of 256 bytes / "
+            "256-byte aligned");
+    return CSPLAT_ERR_WORKSPACE;
+  }
+  if (n_views == 0) return CSPLAT_OK;
+  RET_IF(check_device());
+  csplat::DecodeArgs d;
+  if (cb) d = decode_args(cb);
+  const csplat::CamInfo ci = csplat::cam_info(*cam);
+  const int64_t words = ((int64_t)ci.tiles_x * ci.tiles_y + 31) / 32;
+  return cuda_status(csplat::launch_project_views(*g, cb ? &d : nullptr, *cam, views, n_views,
+                                                  mask_tau(prm->mask_eps), prm->dilation, rec,
+                                                  count, ws, (int64_t)ws_bytes_per_view,
+                                                  pair_capacity, tile_active, words, pair_gid,
+                                                  tile_range, n_pairs_dev,
+                                                  static_cast<cudaStream_t>(stream)),
+                     "csplat_project_bin_views");
+}
+
+int csplat_chain_views(const csplat_gaussians *g, const csplat_codebook *cb,
+                       const csplat_camera *cam, const csplat_view *views, int32_t n_views,
+                       const csplat_params *prm, const void *rec, void *ws, uint32_t flags,
+                       const csplat_grads *out, void *stream) {
+  RET_IF(check_gaussians(g));
+  RET_IF(check_camera(cam));
+  RET_IF(check_codebook(cb, true));
+  if (n_views < 0) return invalid("n_views < 0");
+  if ((n_views > 0 && !views) || !prm || !out) return invalid("views/params/out NULL");
+  if (flags & CSPLAT_POSE_ONLY) return invalid("chain_views: POSE_ONLY is not supported");
+  if (g->n > 0 && n_views > 0 && (!rec || !ws)) return invalid("rec/ws NULL");
+  if (!cb && g->n > 0 && (!g->log_scale || !g->quat)) return invalid("log_scale/quat NULL");
+  if (!aligned16(rec) || (reinterpret_cast<uintptr_t>(ws) & 255u)) {
+    set_err("rec must be 16-byte aligned, ws 256-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  RET_IF(check_device());
+  csplat::DecodeArgs d;
+  if (cb) d = decode_args(cb);
+  return cuda_status(csplat::launch_chain_views(*g, cb ? &d : nullptr, *cam, views, n_views, *prm,
+                                                rec, ws, flags, *out,
+                                                static_cast<cudaStream_t>(stream)),
+                     "csplat_chain_views");
+}
+
 static int project_bin_impl(const csplat_gaussians *g, const csplat_codebook *cb,
                             const csplat_camera *cam, const csplat_view *view,
                             const float *view_dev, const csplat_params *prm, void *rec,

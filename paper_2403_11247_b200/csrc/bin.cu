@@ -142,12 +142,17 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long *a, int len, int
 // bits 0-27 and the pair's 8x8-block cull mask (block_mask, from the record's
 // words 0-7 and 12-13) in bits 28-31 -- what the renderers need per entry,
 // so they gather the record itself from rec and compute nothing per entry.
+__device__ __forceinline__ uint32_t pair_entry(unsigned long long key,
+                                               const uint4 *__restrict__ rec4, int X0, int Y0) {
+  const uint32_t gid = (uint32_t)(key & 0xffffffffull);
+  const uint4 *r = rec4 + (int64_t)gid * 4;
+  return gid | (block_mask(r[0], r[1], r[3], X0, Y0) << kPairMaskShift);
+}
+
 __device__ __forceinline__ void emit_entry(unsigned long long key, int64_t pos,
                                            const uint4 *__restrict__ rec4,
                                            uint32_t *__restrict__ pair_gid, int X0, int Y0) {
-  const uint32_t gid = (uint32_t)(key & 0xffffffffull);
-  const uint4 *r = rec4 + (int64_t)gid * 4;
-  pair_gid[pos] = gid | (block_mask(r[0], r[1], r[3], X0, Y0) << kPairMaskShift);
+  pair_gid[pos] = pair_entry(key, rec4, X0, Y0);
 }
 
 __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len, uint32_t start,
@@ -223,7 +228,15 @@ constexpr unsigned long long kRangeP = 1ull << 63;
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int64_t T, uint32_t *__restrict__ range, int64_t *__restrict__ n_pairs, BinWs w,
     int64_t cap, const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid, int tiles_x,
-    int64_t tile0) {
+    int64_t tile0, SortViews sv) {
+  if (gridDim.y > 1) {  // batched views: this CTA's view
+    const int64_t v = blockIdx.y;
+    w = ws_at(w, v * sv.ws_stride);
+    rec4 += v * sv.rec_stride;
+    pair_gid += v * sv.gid_stride;
+    range += v * sv.range_stride;
+    n_pairs += v;
+  }
   __shared__ __align__(16) unsigned long long sk[kCtaCap];
   __shared__ uint32_t fill, s_start, s_end;
   const int64_t tile = tile0 + blockIdx.x;
@@ -248,6 +261,14 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int np2 = 2;
     while (np2 < n0) np2 <<= 1;
     sort_regs256(x0, x1, np2, reinterpret_cast<unsigned long long(*)[2 * kSortThreads]>(sk));
+  }
+  // the entries (index | block mask) need only the sorted keys and the records:
+  // gather + mask them now, so the record loads' latency overlaps the look-back
+  uint32_t e0 = 0, e1 = 0;
+  if (reg_path) {
+    const int t = threadIdx.x;
+    if (2 * t < (int)cnt_t) e0 = pair_entry(x0, rec4, X0, Y0);
+    if (2 * t + 1 < (int)cnt_t) e1 = pair_entry(x1, rec4, X0, Y0);
   }
   if (threadIdx.x < 32) {  // the tile's output offset: a look-back over the preceding tiles
     const int lane = threadIdx.x;
@@ -294,10 +315,10 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   const uint32_t start = s_start, end = s_end;
   const int len = (int)(end - start);  // the tile's pair count, or 0 (empty or cut)
   if (len == 0) return;
-  if (reg_path) {  // sorted above; len < cnt_t only beyond the capacity (reported)
+  if (reg_path) {  // sorted and masked above; len is cnt_t (or 0 when cut)
     const int t = threadIdx.x;
-    if (2 * t < len) emit_entry(x0, (int64_t)start + 2 * t, rec4, pair_gid, X0, Y0);
-    if (2 * t + 1 < len) emit_entry(x1, (int64_t)start + 2 * t + 1, rec4, pair_gid, X0, Y0);
+    if (2 * t < len) pair_gid[(int64_t)start + 2 * t] = e0;
+    if (2 * t + 1 < len) pair_gid[(int64_t)start + 2 * t + 1] = e1;
     return;
   }
   unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
@@ -332,9 +353,23 @@ cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t ca
   if (ntiles <= 0) return cudaSuccess;
   k_sort_tiles<<<(unsigned)ntiles, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
                                                          static_cast<const uint4 *>(rec),
-                                                         pair_gid, tiles_x, tile0);
+                                                         pair_gid, tiles_x, tile0, SortViews{});
   return cudaGetLastError();
 }
+
+cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
+                                    const void *rec, uint32_t *pair_gid, uint32_t *tile_range,
+                                    int64_t *n_pairs_dev, const SortViews &sv, int nv,
+                                    cudaStream_t s) {
+  if (T <= 0 || nv <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)T, (unsigned)nv);
+  k_sort_tiles<<<grid, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
+                                             static_cast<const uint4 *>(rec), pair_gid, tiles_x, 0,
+                                             sv);
+  return cudaGetLastError();
+}
+
+size_t bin_head_bytes(int64_t T) { return align_up(T * 4) + align_up(4) + align_up(T * 8); }
 
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
                        int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,

@@ -20,6 +20,15 @@ struct BinWs {
 };
 
 BinWs bin_carve(void *ws, int64_t cap, int64_t T);
+// the workspace of view v of a batched call: every region offset by v * stride bytes
+__host__ __device__ __forceinline__ BinWs ws_at(BinWs w, int64_t off) {
+  auto mv = [off](auto *p) { return reinterpret_cast<decltype(p)>(reinterpret_cast<char *>(p) + off); };
+  w.cur = mv(w.cur); w.ovf_n = mv(w.ovf_n); w.status = mv(w.status); w.bucket = mv(w.bucket);
+  w.ovf_tile = mv(w.ovf_tile); w.ovf_key = mv(w.ovf_key); w.keys = mv(w.keys);
+  return w;
+}
+// bytes of the head (cursors, overflow length, look-back words) bin_reset zeroes
+size_t bin_head_bytes(int64_t T);
 // zero the cursors, the overflow length and the look-back words (one memset)
 cudaError_t bin_reset(const BinWs &w, int64_t T, cudaStream_t s);
 // a5: k_sort_tiles over the buckets filled by k_bucket or the fused projection
@@ -29,6 +38,16 @@ cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t ca
                               const void *rec, uint32_t *pair_gid,
                               uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,
                               int64_t tile0 = 0, int64_t ntiles = -1);
+// the same over nv views at once (grid.y = view): view v's workspace at
+// + v ws_stride bytes, records + v rec_stride (uint4 units), pair_gid + v
+// gid_stride, tile_range + v range_stride, n_pairs_dev + v
+struct SortViews {
+  int64_t ws_stride, rec_stride, gid_stride, range_stride;
+};
+cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
+                                    const void *rec, uint32_t *pair_gid, uint32_t *tile_range,
+                                    int64_t *n_pairs_dev, const SortViews &sv, int nv,
+                                    cudaStream_t s);
 
 // Warp-cooperative expansion of 32 Gaussians' tile rectangles.  Lane l holds
 // Gaussian base + l's pair count c, its pixel rectangle corners rx, ry (record

@@ -421,6 +421,20 @@ cudaError_t launch_rvq_code_grad(const float *g, int64_t n, const int64_t *n_dev
 cudaError_t launch_rvq_init_stage(const float *x, int64_t n, int d, float *codes, int P, int l,
                                   const void *idx, int idx_bytes, const int64_t *sample,
                                   cudaStream_t s);
+// multi-view (SURVEY §8(e) window): projection (+ bucket + batched sort) of nv
+// views reading each Gaussian once (project.cu), the chain summed over views
+// (chain.cu)
+cudaError_t launch_project_views(const csplat_gaussians &g, const DecodeArgs *dec,
+                                 const csplat_camera &cam, const csplat_view *views, int nv,
+                                 float tau, float dilation, void *rec, int32_t *count,
+                                 void *ws, int64_t ws_stride, int64_t cap,
+                                 const uint32_t *active, int64_t active_stride,
+                                 uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
+                                 cudaStream_t s);
+cudaError_t launch_chain_views(const csplat_gaussians &g, const DecodeArgs *dec,
+                               const csplat_camera &cam, const csplat_view *views, int nv,
+                               const csplat_params &prm, const void *rec, void *ws,
+                               uint32_t flags, const csplat_grads &out, cudaStream_t s);
 // the calling thread's fork streams / events of the composed calls (project.cu)
 void release_thread_fork_resources();
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
@@ -460,6 +474,8 @@ cudaError_t launch_project_bin_render(const csplat_gaussians &g, const DecodeArg
                                       int32_t *n_contrib, cudaStream_t s);
 
 size_t bwd_workspace_bytes(int64_t n);
+// the render_bwd workspace's bitmap of Gaussians that received partials
+uint32_t *bwd_alive_bits(void *ws, int64_t n);
 struct TrackingLoss;
 cudaError_t bwd_prep(const csplat_gaussians &g, uint32_t flags, const csplat_grads &out,
                      void *ws, const TrackingLoss *loss, cudaStream_t s);
@@ -468,7 +484,7 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
                                     const uint32_t *pair_gid, const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
-                                    cudaStream_t s, int tile0, int ntiles);
+                                    int64_t n, cudaStream_t s, int tile0, int ntiles);
 
 // csplat_render_step: a3 .. a8 for one view -- projection + bucket, then per
 // tile chunk (on its own library stream) the sort, the forward and the

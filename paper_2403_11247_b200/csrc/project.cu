@@ -5,6 +5,7 @@
 // the R-VQ decode gathers from the (L1/L2-resident) codebooks, and one 64-byte
 // record written as four 16-byte stores.  HBM-bound: 60 B in + 64 B + 4 B out
 // per Gaussian (raw geometry); DA keeps it at ~300 instructions per Gaussian.
+#include <algorithm>
 #include <mutex>
 
 #include "bin_dev.cuh"
@@ -24,23 +25,24 @@ struct ProjConst {
   float tau, dil;
 };
 
-// Gaussian i (< n): its 64-byte record and pair count; for the fused bucket
-// pass also the count, the pixel-rectangle words and bits(z_c) (0 if culled).
+// The view-independent part of Gaussian i's projection (mask, decode,
+// activations, Sigma = R S S^T R^T of Eq 1) -- computed once per Gaussian
+// for any number of views (csplat_project_views).  ok = false: culled in
+// every view.  Exactly the single-view DA expressions; the culls of the two
+// parts are ANDed, so their evaluation order does not change any output.
+struct GPre {
+  bool ok;
+  float mx, my, mz, oh, k2, cr, cg, cb;
+  float S00, S01, S02, S11, S12, S22;
+};
+
 template <int LF>
-__device__ __forceinline__ void project_one(
+__device__ __forceinline__ void project_prelude(
     int64_t i, int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
     const float *__restrict__ opac, const float *__restrict__ rgb,
     const float *__restrict__ lsc, const float *__restrict__ quat,
-    const float *__restrict__ mask, const DecodeArgs &dec, int use_dec, ProjConst &pc,
-    const float *__restrict__ view_dev, float4 *__restrict__ rec, int32_t *__restrict__ count,
-    int &c_out, uint32_t &rx_out, uint32_t &ry_out, uint32_t &zb_out) {
-  if (view_dev) {  // the view lives in device memory (graph-captured pose updates)
-#pragma unroll
-    for (int k = 0; k < 12; k++) pc.V[k] = __ldg(view_dev + k);
-  }
+    const float *__restrict__ mask, const DecodeArgs &dec, int use_dec, float tau, GPre &g) {
   const int64_t ne = eff_n(n, n_dev);
-  float4 *r = rec + i * 4;
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   bool ok = i < ne;
   // every attribute load is independent of the mask test: issue them all at
   // once (the Gaussian's planes, then the R-VQ codes), one memory round trip
@@ -50,42 +52,35 @@ __device__ __forceinline__ void project_one(
   float ls[3], qv[4];
   if (use_dec) {
     // Eq 10: S_hat^L = sum_l C^l[i^l] (R17, R20); a bad index culls (NaN)
-    rvq_decode<LF>(dec, n, j, ls, qv, ok && (m > pc.tau));
+    rvq_decode<LF>(dec, n, j, ls, qv, ok && (m > tau));
   } else {
     ls[0] = lsc[j]; ls[1] = lsc[n + j]; ls[2] = lsc[2 * n + j];
     qv[0] = quat[j]; qv[1] = quat[n + j]; qv[2] = quat[2 * n + j]; qv[3] = quat[3 * n + j];
   }
-  const float mx = mean[j], my = mean[n + j], mz = mean[2 * n + j];
+  g.mx = mean[j]; g.my = mean[n + j]; g.mz = mean[2 * n + j];
   const float o = opac[j];
-  const float cr = rgb[j], cg = rgb[n + j], cb = rgb[2 * n + j];
+  g.cr = rgb[j]; g.cg = rgb[n + j]; g.cb = rgb[2 * n + j];
   const float ls0 = ls[0], ls1 = ls[1], ls2 = ls[2];
   const float qw = qv[0], qx = qv[1], qy = qv[2], qz = qv[3];
-  ok = ok && (m > pc.tau);  // Eq 6: M = 1[Sig(m) > eps]  <=>  m > tau (R12)
-  ok = ok && isfinite(mx) && isfinite(my) && isfinite(mz) && isfinite(o) && isfinite(ls0) &&
+  ok = ok && (m > tau);  // Eq 6: M = 1[Sig(m) > eps]  <=>  m > tau (R12)
+  ok = ok && isfinite(g.mx) && isfinite(g.my) && isfinite(g.mz) && isfinite(o) && isfinite(ls0) &&
        isfinite(ls1) && isfinite(ls2) && isfinite(qw) && isfinite(qx) && isfinite(qy) &&
-       isfinite(qz) && isfinite(cr) && isfinite(cg) && isfinite(cb);
-  float oh = 0, k2 = 0, xc = 0, yc = 0, zc = 0;
+       isfinite(qz) && isfinite(g.cr) && isfinite(g.cg) && isfinite(g.cb);
+  g.oh = 0.f;
+  g.k2 = 0.f;
   if (ok) {
-    oh = da_sigm(o);
-    const float a255 = DMUL(255.0f, oh);
+    g.oh = da_sigm(o);
+    const float a255 = DMUL(255.0f, g.oh);
     ok = a255 > 1.0f;  // alpha >= 1/255 reachable (R2)
-    k2 = DMUL(2.0f, da_plog(a255));
-    const float *V = pc.V;
-    xc = DADD(DADD(DADD(DMUL(V[0], mx), DMUL(V[1], my)), DMUL(V[2], mz)), V[3]);
-    yc = DADD(DADD(DADD(DMUL(V[4], mx), DMUL(V[5], my)), DMUL(V[6], mz)), V[7]);
-    zc = DADD(DADD(DADD(DMUL(V[8], mx), DMUL(V[9], my)), DMUL(V[10], mz)), V[11]);
-    ok = ok && (zc > pc.near_z) && (zc < pc.far_z);  // R21
+    g.k2 = DMUL(2.0f, da_plog(a255));
   }
   float nq = 0;
   if (ok) {
     nq = DADD(DADD(DADD(DMUL(qw, qw), DMUL(qx, qx)), DMUL(qy, qy)), DMUL(qz, qz));
     ok = nq > 0.0f;
   }
-  if (!ok) {
-    r[0] = z4; r[1] = z4; r[2] = z4; r[3] = z4;
-    count[i] = 0;
-    return;
-  }
+  g.ok = ok;
+  if (!ok) return;
   const float s0 = da_pexp(ls0), s1 = da_pexp(ls1), s2 = da_pexp(ls2);
   const float rn = DDIV(1.0f, DSQRT(nq));
   const float w = DMUL(qw, rn), x = DMUL(qx, rn), y = DMUL(qy, rn), z = DMUL(qz, rn);
@@ -105,14 +100,37 @@ __device__ __forceinline__ void project_one(
   for (int a = 0; a < 3; a++)
 #pragma unroll
     for (int b = 0; b < 3; b++) M[a][b] = DMUL(R[a][b], sv[b]);
-  float S[3][3];  // Eq 1: Sigma = R S S^T R^T
-#pragma unroll
-  for (int a = 0; a < 3; a++)
-#pragma unroll
-    for (int b = a; b < 3; b++) {
-      S[a][b] = DADD(DADD(DMUL(M[a][0], M[b][0]), DMUL(M[a][1], M[b][1])), DMUL(M[a][2], M[b][2]));
-      S[b][a] = S[a][b];
-    }
+  auto sig = [&](int a, int b) {  // Eq 1: Sigma = R S S^T R^T
+    return DADD(DADD(DMUL(M[a][0], M[b][0]), DMUL(M[a][1], M[b][1])), DMUL(M[a][2], M[b][2]));
+  };
+  g.S00 = sig(0, 0); g.S01 = sig(0, 1); g.S02 = sig(0, 2);
+  g.S11 = sig(1, 1); g.S12 = sig(1, 2); g.S22 = sig(2, 2);
+}
+
+// The view part (Eq 2, R2-R7, R21): Gaussian i's 64-byte record and pair count
+// in the view of pc; for the fused bucket pass also the count, the
+// pixel-rectangle words and bits(z_c) (0 if culled).
+__device__ __forceinline__ void project_view(int64_t i, const GPre &g, const ProjConst &pc,
+                                             const float *V, float4 *__restrict__ r,
+                                             int32_t *__restrict__ count, int &c_out,
+                                             uint32_t &rx_out, uint32_t &ry_out,
+                                             uint32_t &zb_out) {
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  c_out = 0; rx_out = 0; ry_out = 0; zb_out = 0;
+  bool ok = g.ok;
+  float xc = 0, yc = 0, zc = 0;
+  if (ok) {
+    xc = DADD(DADD(DADD(DMUL(V[0], g.mx), DMUL(V[1], g.my)), DMUL(V[2], g.mz)), V[3]);
+    yc = DADD(DADD(DADD(DMUL(V[4], g.mx), DMUL(V[5], g.my)), DMUL(V[6], g.mz)), V[7]);
+    zc = DADD(DADD(DADD(DMUL(V[8], g.mx), DMUL(V[9], g.my)), DMUL(V[10], g.mz)), V[11]);
+    ok = (zc > pc.near_z) && (zc < pc.far_z);  // R21
+  }
+  if (!ok) {
+    r[0] = z4; r[1] = z4; r[2] = z4; r[3] = z4;
+    count[i] = 0;
+    return;
+  }
+  const float S[3][3] = {{g.S00, g.S01, g.S02}, {g.S01, g.S11, g.S12}, {g.S02, g.S12, g.S22}};
   const float iz = DDIV(1.0f, zc);
   const float txz = DMUL(xc, iz), tyz = DMUL(yc, iz);
   const float tx = DMUL(fminf(fmaxf(txz, pc.lx_lo), pc.lx_hi), zc);  // R6
@@ -120,7 +138,6 @@ __device__ __forceinline__ void project_one(
   const float iz2 = DMUL(iz, iz);
   const float J00 = DMUL(pc.fx, iz), J02 = DMUL(-DMUL(pc.fx, tx), iz2);
   const float J11 = DMUL(pc.fy, iz), J12 = DMUL(-DMUL(pc.fy, ty), iz2);
-  const float *V = pc.V;
   float A[2][3];  // A = J W
 #pragma unroll
   for (int j = 0; j < 3; j++) {
@@ -141,7 +158,7 @@ __device__ __forceinline__ void project_one(
   bool ok2 = det > 0.0f;
   const float ca = DDIV(sc, det), cbn = DDIV(-sb, det), cc = DDIV(sa, det);
   const float u = DADD(DMUL(pc.fx, txz), pc.cx), v = DADD(DMUL(pc.fy, tyz), pc.cy);
-  const float ex = DADD(DSQRT(DMUL(k2, sa)), 1e-3f), ey = DADD(DSQRT(DMUL(k2, sc)), 1e-3f);
+  const float ex = DADD(DSQRT(DMUL(g.k2, sa)), 1e-3f), ey = DADD(DSQRT(DMUL(g.k2, sc)), 1e-3f);
   const float X0 = ceilf(DSUB(u, ex)), X1 = floorf(DADD(u, ex));
   const float Y0 = ceilf(DSUB(v, ey)), Y1 = floorf(DADD(v, ey));
   ok2 = ok2 && (X0 <= DSUB(pc.Wf, 1.0f)) && (X1 >= 0.0f) && (Y0 <= DSUB(pc.Hf, 1.0f)) &&
@@ -155,8 +172,8 @@ __device__ __forceinline__ void project_one(
   const int py0 = (int)fmaxf(Y0, 0.0f), py1 = (int)fminf(Y1, DSUB(pc.Hf, 1.0f));
   const int tx0 = px0 / kTile, tx1 = px1 / kTile, ty0 = py0 / kTile, ty1 = py1 / kTile;
   r[0] = make_float4(u, v, ca, DADD(cbn, cbn));
-  r[1] = make_float4(cc, oh, k2, zc);
-  r[2] = make_float4(cr, cg, cb, __uint_as_float((uint32_t)i));
+  r[1] = make_float4(cc, g.oh, g.k2, zc);
+  r[2] = make_float4(g.cr, g.cg, g.cb, __uint_as_float((uint32_t)i));
   // inclusive pixel rectangle as two u16x2 corners (low | high), DESIGN.md §4
   r[3] = make_float4(__uint_as_float((uint32_t)px0 | ((uint32_t)py0 << 16)),
                      __uint_as_float((uint32_t)px1 | ((uint32_t)py1 << 16)), 0.f, 0.f);
@@ -165,6 +182,25 @@ __device__ __forceinline__ void project_one(
   ry_out = (uint32_t)px1 | ((uint32_t)py1 << 16);
   zb_out = __float_as_uint(zc);
   count[i] = c_out;
+}
+
+// Gaussian i (< n) in one view: its 64-byte record and pair count (+ the
+// fused bucket pass's count, rectangle words and bits(z_c)).
+template <int LF>
+__device__ __forceinline__ void project_one(
+    int64_t i, int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
+    const float *__restrict__ opac, const float *__restrict__ rgb,
+    const float *__restrict__ lsc, const float *__restrict__ quat,
+    const float *__restrict__ mask, const DecodeArgs &dec, int use_dec, ProjConst &pc,
+    const float *__restrict__ view_dev, float4 *__restrict__ rec, int32_t *__restrict__ count,
+    int &c_out, uint32_t &rx_out, uint32_t &ry_out, uint32_t &zb_out) {
+  if (view_dev) {  // the view lives in device memory (graph-captured pose updates)
+#pragma unroll
+    for (int k = 0; k < 12; k++) pc.V[k] = __ldg(view_dev + k);
+  }
+  GPre g;
+  project_prelude<LF>(i, n, n_dev, mean, opac, rgb, lsc, quat, mask, dec, use_dec, pc.tau, g);
+  project_view(i, g, pc, pc.V, rec + i * 4, count, c_out, rx_out, ry_out, zb_out);
 }
 
 // a1 + a2-decode + a3 (+ a4, BIN): one thread per Gaussian; with BIN the warp
@@ -193,12 +229,51 @@ __global__ void __launch_bounds__(256) k_project(
   }
 }
 
-static cudaError_t launch_project_impl(const csplat_gaussians &g, const DecodeArgs *dec,
-                                      const csplat_camera &cam, const csplat_view &view,
-                                      const float *view_dev, float tau, float dilation,
-                                      void *rec, int32_t *count, const BinWs *bw, int tiles_x,
-                                      int64_t cap, const uint32_t *active, cudaStream_t s) {
-  if (g.n == 0) return cudaSuccess;
+// csplat_project_views / csplat_project_bin_views (SURVEY §8(b) n_views):
+// one thread per Gaussian reads and decodes it and forms Sigma ONCE
+// (project_prelude), then projects it into each of the launch's views
+// (project_view, the single-view DA, so every view's outputs are bit-identical
+// to csplat_project's); with BIN the warp spreads view v's pairs into view v's
+// tile buckets right after (bin_dev.cuh).  Outputs of view v at
+// rec + v rec_stride, count + v count_stride, workspace + v ws_stride bytes.
+constexpr int kMaxViewsPerLaunch = 64;
+struct ViewMats {
+  float V[kMaxViewsPerLaunch][12];
+};
+
+template <int LF, bool BIN>
+__global__ void __launch_bounds__(256) k_project_views(
+    int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
+    const float *__restrict__ opac, const float *__restrict__ rgb,
+    const float *__restrict__ lsc, const float *__restrict__ quat,
+    const float *__restrict__ mask, DecodeArgs dec, int use_dec, ProjConst pc,
+    const __grid_constant__ ViewMats vm, int nv, float4 *__restrict__ rec, int64_t rec_stride,
+    int32_t *__restrict__ count, int64_t count_stride, BinWs w, int64_t ws_stride, int tiles_x,
+    int64_t cap, const uint32_t *__restrict__ active, int64_t active_stride) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  GPre g;
+  g.ok = false;
+  if (i < n)
+    project_prelude<LF>(i, n, n_dev, mean, opac, rgb, lsc, quat, mask, dec, use_dec, pc.tau, g);
+  for (int v = 0; v < nv; v++) {
+    int c = 0;
+    uint32_t rx = 0, ry = 0, zb = 0;
+    if (i < n)
+      project_view(i, g, pc, vm.V[v], rec + v * rec_stride + i * 4, count + v * count_stride, c,
+                   rx, ry, zb);
+    if constexpr (BIN) {
+      const BinWs wv = ws_at(w, v * ws_stride);
+      const uint32_t *act = active ? active + v * active_stride : nullptr;
+      expand_warp_regs(i - (threadIdx.x & 31), c, rx, ry, zb, tiles_x,
+                       [&](uint32_t gid, int tile, uint32_t z) {
+                         bucket_put(wv, cap, act, gid, tile, z);
+                       });
+    }
+  }
+}
+
+static ProjConst make_proj_const(const csplat_camera &cam, const csplat_view &view, float tau,
+                                 float dilation) {
   ProjConst pc;
   for (int k = 0; k < 12; k++) pc.V[k] = view.m[k];
   pc.fx = cam.fx; pc.fy = cam.fy; pc.cx = cam.cx; pc.cy = cam.cy;
@@ -216,6 +291,16 @@ static cudaError_t launch_project_impl(const csplat_gaussians &g, const DecodeAr
   pc.ly_hi = b4 / pc.fy;
   pc.tau = tau;
   pc.dil = dilation;
+  return pc;
+}
+
+static cudaError_t launch_project_impl(const csplat_gaussians &g, const DecodeArgs *dec,
+                                      const csplat_camera &cam, const csplat_view &view,
+                                      const float *view_dev, float tau, float dilation,
+                                      void *rec, int32_t *count, const BinWs *bw, int tiles_x,
+                                      int64_t cap, const uint32_t *active, cudaStream_t s) {
+  if (g.n == 0) return cudaSuccess;
+  const ProjConst pc = make_proj_const(cam, view, tau, dilation);
   DecodeArgs d{};
   if (dec) d = *dec;
   const int threads = 256;
@@ -232,6 +317,61 @@ static cudaError_t launch_project_impl(const csplat_gaussians &g, const DecodeAr
                                             reinterpret_cast<float4 *>(rec), count,
                                             bin ? *bw : BinWs{}, tiles_x, cap, active);
   return cudaGetLastError();
+}
+
+// nv views (chunks of kMaxViewsPerLaunch per launch); with ws: the fused
+// bucket pass into view v's workspace (+ v ws_stride bytes, reset here) and
+// then the batched per-tile sort of every view
+cudaError_t launch_project_views(const csplat_gaussians &g, const DecodeArgs *dec,
+                                 const csplat_camera &cam, const csplat_view *views, int nv,
+                                 float tau, float dilation, void *rec, int32_t *count,
+                                 void *ws, int64_t ws_stride, int64_t cap,
+                                 const uint32_t *active, int64_t active_stride,
+                                 uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
+                                 cudaStream_t s) {
+  const CamInfo ci = cam_info(cam);
+  const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
+  const bool bin = ws != nullptr;
+  BinWs w{};
+  cudaError_t e = cudaSuccess;
+  if (bin) {
+    w = bin_carve(ws, cap, T);
+    // every view's head (cursors, overflow length, look-back words): one 2-D memset
+    e = cudaMemset2DAsync(ws, (size_t)ws_stride, 0, bin_head_bytes(T), (size_t)nv, s);
+    if (e != cudaSuccess) return e;
+  }
+  DecodeArgs d{};
+  if (dec) d = *dec;
+  const int64_t n = g.n;
+  if (n > 0) {
+    const int threads = 256;
+    const int64_t blocks = (n + threads - 1) / threads;
+    auto kern = bin ? k_project_views<0, true> : k_project_views<0, false>;
+    switch (rvq_lf(dec)) {
+      case 4: kern = bin ? k_project_views<4, true> : k_project_views<4, false>; break;
+      case 2: kern = bin ? k_project_views<2, true> : k_project_views<2, false>; break;
+      default: break;
+    }
+    const int64_t words = (T + 31) / 32;
+    for (int v0 = 0; v0 < nv; v0 += kMaxViewsPerLaunch) {
+      const int m = std::min(nv - v0, kMaxViewsPerLaunch);
+      ViewMats vm;
+      for (int v = 0; v < m; v++)
+        for (int k = 0; k < 12; k++) vm.V[v][k] = views[v0 + v].m[k];
+      const ProjConst pc = make_proj_const(cam, views[v0], tau, dilation);
+      kern<<<(unsigned)blocks, threads, 0, s>>>(
+          n, g.n_dev, g.mean, g.opacity, g.rgb, g.log_scale, g.quat, g.mask, d, dec ? 1 : 0, pc,
+          vm, m, reinterpret_cast<float4 *>(rec) + (int64_t)v0 * n * 4, n * 4,
+          count + (int64_t)v0 * n, n, bin ? ws_at(w, v0 * ws_stride) : BinWs{}, ws_stride,
+          ci.tiles_x, cap, active ? active + v0 * active_stride : nullptr, active_stride);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      (void)words;
+    }
+  }
+  if (!bin) return cudaSuccess;
+  const SortViews sv{ws_stride, n * 4, cap, 2 * (T + 1)};
+  return launch_sort_tiles_views(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range, n_pairs_dev,
+                                 sv, nv, s);
 }
 
 cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,
@@ -358,7 +498,7 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
                             n_contrib, sc, (int)t0, (int)nt);
     if (e == cudaSuccess && bwd)
       e = launch_render_bwd_tiles(cam, bwd->loss, prm, rec, pair_gid, tile_range, t_final, n_contrib,
-                                  bwd->d_color, bwd->d_depth, bwd->d_sil, bwd->ws, sc, (int)t0,
+                                  bwd->d_color, bwd->d_depth, bwd->d_sil, bwd->ws, g.n, sc, (int)t0,
                                   (int)nt);
   }
   // join every forked stream back into the caller's stream before returning --

@@ -41,7 +41,17 @@ constexpr int kG = 3;             // active entries per transposed reduction: kG
 constexpr int kV = 10;            // partials per (pixel, entry)
 constexpr int kBwdMinBlocks = 5;  // CTAs per SM the register budget targets (6-7 measured slower)
 
-size_t bwd_workspace_bytes(int64_t n) { return (size_t)(n > 0 ? n : 1) * kAcc * sizeof(float); }
+// workspace: the [n][12] float accumulator, then a [ceil(n/32)] u32 bitmap of
+// the Gaussians that received any partial (the chains visit only those)
+static inline size_t acc_bytes(int64_t n) {
+  return ((size_t)(n > 0 ? n : 1) * kAcc * sizeof(float) + 255) & ~size_t(255);
+}
+size_t bwd_workspace_bytes(int64_t n) {
+  return acc_bytes(n) + ((size_t)((n > 0 ? n : 1) + 31) / 32 * 4 + 255) / 256 * 256;
+}
+uint32_t *bwd_alive_bits(void *ws, int64_t n) {
+  return reinterpret_cast<uint32_t *>(static_cast<char *>(ws) + acc_bytes(n));
+}
 
 struct BwdSmem {
   float4 buf[kBS][kBB * 4];             // staged records
@@ -151,7 +161,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     int tiles_x, float amax, const float *__restrict__ t_final,
     const int32_t *__restrict__ n_contrib, const float *__restrict__ dC,
     const float *__restrict__ dD, const float *__restrict__ dS, float *__restrict__ acc,
-    LossArgs la, int tile0) {
+    uint32_t *__restrict__ alive, LossArgs la, int tile0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -254,6 +264,7 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
         red_add_v4(dst, s0.x, s0.y, s0.z, s0.w);
         red_add_v4(dst + 4, s1.x, s1.y, s1.z, s1.w);
         red_add_v4(dst + 8, s2.x, s2.y, 0.f, 0.f);
+        atomicOr(alive + (gid >> 5), 1u << (gid & 31));  // the chain visits this Gaussian
       }
     };
     // replay batch k = list batch b = nb - 1 - k: lane l takes list entry
@@ -371,7 +382,8 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
 // zero the accumulator (and the pose gradient unless accumulating)
 cudaError_t bwd_prep(const csplat_gaussians &g, uint32_t flags, const csplat_grads &out,
                      void *ws, const TrackingLoss *loss, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(ws, 0, bwd_workspace_bytes(g.n), s);
+  cudaError_t e = cudaSuccess;
+  if (!(flags & CSPLAT_WS_ZEROED)) e = cudaMemsetAsync(ws, 0, bwd_workspace_bytes(g.n), s);
   if (e != cudaSuccess) return e;
   if (out.pose && !(flags & (CSPLAT_ACCUMULATE | CSPLAT_SKIP_CHAIN))) {
     e = cudaMemsetAsync(out.pose, 0, 6 * sizeof(float), s);
@@ -389,9 +401,10 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
                                     const uint32_t *pair_gid, const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
-                                    cudaStream_t s, int tile0, int ntiles) {
+                                    int64_t n, cudaStream_t s, int tile0, int ntiles) {
   const CamInfo ci = cam_info(cam);
   float *acc = static_cast<float *>(ws);
+  uint32_t *alive = bwd_alive_bits(ws, n);
   const size_t smem = sizeof(BwdSmem);
   // the opt-in shared-memory size: set once per device (a race between host
   // threads only repeats the idempotent call)
@@ -423,11 +436,11 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
     la.loss3 = loss->loss3;
     k_render_bwd<true><<<ntiles, kBwdThreads, smem, s>>>(
         tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, nullptr, nullptr, nullptr, acc, la, tile0);
+        t_final, n_contrib, nullptr, nullptr, nullptr, acc, alive, la, tile0);
   } else {
     k_render_bwd<false><<<ntiles, kBwdThreads, smem, s>>>(
         tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, d_color, d_depth, d_sil, acc, la, tile0);
+        t_final, n_contrib, d_color, d_depth, d_sil, acc, alive, la, tile0);
   }
   return cudaGetLastError();
 }
@@ -443,7 +456,7 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
   cudaError_t e = bwd_prep(g, flags, out, ws, loss, s);
   if (e != cudaSuccess) return e;
   e = launch_render_bwd_tiles(cam, loss, prm, rec, pair_gid, tile_range, t_final, n_contrib, d_color,
-                              d_depth, d_sil, ws, s, 0, -1);
+                              d_depth, d_sil, ws, g.n, s, 0, -1);
   if (e != cudaSuccess || g.n == 0 || (flags & CSPLAT_SKIP_CHAIN)) return e;
   return launch_chain(g, dec, cam, view, view_dev, prm, rec, static_cast<float *>(ws), flags,
                       out, s);

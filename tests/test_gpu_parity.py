@@ -565,7 +565,8 @@ def test_replica_c2_flag_window_sweep(env):
     assert pol["flagged"] <= FLAG_BUDGET * cam["width"] * cam["height"], sweep
 
 
-@pytest.mark.parametrize("mode", ["sequential", "pipelined", "pipelined_graph"])
+@pytest.mark.parametrize("mode", ["sequential", "pipelined", "pipelined_graph", "batched",
+                                  "batched_graph", "batched_chainviews"])
 def test_window_accumulate_matches_sum_of_views(env, mode):
     """§8(e) on one GPU: a window iteration over 3 keyframes (ACCUMULATE into the
     flat buffer) equals the sum of the 3 single-view backward passes; each
@@ -587,8 +588,9 @@ def test_window_accumulate_matches_sum_of_views(env, mode):
         st.render(v)
         singles.append(st.grads["flat"].clone())
         poses.append(st.grads["pose"].clone())
-    win = gpu_window(st, views, rank=0, world=1, pipelined=mode != "sequential")
-    if mode == "pipelined_graph":
+    win = gpu_window(st, views, rank=0, world=1, pipelined=mode != "sequential",
+                     batched=mode.startswith("batched"), chain_views=mode.endswith("chainviews"))
+    if mode.endswith("_graph"):
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
@@ -607,9 +609,15 @@ def test_window_accumulate_matches_sum_of_views(env, mode):
     ref = sum(s.double() for s in singles)
     n = st.n
     err = (flat[:15 * n].double() - ref[:15 * n]).norm() / ref[:15 * n].norm()
-    assert err < 1e-5
+    # batched: the chain's Sigma -> (R, S) part runs once on the summed views
+    # (float32 summation order only)
+    assert err < (1e-4 if mode.startswith("batched") else 1e-5), err
     for k in range(3):
         assert torch.allclose(win.poses[k], poses[k], rtol=1e-4, atol=1e-4)
+    if mode.startswith("batched"):
+        assert win.check_capacity() > 0
+        if mode.endswith("chainviews"):
+            assert not win.acc.any()    # the accumulators are left zero (WS_ZEROED)
 
 
 # ------------------------------------------------------------------ NEXT-3 window mask schedule
@@ -971,3 +979,56 @@ def test_rvq_init_parity(env, d):
         cs.rvq_assign(xt, codes[:l + 1], idx=idx[:l + 1], want_recon=False)
         assert np.array_equal(codes.cpu().numpy(), codes_o), l
         assert np.array_equal(idx.cpu().numpy().astype(np.uint16), idx_o), l
+
+
+# ------------------------------------------------------------------ multi-view projection (n_views)
+
+def test_project_views_bit_exact(env):
+    """csplat_project_views (SURVEY §8(b) n_views): every view's records and
+    counts equal the single-view csplat_project's and the oracle's, bit for bit."""
+    torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
+    sc = synth.window_scene(0, n=30000, n_keyframes=6)
+    cb, cbo = _codebooks(env, sc)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    rec, cnt = cs.project_views(g, sc.cam, sc.views, cb=cb)
+    S = orc.Scene(**sc.planes())
+    for v, view in enumerate(sc.views):
+        r1, c1 = cs.project(g, sc.cam, view, cb=cb)
+        assert torch.equal(rec[v], r1) and torch.equal(cnt[v], c1), v
+        if v in (0, 3):
+            ro, co = orc.project(S, sc.cam, view, codebook=cbo)
+            assert np.array_equal(rec[v].cpu().numpy().view(np.uint32), ro)
+            assert np.array_equal(cnt[v].cpu().numpy(), co)
+
+
+def test_project_bin_views_matches_single_view(env):
+    """csplat_project_bin_views: per view the same records, pair lists (with
+    block masks), tile ranges and pair counts as csplat_project_bin; also with
+    per-view active-tile masks (NEXT-4) and more views than one launch holds."""
+    torch, cs, dev = env["torch"], env["cs"], env["dev"]
+    sc = synth.window_scene(0, n=20000, n_keyframes=70)
+    g = cs.GaussianMap.from_numpy(sc.planes(), device=dev)
+    views = sc.views
+    cap = 0
+    for view in views:
+        _, cnt = cs.project(g, sc.cam, view)
+        cap = max(cap, int(cnt.sum().item()))
+    cap += 64
+    tx, ty = cs.tiles(sc.cam)
+    T = tx * ty
+    words = (T + 31) // 32
+    r = np.random.default_rng(5)
+    act = r.integers(0, 2**32, (len(views), words), dtype=np.uint64).astype(np.uint32)
+    act_t = torch.tensor(act.view(np.int32), device=dev)
+    for active in (None, act_t):
+        vb = cs.alloc_views(g.n, len(views), cap, sc.cam, dev)
+        cs.project_bin_views(g, sc.cam, views, vb, tile_active=active)
+        torch.cuda.synchronize()
+        for v in (0, 1, 33, 64, 69):
+            rec, cnt, b = cs.project_bin(g, sc.cam, views[v], cap, sync=True,
+                                         tile_active=None if active is None else active[v])
+            n = int(b["n_pairs_dev"].item())
+            assert n == int(vb["n_pairs_dev"][v].item())
+            assert torch.equal(vb["rec"][v], rec) and torch.equal(vb["count"][v], cnt)
+            assert torch.equal(vb["pair_gid"][v][:n], b["pair_gid"][:n])
+            assert torch.equal(vb["tile_range"][v], b["tile_range"])
