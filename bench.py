@@ -299,7 +299,7 @@ def bench_ba(dev, n_rays=65536, iters=5):
     (synthetic).  Device time per iteration (CUDA events, median)."""
     import torch
     from paper_2403_11247_b200 import csplat as cs
-    from paper_2403_11247_b200.ba import ba_loss_value, gpu_ba
+    from paper_2403_11247_b200.ba import BatchedBA, ba_loss_value
     from paper_2403_11247_b200.pipeline import RenderStep
     from scenes import synth
     sc = synth.window_scene(0)
@@ -313,7 +313,7 @@ def bench_ba(dev, n_rays=65536, iters=5):
         oc.append(st.img["color"].clone())
         od.append(st.img["depth"].clone())
     patches = synth.sample_patches(1, len(sc.views), sc.cam["width"], sc.cam["height"], n_rays)
-    ba = gpu_ba(st, sc.views, oc, od, patches, rank=0, world=1)
+    ba = BatchedBA(st, sc.views, oc, od, patches, rank=0, world=1)
     stream = torch.cuda.current_stream(dev)
     ba.run()
     torch.cuda.synchronize()

@@ -170,11 +170,17 @@ int csplat_project_views(const csplat_gaussians *g, const csplat_codebook *cb,
  * CSPLAT_OP_BIN_TILES, n, pair_capacity, cam), a multiple of 256; ws 256-byte
  * aligned), tile_active (optional) + v ceil(T/32) words.  Outputs bit-identical
  * to csplat_project_bin per view.  No host synchronisation (overflow: the
- * status slots). */
+ * status slots).  tile_lists (optional, NEXT-4's sparse views; needs
+ * tile_active): per view v at tile_lists + v list_stride a device int32 list
+ * {count, tile_0 < tile_1 < ...} of exactly the tiles set in its tile_active
+ * words, count <= max_list (host): only those tiles are sorted and get
+ * ranges, every other tile's range is empty (the same output as without the
+ * list, at max_list instead of T CTAs per view). */
 int csplat_project_bin_views(const csplat_gaussians *g, const csplat_codebook *cb,
                              const csplat_camera *cam, const csplat_view *views, int32_t n_views,
-                             const csplat_params *prm, const uint32_t *tile_active, void *rec,
-                             int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
+                             const csplat_params *prm, const uint32_t *tile_active,
+                             const int32_t *tile_lists, int64_t list_stride, int32_t max_list,
+                             void *rec, int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
                              uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                              size_t ws_bytes_per_view, void *stream);
 
@@ -340,6 +346,24 @@ int csplat_render_fwd(const void *rec, const uint32_t *pair_gid, const uint32_t 
                       const csplat_camera *cam, const csplat_params *prm, float *color,
                       float *depth, float *silhouette, float *t_final, int32_t *n_contrib,
                       void *stream);
+
+/* csplat_render_fwd / csplat_render_bwd over the tiles of a device list only
+ * (NEXT-4's sparse views: a few active tiles per keyframe): tile_list =
+ * {count, tile_0, tile_1, ...} (device int32, count <= max_tiles, the host's
+ * bound for the grid).  Pixels of other tiles are not written (forward) and
+ * not replayed (backward); everything else as the full calls. */
+int csplat_render_fwd_list(const void *rec, const uint32_t *pair_gid, const uint32_t *tile_range,
+                           const int32_t *tile_list, int32_t max_tiles, const csplat_camera *cam,
+                           const csplat_params *prm, float *color, float *depth, float *silhouette,
+                           float *t_final, int32_t *n_contrib, void *stream);
+int csplat_render_bwd_list(const csplat_gaussians *g, const csplat_codebook *cb,
+                           const csplat_camera *cam, const csplat_view *view,
+                           const csplat_params *prm, const void *rec, const uint32_t *pair_gid,
+                           const uint32_t *tile_range, const int32_t *tile_list,
+                           int32_t max_tiles, const float *t_final, const int32_t *n_contrib,
+                           const float *d_color, const float *d_depth, const float *d_silhouette,
+                           uint32_t flags, const csplat_grads *out, void *ws, size_t ws_bytes,
+                           void *stream);
 
 /* a7 + a8: backward of a6 through a3, a2-decode and the STE mask (Eq 6), with
  * the pose gradient (R14, R20, R22, R23).  d_color [3][H][W], d_depth,

@@ -119,8 +119,11 @@ def lib():
         L.csplat_render_bwd.argtypes = [vp] * 13 + [u32, vp, vp, C.c_size_t, vp]
         L.csplat_rvq_assign.argtypes = [vp, i64, vp, i32, vp, i32, i32, vp, i32, vp, vp]
         L.csplat_project_views.argtypes = [vp] * 4 + [i32, vp, vp, vp, vp]
-        L.csplat_project_bin_views.argtypes = [vp] * 4 + [i32] + [vp] * 4 + [i64] + \
-            [vp] * 4 + [C.c_size_t, vp]
+        L.csplat_project_bin_views.argtypes = [vp] * 4 + [i32] + [vp] * 3 + [i64, i32] + \
+            [vp] * 2 + [i64] + [vp] * 4 + [C.c_size_t, vp]
+        L.csplat_render_fwd_list.argtypes = [vp] * 4 + [i32] + [vp] * 8
+        L.csplat_render_bwd_list.argtypes = [vp] * 9 + [i32] + [vp] * 5 + [u32, vp, vp,
+                                                                       C.c_size_t, vp]
         L.csplat_chain_views.argtypes = [vp] * 4 + [i32, vp, vp, vp, u32, vp, vp]
         L.csplat_rvq_code_grad.argtypes = [vp, i64, vp, i32, vp, i32, i32, i32, vp, u32, vp]
         L.csplat_rvq_init_stage.argtypes = [vp, i64, i32, vp, i32, i32, i32, vp, i32, vp, vp]
@@ -504,7 +507,7 @@ def bin_tiles(rec, count, cam: dict, capacity: int, ws=None, out=None, sync=True
 
 
 def render_fwd(rec, pair_gid, tile_range, cam: dict, prm: Params | None = None, out=None,
-               stream=None):
+               stream=None, tile_list=None, max_tiles: int = 0):
     """a6.  Returns dict(color [3,H,W], depth, sil, t_final [H,W], n_contrib [H,W])."""
     H, W = cam["height"], cam["width"]
     dev = tile_range.device
@@ -513,6 +516,13 @@ def render_fwd(rec, pair_gid, tile_range, cam: dict, prm: Params | None = None, 
                    depth=torch.empty((H, W), device=dev), sil=torch.empty((H, W), device=dev),
                    t_final=torch.empty((H, W), device=dev),
                    n_contrib=torch.empty((H, W), dtype=torch.int32, device=dev))
+    if tile_list is not None:  # only the listed tiles ({count, tiles...})
+        _check(lib().csplat_render_fwd_list(
+            _ptr(rec), _ptr(pair_gid), _ptr(tile_range), _ptr(tile_list), int(max_tiles),
+            C.byref(camera(cam)), C.byref(prm or params()), _ptr(out["color"]), _ptr(out["depth"]),
+            _ptr(out["sil"]), _ptr(out["t_final"]), _ptr(out["n_contrib"]), _stream(stream)),
+            "csplat_render_fwd_list")
+        return out
     _check(lib().csplat_render_fwd(_ptr(rec), _ptr(pair_gid), _ptr(tile_range), C.byref(camera(cam)),
                                    C.byref(prm or params()), _ptr(out["color"]),
                                    _ptr(out["depth"]), _ptr(out["sil"]), _ptr(out["t_final"]),
@@ -563,7 +573,8 @@ def alloc_views(n: int, V: int, capacity: int, cam: dict, device):
 
 
 def project_bin_views(g: GaussianMap, cam: dict, views, out: dict, prm: Params | None = None,
-                      cb: CodebookT | None = None, tile_active=None, stream=None):
+                      cb: CodebookT | None = None, tile_active=None, tile_lists=None,
+                      max_list: int = 0, stream=None):
     """a1-a5 over V views (projection once per Gaussian + per-view bucket + one
     batched sort) into the per-view buffers of alloc_views."""
     V = len(views)
@@ -573,7 +584,9 @@ def project_bin_views(g: GaussianMap, cam: dict, views, out: dict, prm: Params |
     off = (-base) % 256                     # 256-byte aligned workspace base
     _check(lib().csplat_project_bin_views(
         C.byref(gs), _byref(cbs), C.byref(camera(cam)), _views_arr(views), V,
-        C.byref(prm or params()), _ptr(tile_active), _ptr(out["rec"]), _ptr(out["count"]),
+        C.byref(prm or params()), _ptr(tile_active), _ptr(tile_lists),
+        int(tile_lists.shape[1]) if tile_lists is not None else 0, int(max_list),
+        _ptr(out["rec"]), _ptr(out["count"]),
         out["capacity"], _ptr(out["pair_gid"]), _ptr(out["tile_range"]), _ptr(out["n_pairs_dev"]),
         C.c_void_p(base + off), out["ws_per_view"], _stream(stream)), "csplat_project_bin_views")
     return out
@@ -614,7 +627,8 @@ def alloc_grads(n: int, device="cuda", pose_only=False):
 
 def render_bwd(g: GaussianMap, cam: dict, v, rec, pair_gid, tile_range, t_final, n_contrib,
                d_color, d_depth, d_sil, prm: Params | None = None, cb: CodebookT | None = None,
-               flags: int = 0, grads=None, ws=None, stream=None):
+               flags: int = 0, grads=None, ws=None, stream=None, tile_list=None,
+               max_tiles: int = 0):
     """a7+a8.  Returns the grads dict (mean, opacity, rgb, log_scale, quat, mask, pose)."""
     n = g.n
     dev = g.opacity.device
@@ -625,6 +639,14 @@ def render_bwd(g: GaussianMap, cam: dict, v, rec, pair_gid, tile_range, t_final,
     gr = Grads(*[_ptr(grads.get(k)) for k in ("mean", "opacity", "rgb", "log_scale", "quat",
                                                "mask", "pose")])
     gs, cbs = g.struct(), cb.struct() if cb is not None else None
+    if tile_list is not None:  # only the listed tiles ({count, tiles...})
+        _check(lib().csplat_render_bwd_list(
+            C.byref(gs), _byref(cbs), C.byref(camera(cam)), C.byref(view(v)),
+            C.byref(prm or params()), _ptr(rec), _ptr(pair_gid), _ptr(tile_range), _ptr(tile_list),
+            int(max_tiles), _ptr(t_final), _ptr(n_contrib), _ptr(d_color), _ptr(d_depth),
+            _ptr(d_sil), flags, C.byref(gr), _ptr(ws), ws.numel(), _stream(stream)),
+            "csplat_render_bwd_list")
+        return grads
     if _on_device(v):
         _check(lib().csplat_render_bwd_dv(C.byref(gs), _byref(cbs), C.byref(camera(cam)), _ptr(v),
                                           C.byref(prm or params()), _ptr(rec), _ptr(pair_gid),

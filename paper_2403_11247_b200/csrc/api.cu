@@ -220,15 +220,16 @@ int csplat_project_views(const csplat_gaussians *g, const csplat_codebook *cb,
   return cuda_status(csplat::launch_project_views(*g, cb ? &d : nullptr, *cam, views, n_views,
                                                   mask_tau(prm->mask_eps), prm->dilation, rec,
                                                   count, nullptr, 0, 0, nullptr, 0, nullptr,
-                                                  nullptr, nullptr,
+                                                  nullptr, nullptr, nullptr, 0, 0,
                                                   static_cast<cudaStream_t>(stream)),
                      "csplat_project_views");
 }
 
 int csplat_project_bin_views(const csplat_gaussians *g, const csplat_codebook *cb,
                              const csplat_camera *cam, const csplat_view *views, int32_t n_views,
-                             const csplat_params *prm, const uint32_t *tile_active, void *rec,
-                             int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
+                             const csplat_params *prm, const uint32_t *tile_active,
+                             const int32_t *tile_lists, int64_t list_stride, int32_t max_list,
+                             void *rec, int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
                              uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                              size_t ws_bytes_per_view, void *stream) {
   RET_IF(check_gaussians(g));
@@ -254,6 +255,8 @@ int csplat_project_bin_views(const csplat_gaussians *g, const csplat_codebook *c
             "256-byte aligned");
     return CSPLAT_ERR_WORKSPACE;
   }
+  if (tile_lists && (!tile_active || max_list < 0))
+    return invalid("tile_lists needs tile_active and max_list >= 0");
   if (n_views == 0) return CSPLAT_OK;
   RET_IF(check_device());
   csplat::DecodeArgs d;
@@ -264,7 +267,8 @@ int csplat_project_bin_views(const csplat_gaussians *g, const csplat_codebook *c
                                                   mask_tau(prm->mask_eps), prm->dilation, rec,
                                                   count, ws, (int64_t)ws_bytes_per_view,
                                                   pair_capacity, tile_active, words, pair_gid,
-                                                  tile_range, n_pairs_dev,
+                                                  tile_range, n_pairs_dev, tile_lists,
+                                                  list_stride, max_list,
                                                   static_cast<cudaStream_t>(stream)),
                      "csplat_project_bin_views");
 }
@@ -610,6 +614,26 @@ int csplat_ba_patch_loss(const float *color, const float *depth, const float *ob
       "csplat_ba_patch_loss");
 }
 
+int csplat_render_fwd_list(const void *rec, const uint32_t *pair_gid, const uint32_t *tile_range,
+                           const int32_t *tile_list, int32_t max_tiles, const csplat_camera *cam,
+                           const csplat_params *prm, float *color, float *depth, float *silhouette,
+                           float *t_final, int32_t *n_contrib, void *stream) {
+  RET_IF(check_camera(cam));
+  if (!prm || !tile_range || !tile_list || !color || !depth || !silhouette || !t_final ||
+      !n_contrib || max_tiles < 0)
+    return invalid("render_fwd_list: NULL argument / max_tiles < 0");
+  if (!aligned16(rec)) {
+    set_err("rec must be 16-byte aligned");
+    return CSPLAT_ERR_ALIGNMENT;
+  }
+  RET_IF(check_device());
+  return cuda_status(csplat::launch_render_fwd(rec, pair_gid, tile_range, *cam, *prm, color, depth,
+                                               silhouette, t_final, n_contrib,
+                                               static_cast<cudaStream_t>(stream), 0, max_tiles,
+                                               tile_list),
+                     "csplat_render_fwd_list");
+}
+
 int csplat_render_fwd(const void *rec, const uint32_t *pair_gid, const uint32_t *tile_range,
                       const csplat_camera *cam, const csplat_params *prm, float *color,
                       float *depth, float *silhouette, float *t_final, int32_t *n_contrib,
@@ -635,7 +659,8 @@ static int render_bwd_impl(const csplat_gaussians *g, const csplat_codebook *cb,
                       const float *t_final, const int32_t *n_contrib, const float *d_color,
                       const float *d_depth, const float *d_silhouette, uint32_t flags,
                       const csplat_grads *out, void *ws, size_t ws_bytes, void *stream,
-                      const csplat::TrackingLoss *loss = nullptr) {
+                      const csplat::TrackingLoss *loss = nullptr, const int32_t *list = nullptr,
+                      int max_tiles = 0) {
   RET_IF(check_gaussians(g, false));
   RET_IF(check_camera(cam));
   RET_IF(check_codebook(cb, true));
@@ -660,8 +685,23 @@ static int render_bwd_impl(const csplat_gaussians *g, const csplat_codebook *cb,
                                                *prm, rec,
                                                pair_gid, tile_range, t_final, n_contrib, d_color,
                                                d_depth, d_silhouette, flags, *out, ws,
-                                               static_cast<cudaStream_t>(stream)),
+                                               static_cast<cudaStream_t>(stream), list, max_tiles),
                      "csplat_render_bwd");
+}
+
+int csplat_render_bwd_list(const csplat_gaussians *g, const csplat_codebook *cb,
+                           const csplat_camera *cam, const csplat_view *view,
+                           const csplat_params *prm, const void *rec, const uint32_t *pair_gid,
+                           const uint32_t *tile_range, const int32_t *tile_list,
+                           int32_t max_tiles, const float *t_final, const int32_t *n_contrib,
+                           const float *d_color, const float *d_depth, const float *d_silhouette,
+                           uint32_t flags, const csplat_grads *out, void *ws, size_t ws_bytes,
+                           void *stream) {
+  if (!view) return invalid("view NULL");
+  if (!tile_list || max_tiles < 0) return invalid("tile_list NULL / max_tiles < 0");
+  return render_bwd_impl(g, cb, cam, view, nullptr, prm, rec, pair_gid, tile_range, t_final,
+                         n_contrib, d_color, d_depth, d_silhouette, flags, out, ws, ws_bytes,
+                         stream, nullptr, tile_list, max_tiles);
 }
 
 int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,

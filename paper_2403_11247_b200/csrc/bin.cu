@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int64_t T, uint32_t *__restrict__ range, int64_t *__restrict__ n_pairs, BinWs w,
     int64_t cap, const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid, int tiles_x,
     int64_t tile0, SortViews sv) {
+  const int32_t *list = sv.list;
   if (gridDim.y > 1) {  // batched views: this CTA's view
     const int64_t v = blockIdx.y;
     w = ws_at(w, v * sv.ws_stride);
@@ -236,10 +237,15 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     pair_gid += v * sv.gid_stride;
     range += v * sv.range_stride;
     n_pairs += v;
+    if (list) list += v * sv.list_stride;
   }
   __shared__ __align__(16) unsigned long long sk[kCtaCap];
   __shared__ uint32_t fill, s_start, s_end;
-  const int64_t tile = tile0 + blockIdx.x;
+  // list mode: this CTA's list position; the look-back runs over positions
+  const int64_t pos = tile0 + blockIdx.x;
+  const int64_t npos = list ? (int64_t)list[0] : T;
+  if (pos >= npos) return;  // (block-uniform, before any barrier)
+  const int64_t tile = list ? (int64_t)list[1 + pos] : pos;
   const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
   // the common case first: a list that fits the threads' registers is sorted
   // BEFORE the look-back (the sort needs only the tile's own count), so by the
@@ -274,14 +280,14 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     const int lane = threadIdx.x;
     const unsigned long long cnt = w.cur[tile];
     unsigned long long prefix = 0;
-    for (int64_t j = tile - 1; j >= 0; j -= 32) {
+    for (int64_t j = pos - 1; j >= 0; j -= 32) {
       const int64_t jj = j - lane;
-      unsigned long long v = 0;  // before tile 0: an inclusive prefix of 0
+      unsigned long long v = 0;  // before position 0: an inclusive prefix of 0
       bool pub = true;
       if (jj >= 0) {
         const unsigned long long st = *reinterpret_cast<volatile unsigned long long *>(w.status + jj);
         pub = (st & kRangeP) != 0;
-        v = pub ? (st & ~kRangeP) : (unsigned long long)w.cur[jj];
+        v = pub ? (st & ~kRangeP) : (unsigned long long)w.cur[list ? list[1 + jj] : jj];
       }
       const unsigned pm = __ballot_sync(0xffffffffu, pub);
       const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest published prefix
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     }
     if (lane == 0) {
       const unsigned long long tot = prefix + cnt;
-      atomicExch(w.status + tile, kRangeP | tot);
+      atomicExch(w.status + pos, kRangeP | tot);
       const unsigned long long c = (unsigned long long)cap;
       // capacity overflow (csplat.h): a tile whose pairs do not all fit -- past
       // the capacity, or with bucket spill lost from a full overflow list --
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
       range[2 * tile] = s_start;
       range[2 * tile + 1] = s_end;
       if (cut) atomicOr(range + 2 * T, CSPLAT_STATUS_CAPACITY);
-      if (tile == T - 1) {
+      if (pos == npos - 1) {  // the last tile (position): the total
         *n_pairs = (int64_t)tot;
         atomicMax(range + 2 * T + 1, (uint32_t)(tot < 0xffffffffull ? tot : 0xffffffffull));
       }
@@ -357,12 +363,12 @@ cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t ca
   return cudaGetLastError();
 }
 
-cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
-                                    const void *rec, uint32_t *pair_gid, uint32_t *tile_range,
-                                    int64_t *n_pairs_dev, const SortViews &sv, int nv,
-                                    cudaStream_t s) {
-  if (T <= 0 || nv <= 0) return cudaSuccess;
-  const dim3 grid((unsigned)T, (unsigned)nv);
+cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t nctas, int64_t T, int tiles_x,
+                                    int64_t cap, const void *rec, uint32_t *pair_gid,
+                                    uint32_t *tile_range, int64_t *n_pairs_dev,
+                                    const SortViews &sv, int nv, cudaStream_t s) {
+  if (nctas <= 0 || nv <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)nctas, (unsigned)nv);
   k_sort_tiles<<<grid, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
                                              static_cast<const uint4 *>(rec), pair_gid, tiles_x, 0,
                                              sv);

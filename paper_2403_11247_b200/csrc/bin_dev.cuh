@@ -41,13 +41,19 @@ cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t ca
 // the same over nv views at once (grid.y = view): view v's workspace at
 // + v ws_stride bytes, records + v rec_stride (uint4 units), pair_gid + v
 // gid_stride, tile_range + v range_stride, n_pairs_dev + v
+// list (optional): per view a device tile list {count, tile_0 < tile_1 < ...}
+// at list + v list_stride -- only those tiles are sorted (their buckets hold
+// every pair: the bucket pass saw only those tiles), the offsets scan the list
+// positions, and the other tiles' ranges must be empty (zeroed by the caller)
 struct SortViews {
   int64_t ws_stride, rec_stride, gid_stride, range_stride;
+  const int32_t *list;
+  int64_t list_stride;
 };
-cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
-                                    const void *rec, uint32_t *pair_gid, uint32_t *tile_range,
-                                    int64_t *n_pairs_dev, const SortViews &sv, int nv,
-                                    cudaStream_t s);
+cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t nctas, int64_t T, int tiles_x,
+                                    int64_t cap, const void *rec, uint32_t *pair_gid,
+                                    uint32_t *tile_range, int64_t *n_pairs_dev,
+                                    const SortViews &sv, int nv, cudaStream_t s);
 
 // Warp-cooperative expansion of 32 Gaussians' tile rectangles.  Lane l holds
 // Gaussian base + l's pair count c, its pixel rectangle corners rx, ry (record

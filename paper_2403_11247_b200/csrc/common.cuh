@@ -430,6 +430,7 @@ cudaError_t launch_project_views(const csplat_gaussians &g, const DecodeArgs *de
                                  void *ws, int64_t ws_stride, int64_t cap,
                                  const uint32_t *active, int64_t active_stride,
                                  uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
+                                 const int32_t *tile_lists, int64_t list_stride, int max_list,
                                  cudaStream_t s);
 cudaError_t launch_chain_views(const csplat_gaussians &g, const DecodeArgs *dec,
                                const csplat_camera &cam, const csplat_view *views, int nv,
@@ -459,7 +460,8 @@ cudaError_t launch_render_fwd(const void *rec, const uint32_t *pair_gid,
                               const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
                               float *depth, float *sil, float *t_final, int32_t *n_contrib,
-                              cudaStream_t s, int tile0 = 0, int ntiles = -1);
+                              cudaStream_t s, int tile0 = 0, int ntiles = -1,
+                              const int32_t *list = nullptr);
 
 // csplat_project_bin_render: projection + bucket, then the per-tile sort and
 // the forward in tile chunks, the sort of chunk c+1 overlapping the forward
@@ -484,7 +486,8 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
                                     const uint32_t *pair_gid, const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
-                                    int64_t n, cudaStream_t s, int tile0, int ntiles);
+                                    int64_t n, cudaStream_t s, int tile0, int ntiles,
+                                    const int32_t *list = nullptr);
 
 // csplat_render_step: a3 .. a8 for one view -- projection + bucket, then per
 // tile chunk (on its own library stream) the sort, the forward and the
@@ -524,7 +527,8 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                               const uint32_t *tile_range, const float *t_final,
                               const int32_t *n_contrib, const float *d_color, const float *d_depth,
                               const float *d_sil, uint32_t flags, const csplat_grads &out,
-                              void *ws, cudaStream_t s);
+                              void *ws, cudaStream_t s, const int32_t *list = nullptr,
+                              int max_tiles = 0);
 
 cudaError_t launch_rvq(const float *x, int64_t n, const int64_t *n_dev, int d, const float *codes,
                        int L, int P, void *idx, int idx_bytes, float *recon, cudaStream_t s);

@@ -328,6 +328,7 @@ cudaError_t launch_project_views(const csplat_gaussians &g, const DecodeArgs *de
                                  void *ws, int64_t ws_stride, int64_t cap,
                                  const uint32_t *active, int64_t active_stride,
                                  uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
+                                 const int32_t *tile_lists, int64_t list_stride, int max_list,
                                  cudaStream_t s) {
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
@@ -369,9 +370,14 @@ cudaError_t launch_project_views(const csplat_gaussians &g, const DecodeArgs *de
     }
   }
   if (!bin) return cudaSuccess;
-  const SortViews sv{ws_stride, n * 4, cap, 2 * (T + 1)};
-  return launch_sort_tiles_views(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range, n_pairs_dev,
-                                 sv, nv, s);
+  const SortViews sv{ws_stride, n * 4, cap, 2 * (T + 1), tile_lists, list_stride};
+  if (tile_lists) {  // only the listed tiles get ranges: the others empty, the totals from 0
+    e = cudaMemset2DAsync(tile_range, (size_t)(T + 1) * 8, 0, (size_t)T * 8, (size_t)nv, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(n_pairs_dev, 0, (size_t)nv * sizeof(int64_t), s);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_sort_tiles_views(w, tile_lists ? max_list : T, T, ci.tiles_x, cap, rec, pair_gid,
+                                 tile_range, n_pairs_dev, sv, nv, s);
 }
 
 cudaError_t launch_project(const csplat_gaussians &g, const DecodeArgs *dec,

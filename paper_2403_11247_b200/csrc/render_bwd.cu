@@ -161,12 +161,14 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
     int tiles_x, float amax, const float *__restrict__ t_final,
     const int32_t *__restrict__ n_contrib, const float *__restrict__ dC,
     const float *__restrict__ dD, const float *__restrict__ dS, float *__restrict__ acc,
-    uint32_t *__restrict__ alive, LossArgs la, int tile0) {
+    uint32_t *__restrict__ alive, LossArgs la, int tile0, const int32_t *__restrict__ list) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   BwdSmem &sm = *reinterpret_cast<BwdSmem *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int tb = (int)blockIdx.x;
-  const int tile = tile0 + tb;
+  // list mode (NEXT-4 sparse views): CTA b replays list tile b of list[0]
+  if (list && tb >= list[0]) return;
+  const int tile = list ? list[1 + tb] : tile0 + tb;
   const int blk = wid;  // the warp's 8x8 block of the tile
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const uint32_t start = range[2 * tile];
@@ -401,7 +403,8 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
                                     const uint32_t *pair_gid, const uint32_t *tile_range, const float *t_final,
                                     const int32_t *n_contrib, const float *d_color,
                                     const float *d_depth, const float *d_sil, void *ws,
-                                    int64_t n, cudaStream_t s, int tile0, int ntiles) {
+                                    int64_t n, cudaStream_t s, int tile0, int ntiles,
+                                    const int32_t *list) {
   const CamInfo ci = cam_info(cam);
   float *acc = static_cast<float *>(ws);
   uint32_t *alive = bwd_alive_bits(ws, n);
@@ -436,11 +439,11 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
     la.loss3 = loss->loss3;
     k_render_bwd<true><<<ntiles, kBwdThreads, smem, s>>>(
         tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, nullptr, nullptr, nullptr, acc, alive, la, tile0);
+        t_final, n_contrib, nullptr, nullptr, nullptr, acc, alive, la, tile0, list);
   } else {
     k_render_bwd<false><<<ntiles, kBwdThreads, smem, s>>>(
         tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-        t_final, n_contrib, d_color, d_depth, d_sil, acc, alive, la, tile0);
+        t_final, n_contrib, d_color, d_depth, d_sil, acc, alive, la, tile0, list);
   }
   return cudaGetLastError();
 }
@@ -452,11 +455,11 @@ cudaError_t launch_render_bwd(const csplat_gaussians &g, const DecodeArgs *dec,
                               const uint32_t *tile_range, const float *t_final,
                               const int32_t *n_contrib, const float *d_color, const float *d_depth,
                               const float *d_sil, uint32_t flags, const csplat_grads &out,
-                              void *ws, cudaStream_t s) {
+                              void *ws, cudaStream_t s, const int32_t *list, int max_tiles) {
   cudaError_t e = bwd_prep(g, flags, out, ws, loss, s);
   if (e != cudaSuccess) return e;
   e = launch_render_bwd_tiles(cam, loss, prm, rec, pair_gid, tile_range, t_final, n_contrib, d_color,
-                              d_depth, d_sil, ws, g.n, s, 0, -1);
+                              d_depth, d_sil, ws, g.n, s, 0, list ? max_tiles : -1, list);
   if (e != cudaSuccess || g.n == 0 || (flags & CSPLAT_SKIP_CHAIN)) return e;
   return launch_chain(g, dec, cam, view, view_dev, prm, rec, static_cast<float *>(ws), flags,
                       out, s);

@@ -80,13 +80,15 @@ __global__ void __launch_bounds__((kPW + 1) * 32) k_render_fwd(
     const uint32_t *__restrict__ range, int W, int H,
     int tiles_x, float amax, float tmin, float *__restrict__ color, float *__restrict__ depth,
     float *__restrict__ sil, float *__restrict__ t_final, int32_t *__restrict__ n_contrib,
-    int tile0) {
+    int tile0, const int32_t *__restrict__ list) {
   __shared__ __align__(128) float4 buf[kStages][kBatch * 4];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ uint32_t msk[kStages][kBatch];  // the entries' 8x8-block cull masks
   __shared__ int done_cnt, end_b;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tile = tile0 + (int)blockIdx.x;
+  // list mode (NEXT-4 sparse views): CTA b renders list tile b of list[0]
+  if (list && (int)blockIdx.x >= list[0]) return;
+  const int tile = list ? list[1 + blockIdx.x] : tile0 + (int)blockIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
   const int len = (int)(end - start);
@@ -194,7 +196,7 @@ cudaError_t launch_render_fwd(const void *rec, const uint32_t *pair_gid,
                               const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
                               float *depth, float *sil, float *t_final, int32_t *n_contrib,
-                              cudaStream_t s, int tile0, int ntiles) {
+                              cudaStream_t s, int tile0, int ntiles, const int32_t *list) {
   const CamInfo ci = cam_info(cam);
   const int T = ci.tiles_x * ci.tiles_y;
   if (ntiles < 0) ntiles = T - tile0;
@@ -204,7 +206,7 @@ cudaError_t launch_render_fwd(const void *rec, const uint32_t *pair_gid,
   if (e != cudaSuccess) return e;
   k_render_fwd<<<ntiles, (kPW + 1) * 32, 0, s>>>(
       tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
-      prm.t_min, color, depth, sil, t_final, n_contrib, tile0);
+      prm.t_min, color, depth, sil, t_final, n_contrib, tile0, list);
   return cudaGetLastError();
 }
 

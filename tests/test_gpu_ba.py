@@ -104,13 +104,14 @@ def test_ba_patch_loss_parity(env):
         assert np.abs(a - r).max() <= 1e-5 * max(np.abs(r).max(), 1e-6)
 
 
-@pytest.mark.parametrize("seed", [0, 1])
-def test_ba_iteration_parity(env, seed):
+@pytest.mark.parametrize("seed,driver", [(0, "pipelined"), (1, "pipelined"), (0, "batched"),
+                                         (1, "batched")])
+def test_ba_iteration_parity(env, seed, driver):
     """One BA iteration over 4 keyframes (RenderStep: prune -> project ->
     active bin -> fwd -> loss -> bwd ACCUMULATE) against the oracle's sum of
     per-keyframe gradients on the pruned map; per-keyframe pose gradients."""
     torch, cs, orc, dev = env["torch"], env["cs"], env["orc"], env["dev"]
-    from paper_2403_11247_b200.ba import ba_loss_value, gpu_ba
+    from paper_2403_11247_b200.ba import BatchedBA, ba_loss_value, gpu_ba
     from paper_2403_11247_b200.pipeline import RenderStep
     sc = synth.mid_scene(20 + seed)
     cam = sc.cam
@@ -153,7 +154,10 @@ def test_ba_iteration_parity(env, seed):
     st.size_pairs(rviews[0], views=rviews[1:])
     oc = [torch.tensor(o[0], device=dev) for o in obs]
     od = [torch.tensor(o[1], device=dev) for o in obs]
-    ba = gpu_ba(st, rviews, oc, od, patches, rank=0, world=1)
+    if driver == "batched":  # one multi-view front, tile-list renders, one chain over views
+        ba = BatchedBA(st, rviews, oc, od, patches, rank=0, world=1)
+    else:
+        ba = gpu_ba(st, rviews, oc, od, patches, rank=0, world=1)
     ba.run()
     torch.cuda.synchronize()
     assert ba.n_rays == n_rays and int(ba.n_valid.item()) == n_valid
