@@ -9,17 +9,22 @@
 //               key = bits(z_c) << 32 | index goes into its tile's fixed-size
 //               bucket (slot from the tile's atomic cursor, order fixed in 3),
 //               or, once the bucket is full, into one shared overflow list;
-//   2. sort:    one CTA per tile finds its output offset (the exclusive scan of
-//               the T cursor values, by a decoupled look-back that never waits:
-//               every tile's count is already final) -> tile_range [start, end),
-//               gathers its bucket (+ its overflow entries),
-//               sorts it in shared memory (bitonic network, all-ascending form,
-//               no padding; warp-local stages synchronise only the warp), then
-//               writes pair_gid and the pair-ordered 64-byte record payload
-//               that the renderer streams with TMA bulk copies (word 14 of the
-//               payload: the pair's 8x8-block cull mask, block_mask below).
+//   2. scan:    one CTA per view: the exclusive scan of the T cursor values
+//               (the tiles' pair counts, all final once the bucket pass ends)
+//               -> every tile's output offset, in the look-up words;
+//   3. sort:    one CTA per tile reads its offset -> tile_range [start, end),
+//               gathers its bucket (+ its overflow entries), sorts it
+//               (registers for <= 256 keys, else shared memory: bitonic
+//               network, all-ascending form, no padding; warp-local stages
+//               synchronise only the warp), then writes its pair entries
+//               (Gaussian index | 8x8-block cull mask << 28, pair_entry below).
 //               Buckets longer than the CTA's shared-memory slice are sorted in
 //               global memory (pathological inputs only).
+// The offsets were first found by a decoupled look-back inside the sort
+// (round 1); with ~1.6k tiles per launch all resident at once, the look-back
+// walked back over many not-yet-published tiles (two dependent L2 loads per 32
+// tiles) and was the sort's top stall (profiles/r2b_kernels.md), so the scan
+// is a separate ~2 us kernel and the sort CTAs never touch another tile.
 // Keys are unique (the index is in the low word), so the order is unique and
 // bit-exact: (tile, bits(z_c), index) ascending.
 #include "bin_dev.cuh"
@@ -218,13 +223,68 @@ __device__ __forceinline__ void sort_regs256(unsigned long long &x0, unsigned lo
   }
 }
 
-// One 128-thread CTA per tile: enough warps in flight to hide the latency of
-// the record gathers in emit_sorted (there are only ~3k tiles per view).
-// Tile-range scan status words: bit 63 set = inclusive prefix through the tile
-// published (bits 0-62); the tiles' own counts are the bucket cursors, all known
-// when k_sort_tiles starts, so a tile never waits for a predecessor.
-constexpr unsigned long long kRangeP = 1ull << 63;
+// a5 offsets: the exclusive scan of the tiles' (or list positions') pair counts
+// into the look-up words, one CTA per view (grid.x = view)
+constexpr int kScanThreads = 1024, kScanPer = 4;
+__global__ void __launch_bounds__(kScanThreads) k_tile_scan(int64_t T, BinWs w, int64_t ws_stride,
+                                                            const int32_t *__restrict__ list,
+                                                            int64_t list_stride) {
+  if (blockIdx.x > 0) {
+    w = ws_at(w, (int64_t)blockIdx.x * ws_stride);
+    if (list) list += (int64_t)blockIdx.x * list_stride;
+  }
+  __shared__ unsigned long long wsum[32];
+  const int64_t npos = list ? (int64_t)list[0] : T;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  unsigned long long carry = 0;
+  for (int64_t base = 0; base < npos; base += kScanThreads * kScanPer) {
+    uint32_t c[kScanPer];
+    unsigned long long own = 0;
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      const int64_t p = base + (int64_t)t * kScanPer + k;
+      c[k] = p < npos ? w.cur[list ? list[1 + p] : p] : 0u;
+      own += c[k];
+    }
+    unsigned long long inc = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long v = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    unsigned long long ex = carry + (wid > 0 ? wsum[wid - 1] : 0ull) + inc - own;
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+      const int64_t p = base + (int64_t)t * kScanPer + k;
+      if (p < npos) w.status[p] = ex;
+      ex += c[k];
+    }
+    carry += wsum[31];
+    __syncthreads();  // wsum is rewritten by the next round
+  }
+}
 
+cudaError_t launch_tile_scan(const BinWs &w, int64_t T, int nv, int64_t ws_stride,
+                             const int32_t *list, int64_t list_stride, cudaStream_t s) {
+  if (nv <= 0) return cudaSuccess;
+  k_tile_scan<<<(unsigned)nv, kScanThreads, 0, s>>>(T, w, ws_stride, list, list_stride);
+  return cudaGetLastError();
+}
+
+// One 128-thread CTA per tile: enough warps in flight to hide the latency of
+// the record gathers in pair_entry (there are only ~3k tiles per view).
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int64_t T, uint32_t *__restrict__ range, int64_t *__restrict__ n_pairs, BinWs w,
     int64_t cap, const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid, int tiles_x,
@@ -240,91 +300,50 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     if (list) list += v * sv.list_stride;
   }
   __shared__ __align__(16) unsigned long long sk[kCtaCap];
-  __shared__ uint32_t fill, s_start, s_end;
-  // list mode: this CTA's list position; the look-back runs over positions
+  __shared__ uint32_t fill;
+  // list mode: this CTA's list position; the offsets are over positions
   const int64_t pos = tile0 + blockIdx.x;
   const int64_t npos = list ? (int64_t)list[0] : T;
   if (pos >= npos) return;  // (block-uniform, before any barrier)
   const int64_t tile = list ? (int64_t)list[1 + pos] : pos;
   const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
-  // the common case first: a list that fits the threads' registers is sorted
-  // BEFORE the look-back (the sort needs only the tile's own count), so by the
-  // time the look-back runs the preceding tiles have mostly published and the
-  // CTA does not idle at a barrier behind it
   const uint32_t cnt_t = w.cur[tile];
-  const bool reg_path = cnt_t <= 2u * kSortThreads;  // block-uniform
-  unsigned long long x0 = ~0ull, x1 = ~0ull;
-  if (reg_path && cnt_t > 0) {
-    const int t = threadIdx.x, n0 = (int)cnt_t;
+  const unsigned long long prefix = w.status[pos];  // k_tile_scan's exclusive offset
+  // capacity overflow (csplat.h): a tile whose pairs do not all fit -- past
+  // the capacity, or with bucket spill lost from a full overflow list -- gets
+  // an EMPTY range (the renderers treat it as background) and sets the status
+  // bit; every other tile's list is exact
+  const unsigned long long tot = prefix + cnt_t, c = (unsigned long long)cap;
+  const bool cut = tot > c || (cnt_t > (uint32_t)kBucketCap && (int64_t)*w.ovf_n > cap);
+  const uint32_t start = (uint32_t)(prefix < c ? prefix : c);
+  const uint32_t end = cut ? start : (uint32_t)tot;
+  if (threadIdx.x == 0) {
+    range[2 * tile] = start;
+    range[2 * tile + 1] = end;
+    if (cut) atomicOr(range + 2 * T, CSPLAT_STATUS_CAPACITY);
+    if (pos == npos - 1) {  // the last tile (position): the total
+      *n_pairs = (int64_t)tot;
+      atomicMax(range + 2 * T + 1, (uint32_t)(tot < 0xffffffffull ? tot : 0xffffffffull));
+    }
+  }
+  const int len = (int)(end - start);  // the tile's pair count, or 0 (empty or cut)
+  if (len == 0) return;                // (block-uniform)
+  if (len <= 2 * kSortThreads) {  // the common case: sorted in registers
+    const int t = threadIdx.x;
     const unsigned long long *bk = w.bucket + tile * kBucketCap;
-    if (2 * t + 1 < n0) {
+    unsigned long long x0 = ~0ull, x1 = ~0ull;
+    if (2 * t + 1 < len) {
       const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(bk)[t];
       x0 = v.x;
       x1 = v.y;
-    } else if (2 * t < n0) {
+    } else if (2 * t < len) {
       x0 = bk[2 * t];
     }
     int np2 = 2;
-    while (np2 < n0) np2 <<= 1;
+    while (np2 < len) np2 <<= 1;
     sort_regs256(x0, x1, np2, reinterpret_cast<unsigned long long(*)[2 * kSortThreads]>(sk));
-  }
-  // the entries (index | block mask) need only the sorted keys and the records:
-  // gather + mask them now, so the record loads' latency overlaps the look-back
-  uint32_t e0 = 0, e1 = 0;
-  if (reg_path) {
-    const int t = threadIdx.x;
-    if (2 * t < (int)cnt_t) e0 = pair_entry(x0, rec4, X0, Y0);
-    if (2 * t + 1 < (int)cnt_t) e1 = pair_entry(x1, rec4, X0, Y0);
-  }
-  if (threadIdx.x < 32) {  // the tile's output offset: a look-back over the preceding tiles
-    const int lane = threadIdx.x;
-    const unsigned long long cnt = w.cur[tile];
-    unsigned long long prefix = 0;
-    for (int64_t j = pos - 1; j >= 0; j -= 32) {
-      const int64_t jj = j - lane;
-      unsigned long long v = 0;  // before position 0: an inclusive prefix of 0
-      bool pub = true;
-      if (jj >= 0) {
-        const unsigned long long st = *reinterpret_cast<volatile unsigned long long *>(w.status + jj);
-        pub = (st & kRangeP) != 0;
-        v = pub ? (st & ~kRangeP) : (unsigned long long)w.cur[list ? list[1 + jj] : jj];
-      }
-      const unsigned pm = __ballot_sync(0xffffffffu, pub);
-      const int stop = pm ? __ffs(pm) - 1 : 32;  // nearest published prefix
-      unsigned long long add = lane <= stop ? v : 0ull;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
-      prefix += add;
-      if (pm) break;
-    }
-    if (lane == 0) {
-      const unsigned long long tot = prefix + cnt;
-      atomicExch(w.status + pos, kRangeP | tot);
-      const unsigned long long c = (unsigned long long)cap;
-      // capacity overflow (csplat.h): a tile whose pairs do not all fit -- past
-      // the capacity, or with bucket spill lost from a full overflow list --
-      // gets an EMPTY range (the renderers treat it as background) and sets
-      // the status bit; every other tile's list is exact
-      const bool cut = tot > c || (cnt > (unsigned long long)kBucketCap && (int64_t)*w.ovf_n > cap);
-      s_start = (uint32_t)(prefix < c ? prefix : c);
-      s_end = cut ? s_start : (uint32_t)tot;
-      range[2 * tile] = s_start;
-      range[2 * tile + 1] = s_end;
-      if (cut) atomicOr(range + 2 * T, CSPLAT_STATUS_CAPACITY);
-      if (pos == npos - 1) {  // the last tile (position): the total
-        *n_pairs = (int64_t)tot;
-        atomicMax(range + 2 * T + 1, (uint32_t)(tot < 0xffffffffull ? tot : 0xffffffffull));
-      }
-    }
-  }
-  __syncthreads();
-  const uint32_t start = s_start, end = s_end;
-  const int len = (int)(end - start);  // the tile's pair count, or 0 (empty or cut)
-  if (len == 0) return;
-  if (reg_path) {  // sorted and masked above; len is cnt_t (or 0 when cut)
-    const int t = threadIdx.x;
-    if (2 * t < len) pair_gid[(int64_t)start + 2 * t] = e0;
-    if (2 * t + 1 < len) pair_gid[(int64_t)start + 2 * t + 1] = e1;
+    if (2 * t < len) pair_gid[(int64_t)start + 2 * t] = pair_entry(x0, rec4, X0, Y0);
+    if (2 * t + 1 < len) pair_gid[(int64_t)start + 2 * t + 1] = pair_entry(x1, rec4, X0, Y0);
     return;
   }
   unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
@@ -337,17 +356,12 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     const int64_t no = min((int64_t)*w.ovf_n, cap);
     for (int64_t o = threadIdx.x; o < no; o += kSortThreads)
       if (w.ovf_tile[o] == (uint32_t)tile) {
-        const uint32_t pos = atomicAdd(&fill, 1u);
-        if (pos < (uint32_t)len) a[pos] = w.ovf_key[o];
+        const uint32_t q = atomicAdd(&fill, 1u);
+        if (q < (uint32_t)len) a[q] = w.ovf_key[o];
       }
   }
   __syncthreads();
-  if (len <= 32) {  // one warp sorts a short list; the others only help emit
-    if (threadIdx.x < 32) bitonic_sort(a, len, threadIdx.x, 32, [] { __syncwarp(); });
-    __syncthreads();
-  } else {
-    bitonic_sort(a, len, threadIdx.x, kSortThreads, [] { __syncthreads(); });
-  }
+  bitonic_sort(a, len, threadIdx.x, kSortThreads, [] { __syncthreads(); });
   emit_sorted(a, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, X0, Y0);
 }
 
@@ -397,6 +411,7 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   if (n > 0) k_bucket<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, cap,
                                                       tile_active, w);
   e = cudaGetLastError();
+  if (e == cudaSuccess) e = launch_tile_scan(w, T, 1, 0, nullptr, 0, s);
   if (e != cudaSuccess) return e;
   return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range,
                            n_pairs_dev, s);

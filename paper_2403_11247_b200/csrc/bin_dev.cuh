@@ -12,7 +12,7 @@ constexpr int kBucketCap = 512;    // bucket slots per tile; later pairs go to t
 struct BinWs {
   uint32_t *cur;                     // [T] pairs per tile (atomic cursor)
   uint32_t *ovf_n;                   // overflow-list length
-  unsigned long long *status;        // [T] look-back words of the tile-range scan
+  unsigned long long *status;        // [T] each tile's (list position's) output offset (k_tile_scan)
   unsigned long long *bucket;        // [T][kBucketCap] keys
   uint32_t *ovf_tile;                // [cap] tile of each overflow entry
   unsigned long long *ovf_key;       // [cap] its key
@@ -27,13 +27,19 @@ __host__ __device__ __forceinline__ BinWs ws_at(BinWs w, int64_t off) {
   w.ovf_tile = mv(w.ovf_tile); w.ovf_key = mv(w.ovf_key); w.keys = mv(w.keys);
   return w;
 }
-// bytes of the head (cursors, overflow length, look-back words) bin_reset zeroes
+// bytes of the head (cursors, overflow length, offset words) bin_reset zeroes
 size_t bin_head_bytes(int64_t T);
-// zero the cursors, the overflow length and the look-back words (one memset)
+// zero the cursors, the overflow length and the offset words (one memset)
 cudaError_t bin_reset(const BinWs &w, int64_t T, cudaStream_t s);
-// a5: k_sort_tiles over the buckets filled by k_bucket or the fused projection
-// (tiles [tile0, tile0 + ntiles) only, ntiles < 0 = to the end: the tile-range
-// look-back never waits, so any split of the tiles into launches is valid)
+// a5 offsets: the exclusive scan of the pair counts of nv views' tiles (view v's
+// workspace at + v ws_stride bytes; list: per view a tile list as below, the
+// scan then runs over its positions) -- after the bucket pass, before the sort
+cudaError_t launch_tile_scan(const BinWs &w, int64_t T, int nv, int64_t ws_stride,
+                             const int32_t *list, int64_t list_stride, cudaStream_t s);
+// a5: k_sort_tiles over the buckets filled by k_bucket or the fused projection,
+// after launch_tile_scan (tiles [tile0, tile0 + ntiles) only, ntiles < 0 = to
+// the end: every tile reads only its own offset, so any split of the tiles
+// into launches is valid)
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
                               const void *rec, uint32_t *pair_gid,
                               uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,

@@ -337,7 +337,7 @@ cudaError_t launch_project_views(const csplat_gaussians &g, const DecodeArgs *de
   cudaError_t e = cudaSuccess;
   if (bin) {
     w = bin_carve(ws, cap, T);
-    // every view's head (cursors, overflow length, look-back words): one 2-D memset
+    // every view's head (cursors, overflow length, offset words): one 2-D memset
     e = cudaMemset2DAsync(ws, (size_t)ws_stride, 0, bin_head_bytes(T), (size_t)nv, s);
     if (e != cudaSuccess) return e;
   }
@@ -376,6 +376,8 @@ cudaError_t launch_project_views(const csplat_gaussians &g, const DecodeArgs *de
     if (e == cudaSuccess) e = cudaMemsetAsync(n_pairs_dev, 0, (size_t)nv * sizeof(int64_t), s);
     if (e != cudaSuccess) return e;
   }
+  if ((e = launch_tile_scan(w, T, nv, ws_stride, tile_lists, list_stride, s)) != cudaSuccess)
+    return e;
   return launch_sort_tiles_views(w, tile_lists ? max_list : T, T, ci.tiles_x, cap, rec, pair_gid,
                                  tile_range, n_pairs_dev, sv, nv, s);
 }
@@ -401,6 +403,7 @@ cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
   if (e != cudaSuccess) return e;
   e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
                           ci.tiles_x, cap, tile_active, s);
+  if (e == cudaSuccess) e = launch_tile_scan(w, T, 1, 0, nullptr, 0, s);
   if (e != cudaSuccess) return e;
   return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range,
                            n_pairs_dev, s);
@@ -482,6 +485,7 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
     return e;
   e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
                           ci.tiles_x, cap, nullptr, s);
+  if (e == cudaSuccess) e = launch_tile_scan(w, T, 1, 0, nullptr, 0, s);
   if (e != cudaSuccess) return e;
   // fork into K streams, one tile chunk each: sort the chunk, render it (and
   // run its backward); the chunks run concurrently, so one chunk's issue-bound
