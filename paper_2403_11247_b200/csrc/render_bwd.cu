@@ -95,9 +95,22 @@ struct BPix2 {
   int last0, last1;
 };
 
-__device__ __forceinline__ bool bwd_pair(BPix2 &P, int j, float dx, f2_t DY, const float4 &r0,
-                                         const float4 &r1, const float4 &r2, float amax,
-                                         float (&v)[kV]) {
+// bwd_pair in three pieces, so two entries can be interleaved (bwd_two): the
+// per-entry front (q, validity, G, alpha, 1/(1 - alpha), v -- independent of
+// the pixels' replay state), the state update (T_j, v - B, B: the only
+// loop-carried part) and the partials (independent again).
+struct BFront {
+  f2_t G, AL, RC, VV, DY;
+  float dx;
+  bool nc0, nc1, any;  // alpha below the cap (R23), either pixel composites
+};
+
+__device__ __forceinline__ BFront bwd_front(const BPix2 &P, int j, float dx, f2_t DY,
+                                            const float4 &r0, const float4 &r1,
+                                            const float4 &r2, float amax) {
+  BFront F;
+  F.dx = dx;
+  F.DY = DY;
   const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
   const f2_t Y = mul2(mul2(pk2(r1.x, r1.x), DY), DY);
   const f2_t X = fma2(pk2(cbdx, cbdx), DY, Y);
@@ -105,30 +118,46 @@ __device__ __forceinline__ bool bwd_pair(BPix2 &P, int j, float dx, f2_t DY, con
   const float q0 = lo2(Q), q1 = hi2(Q);
   const bool val0 = (j < P.last0) & da_in_range(q0, r1.z);
   const bool val1 = (j < P.last1) & da_in_range(q1, r1.z);
+  F.any = val0 | val1;
   const f2_t QM = pk2(val0 ? q0 : __int_as_float(0x7f800000), val1 ? q1 : __int_as_float(0x7f800000));
   const f2_t QE = mul2(QM, pk2(-0.72134752f, -0.72134752f));
-  const f2_t G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
-  const f2_t AR = mul2(pk2(r1.y, r1.y), G);
-  const f2_t AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));  // R1
-  const f2_t OM = sub2(pk2(1.0f, 1.0f), AL);
+  F.G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
+  const f2_t AR = mul2(pk2(r1.y, r1.y), F.G);
+  F.AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));  // R1
+  F.nc0 = lo2(AR) < amax;
+  F.nc1 = hi2(AR) < amax;
+  const f2_t OM = sub2(pk2(1.0f, 1.0f), F.AL);
   float rc0, rc1;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));  // alpha <= alpha_max < 1
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc1) : "f"(hi2(OM)));
-  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(P.T) : "l"(pk2(rc0, rc1)));
-  const f2_t W = mul2(AL, P.T);
-  const f2_t VV = fma2(pk2(r2.x, r2.x), P.gr,
-                       fma2(pk2(r2.y, r2.y), P.gg,
-                            fma2(pk2(r2.z, r2.z), P.gb, fma2(pk2(r1.w, r1.w), P.gd, P.gs))));
-  const f2_t VB = sub2(VV, P.B);
-  const f2_t D0 = mul2(P.T, VB);
+  F.RC = pk2(rc0, rc1);
+  F.VV = fma2(pk2(r2.x, r2.x), P.gr,
+              fma2(pk2(r2.y, r2.y), P.gg,
+                   fma2(pk2(r2.z, r2.z), P.gb, fma2(pk2(r1.w, r1.w), P.gd, P.gs))));
+  return F;
+}
+
+// the loop-carried part: T_j = T_{j+1} / (1 - alpha_j); returns T_j and v - B;
+// B_{j-1} = B_j + alpha_j (v_j - B_j)
+__device__ __forceinline__ void bwd_state(BPix2 &P, const BFront &F, f2_t &T, f2_t &VB) {
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(P.T) : "l"(F.RC));
+  T = P.T;
+  VB = sub2(F.VV, P.B);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(P.B) : "l"(F.AL), "l"(VB));
+}
+
+__device__ __forceinline__ void bwd_partials(const BPix2 &P, const BFront &F, f2_t T, f2_t VB,
+                                             float (&v)[kV]) {
+  const f2_t W = mul2(F.AL, T);
+  const f2_t D0 = mul2(T, VB);
   // R23: no gradient through a capped alpha
-  const f2_t DL = pk2(lo2(AR) < amax ? lo2(D0) : 0.0f, hi2(AR) < amax ? hi2(D0) : 0.0f);
-  const f2_t AV = mul2(AL, DL);
-  const f2_t GD = mul2(G, DL);
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(P.B) : "l"(AL), "l"(VB));
-  const f2_t TT = mul2(AV, DY);
-  const f2_t T2 = mul2(TT, DY);
+  const f2_t DL = pk2(F.nc0 ? lo2(D0) : 0.0f, F.nc1 ? hi2(D0) : 0.0f);
+  const f2_t AV = mul2(F.AL, DL);
+  const f2_t GD = mul2(F.G, DL);
+  const f2_t TT = mul2(AV, F.DY);
+  const f2_t T2 = mul2(TT, F.DY);
   const f2_t WD = mul2(W, P.gd), WR = mul2(W, P.gr), WG = mul2(W, P.gg), WB = mul2(W, P.gb);
+  const float dx = F.dx;
   const float sx = dx * (lo2(AV) + hi2(AV));
   const float sy = lo2(TT) + hi2(TT);
   v[0] = sx;
@@ -141,7 +170,16 @@ __device__ __forceinline__ bool bwd_pair(BPix2 &P, int j, float dx, f2_t DY, con
   v[7] = lo2(WR) + hi2(WR);
   v[8] = lo2(WG) + hi2(WG);
   v[9] = lo2(WB) + hi2(WB);
-  return val0 | val1;
+}
+
+__device__ __forceinline__ bool bwd_pair(BPix2 &P, int j, float dx, f2_t DY, const float4 &r0,
+                                         const float4 &r1, const float4 &r2, float amax,
+                                         float (&v)[kV]) {
+  const BFront F = bwd_front(P, j, dx, DY, r0, r1, r2, amax);
+  f2_t T, VB;
+  bwd_state(P, F, T, VB);
+  bwd_partials(P, F, T, VB, v);
+  return F.any;
 }
 
 // NEXT-1 loss-fused mode: the upstream gradients are
@@ -345,21 +383,9 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
       // block mask (payload word 14, bin.cu) and replay range (j < wmax)
       const uint32_t bml = lane < cnt ? sm.msk[s][lane] : 0u;
       uint32_t todo = __ballot_sync(0xffffffffu, ((bml >> blk) & 1u) && b * kBB + lane < wmax);
-      while (todo) {  // back to front
-        int e;  // the highest set bit (bfind = 31 - clz in one instruction)
-        asm("bfind.u32 %0, %1;" : "=r"(e) : "r"(todo));
-        uint32_t below;  // bits 0 .. e-1
-        asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(e));
-        todo &= below;
-        const int j = b * kBB + e;
-        const float4 r0 = rb[e * 4 + 0];
-        const float4 r1 = rb[e * 4 + 1];
-        const float4 r2 = rb[e * 4 + 2];
-        float v[kV];
-        const bool a = bwd_pair(P, j, DSUB(fpx, r0.x), sub2(FPY, pk2(r0.y, r0.y)), r0, r1, r2,
-                                amax, v);
-        if (!__any_sync(0xffffffffu, a)) continue;
-        // every lane writes its (possibly zero) partials as row nq*kV + c
+      // entry e's lane partials as rows nq*kV + c of the warp's reduction
+      // buffer (every lane, possibly zeros); a full group is reduced
+      auto push = [&](int e, const float (&v)[kV]) {
 #pragma unroll
         for (int c = 0; c < kV; c++) red[nq * kV + c][lane] = v[c];
         ents = ents * 256u + (uint32_t)e;  // entry q of the group in byte nq - 1 - q
@@ -371,6 +397,44 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
           nq = 0;
           ents = 0;
         }
+      };
+      auto top = [&]() {  // the highest set bit of todo (bfind), cleared
+        int e;
+        asm("bfind.u32 %0, %1;" : "=r"(e) : "r"(todo));
+        uint32_t below;  // bits 0 .. e-1
+        asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(below) : "r"(e));
+        todo &= below;
+        return e;
+      };
+      while (todo) {  // back to front
+        const int e1 = top();
+        const float4 a0 = rb[e1 * 4 + 0], a1 = rb[e1 * 4 + 1], a2 = rb[e1 * 4 + 2];
+        if (todo) {
+          // two entries e1 > e2 at once: both fronts, the two state updates in
+          // replay order, both partials -- the independent halves interleave
+          // (one warp issues in order: with one entry per iteration its long
+          // dependent chain left ~35% of issue slots empty; C2 backward kernel
+          // 178.8 -> 167.9 us; 4 CTAs/SM with the registers to spare: 174.0)
+          const int e2 = top();
+          const float4 b0 = rb[e2 * 4 + 0], b1 = rb[e2 * 4 + 1], b2 = rb[e2 * 4 + 2];
+          const BFront FA = bwd_front(P, b * kBB + e1, DSUB(fpx, a0.x),
+                                      sub2(FPY, pk2(a0.y, a0.y)), a0, a1, a2, amax);
+          const BFront FB = bwd_front(P, b * kBB + e2, DSUB(fpx, b0.x),
+                                      sub2(FPY, pk2(b0.y, b0.y)), b0, b1, b2, amax);
+          f2_t TA, VA, TB, VB;
+          bwd_state(P, FA, TA, VA);
+          bwd_state(P, FB, TB, VB);
+          float va[kV], vb[kV];
+          bwd_partials(P, FA, TA, VA, va);
+          bwd_partials(P, FB, TB, VB, vb);
+          if (__any_sync(0xffffffffu, FA.any)) push(e1, va);
+          if (__any_sync(0xffffffffu, FB.any)) push(e2, vb);
+          continue;
+        }
+        float v[kV];
+        const bool act = bwd_pair(P, b * kBB + e1, DSUB(fpx, a0.x), sub2(FPY, pk2(a0.y, a0.y)),
+                                  a0, a1, a2, amax, v);
+        if (__any_sync(0xffffffffu, act)) push(e1, v);
       }
       if (nq) reduce(nq, ents);
     }
