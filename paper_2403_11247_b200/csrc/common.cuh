@@ -197,6 +197,9 @@ __device__ __forceinline__ void gather_batch(float4 *slot, uint32_t *msk, const 
   else mbar_arrive(full);
 }
 
+__device__ __forceinline__ void red_add_v2(float *addr, float a, float b) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(b) : "memory");
+}
 __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
                "f"(c), "f"(d)
@@ -370,46 +373,75 @@ size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam);
 // so at most two 1-D clamped minimisations per block.  The margin covers the
 // float32 evaluation of q at any pixel of the block, so a
 // cleared bit never skips a pixel the per-pixel test would have composited.
-__device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1, const uint4 &v3,
-                                               int X0, int Y0) {
-  const float u = __uint_as_float(v0.x), v = __uint_as_float(v0.y);
-  const float ca = __uint_as_float(v0.z), cb2 = __uint_as_float(v0.w);
-  const float cc = __uint_as_float(v1.x), k2 = __uint_as_float(v1.z);
-  const int rx0 = (int)(v3.x & 0xffffu), ry0 = (int)(v3.x >> 16);
-  const int rx1 = (int)(v3.y & 0xffffu), ry1 = (int)(v3.y >> 16);
-  const bool conic_ok = ca > 0.0f && cc > 0.0f;
+// The box test of one pixel block [bx0, bx1] x [by0, by1] (inclusive) against
+// one record: false only when the minimum of q over the box exceeds k^2 + margin.
+struct BoxConic {
+  float u, v, ca, cb2, cc, k2, sx, sy;
+  int rx0, ry0, rx1, ry1;
+  bool conic_ok;
+};
+__device__ __forceinline__ BoxConic box_conic(const uint4 &v0, const uint4 &v1, const uint4 &v3) {
+  BoxConic c;
+  c.u = __uint_as_float(v0.x); c.v = __uint_as_float(v0.y);
+  c.ca = __uint_as_float(v0.z); c.cb2 = __uint_as_float(v0.w);
+  c.cc = __uint_as_float(v1.x); c.k2 = __uint_as_float(v1.z);
+  c.rx0 = (int)(v3.x & 0xffffu); c.ry0 = (int)(v3.x >> 16);
+  c.rx1 = (int)(v3.y & 0xffffu); c.ry1 = (int)(v3.y >> 16);
+  c.conic_ok = c.ca > 0.0f && c.cc > 0.0f;
   // the edge minimisers' slopes, once per pair: on a vertical edge at dx = ex the
   // convex q is least at dy = -cb2 ex / (2 cc) (horizontal edges alike); any
   // rounding of this location only moves the probe along the edge, which can
   // raise q by at most cc * (location error)^2 -- far below the margin
-  const float sy = conic_ok ? -cb2 / (2.0f * cc) : 0.0f, sx = conic_ok ? -cb2 / (2.0f * ca) : 0.0f;
+  c.sy = c.conic_ok ? -c.cb2 / (2.0f * c.cc) : 0.0f;
+  c.sx = c.conic_ok ? -c.cb2 / (2.0f * c.ca) : 0.0f;
+  return c;
+}
+__device__ __forceinline__ bool box_may_hit(const BoxConic &c, int bx0, int by0, int bx1, int by1) {
+  if (c.rx1 < bx0 || c.rx0 > bx1 || c.ry1 < by0 || c.ry0 > by1) return false;  // rectangle cull
+  if (!c.conic_ok) return true;
+  const float dx0 = (float)bx0 - c.u, dx1 = (float)bx1 - c.u;
+  const float dy0 = (float)by0 - c.v, dy1 = (float)by1 - c.v;
+  const bool ox = dx0 > 0.0f || dx1 < 0.0f, oy = dy0 > 0.0f || dy1 < 0.0f;
+  float qmin = 0.0f;
+  if (ox || oy) {
+    qmin = INFINITY;
+    if (ox) {  // near vertical edge, dy clamped to the block
+      const float ex = dx0 > 0.0f ? dx0 : dx1;
+      const float dy = fminf(fmaxf(c.sy * ex, dy0), dy1);
+      qmin = fminf(qmin, c.ca * ex * ex + c.cb2 * ex * dy + c.cc * dy * dy);
+    }
+    if (oy) {  // near horizontal edge
+      const float ey = dy0 > 0.0f ? dy0 : dy1;
+      const float dx = fminf(fmaxf(c.sx * ey, dx0), dx1);
+      qmin = fminf(qmin, c.ca * dx * dx + c.cb2 * dx * ey + c.cc * ey * ey);
+    }
+  }
+  const float DX = fmaxf(fabsf(dx0), fabsf(dx1)), DY = fmaxf(fabsf(dy0), fabsf(dy1));
+  const float margin = 0.01f + 2e-5f * (c.ca * DX * DX + fabsf(c.cb2) * DX * DY + c.cc * DY * DY);
+  return !(qmin > c.k2 + margin);  // NaN keeps the block
+}
+__device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1, const uint4 &v3,
+                                               int X0, int Y0) {
+  const BoxConic c = box_conic(v0, v1, v3);
   uint32_t m = 0;
 #pragma unroll
   for (int w = 0; w < 4; w++) {
     const int bx0 = X0 + (w & 1) * 8, by0 = Y0 + (w >> 1) * 8;
-    const int bx1 = bx0 + 7, by1 = by0 + 7;
-    if (rx1 < bx0 || rx0 > bx1 || ry1 < by0 || ry0 > by1) continue;  // rectangle cull
-    if (!conic_ok) { m |= 1u << w; continue; }
-    const float dx0 = (float)bx0 - u, dx1 = (float)bx1 - u;
-    const float dy0 = (float)by0 - v, dy1 = (float)by1 - v;
-    const bool ox = dx0 > 0.0f || dx1 < 0.0f, oy = dy0 > 0.0f || dy1 < 0.0f;
-    float qmin = 0.0f;
-    if (ox || oy) {
-      qmin = INFINITY;
-      if (ox) {  // near vertical edge, dy clamped to the block
-        const float ex = dx0 > 0.0f ? dx0 : dx1;
-        const float dy = fminf(fmaxf(sy * ex, dy0), dy1);
-        qmin = fminf(qmin, ca * ex * ex + cb2 * ex * dy + cc * dy * dy);
-      }
-      if (oy) {  // near horizontal edge
-        const float ey = dy0 > 0.0f ? dy0 : dy1;
-        const float dx = fminf(fmaxf(sx * ey, dx0), dx1);
-        qmin = fminf(qmin, ca * dx * dx + cb2 * dx * ey + cc * ey * ey);
-      }
-    }
-    const float DX = fmaxf(fabsf(dx0), fabsf(dx1)), DY = fmaxf(fabsf(dy0), fabsf(dy1));
-    const float margin = 0.01f + 2e-5f * (ca * DX * DX + fabsf(cb2) * DX * DY + cc * DY * DY);
-    if (!(qmin > k2 + margin)) m |= 1u << w;  // NaN keeps the block
+    if (box_may_hit(c, bx0, by0, bx0 + 7, by0 + 7)) m |= 1u << w;
+  }
+  return m;
+}
+// The same test on the tile's sixteen 4x4 blocks (bit qy * 4 + qx), evaluated
+// only inside the 8x8 blocks whose bit m8 carries (a 4x4 block of a culled
+// 8x8 block is culled): the backward's per-ring selection (render_bwd.cu).
+__device__ __forceinline__ uint32_t quarter_mask(const BoxConic &c, int X0, int Y0, uint32_t m8) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int b = 0; b < 16; b++) {
+    const int qx = b & 3, qy = b >> 2;
+    if (!((m8 >> ((qx >> 1) + 2 * (qy >> 1))) & 1u)) continue;
+    const int bx0 = X0 + qx * 4, by0 = Y0 + qy * 4;
+    if (box_may_hit(c, bx0, by0, bx0 + 3, by0 + 3)) m |= 1u << b;
   }
   return m;
 }

@@ -40,6 +40,9 @@ constexpr int kBwdThreads = (kCW + 1) * 32;  // + 1 producer warp
 constexpr int kG = 3;             // active entries per transposed reduction: kG*kV <= 32 rows = one pass
 constexpr int kV = 10;            // partials per (pixel, entry)
 constexpr int kBwdMinBlocks = 5;  // CTAs per SM the register budget targets (6-7 measured slower)
+#ifndef CSPLAT_BWD_QUAD
+#define CSPLAT_BWD_QUAD 1
+#endif
 
 // workspace: the [n][12] float accumulator, then a [ceil(n/32)] u32 bitmap of
 // the Gaussians that received any partial (the chains visit only those)
@@ -445,6 +448,417 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
   }
 }
 
+// ---------------------------------------------------------------------------
+// The block-list backward (CSPLAT_BWD_QUAD, default).  k_render_bwd above
+// replays, for each 8x8 pixel block (one warp), every entry the block may
+// touch: on C2 61 % of those (pixel, entry) slots lie outside the entry's
+// ellipse, and the warp-wide reduction of the per-entry partials through shared
+// memory costs as much as the replay.  Here each 4x4 block has its own entry
+// list and its own four lanes (a QUAD), so a warp replays eight independent
+// streams:
+//  1. gather (per chunk of up to kChunk list entries, back to front): the
+//     chunk's records go to shared memory; an entry is listed for a 4x4 block
+//     if its pixel rectangle overlaps the block, the 8x8 block around it is
+//     flagged in the pair entry (block_mask, the sort's conservative ellipse
+//     test) and its list position is below the block's last contributor;
+//  2. replay: quad lane q owns column q of its block (two vertically adjacent
+//     pixel pairs, state and upstream in registers) and walks the block's list
+//     back to front with the recurrence of bwd_front / bwd_state above
+//     (T_j = T_{j+1} rcp(1 - alpha_j), B_{j-1} = B_j + alpha_j (v_j - B_j)) in
+//     the same arithmetic;
+//  3. per entry the quad sums its four lanes' ten partials with a transposed
+//     shuffle reduction (11 SHFL) and adds them to the [n][12] accumulator with
+//     one red.global.add.v4.f32 from each of two lanes and one .v2 from a third.
+// No producer warp, no barriers inside the replay; the shared-memory traffic per
+// entry is the record (three broadcast loads per quad).
+namespace quad {
+constexpr int kPW = 2;                    // warps per CTA (16x8 pixels each)
+constexpr int kThreads = kPW * 32;
+constexpr int kNB = 16;                   // 4x4 blocks (quads) per tile
+constexpr int kChunk = 256;               // list entries per gather
+#ifndef CSPLAT_QUAD_MINB
+#define CSPLAT_QUAD_MINB 5
+#endif
+#ifndef CSPLAT_QUAD_UNROLL
+#define CSPLAT_QUAD_UNROLL 1
+#endif
+#ifndef CSPLAT_QUAD_PAIR
+#define CSPLAT_QUAD_PAIR 1
+#endif
+constexpr int kMinBlocks = CSPLAT_QUAD_MINB;
+constexpr int kUnroll = CSPLAT_QUAD_UNROLL;
+
+struct Smem {
+  float4 rec[kChunk + 1][3];              // the chunk's records, words 0-11 (+ a zero record)
+  uint16_t m16[kChunk];                   // the entries' 4x4-block masks
+  uint8_t lst[kNB][kChunk];               // per block: its entries (chunk index), back to front
+  int wmax[kNB];
+  int nitems[kNB];
+};
+
+// one pixel pair's replay state and upstream (registers of its lane)
+struct QPair {
+  f2_t T, B, FPY, GR, GG, GB, GD, GS;
+  int last0, last1;
+};
+
+// the replay of one entry at one pixel pair: returns the pair's partial terms
+// (f32x2, to be summed over the quad's pixels)
+struct QTerms {
+  f2_t AV, TT, T2, GDL, WD, WR, WG, WB;
+};
+__device__ __forceinline__ QTerms pair_replay(QPair &P, int j, float dx, float cadx, float cbdx,
+                                              const float4 &r0, const float4 &r1,
+                                              const float4 &r2, float amax) {
+  const f2_t DY = sub2(P.FPY, pk2(r0.y, r0.y));
+  const f2_t Y = mul2(mul2(pk2(r1.x, r1.x), DY), DY);
+  const f2_t X = fma2(pk2(cbdx, cbdx), DY, Y);
+  const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx), X);
+  const float q0 = lo2(Q), q1 = hi2(Q);
+  const bool val0 = (j < P.last0) & da_in_range(q0, r1.z);
+  const bool val1 = (j < P.last1) & da_in_range(q1, r1.z);
+  const f2_t QM = pk2(val0 ? q0 : __int_as_float(0x7f800000), val1 ? q1 : __int_as_float(0x7f800000));
+  const f2_t QE = mul2(QM, pk2(-0.72134752f, -0.72134752f));
+  const f2_t G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
+  const f2_t AR = mul2(pk2(r1.y, r1.y), G);
+  const f2_t AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));  // R1
+  const bool nc0 = lo2(AR) < amax, nc1 = hi2(AR) < amax;
+  const f2_t OM = sub2(pk2(1.0f, 1.0f), AL);
+  float rc0, rc1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));  // alpha <= alpha_max < 1
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc1) : "f"(hi2(OM)));
+  const f2_t VV = fma2(pk2(r2.x, r2.x), P.GR,
+                       fma2(pk2(r2.y, r2.y), P.GG,
+                            fma2(pk2(r2.z, r2.z), P.GB, fma2(pk2(r1.w, r1.w), P.GD, P.GS))));
+  // T_j = T_{j+1} / (1 - alpha_j); v - B; B_{j-1} = B_j + alpha_j (v_j - B_j)
+  P.T = mul2(P.T, pk2(rc0, rc1));
+  const f2_t VB = sub2(VV, P.B);
+  P.B = fma2(AL, VB, P.B);
+  QTerms o;
+  const f2_t W = mul2(AL, P.T);
+  const f2_t D0 = mul2(P.T, VB);
+  const f2_t DL = pk2(nc0 ? lo2(D0) : 0.0f, nc1 ? hi2(D0) : 0.0f);  // R23
+  o.AV = mul2(AL, DL);
+  o.GDL = mul2(G, DL);
+  o.TT = mul2(o.AV, DY);
+  o.T2 = mul2(o.TT, DY);
+  o.WD = mul2(W, P.GD);
+  o.WR = mul2(W, P.GR);
+  o.WG = mul2(W, P.GG);
+  o.WB = mul2(W, P.GB);
+  return o;
+}
+// pair_replay in two pieces, so two entries can interleave: the front (q, the
+// validity, G, alpha, 1 / (1 - alpha), v -- independent of the replay state)
+// and the state update with the partial terms
+struct QFront {
+  f2_t DY, G, AL, RC, VV;
+  bool nc0, nc1;
+};
+__device__ __forceinline__ QFront pair_front(const QPair &P, int j, float dx, float cadx,
+                                             float cbdx, const float4 &r0, const float4 &r1,
+                                             const float4 &r2, float amax) {
+  QFront f;
+  f.DY = sub2(P.FPY, pk2(r0.y, r0.y));
+  const f2_t Y = mul2(mul2(pk2(r1.x, r1.x), f.DY), f.DY);
+  const f2_t X = fma2(pk2(cbdx, cbdx), f.DY, Y);
+  const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx), X);
+  const float q0 = lo2(Q), q1 = hi2(Q);
+  const bool val0 = (j < P.last0) & da_in_range(q0, r1.z);
+  const bool val1 = (j < P.last1) & da_in_range(q1, r1.z);
+  const f2_t QM = pk2(val0 ? q0 : __int_as_float(0x7f800000), val1 ? q1 : __int_as_float(0x7f800000));
+  const f2_t QE = mul2(QM, pk2(-0.72134752f, -0.72134752f));
+  f.G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
+  const f2_t AR = mul2(pk2(r1.y, r1.y), f.G);
+  f.AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));  // R1
+  f.nc0 = lo2(AR) < amax;
+  f.nc1 = hi2(AR) < amax;
+  const f2_t OM = sub2(pk2(1.0f, 1.0f), f.AL);
+  float rc0, rc1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));  // alpha <= alpha_max < 1
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc1) : "f"(hi2(OM)));
+  f.RC = pk2(rc0, rc1);
+  f.VV = fma2(pk2(r2.x, r2.x), P.GR,
+              fma2(pk2(r2.y, r2.y), P.GG,
+                   fma2(pk2(r2.z, r2.z), P.GB, fma2(pk2(r1.w, r1.w), P.GD, P.GS))));
+  return f;
+}
+__device__ __forceinline__ QTerms pair_state(QPair &P, const QFront &f) {
+  P.T = mul2(P.T, f.RC);
+  const f2_t VB = sub2(f.VV, P.B);
+  P.B = fma2(f.AL, VB, P.B);
+  QTerms o;
+  const f2_t W = mul2(f.AL, P.T);
+  const f2_t D0 = mul2(P.T, VB);
+  const f2_t DL = pk2(f.nc0 ? lo2(D0) : 0.0f, f.nc1 ? hi2(D0) : 0.0f);  // R23
+  o.AV = mul2(f.AL, DL);
+  o.GDL = mul2(f.G, DL);
+  o.TT = mul2(o.AV, f.DY);
+  o.T2 = mul2(o.TT, f.DY);
+  o.WD = mul2(W, P.GD);
+  o.WR = mul2(W, P.GR);
+  o.WG = mul2(W, P.GG);
+  o.WB = mul2(W, P.GB);
+  return o;
+}
+// the quad's ten sums of one entry's terms over its four lanes (transposed
+// shuffle reduction) into the accumulator
+__device__ __forceinline__ void quad_flush(const QTerms &a, float dx, bool hi, int ri, bool act,
+                                           float *dst) {
+  float v[kV];
+  const float sav = lo2(a.AV) + hi2(a.AV), stt = lo2(a.TT) + hi2(a.TT);
+  v[0] = dx * sav;
+  v[1] = stt;
+  v[2] = dx * v[0];
+  v[3] = dx * stt;
+  v[4] = lo2(a.T2) + hi2(a.T2);
+  v[5] = lo2(a.GDL) + hi2(a.GDL);
+  v[6] = lo2(a.WD) + hi2(a.WD);
+  v[7] = lo2(a.WR) + hi2(a.WR);
+  v[8] = lo2(a.WG) + hi2(a.WG);
+  v[9] = lo2(a.WB) + hi2(a.WB);
+  // lanes 0-1 keep (v0 v1 v2 v3 v8), lanes 2-3 (v4 v5 v6 v7 v9); then a
+  // butterfly over the lane pair
+  float x[5];
+#pragma unroll
+  for (int k = 0; k < 5; k++) {
+    const float s1 = k < 4 ? v[k] : v[8], s2 = k < 4 ? v[4 + k] : v[9];
+    const float keep = hi ? s2 : s1, send = hi ? s1 : s2;
+    x[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+#pragma unroll
+  for (int k = 0; k < 5; k++) x[k] += __shfl_xor_sync(0xffffffffu, x[k], 1);
+  const float v9 = __shfl_xor_sync(0xffffffffu, x[4], 2);  // lane 1 <- lane 3's v9
+  if (act) {
+    if ((ri & 1) == 0) red_add_v4(dst + (hi ? 4 : 0), x[0], x[1], x[2], x[3]);
+    else if (!hi) red_add_v2(dst + 8, x[4], v9);
+  }
+}
+__device__ __forceinline__ QTerms qadd(const QTerms &a, const QTerms &b) {
+  QTerms o;
+  o.AV = add2(a.AV, b.AV); o.TT = add2(a.TT, b.TT); o.T2 = add2(a.T2, b.T2);
+  o.GDL = add2(a.GDL, b.GDL); o.WD = add2(a.WD, b.WD); o.WR = add2(a.WR, b.WR);
+  o.WG = add2(a.WG, b.WG); o.WB = add2(a.WB, b.WB);
+  return o;
+}
+__device__ __forceinline__ float hsum(f2_t a, f2_t b) {
+  const f2_t s = add2(a, b);
+  return lo2(s) + hi2(s);
+}
+
+template <bool LOSS>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_render_bwd_quad(
+    const float4 *__restrict__ recs, const uint32_t *__restrict__ pair_gid,
+    const uint32_t *__restrict__ range, int W, int H,
+    int tiles_x, float amax, const float *__restrict__ t_final,
+    const int32_t *__restrict__ n_contrib, const float *__restrict__ dC,
+    const float *__restrict__ dD, const float *__restrict__ dS, float *__restrict__ accg,
+    uint32_t *__restrict__ alive, LossArgs la, int tile0, const int32_t *__restrict__ list) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int tb = (int)blockIdx.x;
+  if (list && tb >= list[0]) return;
+  const int tile = list ? list[1 + tb] : tile0 + tb;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
+  const uint32_t start = range[2 * tile];
+  // quad geometry: warp w covers tile rows [8w, 8w + 8); quad r = lane / 4 the
+  // 4x4 block (r & 3, r >> 2) of it, block index B = qy * 4 + qx in the tile;
+  // quad lane ri owns column ri of the block: pairs (rows 0-1) and (rows 2-3)
+  const int r = lane >> 2, ri = lane & 3;
+  const int B = wid * 8 + r;
+  const int px = tx * kTile + (r & 3) * 4 + ri, by = ty * kTile + wid * 8 + (r >> 2) * 4;
+
+  // ---- prologue: the lane's two pixel pairs
+  float lc = 0.f, ld = 0.f;
+  QPair P[2];
+  int mylast = 0;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int py0 = by + 2 * h;
+    float Tv[2], g[2][5];
+    int lastv[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const int py = py0 + k;
+      Tv[k] = 1.f; lastv[k] = 0;
+      g[k][0] = g[k][1] = g[k][2] = g[k][3] = g[k][4] = 0.f;
+      if (px < W && py < H) {
+        const int64_t HW = (int64_t)W * H, q = (int64_t)py * W + px;
+        Tv[k] = t_final[q];
+        lastv[k] = n_contrib[q];
+        if constexpr (LOSS) {
+          const unsigned long long nv = *la.n_valid;
+          const float inv_r = 1.0f / (float)(nv > 0 ? nv : 1ull);
+          const float gt = la.sil[q] > la.gate ? 1.0f : 0.0f;
+          const float obd = la.obs_depth[q];
+          const float vd = obd > 0.0f ? 1.0f : 0.0f;
+          const float r0 = la.color[q] - la.obs_color[q];
+          const float r1 = la.color[HW + q] - la.obs_color[HW + q];
+          const float r2 = la.color[2 * HW + q] - la.obs_color[2 * HW + q];
+          const float rd = la.depth[q] - obd;
+          lc += gt * (r0 * r0 + r1 * r1 + r2 * r2);
+          ld += gt * vd * rd * rd;
+          const float sc = 2.0f * gt * la.inv_n;
+          g[k][0] = sc * r0; g[k][1] = sc * r1; g[k][2] = sc * r2;
+          g[k][3] = 2.0f * la.lambda_d * gt * vd * rd * inv_r;
+          g[k][4] = 0.0f;
+        } else {
+          g[k][0] = dC[q]; g[k][1] = dC[HW + q]; g[k][2] = dC[2 * HW + q];
+          g[k][3] = dD[q]; g[k][4] = dS[q];
+        }
+        // all-zero upstream: exact zeros in every partial, no replay
+        if (g[k][0] == 0.f && g[k][1] == 0.f && g[k][2] == 0.f && g[k][3] == 0.f &&
+            g[k][4] == 0.f)
+          lastv[k] = 0;
+      }
+    }
+    mylast = max(mylast, max(lastv[0], lastv[1]));
+    P[h].T = pk2(Tv[0], Tv[1]);
+    P[h].B = pk2(0.f, 0.f);
+    P[h].FPY = pk2((float)py0, (float)(py0 + 1));
+    P[h].GR = pk2(g[0][0], g[1][0]); P[h].GG = pk2(g[0][1], g[1][1]);
+    P[h].GB = pk2(g[0][2], g[1][2]); P[h].GD = pk2(g[0][3], g[1][3]);
+    P[h].GS = pk2(g[0][4], g[1][4]);
+    P[h].last0 = lastv[0]; P[h].last1 = lastv[1];
+  }
+  mylast = max(mylast, __shfl_xor_sync(0xffffffffu, mylast, 1));
+  mylast = max(mylast, __shfl_xor_sync(0xffffffffu, mylast, 2));
+  if (ri == 0) sm.wmax[B] = mylast;
+  if constexpr (LOSS) {
+    lc = warp_sum(lc);
+    ld = warp_sum(ld);
+    if (lane == 0 && (lc != 0.f || ld != 0.f)) {
+      const unsigned long long nv = *la.n_valid;
+      const float a = lc * la.inv_n, b = ld / (float)(nv > 0 ? nv : 1ull);
+      atomicAdd(la.loss3 + 0, a + la.lambda_d * b);
+      atomicAdd(la.loss3 + 1, a);
+      atomicAdd(la.loss3 + 2, b);
+    }
+  }
+  __syncthreads();
+  int maxlast = 0;
+#pragma unroll
+  for (int b = 0; b < kNB; b++) maxlast = max(maxlast, sm.wmax[b]);
+  const int X0 = tx * kTile, Y0 = ty * kTile;
+  const float fpx = (float)px;
+
+  // chunks of the list, back to front
+  for (int c1 = maxlast; c1 > 0; c1 -= kChunk) {
+    const int c0 = max(0, c1 - kChunk), len = c1 - c0;
+    // 1a. the chunk's records and 4x4-block masks
+    constexpr int kPer = kChunk / kThreads;
+    uint32_t ent[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+      const int i = tid + k * kThreads;
+      ent[k] = i < len ? pair_gid[start + c0 + i] : 0u;
+    }
+    uint4 w[kPer][4];
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+      const uint4 *rw = reinterpret_cast<const uint4 *>(recs + (size_t)(ent[k] & kPairGidMask) * 4);
+      if (tid + k * kThreads < len) {
+        w[k][0] = __ldg(rw); w[k][1] = __ldg(rw + 1); w[k][2] = __ldg(rw + 2); w[k][3] = __ldg(rw + 3);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+      const int i = tid + k * kThreads;
+      if (i >= len) continue;
+      sm.rec[i][0] = make_float4(__uint_as_float(w[k][0].x), __uint_as_float(w[k][0].y),
+                                 __uint_as_float(w[k][0].z), __uint_as_float(w[k][0].w));
+      sm.rec[i][1] = make_float4(__uint_as_float(w[k][1].x), __uint_as_float(w[k][1].y),
+                                 __uint_as_float(w[k][1].z), __uint_as_float(w[k][1].w));
+      sm.rec[i][2] = make_float4(__uint_as_float(w[k][2].x), __uint_as_float(w[k][2].y),
+                                 __uint_as_float(w[k][2].z), __uint_as_float(w[k][2].w));
+      // the 4x4 blocks the pixel rectangle overlaps (rows x columns) ...
+      const int rx0 = (int)(w[k][3].x & 0xffffu) - X0, ry0 = (int)(w[k][3].x >> 16) - Y0;
+      const int rx1 = (int)(w[k][3].y & 0xffffu) - X0, ry1 = (int)(w[k][3].y >> 16) - Y0;
+      const int cx0 = max(rx0, 0) >> 2, cx1 = min(rx1, kTile - 1) >> 2;
+      const int cy0 = max(ry0, 0) >> 2, cy1 = min(ry1, kTile - 1) >> 2;
+      const uint32_t cols = (0xfu >> (3 - cx1)) & (0xfu << cx0);
+      const uint32_t rows = (0xfu >> (3 - cy1)) & (0xfu << cy0);
+      uint32_t rowspread = 0;
+#pragma unroll
+      for (int q = 0; q < 4; q++) rowspread |= ((rows >> q) & 1u) << (4 * q);
+      // ... inside the 8x8 blocks the pair entry flags
+      const uint32_t m8 = ent[k] >> kPairMaskShift;
+      const uint32_t m8x = ((m8 & 1u) ? 0x0033u : 0u) | ((m8 & 2u) ? 0x00ccu : 0u) |
+                           ((m8 & 4u) ? 0x3300u : 0u) | ((m8 & 8u) ? 0xcc00u : 0u);
+      const uint32_t m = cols * rowspread & m8x;
+      sm.m16[i] = (uint16_t)m;
+      if (m) {
+        const uint32_t gid = ent[k] & kPairGidMask;
+        atomicOr(alive + (gid >> 5), 1u << (gid & 31));  // the chain visits this Gaussian
+      }
+    }
+    if (tid < 3) sm.rec[kChunk][tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    // 1b. each warp lists its own eight blocks' entries, back to front
+    {
+      int cnt = 0;  // lane rr < 8: block 8 wid + rr's count
+      for (int base = len - 32; base > -32; base -= 32) {
+        const int i = base + lane;
+        const uint32_t m = i >= 0 ? sm.m16[i] : 0u;
+#pragma unroll
+        for (int rr = 0; rr < 8; rr++) {
+          // a block whose pixels all finished before this entry has nothing to replay
+          const bool sel = ((m >> (wid * 8 + rr)) & 1u) && c0 + i < sm.wmax[wid * 8 + rr];
+          const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+          const int before = __shfl_sync(0xffffffffu, cnt, rr);
+          if (sel) sm.lst[wid * 8 + rr][before + __popc(bal >> lane >> 1)] = (uint8_t)i;
+          if (lane == rr) cnt += __popc(bal);
+        }
+      }
+      if (lane < 8) sm.nitems[wid * 8 + lane] = cnt;
+      __syncwarp();
+    }
+    // 2. the replay: the quad walks its block's list; 3. quad sums -> accumulator
+    const int nr = sm.nitems[B];
+    const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nr);
+    const uint8_t *lst = sm.lst[B];
+    const bool hi = ri >= 2;
+#if CSPLAT_QUAD_PAIR
+    // two list entries per iteration: both fronts, the two state updates in
+    // list order, both partial sums -- the independent halves interleave
+    for (int e = 0; e < nmax; e += 2) {
+      const bool actA = e < nr, actB = e + 1 < nr;
+      const int iA = actA ? (int)lst[e] : kChunk, iB = actB ? (int)lst[e + 1] : kChunk;
+      const float4 a0 = sm.rec[iA][0], a1 = sm.rec[iA][1], a2 = sm.rec[iA][2];
+      const float4 b0 = sm.rec[iB][0], b1 = sm.rec[iB][1], b2 = sm.rec[iB][2];
+      const int jA = actA ? c0 + iA : 0x7fffffff, jB = actB ? c0 + iB : 0x7fffffff;
+      const float dxA = DSUB(fpx, a0.x), dxB = DSUB(fpx, b0.x);
+      const QFront fA0 = pair_front(P[0], jA, dxA, DMUL(a0.z, dxA), DMUL(a0.w, dxA), a0, a1, a2, amax);
+      const QFront fA1 = pair_front(P[1], jA, dxA, DMUL(a0.z, dxA), DMUL(a0.w, dxA), a0, a1, a2, amax);
+      const QFront fB0 = pair_front(P[0], jB, dxB, DMUL(b0.z, dxB), DMUL(b0.w, dxB), b0, b1, b2, amax);
+      const QFront fB1 = pair_front(P[1], jB, dxB, DMUL(b0.z, dxB), DMUL(b0.w, dxB), b0, b1, b2, amax);
+      const QTerms tA0 = pair_state(P[0], fA0), tA1 = pair_state(P[1], fA1);
+      const QTerms tB0 = pair_state(P[0], fB0), tB1 = pair_state(P[1], fB1);
+      quad_flush(qadd(tA0, tA1), dxA, hi, ri, actA, accg + (int64_t)__float_as_uint(a2.w) * kAcc);
+      quad_flush(qadd(tB0, tB1), dxB, hi, ri, actB, accg + (int64_t)__float_as_uint(b2.w) * kAcc);
+    }
+#else
+#pragma unroll kUnroll
+    for (int e = 0; e < nmax; e++) {
+      // past its list a quad replays the zero record with j beyond every
+      // pixel's last contributor: no state change, exact zero partials
+      const bool act = e < nr;
+      const int i = act ? (int)lst[e] : kChunk;
+      const float4 r0 = sm.rec[i][0], r1 = sm.rec[i][1], r2 = sm.rec[i][2];
+      const int j = act ? c0 + i : 0x7fffffff;
+      const float dx = DSUB(fpx, r0.x);
+      const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
+      const QTerms a = pair_replay(P[0], j, dx, cadx, cbdx, r0, r1, r2, amax);
+      const QTerms b = pair_replay(P[1], j, dx, cadx, cbdx, r0, r1, r2, amax);
+      quad_flush(qadd(a, b), dx, hi, ri, act, accg + (int64_t)__float_as_uint(r2.w) * kAcc);
+    }
+#endif
+    __syncthreads();  // before the next chunk overwrites the records and lists
+  }
+}
+}  // namespace quad
+
 // zero the accumulator (and the pose gradient unless accumulating)
 cudaError_t bwd_prep(const csplat_gaussians &g, uint32_t flags, const csplat_grads &out,
                      void *ws, const TrackingLoss *loss, cudaStream_t s) {
@@ -476,16 +890,27 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
   // the opt-in shared-memory size: set once per device (a race between host
   // threads only repeats the idempotent call)
   static std::atomic<unsigned long long> attr_done{0};
+#if CSPLAT_BWD_QUAD
+  const size_t smem_quad = sizeof(quad::Smem);
+#endif
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   const unsigned long long bit = 1ull << (dev & 63);
   if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+#if CSPLAT_BWD_QUAD
+    e = cudaFuncSetAttribute(quad::k_render_bwd_quad<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_quad);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(quad::k_render_bwd_quad<true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_quad);
+#else
     e = cudaFuncSetAttribute(k_render_bwd<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(k_render_bwd<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem);
+#endif
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
   }
@@ -501,13 +926,25 @@ cudaError_t launch_render_bwd_tiles(const csplat_camera &cam, const TrackingLoss
     la.n_valid = loss->n_valid; la.lambda_d = loss->lambda_d; la.gate = loss->gate;
     la.inv_n = 1.0f / (float)((int64_t)ci.W * ci.H);
     la.loss3 = loss->loss3;
+#if CSPLAT_BWD_QUAD
+    quad::k_render_bwd_quad<true><<<ntiles, quad::kThreads, smem_quad, s>>>(
+        static_cast<const float4 *>(rec), pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
+        t_final, n_contrib, nullptr, nullptr, nullptr, acc, alive, la, tile0, list);
+#else
     k_render_bwd<true><<<ntiles, kBwdThreads, smem, s>>>(
         tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
         t_final, n_contrib, nullptr, nullptr, nullptr, acc, alive, la, tile0, list);
+#endif
   } else {
+#if CSPLAT_BWD_QUAD
+    quad::k_render_bwd_quad<false><<<ntiles, quad::kThreads, smem_quad, s>>>(
+        static_cast<const float4 *>(rec), pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
+        t_final, n_contrib, d_color, d_depth, d_sil, acc, alive, la, tile0, list);
+#else
     k_render_bwd<false><<<ntiles, kBwdThreads, smem, s>>>(
         tmap, pair_gid, tile_range, ci.W, ci.H, ci.tiles_x, prm.alpha_max,
         t_final, n_contrib, d_color, d_depth, d_sil, acc, alive, la, tile0, list);
+#endif
   }
   return cudaGetLastError();
 }
