@@ -23,6 +23,7 @@
 #include <atomic>
 
 #include "common.cuh"
+#include "quad.cuh"
 
 namespace csplat {
 
@@ -472,28 +473,14 @@ __global__ void __launch_bounds__(kBwdThreads, kBwdMinBlocks) k_render_bwd(
 // No producer warp, no barriers inside the replay; the shared-memory traffic per
 // entry is the record (three broadcast loads per quad).
 namespace quad {
-constexpr int kPW = 2;                    // warps per CTA (16x8 pixels each)
-constexpr int kThreads = kPW * 32;
-constexpr int kNB = 16;                   // 4x4 blocks (quads) per tile
-constexpr int kChunk = 256;               // list entries per gather
 #ifndef CSPLAT_QUAD_MINB
-#define CSPLAT_QUAD_MINB 5
-#endif
-#ifndef CSPLAT_QUAD_UNROLL
-#define CSPLAT_QUAD_UNROLL 1
-#endif
-#ifndef CSPLAT_QUAD_PAIR
-#define CSPLAT_QUAD_PAIR 1
+#define CSPLAT_QUAD_MINB 8
 #endif
 constexpr int kMinBlocks = CSPLAT_QUAD_MINB;
-constexpr int kUnroll = CSPLAT_QUAD_UNROLL;
 
 struct Smem {
-  float4 rec[kChunk + 1][3];              // the chunk's records, words 0-11 (+ a zero record)
-  uint16_t m16[kChunk];                   // the entries' 4x4-block masks
-  uint8_t lst[kNB][kChunk];               // per block: its entries (chunk index), back to front
+  Lists L;
   int wmax[kNB];
-  int nitems[kNB];
 };
 
 // one pixel pair's replay state and upstream (registers of its lane)
@@ -502,53 +489,12 @@ struct QPair {
   int last0, last1;
 };
 
-// the replay of one entry at one pixel pair: returns the pair's partial terms
-// (f32x2, to be summed over the quad's pixels)
+// a pixel pair's partial terms of one entry (f32x2, summed over the quad's pixels)
 struct QTerms {
   f2_t AV, TT, T2, GDL, WD, WR, WG, WB;
 };
-__device__ __forceinline__ QTerms pair_replay(QPair &P, int j, float dx, float cadx, float cbdx,
-                                              const float4 &r0, const float4 &r1,
-                                              const float4 &r2, float amax) {
-  const f2_t DY = sub2(P.FPY, pk2(r0.y, r0.y));
-  const f2_t Y = mul2(mul2(pk2(r1.x, r1.x), DY), DY);
-  const f2_t X = fma2(pk2(cbdx, cbdx), DY, Y);
-  const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx), X);
-  const float q0 = lo2(Q), q1 = hi2(Q);
-  const bool val0 = (j < P.last0) & da_in_range(q0, r1.z);
-  const bool val1 = (j < P.last1) & da_in_range(q1, r1.z);
-  const f2_t QM = pk2(val0 ? q0 : __int_as_float(0x7f800000), val1 ? q1 : __int_as_float(0x7f800000));
-  const f2_t QE = mul2(QM, pk2(-0.72134752f, -0.72134752f));
-  const f2_t G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
-  const f2_t AR = mul2(pk2(r1.y, r1.y), G);
-  const f2_t AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));  // R1
-  const bool nc0 = lo2(AR) < amax, nc1 = hi2(AR) < amax;
-  const f2_t OM = sub2(pk2(1.0f, 1.0f), AL);
-  float rc0, rc1;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));  // alpha <= alpha_max < 1
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc1) : "f"(hi2(OM)));
-  const f2_t VV = fma2(pk2(r2.x, r2.x), P.GR,
-                       fma2(pk2(r2.y, r2.y), P.GG,
-                            fma2(pk2(r2.z, r2.z), P.GB, fma2(pk2(r1.w, r1.w), P.GD, P.GS))));
-  // T_j = T_{j+1} / (1 - alpha_j); v - B; B_{j-1} = B_j + alpha_j (v_j - B_j)
-  P.T = mul2(P.T, pk2(rc0, rc1));
-  const f2_t VB = sub2(VV, P.B);
-  P.B = fma2(AL, VB, P.B);
-  QTerms o;
-  const f2_t W = mul2(AL, P.T);
-  const f2_t D0 = mul2(P.T, VB);
-  const f2_t DL = pk2(nc0 ? lo2(D0) : 0.0f, nc1 ? hi2(D0) : 0.0f);  // R23
-  o.AV = mul2(AL, DL);
-  o.GDL = mul2(G, DL);
-  o.TT = mul2(o.AV, DY);
-  o.T2 = mul2(o.TT, DY);
-  o.WD = mul2(W, P.GD);
-  o.WR = mul2(W, P.GR);
-  o.WG = mul2(W, P.GG);
-  o.WB = mul2(W, P.GB);
-  return o;
-}
-// pair_replay in two pieces, so two entries can interleave: the front (q, the
+
+// one entry at one pixel pair in two pieces, so two entries can interleave: the front (q, the
 // validity, G, alpha, 1 / (1 - alpha), v -- independent of the replay state)
 // and the state update with the partial terms
 struct QFront {
@@ -641,10 +587,6 @@ __device__ __forceinline__ QTerms qadd(const QTerms &a, const QTerms &b) {
   o.WG = add2(a.WG, b.WG); o.WB = add2(a.WB, b.WB);
   return o;
 }
-__device__ __forceinline__ float hsum(f2_t a, f2_t b) {
-  const f2_t s = add2(a, b);
-  return lo2(s) + hi2(s);
-}
 
 template <bool LOSS>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_render_bwd_quad(
@@ -662,12 +604,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_render_bwd_quad(
   const int tile = list ? list[1 + tb] : tile0 + tb;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const uint32_t start = range[2 * tile];
-  // quad geometry: warp w covers tile rows [8w, 8w + 8); quad r = lane / 4 the
-  // 4x4 block (r & 3, r >> 2) of it, block index B = qy * 4 + qx in the tile;
-  // quad lane ri owns column ri of the block: pairs (rows 0-1) and (rows 2-3)
-  const int r = lane >> 2, ri = lane & 3;
-  const int B = wid * 8 + r;
-  const int px = tx * kTile + (r & 3) * 4 + ri, by = ty * kTile + wid * 8 + (r >> 2) * 4;
+  const Geo gq = geo(tx, ty, wid, lane);
+  const int ri = gq.ri, B = gq.B, px = gq.px, by = gq.by;
 
   // ---- prologue: the lane's two pixel pairs
   float lc = 0.f, ld = 0.f;
@@ -746,87 +684,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_render_bwd_quad(
   // chunks of the list, back to front
   for (int c1 = maxlast; c1 > 0; c1 -= kChunk) {
     const int c0 = max(0, c1 - kChunk), len = c1 - c0;
-    // 1a. the chunk's records and 4x4-block masks
-    constexpr int kPer = kChunk / kThreads;
-    uint32_t ent[kPer];
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-      const int i = tid + k * kThreads;
-      ent[k] = i < len ? pair_gid[start + c0 + i] : 0u;
-    }
-    uint4 w[kPer][4];
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-      const uint4 *rw = reinterpret_cast<const uint4 *>(recs + (size_t)(ent[k] & kPairGidMask) * 4);
-      if (tid + k * kThreads < len) {
-        w[k][0] = __ldg(rw); w[k][1] = __ldg(rw + 1); w[k][2] = __ldg(rw + 2); w[k][3] = __ldg(rw + 3);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kPer; k++) {
-      const int i = tid + k * kThreads;
-      if (i >= len) continue;
-      sm.rec[i][0] = make_float4(__uint_as_float(w[k][0].x), __uint_as_float(w[k][0].y),
-                                 __uint_as_float(w[k][0].z), __uint_as_float(w[k][0].w));
-      sm.rec[i][1] = make_float4(__uint_as_float(w[k][1].x), __uint_as_float(w[k][1].y),
-                                 __uint_as_float(w[k][1].z), __uint_as_float(w[k][1].w));
-      sm.rec[i][2] = make_float4(__uint_as_float(w[k][2].x), __uint_as_float(w[k][2].y),
-                                 __uint_as_float(w[k][2].z), __uint_as_float(w[k][2].w));
-      // the 4x4 blocks the pixel rectangle overlaps (rows x columns) ...
-      const int rx0 = (int)(w[k][3].x & 0xffffu) - X0, ry0 = (int)(w[k][3].x >> 16) - Y0;
-      const int rx1 = (int)(w[k][3].y & 0xffffu) - X0, ry1 = (int)(w[k][3].y >> 16) - Y0;
-      const int cx0 = max(rx0, 0) >> 2, cx1 = min(rx1, kTile - 1) >> 2;
-      const int cy0 = max(ry0, 0) >> 2, cy1 = min(ry1, kTile - 1) >> 2;
-      const uint32_t cols = (0xfu >> (3 - cx1)) & (0xfu << cx0);
-      const uint32_t rows = (0xfu >> (3 - cy1)) & (0xfu << cy0);
-      uint32_t rowspread = 0;
-#pragma unroll
-      for (int q = 0; q < 4; q++) rowspread |= ((rows >> q) & 1u) << (4 * q);
-      // ... inside the 8x8 blocks the pair entry flags
-      const uint32_t m8 = ent[k] >> kPairMaskShift;
-      const uint32_t m8x = ((m8 & 1u) ? 0x0033u : 0u) | ((m8 & 2u) ? 0x00ccu : 0u) |
-                           ((m8 & 4u) ? 0x3300u : 0u) | ((m8 & 8u) ? 0xcc00u : 0u);
-      const uint32_t m = cols * rowspread & m8x;
-      sm.m16[i] = (uint16_t)m;
-      if (m) {
-        const uint32_t gid = ent[k] & kPairGidMask;
-        atomicOr(alive + (gid >> 5), 1u << (gid & 31));  // the chain visits this Gaussian
-      }
-    }
-    if (tid < 3) sm.rec[kChunk][tid] = make_float4(0.f, 0.f, 0.f, 0.f);
-    __syncthreads();
-    // 1b. each warp lists its own eight blocks' entries, back to front
-    {
-      int cnt = 0;  // lane rr < 8: block 8 wid + rr's count
-      for (int base = len - 32; base > -32; base -= 32) {
-        const int i = base + lane;
-        const uint32_t m = i >= 0 ? sm.m16[i] : 0u;
-#pragma unroll
-        for (int rr = 0; rr < 8; rr++) {
-          // a block whose pixels all finished before this entry has nothing to replay
-          const bool sel = ((m >> (wid * 8 + rr)) & 1u) && c0 + i < sm.wmax[wid * 8 + rr];
-          const uint32_t bal = __ballot_sync(0xffffffffu, sel);
-          const int before = __shfl_sync(0xffffffffu, cnt, rr);
-          if (sel) sm.lst[wid * 8 + rr][before + __popc(bal >> lane >> 1)] = (uint8_t)i;
-          if (lane == rr) cnt += __popc(bal);
-        }
-      }
-      if (lane < 8) sm.nitems[wid * 8 + lane] = cnt;
-      __syncwarp();
-    }
+    // 1. the chunk's records, 4x4-block masks and the blocks' lists, back to front
+    gather(sm.L, recs, pair_gid, start, c0, len, X0, Y0, alive, tid);
+    build_lists<true>(sm.L, c0, len, sm.wmax, wid, lane);
     // 2. the replay: the quad walks its block's list; 3. quad sums -> accumulator
-    const int nr = sm.nitems[B];
+    const int nr = sm.L.nitems[B];
     const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nr);
-    const uint8_t *lst = sm.lst[B];
+    const uint8_t *lst = sm.L.lst[B];
     const bool hi = ri >= 2;
-#if CSPLAT_QUAD_PAIR
     // two list entries per iteration: both fronts, the two state updates in
     // list order, both partial sums -- the independent halves interleave
     for (int e = 0; e < nmax; e += 2) {
       const bool actA = e < nr, actB = e + 1 < nr;
       const int iA = actA ? (int)lst[e] : kChunk, iB = actB ? (int)lst[e + 1] : kChunk;
-      const float4 a0 = sm.rec[iA][0], a1 = sm.rec[iA][1], a2 = sm.rec[iA][2];
-      const float4 b0 = sm.rec[iB][0], b1 = sm.rec[iB][1], b2 = sm.rec[iB][2];
+      const float4 a0 = sm.L.rec[iA][0], a1 = sm.L.rec[iA][1], a2 = sm.L.rec[iA][2];
+      const float4 b0 = sm.L.rec[iB][0], b1 = sm.L.rec[iB][1], b2 = sm.L.rec[iB][2];
       const int jA = actA ? c0 + iA : 0x7fffffff, jB = actB ? c0 + iB : 0x7fffffff;
       const float dxA = DSUB(fpx, a0.x), dxB = DSUB(fpx, b0.x);
       const QFront fA0 = pair_front(P[0], jA, dxA, DMUL(a0.z, dxA), DMUL(a0.w, dxA), a0, a1, a2, amax);
@@ -838,22 +710,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_render_bwd_quad(
       quad_flush(qadd(tA0, tA1), dxA, hi, ri, actA, accg + (int64_t)__float_as_uint(a2.w) * kAcc);
       quad_flush(qadd(tB0, tB1), dxB, hi, ri, actB, accg + (int64_t)__float_as_uint(b2.w) * kAcc);
     }
-#else
-#pragma unroll kUnroll
-    for (int e = 0; e < nmax; e++) {
-      // past its list a quad replays the zero record with j beyond every
-      // pixel's last contributor: no state change, exact zero partials
-      const bool act = e < nr;
-      const int i = act ? (int)lst[e] : kChunk;
-      const float4 r0 = sm.rec[i][0], r1 = sm.rec[i][1], r2 = sm.rec[i][2];
-      const int j = act ? c0 + i : 0x7fffffff;
-      const float dx = DSUB(fpx, r0.x);
-      const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
-      const QTerms a = pair_replay(P[0], j, dx, cadx, cbdx, r0, r1, r2, amax);
-      const QTerms b = pair_replay(P[1], j, dx, cadx, cbdx, r0, r1, r2, amax);
-      quad_flush(qadd(a, b), dx, hi, ri, act, accg + (int64_t)__float_as_uint(r2.w) * kAcc);
-    }
-#endif
     __syncthreads();  // before the next chunk overwrites the records and lists
   }
 }
