@@ -81,20 +81,13 @@ __global__ void __launch_bounds__(256) k_bucket(int64_t n, const int32_t *__rest
   const int lane = threadIdx.x & 31;
   for (int64_t b = warp; b * 32 < n; b += nwarps) {
     const int64_t i = b * 32 + lane;
-    int c = 0;
-    uint32_t rx = 0, ry = 0, zb = 0;
+    PairSrc src = pair_src_none();
     if (i < n) {
-      c = count[i];
-      if (c > 0) {
-        const uint4 r1 = rec4[i * 4 + 1];
-        const uint4 r3 = rec4[i * 4 + 3];
-        zb = r1.w;
-        rx = r3.x;
-        ry = r3.y;
-      }
+      const int c = count[i];
+      if (c > 0) src = pair_src_rec(c, rec4[i * 4 + 0], rec4[i * 4 + 1], rec4[i * 4 + 3]);
     }
-    expand_warp_regs(b * 32, c, rx, ry, zb, tiles_x, [&](uint32_t gid, int tile, uint32_t z) {
-      bucket_put(w, cap, active, gid, tile, z);
+    expand_warp_regs(b * 32, src, tiles_x, [&](uint32_t gid, int tile, uint32_t z, uint32_t m) {
+      bucket_put(w, cap, active, gid, tile, z, m);
     });
   }
 }
@@ -143,27 +136,17 @@ __device__ __forceinline__ void bitonic_sort(unsigned long long *a, int len, int
   cta_sync();
 }
 
-// Pair entry `pos` of the sorted order: the Gaussian index (key low word) in
-// bits 0-27 and the pair's 8x8-block cull mask (block_mask, from the record's
-// words 0-7 and 12-13) in bits 28-31 -- what the renderers need per entry,
-// so they gather the record itself from rec and compute nothing per entry.
-__device__ __forceinline__ uint32_t pair_entry(unsigned long long key,
-                                               const uint4 *__restrict__ rec4, int X0, int Y0) {
-  const uint32_t gid = (uint32_t)(key & 0xffffffffull);
-  const uint4 *r = rec4 + (int64_t)gid * 4;
-  return gid | (block_mask(r[0], r[1], r[3], X0, Y0) << kPairMaskShift);
-}
-
-__device__ __forceinline__ void emit_entry(unsigned long long key, int64_t pos,
-                                           const uint4 *__restrict__ rec4,
-                                           uint32_t *__restrict__ pair_gid, int X0, int Y0) {
-  pair_gid[pos] = pair_entry(key, rec4, X0, Y0);
+// Pair entry of a sorted key: the Gaussian index (key bits 4-31) in bits 0-27
+// and the pair's 8x8-block cull mask (key bits 0-3, computed by the bucket
+// pass) in bits 28-31 -- what the renderers need per entry.
+__device__ __forceinline__ uint32_t pair_entry(unsigned long long key) {
+  const uint32_t lo = (uint32_t)(key & 0xffffffffull);
+  return (lo >> 4) | ((lo & 0xfu) << kPairMaskShift);
 }
 
 __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len, uint32_t start,
-                                            int tid, int nthr, const uint4 *__restrict__ rec4,
-                                            uint32_t *__restrict__ pair_gid, int X0, int Y0) {
-  for (int k = tid; k < len; k += nthr) emit_entry(a[k], (int64_t)start + k, rec4, pair_gid, X0, Y0);
+                                            int tid, int nthr, uint32_t *__restrict__ pair_gid) {
+  for (int k = tid; k < len; k += nthr) pair_gid[(int64_t)start + k] = pair_entry(a[k]);
 }
 
 // Register-resident bitonic sort of up to 2 * kSortThreads = 256 keys: thread t
@@ -306,7 +289,6 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   const int64_t npos = list ? (int64_t)list[0] : T;
   if (pos >= npos) return;  // (block-uniform, before any barrier)
   const int64_t tile = list ? (int64_t)list[1 + pos] : pos;
-  const int X0 = (int)(tile % tiles_x) * kTile, Y0 = (int)(tile / tiles_x) * kTile;
   const uint32_t cnt_t = w.cur[tile];
   const unsigned long long prefix = w.status[pos];  // k_tile_scan's exclusive offset
   // capacity overflow (csplat.h): a tile whose pairs do not all fit -- past
@@ -342,8 +324,8 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int np2 = 2;
     while (np2 < len) np2 <<= 1;
     sort_regs256(x0, x1, np2, reinterpret_cast<unsigned long long(*)[2 * kSortThreads]>(sk));
-    if (2 * t < len) pair_gid[(int64_t)start + 2 * t] = pair_entry(x0, rec4, X0, Y0);
-    if (2 * t + 1 < len) pair_gid[(int64_t)start + 2 * t + 1] = pair_entry(x1, rec4, X0, Y0);
+    if (2 * t < len) pair_gid[(int64_t)start + 2 * t] = pair_entry(x0);
+    if (2 * t + 1 < len) pair_gid[(int64_t)start + 2 * t + 1] = pair_entry(x1);
     return;
   }
   unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
@@ -362,7 +344,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   }
   __syncthreads();
   bitonic_sort(a, len, threadIdx.x, kSortThreads, [] { __syncthreads(); });
-  emit_sorted(a, len, start, threadIdx.x, kSortThreads, rec4, pair_gid, X0, Y0);
+  emit_sorted(a, len, start, threadIdx.x, kSortThreads, pair_gid);
 }
 
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,

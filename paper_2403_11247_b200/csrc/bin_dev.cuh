@@ -61,14 +61,41 @@ cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t nctas, int64_t T, in
                                     uint32_t *tile_range, int64_t *n_pairs_dev,
                                     const SortViews &sv, int nv, cudaStream_t s);
 
+// What a Gaussian contributes to the bucket pass: its pair count c, its pixel
+// rectangle corners rx, ry (record words 12, 13), bits(z_c) zb, and the conic
+// and extent the pairs' 8x8-block cull masks need (block_mask_c, DESIGN.md §4:
+// the sort used to gather the record per pair for it).
+struct PairSrc {
+  int c;
+  uint32_t rx, ry, zb;
+  float u, v, ca, cb2, cc, k2;
+};
+__device__ __forceinline__ PairSrc pair_src_none() {
+  PairSrc s;
+  s.c = 0; s.rx = s.ry = s.zb = 0u;
+  s.u = s.v = s.ca = s.cb2 = s.cc = s.k2 = 0.f;
+  return s;
+}
+// from a record (words 0-7, 12-13) and its pair count
+__device__ __forceinline__ PairSrc pair_src_rec(int c, const uint4 &r0, const uint4 &r1,
+                                                const uint4 &r3) {
+  PairSrc s;
+  s.c = c; s.rx = r3.x; s.ry = r3.y; s.zb = r1.w;
+  s.u = __uint_as_float(r0.x); s.v = __uint_as_float(r0.y);
+  s.ca = __uint_as_float(r0.z); s.cb2 = __uint_as_float(r0.w);
+  s.cc = __uint_as_float(r1.x); s.k2 = __uint_as_float(r1.z);
+  return s;
+}
+
 // Warp-cooperative expansion of 32 Gaussians' tile rectangles.  Lane l holds
-// Gaussian base + l's pair count c, its pixel rectangle corners rx, ry (record
-// words 12, 13) and bits(z_c) zb.  Calls f(gid, tile, zb) once per (Gaussian,
-// tile) pair; all 32 lanes must be converged on entry.
+// Gaussian base + l's PairSrc.  Calls f(gid, tile, zb, mask) once per
+// (Gaussian, tile) pair, mask = the pair's 8x8-block cull mask; all 32 lanes
+// must be converged on entry.
 template <typename F>
-__device__ __forceinline__ void expand_warp_regs(int64_t base, int c, uint32_t rx, uint32_t ry,
-                                                 uint32_t zb, int tiles_x, F f) {
+__device__ __forceinline__ void expand_warp_regs(int64_t base, const PairSrc &src, int tiles_x,
+                                                 F f) {
   const int lane = threadIdx.x & 31;
+  const int c = src.c;
   int incl = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -77,6 +104,10 @@ __device__ __forceinline__ void expand_warp_regs(int64_t base, int c, uint32_t r
   }
   const int excl = incl - c;
   const int total = __shfl_sync(0xffffffffu, incl, 31);
+  // the edge minimisers' slopes of the box test, once per Gaussian
+  const bool ok = src.ca > 0.0f && src.cc > 0.0f;
+  const float sy = ok ? -src.cb2 / (2.0f * src.cc) : 0.0f;
+  const float sx = ok ? -src.cb2 / (2.0f * src.ca) : 0.0f;
   for (int kb = 0; kb < total; kb += 32) {
     const int k = kb + lane;
     int owner = 0;
@@ -87,29 +118,45 @@ __device__ __forceinline__ void expand_warp_regs(int64_t base, int c, uint32_t r
       if (cand < 32 && e <= k) owner = cand;
     }
     const int oe = __shfl_sync(0xffffffffu, excl, owner);
-    const uint32_t orx = __shfl_sync(0xffffffffu, rx, owner);
-    const uint32_t ory = __shfl_sync(0xffffffffu, ry, owner);
-    const uint32_t ozb = __shfl_sync(0xffffffffu, zb, owner);
+    const uint32_t orx = __shfl_sync(0xffffffffu, src.rx, owner);
+    const uint32_t ory = __shfl_sync(0xffffffffu, src.ry, owner);
+    const uint32_t ozb = __shfl_sync(0xffffffffu, src.zb, owner);
+    BoxConic bc;
+    bc.u = __shfl_sync(0xffffffffu, src.u, owner);
+    bc.v = __shfl_sync(0xffffffffu, src.v, owner);
+    bc.ca = __shfl_sync(0xffffffffu, src.ca, owner);
+    bc.cb2 = __shfl_sync(0xffffffffu, src.cb2, owner);
+    bc.cc = __shfl_sync(0xffffffffu, src.cc, owner);
+    bc.k2 = __shfl_sync(0xffffffffu, src.k2, owner);
+    bc.sx = __shfl_sync(0xffffffffu, sx, owner);
+    bc.sy = __shfl_sync(0xffffffffu, sy, owner);
     if (k < total) {
       // rx = px0 | py0 << 16 (low corner), ry = px1 | py1 << 16 (high corner)
-      const int tx0 = (int)(orx & 0xffffu) / kTile, tx1 = (int)(ory & 0xffffu) / kTile;
-      const int ty0 = (int)(orx >> 16) / kTile;
+      bc.rx0 = (int)(orx & 0xffffu); bc.ry0 = (int)(orx >> 16);
+      bc.rx1 = (int)(ory & 0xffffu); bc.ry1 = (int)(ory >> 16);
+      bc.conic_ok = bc.ca > 0.0f && bc.cc > 0.0f;
+      const int tx0 = bc.rx0 / kTile, tx1 = bc.rx1 / kTile;
+      const int ty0 = bc.ry0 / kTile;
       const int w = tx1 - tx0 + 1;
       const int li = k - oe;
-      const int tile = (ty0 + li / w) * tiles_x + tx0 + li % w;
-      f((uint32_t)(base + owner), tile, ozb);
+      const int ty = ty0 + li / w, tx = tx0 + li % w;
+      f((uint32_t)(base + owner), ty * tiles_x + tx, ozb, block_mask_c(bc, tx * kTile, ty * kTile));
     }
   }
 }
 
 // the pair's key into its tile's bucket (slot from the tile's atomic cursor),
 // or into the overflow list once the bucket is full; with an active-tile mask
-// (NEXT-4) only the pairs of active tiles
+// (NEXT-4) only the pairs of active tiles.  Key = bits(z_c) << 32 | gid << 4 |
+// 8x8-block mask: (tile, bits(z_c), gid) order as before (gids are unique, so
+// the mask bits below them never decide), and the sort emits the pair entry
+// without touching the record.
 __device__ __forceinline__ void bucket_put(const BinWs &w, int64_t cap,
                                            const uint32_t *__restrict__ active, uint32_t gid,
-                                           int tile, uint32_t zb) {
+                                           int tile, uint32_t zb, uint32_t mask) {
   if (active && !((active[tile >> 5] >> (tile & 31)) & 1u)) return;  // tile not sampled
-  const unsigned long long key = ((unsigned long long)zb << 32) | (unsigned long long)gid;
+  const unsigned long long key =
+      ((unsigned long long)zb << 32) | (unsigned long long)((gid << 4) | mask);
   const uint32_t slot = atomicAdd(w.cur + tile, 1u);
   if (slot < (uint32_t)kBucketCap) {
     w.bucket[(int64_t)tile * kBucketCap + slot] = key;

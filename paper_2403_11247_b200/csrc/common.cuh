@@ -420,9 +420,7 @@ __device__ __forceinline__ bool box_may_hit(const BoxConic &c, int bx0, int by0,
   const float margin = 0.01f + 2e-5f * (c.ca * DX * DX + fabsf(c.cb2) * DX * DY + c.cc * DY * DY);
   return !(qmin > c.k2 + margin);  // NaN keeps the block
 }
-__device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1, const uint4 &v3,
-                                               int X0, int Y0) {
-  const BoxConic c = box_conic(v0, v1, v3);
+__device__ __forceinline__ uint32_t block_mask_c(const BoxConic &c, int X0, int Y0) {
   uint32_t m = 0;
 #pragma unroll
   for (int w = 0; w < 4; w++) {
@@ -430,6 +428,10 @@ __device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1,
     if (box_may_hit(c, bx0, by0, bx0 + 7, by0 + 7)) m |= 1u << w;
   }
   return m;
+}
+__device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1, const uint4 &v3,
+                                               int X0, int Y0) {
+  return block_mask_c(box_conic(v0, v1, v3), X0, Y0);
 }
 // The same test on the tile's sixteen 4x4 blocks (bit qy * 4 + qx), evaluated
 // only inside the 8x8 blocks whose bit m8 carries (a 4x4 block of a culled

@@ -108,15 +108,14 @@ __device__ __forceinline__ void project_prelude(
 }
 
 // The view part (Eq 2, R2-R7, R21): Gaussian i's 64-byte record and pair count
-// in the view of pc; for the fused bucket pass also the count, the
-// pixel-rectangle words and bits(z_c) (0 if culled).
+// in the view of pc; for the fused bucket pass also what the pairs need
+// (PairSrc: the count, the pixel-rectangle words, bits(z_c) and the conic;
+// count 0 if culled).
 __device__ __forceinline__ void project_view(int64_t i, const GPre &g, const ProjConst &pc,
                                              const float *V, float4 *__restrict__ r,
-                                             int32_t *__restrict__ count, int &c_out,
-                                             uint32_t &rx_out, uint32_t &ry_out,
-                                             uint32_t &zb_out) {
+                                             int32_t *__restrict__ count, PairSrc &ps) {
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  c_out = 0; rx_out = 0; ry_out = 0; zb_out = 0;
+  ps = pair_src_none();
   bool ok = g.ok;
   float xc = 0, yc = 0, zc = 0;
   if (ok) {
@@ -177,11 +176,12 @@ __device__ __forceinline__ void project_view(int64_t i, const GPre &g, const Pro
   // inclusive pixel rectangle as two u16x2 corners (low | high), DESIGN.md §4
   r[3] = make_float4(__uint_as_float((uint32_t)px0 | ((uint32_t)py0 << 16)),
                      __uint_as_float((uint32_t)px1 | ((uint32_t)py1 << 16)), 0.f, 0.f);
-  c_out = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
-  rx_out = (uint32_t)px0 | ((uint32_t)py0 << 16);
-  ry_out = (uint32_t)px1 | ((uint32_t)py1 << 16);
-  zb_out = __float_as_uint(zc);
-  count[i] = c_out;
+  ps.c = (tx1 - tx0 + 1) * (ty1 - ty0 + 1);
+  ps.rx = (uint32_t)px0 | ((uint32_t)py0 << 16);
+  ps.ry = (uint32_t)px1 | ((uint32_t)py1 << 16);
+  ps.zb = __float_as_uint(zc);
+  ps.u = u; ps.v = v; ps.ca = ca; ps.cb2 = DADD(cbn, cbn); ps.cc = cc; ps.k2 = g.k2;
+  count[i] = ps.c;
 }
 
 // Gaussian i (< n) in one view: its 64-byte record and pair count (+ the
@@ -193,14 +193,14 @@ __device__ __forceinline__ void project_one(
     const float *__restrict__ lsc, const float *__restrict__ quat,
     const float *__restrict__ mask, const DecodeArgs &dec, int use_dec, ProjConst &pc,
     const float *__restrict__ view_dev, float4 *__restrict__ rec, int32_t *__restrict__ count,
-    int &c_out, uint32_t &rx_out, uint32_t &ry_out, uint32_t &zb_out) {
+    PairSrc &ps) {
   if (view_dev) {  // the view lives in device memory (graph-captured pose updates)
 #pragma unroll
     for (int k = 0; k < 12; k++) pc.V[k] = __ldg(view_dev + k);
   }
   GPre g;
   project_prelude<LF>(i, n, n_dev, mean, opac, rgb, lsc, quat, mask, dec, use_dec, pc.tau, g);
-  project_view(i, g, pc, pc.V, rec + i * 4, count, c_out, rx_out, ry_out, zb_out);
+  project_view(i, g, pc, pc.V, rec + i * 4, count, ps);
 }
 
 // a1 + a2-decode + a3 (+ a4, BIN): one thread per Gaussian; with BIN the warp
@@ -216,15 +216,14 @@ __global__ void __launch_bounds__(256) k_project(
     const float *__restrict__ view_dev, float4 *__restrict__ rec, int32_t *__restrict__ count,
     BinWs w, int tiles_x, int64_t cap, const uint32_t *__restrict__ active) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int c = 0;
-  uint32_t rx = 0, ry = 0, zb = 0;
+  PairSrc ps = pair_src_none();
   if (i < n)
     project_one<LF>(i, n, n_dev, mean, opac, rgb, lsc, quat, mask, dec, use_dec, pc, view_dev,
-                    rec, count, c, rx, ry, zb);
+                    rec, count, ps);
   if constexpr (BIN) {
-    expand_warp_regs(i - (threadIdx.x & 31), c, rx, ry, zb, tiles_x,
-                     [&](uint32_t gid, int tile, uint32_t z) {
-                       bucket_put(w, cap, active, gid, tile, z);
+    expand_warp_regs(i - (threadIdx.x & 31), ps, tiles_x,
+                     [&](uint32_t gid, int tile, uint32_t z, uint32_t m) {
+                       bucket_put(w, cap, active, gid, tile, z, m);
                      });
   }
 }
@@ -256,17 +255,15 @@ __global__ void __launch_bounds__(256) k_project_views(
   if (i < n)
     project_prelude<LF>(i, n, n_dev, mean, opac, rgb, lsc, quat, mask, dec, use_dec, pc.tau, g);
   for (int v = 0; v < nv; v++) {
-    int c = 0;
-    uint32_t rx = 0, ry = 0, zb = 0;
+    PairSrc ps = pair_src_none();
     if (i < n)
-      project_view(i, g, pc, vm.V[v], rec + v * rec_stride + i * 4, count + v * count_stride, c,
-                   rx, ry, zb);
+      project_view(i, g, pc, vm.V[v], rec + v * rec_stride + i * 4, count + v * count_stride, ps);
     if constexpr (BIN) {
       const BinWs wv = ws_at(w, v * ws_stride);
       const uint32_t *act = active ? active + v * active_stride : nullptr;
-      expand_warp_regs(i - (threadIdx.x & 31), c, rx, ry, zb, tiles_x,
-                       [&](uint32_t gid, int tile, uint32_t z) {
-                         bucket_put(wv, cap, act, gid, tile, z);
+      expand_warp_regs(i - (threadIdx.x & 31), ps, tiles_x,
+                       [&](uint32_t gid, int tile, uint32_t z, uint32_t m) {
+                         bucket_put(wv, cap, act, gid, tile, z, m);
                        });
     }
   }
