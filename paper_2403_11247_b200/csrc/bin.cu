@@ -31,8 +31,8 @@
 
 namespace csplat {
 
-constexpr int kCtaCap = 2048;      // keys per tile sorted in shared memory (16 KB)
-constexpr int kSortThreads = 128;  // threads per tile in k_sort_tiles
+constexpr int kCtaCap = 1024;      // keys per tile sorted in shared memory (8 KB: ~28 one-warp CTAs per SM)
+constexpr int kSortThreads = 32;   // threads per tile in k_sort_tiles (one warp)
 static inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 BinWs bin_carve(void *ws, int64_t cap, int64_t T) {
@@ -149,61 +149,57 @@ __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len
   for (int k = tid; k < len; k += nthr) pair_gid[(int64_t)start + k] = pair_entry(a[k]);
 }
 
-// Register-resident bitonic sort of up to 2 * kSortThreads = 256 keys: thread t
-// holds elements 2t (x0) and 2t+1 (x1); missing elements are +inf (~0, above
-// every key: bits(z_c) of a finite depth is below 0x7f800000).  Same
-// all-ascending network as bitonic_sort, run for blocks up to np2: the
-// compare-exchange partner is in the same thread (distance 1), in lane
-// t ^ (distance / 2) of the same warp (shuffles), or in another warp (one
-// double-buffered shared-memory exchange and one CTA barrier per stage; three
-// such stages at np2 = 256).
-__device__ __forceinline__ void cx2(unsigned long long &x, unsigned long long p, bool keep_min) {
-  x = keep_min ? (p < x ? p : x) : (p < x ? x : p);
+// One warp sorts up to 256 keys in registers: lane l holds elements 8l .. 8l+7
+// (blocked), missing elements +inf.  The same all-ascending bitonic network as
+// above; a compare-exchange at distance m < 8 is inside the lane, at m >= 8 the
+// partner is element t ^ (m & 7) of lane l ^ (m >> 3) (one 64-bit shuffle per
+// element).  21 of the 36 stages at 256 keys are lane-local, and there is no
+// CTA barrier (round 1's 128-thread form: 33 shuffle stages, 3 barriers).
+__device__ __forceinline__ void cx_lane(unsigned long long (&x)[8], int a, int b) {
+  const unsigned long long lo = x[a] < x[b] ? x[a] : x[b], hi = x[a] < x[b] ? x[b] : x[a];
+  x[a] = lo;
+  x[b] = hi;
 }
-
-__device__ __forceinline__ void sort_regs256(unsigned long long &x0, unsigned long long &x1,
-                                             int np2, unsigned long long (*xb)[2 * kSortThreads]) {
-  const int t = threadIdx.x;
-  int buf = 0;
-  // partner values of (x0, x1) from thread t ^ m; `swap` = the partner's elements
-  // in reverse order (the mirror stage pairs element 2t with 2(t^m)+1)
-  auto fetch = [&](int m, bool swap, unsigned long long &p0, unsigned long long &p1) {
-    if (m < 32) {
-      const unsigned long long a = __shfl_xor_sync(0xffffffffu, x0, m);
-      const unsigned long long b = __shfl_xor_sync(0xffffffffu, x1, m);
-      p0 = swap ? b : a;
-      p1 = swap ? a : b;
-    } else {
-      xb[buf][2 * t] = x0;
-      xb[buf][2 * t + 1] = x1;
-      __syncthreads();
-      const int u = t ^ m;
-      p0 = xb[buf][2 * u + (swap ? 1 : 0)];
-      p1 = xb[buf][2 * u + (swap ? 0 : 1)];
-      buf ^= 1;
-    }
-  };
-  for (int k = 2; k <= np2; k <<= 1) {
-    unsigned long long p0, p1;
-    if (k == 2) {  // mirror of the pair (2t, 2t+1): in-thread
-      p0 = x1; x1 = x0 < x1 ? x1 : x0; x0 = p0 < x0 ? p0 : x0;
-    } else {       // mirror stage: element e pairs with e ^ (k - 1)
-      fetch((k - 1) >> 1, true, p0, p1);
-      const bool lower = ((2 * t) & (k >> 1)) == 0;
-      cx2(x0, p0, lower);
-      cx2(x1, p1, lower);
-    }
-    for (int j = k >> 2; j >= 1; j >>= 1) {  // element e pairs with e ^ j
-      if (j == 1) {
-        p0 = x1; x1 = x0 < x1 ? x1 : x0; x0 = p0 < x0 ? p0 : x0;
-      } else {
-        fetch(j >> 1, false, p0, p1);
-        const bool lower = ((2 * t) & j) == 0;
-        cx2(x0, p0, lower);
-        cx2(x1, p1, lower);
-      }
+template <int M, int HIBIT>
+__device__ __forceinline__ void warp_stage(unsigned long long (&x)[8], int lane) {
+  // partner e ^ M; the pair's lower element keeps the min
+  if constexpr (M < 8) {
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+      if ((t ^ M) > t) cx_lane(x, t, t ^ M);
+  } else {
+    constexpr int ml = M >> 3, mt = M & 7;
+    const bool lower = (lane & (HIBIT >> 3)) == 0;
+    unsigned long long p[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++) p[t] = __shfl_xor_sync(0xffffffffu, x[t ^ mt], ml);
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      const bool pl = p[t] < x[t];
+      x[t] = (pl == lower) ? p[t] : x[t];
     }
   }
+}
+template <int K, int J>
+__device__ __forceinline__ void warp_cleaners(unsigned long long (&x)[8], int lane) {
+  if constexpr (J >= 1) {
+    warp_stage<J, J>(x, lane);
+    warp_cleaners<K, J / 2>(x, lane);
+  }
+}
+template <int K, int NP2>
+__device__ __forceinline__ void warp_merges(unsigned long long (&x)[8], int lane) {
+  if constexpr (K <= NP2) {
+    warp_stage<K - 1, K / 2>(x, lane);  // mirror
+    warp_cleaners<K, K / 4>(x, lane);   // half-cleaners
+    warp_merges<2 * K, NP2>(x, lane);
+  }
+}
+// the network for NP2 (64, 128 or 256) elements, all stage distances
+// compile-time so the eight keys stay in registers
+template <int NP2>
+__device__ __forceinline__ void sort_warp(unsigned long long (&x)[8]) {
+  warp_merges<2, NP2>(x, threadIdx.x & 31);
 }
 
 // a5 offsets: the exclusive scan of the tiles' (or list positions') pair counts
@@ -310,22 +306,18 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   }
   const int len = (int)(end - start);  // the tile's pair count, or 0 (empty or cut)
   if (len == 0) return;                // (block-uniform)
-  if (len <= 2 * kSortThreads) {  // the common case: sorted in registers
-    const int t = threadIdx.x;
+  if (len <= 256) {  // the common case: one warp, in registers
+    const int l = threadIdx.x;
     const unsigned long long *bk = w.bucket + tile * kBucketCap;
-    unsigned long long x0 = ~0ull, x1 = ~0ull;
-    if (2 * t + 1 < len) {
-      const ulonglong2 v = reinterpret_cast<const ulonglong2 *>(bk)[t];
-      x0 = v.x;
-      x1 = v.y;
-    } else if (2 * t < len) {
-      x0 = bk[2 * t];
-    }
-    int np2 = 2;
-    while (np2 < len) np2 <<= 1;
-    sort_regs256(x0, x1, np2, reinterpret_cast<unsigned long long(*)[2 * kSortThreads]>(sk));
-    if (2 * t < len) pair_gid[(int64_t)start + 2 * t] = pair_entry(x0);
-    if (2 * t + 1 < len) pair_gid[(int64_t)start + 2 * t + 1] = pair_entry(x1);
+    unsigned long long x[8];
+#pragma unroll
+    for (int t = 0; t < 8; t++) x[t] = 8 * l + t < len ? bk[8 * l + t] : ~0ull;
+    if (len <= 64) sort_warp<64>(x);         // lanes 8+ hold only +inf: 21 stages
+    else if (len <= 128) sort_warp<128>(x);  // 28 stages
+    else sort_warp<256>(x);                  // 36 stages
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+      if (8 * l + t < len) pair_gid[(int64_t)start + 8 * l + t] = pair_entry(x[t]);
     return;
   }
   unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
