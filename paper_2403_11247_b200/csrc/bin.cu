@@ -74,8 +74,8 @@ size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam) {
 // mask (NEXT-4, csplat_bin_tiles_active) only the pairs of active tiles.
 __global__ void __launch_bounds__(256) k_bucket(int64_t n, const int32_t *__restrict__ count,
                                                 const uint4 *__restrict__ rec4, int tiles_x,
-                                                int64_t cap, const uint32_t *__restrict__ active,
-                                                BinWs w) {
+                                                int64_t T, int64_t cap,
+                                                const uint32_t *__restrict__ active, BinWs w) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(256) k_bucket(int64_t n, const int32_t *__rest
       bucket_put(w, cap, active, gid, tile, z, m);
     });
   }
+  bucket_pass_done(w, T);
 }
 
 
@@ -204,7 +205,7 @@ __device__ __forceinline__ void sort_warp(unsigned long long (&x)[8]) {
 
 // a5 offsets: the exclusive scan of the tiles' (or list positions') pair counts
 // into the look-up words, one CTA per view (grid.x = view)
-constexpr int kScanThreads = 1024, kScanPer = 4;
+constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(int64_t T, BinWs w, int64_t ws_stride,
                                                             const int32_t *__restrict__ list,
                                                             int64_t list_stride) {
@@ -212,47 +213,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(int64_t T, BinWs w, 
     w = ws_at(w, (int64_t)blockIdx.x * ws_stride);
     if (list) list += (int64_t)blockIdx.x * list_stride;
   }
-  __shared__ unsigned long long wsum[32];
-  const int64_t npos = list ? (int64_t)list[0] : T;
-  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  unsigned long long carry = 0;
-  for (int64_t base = 0; base < npos; base += kScanThreads * kScanPer) {
-    uint32_t c[kScanPer];
-    unsigned long long own = 0;
-#pragma unroll
-    for (int k = 0; k < kScanPer; k++) {
-      const int64_t p = base + (int64_t)t * kScanPer + k;
-      c[k] = p < npos ? w.cur[list ? list[1 + p] : p] : 0u;
-      own += c[k];
-    }
-    unsigned long long inc = own;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += y;
-    }
-    if (lane == 31) wsum[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      unsigned long long v = wsum[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += y;
-      }
-      wsum[lane] = v;
-    }
-    __syncthreads();
-    unsigned long long ex = carry + (wid > 0 ? wsum[wid - 1] : 0ull) + inc - own;
-#pragma unroll
-    for (int k = 0; k < kScanPer; k++) {
-      const int64_t p = base + (int64_t)t * kScanPer + k;
-      if (p < npos) w.status[p] = ex;
-      ex += c[k];
-    }
-    carry += wsum[31];
-    __syncthreads();  // wsum is rewritten by the next round
-  }
+  tile_scan_cta(w, list ? (int64_t)list[0] : T, list);
 }
 
 cudaError_t launch_tile_scan(const BinWs &w, int64_t T, int nv, int64_t ws_stride,
@@ -382,10 +343,10 @@ cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const c
   const int64_t max_blocks = (int64_t)sms * 8;
   if (blocks > max_blocks) blocks = max_blocks;
   if (blocks < 1) blocks = 1;
-  if (n > 0) k_bucket<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, cap,
+  if (n > 0) k_bucket<<<(unsigned)blocks, 256, 0, s>>>(n, count, rec4, ci.tiles_x, T, cap,
                                                       tile_active, w);
   e = cudaGetLastError();
-  if (e == cudaSuccess) e = launch_tile_scan(w, T, 1, 0, nullptr, 0, s);
+  // (n == 0: no bucket pass; every offset is 0 from the reset)
   if (e != cudaSuccess) return e;
   return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range,
                            n_pairs_dev, s);

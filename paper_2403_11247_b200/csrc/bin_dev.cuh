@@ -17,6 +17,8 @@ struct BinWs {
   uint32_t *ovf_tile;                // [cap] tile of each overflow entry
   unsigned long long *ovf_key;       // [cap] its key
   unsigned long long *keys;          // [cap] global-memory sort scratch (tiles > kCtaCap)
+  // ovf_n[1]: CTAs of the bucket pass that finished (the last one runs the
+  // offset scan, tile_scan_cta); zeroed with the head
 };
 
 BinWs bin_carve(void *ws, int64_t cap, int64_t T);
@@ -60,6 +62,71 @@ cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t nctas, int64_t T, in
                                     int64_t cap, const void *rec, uint32_t *pair_gid,
                                     uint32_t *tile_range, int64_t *n_pairs_dev,
                                     const SortViews &sv, int nv, cudaStream_t s);
+
+// a5 offsets: the exclusive scan of the T cursors (the tiles' pair counts, or
+// of list positions' counts) into the offset words, by one whole CTA
+// (blockDim.x a multiple of 32, <= 1024)
+__device__ __forceinline__ void tile_scan_cta(const BinWs &w, int64_t npos,
+                                              const int32_t *__restrict__ list) {
+  constexpr int kPer = 4;
+  __shared__ unsigned long long wsum[32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
+  const int64_t step = (int64_t)blockDim.x * kPer;
+  unsigned long long carry = 0;
+  for (int64_t base = 0; base < npos; base += step) {
+    uint32_t c[kPer];
+    unsigned long long own = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+      const int64_t p = base + (int64_t)t * kPer + k;
+      c[k] = p < npos ? *(volatile uint32_t *)&w.cur[list ? list[1 + p] : p] : 0u;
+      own += c[k];
+    }
+    unsigned long long inc = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long v = lane < nw ? wsum[lane] : 0ull;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    unsigned long long ex = carry + (wid > 0 ? wsum[wid - 1] : 0ull) + inc - own;
+#pragma unroll
+    for (int k = 0; k < kPer; k++) {
+      const int64_t p = base + (int64_t)t * kPer + k;
+      if (p < npos) w.status[p] = ex;
+      ex += c[k];
+    }
+    carry += wsum[nw - 1];
+    __syncthreads();  // wsum is rewritten by the next round
+  }
+}
+// The end of a bucket-pass kernel: the CTA that finishes last (every other
+// CTA's cursor atomics are visible after its fence and ticket) runs the offset
+// scan, so the sort needs no separate scan launch.  Block-uniform; all threads.
+__device__ __forceinline__ void bucket_pass_done(const BinWs &w, int64_t T) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(w.ovf_n + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    tile_scan_cta(w, T, nullptr);
+  }
+}
 
 // What a Gaussian contributes to the bucket pass: its pair count c, its pixel
 // rectangle corners rx, ry (record words 12, 13), bits(z_c) zb, and the conic

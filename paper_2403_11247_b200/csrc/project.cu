@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(256) k_project(
     const float *__restrict__ lsc, const float *__restrict__ quat,
     const float *__restrict__ mask, DecodeArgs dec, int use_dec, ProjConst pc,
     const float *__restrict__ view_dev, float4 *__restrict__ rec, int32_t *__restrict__ count,
-    BinWs w, int tiles_x, int64_t cap, const uint32_t *__restrict__ active) {
+    BinWs w, int tiles_x, int64_t T, int64_t cap, const uint32_t *__restrict__ active) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   PairSrc ps = pair_src_none();
   if (i < n)
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(256) k_project(
                      [&](uint32_t gid, int tile, uint32_t z, uint32_t m) {
                        bucket_put(w, cap, active, gid, tile, z, m);
                      });
+    bucket_pass_done(w, T);
   }
 }
 
@@ -298,6 +299,8 @@ static cudaError_t launch_project_impl(const csplat_gaussians &g, const DecodeAr
                                       int64_t cap, const uint32_t *active, cudaStream_t s) {
   if (g.n == 0) return cudaSuccess;
   const ProjConst pc = make_proj_const(cam, view, tau, dilation);
+  const CamInfo ci = cam_info(cam);
+  const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
   DecodeArgs d{};
   if (dec) d = *dec;
   const int threads = 256;
@@ -312,7 +315,7 @@ static cudaError_t launch_project_impl(const csplat_gaussians &g, const DecodeAr
   kern<<<(unsigned)blocks, threads, 0, s>>>(g.n, g.n_dev, g.mean, g.opacity, g.rgb, g.log_scale,
                                             g.quat, g.mask, d, dec ? 1 : 0, pc, view_dev,
                                             reinterpret_cast<float4 *>(rec), count,
-                                            bin ? *bw : BinWs{}, tiles_x, cap, active);
+                                            bin ? *bw : BinWs{}, tiles_x, T, cap, active);
   return cudaGetLastError();
 }
 
@@ -398,9 +401,9 @@ cudaError_t launch_project_bin(const csplat_gaussians &g, const DecodeArgs *dec,
   BinWs w = bin_carve(ws, cap, T);
   cudaError_t e = bin_reset(w, T, s);
   if (e != cudaSuccess) return e;
+  // (the bucket pass's last CTA writes the tile offsets: bucket_pass_done)
   e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
                           ci.tiles_x, cap, tile_active, s);
-  if (e == cudaSuccess) e = launch_tile_scan(w, T, 1, 0, nullptr, 0, s);
   if (e != cudaSuccess) return e;
   return launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range,
                            n_pairs_dev, s);
@@ -480,9 +483,9 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
   if (e != cudaSuccess) return e;
   if (bwd && (e = bwd_prep(g, bwd->flags, bwd->out, bwd->ws, bwd->loss, s)) != cudaSuccess)
     return e;
+  // (the bucket pass's last CTA writes the tile offsets: bucket_pass_done)
   e = launch_project_impl(g, dec, cam, view, view_dev, tau, dilation, rec, count, &w,
                           ci.tiles_x, cap, nullptr, s);
-  if (e == cudaSuccess) e = launch_tile_scan(w, T, 1, 0, nullptr, 0, s);
   if (e != cudaSuccess) return e;
   // fork into K streams, one tile chunk each: sort the chunk, render it (and
   // run its backward); the chunks run concurrently, so one chunk's issue-bound
