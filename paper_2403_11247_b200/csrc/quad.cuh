@@ -65,10 +65,13 @@ __device__ __forceinline__ uint32_t mask16(uint32_t entry, const uint4 &w3, int 
 // the chunk [c0, c0 + len) of the tile list starting at `start`: records to
 // L.rec (cp.async, no register staging), 4x4 masks to L.m16, and (backward)
 // the reached-Gaussian bits.  Ends with a CTA barrier.
+// need8: the 8x8 blocks some pixel of which still needs entries (entries whose
+// pair-entry mask misses all of them are not copied: their m16 is 0)
 __device__ __forceinline__ void gather(Lists &L, const float4 *__restrict__ recs,
                                        const uint32_t *__restrict__ pair_gid, uint32_t start,
                                        int c0, int len, int X0, int Y0,
-                                       uint32_t *__restrict__ alive, int tid) {
+                                       uint32_t *__restrict__ alive, int tid,
+                                       uint32_t need8 = 0xfu) {
   constexpr int kPer = kChunk / kThreads;
   uint32_t ent[kPer];
 #pragma unroll
@@ -79,7 +82,7 @@ __device__ __forceinline__ void gather(Lists &L, const float4 *__restrict__ recs
 #pragma unroll
   for (int k = 0; k < kPer; k++) {
     const int i = tid + k * kThreads;
-    if (i >= len) continue;
+    if (i >= len || !((ent[k] >> kPairMaskShift) & need8)) continue;
     const float4 *src = recs + (size_t)(ent[k] & kPairGidMask) * 4;
 #pragma unroll
     for (int q = 0; q < 4; q++)
@@ -94,8 +97,11 @@ __device__ __forceinline__ void gather(Lists &L, const float4 *__restrict__ recs
   for (int k = 0; k < kPer; k++) {
     const int i = tid + k * kThreads;
     if (i >= len) continue;
-    const uint4 w3 = *reinterpret_cast<const uint4 *>(&L.rec[i][3]);
-    const uint32_t m = mask16(ent[k], w3, X0, Y0);
+    uint32_t m = 0;
+    if ((ent[k] >> kPairMaskShift) & need8) {
+      const uint4 w3 = *reinterpret_cast<const uint4 *>(&L.rec[i][3]);
+      m = mask16(ent[k], w3, X0, Y0);
+    }
     L.m16[i] = (uint16_t)m;
     if (alive && m) {
       const uint32_t gid = ent[k] & kPairGidMask;

@@ -272,8 +272,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_render_bwd_quad(
   }
   __syncthreads();
   int maxlast = 0;
+  uint32_t need8 = 0;  // 8x8 blocks with a pixel to replay (sparse upstream: the BA's patches)
 #pragma unroll
-  for (int b = 0; b < kNB; b++) maxlast = max(maxlast, sm.wmax[b]);
+  for (int b = 0; b < kNB; b++) {
+    maxlast = max(maxlast, sm.wmax[b]);
+    if (sm.wmax[b] > 0) need8 |= 1u << (((b & 3) >> 1) + 2 * ((b >> 2) >> 1));
+  }
   const int X0 = tx * kTile, Y0 = ty * kTile;
   const float fpx = (float)px;
 
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_render_bwd_quad(
   for (int c1 = maxlast; c1 > 0; c1 -= kChunk) {
     const int c0 = max(0, c1 - kChunk), len = c1 - c0;
     // 1. the chunk's records, 4x4-block masks and the blocks' lists, back to front
-    gather(sm.L, recs, pair_gid, start, c0, len, X0, Y0, alive, tid);
+    gather(sm.L, recs, pair_gid, start, c0, len, X0, Y0, alive, tid, need8);
     build_lists<true>(sm.L, c0, len, sm.wmax, wid, lane);
     // 2. the replay: the quad walks its block's list; 3. quad sums -> accumulator
     const int nr = sm.L.nitems[B];
