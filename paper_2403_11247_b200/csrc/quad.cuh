@@ -1,5 +1,5 @@
-// quad.cuh -- the per-4x4-block entry lists the block-list renderers share
-// (k_render_fwd_quad, render_fwd.cu; k_render_bwd_quad, render_bwd.cu).
+// quad.cuh -- the per-4x4-block entry lists of the block-list backward
+// (k_render_bwd_quad, render_bwd.cu).
 //
 // A CTA of two warps takes one 16x16 tile.  Its sixteen 4x4 pixel blocks each
 // get their own list of the tile's entries; the four lanes of a QUAD (lane / 4
@@ -111,26 +111,24 @@ __device__ __forceinline__ void gather(Lists &L, const float4 *__restrict__ recs
   __syncthreads();
 }
 
-// the warp's eight blocks' lists from L.m16 (after gather): ascending
-// chunk index (forward) or descending (BACK, the backward's replay order);
-// entries at list position >= lim[B] are left out (the backward: a block whose
-// pixels all finished before an entry has nothing to replay)
-template <bool BACK>
+// the warp's eight blocks' lists from L.m16 (after gather), in the backward's
+// replay order (descending chunk index); entries at list position >= lim[B]
+// are left out (a block whose pixels all finished before an entry has nothing
+// to replay)
 __device__ __forceinline__ void build_lists(Lists &L, int c0, int len, const int *lim, int wid,
                                             int lane) {
   int cnt = 0;  // lane rr < 8: block 8 wid + rr's count
   const int rounds = (len + 31) / 32;
   for (int k = 0; k < rounds; k++) {
-    const int i = BACK ? len - 32 * (k + 1) + lane : 32 * k + lane;
-    const uint32_t m = (i >= 0 && i < len) ? L.m16[i] : 0u;
+    const int i = len - 32 * (k + 1) + lane;
+    const uint32_t m = i >= 0 ? L.m16[i] : 0u;
 #pragma unroll
     for (int rr = 0; rr < 8; rr++) {
       const int B = wid * 8 + rr;
-      const bool sel = ((m >> B) & 1u) && (lim == nullptr || c0 + i < lim[B]);
+      const bool sel = ((m >> B) & 1u) && c0 + i < lim[B];
       const uint32_t bal = __ballot_sync(0xffffffffu, sel);
       const int before = __shfl_sync(0xffffffffu, cnt, rr);
-      const int rank = BACK ? __popc(bal >> lane >> 1) : __popc(bal & ((1u << lane) - 1u));
-      if (sel) L.lst[B][before + rank] = (uint8_t)i;
+      if (sel) L.lst[B][before + __popc(bal >> lane >> 1)] = (uint8_t)i;
       if (lane == rr) cnt += __popc(bal);
     }
   }

@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_render_bwd_quad(
     const int c0 = max(0, c1 - kChunk), len = c1 - c0;
     // 1. the chunk's records, 4x4-block masks and the blocks' lists, back to front
     gather(sm.L, recs, pair_gid, start, c0, len, X0, Y0, alive, tid, need8);
-    build_lists<true>(sm.L, c0, len, sm.wmax, wid, lane);
+    build_lists(sm.L, c0, len, sm.wmax, wid, lane);
     // 2. the replay: the quad walks its block's list; 3. quad sums -> accumulator
     const int nr = sm.L.nitems[B];
     const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nr);

@@ -14,7 +14,6 @@
 // the DA of DESIGN.md §3 (bit-exact with the oracle); alpha, T and the sums
 // are float32 with ex2.approx.
 #include "common.cuh"
-#include "quad.cuh"
 
 namespace csplat {
 
@@ -193,100 +192,6 @@ __global__ void __launch_bounds__((kPW + 1) * 32) k_render_fwd(
   }
 }
 
-// ---------------------------------------------------------------------------
-// The block-list forward (CSPLAT_FWD_QUAD, default): the tile's sixteen 4x4
-// blocks each walk their own entry list (quad.cuh) with four lanes, front to
-// back, instead of a warp replaying for its 8x8 block every entry that block
-// may touch (61 % of those (pixel, entry) slots are outside the entry's ellipse
-// on C2).  Quad lane q owns column q of its block: two vertically adjacent
-// pixel pairs, composited with composite_pair above (the same arithmetic).  A
-// quad stops once its 16 pixels terminated (R3), a warp once its quads did, the
-// tile once every pixel did (before gathering the next chunk).
-#ifndef CSPLAT_FWD_QUAD
-#define CSPLAT_FWD_QUAD 0
-#endif
-namespace quad {
-constexpr int kFwdMinBlocks = 10;
-
-__global__ void __launch_bounds__(kThreads, kFwdMinBlocks) k_render_fwd_quad(
-    const float4 *__restrict__ recs, const uint32_t *__restrict__ pair_gid,
-    const uint32_t *__restrict__ range, int W, int H, int tiles_x, float amax, float tmin,
-    float *__restrict__ color, float *__restrict__ depth, float *__restrict__ sil,
-    float *__restrict__ t_final, int32_t *__restrict__ n_contrib, int tile0,
-    const int32_t *__restrict__ list) {
-  __shared__ __align__(16) Lists L;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int tb = (int)blockIdx.x;
-  if (list && tb >= list[0]) return;
-  const int tile = list ? list[1 + tb] : tile0 + tb;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const uint32_t start = range[2 * tile], end = range[2 * tile + 1];
-  const int len = (int)(end - start);
-  const Geo gq = geo(tx, ty, wid, lane);
-  const int X0 = tx * kTile, Y0 = ty * kTile;
-  // the lane's pixels: p[h][k] = (column px, row by + 2h + k)
-  PixState p[2][2];
-#pragma unroll
-  for (int h = 0; h < 2; h++)
-#pragma unroll
-    for (int k = 0; k < 2; k++)
-      p[h][k] = PixState{1.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0,
-                         (gq.px < W && gq.by + 2 * h + k < H) ? 0 : 1};
-  const float fpx = (float)gq.px;
-  const f2_t FPY0 = pk2((float)gq.by, (float)(gq.by + 1));
-  const f2_t FPY1 = pk2((float)(gq.by + 2), (float)(gq.by + 3));
-  auto lane_done = [&]() { return (p[0][0].done & p[0][1].done & p[1][0].done & p[1][1].done) != 0; };
-  for (int c0 = 0; c0 < len; c0 += kChunk) {
-    const int clen = min(kChunk, len - c0);
-    gather(L, recs, pair_gid, start, c0, clen, X0, Y0, nullptr, tid);
-    build_lists<false>(L, c0, clen, nullptr, wid, lane);
-    const int nr = L.nitems[gq.B];
-    const uint8_t *lst = L.lst[gq.B];
-    for (int e = 0;; e++) {
-      // the quad's four lanes all terminated: the block is done
-      const uint32_t dn = __ballot_sync(0xffffffffu, lane_done());
-      const bool qdone = ((dn >> (4 * gq.r)) & 0xfu) == 0xfu;
-      const bool act = e < nr && !qdone;
-      if (!__any_sync(0xffffffffu, act)) break;
-      const int i = act ? (int)lst[e] : kChunk;
-      const float4 r0 = L.rec[i][0], r1 = L.rec[i][1];
-      const float dx = DSUB(fpx, r0.x);
-      const float cadx = DMUL(r0.z, dx), cbdx = DMUL(r0.w, dx);
-      const int idx = c0 + i + 1;
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        // the DA q of both pixels of the pair on f32x2 (same roundings as the scalar form)
-        const f2_t DY = sub2(h ? FPY1 : FPY0, pk2(r0.y, r0.y));
-        const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx),
-                            fma2(pk2(cbdx, cbdx), DY, mul2(mul2(pk2(r1.x, r1.x), DY), DY)));
-        const float q0 = lo2(Q), q1 = hi2(Q);
-        const bool h0 = act & (p[h][0].done == 0) & da_in_range(q0, r1.z);
-        const bool h1 = act & (p[h][1].done == 0) & da_in_range(q1, r1.z);
-        const float4 r2 = L.rec[i][2];
-        composite_pair(p[h][0], p[h][1], h0, h1, q0, q1, r1.y, r1.w, r2, amax, tmin, idx);
-      }
-    }
-    // every pixel of the tile terminated: no later chunk can change it (this
-    // barrier also keeps the next gather from overwriting the lists in use)
-    if (__syncthreads_and(lane_done())) break;
-  }
-  const int64_t HW = (int64_t)W * H;
-  if (gq.px < W) {
-#pragma unroll
-    for (int h = 0; h < 2; h++)
-#pragma unroll
-      for (int k = 0; k < 2; k++) {
-        const int py = gq.by + 2 * h + k;
-        if (py >= H) continue;
-        const int64_t o = (int64_t)py * W + gq.px;
-        const PixState &q = p[h][k];
-        color[o] = q.r; color[HW + o] = q.g; color[2 * HW + o] = q.b;
-        depth[o] = q.D; sil[o] = q.S; t_final[o] = q.T; n_contrib[o] = q.last;
-      }
-  }
-}
-}  // namespace quad
-
 cudaError_t launch_render_fwd(const void *rec, const uint32_t *pair_gid,
                               const uint32_t *tile_range,
                               const csplat_camera &cam, const csplat_params &prm, float *color,
@@ -296,12 +201,6 @@ cudaError_t launch_render_fwd(const void *rec, const uint32_t *pair_gid,
   const int T = ci.tiles_x * ci.tiles_y;
   if (ntiles < 0) ntiles = T - tile0;
   if (ntiles <= 0) return cudaSuccess;
-#if CSPLAT_FWD_QUAD
-  quad::k_render_fwd_quad<<<ntiles, quad::kThreads, 0, s>>>(
-      static_cast<const float4 *>(rec), pair_gid, tile_range, ci.W, ci.H, ci.tiles_x,
-      prm.alpha_max, prm.t_min, color, depth, sil, t_final, n_contrib, tile0, list);
-  return cudaGetLastError();
-#endif
   CUtensorMap tmap;
   cudaError_t e = rec_tensor_map(rec, &tmap);
   if (e != cudaSuccess) return e;
