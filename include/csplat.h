@@ -209,7 +209,8 @@ int csplat_chain_views(const csplat_gaussians *g, const csplat_codebook *cb,
  *                             y half w >> 1 of the tile) set unless alpha < 1/255
  *                             provably holds over that whole block.
  *                             The renderers gather each listed record from rec
- *                             (one 64-byte TMA bulk copy per entry).
+ *                             (the forward by TMA gather4, the backward by
+ *                             cp.async into shared memory).
  *   tile_range[T+1][2]        [start, end) of every tile, T = ceil(W/16)*ceil(H/16);
  *                             entry T is the view's STATUS slot {status word, max
  *                             n_pairs}: the library ORs CSPLAT_STATUS_CAPACITY into
