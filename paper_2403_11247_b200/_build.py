@@ -21,7 +21,7 @@ def nvcc_flags(extra=()):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, h) for h in ("common.cuh", "bin_dev.cuh")] + \
+    deps = srcs + [os.path.join(CSRC, h) for h in ("common.cuh", "bin_dev.cuh", "quad.cuh", "composite.cuh")] + \
         [os.path.join(ROOT, "include", "csplat.h")]
     if not force and os.path.exists(LIB):
         t = os.path.getmtime(LIB)

@@ -1,5 +1,5 @@
-// quad.cuh -- the per-4x4-block entry lists of the block-list backward
-// (k_render_bwd_quad, render_bwd.cu).
+// quad.cuh -- the per-4x4-block entry lists and the replay of the block-list
+// backward (k_render_bwd_quad, render_bwd.cu).
 //
 // A CTA of two warps takes one 16x16 tile.  Its sixteen 4x4 pixel blocks each
 // get their own list of the tile's entries; the four lanes of a QUAD (lane / 4
@@ -14,6 +14,16 @@
 #include "common.cuh"
 
 namespace csplat {
+
+constexpr int kAcc = 12;          // backward accumulator floats per Gaussian
+constexpr int kV = 10;            // backward partials per (pixel, entry)
+
+__device__ __forceinline__ float ex2_approx_b(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 namespace quad {
 
 constexpr int kPW = 2;                    // warps per CTA (16x8 pixels each)
@@ -134,6 +144,143 @@ __device__ __forceinline__ void build_lists(Lists &L, int c0, int len, const int
   }
   if (lane < 8) L.nitems[wid * 8 + lane] = cnt;
   __syncwarp();
+}
+
+// ---- the replay (render_bwd.cu's header comment): quad lane q's two pixel
+// pairs, the per-entry pieces, the quad reduction, and one chunk's walk
+// one pixel pair's replay state and upstream (registers of its lane)
+struct QPair {
+  f2_t T, B, FPY, GR, GG, GB, GD, GS;
+  int last0, last1;
+};
+
+// a pixel pair's partial terms of one entry (f32x2, summed over the quad's pixels)
+struct QTerms {
+  f2_t AV, TT, T2, GDL, WD, WR, WG, WB;
+};
+
+// one entry at one pixel pair in two pieces, so two entries can interleave: the front (q, the
+// validity, G, alpha, 1 / (1 - alpha), v -- independent of the replay state)
+// and the state update with the partial terms
+struct QFront {
+  f2_t DY, G, AL, RC, VV;
+  bool nc0, nc1;
+};
+__device__ __forceinline__ QFront pair_front(const QPair &P, int j, float dx, float cadx,
+                                             float cbdx, const float4 &r0, const float4 &r1,
+                                             const float4 &r2, float amax) {
+  QFront f;
+  f.DY = sub2(P.FPY, pk2(r0.y, r0.y));
+  const f2_t Y = mul2(mul2(pk2(r1.x, r1.x), f.DY), f.DY);
+  const f2_t X = fma2(pk2(cbdx, cbdx), f.DY, Y);
+  const f2_t Q = fma2(pk2(cadx, cadx), pk2(dx, dx), X);
+  const float q0 = lo2(Q), q1 = hi2(Q);
+  const bool val0 = (j < P.last0) & da_in_range(q0, r1.z);
+  const bool val1 = (j < P.last1) & da_in_range(q1, r1.z);
+  const f2_t QM = pk2(val0 ? q0 : __int_as_float(0x7f800000), val1 ? q1 : __int_as_float(0x7f800000));
+  const f2_t QE = mul2(QM, pk2(-0.72134752f, -0.72134752f));
+  f.G = pk2(ex2_approx_b(lo2(QE)), ex2_approx_b(hi2(QE)));
+  const f2_t AR = mul2(pk2(r1.y, r1.y), f.G);
+  f.AL = pk2(fminf(amax, lo2(AR)), fminf(amax, hi2(AR)));  // R1
+  f.nc0 = lo2(AR) < amax;
+  f.nc1 = hi2(AR) < amax;
+  const f2_t OM = sub2(pk2(1.0f, 1.0f), f.AL);
+  float rc0, rc1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc0) : "f"(lo2(OM)));  // alpha <= alpha_max < 1
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc1) : "f"(hi2(OM)));
+  f.RC = pk2(rc0, rc1);
+  f.VV = fma2(pk2(r2.x, r2.x), P.GR,
+              fma2(pk2(r2.y, r2.y), P.GG,
+                   fma2(pk2(r2.z, r2.z), P.GB, fma2(pk2(r1.w, r1.w), P.GD, P.GS))));
+  return f;
+}
+__device__ __forceinline__ QTerms pair_state(QPair &P, const QFront &f) {
+  P.T = mul2(P.T, f.RC);
+  const f2_t VB = sub2(f.VV, P.B);
+  P.B = fma2(f.AL, VB, P.B);
+  QTerms o;
+  const f2_t W = mul2(f.AL, P.T);
+  const f2_t D0 = mul2(P.T, VB);
+  const f2_t DL = pk2(f.nc0 ? lo2(D0) : 0.0f, f.nc1 ? hi2(D0) : 0.0f);  // R23
+  o.AV = mul2(f.AL, DL);
+  o.GDL = mul2(f.G, DL);
+  o.TT = mul2(o.AV, f.DY);
+  o.T2 = mul2(o.TT, f.DY);
+  o.WD = mul2(W, P.GD);
+  o.WR = mul2(W, P.GR);
+  o.WG = mul2(W, P.GG);
+  o.WB = mul2(W, P.GB);
+  return o;
+}
+// the quad's ten sums of one entry's terms over its four lanes (transposed
+// shuffle reduction) into the accumulator
+__device__ __forceinline__ void quad_flush(const QTerms &a, float dx, bool hi, int ri, bool act,
+                                           float *dst) {
+  float v[kV];
+  const float sav = lo2(a.AV) + hi2(a.AV), stt = lo2(a.TT) + hi2(a.TT);
+  v[0] = dx * sav;
+  v[1] = stt;
+  v[2] = dx * v[0];
+  v[3] = dx * stt;
+  v[4] = lo2(a.T2) + hi2(a.T2);
+  v[5] = lo2(a.GDL) + hi2(a.GDL);
+  v[6] = lo2(a.WD) + hi2(a.WD);
+  v[7] = lo2(a.WR) + hi2(a.WR);
+  v[8] = lo2(a.WG) + hi2(a.WG);
+  v[9] = lo2(a.WB) + hi2(a.WB);
+  // lanes 0-1 keep (v0 v1 v2 v3 v8), lanes 2-3 (v4 v5 v6 v7 v9); then a
+  // butterfly over the lane pair
+  float x[5];
+#pragma unroll
+  for (int k = 0; k < 5; k++) {
+    const float s1 = k < 4 ? v[k] : v[8], s2 = k < 4 ? v[4 + k] : v[9];
+    const float keep = hi ? s2 : s1, send = hi ? s1 : s2;
+    x[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+#pragma unroll
+  for (int k = 0; k < 5; k++) x[k] += __shfl_xor_sync(0xffffffffu, x[k], 1);
+  const float v9 = __shfl_xor_sync(0xffffffffu, x[4], 2);  // lane 1 <- lane 3's v9
+  if (act) {
+    if ((ri & 1) == 0) red_add_v4(dst + (hi ? 4 : 0), x[0], x[1], x[2], x[3]);
+    else if (!hi) red_add_v2(dst + 8, x[4], v9);
+  }
+}
+__device__ __forceinline__ QTerms qadd(const QTerms &a, const QTerms &b) {
+  QTerms o;
+  o.AV = add2(a.AV, b.AV); o.TT = add2(a.TT, b.TT); o.T2 = add2(a.T2, b.T2);
+  o.GDL = add2(a.GDL, b.GDL); o.WD = add2(a.WD, b.WD); o.WR = add2(a.WR, b.WR);
+  o.WG = add2(a.WG, b.WG); o.WB = add2(a.WB, b.WB);
+  return o;
+}
+
+
+// the quad walks its block's list of the chunk [c0, ...) (L, back to front),
+// two entries per iteration: both fronts, the two state updates in list order,
+// both partial sums -- the independent halves interleave
+__device__ __forceinline__ void replay_chunk(const Lists &L, QPair (&P)[2], int B, int ri, int c0,
+                                             float fpx, float amax, float *__restrict__ accg) {
+  const int nr = L.nitems[B];
+  const int nmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nr);
+  const uint8_t *lst = L.lst[B];
+  const bool hi = ri >= 2;
+  for (int e = 0; e < nmax; e += 2) {
+    // past its list a quad replays the zero record with j beyond every pixel's
+    // last contributor: no state change, exact zero partials
+    const bool actA = e < nr, actB = e + 1 < nr;
+    const int iA = actA ? (int)lst[e] : kChunk, iB = actB ? (int)lst[e + 1] : kChunk;
+    const float4 a0 = L.rec[iA][0], a1 = L.rec[iA][1], a2 = L.rec[iA][2];
+    const float4 b0 = L.rec[iB][0], b1 = L.rec[iB][1], b2 = L.rec[iB][2];
+    const int jA = actA ? c0 + iA : 0x7fffffff, jB = actB ? c0 + iB : 0x7fffffff;
+    const float dxA = DSUB(fpx, a0.x), dxB = DSUB(fpx, b0.x);
+    const QFront fA0 = pair_front(P[0], jA, dxA, DMUL(a0.z, dxA), DMUL(a0.w, dxA), a0, a1, a2, amax);
+    const QFront fA1 = pair_front(P[1], jA, dxA, DMUL(a0.z, dxA), DMUL(a0.w, dxA), a0, a1, a2, amax);
+    const QFront fB0 = pair_front(P[0], jB, dxB, DMUL(b0.z, dxB), DMUL(b0.w, dxB), b0, b1, b2, amax);
+    const QFront fB1 = pair_front(P[1], jB, dxB, DMUL(b0.z, dxB), DMUL(b0.w, dxB), b0, b1, b2, amax);
+    const QTerms tA0 = pair_state(P[0], fA0), tA1 = pair_state(P[1], fA1);
+    const QTerms tB0 = pair_state(P[0], fB0), tB1 = pair_state(P[1], fB1);
+    quad_flush(qadd(tA0, tA1), dxA, hi, ri, actA, accg + (int64_t)__float_as_uint(a2.w) * kAcc);
+    quad_flush(qadd(tB0, tB1), dxB, hi, ri, actB, accg + (int64_t)__float_as_uint(b2.w) * kAcc);
+  }
 }
 
 }  // namespace quad
