@@ -4,6 +4,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "common.cuh"
 
@@ -114,6 +117,28 @@ float mask_tau(float eps) {
     if (_s != CSPLAT_OK) return _s; \
   } while (0)
 
+// NVTX ranges per ABI call (SURVEY §5 tracing): pushed only when the
+// environment sets CSPLAT_NVTX=1 (read once), so a normal call pays one
+// predictable branch.  nvtx3 is header-only: without a tool attached the push
+// and pop are no-ops.
+bool nvtx_on() {
+  static const bool on = [] {
+    const char *e = std::getenv("CSPLAT_NVTX");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char *name) : on(nvtx_on()) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
+#define CSPLAT_TRACE NvtxRange _nvtx_range(__func__)
+
 }  // namespace
 
 extern "C" {
@@ -121,6 +146,7 @@ extern "C" {
 int csplat_version(void) { return (2 << 16) | 0; }  // 2.0: tile_range status slot, codebook status
 
 int csplat_release_thread_resources(void) {
+  CSPLAT_TRACE;
   csplat::release_thread_fork_resources();
   return CSPLAT_OK;
 }
@@ -139,6 +165,7 @@ const char *csplat_status_string(int s) {
 }
 
 int csplat_last_error(char *buf, size_t len) {
+  CSPLAT_TRACE;
   const int n = (int)std::strlen(g_err);
   if (buf && len) {
     std::strncpy(buf, g_err, len - 1);
@@ -187,6 +214,7 @@ static int project_impl(const csplat_gaussians *g, const csplat_codebook *cb,
 int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const csplat_camera *cam,
                    const csplat_view *view, const csplat_params *prm, void *rec, int32_t *count,
                    void *stream) {
+  CSPLAT_TRACE;
   if (!view) return invalid("view NULL");
   return project_impl(g, cb, cam, view, nullptr, prm, rec, count, stream);
 }
@@ -194,6 +222,7 @@ int csplat_project(const csplat_gaussians *g, const csplat_codebook *cb, const c
 int csplat_project_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                       const csplat_camera *cam, const float *view_dev, const csplat_params *prm,
                       void *rec, int32_t *count, void *stream) {
+  CSPLAT_TRACE;
   if (!view_dev) return invalid("view_dev NULL");
   return project_impl(g, cb, cam, nullptr, view_dev, prm, rec, count, stream);
 }
@@ -201,6 +230,7 @@ int csplat_project_dv(const csplat_gaussians *g, const csplat_codebook *cb,
 int csplat_project_views(const csplat_gaussians *g, const csplat_codebook *cb,
                          const csplat_camera *cam, const csplat_view *views, int32_t n_views,
                          const csplat_params *prm, void *rec, int32_t *count, void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_gaussians(g));
   RET_IF(check_camera(cam));
   RET_IF(check_codebook(cb, true));
@@ -232,6 +262,7 @@ int csplat_project_bin_views(const csplat_gaussians *g, const csplat_codebook *c
                              void *rec, int32_t *count, int64_t pair_capacity, uint32_t *pair_gid,
                              uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                              size_t ws_bytes_per_view, void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_gaussians(g));
   RET_IF(check_camera(cam));
   RET_IF(check_codebook(cb, true));
@@ -277,6 +308,7 @@ int csplat_chain_views(const csplat_gaussians *g, const csplat_codebook *cb,
                        const csplat_camera *cam, const csplat_view *views, int32_t n_views,
                        const csplat_params *prm, const void *rec, void *ws, uint32_t flags,
                        const csplat_grads *out, void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_gaussians(g));
   RET_IF(check_camera(cam));
   RET_IF(check_codebook(cb, true));
@@ -354,6 +386,7 @@ int csplat_project_bin(const csplat_gaussians *g, const csplat_codebook *cb,
                        const csplat_params *prm, void *rec, int32_t *count,
                        const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                        uint32_t flags, void *ws, size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   if (!view) return invalid("view NULL");
   return project_bin_impl(g, cb, cam, view, nullptr, prm, rec, count, tile_active, pair_capacity,
                           pair_gid, tile_range, n_pairs_dev, flags, ws, ws_bytes, stream);
@@ -364,6 +397,7 @@ int csplat_project_bin_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                           const csplat_params *prm, void *rec, int32_t *count,
                           const uint32_t *tile_active, int64_t pair_capacity, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev,
                           uint32_t flags, void *ws, size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   if (!view_dev) return invalid("view_dev NULL");
   return project_bin_impl(g, cb, cam, nullptr, view_dev, prm, rec, count, tile_active,
                           pair_capacity, pair_gid, tile_range, n_pairs_dev, flags, ws,
@@ -417,6 +451,7 @@ int csplat_project_bin_render(const csplat_gaussians *g, const csplat_codebook *
                               uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                               size_t ws_bytes, float *color, float *depth, float *silhouette,
                               float *t_final, int32_t *n_contrib, void *stream) {
+  CSPLAT_TRACE;
   if (!view) return invalid("view NULL");
   return project_bin_render_impl(g, cb, cam, view, nullptr, prm, rec, count, pair_capacity,
                                  pair_gid, tile_range, n_pairs_dev, ws, ws_bytes, color,
@@ -430,6 +465,7 @@ int csplat_project_bin_render_dv(const csplat_gaussians *g, const csplat_codeboo
                                  uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,
                                  size_t ws_bytes, float *color, float *depth, float *silhouette,
                                  float *t_final, int32_t *n_contrib, void *stream) {
+  CSPLAT_TRACE;
   if (!view_dev) return invalid("view_dev NULL");
   return project_bin_render_impl(g, cb, cam, nullptr, view_dev, prm, rec, count, pair_capacity,
                                  pair_gid, tile_range, n_pairs_dev, ws, ws_bytes, color,
@@ -497,6 +533,7 @@ int csplat_render_step(const csplat_gaussians *g, const csplat_codebook *cb,
                        const float *d_depth, const float *d_silhouette, uint32_t flags,
                        const csplat_grads *out, void *ws_bwd, size_t ws_bwd_bytes,
                        void *stream) {
+  CSPLAT_TRACE;
   if (!view) return invalid("view NULL");
   return render_step_impl(g, cb, cam, view, nullptr, prm, rec, count, pair_capacity, pair_gid,
                           tile_range, n_pairs_dev, ws_bin, ws_bin_bytes, color, depth,
@@ -514,6 +551,7 @@ int csplat_tracking_step(const csplat_gaussians *g, const csplat_codebook *cb,
                          const uint64_t *n_valid_dev, float lambda_depth, float sil_gate,
                          uint32_t flags, const csplat_grads *out, float *loss3_dev,
                          void *ws_bwd, size_t ws_bwd_bytes, void *stream) {
+  CSPLAT_TRACE;
   if ((view == nullptr) == (view_dev == nullptr)) return invalid("give exactly one of view / view_dev");
   if (!obs_color || !obs_depth || !n_valid_dev || !loss3_dev)
     return invalid("tracking_step: NULL observation argument");
@@ -533,6 +571,7 @@ int csplat_bin_tiles_active(const void *rec, const int32_t *count, int64_t n,
                             int64_t pair_capacity, uint32_t *pair_gid,
                      uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
                      size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_camera(cam));
   if (n < 0 || n > (int64_t)csplat::kPairGidMask + 1 || pair_capacity < 0 ||
       pair_capacity > 0xffffffffLL)
@@ -572,6 +611,7 @@ int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csp
                      int64_t pair_capacity, uint32_t *pair_gid,
                      uint32_t *tile_range, int64_t *n_pairs_dev, uint32_t flags, void *ws,
                      size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   return csplat_bin_tiles_active(rec, count, n, cam, nullptr, pair_capacity, pair_gid,
                                  tile_range, n_pairs_dev, flags, ws, ws_bytes, stream);
 }
@@ -579,6 +619,7 @@ int csplat_bin_tiles(const void *rec, const int32_t *count, int64_t n, const csp
 int csplat_ba_patches(const float *obs_depth, const csplat_camera *cam, const int32_t *patches,
                       int64_t n_patches, uint32_t *tile_active, uint64_t *n_valid_dev,
                       void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_camera(cam));
   if (n_patches < 0) return invalid("n_patches < 0");
   if (!tile_active || !n_valid_dev || (n_patches > 0 && (!obs_depth || !patches)))
@@ -595,6 +636,7 @@ int csplat_ba_patch_loss(const float *color, const float *depth, const float *ob
                          int64_t n_patches, int64_t n_rays, const uint64_t *n_valid_dev,
                          float lambda_depth, float lambda_ssim, float *d_color, float *d_depth,
                          float *d_silhouette, float *loss3_dev, void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_camera(cam));
   if (n_patches < 0 || (n_patches > 0 && n_rays <= 0))
     return invalid("need n_patches >= 0 and n_rays > 0");
@@ -618,6 +660,7 @@ int csplat_render_fwd_list(const void *rec, const uint32_t *pair_gid, const uint
                            const int32_t *tile_list, int32_t max_tiles, const csplat_camera *cam,
                            const csplat_params *prm, float *color, float *depth, float *silhouette,
                            float *t_final, int32_t *n_contrib, void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_camera(cam));
   if (!prm || !tile_range || !tile_list || !color || !depth || !silhouette || !t_final ||
       !n_contrib || max_tiles < 0)
@@ -638,6 +681,7 @@ int csplat_render_fwd(const void *rec, const uint32_t *pair_gid, const uint32_t 
                       const csplat_camera *cam, const csplat_params *prm, float *color,
                       float *depth, float *silhouette, float *t_final, int32_t *n_contrib,
                       void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_camera(cam));
   if (!prm || !tile_range || !color || !depth || !silhouette || !t_final || !n_contrib)
     return invalid("render_fwd: NULL argument");
@@ -697,6 +741,7 @@ int csplat_render_bwd_list(const csplat_gaussians *g, const csplat_codebook *cb,
                            const float *d_color, const float *d_depth, const float *d_silhouette,
                            uint32_t flags, const csplat_grads *out, void *ws, size_t ws_bytes,
                            void *stream) {
+  CSPLAT_TRACE;
   if (!view) return invalid("view NULL");
   if (!tile_list || max_tiles < 0) return invalid("tile_list NULL / max_tiles < 0");
   return render_bwd_impl(g, cb, cam, view, nullptr, prm, rec, pair_gid, tile_range, t_final,
@@ -710,6 +755,7 @@ int csplat_render_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
                       const float *t_final, const int32_t *n_contrib, const float *d_color,
                       const float *d_depth, const float *d_silhouette, uint32_t flags,
                       const csplat_grads *out, void *ws, size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   if (!view) return invalid("view NULL");
   return render_bwd_impl(g, cb, cam, view, nullptr, prm, rec, pair_gid, tile_range, t_final,
                          n_contrib, d_color, d_depth, d_silhouette, flags, out, ws, ws_bytes,
@@ -723,6 +769,7 @@ int csplat_render_bwd_dv(const csplat_gaussians *g, const csplat_codebook *cb,
                          const int32_t *n_contrib, const float *d_color, const float *d_depth,
                          const float *d_silhouette, uint32_t flags, const csplat_grads *out,
                          void *ws, size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   if (!view_dev) return invalid("view_dev NULL");
   return render_bwd_impl(g, cb, cam, nullptr, view_dev, prm, rec, pair_gid, tile_range, t_final,
                          n_contrib, d_color, d_depth, d_silhouette, flags, out, ws, ws_bytes,
@@ -731,6 +778,7 @@ int csplat_render_bwd_dv(const csplat_gaussians *g, const csplat_codebook *cb,
 
 int csplat_count_valid_depth(const float *obs_depth, int32_t width, int32_t height,
                              uint64_t *n_valid_dev, void *stream) {
+  CSPLAT_TRACE;
   if (width <= 0 || height <= 0) return invalid("width/height must be > 0");
   if (!obs_depth || !n_valid_dev) return invalid("count_valid_depth: NULL argument");
   RET_IF(check_device());
@@ -749,6 +797,7 @@ int csplat_tracking_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
                         const uint64_t *n_valid_dev, float lambda_depth, float sil_gate,
                         uint32_t flags, const csplat_grads *out, float *loss3_dev, void *ws,
                         size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   if ((view == nullptr) == (view_dev == nullptr)) return invalid("give exactly one of view / view_dev");
   if (!color || !depth || !silhouette || !obs_color || !obs_depth || !n_valid_dev)
     return invalid("tracking_bwd: NULL image argument");
@@ -764,6 +813,7 @@ int csplat_tracking_bwd(const csplat_gaussians *g, const csplat_codebook *cb,
 
 int csplat_pose_step(float *view_dev, const float *pose_grad_dev, float lr_rot, float lr_trans,
                      void *stream) {
+  CSPLAT_TRACE;
   if (!view_dev || !pose_grad_dev) return invalid("pose_step: NULL argument");
   if (!std::isfinite(lr_rot) || !std::isfinite(lr_trans)) return invalid("lr must be finite");
   RET_IF(check_device());
@@ -777,6 +827,7 @@ int csplat_tracking_loss(const float *color, const float *depth, const float *si
                          int32_t height, float lambda_depth, float sil_gate, float *d_color,
                          float *d_depth, float *d_silhouette, float *loss3_dev, void *ws,
                          size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   if (width <= 0 || height <= 0) return invalid("width/height must be > 0");
   if (!color || !depth || !silhouette || !obs_color || !obs_depth || !d_color || !d_depth ||
       !d_silhouette)
@@ -797,6 +848,7 @@ int csplat_tracking_loss(const float *color, const float *depth, const float *si
 
 int csplat_mask_loss(const csplat_gaussians *g, const int32_t *count, float lambda,
                      float *d_mask, float *loss_dev, void *ws, size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   if (!g || g->n < 0) return invalid("gaussians NULL / n < 0");
   if (g->n > 0 && (!g->mask || !count || !d_mask)) return invalid("mask_loss: NULL argument");
   if (!std::isfinite(lambda)) return invalid("lambda must be finite");
@@ -813,6 +865,7 @@ int csplat_mask_loss(const csplat_gaussians *g, const int32_t *count, float lamb
 int csplat_keyframe_overlap(const float *depth, const csplat_camera *cam, const csplat_view *cur,
                             const csplat_view *views, int32_t K, int64_t *counts_dev, void *ws,
                             size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_camera(cam));
   if (K < 0 || K > 256) return invalid("K must be 0..256");
   if (!depth || !cur || (K > 0 && (!views || !counts_dev))) return invalid("overlap: NULL argument");
@@ -835,6 +888,7 @@ int csplat_rvq_update(const float *x, int64_t n, const int64_t *n_dev, int32_t d
                       const float *codes, int32_t L, int32_t P, const void *idx, int32_t idx_bytes,
                       float *codes_out, int32_t *counts_out, float *loss_out, void *ws,
                       size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   if (n < 0) return invalid("n < 0");
   if (d < 1 || d > 8) return invalid("d must be 1..8");
   if (L < 1 || L > 16) return invalid("L must be 1..16");
@@ -855,6 +909,7 @@ int csplat_rvq_update(const float *x, int64_t n, const int64_t *n_dev, int32_t d
 int csplat_rvq_code_grad(const float *d_shat, int64_t n, const int64_t *n_dev, int32_t d,
                          const void *idx, int32_t idx_bytes, int32_t L, int32_t P,
                          float *d_codes, uint32_t flags, void *stream) {
+  CSPLAT_TRACE;
   if (n < 0) return invalid("n < 0");
   if (d < 1 || d > 8) return invalid("d must be 1..8");
   if (L < 1 || L > 16) return invalid("L must be 1..16");
@@ -875,6 +930,7 @@ int csplat_rvq_code_grad(const float *d_shat, int64_t n, const int64_t *n_dev, i
 int csplat_rvq_init_stage(const float *x, int64_t n, int32_t d, float *codes, int32_t L,
                           int32_t P, int32_t stage, const void *idx, int32_t idx_bytes,
                           const int64_t *sample, void *stream) {
+  CSPLAT_TRACE;
   if (n < 1) return invalid("n must be >= 1");
   if (d < 1 || d > 8) return invalid("d must be 1..8");
   if (L < 1 || L > 16) return invalid("L must be 1..16");
@@ -891,6 +947,7 @@ int csplat_rvq_init_stage(const float *x, int64_t n, int32_t d, float *codes, in
 int csplat_rvq_assign(const float *x, int64_t n, const int64_t *n_dev, int32_t d,
                       const float *codes, int32_t L, int32_t P, void *idx_out, int32_t idx_bytes,
                       float *recon_out, void *stream) {
+  CSPLAT_TRACE;
   if (n < 0) return invalid("n < 0");
   if (d < 1 || d > 8) return invalid("d must be 1..8");
   if (L < 1 || L > 16) return invalid("L must be 1..16");
@@ -908,6 +965,7 @@ int csplat_mask_prune(const csplat_gaussians *in, const csplat_codebook *in_idx,
                       float reset_mask_logit, const csplat_gaussians_out *out,
                       void *out_scale_idx, void *out_rot_idx, int32_t *keep_map,
                       int64_t *n_kept_dev, void *ws, size_t ws_bytes, void *stream) {
+  CSPLAT_TRACE;
   RET_IF(check_gaussians(in));
   if (in->n > 0 && (!in->log_scale || !in->quat)) return invalid("log_scale/quat NULL");
   if (!out || !n_kept_dev) return invalid("out/n_kept NULL");
