@@ -337,10 +337,11 @@ def test_empty_and_all_culled(env):
 
 
 def test_long_tile_lists(env):
-    """Buckets longer than a warp's shared-memory slice (CTA-wide sort) and
-    longer than the CTA's shared memory (global-memory sort)."""
+    """Tile lists past the one-warp register sort (256 keys): the shared-memory
+    sort (<= 1024 keys, with bucket overflow past 512) and the global-memory
+    sort; the backward over several list chunks."""
     rng = np.random.default_rng(9)
-    for n in (1500, 4000, 13000):   # CTA sort / CTA-wide long sort / global-memory sort
+    for n in (600, 1500, 4000, 13000):   # smem sort + overflow / global-memory sorts
         cam = dict(fx=20.0, fy=20.0, cx=7.5, cy=7.5, width=32, height=16, near=0.01, far=100.0)
         z = rng.uniform(1, 5, n)
         px, py = rng.uniform(0, 15, n), rng.uniform(0, 15, n)
