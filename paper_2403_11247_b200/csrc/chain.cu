@@ -50,20 +50,10 @@ __global__ void __launch_bounds__(256, 3) k_chain(
   if (alive) {
     a0 = acc4[j * 3 + 0]; a1 = acc4[j * 3 + 1]; a2 = acc4[j * 3 + 2];
   }
-  // ACCUMULATE: all 15 old gradient values are loaded up front -- the planes
-  // may alias as far as the compiler knows, so an interleaved += would
-  // serialise 15 load -> store round trips (C5: 50 -> ~28 us per view), and
-  // issued here they overlap the R-VQ decode and the chain arithmetic
-  float old[15];
-  if (alive && (flags & CSPLAT_ACCUMULATE) && !(flags & CSPLAT_POSE_ONLY)) {
-    auto get = [&](const float *plane, int k, int64_t off) { old[k] = plane ? plane[off] : 0.f; };
-    for (int k = 0; k < 3; k++) get(out.mean, k, (int64_t)k * n + i);
-    get(out.opacity, 3, i);
-    for (int k = 0; k < 3; k++) get(out.rgb, 4 + k, (int64_t)k * n + i);
-    for (int k = 0; k < 3; k++) get(out.log_scale, 7 + k, (int64_t)k * n + i);
-    for (int k = 0; k < 4; k++) get(out.quat, 10 + k, (int64_t)k * n + i);
-    get(out.mask, 14, i);
-  }
+  // ACCUMULATE adds into the planes with fire-and-forget reductions
+  // (red.global.add: the same float add of the old value as a load + add +
+  // store, in stream order -- the window's chains run in keyframe order on one
+  // stream -- but the thread never waits on the old values' loads)
   if (alive) {
     // k_render_bwd accumulates the raw moments Sx, Sy, Sxx, Sxy, Syy of
     // a = alpha dL/dalpha; map them through the record's DA conic
@@ -231,12 +221,10 @@ __global__ void __launch_bounds__(256, 3) k_chain(
   }
   const bool accu = (flags & CSPLAT_ACCUMULATE) != 0;
   if (!(flags & CSPLAT_POSE_ONLY) && i < n && (alive || !accu)) {
-    if (accu) {
-#pragma unroll
-      for (int k = 0; k < 15; k++) g[k] += old[k];
-    }
     auto put = [&](float *plane, int k, int64_t off) {
-      if (plane) plane[off] = g[k];
+      if (!plane) return;
+      if (accu) atomicAdd(plane + off, g[k]);  // result unused: RED.E.ADD.F32
+      else plane[off] = g[k];
     };
     for (int k = 0; k < 3; k++) put(out.mean, k, (int64_t)k * n + i);
     put(out.opacity, 3, i);
