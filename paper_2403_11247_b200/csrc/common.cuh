@@ -420,12 +420,41 @@ __device__ __forceinline__ bool box_may_hit(const BoxConic &c, int bx0, int by0,
   const float margin = 0.01f + 2e-5f * (c.ca * DX * DX + fabsf(c.cb2) * DX * DY + c.cc * DY * DY);
   return !(qmin > c.k2 + margin);  // NaN keeps the block
 }
+// block_mask over a tile's four 8x8 blocks, branch-free (the bucket pass runs
+// it for 32 different pairs per warp: box_may_hit's branches diverge there).
+// The same arithmetic as box_may_hit per block -- the edge offsets shared
+// between the blocks, both edge probes evaluated and selected -- so the masks
+// are bit-identical to it.
 __device__ __forceinline__ uint32_t block_mask_c(const BoxConic &c, int X0, int Y0) {
+  const float inf = __int_as_float(0x7f800000);
+  float ex[4], ey[4];  // offsets of the block edges X0, X0+7, X0+8, X0+15 (y alike)
+#pragma unroll
+  for (int e = 0; e < 4; e++) {
+    ex[e] = (float)(X0 + (e >> 1) * 8 + (e & 1) * 7) - c.u;
+    ey[e] = (float)(Y0 + (e >> 1) * 8 + (e & 1) * 7) - c.v;
+  }
   uint32_t m = 0;
 #pragma unroll
   for (int w = 0; w < 4; w++) {
-    const int bx0 = X0 + (w & 1) * 8, by0 = Y0 + (w >> 1) * 8;
-    if (box_may_hit(c, bx0, by0, bx0 + 7, by0 + 7)) m |= 1u << w;
+    const int hx = w & 1, hy = w >> 1;
+    const int bx0 = X0 + hx * 8, by0 = Y0 + hy * 8;
+    const bool rect = !(c.rx1 < bx0 || c.rx0 > bx0 + 7 || c.ry1 < by0 || c.ry0 > by0 + 7);
+    const float dx0 = ex[2 * hx], dx1 = ex[2 * hx + 1];
+    const float dy0 = ey[2 * hy], dy1 = ey[2 * hy + 1];
+    const bool ox = dx0 > 0.0f || dx1 < 0.0f, oy = dy0 > 0.0f || dy1 < 0.0f;
+    // near vertical edge, dy clamped to the block
+    const float exn = dx0 > 0.0f ? dx0 : dx1;
+    const float dyv = fminf(fmaxf(c.sy * exn, dy0), dy1);
+    const float qv = c.ca * exn * exn + c.cb2 * exn * dyv + c.cc * dyv * dyv;
+    // near horizontal edge
+    const float eyn = dy0 > 0.0f ? dy0 : dy1;
+    const float dxh = fminf(fmaxf(c.sx * eyn, dx0), dx1);
+    const float qh = c.ca * dxh * dxh + c.cb2 * dxh * eyn + c.cc * eyn * eyn;
+    const float qmin = (ox || oy) ? fminf(ox ? qv : inf, oy ? qh : inf) : 0.0f;
+    const float DX = fmaxf(fabsf(dx0), fabsf(dx1)), DY = fmaxf(fabsf(dy0), fabsf(dy1));
+    const float margin = 0.01f + 2e-5f * (c.ca * DX * DX + fabsf(c.cb2) * DX * DY + c.cc * DY * DY);
+    const bool hit = rect && (!c.conic_ok || !(qmin > c.k2 + margin));  // NaN keeps the block
+    m |= hit ? 1u << w : 0u;
   }
   return m;
 }
