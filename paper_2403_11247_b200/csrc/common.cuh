@@ -373,58 +373,23 @@ size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam);
 // so at most two 1-D clamped minimisations per block.  The margin covers the
 // float32 evaluation of q at any pixel of the block, so a
 // cleared bit never skips a pixel the per-pixel test would have composited.
-// The box test of one pixel block [bx0, bx1] x [by0, by1] (inclusive) against
-// one record: false only when the minimum of q over the box exceeds k^2 + margin.
+// The conic, extent and edge slopes of one (tile, Gaussian) pair's box tests
+// (the bucket pass fills it from the owner lane's PairSrc, bin_dev.cuh).
 struct BoxConic {
   float u, v, ca, cb2, cc, k2, sx, sy;
   int rx0, ry0, rx1, ry1;
   bool conic_ok;
 };
-__device__ __forceinline__ BoxConic box_conic(const uint4 &v0, const uint4 &v1, const uint4 &v3) {
-  BoxConic c;
-  c.u = __uint_as_float(v0.x); c.v = __uint_as_float(v0.y);
-  c.ca = __uint_as_float(v0.z); c.cb2 = __uint_as_float(v0.w);
-  c.cc = __uint_as_float(v1.x); c.k2 = __uint_as_float(v1.z);
-  c.rx0 = (int)(v3.x & 0xffffu); c.ry0 = (int)(v3.x >> 16);
-  c.rx1 = (int)(v3.y & 0xffffu); c.ry1 = (int)(v3.y >> 16);
-  c.conic_ok = c.ca > 0.0f && c.cc > 0.0f;
-  // the edge minimisers' slopes, once per pair: on a vertical edge at dx = ex the
-  // convex q is least at dy = -cb2 ex / (2 cc) (horizontal edges alike); any
-  // rounding of this location only moves the probe along the edge, which can
-  // raise q by at most cc * (location error)^2 -- far below the margin
-  c.sy = c.conic_ok ? -c.cb2 / (2.0f * c.cc) : 0.0f;
-  c.sx = c.conic_ok ? -c.cb2 / (2.0f * c.ca) : 0.0f;
-  return c;
-}
-__device__ __forceinline__ bool box_may_hit(const BoxConic &c, int bx0, int by0, int bx1, int by1) {
-  if (c.rx1 < bx0 || c.rx0 > bx1 || c.ry1 < by0 || c.ry0 > by1) return false;  // rectangle cull
-  if (!c.conic_ok) return true;
-  const float dx0 = (float)bx0 - c.u, dx1 = (float)bx1 - c.u;
-  const float dy0 = (float)by0 - c.v, dy1 = (float)by1 - c.v;
-  const bool ox = dx0 > 0.0f || dx1 < 0.0f, oy = dy0 > 0.0f || dy1 < 0.0f;
-  float qmin = 0.0f;
-  if (ox || oy) {
-    qmin = INFINITY;
-    if (ox) {  // near vertical edge, dy clamped to the block
-      const float ex = dx0 > 0.0f ? dx0 : dx1;
-      const float dy = fminf(fmaxf(c.sy * ex, dy0), dy1);
-      qmin = fminf(qmin, c.ca * ex * ex + c.cb2 * ex * dy + c.cc * dy * dy);
-    }
-    if (oy) {  // near horizontal edge
-      const float ey = dy0 > 0.0f ? dy0 : dy1;
-      const float dx = fminf(fmaxf(c.sx * ey, dx0), dx1);
-      qmin = fminf(qmin, c.ca * dx * dx + c.cb2 * dx * ey + c.cc * ey * ey);
-    }
-  }
-  const float DX = fmaxf(fabsf(dx0), fabsf(dx1)), DY = fmaxf(fabsf(dy0), fabsf(dy1));
-  const float margin = 0.01f + 2e-5f * (c.ca * DX * DX + fabsf(c.cb2) * DX * DY + c.cc * DY * DY);
-  return !(qmin > c.k2 + margin);  // NaN keeps the block
-}
-// block_mask over a tile's four 8x8 blocks, branch-free (the bucket pass runs
-// it for 32 different pairs per warp: box_may_hit's branches diverge there).
-// The same arithmetic as box_may_hit per block -- the edge offsets shared
-// between the blocks, both edge probes evaluated and selected -- so the masks
-// are bit-identical to it.
+// The mask over a tile's four 8x8 blocks, branch-free (the bucket pass runs it
+// for 32 different pairs per warp, where per-block branches diverge).
+// Per block: the rectangle cull, then the minimum of q over the block (0 when
+// the block holds the centre, else the clamped minimisations on the one or two
+// edges facing the centre, the edge offsets shared between the blocks and both
+// probes evaluated and selected), kept unless it exceeds k^2 + margin.  The
+// edge slopes sx, sy: on a vertical edge at dx = e the convex q is least at
+// dy = -cb2 e / (2 cc) (horizontal edges alike); any rounding of this location
+// only moves the probe along the edge, which can raise q by at most
+// cc (location error)^2 -- far below the margin.
 __device__ __forceinline__ uint32_t block_mask_c(const BoxConic &c, int X0, int Y0) {
   const float inf = __int_as_float(0x7f800000);
   float ex[4], ey[4];  // offsets of the block edges X0, X0+7, X0+8, X0+15 (y alike)
@@ -458,25 +423,6 @@ __device__ __forceinline__ uint32_t block_mask_c(const BoxConic &c, int X0, int 
   }
   return m;
 }
-__device__ __forceinline__ uint32_t block_mask(const uint4 &v0, const uint4 &v1, const uint4 &v3,
-                                               int X0, int Y0) {
-  return block_mask_c(box_conic(v0, v1, v3), X0, Y0);
-}
-// The same test on the tile's sixteen 4x4 blocks (bit qy * 4 + qx), evaluated
-// only inside the 8x8 blocks whose bit m8 carries (a 4x4 block of a culled
-// 8x8 block is culled): the backward's per-ring selection (render_bwd.cu).
-__device__ __forceinline__ uint32_t quarter_mask(const BoxConic &c, int X0, int Y0, uint32_t m8) {
-  uint32_t m = 0;
-#pragma unroll
-  for (int b = 0; b < 16; b++) {
-    const int qx = b & 3, qy = b >> 2;
-    if (!((m8 >> ((qx >> 1) + 2 * (qy >> 1))) & 1u)) continue;
-    const int bx0 = X0 + qx * 4, by0 = Y0 + qy * 4;
-    if (box_may_hit(c, bx0, by0, bx0 + 3, by0 + 3)) m |= 1u << b;
-  }
-  return m;
-}
-
 // NEXT-2 (rvq_update.cu): the STE code gradient and the Fig 4 stage init
 cudaError_t launch_rvq_code_grad(const float *g, int64_t n, const int64_t *n_dev, int d, int L,
                                  int P, const void *idx, int idx_bytes, float *dcodes,
