@@ -150,57 +150,72 @@ __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len
   for (int k = tid; k < len; k += nthr) pair_gid[(int64_t)start + k] = pair_entry(a[k]);
 }
 
-// One warp sorts up to 256 keys in registers: lane l holds elements 8l .. 8l+7
-// (blocked), missing elements +inf.  The same all-ascending bitonic network as
-// above; a compare-exchange at distance m < 8 is inside the lane, at m >= 8 the
-// partner is element t ^ (m & 7) of lane l ^ (m >> 3) (one 64-bit shuffle per
-// element).  21 of the 36 stages at 256 keys are lane-local, and there is no
+// One warp sorts up to 32 * KPL keys in registers: lane l holds elements
+// KPL l .. KPL l + KPL - 1 (blocked), missing elements +inf.  The same
+// all-ascending bitonic network as above; a compare-exchange at distance
+// m < KPL is inside the lane, at m >= KPL the partner is element t ^ (m % KPL)
+// of lane l ^ (m / KPL) (one 64-bit shuffle per element).  KPL = 8 (<= 256
+// keys): 21 of the 36 stages are lane-local; KPL = 16 (<= 512): 30 of 45.  No
 // CTA barrier (round 1's 128-thread form: 33 shuffle stages, 3 barriers).
-__device__ __forceinline__ void cx_lane(unsigned long long (&x)[8], int a, int b) {
+template <int KPL>
+__device__ __forceinline__ void cx_lane(unsigned long long (&x)[KPL], int a, int b) {
   const unsigned long long lo = x[a] < x[b] ? x[a] : x[b], hi = x[a] < x[b] ? x[b] : x[a];
   x[a] = lo;
   x[b] = hi;
 }
-template <int M, int HIBIT>
-__device__ __forceinline__ void warp_stage(unsigned long long (&x)[8], int lane) {
+template <int KPL, int M, int HIBIT>
+__device__ __forceinline__ void warp_stage(unsigned long long (&x)[KPL], int lane) {
   // partner e ^ M; the pair's lower element keeps the min
-  if constexpr (M < 8) {
+  if constexpr (M < KPL) {
 #pragma unroll
-    for (int t = 0; t < 8; t++)
-      if ((t ^ M) > t) cx_lane(x, t, t ^ M);
+    for (int t = 0; t < KPL; t++)
+      if ((t ^ M) > t) cx_lane<KPL>(x, t, t ^ M);
   } else {
-    constexpr int ml = M >> 3, mt = M & 7;
-    const bool lower = (lane & (HIBIT >> 3)) == 0;
-    unsigned long long p[8];
+    constexpr int ml = M / KPL, mt = M % KPL;
+    const bool lower = (lane & (HIBIT / KPL)) == 0;
+    unsigned long long p[KPL];
 #pragma unroll
-    for (int t = 0; t < 8; t++) p[t] = __shfl_xor_sync(0xffffffffu, x[t ^ mt], ml);
+    for (int t = 0; t < KPL; t++) p[t] = __shfl_xor_sync(0xffffffffu, x[t ^ mt], ml);
 #pragma unroll
-    for (int t = 0; t < 8; t++) {
+    for (int t = 0; t < KPL; t++) {
       const bool pl = p[t] < x[t];
       x[t] = (pl == lower) ? p[t] : x[t];
     }
   }
 }
-template <int K, int J>
-__device__ __forceinline__ void warp_cleaners(unsigned long long (&x)[8], int lane) {
+template <int KPL, int K, int J>
+__device__ __forceinline__ void warp_cleaners(unsigned long long (&x)[KPL], int lane) {
   if constexpr (J >= 1) {
-    warp_stage<J, J>(x, lane);
-    warp_cleaners<K, J / 2>(x, lane);
+    warp_stage<KPL, J, J>(x, lane);
+    warp_cleaners<KPL, K, J / 2>(x, lane);
   }
 }
-template <int K, int NP2>
-__device__ __forceinline__ void warp_merges(unsigned long long (&x)[8], int lane) {
+template <int KPL, int K, int NP2>
+__device__ __forceinline__ void warp_merges(unsigned long long (&x)[KPL], int lane) {
   if constexpr (K <= NP2) {
-    warp_stage<K - 1, K / 2>(x, lane);  // mirror
-    warp_cleaners<K, K / 4>(x, lane);   // half-cleaners
-    warp_merges<2 * K, NP2>(x, lane);
+    warp_stage<KPL, K - 1, K / 2>(x, lane);  // mirror
+    warp_cleaners<KPL, K, K / 4>(x, lane);   // half-cleaners
+    warp_merges<KPL, 2 * K, NP2>(x, lane);
   }
 }
-// the network for NP2 (64, 128 or 256) elements, all stage distances
-// compile-time so the eight keys stay in registers
-template <int NP2>
-__device__ __forceinline__ void sort_warp(unsigned long long (&x)[8]) {
-  warp_merges<2, NP2>(x, threadIdx.x & 31);
+// the network for NP2 elements (<= 32 KPL), all stage distances compile-time
+// so the keys stay in registers
+template <int KPL, int NP2>
+__device__ __forceinline__ void sort_warp(unsigned long long (&x)[KPL]) {
+  warp_merges<KPL, 2, NP2>(x, threadIdx.x & 31);
+}
+// load a tile's len keys (<= 32 KPL) from its bucket, sort, emit the entries
+template <int KPL, int NP2>
+__device__ __forceinline__ void warp_sort_emit(const unsigned long long *__restrict__ bk, int len,
+                                               uint32_t start, uint32_t *__restrict__ pair_gid) {
+  const int l = threadIdx.x;
+  unsigned long long x[KPL];
+#pragma unroll
+  for (int t = 0; t < KPL; t++) x[t] = KPL * l + t < len ? bk[KPL * l + t] : ~0ull;
+  sort_warp<KPL, NP2>(x);
+#pragma unroll
+  for (int t = 0; t < KPL; t++)
+    if (KPL * l + t < len) pair_gid[(int64_t)start + KPL * l + t] = pair_entry(x[t]);
 }
 
 // a5 offsets: the exclusive scan of the tiles' (or list positions') pair counts
@@ -267,18 +282,12 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   }
   const int len = (int)(end - start);  // the tile's pair count, or 0 (empty or cut)
   if (len == 0) return;                // (block-uniform)
-  if (len <= 256) {  // the common case: one warp, in registers
-    const int l = threadIdx.x;
+  if (len <= 512) {  // the common case: one warp, in registers
     const unsigned long long *bk = w.bucket + tile * kBucketCap;
-    unsigned long long x[8];
-#pragma unroll
-    for (int t = 0; t < 8; t++) x[t] = 8 * l + t < len ? bk[8 * l + t] : ~0ull;
-    if (len <= 64) sort_warp<64>(x);         // lanes 8+ hold only +inf: 21 stages
-    else if (len <= 128) sort_warp<128>(x);  // 28 stages
-    else sort_warp<256>(x);                  // 36 stages
-#pragma unroll
-    for (int t = 0; t < 8; t++)
-      if (8 * l + t < len) pair_gid[(int64_t)start + 8 * l + t] = pair_entry(x[t]);
+    if (len <= 64) warp_sort_emit<8, 64>(bk, len, start, pair_gid);          // 21 stages
+    else if (len <= 128) warp_sort_emit<8, 128>(bk, len, start, pair_gid);   // 28 stages
+    else if (len <= 256) warp_sort_emit<8, 256>(bk, len, start, pair_gid);   // 36 stages
+    else warp_sort_emit<16, 512>(bk, len, start, pair_gid);                  // 45 stages
     return;
   }
   unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
