@@ -7,7 +7,7 @@
 // vertically adjacent pixel pairs) and walk its list.  An entry is listed for a
 // block when the record's pixel rectangle (the k^2-ellipse's bounding box, §4)
 // overlaps the block and the 8x8 block around it has its bit in the pair entry
-// (block_mask, the sort's conservative ellipse test): a superset of the
+// (block_mask_c, the bucket pass's conservative ellipse test): a superset of the
 // entries any of the block's pixels composites, so skipping the others is
 // result-invariant.  The tile list is taken in chunks of kChunk entries.
 #pragma once
