@@ -17,7 +17,7 @@ struct ChainConst {
 };
 
 template <int LF>
-__global__ void __launch_bounds__(256, 3) k_chain(
+__global__ void __launch_bounds__(256, 4) k_chain(
     int64_t n, const int64_t *__restrict__ n_dev, const float *__restrict__ mean,
     const float *__restrict__ opac, const float *__restrict__ lsc, const float *__restrict__ quat,
     const float *__restrict__ mask, DecodeArgs dec, int use_dec, ChainConst cc,
