@@ -197,9 +197,6 @@ __device__ __forceinline__ void gather_batch(float4 *slot, uint32_t *msk, const 
   else mbar_arrive(full);
 }
 
-__device__ __forceinline__ void red_add_v2(float *addr, float a, float b) {
-  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(b) : "memory");
-}
 __device__ __forceinline__ void red_add_v4(float *addr, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b),
                "f"(c), "f"(d)
