@@ -72,6 +72,58 @@ __device__ __forceinline__ uint32_t mask16(uint32_t entry, const uint4 &w3, int 
   return cols * rowspread & m8x;
 }
 
+// the 4x4 blocks of m whose pixels the record's k^2-ellipse can reach: per
+// band of block rows the ellipse's x-extent over the band, from the concave
+// right boundary x_r(dy) = (-cb2 dy + sqrt(4 ca K - det dy^2)) / (2 ca) at the
+// clamp of its maximiser (the ellipse's rightmost point; the convex left
+// boundary alike), with K = k^2 + the 8x8 mask's margin over the whole tile
+// (so the float q <= k^2 test of any kept pixel lies inside),
+// the band widened by 0.25 px and the extent by 0.25 px + 0.2% against the
+// float evaluation here.  A dropped (block, entry) has q > k^2 at every pixel
+// of the block: its replay would change no state and add exact zeros.  Records
+// whose conic is not clearly positive definite keep m.
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t ellipse16(uint32_t m, const float4 &a0, const float4 &a1,
+                                              int X0, int Y0) {
+  const float u = a0.x, v = a0.y, ca = a0.z, cb2 = a0.w, cc = a1.x;
+  const float det = 4.0f * ca * cc - cb2 * cb2;
+  const float DX = fmaxf(fabsf((float)X0 - u), fabsf((float)(X0 + kTile - 1) - u));
+  const float DY = fmaxf(fabsf((float)Y0 - v), fabsf((float)(Y0 + kTile - 1) - v));
+  const float K = a1.z + 0.01f + 2e-5f * (ca * DX * DX + fabsf(cb2) * DX * DY + cc * DY * DY);
+  const bool ok = ca > 0.0f && cc > 0.0f && det > 4e-3f * ca * cc && K < 3.0e38f;
+  const float rdet = rcp_approx(fmaxf(det, 1e-30f));
+  const float ye = sqrt_approx(4.0f * ca * K * rdet), xe = sqrt_approx(4.0f * cc * K * rdet);
+  const float dyr = -cb2 * xe * rcp_approx(2.0f * cc);  // dy of the rightmost point (leftmost: -dyr)
+  const float i2a = rcp_approx(2.0f * ca), fourcak = 4.0f * ca * K;
+  const float sx = 0.25f + 2e-3f * xe;
+  uint32_t out = 0;
+#pragma unroll
+  for (int qy = 0; qy < 4; qy++) {
+    const float y0 = (float)(Y0 + 4 * qy) - v - 0.25f, y1 = y0 + 3.5f;
+    const float a = fmaxf(y0, -ye), b = fminf(y1, ye);
+    const float dR = fminf(fmaxf(dyr, a), b), dL = fminf(fmaxf(-dyr, a), b);
+    const float sR = sqrt_approx(fmaxf(fourcak - det * dR * dR, 0.0f));
+    const float sL = sqrt_approx(fmaxf(fourcak - det * dL * dL, 0.0f));
+    const float xR = (sR - cb2 * dR) * i2a + sx, xL = (-sL - cb2 * dL) * i2a - sx;
+#pragma unroll
+    for (int qx = 0; qx < 4; qx++) {
+      const float x0 = (float)(X0 + 4 * qx) - u;
+      const bool hit = a <= b && x0 <= xR && x0 + 3.0f >= xL;
+      out |= hit ? 1u << (qy * 4 + qx) : 0u;
+    }
+  }
+  return ok ? (m & out) : m;
+}
+
 // the chunk [c0, c0 + len) of the tile list starting at `start`: records to
 // L.rec (cp.async, no register staging), 4x4 masks to L.m16, and (backward)
 // the reached-Gaussian bits.  Ends with a CTA barrier.
@@ -111,6 +163,7 @@ __device__ __forceinline__ void gather(Lists &L, const float4 *__restrict__ recs
     if ((ent[k] >> kPairMaskShift) & need8) {
       const uint4 w3 = *reinterpret_cast<const uint4 *>(&L.rec[i][3]);
       m = mask16(ent[k], w3, X0, Y0);
+      m = ellipse16(m, L.rec[i][0], L.rec[i][1], X0, Y0);
     }
     L.m16[i] = (uint16_t)m;
     if (alive && m) {
