@@ -893,14 +893,19 @@ def main():
                                                sync=False)),
             ("render_fwd", step.forward),
             ("render_bwd", lambda: step.backward(view)),
-            # the compositing backward alone (k_render_bwd, CSPLAT_SKIP_CHAIN): the
-            # dominant kernel the roofline line reports
-            ("render_bwd_kernel", lambda: step.backward(view, flags=cs.SKIP_CHAIN)),
+            # the compositing backward kernel alone (k_render_bwd_quad,
+            # CSPLAT_SKIP_CHAIN; its workspace zeroed before the flush, outside
+            # the timed region, CSPLAT_WS_ZEROED): the dominant kernel the
+            # roofline line reports
+            ("render_bwd_kernel", lambda: step.backward(view, flags=cs.SKIP_CHAIN | cs.WS_ZEROED)),
         ]
+        pre = {"render_bwd_kernel": lambda: step.ws_bwd.zero_()}
         acc = {k: [] for k, _ in stages}
         for _ in range(max(5, min(args.steps, 30))):
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(stages))]
             for i, (k, fn) in enumerate(stages):
+                if k in pre:
+                    pre[k]()
                 flush.fill_(1.0)          # every stage starts with a cold L2
                 ev[2 * i].record(stream)
                 fn()

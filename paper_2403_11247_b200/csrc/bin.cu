@@ -40,7 +40,7 @@ BinWs bin_carve(void *ws, int64_t cap, int64_t T) {
   const size_t c = (size_t)(cap > 0 ? cap : 1);
   BinWs w;
   w.cur = reinterpret_cast<uint32_t *>(p);
-  p += align_up(T * 4);
+  p += align_up(T * 4 * kCurStride);
   w.ovf_n = reinterpret_cast<uint32_t *>(p);
   p += align_up(4);
   w.status = reinterpret_cast<unsigned long long *>(p);
@@ -57,7 +57,7 @@ BinWs bin_carve(void *ws, int64_t cap, int64_t T) {
 
 cudaError_t bin_reset(const BinWs &w, int64_t T, cudaStream_t s) {
   // cur, ovf_n and status are contiguous at the head of the workspace
-  return cudaMemsetAsync(w.cur, 0, align_up(T * 4) + align_up(4) + align_up(T * 8), s);
+  return cudaMemsetAsync(w.cur, 0, bin_head_bytes(T), s);
 }
 
 size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam) {
@@ -65,7 +65,7 @@ size_t bin_workspace_bytes(int64_t n, int64_t cap, const csplat_camera &cam) {
   const CamInfo ci = cam_info(cam);
   const int64_t T = (int64_t)ci.tiles_x * ci.tiles_y;
   const size_t c = (size_t)(cap > 0 ? cap : 1);
-  return align_up(T * 4) + align_up(4) + align_up(T * 8) + align_up((size_t)T * kBucketCap * 8) +
+  return bin_head_bytes(T) + align_up((size_t)T * kBucketCap * 8) +
          align_up(c * 4) + 2 * align_up(c * 8);
 }
 
@@ -86,9 +86,7 @@ __global__ void __launch_bounds__(256) k_bucket(int64_t n, const int32_t *__rest
       const int c = count[i];
       if (c > 0) src = pair_src_rec(c, rec4[i * 4 + 0], rec4[i * 4 + 1], rec4[i * 4 + 3]);
     }
-    expand_warp_regs(b * 32, src, tiles_x, [&](uint32_t gid, int tile, uint32_t z, uint32_t m) {
-      bucket_put(w, cap, active, gid, tile, z, m);
-    });
+    expand_warp_bucket(b * 32, src, tiles_x, w, cap, active);
   }
   bucket_pass_done(w, T);
 }
@@ -261,7 +259,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   const int64_t npos = list ? (int64_t)list[0] : T;
   if (pos >= npos) return;  // (block-uniform, before any barrier)
   const int64_t tile = list ? (int64_t)list[1 + pos] : pos;
-  const uint32_t cnt_t = w.cur[tile];
+  const uint32_t cnt_t = w.cur[tile * kCurStride];
   const unsigned long long prefix = w.status[pos];  // k_tile_scan's exclusive offset
   // capacity overflow (csplat.h): a tile whose pairs do not all fit -- past
   // the capacity, or with bucket spill lost from a full overflow list -- gets
@@ -333,7 +331,9 @@ cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t nctas, int64_t T, in
   return cudaGetLastError();
 }
 
-size_t bin_head_bytes(int64_t T) { return align_up(T * 4) + align_up(4) + align_up(T * 8); }
+size_t bin_head_bytes(int64_t T) {
+  return align_up(T * 4 * kCurStride) + align_up(4) + align_up(T * 8);
+}
 
 cudaError_t launch_bin(const void *rec, const int32_t *count, int64_t n, const csplat_camera &cam,
                        int64_t cap, const uint32_t *tile_active, uint32_t *pair_gid, uint32_t *tile_range, int64_t *n_pairs_dev, void *ws,

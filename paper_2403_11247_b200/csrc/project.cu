@@ -221,10 +221,7 @@ __global__ void __launch_bounds__(256) k_project(
     project_one<LF>(i, n, n_dev, mean, opac, rgb, lsc, quat, mask, dec, use_dec, pc, view_dev,
                     rec, count, ps);
   if constexpr (BIN) {
-    expand_warp_regs(i - (threadIdx.x & 31), ps, tiles_x,
-                     [&](uint32_t gid, int tile, uint32_t z, uint32_t m) {
-                       bucket_put(w, cap, active, gid, tile, z, m);
-                     });
+    expand_warp_bucket(i - (threadIdx.x & 31), ps, tiles_x, w, cap, active);
     bucket_pass_done(w, T);
   }
 }
@@ -262,10 +259,7 @@ __global__ void __launch_bounds__(256) k_project_views(
     if constexpr (BIN) {
       const BinWs wv = ws_at(w, v * ws_stride);
       const uint32_t *act = active ? active + v * active_stride : nullptr;
-      expand_warp_regs(i - (threadIdx.x & 31), ps, tiles_x,
-                       [&](uint32_t gid, int tile, uint32_t z, uint32_t m) {
-                         bucket_put(wv, cap, act, gid, tile, z, m);
-                       });
+      expand_warp_bucket(i - (threadIdx.x & 31), ps, tiles_x, wv, cap, act);
     }
   }
 }

@@ -176,7 +176,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_render_bwd_quad(
     build_lists(sm.L, c0, len, sm.wmax, wid, lane);
     // 2. the replay: the quad walks its block's list; 3. quad sums -> accumulator
     replay_chunk(sm.L, P, B, ri, c0, fpx, amax, accg);
-    __syncthreads();  // before the next chunk overwrites the records and lists
+    // before the next chunk overwrites the records and lists (after the last
+    // chunk a warp just exits)
+    if (c0 > 0) __syncthreads();
   }
 }
 }  // namespace quad
