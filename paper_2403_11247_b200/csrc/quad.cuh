@@ -63,10 +63,8 @@ __device__ __forceinline__ uint32_t mask16(uint32_t entry, const uint4 &w3, int 
   const int cy0 = max(ry0, 0) >> 2, cy1 = min(ry1, kTile - 1) >> 2;
   if (cx0 > cx1 || cy0 > cy1) return 0u;
   const uint32_t cols = (0xfu >> (3 - cx1)) & (0xfu << cx0);
-  const uint32_t rows = (0xfu >> (3 - cy1)) & (0xfu << cy0);
-  uint32_t rowspread = 0;
-#pragma unroll
-  for (int q = 0; q < 4; q++) rowspread |= ((rows >> q) & 1u) << (4 * q);
+  // bit 4 qy for the block rows cy0 <= qy <= cy1
+  const uint32_t rowspread = (0x1111u >> (12 - 4 * cy1)) & (0x1111u << (4 * cy0));
   const uint32_t m8 = entry >> kPairMaskShift;
   const uint32_t m8x = ((m8 & 1u) ? 0x0033u : 0u) | ((m8 & 2u) ? 0x00ccu : 0u) |
                        ((m8 & 4u) ? 0x3300u : 0u) | ((m8 & 8u) ? 0xcc00u : 0u);
@@ -106,6 +104,7 @@ __device__ __forceinline__ uint32_t ellipse16(uint32_t m, const float4 &a0, cons
   const float dyr = -cb2 * xe * rcp_approx(2.0f * cc);  // dy of the rightmost point (leftmost: -dyr)
   const float i2a = rcp_approx(2.0f * ca), fourcak = 4.0f * ca * K;
   const float sx = 0.25f + 2e-3f * xe;
+  const float cu = (u - (float)X0) * 0.25f;
   uint32_t out = 0;
 #pragma unroll
   for (int qy = 0; qy < 4; qy++) {
@@ -115,12 +114,13 @@ __device__ __forceinline__ uint32_t ellipse16(uint32_t m, const float4 &a0, cons
     const float sR = sqrt_approx(fmaxf(fourcak - det * dR * dR, 0.0f));
     const float sL = sqrt_approx(fmaxf(fourcak - det * dL * dL, 0.0f));
     const float xR = (sR - cb2 * dR) * i2a + sx, xL = (-sL - cb2 * dL) * i2a - sx;
-#pragma unroll
-    for (int qx = 0; qx < 4; qx++) {
-      const float x0 = (float)(X0 + 4 * qx) - u;
-      const bool hit = a <= b && x0 <= xR && x0 + 3.0f >= xL;
-      out |= hit ? 1u << (qy * 4 + qx) : 0u;
-    }
+    // the band's block columns qx with X0 + 4 qx - u <= xR and X0 + 4 qx + 3 - u
+    // >= xL, as an integer range (widened by 1e-3 block against the rounding
+    // of the scaled bounds: a superset of the per-column tests)
+    const int hiq = min(__float2int_rd(fmaf(xR, 0.25f, cu) + 1e-3f), 3);
+    const int loq = max(__float2int_ru(fmaf(xL, 0.25f, cu - 0.75f) - 1e-3f), 0);
+    const uint32_t cols = (loq <= hiq && a <= b) ? (0xfu >> (3 - hiq)) & (0xfu << loq) : 0u;
+    out |= cols << (4 * qy);
   }
   return ok ? (m & out) : m;
 }
