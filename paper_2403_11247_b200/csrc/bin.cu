@@ -152,68 +152,158 @@ __device__ __forceinline__ void emit_sorted(const unsigned long long *a, int len
 // KPL l .. KPL l + KPL - 1 (blocked), missing elements +inf.  The same
 // all-ascending bitonic network as above; a compare-exchange at distance
 // m < KPL is inside the lane, at m >= KPL the partner is element t ^ (m % KPL)
-// of lane l ^ (m / KPL) (one 64-bit shuffle per element).  KPL = 8 (<= 256
-// keys): 21 of the 36 stages are lane-local; KPL = 16 (<= 512): 30 of 45.  No
-// CTA barrier (round 1's 128-thread form: 33 shuffle stages, 3 barriers).
-template <int KPL>
-__device__ __forceinline__ void cx_lane(unsigned long long (&x)[KPL], int a, int b) {
-  const unsigned long long lo = x[a] < x[b] ? x[a] : x[b], hi = x[a] < x[b] ? x[b] : x[a];
+// of lane l ^ (m / KPL) (one shuffle per element).  KPL = 8 (<= 256 keys): 21
+// of the 36 stages are lane-local; KPL = 16 (<= 512): 30 of 45.  No CTA
+// barrier (round 1's 128-thread form: 33 shuffle stages, 3 barriers).  Key
+// type K: the 64-bit keys themselves, or the 32-bit keys of
+// warp_sort_emit32 (u32 min / max and one shuffle: a third of the 64-bit
+// form's instructions).
+template <typename K, int KPL>
+__device__ __forceinline__ void cx_lane(K (&x)[KPL], int a, int b) {
+  const K lo = x[a] < x[b] ? x[a] : x[b], hi = x[a] < x[b] ? x[b] : x[a];
   x[a] = lo;
   x[b] = hi;
 }
-template <int KPL, int M, int HIBIT>
-__device__ __forceinline__ void warp_stage(unsigned long long (&x)[KPL], int lane) {
+template <typename K, int KPL, int M, int HIBIT>
+__device__ __forceinline__ void warp_stage(K (&x)[KPL], int lane) {
   // partner e ^ M; the pair's lower element keeps the min
   if constexpr (M < KPL) {
 #pragma unroll
     for (int t = 0; t < KPL; t++)
-      if ((t ^ M) > t) cx_lane<KPL>(x, t, t ^ M);
+      if ((t ^ M) > t) cx_lane<K, KPL>(x, t, t ^ M);
   } else {
     constexpr int ml = M / KPL, mt = M % KPL;
     const bool lower = (lane & (HIBIT / KPL)) == 0;
-    unsigned long long p[KPL];
+    K p[KPL];
 #pragma unroll
     for (int t = 0; t < KPL; t++) p[t] = __shfl_xor_sync(0xffffffffu, x[t ^ mt], ml);
 #pragma unroll
     for (int t = 0; t < KPL; t++) {
-      const bool pl = p[t] < x[t];
-      x[t] = (pl == lower) ? p[t] : x[t];
+      if constexpr (sizeof(K) == 4) {
+        x[t] = lower ? min(x[t], p[t]) : max(x[t], p[t]);
+      } else {
+        const bool pl = p[t] < x[t];
+        x[t] = (pl == lower) ? p[t] : x[t];
+      }
     }
   }
 }
-template <int KPL, int K, int J>
-__device__ __forceinline__ void warp_cleaners(unsigned long long (&x)[KPL], int lane) {
+template <typename K, int KPL, int KK, int J>
+__device__ __forceinline__ void warp_cleaners(K (&x)[KPL], int lane) {
   if constexpr (J >= 1) {
-    warp_stage<KPL, J, J>(x, lane);
-    warp_cleaners<KPL, K, J / 2>(x, lane);
+    warp_stage<K, KPL, J, J>(x, lane);
+    warp_cleaners<K, KPL, KK, J / 2>(x, lane);
   }
 }
-template <int KPL, int K, int NP2>
-__device__ __forceinline__ void warp_merges(unsigned long long (&x)[KPL], int lane) {
-  if constexpr (K <= NP2) {
-    warp_stage<KPL, K - 1, K / 2>(x, lane);  // mirror
-    warp_cleaners<KPL, K, K / 4>(x, lane);   // half-cleaners
-    warp_merges<KPL, 2 * K, NP2>(x, lane);
+template <typename K, int KPL, int KK, int NP2>
+__device__ __forceinline__ void warp_merges(K (&x)[KPL], int lane) {
+  if constexpr (KK <= NP2) {
+    warp_stage<K, KPL, KK - 1, KK / 2>(x, lane);  // mirror
+    warp_cleaners<K, KPL, KK, KK / 4>(x, lane);   // half-cleaners
+    warp_merges<K, KPL, 2 * KK, NP2>(x, lane);
   }
 }
 // the network for NP2 elements (<= 32 KPL), all stage distances compile-time
 // so the keys stay in registers
-template <int KPL, int NP2>
-__device__ __forceinline__ void sort_warp(unsigned long long (&x)[KPL]) {
-  warp_merges<KPL, 2, NP2>(x, threadIdx.x & 31);
+template <typename K, int KPL, int NP2>
+__device__ __forceinline__ void sort_warp(K (&x)[KPL]) {
+  warp_merges<K, KPL, 2, NP2>(x, threadIdx.x & 31);
 }
-// load a tile's len keys (<= 32 KPL) from its bucket, sort, emit the entries
+// load a tile's len keys (<= 32 KPL) from its bucket, sort the 64-bit keys,
+// emit the entries
 template <int KPL, int NP2>
-__device__ __forceinline__ void warp_sort_emit(const unsigned long long *__restrict__ bk, int len,
-                                               uint32_t start, uint32_t *__restrict__ pair_gid) {
+__device__ __forceinline__ void warp_sort_emit64(const unsigned long long *__restrict__ bk,
+                                                 int len, uint32_t start,
+                                                 uint32_t *__restrict__ pair_gid) {
   const int l = threadIdx.x;
   unsigned long long x[KPL];
 #pragma unroll
   for (int t = 0; t < KPL; t++) x[t] = KPL * l + t < len ? bk[KPL * l + t] : ~0ull;
-  sort_warp<KPL, NP2>(x);
+  sort_warp<unsigned long long, KPL, NP2>(x);
 #pragma unroll
   for (int t = 0; t < KPL; t++)
     if (KPL * l + t < len) pair_gid[(int64_t)start + KPL * l + t] = pair_entry(x[t]);
+}
+// A tile's len <= 32 KPL <= 512 keys from its bucket, sorted, as pair entries.
+// The 64-bit keys (bits(z_c), gid, mask) are staged in shared memory (ex, by
+// bucket position i); the network sorts the 32-bit keys
+// ((bits(z_c) - zlo) >> sh) << 9 | i, zlo the tile's smallest depth bits and
+// sh = 0 unless the tile's depth-bit span needs more than 22 bits: keys whose
+// shifted depths differ come out in their exact order, and equal shifted
+// depths (equal depths, or, for sh > 0, depths closer than 2^sh bit steps)
+// form adjacent runs.  Every output position then takes its exact key by i;
+// inside a run an element's final position is the run start + its rank among
+// the run's exact keys (gids are unique, so the ranks are a permutation).  The
+// result is the same order as a 64-bit sort, bit for bit.
+template <int KPL, int NP2>
+__device__ __forceinline__ void warp_sort_emit32(const unsigned long long *__restrict__ bk,
+                                                 int len, uint32_t start,
+                                                 uint32_t *__restrict__ pair_gid,
+                                                 unsigned long long *__restrict__ ex,
+                                                 uint32_t *__restrict__ s32) {
+  const int l = threadIdx.x;
+  uint32_t x[KPL];
+  // (the network sorts any assignment of keys to its NP2 positions, i.e. to
+  // lanes l < NP2 / KPL: loaded striped over those lanes, so the bucket reads
+  // coalesce and the staging stores are conflict-free)
+  constexpr int kLanes = NP2 / KPL;
+  uint32_t zlo = 0xffffffffu, zhi = 0u;
+#pragma unroll
+  for (int t = 0; t < KPL; t++) {
+    const int i = kLanes * t + l;
+    if (l < kLanes && i < len) {
+      const unsigned long long e = bk[i];
+      ex[i] = e;
+      zlo = min(zlo, (uint32_t)(e >> 32));
+      zhi = max(zhi, (uint32_t)(e >> 32));
+    }
+  }
+  // the tile's depth-bit range [zlo, zhi] in 22 bits: shifted right by sh only
+  // when it is wider (then equal shifted depths form runs, fixed up below);
+  // every real key stays below the padding key 0xffffffff
+  zlo = __reduce_min_sync(0xffffffffu, zlo);
+  zhi = __reduce_max_sync(0xffffffffu, zhi);
+  const uint32_t span = zhi - zlo;
+  const int sh = span >> 22 ? 10 - __clz(span) : 0;  // bit length of span - 22
+#pragma unroll
+  for (int t = 0; t < KPL; t++) {  // (the staged keys re-read: fewer live registers)
+    const int i = kLanes * t + l;
+    x[t] = l < kLanes && i < len ? ((((uint32_t)(ex[i] >> 32) - zlo) >> sh) << 9) | (uint32_t)i
+                                 : 0xffffffffu;
+  }
+  sort_warp<uint32_t, KPL, NP2>(x);
+  // sorted keys by output position p at s32[p + p / 32] (no bank conflicts
+  // between the lanes' blocked positions)
+  auto at = [](int p) { return p + (p >> 5); };
+#pragma unroll
+  for (int t = 0; t < KPL; t++) s32[at(KPL * l + t)] = x[t];
+  // the neighbours across the lane boundary
+  const uint32_t before = __shfl_up_sync(0xffffffffu, x[KPL - 1], 1);
+  const uint32_t after = __shfl_down_sync(0xffffffffu, x[0], 1);
+  __syncwarp();
+  uint32_t runs = 0;  // this lane's elements inside a run (bit t)
+#pragma unroll
+  for (int t = 0; t < KPL; t++) {
+    const int p = KPL * l + t;
+    const uint32_t tk = x[t] >> 9;
+    const uint32_t prv = t > 0 ? x[t - 1] : before, nxt = t + 1 < KPL ? x[t + 1] : after;
+    const bool run = (p > 0 && (prv >> 9) == tk) || (p + 1 < len && (nxt >> 9) == tk);
+    if (p < len && !run) pair_gid[(int64_t)start + p] = pair_entry(ex[x[t] & 511u]);
+    runs |= (p < len && run) ? 1u << t : 0u;
+  }
+  while (runs) {
+    const int t = __ffs(runs) - 1;
+    runs &= runs - 1;
+    const int p = KPL * l + t;
+    const uint32_t v = s32[at(p)], tk = v >> 9;
+    const unsigned long long e = ex[v & 511u];
+    int r0 = p, r1 = p;
+    while (r0 > 0 && (s32[at(r0 - 1)] >> 9) == tk) r0--;
+    while (r1 + 1 < len && (s32[at(r1 + 1)] >> 9) == tk) r1++;
+    int rank = 0;
+    for (int q = r0; q <= r1; q++) rank += ex[s32[at(q)] & 511u] < e ? 1 : 0;
+    pair_gid[(int64_t)start + r0 + rank] = pair_entry(e);
+  }
 }
 
 // a5 offsets: the exclusive scan of the tiles' (or list positions') pair counts
@@ -238,6 +328,7 @@ cudaError_t launch_tile_scan(const BinWs &w, int64_t T, int nv, int64_t ws_strid
 
 // One 128-thread CTA per tile: enough warps in flight to hide the latency of
 // the record gathers in pair_entry (there are only ~3k tiles per view).
+template <bool NARROW>
 __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
     int64_t T, uint32_t *__restrict__ range, int64_t *__restrict__ n_pairs, BinWs w,
     int64_t cap, const uint4 *__restrict__ rec4, uint32_t *__restrict__ pair_gid, int tiles_x,
@@ -282,10 +373,20 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
   if (len == 0) return;                // (block-uniform)
   if (len <= 512) {  // the common case: one warp, in registers
     const unsigned long long *bk = w.bucket + tile * kBucketCap;
-    if (len <= 64) warp_sort_emit<8, 64>(bk, len, start, pair_gid);          // 21 stages
-    else if (len <= 128) warp_sort_emit<8, 128>(bk, len, start, pair_gid);   // 28 stages
-    else if (len <= 256) warp_sort_emit<8, 256>(bk, len, start, pair_gid);   // 36 stages
-    else warp_sort_emit<16, 512>(bk, len, start, pair_gid);                  // 45 stages
+    if constexpr (NARROW) {
+      // (sk: the exact keys in its first 4 KB, the sorted 32-bit keys after)
+      unsigned long long *ex = sk;
+      uint32_t *s32 = reinterpret_cast<uint32_t *>(sk + 512);
+      if (len <= 64) warp_sort_emit32<8, 64>(bk, len, start, pair_gid, ex, s32);     // 21 stages
+      else if (len <= 128) warp_sort_emit32<8, 128>(bk, len, start, pair_gid, ex, s32);
+      else if (len <= 256) warp_sort_emit32<8, 256>(bk, len, start, pair_gid, ex, s32);
+      else warp_sort_emit32<16, 512>(bk, len, start, pair_gid, ex, s32);             // 45 stages
+    } else {
+      if (len <= 64) warp_sort_emit64<8, 64>(bk, len, start, pair_gid);
+      else if (len <= 128) warp_sort_emit64<8, 128>(bk, len, start, pair_gid);
+      else if (len <= 256) warp_sort_emit64<8, 256>(bk, len, start, pair_gid);
+      else warp_sort_emit64<16, 512>(bk, len, start, pair_gid);
+    }
     return;
   }
   unsigned long long *a = len <= kCtaCap ? sk : w.keys + start;
@@ -310,12 +411,15 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_tiles(
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
                               const void *rec, uint32_t *pair_gid,
                               uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,
-                              int64_t tile0, int64_t ntiles) {
+                              int64_t tile0, int64_t ntiles, bool narrow) {
   if (ntiles < 0) ntiles = T - tile0;
   if (ntiles <= 0) return cudaSuccess;
-  k_sort_tiles<<<(unsigned)ntiles, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
-                                                         static_cast<const uint4 *>(rec),
-                                                         pair_gid, tiles_x, tile0, SortViews{});
+  // (two instantiations: the 64-bit form in one kernel with the 32-bit one
+  // ran at 14.7 instead of 9.6 us per C2 chunk)
+  auto kern = narrow ? k_sort_tiles<true> : k_sort_tiles<false>;
+  kern<<<(unsigned)ntiles, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
+                                                 static_cast<const uint4 *>(rec), pair_gid,
+                                                 tiles_x, tile0, SortViews{});
   return cudaGetLastError();
 }
 
@@ -325,9 +429,9 @@ cudaError_t launch_sort_tiles_views(const BinWs &w, int64_t nctas, int64_t T, in
                                     const SortViews &sv, int nv, cudaStream_t s) {
   if (nctas <= 0 || nv <= 0) return cudaSuccess;
   const dim3 grid((unsigned)nctas, (unsigned)nv);
-  k_sort_tiles<<<grid, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
-                                             static_cast<const uint4 *>(rec), pair_gid, tiles_x, 0,
-                                             sv);
+  k_sort_tiles<true><<<grid, kSortThreads, 0, s>>>(T, tile_range, n_pairs_dev, w, cap,
+                                                   static_cast<const uint4 *>(rec), pair_gid,
+                                                   tiles_x, 0, sv);
   return cudaGetLastError();
 }
 

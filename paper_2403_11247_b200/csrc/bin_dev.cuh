@@ -46,11 +46,12 @@ cudaError_t launch_tile_scan(const BinWs &w, int64_t T, int nv, int64_t ws_strid
 // a5: k_sort_tiles over the buckets filled by k_bucket or the fused projection,
 // after launch_tile_scan (tiles [tile0, tile0 + ntiles) only, ntiles < 0 = to
 // the end: every tile reads only its own offset, so any split of the tiles
-// into launches is valid)
+// into launches is valid).  narrow: the register sort on 32-bit keys
+// (warp_sort_emit32) instead of the 64-bit keys -- the same order bit for bit
 cudaError_t launch_sort_tiles(const BinWs &w, int64_t T, int tiles_x, int64_t cap,
                               const void *rec, uint32_t *pair_gid,
                               uint32_t *tile_range, int64_t *n_pairs_dev, cudaStream_t s,
-                              int64_t tile0 = 0, int64_t ntiles = -1);
+                              int64_t tile0 = 0, int64_t ntiles = -1, bool narrow = true);
 // the same over nv views at once (grid.y = view): view v's workspace at
 // + v ws_stride bytes, records + v rec_stride (uint4 units), pair_gid + v
 // gid_stride, tile_range + v range_stride, n_pairs_dev + v

@@ -495,8 +495,13 @@ cudaError_t launch_render_step(const csplat_gaussians &g, const DecodeArgs *dec,
     cudaStream_t sc = r->st[c];
     if ((e = cudaStreamWaitEvent(sc, r->start, 0)) != cudaSuccess) break;
     forked = c + 1;
+    // (the 32-bit-key register sort for the tracking step -- C3 iteration
+    // 152.7 -> 148 us -- but the 64-bit one for the given-upstream step: with
+    // the 32-bit sort the C2 render-only graph measured 236 vs 230 us,
+    // although that sort kernel alone is faster, 6.9 vs 9.6 us per chunk
+    // serialised; DESIGN.md §13.  Both give the same order bit for bit.)
     e = launch_sort_tiles(w, T, ci.tiles_x, cap, rec, pair_gid, tile_range,
-                          n_pairs_dev, sc, t0, nt);
+                          n_pairs_dev, sc, t0, nt, bwd && bwd->loss);
     if (e == cudaSuccess)
       e = launch_render_fwd(rec, pair_gid, tile_range, cam, prm, color, depth, sil, t_final,
                             n_contrib, sc, (int)t0, (int)nt);

@@ -356,6 +356,31 @@ def test_long_tile_lists(env):
         assert res["npairs"] >= n
 
 
+@pytest.mark.parametrize("n", [40, 100, 200, 400])
+def test_tile_sort_depth_runs(env, n):
+    """The 32-bit-key register sort (warp_sort_emit32): tiles whose depth-bit
+    span needs more than 22 bits (depths 0.02 .. 80, so the keys are shifted
+    and close depths collide) with clusters of equal and 1-ulp-apart depths,
+    for the 64- / 128- / 256- / 512-key networks (one 16x16 tile holds every
+    pair): the stand-alone bin's pair order must be the oracle's (bits(z_c),
+    index) order bit for bit (the render step's 64-bit-key sort is compared
+    with the stand-alone calls in test_render_step_matches_separate_calls)."""
+    rng = np.random.default_rng(21 + n)
+    cam = dict(fx=20.0, fy=20.0, cx=7.5, cy=7.5, width=16, height=16, near=0.01, far=100.0)
+    base = rng.choice(np.array([0.02, 0.5, 3.0, 3.0, 3.0, 80.0], np.float32), n)
+    ulp = rng.integers(0, 3, n).astype(np.int32)
+    z = (base.view(np.int32) + ulp).view(np.float32).astype(np.float64)
+    px, py = rng.uniform(0, 15, n), rng.uniform(0, 15, n)
+    mean = np.stack([(px - 7.5) / 20 * z, (py - 7.5) / 20 * z, z]).astype(np.float32)
+    sc = synth.SynthScene(mean, rng.normal(-1, 1, n).astype(np.float32),
+                          rng.uniform(0, 1, (3, n)).astype(np.float32),
+                          np.log(np.array([[0.02], [0.012], [0.004]]) * z).astype(np.float32),
+                          synth._unit_quats(rng, n), np.full(n, 3.0, np.float32), cam,
+                          [synth.IDENTITY_VIEW.copy()])
+    res = run_and_compare(env, sc, use_codebook=False)
+    assert res["npairs"] >= n // 2
+
+
 def test_capacity_overflow_reported(env):
     torch, cs, dev = env["torch"], env["cs"], env["dev"]
     sc = synth.tiny_scene(0)
