@@ -489,8 +489,9 @@ def bench_c5_window(dev, rank, world, iters=3):
         per = [tuple(float(x) for x in a_.cpu()) for a_ in allr]
     else:
         per = [(t_local, 0.0)]
+    coll = (dist.get_backend().upper() if world > 1 else "NCCL") + " all-reduce"
     return {"workload": "C5 window: 64 keyframes x 500k Gaussians, R-VQ 4x256, "
-                        f"keyframes sharded over {world} GPU(s) + NCCL all-reduce",
+                        f"keyframes sharded over {world} GPU(s) + {coll}",
             "n_gpus": world, "keyframes_per_rank": len(win.local), "ms_per_window_iter": t,
             "window_iters_per_s": 1e3 / t, "keyframe_renders_per_s": 64e3 / t,
             "reduced_grad_checksum": float(chk.item()), "replicas_identical": same,
